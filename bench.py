@@ -1,0 +1,414 @@
+#!/usr/bin/env python3
+"""Bench: triangles/s of the fused edge-generation -> red-refinement -> assembly
+step (fp64) on B200, with the HBM-roofline fraction, the end-to-end (host
+buffers through the C ABI) number and the CPU baseline.
+
+Workload (BASELINE.json configs[4], "config 5"): unit square (2-triangle coarse
+mesh), the L12 mesh (33.5 M triangles) resident in HBM; one step =
+build_topology(L12) -> red_refine -> build_topology(L13) -> classify_edges ->
+B, D, M, M0 blocks + load (b + LN) + C in CSR + bD on the 134 M-triangle L13
+mesh, config-2 coefficients (per-element A(x_c), delta(x_c), p = (0.1,-0.1)).
+Inputs are far larger than L2 (126 MB), so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "triangles/sec for edge-gen+refine+assembly (fp64), % of HBM roofline, 1/2/4/8 GPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- algorithmic (compulsory) bytes, SURVEY.md §8(d) -------------------------
+def eg_bytes(nE, E):
+    return 27 * nE + 32 * E
+
+
+def rf_bytes(nC, nE, E):  # parent sizes
+    return 32 * nC + 72 * nE + 24 * E
+
+
+def as_bytes(nC, nE, E, L, nnz):
+    return 16 * nC + 324 * nE + 28 * E + 12 * L + 12 * nnz
+
+
+def kernel_bytes(name, s):
+    """Algorithmic bytes of one launch of a kernel (inputs read once, outputs
+    written once) for the final-level sizes s."""
+    nC, nE, E, L, nnz = s["nC"], s["nE"], s["E"], s["L"], s["nnz"]
+    return {
+        "k_volume": 12 * nE + 16 * nC + 312 * nE,
+        "k_eg_bucket": 24 * nE + 28 * E + 12 * nE + 4 * nC,
+        "k_eg_scatter": 12 * nE + 24 * nE,
+        "k_eg_count": 12 * nE,
+        "k_constraint_csr": 28 * E + 16 * nC + 4 * L + 12 * nnz,
+        "k_cls_retained": E // 8 + 4 * E + 4 * L,
+    }.get(name)
+
+
+# ---- clocks during the timed region -------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---- distributed plumbing (torchrun) -------------------------------------------
+def dist_init(n_gpus):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def dist_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---- CPU side -------------------------------------------------------------------
+def cpu_sample_worker(args):
+    level, steps, warmup, q = args
+    from oracle import oracle as O
+    from paper_2401_15557_b200 import meshgen as G
+    hm = O.refine_levels(G.square_2tri(), level)
+    fields = G.config_fields(5)
+    times = []
+    nE = 0
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = O.pipeline(hm, 1, *fields)
+        dt = time.perf_counter() - t0
+        nE = r["mesh"].nE
+        del r
+        if i >= warmup:
+            times.append(dt)
+    return nE, times
+
+
+def cpu_workers_available(per_worker_gb: float) -> int:
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        with open("/proc/meminfo") as f:
+            mem = {l.split(":")[0]: int(l.split()[1]) for l in f}
+        avail_gb = mem.get("MemAvailable", 0) / 1e6
+    except Exception:
+        avail_gb = 8.0
+    return max(1, min(cores, int(avail_gb * 0.6 / per_worker_gb)))
+
+
+def cpu_baseline_single(level=10):
+    """The oracle port, one core, one bounded sample (L10 -> L11, 8.4 M triangles)."""
+    nE, times = cpu_sample_worker((level, 1, 0, None))
+    return {"value": nE / times[0], "unit": "triangles/s", "cores": 1, "kind": "port",
+            "sample": f"square L{level} -> L{level + 1} pipeline ({nE} triangles), oracle/phfem_oracle.c, "
+                      f"1 thread, {times[0]:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    level = args.ref_level
+    P = cpu_workers_available(per_worker_gb=1.5)
+    with mp.get_context("fork").Pool(P) as pool:
+        res = pool.map(cpu_sample_worker, [(level, args.steps, args.warmup, None)] * P)
+    nE = res[0][0]
+    per_step = [max(r[1][i] for r in res) for i in range(args.steps)]
+    t = statistics.mean(per_step)
+    value = P * nE / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "triangles/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"config5 pipeline sample: square L{level} -> L{level + 1}, "
+                               f"{P} concurrent single-threaded samples", "triangles_per_sample": nE},
+        "cpu_baseline": {"value": value, "unit": "triangles/s", "cores": P, "kind": "port",
+                         "sample": f"{P} x square L{level}->L{level + 1} ({nE} tri each), "
+                                   "oracle/phfem_oracle.c (C restatement of the reference; the reference "
+                                   "itself is single-threaded, so one sample per core)"},
+        "e2e": {"value": value, "unit": "triangles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- GPU side ---------------------------------------------------------------------
+def build_input(ctx, level):
+    from paper_2401_15557_b200 import capi, meshgen as G
+    dm = capi.DeviceMesh.upload(ctx, G.square_2tri())
+    for _ in range(level):
+        t = capi.build_topology(ctx, dm)
+        nxt = capi.red_refine(ctx, dm, t)
+        t.release()
+        dm.release()
+        dm = nxt
+    ctx.sync()
+    return dm
+
+
+def run_ours(args):
+    from paper_2401_15557_b200 import capi, meshgen as G
+    rank, world, local = dist_init(args.gpus)
+    ctx = capi.Context(local)
+    fields = G.config_fields(5)
+    dm = build_input(ctx, args.level - 1)          # L12 input, resident in HBM
+    # sizes at both levels (one untimed run)
+    r = capi.pipeline(ctx, dm, 1, *fields)
+    o = r.out
+    s = {"nC": o.mesh.nC, "nE": o.mesh.nE, "E": o.topo.E, "L": o.cls.L, "nnz": o.C.nnz}
+    r.release()
+    t0 = capi.build_topology(ctx, dm)
+    s0 = {"nC": dm.m.nC, "nE": dm.m.nE, "E": t0.E}
+    t0.release()
+    compulsory = (eg_bytes(s0["nE"], s0["E"]) + rf_bytes(s0["nC"], s0["nE"], s0["E"]) +
+                  eg_bytes(s["nE"], s["E"]) + as_bytes(s["nC"], s["nE"], s["E"], s["L"], s["nnz"]))
+
+    for _ in range(args.warmup):
+        capi.pipeline(ctx, dm, 1, *fields).release()
+    ctx.sync()
+
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist_barrier(world)
+    ctx.sync()
+    launches0 = ctx.launches
+    ctx.profile(True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            capi.pipeline(ctx, dm, 1, *fields).release()
+        ev1.record(stream)
+        ctx.sync()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = (ctx.launches - launches0) // args.steps
+    ms = dist_max(ms_local, world)
+    dist_barrier(world)
+    value = world * s["nE"] / (ms * 1e-3)
+
+    peak, peak_kind = peaks()
+    # dominant kernel -> roofline
+    named = {k: v for k, v in prof.items() if kernel_bytes(k, s) is not None}
+    dom = max(named, key=lambda k: named[k][0])
+    dom_ms, dom_n = named[dom]
+    # final-level launches only: the L12 launch of the same kernel is 4x smaller
+    lvl_bytes = kernel_bytes(dom, s)
+    if dom in ("k_eg_bucket", "k_eg_scatter", "k_eg_count"):
+        small = kernel_bytes(dom, {"nC": s0["nC"], "nE": s0["nE"], "E": s0["E"], "L": 0, "nnz": 0})
+        per_step_bytes = lvl_bytes + small
+    else:
+        per_step_bytes = lvl_bytes * (dom_n // args.steps)
+    achieved = per_step_bytes / (dom_ms / args.steps * 1e-3) / 1e9
+    step_share = {k: round(v[0] / args.steps / ms_local, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_step": per_step_bytes,
+                "kernel_ms_per_step": round(dom_ms / args.steps, 4)}
+    pipeline_gbs = compulsory / (ms_local * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "triangles/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} "
+                               f"({s['nE']} triangles): EG+RF+EG+AS, config-2 coefficients",
+                   "triangles": s["nE"], "edges": s["E"], "multipliers": s["L"], "nnz_C": s["nnz"],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (no flush)"},
+        "roofline": roofline,
+        "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(pipeline_gbs, 1),
+                              "peak": peak, "frac": round(pipeline_gbs / peak, 4)},
+        "kernel_share": step_share,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = run_e2e(ctx, args, fields)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_single(args.cpu_level)
+    dm.release()
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(ctx, args, fields):
+    """Same step through the host-buffer C-ABI calls: pinned host mesh in,
+    every output copied back into pinned host buffers, copies timed."""
+    import ctypes as C
+    import torch
+    from paper_2401_15557_b200 import capi
+    hm = build_input(ctx, args.e2e_level - 1).download()
+    out = capi.phfem_pipeline_out()
+    lib = ctx.lib
+
+    def pinned(n, dt):
+        return torch.empty(int(n), dtype=dt, pin_memory=True)
+
+    inp = {"coords": pinned(hm.coords.size, torch.float64), "elements": pinned(hm.elements.size, torch.int32),
+           "dirichlet": pinned(max(hm.dirichlet.size, 1), torch.int32),
+           "neumann": pinned(max(hm.neumann.size, 1), torch.int32)}
+    inp["coords"].numpy()[:] = hm.coords.ravel()
+    inp["elements"].numpy()[:] = hm.elements.ravel()
+    inp["dirichlet"].numpy()[:hm.dirichlet.size] = hm.dirichlet.ravel()
+    inp["neumann"].numpy()[:hm.neumann.size] = hm.neumann.ravel()
+    h2d = 16 * hm.nC + 12 * hm.nE + 8 * (len(hm.dirichlet) + len(hm.neumann))
+
+    def run_once(dst):
+        ctx.check(lib.phfem_pipeline_from_host(
+            ctx.ptr, C.c_void_p(inp["coords"].data_ptr()), C.c_void_p(inp["elements"].data_ptr()),
+            C.c_void_p(inp["dirichlet"].data_ptr()), C.c_void_p(inp["neumann"].data_ptr()), hm.nC, hm.nE,
+            len(hm.dirichlet), len(hm.neumann), 1, C.byref(fields[0]), C.byref(fields[1]), C.byref(fields[2]),
+            C.byref(fields[3]), 0.0, C.byref(out)))
+        if dst is not None:
+            ctx.check(lib.phfem_pipeline_download(ctx.ptr, C.byref(out), C.byref(dst)))
+        lib.phfem_pipeline_release(ctx.ptr, C.byref(out))
+
+    # sizes -> pinned destination buffers
+    ctx.check(lib.phfem_pipeline_from_host(
+        ctx.ptr, C.c_void_p(inp["coords"].data_ptr()), C.c_void_p(inp["elements"].data_ptr()),
+        C.c_void_p(inp["dirichlet"].data_ptr()), C.c_void_p(inp["neumann"].data_ptr()), hm.nC, hm.nE,
+        len(hm.dirichlet), len(hm.neumann), 1, C.byref(fields[0]), C.byref(fields[1]), C.byref(fields[2]),
+        C.byref(fields[3]), 0.0, C.byref(out)))
+    o = out
+    sizes = {"coords": (2 * o.mesh.nC, torch.float64), "elements": (3 * o.mesh.nE, torch.int32),
+             "dirichlet": (2 * o.mesh.nD, torch.int32), "neumann": (2 * o.mesh.nN, torch.int32),
+             "edge_nodes": (2 * o.topo.E, torch.int32), "edge_elements": (2 * o.topo.E, torch.int32),
+             "local_in_tplus": (o.topo.E, torch.int32), "local_in_tminus": (o.topo.E, torch.int32),
+             "interior_edges": (o.topo.n_interior, torch.int32), "boundary_edges": (o.topo.n_boundary, torch.int32),
+             "elem_edge": (3 * o.mesh.nE, torch.int32), "dirichlet_edge_ids": (o.cls.nD, torch.int32),
+             "neumann_edge_ids": (o.cls.nN, torch.int32), "retained_edges": (o.cls.L, torch.int32),
+             "retained_pos": (o.topo.E, torch.int32), "C_row_ptr": (o.cls.L + 1, torch.int32),
+             "C_col_idx": (o.C.nnz, torch.int32), "C_values": (o.C.nnz, torch.float64),
+             "B": (9 * o.mesh.nE, torch.float64), "D": (9 * o.mesh.nE, torch.float64),
+             "M": (9 * o.mesh.nE, torch.float64), "M0": (9 * o.mesh.nE, torch.float64),
+             "load": (3 * o.mesh.nE, torch.float64), "bd": (o.cls.L, torch.float64)}
+    nE_final = o.mesh.nE
+    need = sum(n * (8 if dt == torch.float64 else 4) for n, dt in sizes.values())
+    lib.phfem_pipeline_release(ctx.ptr, C.byref(out))
+    try:
+        with open("/proc/meminfo") as f:
+            avail = {l.split(":")[0]: int(l.split()[1]) for l in f}.get("MemAvailable", 0) * 1024
+    except Exception:
+        avail = 0
+    if need > 0.7 * avail:
+        return {"value": None, "unit": "triangles/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": need,
+                "skipped": f"host RAM {avail / 1e9:.0f} GB < 1.4 x {need / 1e9:.0f} GB of pinned outputs"}
+    bufs = {k: pinned(max(n, 1), dt) for k, (n, dt) in sizes.items()}
+    dst = capi.phfem_pipeline_host(**{k: bufs[k].data_ptr() for k in bufs})
+    steps = max(1, min(args.steps, args.e2e_steps))
+    run_once(dst)
+    ctx.sync()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run_once(dst)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": nE_final / dt, "unit": "triangles/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": need, "ms_per_step": dt * 1e3, "steps": steps,
+            "note": "phfem_pipeline_from_host + phfem_pipeline_download (every output) with pinned host buffers"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--level", type=int, default=13, help="final refinement level (config 5: 13)")
+    ap.add_argument("--e2e-level", type=int, default=13)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-level", type=int, default=10)
+    ap.add_argument("--ref-level", type=int, default=9)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+/*
+ * phfem_fields.h — closed descriptors for the data fields and coefficients of
+ * the primal hybrid FEM hot path, plus the ONE inline formula per kind that
+ * every side evaluates (CUDA kernels, the C-ABI host code, the C oracle and the
+ * lambdas handed to the reference build).
+ *
+ * Why: the reference passes data as std::function (proj/include/phfem/
+ * assembly.hpp:15-19, ScalarField / FluxField), which cannot cross to the
+ * device.  The drop-in boundary therefore takes a tagged union; both the GPU
+ * path and the CPU oracle call the same expression below, so any difference
+ * between them is the libm-vs-CUDA sin/cos/exp ulp, nothing else.
+ *
+ * Every expression is written in the exact left-to-right operation order the
+ * reference / BASELINE formula uses; kernels are compiled with --fmad=false so
+ * no contraction changes the rounding.
+ */
+#ifndef PHFEM_FIELDS_H
+#define PHFEM_FIELDS_H
+
+#include <stdint.h>
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define PHFEM_HD __host__ __device__ __forceinline__
+#else
+#define PHFEM_HD static inline
+#endif
+
+#ifndef PHFEM_PI
+#define PHFEM_PI 3.14159265358979323846
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- scalar fields f(x, t), u_D(x, t) (reference ScalarField) ------------ */
+enum phfem_field_kind {
+  PHFEM_FIELD_ZERO = 0,       /* 0                                           */
+  PHFEM_FIELD_CONST = 1,      /* p0                                          */
+  PHFEM_FIELD_SINSIN = 2,     /* p0 * sin(pi x) * sin(pi y)   (cfg 1/2: p0 = 2 pi^2) */
+  PHFEM_FIELD_EXP_SINSIN = 3, /* exp(-t) * p0 * sin(pi x) * sin(pi y) (cfg 3: p0 = 2 pi^2 - 1) */
+  PHFEM_FIELD_AFFINE = 4,     /* p0 + p1 x + p2 y + p3 t                     */
+  PHFEM_FIELD_SIN3X = 5,      /* sin(3x) (1 + y^2)  (test_assembly.cpp:295-297 KAT) */
+  PHFEM_FIELD_NAN = 6         /* quiet NaN (error-path tests, test_assembly.cpp:286-289) */
+};
+
+/* ---- Neumann fluxes g(x, nu, t) (reference FluxField) -------------------- */
+enum phfem_flux_kind {
+  PHFEM_FLUX_ZERO = 0,        /* 0                                           */
+  PHFEM_FLUX_CONST = 1,       /* p0                                          */
+  PHFEM_FLUX_GRAD_SINSIN = 2, /* grad(p0 sin(pi x) sin(pi y)) . nu   (cfg 1) */
+  PHFEM_FLUX_VEC_KAT = 3      /* (cos y + x, x y - 1) . nu  (test_assembly.cpp:353-358) */
+};
+
+/* ---- coefficients A, p, delta (reference ProblemCoefficients) ------------ */
+enum phfem_coeff_kind {
+  PHFEM_COEFF_CONST = 0,         /* A = [[p0,p1],[p2,p3]], p = (p4,p5), delta = p6 */
+  PHFEM_COEFF_CENTROID_POLY = 1  /* cfg 2/4: at centroid xc: A = [[1+x^2, 0.5xy],[0.5xy, 1+y^2]],
+                                    p = (p4, p5), delta = 1 + x + y          */
+};
+
+typedef struct phfem_field {
+  int32_t kind;
+  int32_t reserved;
+  double p[6];
+} phfem_field;
+
+typedef struct phfem_coeffs {
+  int32_t kind;
+  int32_t reserved;
+  double p[8];
+} phfem_coeffs;
+
+/* Per-element coefficient values after evaluation. */
+typedef struct phfem_coeff_values {
+  double a00, a01, a10, a11, px, py, delta;
+} phfem_coeff_values;
+
+PHFEM_HD double phfem_field_eval(const phfem_field* f, double x, double y, double t) {
+  switch (f->kind) {
+    case PHFEM_FIELD_CONST: return f->p[0];
+    case PHFEM_FIELD_SINSIN: return f->p[0] * sin(PHFEM_PI * x) * sin(PHFEM_PI * y);
+    case PHFEM_FIELD_EXP_SINSIN: return exp(-t) * f->p[0] * sin(PHFEM_PI * x) * sin(PHFEM_PI * y);
+    case PHFEM_FIELD_AFFINE: return f->p[0] + f->p[1] * x + f->p[2] * y + f->p[3] * t;
+    case PHFEM_FIELD_SIN3X: return sin(3.0 * x) * (1.0 + y * y);
+    case PHFEM_FIELD_NAN: return NAN;
+    default: return 0.0;
+  }
+}
+
+PHFEM_HD double phfem_flux_eval(const phfem_field* g, double x, double y, double nx, double ny,
+                                double t) {
+  (void)t;
+  switch (g->kind) {
+    case PHFEM_FLUX_CONST: return g->p[0];
+    case PHFEM_FLUX_GRAD_SINSIN: {
+      const double gx = g->p[0] * PHFEM_PI * cos(PHFEM_PI * x) * sin(PHFEM_PI * y);
+      const double gy = g->p[0] * PHFEM_PI * sin(PHFEM_PI * x) * cos(PHFEM_PI * y);
+      return gx * nx + gy * ny; /* Eigen dot: x*x' + y*y' */
+    }
+    case PHFEM_FLUX_VEC_KAT: {
+      const double vx = cos(y) + x;
+      const double vy = x * y - 1.0;
+      return vx * nx + vy * ny;
+    }
+    default: return 0.0;
+  }
+}
+
+/* Coefficients of element with vertices (x0,y0),(x1,y1),(x2,y2). */
+PHFEM_HD phfem_coeff_values phfem_coeffs_eval(const phfem_coeffs* c, double x0, double y0,
+                                              double x1, double y1, double x2, double y2) {
+  phfem_coeff_values v;
+  if (c->kind == PHFEM_COEFF_CENTROID_POLY) {
+    const double xc = (x0 + x1 + x2) / 3.0;
+    const double yc = (y0 + y1 + y2) / 3.0;
+    v.a00 = 1.0 + xc * xc;
+    v.a01 = 0.5 * xc * yc;
+    v.a10 = v.a01;
+    v.a11 = 1.0 + yc * yc;
+    v.px = c->p[4];
+    v.py = c->p[5];
+    v.delta = 1.0 + xc + yc;
+  } else {
+    v.a00 = c->p[0];
+    v.a01 = c->p[1];
+    v.a10 = c->p[2];
+    v.a11 = c->p[3];
+    v.px = c->p[4];
+    v.py = c->p[5];
+    v.delta = c->p[6];
+  }
+  return v;
+}
+
+/*
+ * Local element matrices in the reference's exact operation order
+ * (proj/src/assembly.cpp:17-27 element_geometry, :53-78 local_element_matrices,
+ * :134-140 unit mass).  Output blocks are column-major 3x3 (out[3*j+i] = X(i,j)),
+ * i.e. exactly the 9 values assemble_block_diagonal writes per element
+ * (assembly.cpp:106-114).  Returns twice the signed area; the caller treats
+ * !(t2 > 0) as the reference's "degenerate or non-CCW triangle" error.
+ */
+PHFEM_HD double phfem_local_blocks(double x0, double y0, double x1, double y1, double x2,
+                                   double y2, const phfem_coeff_values* c, double* Bk,
+                                   double* Dk, double* Mk, double* M0k) {
+  /* mesh.cpp:104-106 signed_area2 */
+  const double t2 = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
+  const double area = 0.5 * t2;
+  /* assembly.cpp:23-25: Vec2(...) / twice_area (component-wise division) */
+  double gx[3], gy[3];
+  gx[0] = (y1 - y2) / t2;
+  gy[0] = (x2 - x1) / t2;
+  gx[1] = (y2 - y0) / t2;
+  gy[1] = (x0 - x2) / t2;
+  gx[2] = (y0 - y1) / t2;
+  gy[2] = (x1 - x0) / t2;
+  /* :59-64 stiffness from the upper triangle: area * (A g_i) . g_j */
+  for (int i = 0; i < 3; ++i) {
+    const double rx = c->a00 * gx[i] + c->a01 * gy[i];
+    const double ry = c->a10 * gx[i] + c->a11 * gy[i];
+    for (int j = i; j < 3; ++j) {
+      const double v = area * (rx * gx[j] + ry * gy[j]);
+      Bk[3 * j + i] = v;
+      Bk[3 * i + j] = v;
+    }
+  }
+  /* :68-71 convection: column-constant area/3 * p . g_j */
+  for (int j = 0; j < 3; ++j) {
+    const double dj = area / 3.0 * (c->px * gx[j] + c->py * gy[j]);
+    Dk[3 * j + 0] = dj;
+    Dk[3 * j + 1] = dj;
+    Dk[3 * j + 2] = dj;
+  }
+  /* :73-75 mass (delta-scaled) and :134-140 unit mass */
+  const double md = c->delta * area * (1.0 / 6.0);
+  const double mo = c->delta * area * (1.0 / 12.0);
+  const double ud = area * (1.0 / 6.0);
+  const double uo = area * (1.0 / 12.0);
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) {
+      Mk[3 * j + i] = (i == j) ? md : mo;
+      M0k[3 * j + i] = (i == j) ? ud : uo;
+    }
+  return t2;
+}
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHFEM_FIELDS_H */

@@ -1,0 +1,269 @@
+/*
+ * phfem_gpu.h — the C ABI of the B200-native edge-generation / red-refinement /
+ * assembly path of the lowest-order primal hybrid FEM (arXiv 2401.15557).
+ *
+ * Plain pointers and sizes only (no torch, no Eigen, no C++ types), so it can
+ * be bound from C++, ctypes, cgo or JNI.  Every entry point replaces one
+ * reference C++ function from /root/reference/proj/include/phfem (cited per
+ * function); the C++ drop-in layer in include/phfem/*.hpp re-exposes the
+ * reference signatures on top of this ABI.
+ *
+ * Conventions
+ *  - ids are int32, 0-based, values IEEE fp64 — as in the reference.
+ *  - "device" pointers live in HBM of the ctx's device; calls are asynchronous
+ *    on the ctx stream except where a data-dependent size must come back
+ *    (E, L, nnz), in which case the call synchronises the stream once.
+ *  - Errors: every call returns a phfem_status.  The message retrievable with
+ *    phfem_ctx_message() is the reference's exception text (1-based ids), so a
+ *    wrapper rethrows the same exception type with the same what().
+ *  - Library-owned outputs (data-dependent sizes) are released with the
+ *    matching *_release(); fixed-size outputs (N = 3 nE blocks, vectors) are
+ *    written into caller-provided device buffers.
+ *  - There is no CPU fallback: without a usable sm_100 device every call
+ *    returns PHFEM_ERR_NO_DEVICE / PHFEM_ERR_CUDA.
+ */
+#ifndef PHFEM_GPU_H
+#define PHFEM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "phfem_fields.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHFEM_ABI_VERSION 1
+
+typedef enum phfem_status {
+  PHFEM_OK = 0,
+  PHFEM_ERR_NONMANIFOLD = 1,        /* runtime_error     edge_topology.cpp:88-91   */
+  PHFEM_ERR_DUP_DIRECTED = 2,       /* runtime_error     edge_topology.cpp:93-99   */
+  PHFEM_ERR_NOT_AN_EDGE = 3,        /* runtime_error     edge_topology.cpp:151-153 */
+  PHFEM_ERR_INTERIOR_BOUNDARY = 4,  /* runtime_error     edge_topology.cpp:154-157 */
+  PHFEM_ERR_DEGENERATE = 5,         /* runtime_error     assembly.cpp:19-20        */
+  PHFEM_ERR_NONFINITE = 6,          /* runtime_error     assembly.cpp:192-194,217-219 */
+  PHFEM_ERR_INVALID_ARGUMENT = 7,   /* invalid_argument  assembly.cpp:46-50,81-84; parabolic.cpp:52 */
+  PHFEM_ERR_OUT_OF_RANGE = 8,       /* out_of_range      sparse.cpp:21-24,114-116  */
+  PHFEM_ERR_MISMATCH = 9,           /* runtime_error     assembly.cpp:148-149; refine.cpp:23 */
+  PHFEM_ERR_OOM = 10,
+  PHFEM_ERR_CUDA = 11,
+  PHFEM_ERR_NO_DEVICE = 12
+} phfem_status;
+
+typedef struct phfem_ctx phfem_ctx;
+
+/* ---- context ------------------------------------------------------------- */
+int phfem_abi_version(void);
+/* stream: a cudaStream_t (NULL = a new non-blocking stream owned by the ctx). */
+phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** out);
+void phfem_ctx_destroy(phfem_ctx* ctx);
+const char* phfem_ctx_message(const phfem_ctx* ctx);
+void* phfem_ctx_stream(const phfem_ctx* ctx);
+phfem_status phfem_ctx_sync(phfem_ctx* ctx);
+/* stream-ordered device memory from the ctx pool */
+phfem_status phfem_alloc(phfem_ctx* ctx, size_t bytes, void** out);
+void phfem_free(phfem_ctx* ctx, void* ptr);
+/* number of kernels this ctx launched so far (bench evidence) */
+int64_t phfem_ctx_launches(const phfem_ctx* ctx);
+/* Per-launch CUDA-event timing on the ctx stream.  enable != 0 clears the
+ * records and starts recording an event pair around every kernel launch;
+ * read synchronises and returns the number of distinct kernel names with the
+ * summed milliseconds and launch counts (names are static strings).        */
+phfem_status phfem_ctx_profile(phfem_ctx* ctx, int enable);
+int phfem_ctx_profile_read(phfem_ctx* ctx, int max_names, const char** names, double* ms,
+                           int64_t* counts);
+
+/* ---- mesh (reference Mesh, mesh.hpp:22-30; coords AoS like Vec2) --------- */
+typedef struct phfem_mesh {
+  double* coords;     /* [nC][2]  (x, y)                                     */
+  int32_t* elements;  /* [nE][3]  CCW node triples                           */
+  int32_t* dirichlet; /* [nD][2]  boundary pairs                             */
+  int32_t* neumann;   /* [nN][2]                                             */
+  int32_t nC, nE, nD, nN;
+  int32_t owned;      /* 1 = library-owned (phfem_mesh_release frees it)     */
+  int32_t reserved;
+} phfem_mesh;
+void phfem_mesh_release(phfem_ctx* ctx, phfem_mesh* mesh);
+
+/* ---- topology (reference EdgeTopology, edge_topology.hpp:21-45) ---------- */
+typedef struct phfem_topology {
+  int32_t nC, nE, E, n_interior, n_boundary, reserved;
+  int32_t* edge_nodes;      /* [E][2] directed (initial, end) of the t_plus cycle */
+  int32_t* edge_elements;   /* [E][2] {t_plus, t_minus or -1}                     */
+  int32_t* local_in_tplus;  /* [E]                                                */
+  int32_t* local_in_tminus; /* [E]  -1 on boundary                                */
+  int32_t* interior_edges;  /* [n_interior] ascending                             */
+  int32_t* boundary_edges;  /* [n_boundary] ascending                             */
+  /* a6: element -> edge map with orientation, elem_edge[3m+k] = id of the edge
+   * opposite vertex k, encoded e (m is t_plus, sign +1) or ~e (m is t_minus,
+   * sign -1).  Equivalent to node_pair_to_edge(t[(k+1)%3], t[(k+2)%3])
+   * (refine.cpp:30-32, analysis.cpp:171-177) with the SPEC.md:393 sign.       */
+  int32_t* elem_edge;       /* [nE][3]                                            */
+  /* node_edge_start[v] = first id of the edges whose larger node is v (edge ids
+   * are grouped by max node, ascending by min node inside a group): the device
+   * lookup table behind node_pair_to_edge.                                      */
+  int32_t* node_edge_start; /* [nC+1]                                             */
+} phfem_topology;
+
+/* build_topology (edge_topology.hpp:49; edge_topology.cpp:52-143) */
+phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_topology* out);
+void phfem_topology_release(phfem_ctx* ctx, phfem_topology* topo);
+
+/* ---- classification (EdgeClassification, edge_topology.hpp:53-64) -------- */
+#define PHFEM_CLS_DUP_NEUMANN 1 /* a Neumann pair is listed more than once */
+typedef struct phfem_classification {
+  int32_t nD, nN, E, L;
+  int32_t flags, reserved;
+  int32_t* dirichlet_edge_ids; /* [nD] mesh list order            */
+  int32_t* neumann_edge_ids;   /* [nN] mesh list order            */
+  int32_t* retained_edges;     /* [L] ascending                   */
+  int32_t* retained_pos;       /* [E] position or -1 (Neumann)    */
+  uint32_t* neumann_bits;      /* [ceil(E/32)] Neumann flag bitmap */
+  int32_t* block_prefix;       /* internal: per-1024-edge-block (boundary, neumann) prefixes */
+} phfem_classification;
+
+/* classify_edges (edge_topology.hpp:64; edge_topology.cpp:145-177) */
+phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology* topo,
+                                  const phfem_mesh* mesh, phfem_classification* out);
+void phfem_classification_release(phfem_ctx* ctx, phfem_classification* cls);
+
+/* ---- refinement (red_refine, refine.hpp:15; refine.cpp:7-53) -------------
+ * out is library-owned: coords [nC+E], elements [4nE] (children 4m..4m+3),
+ * boundary lists bisected in order (pairs resolved like midpoint_id,
+ * refine.cpp:15-19: an unknown pair is the reference's mismatch error).      */
+phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                              phfem_mesh* out);
+
+/* ---- orientation normalisation (config 4; not in the reference) ----------
+ * Swaps v1<->v2 of every element with negative signed area, in place.       */
+phfem_status phfem_orient_ccw(phfem_ctx* ctx, phfem_mesh* mesh);
+
+/* ---- element blocks (assemble_volume_operators, assembly.hpp:68;
+ * assembly.cpp:97-142).  Each output is [nE][9] fp64, the column-major 3x3
+ * block of element m = exactly Eigen valuePtr()[9m .. 9m+8] of the
+ * reference's block-diagonal CSC matrix (outer[c] = 3c, inner = 3m+i are
+ * structural).  Any output pointer may be NULL to skip it.                   */
+phfem_status phfem_assemble_volume(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_coeffs* c,
+                                   double* B, double* D, double* M, double* M0);
+
+/* ---- coupling matrix C (assemble_constraint, assembly.hpp:73-74;
+ * assembly.cpp:144-168).  CSR L x N: rows = retained positions, 2 entries
+ * (boundary) or 4 (interior), columns ascending.                            */
+typedef struct phfem_csr {
+  int32_t rows, cols;
+  int64_t nnz;
+  int32_t* row_ptr; /* [rows+1] */
+  int32_t* col_idx; /* [nnz]    */
+  double* values;   /* [nnz]    */
+} phfem_csr;
+phfem_status phfem_assemble_constraint(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                       const phfem_topology* topo,
+                                       const phfem_classification* cls, phfem_csr* out);
+void phfem_csr_release(phfem_ctx* ctx, phfem_csr* m);
+
+/* Same matrix in the reference's Eigen ColMajor layout (from_triplets
+ * sparse.cpp:30-97): outer [N+1], inner [nnz] (rows ascending per column).  */
+typedef struct phfem_csc {
+  int32_t rows, cols;
+  int64_t nnz;
+  int32_t* outer;
+  int32_t* inner;
+  double* values;
+} phfem_csc;
+phfem_status phfem_constraint_csc(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                  const phfem_topology* topo, const phfem_classification* cls,
+                                  phfem_csc* out);
+void phfem_csc_release(phfem_ctx* ctx, phfem_csc* m);
+
+/* ---- load vectors --------------------------------------------------------
+ * assemble_load (assembly.hpp:84; assembly.cpp:179-203) -> out[3nE]          */
+phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_field* f,
+                                 double t, double* out);
+/* assemble_neumann (assembly.hpp:87-89; assembly.cpp:205-228).
+ * accumulate = 0: out[3nE] is overwritten with LN (zeros elsewhere).
+ * accumulate = 1: out += LN in the reference's elementwise "b + LN" order
+ * (elliptic.cpp:54-55) — touching only the DOFs that carry a Neumann term.  */
+phfem_status phfem_assemble_neumann(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                    const phfem_topology* topo, const phfem_classification* cls,
+                                    const phfem_field* g, double t, double* out, int accumulate);
+/* assemble_dirichlet (assembly.hpp:93-95; assembly.cpp:230-242) -> out[L]   */
+phfem_status phfem_assemble_dirichlet(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                      const phfem_topology* topo,
+                                      const phfem_classification* cls, const phfem_field* uD,
+                                      double t, double* out);
+
+/* ---- Crank-Nicolson right-hand side --------------------------------------
+ * The reference forms it inline in solve_parabolic (parabolic.cpp:100-103):
+ *   rhs = M_minus * [U; Lambda];  rhs.head += k/2 (b^n + LN^n + b^n+1 + LN^n+1);
+ *   rhs.tail += (bD^n + bD^n+1)/2
+ * with M_minus from step_matrices (parabolic.cpp:21-54).  The device path
+ * recomputes the M_minus blocks from the geometry (bit-identical values) and
+ * evaluates f, g, u_D at t_n = n k and t_{n+1}.  state = [U (3nE); Lambda (L)],
+ * rhs same length.                                                            */
+typedef struct phfem_cn_plan phfem_cn_plan;
+phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                  const phfem_topology* topo, const phfem_classification* cls,
+                                  const phfem_coeffs* c, const phfem_field* f,
+                                  const phfem_field* g, const phfem_field* uD, double k,
+                                  phfem_cn_plan** out);
+/* rhs for the step t_n -> t_{n+1} (the reference's loop index n+1).         */
+phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* plan, int n, const double* state,
+                          double* rhs);
+void phfem_cn_plan_destroy(phfem_ctx* ctx, phfem_cn_plan* plan);
+
+/* ---- fused pipeline (the bench step) --------------------------------------
+ * input mesh -> [build_topology -> classify -> red_refine] x levels ->
+ * build_topology -> classify -> B, D, M, M0, C (CSR), load = b + LN
+ * (elliptic.cpp:54-55), bD.  All outputs library-owned in `out`.           */
+typedef struct phfem_pipeline_out {
+  phfem_mesh mesh;             /* final (refined) mesh                      */
+  phfem_topology topo;
+  phfem_classification cls;
+  phfem_csr C;
+  double* B;                   /* [nE][9] */
+  double* D;
+  double* M;
+  double* M0;
+  double* load;                /* [3nE] b + LN */
+  double* bd;                  /* [L]         */
+} phfem_pipeline_out;
+phfem_status phfem_pipeline(phfem_ctx* ctx, const phfem_mesh* mesh_in, int levels,
+                            const phfem_coeffs* c, const phfem_field* f, const phfem_field* g,
+                            const phfem_field* uD, double t, phfem_pipeline_out* out);
+void phfem_pipeline_release(phfem_ctx* ctx, phfem_pipeline_out* out);
+
+/* Host-buffer variant (what a reference caller sees): the input mesh comes
+ * from HOST memory (copied in by the call), outputs land in `out` on the
+ * device; phfem_pipeline_download then copies every output into caller-owned
+ * HOST buffers sized from `out` (any destination may be NULL to skip it).   */
+phfem_status phfem_pipeline_from_host(phfem_ctx* ctx, const double* coords,
+                                      const int32_t* elements, const int32_t* dirichlet,
+                                      const int32_t* neumann, int32_t nC, int32_t nE, int32_t nD,
+                                      int32_t nN, int levels, const phfem_coeffs* c,
+                                      const phfem_field* f, const phfem_field* g,
+                                      const phfem_field* uD, double t, phfem_pipeline_out* out);
+typedef struct phfem_pipeline_host {
+  double* coords; int32_t* elements; int32_t* dirichlet; int32_t* neumann;
+  int32_t* edge_nodes; int32_t* edge_elements; int32_t* local_in_tplus; int32_t* local_in_tminus;
+  int32_t* interior_edges; int32_t* boundary_edges; int32_t* elem_edge;
+  int32_t* dirichlet_edge_ids; int32_t* neumann_edge_ids; int32_t* retained_edges;
+  int32_t* retained_pos;
+  int32_t* C_row_ptr; int32_t* C_col_idx; double* C_values;
+  double* B; double* D; double* M; double* M0; double* load; double* bd;
+} phfem_pipeline_host;
+phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipeline_out* out,
+                                     const phfem_pipeline_host* dst);
+/* bytes phfem_pipeline_download moves for a given `out` and selection */
+int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* out, const phfem_pipeline_host* dst);
+
+/* ---- host <-> device helpers for bindings without a CUDA runtime --------- */
+phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
+phfem_status phfem_memcpy_d2h(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHFEM_GPU_H */

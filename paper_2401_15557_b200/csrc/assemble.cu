@@ -1,0 +1,541 @@
+// assemble.cu — assembly on sm_100a: element blocks + load (one fused element
+// pass), the coupling matrix C (CSR, and the reference's Eigen CSC layout),
+// the Neumann and Dirichlet vectors.
+//
+// Reference: proj/src/assembly.cpp:17-242, sparse.cpp:30-120.
+// Values are bit-identical to the reference: the kernels evaluate the same
+// expressions in the same order (phfem_fields.h) and the library is built with
+// --fmad=false, so no FMA contraction changes a rounding.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace phfem {
+
+// ---------------------------------------------------------------------------
+// Element pass.  One thread per element, 128 elements per tile; every output
+// block goes through a shared-memory tile so the global stores are fully
+// coalesced 16-byte vectors (the per-thread 72-byte blocks would otherwise
+// scatter each store instruction over 32 sectors).
+constexpr int kVolThreads = 128;
+
+__device__ __forceinline__ void tile_store(double* __restrict__ g, int64_t base, int n_valid,
+                                           int per, const double* vals, double* tile, bool vec) {
+  __syncthreads();
+  for (int k = 0; k < per; ++k) tile[threadIdx.x * per + k] = vals[k];
+  __syncthreads();
+  const int count = n_valid * per;
+  double* dst = g + base * per;
+  if (vec) {
+    const double2* src2 = reinterpret_cast<const double2*>(tile);
+    double2* dst2 = reinterpret_cast<double2*>(dst);
+    for (int i = threadIdx.x; i < count / 2; i += blockDim.x) dst2[i] = src2[i];
+    if ((count & 1) && threadIdx.x == 0) dst[count - 1] = tile[count - 1];
+  } else {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = tile[i];
+  }
+}
+
+template <bool kBlocks, bool kLoad>
+__global__ void __launch_bounds__(kVolThreads) k_volume(VolArgs a, phfem_dev_errors* err) {
+  __shared__ __align__(16) double tile[kVolThreads * 9];
+  const int64_t ntiles = ((int64_t)a.nE + kVolThreads - 1) / kVolThreads;
+  for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
+    const int64_t base = tb * kVolThreads;
+    const int n_valid = (int)((int64_t)a.nE - base < kVolThreads ? (int64_t)a.nE - base : kVolThreads);
+    const int64_t m = base + threadIdx.x;
+    const bool valid = threadIdx.x < n_valid;
+    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(1.0, 0.0), v2 = make_double2(0.0, 1.0);
+    if (valid) {
+      const int i0 = __ldg(a.elements + 3 * m), i1 = __ldg(a.elements + 3 * m + 1),
+                i2 = __ldg(a.elements + 3 * m + 2);
+      v0 = __ldg(a.coords + i0);
+      v1 = __ldg(a.coords + i1);
+      v2 = __ldg(a.coords + i2);
+    }
+    if (kBlocks) {
+      const phfem_coeff_values cv = phfem_coeffs_eval(&a.coeffs, v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      double b[9], d[9], mm[9], m0[9];
+      const double t2 = phfem_local_blocks(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, &cv, b, d, mm, m0);
+      if (valid && !(t2 > 0.0)) atomicMin(&err->degenerate, (unsigned long long)m);
+      if (a.B) tile_store(a.B, base, n_valid, 9, b, tile, a.vec);
+      if (a.D) tile_store(a.D, base, n_valid, 9, d, tile, a.vec);
+      if (a.M) tile_store(a.M, base, n_valid, 9, mm, tile, a.vec);
+      if (a.M0) tile_store(a.M0, base, n_valid, 9, m0, tile, a.vec);
+    }
+    if (kLoad) {
+      double bl[3];
+      element_load(v0, v1, v2, &a.f, a.t, bl, valid, m, err);
+      tile_store(a.load, base, n_valid, 3, bl, tile, a.vec);
+    }
+  }
+}
+
+phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool load) {
+  if (a.nE == 0) return PHFEM_OK;
+  const int64_t ntiles = ((int64_t)a.nE + kVolThreads - 1) / kVolThreads;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 16);
+  if (blocks && load)
+    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<true, true><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
+  else if (blocks)
+    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<true, false><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
+  else
+    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<false, true><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
+  return PHFEM_OK;
+}
+
+static bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+VolArgs make_vol_args(const phfem_mesh* mesh) {
+  VolArgs a;
+  memset(&a, 0, sizeof a);
+  a.coords = (const double2*)mesh->coords;
+  a.elements = mesh->elements;
+  a.nE = mesh->nE;
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// C in CSR: one CTA per 1024 consecutive edges.  Row pointers come from the
+// per-block boundary / Neumann prefixes of classify_edges plus an in-block scan
+// (a retained boundary row holds 2 entries, an interior row 4).
+__global__ void __launch_bounds__(1024) k_constraint_csr(
+    const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
+    const int32_t* __restrict__ edge_elements, const int32_t* __restrict__ ltp,
+    const int32_t* __restrict__ ltm, const int32_t* __restrict__ rpos,
+    const int32_t* __restrict__ pre_bnd, const int32_t* __restrict__ pre_neu, int E, int L,
+    int32_t* __restrict__ row_ptr, int32_t* __restrict__ col, double* __restrict__ val) {
+  __shared__ int32_t sm[33];
+  const int blk = blockIdx.x;
+  const int64_t e = (int64_t)blk * 1024 + threadIdx.x;
+  const bool valid = e < E;
+  const int rp = valid ? rpos[e] : -1;
+  const int2 el = valid ? reinterpret_cast<const int2*>(edge_elements)[e] : make_int2(0, 0);
+  const int rb = (valid && rp >= 0 && el.y < 0) ? 1 : 0;
+  int tot;
+  const int ex = block_exclusive_scan(rb, sm, &tot);
+  if (!valid || rp < 0) return;
+  const int bret = pre_bnd[blk] - pre_neu[blk] + ex;
+  int k = 4 * rp - 2 * bret;
+  row_ptr[rp] = k;
+  const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+  const double2 pa = __ldg(coords + ab.x), pb = __ldg(coords + ab.y);
+  const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+  const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+  const int led = ltp[e];
+  const double vp = len * 0.5;     // lengths[e] * kR[led][c]   (assembly.cpp:160)
+  const double vm = -len * 0.5;    // -lengths[e] * kR[ledtn][c] (assembly.cpp:164)
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    if (c != led) {
+      col[k] = 3 * el.x + c;
+      val[k] = vp;
+      ++k;
+    }
+  if (el.y >= 0) {
+    const int ledtn = ltm[e];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (c != ledtn) {
+        col[k] = 3 * el.y + c;
+        val[k] = vm;
+        ++k;
+      }
+  }
+  if (rp == L - 1) row_ptr[L] = k;
+}
+
+// C in Eigen CSC (column = primal DOF 3m+c; <= 2 entries, rows ascending).
+__device__ __forceinline__ void csc_entries(const double2* __restrict__ coords,
+                                            const int32_t* __restrict__ elements,
+                                            const int32_t* __restrict__ elem_edge,
+                                            const int32_t* __restrict__ rpos, int64_t m,
+                                            int rows[3], double vals[3]) {
+  const int t[3] = {__ldg(elements + 3 * m), __ldg(elements + 3 * m + 1), __ldg(elements + 3 * m + 2)};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int s = __ldg(elem_edge + 3 * m + k);
+    const int e = s >= 0 ? s : ~s;
+    rows[k] = rpos[e];
+    const double2 pa = __ldg(coords + t[(k + 1) % 3]), pb = __ldg(coords + t[(k + 2) % 3]);
+    const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+    const double len = sqrt(dx * dx + dy * dy);
+    vals[k] = s >= 0 ? len * 0.5 : -len * 0.5;
+  }
+}
+
+__global__ void k_csc_count(const int32_t* __restrict__ elem_edge, const int32_t* __restrict__ rpos,
+                            int nE, int32_t* __restrict__ counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
+    int r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int s = elem_edge[3 * m + k];
+      r[k] = rpos[s >= 0 ? s : ~s] >= 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) counts[3 * m + c] = r[(c + 1) % 3] + r[(c + 2) % 3];
+  }
+}
+
+__global__ void k_csc_fill(const double2* __restrict__ coords, const int32_t* __restrict__ elements,
+                           const int32_t* __restrict__ elem_edge, const int32_t* __restrict__ rpos,
+                           int nE, const int32_t* __restrict__ outer, int32_t* __restrict__ inner,
+                           double* __restrict__ values) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
+    int rows[3];
+    double vals[3];
+    csc_entries(coords, elements, elem_edge, rpos, m, rows, vals);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      int ka = (c + 1) % 3, kb = (c + 2) % 3;
+      if (rows[kb] >= 0 && (rows[ka] < 0 || rows[kb] < rows[ka])) {
+        const int x = ka;
+        ka = kb;
+        kb = x;
+      }
+      int p = outer[3 * m + c];
+      if (rows[ka] >= 0) {
+        inner[p] = rows[ka];
+        values[p] = vals[ka];
+        ++p;
+      }
+      if (rows[kb] >= 0) {
+        inner[p] = rows[kb];
+        values[p] = vals[kb];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Neumann: entries grouped by their t_plus element in a small open-addressing
+// table (one slot per element carrying Neumann edges).  Per DOF at most two
+// entries carry a non-zero term, so the float sum is order independent and
+// atomics reproduce scatter_add exactly; a duplicated Neumann pair (more terms)
+// switches to a single-thread pass in list order.
+__global__ void k_neu_insert(const int32_t* __restrict__ neu_ids, int nN,
+                             const int32_t* __restrict__ edge_elements, int cap,
+                             int32_t* __restrict__ keys, int32_t* __restrict__ slot_of) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nN;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = edge_elements[2 * neu_ids[i]];
+    uint32_t h = ((uint32_t)m * 2654435761u) & (uint32_t)(cap - 1);
+    while (true) {
+      const int prev = atomicCAS(&keys[h], -1, m);
+      if (prev == -1 || prev == m) break;
+      h = (h + 1) & (uint32_t)(cap - 1);
+    }
+    slot_of[i] = (int)h;
+  }
+}
+
+__device__ __forceinline__ void neu_entry(const NeuArgs& a, int64_t i, double t, double v[3],
+                                          phfem_dev_errors* err) {
+  const int e = a.neu_ids[i];
+  const int2 ab = reinterpret_cast<const int2*>(a.edge_nodes)[e];
+  const double2 pa = a.coords[ab.x], pb = a.coords[ab.y];
+  const double midx = 0.5 * (pa.x + pb.x), midy = 0.5 * (pa.y + pb.y);
+  const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+  const double length = sqrt(dx * dx + dy * dy);
+  const double nx = dy / length, ny = -dx / length;
+  const double g = phfem_flux_eval(&a.g, midx, midy, nx, ny, t);
+  if (!isfinite(g)) atomicMin(&err->flux_nan, (unsigned long long)i);
+  const int led = a.ltp[e];
+  const double lg = length * g;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) v[c] = lg * (c == led ? 0.0 : 0.5);  // length*value*kR[led][c]
+}
+
+__global__ void k_neu_values(NeuArgs a, double t, int seq, phfem_dev_errors* err) {
+  if (seq) {  // exact list-order accumulation (duplicated pairs)
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int64_t i = 0; i < a.nN; ++i) {
+      double v[3];
+      neu_entry(a, i, t, v, err);
+      const int s = a.slot_of[i];
+      for (int c = 0; c < 3; ++c) a.vals[3 * s + c] += v[c];
+    }
+    return;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.nN;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[3];
+    neu_entry(a, i, t, v, err);
+    const int s = a.slot_of[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) atomicAdd(&a.vals[3 * s + c], v[c]);
+  }
+}
+
+__global__ void k_neu_apply(const int32_t* __restrict__ keys, const double* __restrict__ vals,
+                            int cap, double* __restrict__ out, int accumulate) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int m = keys[s];
+    if (m < 0) continue;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = vals[3 * s + c];
+      out[3 * (int64_t)m + c] = accumulate ? out[3 * (int64_t)m + c] + v : v;
+    }
+  }
+}
+
+phfem_status neu_table_build(phfem_ctx* ctx, const phfem_topology* topo,
+                             const phfem_classification* cls, NeuTable* tab) {
+  memset(tab, 0, sizeof(*tab));
+  tab->nN = cls->nN;
+  if (cls->nN == 0) return PHFEM_OK;
+  int cap = 64;
+  while (cap < 2 * cls->nN) cap <<= 1;
+  tab->cap = cap;
+  tab->seq = (cls->flags & PHFEM_CLS_DUP_NEUMANN) ? 1 : 0;
+  PHFEM_TRY(dalloc(ctx, &tab->keys, cap));
+  PHFEM_TRY(dalloc(ctx, &tab->slot_of, cls->nN));
+  PHFEM_TRY(dalloc(ctx, &tab->vals, 3 * (int64_t)cap));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tab->keys, 0xff, sizeof(int32_t) * cap, ctx->stream));
+  PHFEM_LAUNCH(ctx, "k_neu_insert", k_neu_insert<<<grid_for(cls->nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      cls->neumann_edge_ids, cls->nN, topo->edge_elements, cap, tab->keys, tab->slot_of));
+  return PHFEM_OK;
+}
+
+void neu_table_free(phfem_ctx* ctx, NeuTable* tab) {
+  dfree(ctx, tab->keys);
+  dfree(ctx, tab->slot_of);
+  dfree(ctx, tab->vals);
+}
+
+phfem_status neu_table_eval(phfem_ctx* ctx, const NeuTable* tab, const phfem_mesh* mesh,
+                            const phfem_topology* topo, const phfem_classification* cls,
+                            const phfem_field* g, double t, double* vals) {
+  if (tab->nN == 0) return PHFEM_OK;
+  NeuArgs a;
+  a.coords = (const double2*)mesh->coords;
+  a.edge_nodes = topo->edge_nodes;
+  a.ltp = topo->local_in_tplus;
+  a.neu_ids = cls->neumann_edge_ids;
+  a.slot_of = tab->slot_of;
+  a.nN = tab->nN;
+  a.g = *g;
+  a.vals = vals;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(vals, 0, sizeof(double) * 3 * tab->cap, ctx->stream));
+  PHFEM_LAUNCH(ctx, "k_neu_values", k_neu_values<<<tab->seq ? 1 : grid_for(tab->nN, 256, ctx->num_sms * 4), tab->seq ? 1 : 256, 0,
+                 ctx->stream>>>(a, t, tab->seq, ctx->derr));
+  return PHFEM_OK;
+}
+
+phfem_status neu_flux_error(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                            const phfem_classification* cls) {
+  const uint64_t fe = ctx->herr->flux_nan;
+  if (fe == ~0ull) return PHFEM_OK;
+  int32_t e = 0;
+  int32_t ab[2] = {0, 0};
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&e, cls->neumann_edge_ids + fe, sizeof e, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(ab, topo->edge_nodes + 2 * (int64_t)e, sizeof ab,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  (void)mesh;
+  return set_error(ctx, PHFEM_ERR_NONFINITE,
+                   "assemble_neumann: non-finite flux sample on edge (%d,%d)", ab[0] + 1, ab[1] + 1);
+}
+
+phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                          const phfem_classification* cls, const phfem_field* g, double t,
+                          double* out, int accumulate, bool check) {
+  if (cls->nN == 0) return PHFEM_OK;
+  NeuTable tab;
+  PHFEM_TRY(neu_table_build(ctx, topo, cls, &tab));
+  if (check) PHFEM_TRY(errors_reset(ctx));
+  PHFEM_TRY(neu_table_eval(ctx, &tab, mesh, topo, cls, g, t, tab.vals));
+  PHFEM_LAUNCH(ctx, "k_neu_apply", k_neu_apply<<<grid_for(tab.cap, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      tab.keys, tab.vals, tab.cap, out, accumulate));
+  neu_table_free(ctx, &tab);
+  if (check) {
+    PHFEM_TRY(errors_fetch(ctx));
+    PHFEM_TRY(neu_flux_error(ctx, mesh, topo, cls));
+  }
+  return PHFEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_dirichlet(const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
+                            const int32_t* __restrict__ dir_ids, int nD,
+                            const int32_t* __restrict__ rpos, phfem_field uD, double t,
+                            double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nD;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = dir_ids[i];
+    const int pos = rpos[e];
+    if (pos < 0) continue;  // pair listed as both Dirichlet and Neumann
+    const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+    const double2 pa = coords[ab.x], pb = coords[ab.y];
+    const double midx = 0.5 * (pa.x + pb.x), midy = 0.5 * (pa.y + pb.y);
+    const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+    const double length = sqrt(dx * dx + dy * dy);
+    out[pos] = -length * phfem_field_eval(&uD, midx, midy, t);  // assembly.cpp:239
+  }
+}
+
+phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                            const phfem_classification* cls, const phfem_field* uD, double t,
+                            double* out) {
+  if (cls->L > 0)
+    PHFEM_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * cls->L, ctx->stream));
+  if (cls->nD == 0) return PHFEM_OK;
+  PHFEM_LAUNCH(ctx, "k_dirichlet", k_dirichlet<<<grid_for(cls->nD, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      (const double2*)mesh->coords, topo->edge_nodes, cls->dirichlet_edge_ids, cls->nD,
+      cls->retained_pos, *uD, t, out));
+  return PHFEM_OK;
+}
+
+phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                 const phfem_topology* topo, const phfem_classification* cls,
+                                 phfem_csr* out) {
+  memset(out, 0, sizeof(*out));
+  const int E = topo->E, L = cls->L;
+  const int nblk = (E + 1023) / 1024;
+  out->rows = L;
+  out->cols = 3 * mesh->nE;
+  const int64_t bret_total = (int64_t)topo->n_boundary - (int64_t)(E - L);
+  out->nnz = 4 * (int64_t)L - 2 * bret_total;
+  PHFEM_TRY(dalloc(ctx, &out->row_ptr, (int64_t)L + 1));
+  PHFEM_TRY(dalloc(ctx, &out->col_idx, out->nnz));
+  PHFEM_TRY(dalloc(ctx, &out->values, out->nnz));
+  if (L == 0) {
+    PHFEM_CUDA(ctx, cudaMemsetAsync(out->row_ptr, 0, sizeof(int32_t), ctx->stream));
+    return PHFEM_OK;
+  }
+  PHFEM_LAUNCH(ctx, "k_constraint_csr", k_constraint_csr<<<nblk, 1024, 0, ctx->stream>>>(
+      (const double2*)mesh->coords, topo->edge_nodes, topo->edge_elements, topo->local_in_tplus,
+      topo->local_in_tminus, cls->retained_pos, cls->block_prefix, cls->block_prefix + nblk + 1, E,
+      L, out->row_ptr, out->col_idx, out->values));
+  return PHFEM_OK;
+}
+
+phfem_status volume_errors(phfem_ctx* ctx, bool blocks, bool load) {
+  if (blocks && ctx->herr->degenerate != ~0ull)
+    return set_error(ctx, PHFEM_ERR_DEGENERATE,
+                     "local_element_matrices: degenerate or non-CCW triangle");
+  if (load && ctx->herr->load_nan != ~0ull)
+    return set_error(ctx, PHFEM_ERR_NONFINITE,
+                     "assemble_load: non-finite load sample in element %llu",
+                     (unsigned long long)ctx->herr->load_nan + 1ull);
+  return PHFEM_OK;
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API phfem_status phfem_assemble_volume(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                             const phfem_coeffs* c, double* B, double* D,
+                                             double* M, double* M0) {
+  if (!ctx || !mesh || !c) return PHFEM_ERR_INVALID_ARGUMENT;
+  VolArgs a = make_vol_args(mesh);
+  a.coeffs = *c;
+  a.B = B;
+  a.D = D;
+  a.M = M;
+  a.M0 = M0;
+  a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0);
+  PHFEM_TRY(errors_reset(ctx));
+  PHFEM_TRY(launch_volume(ctx, a, true, false));
+  PHFEM_TRY(errors_fetch(ctx));
+  return volume_errors(ctx, true, false);
+}
+
+PHFEM_API phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                           const phfem_field* f, double t, double* out) {
+  if (!ctx || !mesh || !f || (!out && mesh->nE)) return PHFEM_ERR_INVALID_ARGUMENT;
+  VolArgs a = make_vol_args(mesh);
+  a.f = *f;
+  a.t = t;
+  a.load = out;
+  a.vec = aligned16(out);
+  PHFEM_TRY(errors_reset(ctx));
+  PHFEM_TRY(launch_volume(ctx, a, false, true));
+  PHFEM_TRY(errors_fetch(ctx));
+  return volume_errors(ctx, false, true);
+}
+
+PHFEM_API phfem_status phfem_assemble_constraint(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                                 const phfem_topology* topo,
+                                                 const phfem_classification* cls,
+                                                 phfem_csr* out) {
+  if (!ctx || !mesh || !topo || !cls || !out) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (cls->E != topo->E)
+    return set_error(ctx, PHFEM_ERR_MISMATCH,
+                     "assemble_constraint: classification does not match topology");
+  return constraint_csr_into(ctx, mesh, topo, cls, out);
+}
+
+PHFEM_API void phfem_csr_release(phfem_ctx* ctx, phfem_csr* m) {
+  if (!m) return;
+  dfree(ctx, m->row_ptr);
+  dfree(ctx, m->col_idx);
+  dfree(ctx, m->values);
+  m->nnz = 0;
+}
+
+PHFEM_API phfem_status phfem_constraint_csc(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                            const phfem_topology* topo,
+                                            const phfem_classification* cls, phfem_csc* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !mesh || !topo || !cls) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (cls->E != topo->E)
+    return set_error(ctx, PHFEM_ERR_MISMATCH,
+                     "assemble_constraint: classification does not match topology");
+  const int64_t N = 3 * (int64_t)mesh->nE;
+  out->rows = cls->L;
+  out->cols = (int32_t)N;
+  const int64_t bret_total = (int64_t)topo->n_boundary - (int64_t)(topo->E - cls->L);
+  out->nnz = 4 * (int64_t)cls->L - 2 * bret_total;
+  PHFEM_TRY(dalloc(ctx, &out->outer, N + 1));
+  PHFEM_TRY(dalloc(ctx, &out->inner, out->nnz));
+  PHFEM_TRY(dalloc(ctx, &out->values, out->nnz));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->outer + N, 0, sizeof(int32_t), ctx->stream));
+  if (N > 0) {
+    PHFEM_LAUNCH(ctx, "k_csc_count", k_csc_count<<<grid_for(mesh->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        topo->elem_edge, cls->retained_pos, mesh->nE, out->outer));
+  }
+  PHFEM_TRY(scan_exclusive_i32(ctx, out->outer, out->outer, N + 1, nullptr));
+  if (N > 0) {
+    PHFEM_LAUNCH(ctx, "k_csc_fill", k_csc_fill<<<grid_for(mesh->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        (const double2*)mesh->coords, mesh->elements, topo->elem_edge, cls->retained_pos,
+        mesh->nE, out->outer, out->inner, out->values));
+  }
+  return PHFEM_OK;
+}
+
+PHFEM_API void phfem_csc_release(phfem_ctx* ctx, phfem_csc* m) {
+  if (!m) return;
+  dfree(ctx, m->outer);
+  dfree(ctx, m->inner);
+  dfree(ctx, m->values);
+  m->nnz = 0;
+}
+
+PHFEM_API phfem_status phfem_assemble_neumann(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                              const phfem_topology* topo,
+                                              const phfem_classification* cls,
+                                              const phfem_field* g, double t, double* out,
+                                              int accumulate) {
+  if (!ctx || !mesh || !topo || !cls || !g) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (!accumulate && mesh->nE > 0)
+    PHFEM_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * 3 * (int64_t)mesh->nE, ctx->stream));
+  return neumann_into(ctx, mesh, topo, cls, g, t, out, accumulate, true);
+}
+
+PHFEM_API phfem_status phfem_assemble_dirichlet(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                                const phfem_topology* topo,
+                                                const phfem_classification* cls,
+                                                const phfem_field* uD, double t, double* out) {
+  if (!ctx || !mesh || !topo || !cls || !uD) return PHFEM_ERR_INVALID_ARGUMENT;
+  return dirichlet_into(ctx, mesh, topo, cls, uD, t, out);
+}

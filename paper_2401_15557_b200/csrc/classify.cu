@@ -1,0 +1,181 @@
+// classify.cu — classify_edges on sm_100a.
+//
+// Reference: proj/src/edge_topology.cpp:145-177.  Boundary pairs are resolved
+// through the max-node grouping table written by build_topology (edges of one
+// max node are a contiguous id range sorted by min node -> binary search),
+// the Neumann set becomes a bitmap, and retained_pos / retained_edges come
+// from per-1024-edge block prefixes of that bitmap (the reference's E-length
+// flag loop, :166-174).  Per-block boundary prefixes (from the ascending
+// boundary list) are kept for the CSR row pointers of C.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace phfem {
+
+constexpr int kEdgeBlock = 1024;
+
+__global__ void k_cls_pairs(const int32_t* __restrict__ dir_pairs, int nD,
+                            const int32_t* __restrict__ neu_pairs, int nN,
+                            const int32_t* __restrict__ nes, const int32_t* __restrict__ edge_nodes,
+                            const int32_t* __restrict__ edge_elements, int nC,
+                            int32_t* __restrict__ dir_ids, int32_t* __restrict__ neu_ids,
+                            uint32_t* __restrict__ bits, phfem_dev_errors* err) {
+  const int64_t total = (int64_t)nD + nN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_d = i < nD;
+    const int64_t j = is_d ? i : i - nD;
+    const int32_t* pr = is_d ? dir_pairs : neu_pairs;
+    const int a = pr[2 * j], b = pr[2 * j + 1];
+    const int e = find_edge(nes, edge_nodes, nC, a, b);
+    if (e < 0) {
+      atomicMin(&err->classify, ((unsigned long long)i << 2) | 0ull);
+      continue;
+    }
+    if (edge_elements[2 * e + 1] >= 0) {
+      atomicMin(&err->classify, ((unsigned long long)i << 2) | 1ull);
+      continue;
+    }
+    if (is_d) {
+      dir_ids[j] = e;
+    } else {
+      neu_ids[j] = e;
+      const uint32_t bit = 1u << (e & 31);
+      const uint32_t old = atomicOr(&bits[e >> 5], bit);
+      if (old & bit) err->counters[5] = 1;  // duplicate Neumann pair
+    }
+  }
+}
+
+// One thread per 1024-edge block: Neumann count (bitmap popcount) and boundary
+// count (two lower_bounds into the ascending boundary list).
+__global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
+                                   const int32_t* __restrict__ boundary, int nB, int E, int nblk,
+                                   int32_t* __restrict__ cnt_bnd, int32_t* __restrict__ cnt_neu) {
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk > nblk) return;
+  if (blk == nblk) {
+    cnt_bnd[blk] = 0;
+    cnt_neu[blk] = 0;
+    return;
+  }
+  const int nwords = (E + 31) >> 5;
+  int nn = 0;
+  for (int w = blk * 32; w < min(nwords, blk * 32 + 32); ++w) nn += __popc(bits[w]);
+  auto lower = [&](int key) {
+    int l = 0, r = nB;
+    while (l < r) {
+      const int mid = (l + r) >> 1;
+      if (boundary[mid] < key) l = mid + 1;
+      else r = mid;
+    }
+    return l;
+  };
+  cnt_bnd[blk] = lower(min(E, (blk + 1) * kEdgeBlock)) - lower(blk * kEdgeBlock);
+  cnt_neu[blk] = nn;
+}
+
+// CTA of 1024 threads per block of 1024 edges; warp w owns bitmap word w.
+__global__ void __launch_bounds__(kEdgeBlock) k_cls_retained(const uint32_t* __restrict__ bits,
+                                                             const int32_t* __restrict__ pre_neu,
+                                                             int E, int32_t* __restrict__ rpos,
+                                                             int32_t* __restrict__ redges) {
+  __shared__ int32_t wsum[32];
+  const int blk = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blk * kEdgeBlock + threadIdx.x;
+  const int64_t wi = (int64_t)blk * 32 + warp;
+  const uint32_t word = (wi < ((E + 31) >> 5)) ? bits[wi] : 0u;
+  if (lane == 0) wsum[warp] = __popc(word);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = wsum[lane];
+    const int inc = warp_inclusive_scan(v);
+    wsum[lane] = inc - v;
+  }
+  __syncthreads();
+  if (e >= E) return;
+  const int before = pre_neu[blk] + wsum[warp] + __popc(word & ((1u << lane) - 1u));
+  if ((word >> lane) & 1u) {
+    rpos[e] = -1;
+  } else {
+    const int r = (int)e - before;
+    rpos[e] = r;
+    redges[r] = (int)e;
+  }
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API void phfem_classification_release(phfem_ctx* ctx, phfem_classification* c) {
+  if (!c) return;
+  dfree(ctx, c->dirichlet_edge_ids);
+  dfree(ctx, c->neumann_edge_ids);
+  dfree(ctx, c->retained_edges);
+  dfree(ctx, c->retained_pos);
+  dfree(ctx, c->neumann_bits);
+  dfree(ctx, c->block_prefix);
+  c->L = 0;
+}
+
+PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology* topo,
+                                            const phfem_mesh* mesh, phfem_classification* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !topo || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
+  const int E = topo->E, nD = mesh->nD, nN = mesh->nN;
+  out->nD = nD;
+  out->nN = nN;
+  out->E = E;
+  const int nblk = (E + kEdgeBlock - 1) / kEdgeBlock;
+  const int nwords = (E + 31) / 32;
+  PHFEM_TRY(dalloc(ctx, &out->dirichlet_edge_ids, nD));
+  PHFEM_TRY(dalloc(ctx, &out->neumann_edge_ids, nN));
+  PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
+  PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
+  PHFEM_TRY(dalloc(ctx, &out->neumann_bits, nwords));
+  PHFEM_TRY(dalloc(ctx, &out->block_prefix, 2 * ((int64_t)nblk + 1)));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->neumann_bits, 0, sizeof(uint32_t) * std::max(nwords, 1),
+                                  ctx->stream));
+  PHFEM_TRY(errors_reset(ctx));
+  if ((int64_t)nD + nN > 0) {
+    PHFEM_LAUNCH(ctx, "k_cls_pairs", k_cls_pairs<<<grid_for((int64_t)nD + nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        mesh->dirichlet, nD, mesh->neumann, nN, topo->node_edge_start, topo->edge_nodes,
+        topo->edge_elements, topo->nC, out->dirichlet_edge_ids, out->neumann_edge_ids,
+        out->neumann_bits, ctx->derr));
+  }
+  int32_t* pre_bnd = out->block_prefix;
+  int32_t* pre_neu = out->block_prefix + nblk + 1;
+  PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
+      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, pre_bnd, pre_neu));
+  PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
+  if (nblk > 0) {
+    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, kEdgeBlock, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
+                                                         out->retained_pos, out->retained_edges));
+  }
+  // total Neumann count rides back with the error words (one sync)
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[8], pre_neu + nblk, sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_TRY(errors_fetch(ctx));
+  const uint64_t ce = ctx->herr->classify;
+  if (ce != ~0ull) {
+    const int64_t pos = (int64_t)(ce >> 2);
+    const bool interior = ce & 1ull;
+    const bool is_d = pos < nD;
+    const int32_t* src = is_d ? mesh->dirichlet + 2 * pos : mesh->neumann + 2 * (pos - nD);
+    int32_t pr[2] = {0, 0};
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(pr, src, sizeof pr, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    phfem_classification_release(ctx, out);
+    return set_error(ctx, interior ? PHFEM_ERR_INTERIOR_BOUNDARY : PHFEM_ERR_NOT_AN_EDGE,
+                     interior ? "%s pair (%d,%d) resolves to an interior edge"
+                              : "%s pair (%d,%d) is not an edge",
+                     is_d ? "dirichlet" : "neumann", pr[0] + 1, pr[1] + 1);
+  }
+  out->L = E - (int32_t)(ctx->herr->counters[8] & 0xffffffffu);
+  out->flags = ctx->herr->counters[5] ? PHFEM_CLS_DUP_NEUMANN : 0;
+  return PHFEM_OK;
+}

@@ -1,0 +1,207 @@
+// common.cuh — shared plumbing for the sm_100a kernels behind include/phfem_gpu.h:
+// the context (device, stream, stream-ordered pool, device error words), status
+// helpers and the block/device scan primitives the edge and element passes use.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/phfem_gpu.h"
+
+#define PHFEM_API extern "C" __attribute__((visibility("default")))
+
+// Device-side error words, one per failure family.  Each holds an ordering
+// key (smaller = what the reference would have hit first) and is merged with
+// atomicMin, so the host reports exactly the reference's first exception.
+struct phfem_dev_errors {
+  unsigned long long topo;      // (hi<<33)|(lo<<2)|(dup<<1)|dir, canonical order
+  unsigned long long classify;  // (list position<<2)|code
+  unsigned long long degenerate;// element id
+  unsigned long long load_nan;  // element id
+  unsigned long long flux_nan;  // neumann list position
+  unsigned long long misc;      // refine mismatch etc.
+  unsigned long long counters[10];  // small per-call results (E, nI, nB, max bucket, dup flags...)
+};
+
+struct phfem_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaMemPool_t pool = nullptr;
+  phfem_dev_errors* derr = nullptr;   // device
+  phfem_dev_errors* herr = nullptr;   // pinned host mirror
+  int64_t launches = 0;
+  int num_sms = 148;
+  std::string message;
+  // per-launch CUDA-event timing (phfem_ctx_profile): events recorded on the
+  // ctx stream around every kernel, aggregated per kernel name on read
+  bool prof = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> free_events;
+};
+
+namespace phfem {
+
+phfem_status set_error(phfem_ctx* ctx, phfem_status st, const char* fmt, ...);
+phfem_status cuda_fail(phfem_ctx* ctx, cudaError_t e, const char* where);
+
+#define PHFEM_CUDA(ctx, call)                                   \
+  do {                                                          \
+    cudaError_t _e = (call);                                    \
+    if (_e != cudaSuccess) return ::phfem::cuda_fail(ctx, _e, #call); \
+  } while (0)
+
+#define PHFEM_CHECK_LAUNCH(ctx)                                         \
+  do {                                                                  \
+    (ctx)->launches++;                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return ::phfem::cuda_fail(ctx, _e, "kernel launch"); \
+  } while (0)
+
+// Launch + error check + (when profiling) a CUDA-event pair around the launch.
+#define PHFEM_LAUNCH(ctx, name, ...)        \
+  do {                                      \
+    ::phfem::KTimer _kt(ctx, name);         \
+    __VA_ARGS__;                            \
+    PHFEM_CHECK_LAUNCH(ctx);                \
+  } while (0)
+
+#define PHFEM_TRY(expr)                 \
+  do {                                  \
+    phfem_status _s = (expr);           \
+    if (_s != PHFEM_OK) return _s;      \
+  } while (0)
+
+template <typename T>
+phfem_status dalloc(phfem_ctx* ctx, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMallocFromPoolAsync((void**)p, count * sizeof(T), ctx->pool, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, PHFEM_ERR_OOM, "phfem: device allocation of %zu bytes failed (%s)",
+                     count * sizeof(T), cudaGetErrorString(e));
+  }
+  return PHFEM_OK;
+}
+
+template <typename T>
+void dfree(phfem_ctx* ctx, T*& p) {
+  if (p) cudaFreeAsync((void*)p, ctx->stream);
+  p = nullptr;
+}
+
+// RAII timer: records an event pair around the launches in its scope when
+// profiling is enabled on the ctx.
+class KTimer {
+ public:
+  KTimer(phfem_ctx* ctx, const char* name);
+  ~KTimer();
+
+ private:
+  phfem_ctx* ctx_;
+  const char* name_;
+  cudaEvent_t a_ = nullptr;
+};
+
+// Reset the device error words (async) / fetch them (sync).
+phfem_status errors_reset(phfem_ctx* ctx);
+phfem_status errors_fetch(phfem_ctx* ctx);
+
+inline int grid_for(int64_t n, int block, int max_blocks) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// Device-wide exclusive scan of int32 counts (3 launches: tile reduce, scan of
+// tile sums, downsweep).  out may alias in.  Writes the total to *total_dev.
+phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
+                                int32_t* total_dev);
+
+}  // namespace phfem
+
+// ---------------------------------------------------------------------------
+// Warp / block helpers usable in every .cu
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if ((int)lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_reduce_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Edge id of the node pair (a, b) through the max-node grouping table of
+// build_topology: edges with larger node hi occupy ids [nes[hi], nes[hi+1]),
+// ascending by smaller node.  -1 when (a, b) is not an edge (the reference's
+// node_pair_to_edge contract, edge_topology.cpp:36-43).
+__device__ __forceinline__ int find_edge(const int32_t* __restrict__ nes,
+                                         const int32_t* __restrict__ edge_nodes, int nC, int a,
+                                         int b) {
+  const int lo = a < b ? a : b;
+  const int hi = a < b ? b : a;
+  if (lo < 0 || hi >= nC) return -1;
+  int l = nes[hi], r = nes[hi + 1];  // edges with max node hi, ascending min node
+  while (l < r) {
+    const int mid = (l + r) >> 1;
+    const int x = edge_nodes[2 * mid], y = edge_nodes[2 * mid + 1];
+    const int mn = x < y ? x : y;
+    if (mn < lo) l = mid + 1;
+    else r = mid;
+  }
+  if (l < nes[hi + 1]) {
+    const int x = edge_nodes[2 * l], y = edge_nodes[2 * l + 1];
+    if ((x < y ? x : y) == lo) return l;
+  }
+  return -1;
+}
+
+
+// Block exclusive scan of one value per thread; blockDim.x multiple of 32,
+// <= 1024.  `smem` needs 33 slots.  Returns exclusive prefix, *total = sum.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T* total) {
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane_id() == 31) smem[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = (lane_id() < (unsigned)nwarps) ? smem[lane_id()] : T(0);
+    T wi = warp_inclusive_scan(w);
+    if (lane_id() < (unsigned)nwarps) smem[lane_id()] = wi - w;
+    if (lane_id() == 31) smem[32] = wi;
+  }
+  __syncthreads();
+  T res = smem[warp] + inc - v;
+  *total = smem[32];
+  __syncthreads();
+  return res;
+}

@@ -1,0 +1,294 @@
+// ctx.cu — context, stream-ordered memory, error plumbing and the device-wide
+// scan used by the edge / classification passes.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace phfem {
+
+phfem_status set_error(phfem_ctx* ctx, phfem_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->message = buf;
+  return st;
+}
+
+phfem_status cuda_fail(phfem_ctx* ctx, cudaError_t e, const char* where) {
+  cudaGetLastError();
+  return set_error(ctx, e == cudaErrorMemoryAllocation ? PHFEM_ERR_OOM : PHFEM_ERR_CUDA,
+                   "phfem: CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e),
+                   where);
+}
+
+phfem_status errors_reset(phfem_ctx* ctx) {
+  phfem_dev_errors init;
+  memset(&init, 0xff, sizeof init);
+  memset(init.counters, 0, sizeof init.counters);
+  memcpy(ctx->herr, &init, sizeof init);
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(ctx->derr, ctx->herr, sizeof init, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+  return PHFEM_OK;
+}
+
+phfem_status errors_fetch(phfem_ctx* ctx) {
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(phfem_dev_errors),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
+
+static cudaEvent_t take_event(phfem_ctx* ctx) {
+  if (!ctx->free_events.empty()) {
+    cudaEvent_t e = ctx->free_events.back();
+    ctx->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+KTimer::KTimer(phfem_ctx* ctx, const char* name) : ctx_(ctx), name_(name) {
+  if (ctx_ && ctx_->prof) {
+    a_ = take_event(ctx_);
+    cudaEventRecord(a_, ctx_->stream);
+  }
+}
+
+KTimer::~KTimer() {
+  if (a_) {
+    cudaEvent_t b = take_event(ctx_);
+    cudaEventRecord(b, ctx_->stream);
+    ctx_->recs.push_back({name_, a_, b});
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scan: tiles of 4096 int32 (1024 threads x 4).
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 4;
+constexpr int kScanTile = kScanThreads * kScanPer;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const int32_t* __restrict__ in,
+                                                                 int64_t n,
+                                                                 int32_t* __restrict__ sums) {
+  __shared__ int32_t sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) v += in[i];
+  }
+  int32_t tot;
+  block_exclusive_scan(v, sm, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// Single-block exclusive scan of the tile sums (any length).
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(int32_t* sums, int64_t n,
+                                                            int32_t* total) {
+  __shared__ int32_t sm[33];
+  int32_t carry = 0;
+  for (int64_t base = 0; base < n; base += kScanThreads) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < n ? sums[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(v, sm, &tot);
+    if (i < n) sums[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t* in, int32_t* out,
+                                                            int64_t n,
+                                                            const int32_t* __restrict__ sums) {
+  __shared__ int32_t sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  int32_t v[kScanPer];
+  int32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + k;
+    v[k] = i < n ? in[i] : 0;
+    s += v[k];
+  }
+  int32_t tot;
+  int32_t ex = block_exclusive_scan(s, sm, &tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + k;
+    if (i < n) out[i] = ex;
+    ex += v[k];
+  }
+}
+
+phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
+                                int32_t* total_dev) {
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (n == 0) {
+    if (total_dev) PHFEM_CUDA(ctx, cudaMemsetAsync(total_dev, 0, sizeof(int32_t), ctx->stream));
+    return PHFEM_OK;
+  }
+  int32_t* sums = nullptr;
+  PHFEM_TRY(dalloc(ctx, &sums, tiles));
+  // note: the downsweep reads `in` after the tile pass, so in == out is fine
+  // (each tile reads its own range before writing it).
+  KTimer kt(ctx, "scan");
+  k_scan_tile_sums<<<(unsigned)tiles, kScanThreads, 0, ctx->stream>>>(in, n, sums);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan_sums<<<1, kScanThreads, 0, ctx->stream>>>(sums, tiles, total_dev);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan_down<<<(unsigned)tiles, kScanThreads, 0, ctx->stream>>>(in, out, n, sums);
+  PHFEM_CHECK_LAUNCH(ctx);
+  dfree(ctx, sums);
+  return PHFEM_OK;
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API int phfem_abi_version(void) { return PHFEM_ABI_VERSION; }
+
+PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return PHFEM_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) return PHFEM_ERR_INVALID_ARGUMENT;
+  phfem_ctx* ctx = new phfem_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    cudaGetLastError();
+    return PHFEM_ERR_CUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) {
+    ctx->num_sms = prop.multiProcessorCount;
+    if (prop.major < 10) {
+      delete ctx;
+      return PHFEM_ERR_NO_DEVICE;  // sm_100a code only
+    }
+  }
+  if (stream) {
+    ctx->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      cudaGetLastError();
+      return PHFEM_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  if (cudaDeviceGetDefaultMemPool(&ctx->pool, device) != cudaSuccess) {
+    delete ctx;
+    cudaGetLastError();
+    return PHFEM_ERR_CUDA;
+  }
+  uint64_t threshold = UINT64_MAX;  // keep freed blocks cached across pipeline runs
+  cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  if (cudaMalloc((void**)&ctx->derr, sizeof(phfem_dev_errors)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->herr, sizeof(phfem_dev_errors)) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return PHFEM_ERR_OOM;
+  }
+  *out = ctx;
+  return PHFEM_OK;
+}
+
+PHFEM_API void phfem_ctx_destroy(phfem_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& r : ctx->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->free_events) cudaEventDestroy(e);
+  cudaFree(ctx->derr);
+  cudaFreeHost(ctx->herr);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+PHFEM_API const char* phfem_ctx_message(const phfem_ctx* ctx) {
+  return ctx ? ctx->message.c_str() : "";
+}
+
+PHFEM_API void* phfem_ctx_stream(const phfem_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+PHFEM_API int64_t phfem_ctx_launches(const phfem_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+PHFEM_API phfem_status phfem_ctx_sync(phfem_ctx* ctx) {
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_alloc(phfem_ctx* ctx, size_t bytes, void** out) {
+  return dalloc(ctx, (char**)out, bytes);
+}
+
+PHFEM_API void phfem_free(phfem_ctx* ctx, void* ptr) {
+  if (ptr) cudaFreeAsync(ptr, ctx->stream);
+}
+
+PHFEM_API phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PHFEM_OK;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_memcpy_d2h(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PHFEM_OK;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_ctx_profile(phfem_ctx* ctx, int enable) {
+  if (!ctx) return PHFEM_ERR_INVALID_ARGUMENT;
+  for (auto& r : ctx->recs) {
+    ctx->free_events.push_back(r.a);
+    ctx->free_events.push_back(r.b);
+  }
+  ctx->recs.clear();
+  ctx->prof = enable != 0;
+  return PHFEM_OK;
+}
+
+PHFEM_API int phfem_ctx_profile_read(phfem_ctx* ctx, int max_names, const char** names, double* ms,
+                                     int64_t* counts) {
+  if (!ctx) return -1;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  int n = 0;
+  for (auto& r : ctx->recs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    int i = 0;
+    while (i < n && strcmp(names[i], r.name) != 0) ++i;
+    if (i == n) {
+      if (n == max_names) continue;
+      names[n] = r.name;
+      ms[n] = 0.0;
+      counts[n] = 0;
+      ++n;
+    }
+    ms[i] += t;
+    counts[i] += 1;
+  }
+  return n;
+}

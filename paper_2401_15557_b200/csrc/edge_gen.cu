@@ -1,0 +1,433 @@
+// edge_gen.cu — build_topology on sm_100a.
+//
+// Reference: proj/src/edge_topology.cpp:52-143.  The reference emits 3 directed
+// occurrences per element (:61-68), sorts them stably by (max node, min node)
+// with two counting passes (:74-77) and walks the runs (:82-115): the first
+// occurrence of a run is t_plus, ids are handed out in canonical order.
+//
+// Device algorithm (2 global passes over the occurrences):
+//   A  k_eg_count    histogram of occurrences per bucket of 2^bs consecutive
+//                    max-node ids (warp-aggregated atomics)
+//   B  scan          bucket offsets
+//   C  k_eg_scatter  each occurrence packed into one 64-bit item
+//                      [max-node low bits | min node | occurrence index | dir]
+//                    and scattered into its bucket (warp-aggregated cursor)
+//   D  k_eg_bucket   one CTA per bucket: counting sort by max node in SMEM,
+//                    per-node insertion sort of the packed items (the packed
+//                    value orders by (max, min, occurrence) = the reference's
+//                    stable order), run detection with the reference's two
+//                    error checks, and a decoupled look-back over buckets that
+//                    carries (edges, boundary edges) so every CTA writes its
+//                    final edge ids, interior/boundary list slots, the
+//                    element->edge map and the max-node grouping table directly.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace phfem {
+
+struct EgParams {
+  int32_t nC, nE;
+  int lo_bits, occ_bits, total_bits, bs;
+  int nb;
+};
+
+static int bits_for(int64_t max_value) {  // bits to represent 0..max_value
+  int b = 1;
+  while (b < 63 && (int64_t(1) << b) <= max_value) ++b;
+  return b;
+}
+
+__device__ __forceinline__ uint64_t eg_pack(const EgParams& P, uint32_t hl, uint32_t lo,
+                                            uint32_t occ, uint32_t dir) {
+  return ((uint64_t)hl << P.total_bits) | ((uint64_t)lo << (P.occ_bits + 1)) |
+         ((uint64_t)occ << 1) | dir;
+}
+
+// A ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_eg_count(const int32_t* __restrict__ elements, EgParams P,
+                                                  int32_t* __restrict__ bcount,
+                                                  phfem_dev_errors* err) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m0 = (int64_t)blockIdx.x * blockDim.x; m0 < P.nE; m0 += stride) {
+    const int64_t m = m0 + threadIdx.x;
+    const bool valid = m < P.nE;
+    int t[3] = {0, 0, 0};
+    if (valid) {
+      t[0] = __ldg(elements + 3 * m);
+      t[1] = __ldg(elements + 3 * m + 1);
+      t[2] = __ldg(elements + 3 * m + 2);
+      if ((unsigned)t[0] >= (unsigned)P.nC || (unsigned)t[1] >= (unsigned)P.nC ||
+          (unsigned)t[2] >= (unsigned)P.nC)
+        atomicMin(&err->misc, (unsigned long long)m);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      const int hi = a > b ? a : b;
+      const bool ok = valid && (unsigned)hi < (unsigned)P.nC && a >= 0 && b >= 0;
+      const unsigned key = ok ? ((unsigned)hi >> P.bs) : 0xffffffffu;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (ok && lane_id() == (unsigned)(__ffs(grp) - 1)) atomicAdd(&bcount[key], __popc(grp));
+    }
+  }
+}
+
+__global__ void k_eg_max(const int32_t* __restrict__ bcount, int n, phfem_dev_errors* err) {
+  int mx = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    mx = max(mx, bcount[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane_id() == 0) atomicMax(&err->counters[3], (unsigned long long)mx);
+}
+
+// C ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ elements,
+                                                    EgParams P, int32_t* __restrict__ cursor,
+                                                    uint64_t* __restrict__ items) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t hl_mask = (1u << P.bs) - 1u;
+  for (int64_t m0 = (int64_t)blockIdx.x * blockDim.x; m0 < P.nE; m0 += stride) {
+    const int64_t m = m0 + threadIdx.x;
+    const bool valid = m < P.nE;
+    int t[3] = {0, 0, 0};
+    if (valid) {
+      t[0] = __ldg(elements + 3 * m);
+      t[1] = __ldg(elements + 3 * m + 1);
+      t[2] = __ldg(elements + 3 * m + 2);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      const int hi = a > b ? a : b;
+      const int lo = a > b ? b : a;
+      const unsigned key = valid ? ((unsigned)hi >> P.bs) : 0xffffffffu;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(grp) - 1;
+      int base = 0;
+      if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (valid) {
+        const int rank = __popc(grp & lanemask_lt());
+        const uint32_t occ = (uint32_t)(3 * m + s);
+        items[base + rank] = eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
+      }
+    }
+  }
+}
+
+// D ------------------------------------------------------------------------
+struct EgOut {
+  int32_t* edge_nodes;
+  int32_t* edge_elements;
+  int32_t* ltp;
+  int32_t* ltm;
+  int32_t* interior;
+  int32_t* boundary;
+  int32_t* elem_edge;
+  int32_t* node_edge_start;
+};
+
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kPay31 = (1ull << 31) - 1;
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, uint64_t v) {
+  *(volatile unsigned long long*)p = v;
+}
+
+// Decoupled look-back by warp 0 of the CTA owning bucket b.  Returns the
+// exclusive (edges << 32 | boundary) prefix.
+__device__ __forceinline__ uint64_t eg_lookback(unsigned long long* status, int b, uint32_t agg_e,
+                                                uint32_t agg_b) {
+  const unsigned lane = lane_id();
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], (b == 0 ? kFlagPre : kFlagAgg) | ((uint64_t)agg_e << 31) | agg_b);
+  }
+  if (b == 0) return 0;
+  uint64_t ex_e = 0, ex_b = 0;
+  int top = b - 1;
+  while (true) {
+    const int idx = top - (int)lane;
+    uint64_t w;
+    while (true) {
+      w = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPre;
+      if (!__any_sync(0xffffffffu, (w >> 62) == 0)) break;
+      __nanosleep(32);
+    }
+    const unsigned pmask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+    const bool take = (int)lane <= first_p;
+    const uint64_t ve = take ? ((w >> 31) & kPay31) : 0;
+    const uint64_t vb = take ? (w & kPay31) : 0;
+    ex_e += warp_reduce_sum(ve);
+    ex_b += warp_reduce_sum(vb);
+    if (pmask) break;
+    top -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], kFlagPre | ((ex_e + agg_e) << 31) | (ex_b + agg_b));
+  }
+  return (ex_e << 32) | ex_b;
+}
+
+__global__ void k_eg_bucket(const uint64_t* __restrict__ items, const int32_t* __restrict__ boff,
+                            EgParams P, int cap, uint64_t* __restrict__ overflow,
+                            unsigned long long* status, int32_t* ticket, EgOut out,
+                            phfem_dev_errors* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int NB = 1 << P.bs;
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smraw);
+  int32_t* cur = reinterpret_cast<int32_t*>(buf + cap);
+  __shared__ unsigned long long scan_sm[33];
+  __shared__ int s_b;
+  __shared__ unsigned long long s_prefix;
+
+  const int tid = threadIdx.x;
+  const int T = blockDim.x;
+  if (tid == 0) s_b = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int b = s_b;
+  const int64_t s = boff[b];
+  const int n = boff[b + 1] - (int)s;
+  uint64_t* sorted = (n <= cap) ? buf : overflow + s;
+  const int shift = P.total_bits;
+
+  for (int i = tid; i < NB; i += T) cur[i] = 0;
+  __syncthreads();
+  for (int p = tid; p < n; p += T) atomicAdd(&cur[(int)(__ldg(items + s + p) >> shift)], 1);
+  __syncthreads();
+  const int c = tid < NB ? cur[tid] : 0;
+  unsigned long long tot;
+  const int st = (int)block_exclusive_scan((unsigned long long)c, scan_sm, &tot);
+  if (tid < NB) cur[tid] = st;
+  __syncthreads();
+  for (int p = tid; p < n; p += T) {
+    const uint64_t it = __ldg(items + s + p);
+    const int pos = atomicAdd(&cur[(int)(it >> shift)], 1);
+    sorted[pos] = it;
+  }
+  __syncthreads();
+
+  // --- per max-node segment: sort, runs, checks --------------------------
+  const int64_t v = (int64_t)b * NB + tid;
+  const int lo_shift = P.occ_bits + 1;
+  const uint64_t lo_mask = (1ull << P.lo_bits) - 1ull;
+  uint32_t ne_i = 0, nb_i = 0;
+  if (tid < NB && c > 0) {
+    uint64_t* seg = sorted + st;
+    for (int i = 1; i < c; ++i) {  // insertion sort by packed value
+      const uint64_t x = seg[i];
+      int j = i - 1;
+      while (j >= 0 && seg[j] > x) {
+        seg[j + 1] = seg[j];
+        --j;
+      }
+      seg[j + 1] = x;
+    }
+    for (int q = 0; q < c;) {
+      const uint64_t lo = (seg[q] >> lo_shift) & lo_mask;
+      int r = q + 1;
+      while (r < c && ((seg[r] >> lo_shift) & lo_mask) == lo) ++r;
+      const int len = r - q;
+      if (len > 2) {
+        atomicMin(&err->topo, ((uint64_t)v << 33) | (lo << 2) | 0ull);
+      } else if (len == 2 && ((seg[q] ^ seg[q + 1]) & 1ull) == 0) {
+        atomicMin(&err->topo, ((uint64_t)v << 33) | (lo << 2) | 2ull | (seg[q] & 1ull));
+      }
+      ++ne_i;
+      if (len == 1) ++nb_i;
+      q = r;
+    }
+  }
+  unsigned long long agg;
+  const unsigned long long ex =
+      block_exclusive_scan(((unsigned long long)ne_i << 32) | nb_i, scan_sm, &agg);
+  if (tid < 32) {
+    const uint64_t pre = eg_lookback(status, b, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
+    if (tid == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  const uint64_t pre = s_prefix;
+  int32_t e = (int32_t)((pre >> 32) + (ex >> 32));
+  int32_t bpos = (int32_t)((pre & 0xffffffffu) + (ex & 0xffffffffu));
+  int32_t ipos = e - bpos;
+  if (tid < NB && v < P.nC) out.node_edge_start[v] = e;
+  if (tid < NB && c > 0) {
+    const uint64_t* seg = sorted + st;
+    const uint32_t occ_mask = (uint32_t)((1ull << P.occ_bits) - 1ull);
+    for (int q = 0; q < c;) {
+      const uint64_t f = seg[q];
+      const uint64_t lo = (f >> lo_shift) & lo_mask;
+      int r = q + 1;
+      while (r < c && ((seg[r] >> lo_shift) & lo_mask) == lo) ++r;
+      const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
+      const int m_f = (int)(occ_f / 3u);
+      const int l_f = (int)((occ_f % 3u + 2u) % 3u);
+      const bool dir = f & 1ull;
+      out.edge_nodes[2 * (int64_t)e] = dir ? (int32_t)v : (int32_t)lo;
+      out.edge_nodes[2 * (int64_t)e + 1] = dir ? (int32_t)lo : (int32_t)v;
+      out.ltp[e] = l_f;
+      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
+      if (r - q >= 2) {
+        const uint64_t g = seg[q + 1];
+        const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
+        const int m_g = (int)(occ_g / 3u);
+        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
+        out.edge_elements[2 * (int64_t)e] = m_f;
+        out.edge_elements[2 * (int64_t)e + 1] = m_g;
+        out.ltm[e] = l_g;
+        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+        out.interior[ipos++] = e;
+      } else {
+        out.edge_elements[2 * (int64_t)e] = m_f;
+        out.edge_elements[2 * (int64_t)e + 1] = -1;
+        out.ltm[e] = -1;
+        out.boundary[bpos++] = e;
+      }
+      ++e;
+      q = r;
+    }
+  }
+  if (b == P.nb - 1 && tid == 0) {
+    const uint64_t E = (pre >> 32) + (agg >> 32);
+    const uint64_t NBd = (pre & 0xffffffffu) + (agg & 0xffffffffu);
+    err->counters[0] = E;
+    err->counters[1] = E - NBd;
+    err->counters[2] = NBd;
+    out.node_edge_start[P.nC] = (int32_t)E;
+  }
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API void phfem_topology_release(phfem_ctx* ctx, phfem_topology* t) {
+  if (!t) return;
+  dfree(ctx, t->edge_nodes);
+  dfree(ctx, t->edge_elements);
+  dfree(ctx, t->local_in_tplus);
+  dfree(ctx, t->local_in_tminus);
+  dfree(ctx, t->interior_edges);
+  dfree(ctx, t->boundary_edges);
+  dfree(ctx, t->elem_edge);
+  dfree(ctx, t->node_edge_start);
+  t->E = t->n_interior = t->n_boundary = 0;
+}
+
+PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                            phfem_topology* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "set device");
+  const int64_t nE = mesh->nE, nC = mesh->nC;
+  if (nE < 0 || nC < 0 || 3 * nE >= (int64_t(1) << 31))
+    return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: mesh too large for int ids");
+  out->nC = (int32_t)nC;
+  out->nE = (int32_t)nE;
+
+  EgParams P;
+  P.nC = (int32_t)nC;
+  P.nE = (int32_t)nE;
+  P.lo_bits = bits_for(std::max<int64_t>(nC - 1, 1));
+  P.occ_bits = bits_for(std::max<int64_t>(3 * nE - 1, 1));
+  P.total_bits = P.lo_bits + P.occ_bits + 1;
+  P.bs = std::min(8, 64 - P.total_bits);
+  if (P.bs < 1) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: ids too wide");
+  const int NB = 1 << P.bs;
+  P.nb = (int)((nC + NB - 1) / NB);
+  if (P.nb < 1) P.nb = 1;
+  const int64_t nd = 3 * nE;
+  const int64_t cap_e = std::max<int64_t>(nd, 1);
+
+  PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
+  PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * cap_e));
+  PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * cap_e));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tplus, cap_e));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tminus, cap_e));
+  PHFEM_TRY(dalloc(ctx, &out->interior_edges, cap_e / 2 + 1));
+  PHFEM_TRY(dalloc(ctx, &out->boundary_edges, cap_e));
+  PHFEM_TRY(dalloc(ctx, &out->elem_edge, cap_e));
+  if (nE == 0) {
+    PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * (nC + 1), ctx->stream));
+    return PHFEM_OK;
+  }
+
+  PHFEM_TRY(errors_reset(ctx));
+  int32_t *bcount = nullptr, *boff = nullptr, *ticket = nullptr;
+  unsigned long long* status = nullptr;
+  PHFEM_TRY(dalloc(ctx, &bcount, (int64_t)P.nb + 1));
+  PHFEM_TRY(dalloc(ctx, &boff, (int64_t)P.nb + 1));
+  PHFEM_TRY(dalloc(ctx, &status, P.nb));
+  PHFEM_TRY(dalloc(ctx, &ticket, 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (P.nb + 1), ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * P.nb, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(int32_t), ctx->stream));
+
+  const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
+  PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, bcount, ctx->derr));
+  PHFEM_LAUNCH(ctx, "k_eg_max", k_eg_max<<<grid_for(P.nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(bcount, P.nb, ctx->derr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
+  int32_t* cursor = bcount;  // reuse as scatter cursor
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, boff, sizeof(int32_t) * P.nb, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+  PHFEM_TRY(errors_fetch(ctx));
+  if (ctx->herr->misc != ~0ull) {
+    const long long m = (long long)ctx->herr->misc;
+    dfree(ctx, bcount); dfree(ctx, boff); dfree(ctx, status); dfree(ctx, ticket);
+    return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE,
+                     "build_topology: element %lld has a node index outside 1..%lld", m + 1,
+                     (long long)nC);
+  }
+  const int64_t max_bucket = (int64_t)ctx->herr->counters[3];
+
+  uint64_t* items = nullptr;
+  uint64_t* overflow = nullptr;
+  PHFEM_TRY(dalloc(ctx, &items, nd));
+  const int cap = 16 * NB;  // SMEM capacity per bucket (16 occurrences per node)
+  if (max_bucket > cap) PHFEM_TRY(dalloc(ctx, &overflow, nd));
+  PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, cursor, items));
+
+  EgOut o{out->edge_nodes, out->edge_elements, out->local_in_tplus, out->local_in_tminus,
+          out->interior_edges, out->boundary_edges, out->elem_edge, out->node_edge_start};
+  const int threads = std::max(32, NB);
+  const size_t smem = (size_t)cap * sizeof(uint64_t) + (size_t)(NB + 1) * sizeof(int32_t);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_eg_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PHFEM_LAUNCH(ctx, "k_eg_bucket", k_eg_bucket<<<P.nb, threads, smem, ctx->stream>>>(items, boff, P, cap, overflow, status, ticket,
+                                                    o, ctx->derr));
+  dfree(ctx, items);
+  dfree(ctx, overflow);
+  dfree(ctx, bcount);
+  dfree(ctx, boff);
+  dfree(ctx, status);
+  dfree(ctx, ticket);
+  PHFEM_TRY(errors_fetch(ctx));
+  const uint64_t te = ctx->herr->topo;
+  if (te != ~0ull) {
+    const long long hi = (long long)(te >> 33);
+    const long long lo = (long long)((te >> 2) & ((1ull << 31) - 1));
+    const bool dup = (te >> 1) & 1ull;
+    const bool dir = te & 1ull;
+    phfem_topology_release(ctx, out);
+    if (dup) {
+      const long long from = dir ? hi : lo, to = dir ? lo : hi;
+      return set_error(ctx, PHFEM_ERR_DUP_DIRECTED, "build_topology: duplicate directed edge %lld->%lld",
+                       from + 1, to + 1);
+    }
+    return set_error(ctx, PHFEM_ERR_NONMANIFOLD,
+                     "build_topology: non-manifold edge (%lld,%lld) shared by more than two elements",
+                     lo + 1, hi + 1);
+  }
+  out->E = (int32_t)ctx->herr->counters[0];
+  out->n_interior = (int32_t)ctx->herr->counters[1];
+  out->n_boundary = (int32_t)ctx->herr->counters[2];
+  return PHFEM_OK;
+}

@@ -1,0 +1,83 @@
+// kernels.cuh — internal interfaces shared by the assembly, CN-RHS and
+// pipeline translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace phfem {
+
+struct VolArgs {
+  const double2* coords;
+  const int32_t* elements;
+  int nE;
+  int vec;  // outputs 16-byte aligned -> vector stores
+  phfem_coeffs coeffs;
+  phfem_field f;
+  double t;
+  double* B;
+  double* D;
+  double* M;
+  double* M0;
+  double* load;
+};
+
+VolArgs make_vol_args(const phfem_mesh* mesh);
+phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool load);
+phfem_status volume_errors(phfem_ctx* ctx, bool blocks, bool load);
+
+// assemble_load's per-element rule (assembly.cpp:185-201): f at the three edge
+// midpoints, b_i = 0.0 + (|T|/3 * 0.5) * (f_{i+1} + f_{i+2}) (the 0.0 + is
+// scatter_add's zero-initialised accumulation, sparse.cpp:112-118).
+__device__ __forceinline__ void element_load(double2 v0, double2 v1, double2 v2,
+                                             const phfem_field* f, double t, double bl[3],
+                                             bool valid, int64_t m, phfem_dev_errors* err) {
+  const double mx[3] = {0.5 * (v1.x + v2.x), 0.5 * (v2.x + v0.x), 0.5 * (v0.x + v1.x)};
+  const double my[3] = {0.5 * (v1.y + v2.y), 0.5 * (v2.y + v0.y), 0.5 * (v0.y + v1.y)};
+  const double area = 0.5 * ((v1.x - v0.x) * (v2.y - v0.y) - (v1.y - v0.y) * (v2.x - v0.x));
+  double fm[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    fm[i] = phfem_field_eval(f, mx[i], my[i], t);
+    if (valid && !isfinite(fm[i])) atomicMin(&err->load_nan, (unsigned long long)m);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) bl[i] = 0.0 + area / 3.0 * 0.5 * (fm[(i + 1) % 3] + fm[(i + 2) % 3]);
+}
+
+struct NeuArgs {
+  const double2* coords;
+  const int32_t* edge_nodes;
+  const int32_t* ltp;
+  const int32_t* neu_ids;
+  const int32_t* slot_of;
+  int nN;
+  phfem_field g;
+  double* vals;
+};
+
+struct NeuTable {
+  int nN = 0, cap = 0, seq = 0;
+  int32_t* keys = nullptr;     // element id per slot, -1 empty
+  int32_t* slot_of = nullptr;  // slot of each Neumann list entry
+  double* vals = nullptr;      // [cap][3] LN values of the slot's element
+};
+
+phfem_status neu_table_build(phfem_ctx* ctx, const phfem_topology* topo,
+                             const phfem_classification* cls, NeuTable* tab);
+void neu_table_free(phfem_ctx* ctx, NeuTable* tab);
+phfem_status neu_table_eval(phfem_ctx* ctx, const NeuTable* tab, const phfem_mesh* mesh,
+                            const phfem_topology* topo, const phfem_classification* cls,
+                            const phfem_field* g, double t, double* vals);
+phfem_status neu_flux_error(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                            const phfem_classification* cls);
+phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                          const phfem_classification* cls, const phfem_field* g, double t,
+                          double* out, int accumulate, bool check);
+phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                            const phfem_classification* cls, const phfem_field* uD, double t,
+                            double* out);
+phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                 const phfem_topology* topo, const phfem_classification* cls,
+                                 phfem_csr* out);
+
+}  // namespace phfem

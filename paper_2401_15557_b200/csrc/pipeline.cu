@@ -1,0 +1,193 @@
+// pipeline.cu — the fused edge-generation -> red-refinement -> assembly step
+// (the bench workload) and its host-buffer (drop-in, e2e) variant.
+//
+// Reference composition: the refinement chain mesh = red_refine(mesh,
+// build_topology(mesh)) (tools/main.cpp:159,394; acceptance.cpp:70), then
+// build_topology + classify_edges + assemble_operators + the elliptic load
+// b + LN (elliptic.cpp:53-56) and the Dirichlet vector.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace phfem {
+
+static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
+                                  const phfem_coeffs* c, const phfem_field* f,
+                                  const phfem_field* g, const phfem_field* uD, double t,
+                                  phfem_pipeline_out* out) {
+  for (int l = 0; l < levels; ++l) {
+    phfem_topology topo;
+    phfem_status st = phfem_build_topology(ctx, &cur, &topo);
+    if (st != PHFEM_OK) {
+      phfem_mesh_release(ctx, &cur);
+      return st;
+    }
+    phfem_mesh next;
+    st = phfem_red_refine(ctx, &cur, &topo, &next);
+    phfem_topology_release(ctx, &topo);
+    phfem_mesh_release(ctx, &cur);
+    if (st != PHFEM_OK) return st;
+    cur = next;
+  }
+  out->mesh = cur;
+  PHFEM_TRY(phfem_build_topology(ctx, &out->mesh, &out->topo));
+  PHFEM_TRY(phfem_classify_edges(ctx, &out->topo, &out->mesh, &out->cls));
+  const int64_t nE = out->mesh.nE;
+  PHFEM_TRY(dalloc(ctx, &out->B, 9 * nE));
+  PHFEM_TRY(dalloc(ctx, &out->D, 9 * nE));
+  PHFEM_TRY(dalloc(ctx, &out->M, 9 * nE));
+  PHFEM_TRY(dalloc(ctx, &out->M0, 9 * nE));
+  PHFEM_TRY(dalloc(ctx, &out->load, 3 * nE));
+  PHFEM_TRY(dalloc(ctx, &out->bd, std::max(out->cls.L, 1)));
+  PHFEM_TRY(errors_reset(ctx));
+  VolArgs a = make_vol_args(&out->mesh);
+  a.coeffs = *c;
+  a.f = *f;
+  a.t = t;
+  a.B = out->B;
+  a.D = out->D;
+  a.M = out->M;
+  a.M0 = out->M0;
+  a.load = out->load;
+  a.vec = 1;  // pool allocations are 256-byte aligned
+  PHFEM_TRY(launch_volume(ctx, a, true, true));
+  PHFEM_TRY(neumann_into(ctx, &out->mesh, &out->topo, &out->cls, g, t, out->load, 1, false));
+  PHFEM_TRY(constraint_csr_into(ctx, &out->mesh, &out->topo, &out->cls, &out->C));
+  PHFEM_TRY(dirichlet_into(ctx, &out->mesh, &out->topo, &out->cls, uD, t, out->bd));
+  PHFEM_TRY(errors_fetch(ctx));
+  PHFEM_TRY(volume_errors(ctx, true, true));
+  PHFEM_TRY(neu_flux_error(ctx, &out->mesh, &out->topo, &out->cls));
+  return PHFEM_OK;
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API void phfem_pipeline_release(phfem_ctx* ctx, phfem_pipeline_out* out) {
+  if (!out) return;
+  phfem_csr_release(ctx, &out->C);
+  phfem_classification_release(ctx, &out->cls);
+  phfem_topology_release(ctx, &out->topo);
+  phfem_mesh_release(ctx, &out->mesh);
+  dfree(ctx, out->B);
+  dfree(ctx, out->D);
+  dfree(ctx, out->M);
+  dfree(ctx, out->M0);
+  dfree(ctx, out->load);
+  dfree(ctx, out->bd);
+}
+
+PHFEM_API phfem_status phfem_pipeline(phfem_ctx* ctx, const phfem_mesh* mesh_in, int levels,
+                                      const phfem_coeffs* c, const phfem_field* f,
+                                      const phfem_field* g, const phfem_field* uD, double t,
+                                      phfem_pipeline_out* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !mesh_in || !c || !f || !g || !uD || levels < 0) return PHFEM_ERR_INVALID_ARGUMENT;
+  phfem_mesh cur = *mesh_in;
+  cur.owned = 0;  // the caller's mesh is never freed here
+  phfem_status st = pipeline_impl(ctx, cur, levels, c, f, g, uD, t, out);
+  if (st != PHFEM_OK) {
+    const std::string msg = ctx->message;
+    phfem_pipeline_release(ctx, out);
+    ctx->message = msg;
+  }
+  return st;
+}
+
+PHFEM_API phfem_status phfem_pipeline_from_host(phfem_ctx* ctx, const double* coords,
+                                                const int32_t* elements, const int32_t* dirichlet,
+                                                const int32_t* neumann, int32_t nC, int32_t nE,
+                                                int32_t nD, int32_t nN, int levels,
+                                                const phfem_coeffs* c, const phfem_field* f,
+                                                const phfem_field* g, const phfem_field* uD,
+                                                double t, phfem_pipeline_out* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !c || !f || !g || !uD || levels < 0 || nC < 0 || nE < 0 || nD < 0 || nN < 0)
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  phfem_mesh m;
+  memset(&m, 0, sizeof m);
+  m.nC = nC;
+  m.nE = nE;
+  m.nD = nD;
+  m.nN = nN;
+  m.owned = 1;
+  PHFEM_TRY(dalloc(ctx, &m.coords, 2 * (int64_t)nC));
+  PHFEM_TRY(dalloc(ctx, &m.elements, 3 * (int64_t)nE));
+  PHFEM_TRY(dalloc(ctx, &m.dirichlet, 2 * (int64_t)nD));
+  PHFEM_TRY(dalloc(ctx, &m.neumann, 2 * (int64_t)nN));
+  if (nC) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.coords, coords, 16 * (size_t)nC, cudaMemcpyHostToDevice, ctx->stream));
+  if (nE) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.elements, elements, 12 * (size_t)nE, cudaMemcpyHostToDevice, ctx->stream));
+  if (nD) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.dirichlet, dirichlet, 8 * (size_t)nD, cudaMemcpyHostToDevice, ctx->stream));
+  if (nN) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.neumann, neumann, 8 * (size_t)nN, cudaMemcpyHostToDevice, ctx->stream));
+  phfem_status st = pipeline_impl(ctx, m, levels, c, f, g, uD, t, out);
+  if (st != PHFEM_OK) {
+    const std::string msg = ctx->message;
+    phfem_pipeline_release(ctx, out);
+    ctx->message = msg;
+  }
+  return st;
+}
+
+namespace {
+struct Piece {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+}  // namespace
+
+static int collect_pieces(const phfem_pipeline_out* o, const phfem_pipeline_host* d, Piece* p) {
+  int n = 0;
+  auto add = [&](void* dst, const void* src, size_t bytes) {
+    if (dst && bytes) p[n++] = Piece{dst, src, bytes};
+  };
+  const size_t nC = o->mesh.nC, nE = o->mesh.nE, E = o->topo.E, L = o->cls.L;
+  add(d->coords, o->mesh.coords, 16 * nC);
+  add(d->elements, o->mesh.elements, 12 * nE);
+  add(d->dirichlet, o->mesh.dirichlet, 8 * (size_t)o->mesh.nD);
+  add(d->neumann, o->mesh.neumann, 8 * (size_t)o->mesh.nN);
+  add(d->edge_nodes, o->topo.edge_nodes, 8 * E);
+  add(d->edge_elements, o->topo.edge_elements, 8 * E);
+  add(d->local_in_tplus, o->topo.local_in_tplus, 4 * E);
+  add(d->local_in_tminus, o->topo.local_in_tminus, 4 * E);
+  add(d->interior_edges, o->topo.interior_edges, 4 * (size_t)o->topo.n_interior);
+  add(d->boundary_edges, o->topo.boundary_edges, 4 * (size_t)o->topo.n_boundary);
+  add(d->elem_edge, o->topo.elem_edge, 12 * nE);
+  add(d->dirichlet_edge_ids, o->cls.dirichlet_edge_ids, 4 * (size_t)o->cls.nD);
+  add(d->neumann_edge_ids, o->cls.neumann_edge_ids, 4 * (size_t)o->cls.nN);
+  add(d->retained_edges, o->cls.retained_edges, 4 * L);
+  add(d->retained_pos, o->cls.retained_pos, 4 * E);
+  add(d->C_row_ptr, o->C.row_ptr, 4 * (L + 1));
+  add(d->C_col_idx, o->C.col_idx, 4 * (size_t)o->C.nnz);
+  add(d->C_values, o->C.values, 8 * (size_t)o->C.nnz);
+  add(d->B, o->B, 72 * nE);
+  add(d->D, o->D, 72 * nE);
+  add(d->M, o->M, 72 * nE);
+  add(d->M0, o->M0, 72 * nE);
+  add(d->load, o->load, 24 * nE);
+  add(d->bd, o->bd, 8 * L);
+  return n;
+}
+
+PHFEM_API int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* out,
+                                                const phfem_pipeline_host* dst) {
+  Piece p[32];
+  const int n = collect_pieces(out, dst, p);
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) total += (int64_t)p[i].bytes;
+  return total;
+}
+
+PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipeline_out* out,
+                                               const phfem_pipeline_host* dst) {
+  if (!ctx || !out || !dst) return PHFEM_ERR_INVALID_ARGUMENT;
+  Piece p[32];
+  const int n = collect_pieces(out, dst, p);
+  for (int i = 0; i < n; ++i)
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(p[i].dst, p[i].src, p[i].bytes, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
