@@ -137,53 +137,82 @@ PHFEM_HD phfem_coeff_values phfem_coeffs_eval(const phfem_coeffs* c, double x0, 
 /*
  * Local element matrices in the reference's exact operation order
  * (proj/src/assembly.cpp:17-27 element_geometry, :53-78 local_element_matrices,
- * :134-140 unit mass).  Output blocks are column-major 3x3 (out[3*j+i] = X(i,j)),
+ * :134-140 unit mass).  Blocks are column-major 3x3 (out[3*j+i] = X(i,j)),
  * i.e. exactly the 9 values assemble_block_diagonal writes per element
- * (assembly.cpp:106-114).  Returns twice the signed area; the caller treats
- * !(t2 > 0) as the reference's "degenerate or non-CCW triangle" error.
+ * (assembly.cpp:106-114).  The pieces are separate so a kernel can emit one
+ * block at a time; phfem_local_blocks composes them.
  */
-PHFEM_HD double phfem_local_blocks(double x0, double y0, double x1, double y1, double x2,
-                                   double y2, const phfem_coeff_values* c, double* Bk,
-                                   double* Dk, double* Mk, double* M0k) {
+typedef struct phfem_geom {
+  double t2, area;
+  double gx[3], gy[3]; /* grad lambda_i */
+} phfem_geom;
+
+PHFEM_HD phfem_geom phfem_geometry(double x0, double y0, double x1, double y1, double x2,
+                                   double y2) {
+  phfem_geom g;
   /* mesh.cpp:104-106 signed_area2 */
-  const double t2 = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
-  const double area = 0.5 * t2;
+  g.t2 = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
+  g.area = 0.5 * g.t2;
   /* assembly.cpp:23-25: Vec2(...) / twice_area (component-wise division) */
-  double gx[3], gy[3];
-  gx[0] = (y1 - y2) / t2;
-  gy[0] = (x2 - x1) / t2;
-  gx[1] = (y2 - y0) / t2;
-  gy[1] = (x0 - x2) / t2;
-  gx[2] = (y0 - y1) / t2;
-  gy[2] = (x1 - x0) / t2;
-  /* :59-64 stiffness from the upper triangle: area * (A g_i) . g_j */
+  g.gx[0] = (y1 - y2) / g.t2;
+  g.gy[0] = (x2 - x1) / g.t2;
+  g.gx[1] = (y2 - y0) / g.t2;
+  g.gy[1] = (x0 - x2) / g.t2;
+  g.gx[2] = (y0 - y1) / g.t2;
+  g.gy[2] = (x1 - x0) / g.t2;
+  return g;
+}
+
+/* :59-64 stiffness from the upper triangle: area * (A g_i) . g_j */
+PHFEM_HD void phfem_stiffness(const phfem_geom* g, const phfem_coeff_values* c, double* Bk) {
   for (int i = 0; i < 3; ++i) {
-    const double rx = c->a00 * gx[i] + c->a01 * gy[i];
-    const double ry = c->a10 * gx[i] + c->a11 * gy[i];
+    const double rx = c->a00 * g->gx[i] + c->a01 * g->gy[i];
+    const double ry = c->a10 * g->gx[i] + c->a11 * g->gy[i];
     for (int j = i; j < 3; ++j) {
-      const double v = area * (rx * gx[j] + ry * gy[j]);
+      const double v = g->area * (rx * g->gx[j] + ry * g->gy[j]);
       Bk[3 * j + i] = v;
       Bk[3 * i + j] = v;
     }
   }
-  /* :68-71 convection: column-constant area/3 * p . g_j */
+}
+
+/* :68-71 convection: column-constant area/3 * p . g_j */
+PHFEM_HD void phfem_convection(const phfem_geom* g, const phfem_coeff_values* c, double* Dk) {
   for (int j = 0; j < 3; ++j) {
-    const double dj = area / 3.0 * (c->px * gx[j] + c->py * gy[j]);
+    const double dj = g->area / 3.0 * (c->px * g->gx[j] + c->py * g->gy[j]);
     Dk[3 * j + 0] = dj;
     Dk[3 * j + 1] = dj;
     Dk[3 * j + 2] = dj;
   }
-  /* :73-75 mass (delta-scaled) and :134-140 unit mass */
-  const double md = c->delta * area * (1.0 / 6.0);
-  const double mo = c->delta * area * (1.0 / 12.0);
-  const double ud = area * (1.0 / 6.0);
-  const double uo = area * (1.0 / 12.0);
+}
+
+/* :73-75 mass, delta-scaled: delta * area * {1/6, 1/12} */
+PHFEM_HD void phfem_mass(const phfem_geom* g, double delta, double* Mk) {
+  const double md = delta * g->area * (1.0 / 6.0);
+  const double mo = delta * g->area * (1.0 / 12.0);
   for (int j = 0; j < 3; ++j)
-    for (int i = 0; i < 3; ++i) {
-      Mk[3 * j + i] = (i == j) ? md : mo;
-      M0k[3 * j + i] = (i == j) ? ud : uo;
-    }
-  return t2;
+    for (int i = 0; i < 3; ++i) Mk[3 * j + i] = (i == j) ? md : mo;
+}
+
+/* :134-140 unit mass: area * {1/6, 1/12} */
+PHFEM_HD void phfem_unit_mass(const phfem_geom* g, double* M0k) {
+  const double ud = g->area * (1.0 / 6.0);
+  const double uo = g->area * (1.0 / 12.0);
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) M0k[3 * j + i] = (i == j) ? ud : uo;
+}
+
+/* All four blocks; returns twice the signed area (!(t2 > 0) is the
+ * reference's "degenerate or non-CCW triangle" error, assembly.cpp:19-20). */
+PHFEM_HD double phfem_local_blocks(double x0, double y0, double x1, double y1, double x2,
+                                   double y2, const phfem_coeff_values* c, double* Bk,
+                                   double* Dk, double* Mk, double* M0k) {
+  const phfem_geom g = phfem_geometry(x0, y0, x1, y1, x2, y2);
+  phfem_stiffness(&g, c, Bk);
+  phfem_convection(&g, c, Dk);
+  phfem_mass(&g, c->delta, Mk);
+  phfem_unit_mass(&g, M0k);
+  return g.t2;
 }
 
 #ifdef __cplusplus

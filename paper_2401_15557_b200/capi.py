@@ -286,7 +286,7 @@ class Context:
         return int(p.value)
 
     def free(self, ptr: int):
-        if ptr:
+        if ptr and self.ptr:
             self.lib.phfem_free(self.ptr, C.c_void_p(ptr))
 
     def to_device(self, arr: np.ndarray) -> int:
@@ -351,7 +351,7 @@ class DeviceMesh:
                         c.to_host(m.neumann, (m.nN, 2), np.int32))
 
     def release(self):
-        if self.m.owned:
+        if self.m.owned and self.ctx.ptr:
             self.ctx.lib.phfem_mesh_release(self.ctx.ptr, C.byref(self.m))
 
     def __del__(self):
@@ -383,7 +383,7 @@ class Topology:
         }
 
     def release(self):
-        if self.owner:
+        if self.owner and self.ctx.ptr:
             self.ctx.lib.phfem_topology_release(self.ctx.ptr, C.byref(self.t))
             self.owner = False
 
@@ -412,7 +412,7 @@ class Classification:
         }
 
     def release(self):
-        if self.owner:
+        if self.owner and self.ctx.ptr:
             self.ctx.lib.phfem_classification_release(self.ctx.ptr, C.byref(self.c))
             self.owner = False
 
@@ -541,7 +541,7 @@ class CNPlan:
             self.ctx.free(r)
 
     def close(self):
-        if self.ptr:
+        if self.ptr and self.ctx.ptr:
             self.ctx.lib.phfem_cn_plan_destroy(self.ctx.ptr, self.ptr)
             self.ptr = C.c_void_p()
 
@@ -589,7 +589,7 @@ class PipelineResult:
         return Classification(self.ctx, self.out.cls, owner=False)
 
     def release(self):
-        if self.ctx is not None:
+        if self.ctx is not None and self.ctx.ptr:
             self.ctx.lib.phfem_pipeline_release(self.ctx.ptr, C.byref(self.out))
             self.ctx = None
 

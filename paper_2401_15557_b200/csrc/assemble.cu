@@ -14,38 +14,47 @@
 namespace phfem {
 
 // ---------------------------------------------------------------------------
-// Element pass.  One thread per element, 128 elements per tile; every output
-// block goes through a shared-memory tile so the global stores are fully
-// coalesced 16-byte vectors (the per-thread 72-byte blocks would otherwise
-// scatter each store instruction over 32 sectors).
+// Element pass.  One thread per element; each warp owns 32 consecutive
+// elements, so a 3x3 block of the warp is 32 x 72 = 2304 contiguous bytes.
+// A block is computed, staged in the warp's SMEM slice (stride 9 doubles:
+// conflict-free) and written back with 16-byte coalesced stores, one block at
+// a time (low register pressure, no block-wide barrier: warps stream
+// independently, so stores of one warp overlap the fp64 work of others).
 constexpr int kVolThreads = 128;
+constexpr int kVolWarps = kVolThreads / 32;
 
-__device__ __forceinline__ void tile_store(double* __restrict__ g, int64_t base, int n_valid,
-                                           int per, const double* vals, double* tile, bool vec) {
-  __syncthreads();
-  for (int k = 0; k < per; ++k) tile[threadIdx.x * per + k] = vals[k];
-  __syncthreads();
+__device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base, int n_valid,
+                                           int per, const double* vals, double* buf, bool vec) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 9; ++k)
+    if (k < per) buf[lane * per + k] = vals[k];
+  __syncwarp();
   const int count = n_valid * per;
   double* dst = g + base * per;
   if (vec) {
-    const double2* src2 = reinterpret_cast<const double2*>(tile);
+    const double2* src2 = reinterpret_cast<const double2*>(buf);
     double2* dst2 = reinterpret_cast<double2*>(dst);
-    for (int i = threadIdx.x; i < count / 2; i += blockDim.x) dst2[i] = src2[i];
-    if ((count & 1) && threadIdx.x == 0) dst[count - 1] = tile[count - 1];
+    for (int i = lane; i < count / 2; i += 32) __stcs(dst2 + i, src2[i]);
+    if ((count & 1) && lane == 0) dst[count - 1] = buf[count - 1];
   } else {
-    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = tile[i];
+    for (int i = lane; i < count; i += 32) dst[i] = buf[i];
   }
 }
 
 template <bool kBlocks, bool kLoad>
-__global__ void __launch_bounds__(kVolThreads) k_volume(VolArgs a, phfem_dev_errors* err) {
-  __shared__ __align__(16) double tile[kVolThreads * 9];
-  const int64_t ntiles = ((int64_t)a.nE + kVolThreads - 1) / kVolThreads;
-  for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
-    const int64_t base = tb * kVolThreads;
-    const int n_valid = (int)((int64_t)a.nE - base < kVolThreads ? (int64_t)a.nE - base : kVolThreads);
-    const int64_t m = base + threadIdx.x;
-    const bool valid = threadIdx.x < n_valid;
+__global__ void __launch_bounds__(kVolThreads, 8) k_volume(VolArgs a, phfem_dev_errors* err) {
+  __shared__ __align__(16) double wbuf[kVolWarps][32 * 9];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* buf = wbuf[warp];
+  const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
+  for (int64_t ch = (int64_t)blockIdx.x * kVolWarps + warp; ch < nchunks;
+       ch += (int64_t)gridDim.x * kVolWarps) {
+    const int64_t base = ch * 32;
+    const int n_valid = (int)((int64_t)a.nE - base < 32 ? (int64_t)a.nE - base : 32);
+    const int64_t m = base + lane;
+    const bool valid = lane < n_valid;
     double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(1.0, 0.0), v2 = make_double2(0.0, 1.0);
     if (valid) {
       const int i0 = __ldg(a.elements + 3 * m), i1 = __ldg(a.elements + 3 * m + 1),
@@ -54,28 +63,42 @@ __global__ void __launch_bounds__(kVolThreads) k_volume(VolArgs a, phfem_dev_err
       v1 = __ldg(a.coords + i1);
       v2 = __ldg(a.coords + i2);
     }
-    if (kBlocks) {
-      const phfem_coeff_values cv = phfem_coeffs_eval(&a.coeffs, v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
-      double b[9], d[9], mm[9], m0[9];
-      const double t2 = phfem_local_blocks(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, &cv, b, d, mm, m0);
-      if (valid && !(t2 > 0.0)) atomicMin(&err->degenerate, (unsigned long long)m);
-      if (a.B) tile_store(a.B, base, n_valid, 9, b, tile, a.vec);
-      if (a.D) tile_store(a.D, base, n_valid, 9, d, tile, a.vec);
-      if (a.M) tile_store(a.M, base, n_valid, 9, mm, tile, a.vec);
-      if (a.M0) tile_store(a.M0, base, n_valid, 9, m0, tile, a.vec);
-    }
     if (kLoad) {
       double bl[3];
       element_load(v0, v1, v2, &a.f, a.t, bl, valid, m, err);
-      tile_store(a.load, base, n_valid, 3, bl, tile, a.vec);
+      warp_store(a.load, base, n_valid, 3, bl, buf, a.vec);
+    }
+    if (kBlocks) {
+      const phfem_geom g = phfem_geometry(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      if (valid && !(g.t2 > 0.0)) atomicMin(&err->degenerate, (unsigned long long)m);
+      const phfem_coeff_values cv =
+          phfem_coeffs_eval(&a.coeffs, v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      double x[9];
+      if (a.B) {
+        phfem_stiffness(&g, &cv, x);
+        warp_store(a.B, base, n_valid, 9, x, buf, a.vec);
+      }
+      if (a.D) {
+        phfem_convection(&g, &cv, x);
+        warp_store(a.D, base, n_valid, 9, x, buf, a.vec);
+      }
+      if (a.M) {
+        phfem_mass(&g, cv.delta, x);
+        warp_store(a.M, base, n_valid, 9, x, buf, a.vec);
+      }
+      if (a.M0) {
+        phfem_unit_mass(&g, x);
+        warp_store(a.M0, base, n_valid, 9, x, buf, a.vec);
+      }
     }
   }
 }
 
 phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool load) {
   if (a.nE == 0) return PHFEM_OK;
-  const int64_t ntiles = ((int64_t)a.nE + kVolThreads - 1) / kVolThreads;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 16);
+  const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
+  const int grid = (int)std::min<int64_t>((nchunks + kVolWarps - 1) / kVolWarps,
+                                          (int64_t)ctx->num_sms * 8 * 4);
   if (blocks && load)
     PHFEM_LAUNCH(ctx, "k_volume", (k_volume<true, true><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
   else if (blocks)
@@ -97,53 +120,113 @@ VolArgs make_vol_args(const phfem_mesh* mesh) {
 }
 
 // ---------------------------------------------------------------------------
-// C in CSR: one CTA per 1024 consecutive edges.  Row pointers come from the
-// per-block boundary / Neumann prefixes of classify_edges plus an in-block scan
-// (a retained boundary row holds 2 entries, an interior row 4).
-__global__ void __launch_bounds__(1024) k_constraint_csr(
+// C in CSR: one CTA per 1024 consecutive edges, 4 edges per thread (vector
+// loads of the SoA edge arrays, 8 independent coordinate gathers in flight).
+// Row pointers come from the per-block boundary / Neumann prefixes of
+// classify_edges plus an in-block scan (a retained boundary row holds 2
+// entries, an interior row 4).  The block's (col, value) range is contiguous
+// in the output, so it is staged in SMEM and written with coalesced stores.
+constexpr int kCsrEdges = 1024;
+constexpr int kCsrThreads = 256;
+
+__global__ void __launch_bounds__(kCsrThreads) k_constraint_csr(
     const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
     const int32_t* __restrict__ edge_elements, const int32_t* __restrict__ ltp,
     const int32_t* __restrict__ ltm, const int32_t* __restrict__ rpos,
     const int32_t* __restrict__ pre_bnd, const int32_t* __restrict__ pre_neu, int E, int L,
     int32_t* __restrict__ row_ptr, int32_t* __restrict__ col, double* __restrict__ val) {
   __shared__ int32_t sm[33];
+  extern __shared__ __align__(16) unsigned char csr_smem[];
+  double* sval = reinterpret_cast<double*>(csr_smem);              // [4 * kCsrEdges]
+  int32_t* scol = reinterpret_cast<int32_t*>(sval + 4 * kCsrEdges);  // [4 * kCsrEdges]
   const int blk = blockIdx.x;
-  const int64_t e = (int64_t)blk * 1024 + threadIdx.x;
-  const bool valid = e < E;
-  const int rp = valid ? rpos[e] : -1;
-  const int2 el = valid ? reinterpret_cast<const int2*>(edge_elements)[e] : make_int2(0, 0);
-  const int rb = (valid && rp >= 0 && el.y < 0) ? 1 : 0;
-  int tot;
-  const int ex = block_exclusive_scan(rb, sm, &tot);
-  if (!valid || rp < 0) return;
-  const int bret = pre_bnd[blk] - pre_neu[blk] + ex;
-  int k = 4 * rp - 2 * bret;
-  row_ptr[rp] = k;
-  const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
-  const double2 pa = __ldg(coords + ab.x), pb = __ldg(coords + ab.y);
-  const double dx = pb.x - pa.x, dy = pb.y - pa.y;
-  const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
-  const int led = ltp[e];
-  const double vp = len * 0.5;     // lengths[e] * kR[led][c]   (assembly.cpp:160)
-  const double vm = -len * 0.5;    // -lengths[e] * kR[ledtn][c] (assembly.cpp:164)
+  const int64_t e0 = (int64_t)blk * kCsrEdges + 4 * threadIdx.x;
+  int rp[4], tp[4], tm[4], lp[4], lm[4], a[4], b[4];
+  if (e0 + 3 < E) {
+    const int4 r4 = *reinterpret_cast<const int4*>(rpos + e0);
+    const int4 el0 = *reinterpret_cast<const int4*>(edge_elements + 2 * e0);
+    const int4 el1 = *reinterpret_cast<const int4*>(edge_elements + 2 * e0 + 4);
+    const int4 en0 = *reinterpret_cast<const int4*>(edge_nodes + 2 * e0);
+    const int4 en1 = *reinterpret_cast<const int4*>(edge_nodes + 2 * e0 + 4);
+    const int4 p4 = *reinterpret_cast<const int4*>(ltp + e0);
+    const int4 m4 = *reinterpret_cast<const int4*>(ltm + e0);
+    rp[0] = r4.x; rp[1] = r4.y; rp[2] = r4.z; rp[3] = r4.w;
+    tp[0] = el0.x; tm[0] = el0.y; tp[1] = el0.z; tm[1] = el0.w;
+    tp[2] = el1.x; tm[2] = el1.y; tp[3] = el1.z; tm[3] = el1.w;
+    a[0] = en0.x; b[0] = en0.y; a[1] = en0.z; b[1] = en0.w;
+    a[2] = en1.x; b[2] = en1.y; a[3] = en1.z; b[3] = en1.w;
+    lp[0] = p4.x; lp[1] = p4.y; lp[2] = p4.z; lp[3] = p4.w;
+    lm[0] = m4.x; lm[1] = m4.y; lm[2] = m4.z; lm[3] = m4.w;
+  } else {
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-    if (c != led) {
-      col[k] = 3 * el.x + c;
-      val[k] = vp;
-      ++k;
+    for (int q = 0; q < 4; ++q) {
+      const int64_t e = e0 + q;
+      const bool ok = e < E;
+      rp[q] = ok ? rpos[e] : -1;
+      tp[q] = ok ? edge_elements[2 * e] : 0;
+      tm[q] = ok ? edge_elements[2 * e + 1] : -1;
+      a[q] = ok ? edge_nodes[2 * e] : 0;
+      b[q] = ok ? edge_nodes[2 * e + 1] : 0;
+      lp[q] = ok ? ltp[e] : 0;
+      lm[q] = ok ? ltm[e] : 0;
     }
-  if (el.y >= 0) {
-    const int ledtn = ltm[e];
+  }
+  double len[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    len[q] = 0.0;
+    if (rp[q] >= 0) {
+      const double2 pa = __ldg(coords + a[q]), pb = __ldg(coords + b[q]);
+      const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+      len[q] = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+    }
+  }
+  int rb = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rb += (rp[q] >= 0 && tm[q] < 0);
+  int tot;
+  int bret = block_exclusive_scan(rb, sm, &tot) + pre_bnd[blk] - pre_neu[blk];
+  const int64_t eb = (int64_t)blk * kCsrEdges;
+  const int R0 = (int)eb - pre_neu[blk];                  // retained rows before the block
+  const int k_first = 4 * R0 - 2 * (pre_bnd[blk] - pre_neu[blk]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (rp[q] < 0) continue;
+    const int k = 4 * rp[q] - 2 * bret;
+    row_ptr[rp[q]] = k;
+    int loc = k - k_first;
+    const double vp = len[q] * 0.5;   // lengths[e] * kR[led][c]    (assembly.cpp:160)
+    const double vm = -len[q] * 0.5;  // -lengths[e] * kR[ledtn][c] (assembly.cpp:164)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      if (c != ledtn) {
-        col[k] = 3 * el.y + c;
-        val[k] = vm;
-        ++k;
+      if (c != lp[q]) {
+        scol[loc] = 3 * tp[q] + c;
+        sval[loc] = vp;
+        ++loc;
       }
+    if (tm[q] >= 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (c != lm[q]) {
+          scol[loc] = 3 * tm[q] + c;
+          sval[loc] = vm;
+          ++loc;
+        }
+    } else {
+      ++bret;
+    }
+    if (rp[q] == L - 1) row_ptr[L] = k_first + loc;
   }
-  if (rp == L - 1) row_ptr[L] = k;
+  __syncthreads();
+  // block's entries: retained rows R0 .. R0 + nret - 1
+  const int nblock = (int)((int64_t)E - eb < kCsrEdges ? (int64_t)E - eb : kCsrEdges);
+  const int nret = nblock - (pre_neu[blk + 1] - pre_neu[blk]);
+  const int nbret = tot;
+  const int count = 4 * nret - 2 * nbret;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    col[k_first + i] = scol[i];
+    __stcs(val + k_first + i, sval[i]);
+  }
 }
 
 // C in Eigen CSC (column = primal DOF 3m+c; <= 2 entries, rows ascending).
@@ -223,7 +306,7 @@ __global__ void k_neu_insert(const int32_t* __restrict__ neu_ids, int nN,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nN;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int m = edge_elements[2 * neu_ids[i]];
-    uint32_t h = ((uint32_t)m * 2654435761u) & (uint32_t)(cap - 1);
+    uint32_t h = neu_hash(m, cap);
     while (true) {
       const int prev = atomicCAS(&keys[h], -1, m);
       if (prev == -1 || prev == m) break;
@@ -411,7 +494,13 @@ phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
     PHFEM_CUDA(ctx, cudaMemsetAsync(out->row_ptr, 0, sizeof(int32_t), ctx->stream));
     return PHFEM_OK;
   }
-  PHFEM_LAUNCH(ctx, "k_constraint_csr", k_constraint_csr<<<nblk, 1024, 0, ctx->stream>>>(
+  const int smem = 4 * kCsrEdges * (int)(sizeof(double) + sizeof(int32_t));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_constraint_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  PHFEM_LAUNCH(ctx, "k_constraint_csr", k_constraint_csr<<<nblk, kCsrThreads, smem, ctx->stream>>>(
       (const double2*)mesh->coords, topo->edge_nodes, topo->edge_elements, topo->local_in_tplus,
       topo->local_in_tminus, cls->retained_pos, cls->block_prefix, cls->block_prefix + nblk + 1, E,
       L, out->row_ptr, out->col_idx, out->values));

@@ -76,34 +76,44 @@ __global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
   cnt_neu[blk] = nn;
 }
 
-// CTA of 1024 threads per block of 1024 edges; warp w owns bitmap word w.
-__global__ void __launch_bounds__(kEdgeBlock) k_cls_retained(const uint32_t* __restrict__ bits,
-                                                             const int32_t* __restrict__ pre_neu,
-                                                             int E, int32_t* __restrict__ rpos,
-                                                             int32_t* __restrict__ redges) {
-  __shared__ int32_t wsum[32];
+// CTA of 256 threads per block of 1024 edges; thread t owns 4 consecutive
+// edges, all inside bitmap word t/8.
+__global__ void __launch_bounds__(256) k_cls_retained(const uint32_t* __restrict__ bits,
+                                                      const int32_t* __restrict__ pre_neu,
+                                                      int E, int32_t* __restrict__ rpos,
+                                                      int32_t* __restrict__ redges) {
+  __shared__ int32_t wpre[32];
   const int blk = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blk * kEdgeBlock + threadIdx.x;
-  const int64_t wi = (int64_t)blk * 32 + warp;
-  const uint32_t word = (wi < ((E + 31) >> 5)) ? bits[wi] : 0u;
-  if (lane == 0) wsum[warp] = __popc(word);
-  __syncthreads();
-  if (warp == 0) {
-    const int v = wsum[lane];
-    const int inc = warp_inclusive_scan(v);
-    wsum[lane] = inc - v;
+  const int nwords = (E + 31) >> 5;
+  if (threadIdx.x < 32) {
+    const int64_t wi = (int64_t)blk * 32 + threadIdx.x;
+    const int c = wi < nwords ? __popc(bits[wi]) : 0;
+    wpre[threadIdx.x] = warp_inclusive_scan(c) - c;
   }
   __syncthreads();
-  if (e >= E) return;
-  const int before = pre_neu[blk] + wsum[warp] + __popc(word & ((1u << lane) - 1u));
-  if ((word >> lane) & 1u) {
-    rpos[e] = -1;
+  const int t = threadIdx.x;
+  const int64_t e0 = (int64_t)blk * kEdgeBlock + 4 * t;
+  if (e0 >= E) return;
+  const int w = t >> 3;
+  const int64_t wi = (int64_t)blk * 32 + w;
+  const uint32_t word = bits[wi];
+  const int bit0 = (4 * t) & 31;
+  int before = pre_neu[blk] + wpre[w] + __popc(word & ((1u << bit0) - 1u));
+  int r[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool neu = (word >> (bit0 + q)) & 1u;
+    r[q] = neu ? -1 : (int)(e0 + q) - before;
+    before += neu;
+  }
+  if (e0 + 3 < E) {
+    *reinterpret_cast<int4*>(rpos + e0) = make_int4(r[0], r[1], r[2], r[3]);
   } else {
-    const int r = (int)e - before;
-    rpos[e] = r;
-    redges[r] = (int)e;
+    for (int q = 0; q < 4 && e0 + q < E; ++q) rpos[e0 + q] = r[q];
   }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (r[q] >= 0 && e0 + q < E) redges[r[q]] = (int)(e0 + q);
 }
 
 }  // namespace phfem
@@ -153,7 +163,7 @@ PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
   if (nblk > 0) {
-    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, kEdgeBlock, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
+    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
                                                          out->retained_pos, out->retained_edges));
   }
   // total Neumann count rides back with the error words (one sync)

@@ -66,7 +66,7 @@ constexpr int kCnThreads = 128;
 
 __device__ __forceinline__ int neu_lookup(const int32_t* __restrict__ keys, int cap, int m) {
   if (cap == 0) return -1;
-  uint32_t h = ((uint32_t)m * 2654435761u) & (uint32_t)(cap - 1);
+  uint32_t h = neu_hash(m, cap);
   while (true) {
     const int k = keys[h];
     if (k == m) return (int)h;

@@ -96,7 +96,7 @@ phfem_status dalloc(phfem_ctx* ctx, T** p, size_t count) {
 
 template <typename T>
 void dfree(phfem_ctx* ctx, T*& p) {
-  if (p) cudaFreeAsync((void*)p, ctx->stream);
+  if (p && ctx) cudaFreeAsync((void*)p, ctx->stream);
   p = nullptr;
 }
 

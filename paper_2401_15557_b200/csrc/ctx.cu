@@ -239,7 +239,7 @@ PHFEM_API phfem_status phfem_alloc(phfem_ctx* ctx, size_t bytes, void** out) {
 }
 
 PHFEM_API void phfem_free(phfem_ctx* ctx, void* ptr) {
-  if (ptr) cudaFreeAsync(ptr, ctx->stream);
+  if (ptr && ctx) cudaFreeAsync(ptr, ctx->stream);
 }
 
 PHFEM_API phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {

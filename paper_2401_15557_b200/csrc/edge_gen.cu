@@ -73,15 +73,6 @@ __global__ void __launch_bounds__(256) k_eg_count(const int32_t* __restrict__ el
   }
 }
 
-__global__ void k_eg_max(const int32_t* __restrict__ bcount, int n, phfem_dev_errors* err) {
-  int mx = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    mx = max(mx, bcount[i]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane_id() == 0) atomicMax(&err->counters[3], (unsigned long long)mx);
-}
-
 // C ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ elements,
                                                     EgParams P, int32_t* __restrict__ cursor,
@@ -177,125 +168,165 @@ __device__ __forceinline__ uint64_t eg_lookback(unsigned long long* status, int 
   return (ex_e << 32) | ex_b;
 }
 
-__global__ void k_eg_bucket(const uint64_t* __restrict__ items, const int32_t* __restrict__ boff,
-                            EgParams P, int cap, uint64_t* __restrict__ overflow,
-                            unsigned long long* status, int32_t* ticket, EgOut out,
-                            phfem_dev_errors* err) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int NB = 1 << P.bs;
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smraw);
-  int32_t* cur = reinterpret_cast<int32_t*>(buf + cap);
-  __shared__ unsigned long long scan_sm[33];
-  __shared__ int s_b;
-  __shared__ unsigned long long s_prefix;
+// One CTA per tile of kTileNodes consecutive max-node ids (= 256 >> bs
+// consecutive buckets).  Item-parallel throughout: counting sort by node,
+// per-segment rank sort (segments are tiny: ~6 occurrences per node), blocked
+// run detection + block scan, look-back, then every run start emits its edge.
+constexpr int kTileNodes = 256;
+constexpr int kTileThreads = 256;
+constexpr int kTileCap = 10 * kTileNodes;  // items kept in SMEM (10 per node)
 
+struct TileSmem {
+  uint64_t buf1[kTileCap];
+  uint64_t buf2[kTileCap];
+  uint8_t node_of[kTileCap];
+  int32_t cnt[kTileNodes];
+  int32_t seg[kTileNodes];
+  int32_t cur[kTileNodes];
+  int32_t nedge[kTileNodes];
+  int32_t sbo[kTileNodes + 1];
+  unsigned long long scan[33];
+  unsigned long long prefix;
+  int tile;
+};
+
+template <bool kS>
+__device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, const EgParams& P,
+                                        TileSmem& sm, uint64_t* g1, uint64_t* g2, uint8_t* gnode,
+                                        unsigned long long* status, const EgOut& out,
+                                        phfem_dev_errors* err) {
   const int tid = threadIdx.x;
   const int T = blockDim.x;
-  if (tid == 0) s_b = atomicAdd(ticket, 1);
-  __syncthreads();
-  const int b = s_b;
-  const int64_t s = boff[b];
-  const int n = boff[b + 1] - (int)s;
-  uint64_t* sorted = (n <= cap) ? buf : overflow + s;
+  const int tile = sm.tile;
+  const int nsub = kTileNodes >> P.bs;
+  const int64_t s = sm.sbo[0];
+  const int n = sm.sbo[nsub] - (int)s;
+  uint64_t* buf1 = kS ? sm.buf1 : g1 + s;
+  uint64_t* buf2 = kS ? sm.buf2 : g2 + s;
+  uint8_t* node_of = kS ? sm.node_of : gnode + s;
   const int shift = P.total_bits;
+  const uint64_t kmask = (1ull << shift) - 1ull;
+  auto local_node = [&](int p, uint64_t it) -> int {
+    int sub = 0;
+    if (nsub > 1) {  // last sub-bucket whose start <= s + p
+      int lo = 0, hi = nsub - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sm.sbo[mid] - s <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      sub = lo;
+    }
+    return (sub << P.bs) | (int)(it >> shift);
+  };
 
-  for (int i = tid; i < NB; i += T) cur[i] = 0;
+  // counting sort by max node
+  for (int p = tid; p < n; p += T) {
+    const uint64_t it = __ldg(items + s + p);
+    atomicAdd(&sm.cnt[local_node(p, it)], 1);
+  }
   __syncthreads();
-  for (int p = tid; p < n; p += T) atomicAdd(&cur[(int)(__ldg(items + s + p) >> shift)], 1);
-  __syncthreads();
-  const int c = tid < NB ? cur[tid] : 0;
+  const int c_me = sm.cnt[tid];
   unsigned long long tot;
-  const int st = (int)block_exclusive_scan((unsigned long long)c, scan_sm, &tot);
-  if (tid < NB) cur[tid] = st;
+  const int st_me = (int)block_exclusive_scan((unsigned long long)c_me, sm.scan, &tot);
+  sm.seg[tid] = st_me;
+  sm.cur[tid] = st_me;
   __syncthreads();
   for (int p = tid; p < n; p += T) {
     const uint64_t it = __ldg(items + s + p);
-    const int pos = atomicAdd(&cur[(int)(it >> shift)], 1);
-    sorted[pos] = it;
+    const int nd = local_node(p, it);
+    const int pos = atomicAdd(&sm.cur[nd], 1);
+    buf1[pos] = it;
+    node_of[pos] = (uint8_t)nd;
+  }
+  __syncthreads();
+  // rank sort inside each node segment: key = (min node, occurrence, dir)
+  for (int p = tid; p < n; p += T) {
+    const uint64_t it = buf1[p];
+    const uint64_t k = it & kmask;
+    const int nd = node_of[p];
+    const int st = sm.seg[nd], c = sm.cnt[nd];
+    int r = 0;
+    for (int q = st; q < st + c; ++q) r += (buf1[q] & kmask) < k;
+    buf2[st + r] = it;
   }
   __syncthreads();
 
-  // --- per max-node segment: sort, runs, checks --------------------------
-  const int64_t v = (int64_t)b * NB + tid;
+  // blocked run detection
   const int lo_shift = P.occ_bits + 1;
   const uint64_t lo_mask = (1ull << P.lo_bits) - 1ull;
+  const int K = (n + T - 1) / T;
+  const int p0 = min(n, tid * K), p1 = min(n, p0 + K);
   uint32_t ne_i = 0, nb_i = 0;
-  if (tid < NB && c > 0) {
-    uint64_t* seg = sorted + st;
-    for (int i = 1; i < c; ++i) {  // insertion sort by packed value
-      const uint64_t x = seg[i];
-      int j = i - 1;
-      while (j >= 0 && seg[j] > x) {
-        seg[j + 1] = seg[j];
-        --j;
-      }
-      seg[j + 1] = x;
+  for (int p = p0; p < p1; ++p) {
+    const int nd = node_of[p];
+    const int st = sm.seg[nd], en = st + sm.cnt[nd];
+    const uint64_t f = buf2[p];
+    const uint64_t lo = (f >> lo_shift) & lo_mask;
+    if (p != st && ((buf2[p - 1] >> lo_shift) & lo_mask) == lo) continue;
+    int len = 1;
+    while (p + len < en && ((buf2[p + len] >> lo_shift) & lo_mask) == lo) ++len;
+    if (len > 2 || (len == 2 && ((f ^ buf2[p + 1]) & 1ull) == 0)) {
+      const uint64_t v = (uint64_t)tile * kTileNodes + nd;
+      atomicMin(&err->topo, (v << 33) | (lo << 2) | (len > 2 ? 0ull : (2ull | (f & 1ull))));
     }
-    for (int q = 0; q < c;) {
-      const uint64_t lo = (seg[q] >> lo_shift) & lo_mask;
-      int r = q + 1;
-      while (r < c && ((seg[r] >> lo_shift) & lo_mask) == lo) ++r;
-      const int len = r - q;
-      if (len > 2) {
-        atomicMin(&err->topo, ((uint64_t)v << 33) | (lo << 2) | 0ull);
-      } else if (len == 2 && ((seg[q] ^ seg[q + 1]) & 1ull) == 0) {
-        atomicMin(&err->topo, ((uint64_t)v << 33) | (lo << 2) | 2ull | (seg[q] & 1ull));
-      }
-      ++ne_i;
-      if (len == 1) ++nb_i;
-      q = r;
-    }
+    ++ne_i;
+    nb_i += (len == 1);
+    atomicAdd(&sm.nedge[nd], 1);
   }
   unsigned long long agg;
   const unsigned long long ex =
-      block_exclusive_scan(((unsigned long long)ne_i << 32) | nb_i, scan_sm, &agg);
+      block_exclusive_scan(((unsigned long long)ne_i << 32) | nb_i, sm.scan, &agg);
+  // per-node first edge (max-node grouping table)
+  const int ne_node = sm.nedge[tid];
+  unsigned long long tot2;
+  const int nes_local = (int)block_exclusive_scan((unsigned long long)ne_node, sm.scan, &tot2);
   if (tid < 32) {
-    const uint64_t pre = eg_lookback(status, b, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
-    if (tid == 0) s_prefix = pre;
+    const uint64_t pre =
+        eg_lookback(status, tile, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
+    if (tid == 0) sm.prefix = pre;
   }
   __syncthreads();
-  const uint64_t pre = s_prefix;
+  const uint64_t pre = sm.prefix;
+  const int64_t v_me = (int64_t)tile * kTileNodes + tid;
+  if (v_me < P.nC) out.node_edge_start[v_me] = (int32_t)(pre >> 32) + nes_local;
   int32_t e = (int32_t)((pre >> 32) + (ex >> 32));
   int32_t bpos = (int32_t)((pre & 0xffffffffu) + (ex & 0xffffffffu));
   int32_t ipos = e - bpos;
-  if (tid < NB && v < P.nC) out.node_edge_start[v] = e;
-  if (tid < NB && c > 0) {
-    const uint64_t* seg = sorted + st;
-    const uint32_t occ_mask = (uint32_t)((1ull << P.occ_bits) - 1ull);
-    for (int q = 0; q < c;) {
-      const uint64_t f = seg[q];
-      const uint64_t lo = (f >> lo_shift) & lo_mask;
-      int r = q + 1;
-      while (r < c && ((seg[r] >> lo_shift) & lo_mask) == lo) ++r;
-      const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
-      const int m_f = (int)(occ_f / 3u);
-      const int l_f = (int)((occ_f % 3u + 2u) % 3u);
-      const bool dir = f & 1ull;
-      out.edge_nodes[2 * (int64_t)e] = dir ? (int32_t)v : (int32_t)lo;
-      out.edge_nodes[2 * (int64_t)e + 1] = dir ? (int32_t)lo : (int32_t)v;
-      out.ltp[e] = l_f;
-      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
-      if (r - q >= 2) {
-        const uint64_t g = seg[q + 1];
-        const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
-        const int m_g = (int)(occ_g / 3u);
-        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
-        out.edge_elements[2 * (int64_t)e] = m_f;
-        out.edge_elements[2 * (int64_t)e + 1] = m_g;
-        out.ltm[e] = l_g;
-        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
-        out.interior[ipos++] = e;
-      } else {
-        out.edge_elements[2 * (int64_t)e] = m_f;
-        out.edge_elements[2 * (int64_t)e + 1] = -1;
-        out.ltm[e] = -1;
-        out.boundary[bpos++] = e;
-      }
-      ++e;
-      q = r;
+  const uint32_t occ_mask = (uint32_t)((1ull << P.occ_bits) - 1ull);
+  for (int p = p0; p < p1; ++p) {
+    const int nd = node_of[p];
+    const int st = sm.seg[nd], en = st + sm.cnt[nd];
+    const uint64_t f = buf2[p];
+    const uint64_t lo = (f >> lo_shift) & lo_mask;
+    if (p != st && ((buf2[p - 1] >> lo_shift) & lo_mask) == lo) continue;
+    const bool two = p + 1 < en && ((buf2[p + 1] >> lo_shift) & lo_mask) == lo;
+    const int32_t v = (int32_t)(tile * kTileNodes + nd);
+    const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
+    const int m_f = (int)(occ_f / 3u);
+    const int l_f = (int)((occ_f % 3u + 2u) % 3u);
+    const bool dir = f & 1ull;
+    reinterpret_cast<int2*>(out.edge_nodes)[e] =
+        dir ? make_int2(v, (int32_t)lo) : make_int2((int32_t)lo, v);
+    out.ltp[e] = l_f;
+    out.elem_edge[3 * (int64_t)m_f + l_f] = e;
+    if (two) {
+      const uint64_t g = buf2[p + 1];
+      const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
+      const int m_g = (int)(occ_g / 3u);
+      const int l_g = (int)((occ_g % 3u + 2u) % 3u);
+      reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
+      out.ltm[e] = l_g;
+      out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+      out.interior[ipos++] = e;
+    } else {
+      reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
+      out.ltm[e] = -1;
+      out.boundary[bpos++] = e;
     }
+    ++e;
   }
-  if (b == P.nb - 1 && tid == 0) {
+  if (tile == P.nb - 1 && tid == 0) {
     const uint64_t E = (pre >> 32) + (agg >> 32);
     const uint64_t NBd = (pre & 0xffffffffu) + (agg & 0xffffffffu);
     err->counters[0] = E;
@@ -303,6 +334,41 @@ __global__ void k_eg_bucket(const uint64_t* __restrict__ items, const int32_t* _
     err->counters[2] = NBd;
     out.node_edge_start[P.nC] = (int32_t)E;
   }
+}
+
+// P.nb here = number of tiles; boff has one entry per bucket (+1).
+__global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __restrict__ items,
+                                                          const int32_t* __restrict__ boff,
+                                                          int nbuckets, EgParams P, uint64_t* g1,
+                                                          uint64_t* g2, uint8_t* gnode,
+                                                          unsigned long long* status,
+                                                          int32_t* ticket, EgOut out,
+                                                          phfem_dev_errors* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
+  const int tid = threadIdx.x;
+  if (tid == 0) sm.tile = atomicAdd(ticket, 1);
+  sm.cnt[tid] = 0;
+  sm.nedge[tid] = 0;
+  __syncthreads();
+  const int nsub = kTileNodes >> P.bs;
+  for (int i = tid; i <= nsub; i += blockDim.x)
+    sm.sbo[i] = boff[min(sm.tile * nsub + i, nbuckets)];
+  __syncthreads();
+  if (sm.sbo[nsub] - sm.sbo[0] <= kTileCap)
+    eg_tile<true>(items, P, sm, g1, g2, gnode, status, out, err);
+  else
+    eg_tile<false>(items, P, sm, g1, g2, gnode, status, out, err);
+}
+
+__global__ void k_eg_tile_max(const int32_t* __restrict__ boff, int nbuckets, int nsub, int ntiles,
+                              phfem_dev_errors* err) {
+  int mx = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+    mx = max(mx, boff[min((t + 1) * nsub, nbuckets)] - boff[t * nsub]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane_id() == 0) atomicMax(&err->counters[3], (unsigned long long)mx);
 }
 
 }  // namespace phfem
@@ -365,16 +431,20 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   unsigned long long* status = nullptr;
   PHFEM_TRY(dalloc(ctx, &bcount, (int64_t)P.nb + 1));
   PHFEM_TRY(dalloc(ctx, &boff, (int64_t)P.nb + 1));
-  PHFEM_TRY(dalloc(ctx, &status, P.nb));
+  PHFEM_TRY(dalloc(ctx, &status, (P.nC + 255) / 256 + 1));
   PHFEM_TRY(dalloc(ctx, &ticket, 1));
   PHFEM_CUDA(ctx, cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (P.nb + 1), ctx->stream));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * P.nb, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ((P.nC + 255) / 256 + 1),
+                                  ctx->stream));
   PHFEM_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(int32_t), ctx->stream));
 
   const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
+  const int nsub = kTileNodes >> P.bs;
+  const int ntiles = (int)((nC + kTileNodes - 1) / kTileNodes);
   PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, bcount, ctx->derr));
-  PHFEM_LAUNCH(ctx, "k_eg_max", k_eg_max<<<grid_for(P.nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(bcount, P.nb, ctx->derr));
   PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
+  PHFEM_LAUNCH(ctx, "k_eg_tile_max", k_eg_tile_max<<<grid_for(ntiles, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      boff, P.nb, nsub, ntiles, ctx->derr));
   int32_t* cursor = bcount;  // reuse as scatter cursor
   PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, boff, sizeof(int32_t) * P.nb, cudaMemcpyDeviceToDevice,
                                   ctx->stream));
@@ -386,25 +456,35 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
                      "build_topology: element %lld has a node index outside 1..%lld", m + 1,
                      (long long)nC);
   }
-  const int64_t max_bucket = (int64_t)ctx->herr->counters[3];
+  const int64_t max_tile = (int64_t)ctx->herr->counters[3];
 
   uint64_t* items = nullptr;
-  uint64_t* overflow = nullptr;
+  uint64_t *g1 = nullptr, *g2 = nullptr;
+  uint8_t* gnode = nullptr;
   PHFEM_TRY(dalloc(ctx, &items, nd));
-  const int cap = 16 * NB;  // SMEM capacity per bucket (16 occurrences per node)
-  if (max_bucket > cap) PHFEM_TRY(dalloc(ctx, &overflow, nd));
+  if (max_tile > kTileCap) {  // some tile does not fit SMEM: global scratch
+    PHFEM_TRY(dalloc(ctx, &g1, nd));
+    PHFEM_TRY(dalloc(ctx, &g2, nd));
+    PHFEM_TRY(dalloc(ctx, &gnode, nd));
+  }
   PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, cursor, items));
 
   EgOut o{out->edge_nodes, out->edge_elements, out->local_in_tplus, out->local_in_tminus,
           out->interior_edges, out->boundary_edges, out->elem_edge, out->node_edge_start};
-  const int threads = std::max(32, NB);
-  const size_t smem = (size_t)cap * sizeof(uint64_t) + (size_t)(NB + 1) * sizeof(int32_t);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_eg_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  PHFEM_LAUNCH(ctx, "k_eg_bucket", k_eg_bucket<<<P.nb, threads, smem, ctx->stream>>>(items, boff, P, cap, overflow, status, ticket,
-                                                    o, ctx->derr));
+  EgParams PT = P;
+  PT.nb = ntiles;
+  const size_t smem = sizeof(TileSmem);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_eg_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
+      items, boff, P.nb, PT, g1, g2, gnode, status, ticket, o, ctx->derr));
   dfree(ctx, items);
-  dfree(ctx, overflow);
+  dfree(ctx, g1);
+  dfree(ctx, g2);
+  dfree(ctx, gnode);
   dfree(ctx, bcount);
   dfree(ctx, boff);
   dfree(ctx, status);

@@ -44,6 +44,12 @@ __device__ __forceinline__ void element_load(double2 v0, double2 v1, double2 v2,
   for (int i = 0; i < 3; ++i) bl[i] = 0.0 + area / 3.0 * 0.5 * (fm[(i + 1) % 3] + fm[(i + 2) % 3]);
 }
 
+// Fibonacci hashing: the HIGH bits of m * 2^32/phi (element ids of boundary
+// elements are highly structured -- low bits alone collide).
+__device__ __forceinline__ uint32_t neu_hash(int m, int cap) {
+  return (uint32_t)(((uint64_t)(uint32_t)m * 11400714819323198485ull) >> 32) & (uint32_t)(cap - 1);
+}
+
 struct NeuArgs {
   const double2* coords;
   const int32_t* edge_nodes;
