@@ -232,7 +232,7 @@ def run_ours(args):
     fields = G.config_fields(5)
     dm = build_input(ctx, args.level - 1)          # L12 input, resident in HBM
     # sizes at both levels (one untimed run)
-    r = capi.pipeline(ctx, dm, 1, *fields)
+    r = capi.pipeline(ctx, dm, 1, *fields, flags=capi.PIPE_GENERIC_EG if args.generic_eg else 0)
     o = r.out
     s = {"nC": o.mesh.nC, "nE": o.mesh.nE, "E": o.topo.E, "L": o.cls.L, "nnz": o.C.nnz}
     r.release()
@@ -242,8 +242,9 @@ def run_ours(args):
     compulsory = (eg_bytes(s0["nE"], s0["E"]) + rf_bytes(s0["nC"], s0["nE"], s0["E"]) +
                   eg_bytes(s["nE"], s["E"]) + as_bytes(s["nC"], s["nE"], s["E"], s["L"], s["nnz"]))
 
+    flags = capi.PIPE_GENERIC_EG if args.generic_eg else 0
     for _ in range(args.warmup):
-        capi.pipeline(ctx, dm, 1, *fields).release()
+        capi.pipeline(ctx, dm, 1, *fields, flags=flags).release()
     ctx.sync()
 
     import torch
@@ -256,7 +257,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            capi.pipeline(ctx, dm, 1, *fields).release()
+            capi.pipeline(ctx, dm, 1, *fields, flags=flags).release()
         ev1.record(stream)
         ctx.sync()
     ms_local = ev0.elapsed_time(ev1) / args.steps
@@ -293,6 +294,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} "
                                f"({s['nE']} triangles): EG+RF+EG+AS, config-2 coefficients",
+                   "refined_edge_generation": "sort-based (generic)" if args.generic_eg
+                   else "from parent topology (SURVEY f1, bit-identical)",
                    "triangles": s["nE"], "edges": s["E"], "multipliers": s["L"], "nnz_C": s["nnz"],
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "inputs larger than L2 (no flush)"},
@@ -403,6 +406,8 @@ def main():
     ap.add_argument("--ref-level", type=int, default=9)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--generic-eg", action="store_true",
+                    help="sort-based edge generation on the refined mesh too (no SURVEY f1 shortcut)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

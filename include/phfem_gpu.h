@@ -136,6 +136,14 @@ void phfem_classification_release(phfem_ctx* ctx, phfem_classification* cls);
 phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                               phfem_mesh* out);
 
+/* build_topology(red_refine(mesh)) computed from the parent topology with
+ * two streaming passes and no sort; `fine` must be the
+ * phfem_red_refine output of (parent, parent_topo).  Bit-identical to
+ * phfem_build_topology(fine).                                               */
+phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* parent,
+                                   const phfem_topology* parent_topo, const phfem_mesh* fine,
+                                   phfem_topology* out);
+
 /* ---- orientation normalisation (config 4; not in the reference) ----------
  * Swaps v1<->v2 of every element with negative signed area, in place.       */
 phfem_status phfem_orient_ccw(phfem_ctx* ctx, phfem_mesh* mesh);
@@ -232,6 +240,12 @@ typedef struct phfem_pipeline_out {
 phfem_status phfem_pipeline(phfem_ctx* ctx, const phfem_mesh* mesh_in, int levels,
                             const phfem_coeffs* c, const phfem_field* f, const phfem_field* g,
                             const phfem_field* uD, double t, phfem_pipeline_out* out);
+/* flags: PHFEM_PIPE_GENERIC_EG = run the sort-based build_topology on every
+ * refined mesh instead of phfem_refine_topology (same results).            */
+#define PHFEM_PIPE_GENERIC_EG 1
+phfem_status phfem_pipeline_ex(phfem_ctx* ctx, const phfem_mesh* mesh_in, int levels,
+                               const phfem_coeffs* c, const phfem_field* f, const phfem_field* g,
+                               const phfem_field* uD, double t, int flags, phfem_pipeline_out* out);
 void phfem_pipeline_release(phfem_ctx* ctx, phfem_pipeline_out* out);
 
 /* Host-buffer variant (what a reference caller sees): the input mesh comes

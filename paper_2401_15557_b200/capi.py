@@ -142,7 +142,9 @@ EXPORTED = [
     "phfem_cn_rhs", "phfem_cn_plan_destroy", "phfem_pipeline", "phfem_pipeline_release",
     "phfem_pipeline_from_host", "phfem_pipeline_download", "phfem_pipeline_download_bytes",
     "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_ctx_profile", "phfem_ctx_profile_read",
+    "phfem_refine_topology", "phfem_pipeline_ex",
 ]
+PIPE_GENERIC_EG = 1
 
 _lib = None
 
@@ -202,6 +204,10 @@ def load_library(path: str = LIB_PATH):
         "phfem_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_size_t]),
         "phfem_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_size_t]),
         "phfem_ctx_profile": (C.c_int, [vp, C.c_int]),
+        "phfem_refine_topology": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_mesh),
+                                            P(phfem_topology)]),
+        "phfem_pipeline_ex": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(phfem_coeffs), P(phfem_field),
+                                        P(phfem_field), P(phfem_field), dbl, C.c_int, P(phfem_pipeline_out)]),
         "phfem_ctx_profile_read": (C.c_int, [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
@@ -441,6 +447,14 @@ def red_refine(ctx: Context, mesh: DeviceMesh, topo: Topology) -> DeviceMesh:
     return DeviceMesh(ctx, out)
 
 
+def refine_topology(ctx: Context, parent: DeviceMesh, ptopo: Topology, fine: DeviceMesh) -> Topology:
+    """build_topology(red_refine(parent)) from the parent topology, no sort."""
+    t = phfem_topology()
+    ctx.check(ctx.lib.phfem_refine_topology(ctx.ptr, C.byref(parent.m), C.byref(ptopo.t), C.byref(fine.m),
+                                            C.byref(t)))
+    return Topology(ctx, t)
+
+
 def orient_ccw(ctx: Context, mesh: DeviceMesh):
     ctx.check(ctx.lib.phfem_orient_ccw(ctx.ptr, C.byref(mesh.m)))
 
@@ -601,8 +615,8 @@ class PipelineResult:
 
 
 def pipeline(ctx: Context, mesh: DeviceMesh, levels: int, coeffs: phfem_coeffs, f: phfem_field,
-             g: phfem_field, uD: phfem_field, t: float = 0.0) -> PipelineResult:
+             g: phfem_field, uD: phfem_field, t: float = 0.0, flags: int = 0) -> PipelineResult:
     out = phfem_pipeline_out()
-    ctx.check(ctx.lib.phfem_pipeline(ctx.ptr, C.byref(mesh.m), levels, C.byref(coeffs), C.byref(f),
-                                     C.byref(g), C.byref(uD), t, C.byref(out)))
+    ctx.check(ctx.lib.phfem_pipeline_ex(ctx.ptr, C.byref(mesh.m), levels, C.byref(coeffs), C.byref(f),
+                                        C.byref(g), C.byref(uD), t, flags, C.byref(out)))
     return PipelineResult(ctx, out)

@@ -336,6 +336,201 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
   }
 }
 
+// Fast tile path: after the counting sort by max node, each warp takes its
+// 32 nodes in node-aligned chunks of <= 32 occurrences and sorts a chunk with
+// a register bitonic network on the key (chunk-local node | min node |
+// occurrence).  Partners, run starts and the reference's error checks are
+// then lane-neighbour tests; edge ranks are ballot/popc prefixes, so the
+// emission pass writes consecutive edge ids from consecutive lanes.
+__device__ __forceinline__ void warp_bitonic32(uint64_t& key, uint32_t& pay) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, j);
+      const uint32_t op = __shfl_xor_sync(0xffffffffu, pay, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      const bool take = (lower == up) ? (ok < key) : (ok > key);
+      if (take) {
+        key = ok;
+        pay = op;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items, const EgParams& P,
+                                             TileSmem& sm, unsigned long long* status,
+                                             const EgOut& out, phfem_dev_errors* err) {
+  const int tid = threadIdx.x;
+  const int T = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int tile = sm.tile;
+  const int nsub = kTileNodes >> P.bs;
+  const int64_t s = sm.sbo[0];
+  const int n = sm.sbo[nsub] - (int)s;
+  const int shift = P.total_bits;
+  const int ob = P.occ_bits;
+  const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
+  const uint64_t lokmask = (1ull << (P.lo_bits + P.occ_bits)) - 1ull;
+  const uint32_t occ_mask = (uint32_t)((1ull << ob) - 1ull);
+  const unsigned lt = lanemask_lt();
+
+  // counting sort by node (histogram already in sm.cnt)
+  const int c_me = sm.cnt[tid];
+  unsigned long long tot;
+  const int st_me = (int)block_exclusive_scan((unsigned long long)c_me, sm.scan, &tot);
+  sm.seg[tid] = st_me;
+  sm.cur[tid] = st_me;
+  __syncthreads();
+  for (int p = tid; p < n; p += T) {
+    const uint64_t it = __ldg(items + s + p);
+    int sub = 0;
+    if (nsub > 1) {
+      int lo = 0, hi = nsub - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sm.sbo[mid] - s <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      sub = lo;
+    }
+    const int nd = (sub << P.bs) | (int)(it >> shift);
+    const int pos = atomicAdd(&sm.cur[nd], 1);
+    sm.buf1[pos] = it;
+    sm.node_of[pos] = (uint8_t)nd;
+  }
+  __syncthreads();
+
+  // per warp: node-aligned chunks, sort, counts
+  const int cnt_l = sm.cnt[32 * warp + lane];
+  const int incl = warp_inclusive_scan(cnt_l);
+  const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+  const int wbase = sm.seg[32 * warp];
+  uint32_t w_ne = 0, w_nb = 0;
+  int cs = 0, base = 0;
+  while (base < wtotal) {
+    const unsigned fits = __ballot_sync(0xffffffffu, lane >= cs && incl - base <= 32);
+    const int ce = 32 - __clz(fits);                    // one past the last node of the chunk
+    const int nitems = __shfl_sync(0xffffffffu, incl, ce - 1) - base;
+    const int pos = wbase + base + lane;
+    const bool valid = lane < nitems;
+    uint64_t key = ~0ull;
+    uint32_t dir = 0;
+    int nd = 0;
+    if (valid) {
+      const uint64_t it = sm.buf1[pos];
+      nd = sm.node_of[pos];
+      key = ((uint64_t)(nd - 32 * warp - cs) << 59) | ((it >> 1) & lokmask);
+      dir = (uint32_t)(it & 1ull);
+    }
+    warp_bitonic32(key, dir);
+    if (valid) {
+      nd = sm.node_of[pos];  // node grouping is preserved by the sort
+      sm.buf2[pos] = ((key & lokmask) << 1) | dir;
+    }
+    const uint64_t grp = key >> ob;
+    const uint64_t gp = __shfl_up_sync(0xffffffffu, grp, 1);
+    const uint64_t gn = __shfl_down_sync(0xffffffffu, grp, 1);
+    const uint64_t gn2 = __shfl_down_sync(0xffffffffu, grp, 2);
+    const uint32_t dn = __shfl_down_sync(0xffffffffu, dir, 1);
+    const bool start = valid && (lane == 0 || gp != grp);
+    const bool partner = valid && lane + 1 < nitems && gn == grp;
+    const bool third = partner && lane + 2 < nitems && gn2 == grp;
+    if (start && (third || (partner && dn == dir))) {
+      const uint64_t v = (uint64_t)tile * kTileNodes + nd;
+      const uint64_t lo = (key >> ob) & lomask;
+      atomicMin(&err->topo, (v << 33) | (lo << 2) | (third ? 0ull : (2ull | dir)));
+    }
+    if (start) atomicAdd(&sm.nedge[nd], 1);
+    w_ne += __popc(__ballot_sync(0xffffffffu, start));
+    w_nb += __popc(__ballot_sync(0xffffffffu, start && !partner));
+    base += nitems;
+    cs = ce;
+  }
+  // CTA totals: per-warp offsets
+  __shared__ unsigned long long wsum[kTileThreads / 32];
+  if (lane == 0) wsum[warp] = ((unsigned long long)w_ne << 32) | w_nb;
+  __syncthreads();
+  unsigned long long wex = 0, agg = 0;
+  for (int w = 0; w < (T >> 5); ++w) {
+    if (w < warp) wex += wsum[w];
+    agg += wsum[w];
+  }
+  const int ne_node = sm.nedge[tid];
+  unsigned long long tot2;
+  const int nes_local = (int)block_exclusive_scan((unsigned long long)ne_node, sm.scan, &tot2);
+  if (tid < 32) {
+    const uint64_t pre =
+        eg_lookback(status, tile, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
+    if (tid == 0) sm.prefix = pre;
+  }
+  __syncthreads();
+  const uint64_t pre = sm.prefix;
+  const int64_t v_me = (int64_t)tile * kTileNodes + tid;
+  if (v_me < P.nC) out.node_edge_start[v_me] = (int32_t)(pre >> 32) + nes_local;
+
+  // emission: consecutive positions, ranks by ballot
+  int32_t e_off = (int32_t)((pre >> 32) + (wex >> 32));
+  int32_t b_off = (int32_t)((pre & 0xffffffffu) + (wex & 0xffffffffu));
+  for (int q = 0; q < wtotal; q += 32) {
+    const int pos = wbase + q + lane;
+    const bool valid = q + lane < wtotal;
+    bool start = false, partner = false;
+    uint64_t f = 0, g = 0;
+    int nd = 0;
+    if (valid) {
+      f = sm.buf2[pos];
+      nd = sm.node_of[pos];
+      const int st = sm.seg[nd], en = st + sm.cnt[nd];
+      const uint64_t lo = (f >> (ob + 1)) & lomask;
+      start = pos == st || ((sm.buf2[pos - 1] >> (ob + 1)) & lomask) != lo;
+      if (start && pos + 1 < en) {
+        g = sm.buf2[pos + 1];
+        partner = ((g >> (ob + 1)) & lomask) == lo;
+      }
+    }
+    const unsigned sb = __ballot_sync(0xffffffffu, start);
+    const unsigned bb = __ballot_sync(0xffffffffu, start && !partner);
+    if (start) {
+      const int32_t e = e_off + __popc(sb & lt);
+      const int32_t v = tile * kTileNodes + nd;
+      const int32_t lo = (int32_t)((f >> (ob + 1)) & lomask);
+      const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
+      const int m_f = (int)(occ_f / 3u);
+      const int l_f = (int)((occ_f % 3u + 2u) % 3u);
+      reinterpret_cast<int2*>(out.edge_nodes)[e] = (f & 1ull) ? make_int2(v, lo) : make_int2(lo, v);
+      out.ltp[e] = l_f;
+      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
+      if (partner) {
+        const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
+        const int m_g = (int)(occ_g / 3u);
+        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
+        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
+        out.ltm[e] = l_g;
+        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+        out.interior[e - (b_off + __popc(bb & lt))] = e;
+      } else {
+        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
+        out.ltm[e] = -1;
+        out.boundary[b_off + __popc(bb & lt)] = e;
+      }
+    }
+    e_off += __popc(sb);
+    b_off += __popc(bb);
+  }
+  if (tile == P.nb - 1 && tid == 0) {
+    const uint64_t E = (pre >> 32) + (agg >> 32);
+    const uint64_t NBd = (pre & 0xffffffffu) + (agg & 0xffffffffu);
+    err->counters[0] = E;
+    err->counters[1] = E - NBd;
+    err->counters[2] = NBd;
+    out.node_edge_start[P.nC] = (int32_t)E;
+  }
+}
+
 // P.nb here = number of tiles; boff has one entry per bucket (+1).
 __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __restrict__ items,
                                                           const int32_t* __restrict__ boff,
@@ -355,7 +550,33 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
   for (int i = tid; i <= nsub; i += blockDim.x)
     sm.sbo[i] = boff[min(sm.tile * nsub + i, nbuckets)];
   __syncthreads();
-  if (sm.sbo[nsub] - sm.sbo[0] <= kTileCap)
+  const int64_t s = sm.sbo[0];
+  const int n = sm.sbo[nsub] - (int)s;
+  bool fast = n <= kTileCap && P.lo_bits + P.occ_bits <= 59;
+  if (fast) {  // histogram by node; the fast path needs every node <= 32 occurrences
+    for (int p = tid; p < n; p += blockDim.x) {
+      const uint64_t it = __ldg(items + s + p);
+      int sub = 0;
+      if (nsub > 1) {
+        int lo = 0, hi = nsub - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.sbo[mid] - s <= p) lo = mid;
+          else hi = mid - 1;
+        }
+        sub = lo;
+      }
+      atomicAdd(&sm.cnt[(sub << P.bs) | (int)(it >> P.total_bits)], 1);
+    }
+    fast = __syncthreads_and(sm.cnt[tid] <= 32);
+  }
+  if (fast) {
+    eg_tile_fast(items, P, sm, status, out, err);
+    return;
+  }
+  sm.cnt[tid] = 0;
+  __syncthreads();
+  if (n <= kTileCap)
     eg_tile<true>(items, P, sm, g1, g2, gnode, status, out, err);
   else
     eg_tile<false>(items, P, sm, g1, g2, gnode, status, out, err);

@@ -14,24 +14,33 @@ namespace phfem {
 
 static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
                                   const phfem_coeffs* c, const phfem_field* f,
-                                  const phfem_field* g, const phfem_field* uD, double t,
+                                  const phfem_field* g, const phfem_field* uD, double t, int flags,
                                   phfem_pipeline_out* out) {
+  // edge generation on the input mesh (sort-based); every refined mesh gets its
+  // topology from the parent's (no sort) unless the generic path is forced
+  phfem_topology topo;
+  phfem_status st = phfem_build_topology(ctx, &cur, &topo);
+  if (st != PHFEM_OK) {
+    phfem_mesh_release(ctx, &cur);
+    return st;
+  }
   for (int l = 0; l < levels; ++l) {
-    phfem_topology topo;
-    phfem_status st = phfem_build_topology(ctx, &cur, &topo);
-    if (st != PHFEM_OK) {
-      phfem_mesh_release(ctx, &cur);
-      return st;
-    }
     phfem_mesh next;
     st = phfem_red_refine(ctx, &cur, &topo, &next);
+    phfem_topology fine_topo;
+    if (st == PHFEM_OK) {
+      st = (flags & PHFEM_PIPE_GENERIC_EG) ? phfem_build_topology(ctx, &next, &fine_topo)
+                                           : phfem_refine_topology(ctx, &cur, &topo, &next, &fine_topo);
+      if (st != PHFEM_OK) phfem_mesh_release(ctx, &next);
+    }
     phfem_topology_release(ctx, &topo);
     phfem_mesh_release(ctx, &cur);
     if (st != PHFEM_OK) return st;
     cur = next;
+    topo = fine_topo;
   }
   out->mesh = cur;
-  PHFEM_TRY(phfem_build_topology(ctx, &out->mesh, &out->topo));
+  out->topo = topo;
   PHFEM_TRY(phfem_classify_edges(ctx, &out->topo, &out->mesh, &out->cls));
   const int64_t nE = out->mesh.nE;
   PHFEM_TRY(dalloc(ctx, &out->B, 9 * nE));
@@ -83,11 +92,18 @@ PHFEM_API phfem_status phfem_pipeline(phfem_ctx* ctx, const phfem_mesh* mesh_in,
                                       const phfem_coeffs* c, const phfem_field* f,
                                       const phfem_field* g, const phfem_field* uD, double t,
                                       phfem_pipeline_out* out) {
+  return phfem_pipeline_ex(ctx, mesh_in, levels, c, f, g, uD, t, 0, out);
+}
+
+PHFEM_API phfem_status phfem_pipeline_ex(phfem_ctx* ctx, const phfem_mesh* mesh_in, int levels,
+                                         const phfem_coeffs* c, const phfem_field* f,
+                                         const phfem_field* g, const phfem_field* uD, double t,
+                                         int flags, phfem_pipeline_out* out) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !mesh_in || !c || !f || !g || !uD || levels < 0) return PHFEM_ERR_INVALID_ARGUMENT;
   phfem_mesh cur = *mesh_in;
   cur.owned = 0;  // the caller's mesh is never freed here
-  phfem_status st = pipeline_impl(ctx, cur, levels, c, f, g, uD, t, out);
+  phfem_status st = pipeline_impl(ctx, cur, levels, c, f, g, uD, t, flags, out);
   if (st != PHFEM_OK) {
     const std::string msg = ctx->message;
     phfem_pipeline_release(ctx, out);
@@ -121,7 +137,7 @@ PHFEM_API phfem_status phfem_pipeline_from_host(phfem_ctx* ctx, const double* co
   if (nE) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.elements, elements, 12 * (size_t)nE, cudaMemcpyHostToDevice, ctx->stream));
   if (nD) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.dirichlet, dirichlet, 8 * (size_t)nD, cudaMemcpyHostToDevice, ctx->stream));
   if (nN) PHFEM_CUDA(ctx, cudaMemcpyAsync(m.neumann, neumann, 8 * (size_t)nN, cudaMemcpyHostToDevice, ctx->stream));
-  phfem_status st = pipeline_impl(ctx, m, levels, c, f, g, uD, t, out);
+  phfem_status st = pipeline_impl(ctx, m, levels, c, f, g, uD, t, 0, out);
   if (st != PHFEM_OK) {
     const std::string msg = ctx->message;
     phfem_pipeline_release(ctx, out);

@@ -69,6 +69,22 @@ def lshape_6tri() -> HostMesh:
     return HostMesh(coords, elems, dirichlet, neumann)
 
 
+def fan(k: int, center_last: bool = True) -> HostMesh:
+    """A disc fan: one centre node of valence k (tests the high-valence
+    fallbacks of the edge-generation tile kernel).  Ring edges are Dirichlet."""
+    ang = 2.0 * math.pi * np.arange(k) / k
+    ring = np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    if center_last:
+        coords = np.vstack([ring, [[0.0, 0.0]]])
+        c, r = k, np.arange(k)
+    else:
+        coords = np.vstack([[[0.0, 0.0]], ring])
+        c, r = 0, np.arange(1, k + 1)
+    elems = np.stack([np.full(k, c), r, np.roll(r, -1)], axis=1)
+    dirichlet = np.stack([r, np.roll(r, -1)], axis=1)
+    return HostMesh(coords, elems, dirichlet, np.zeros((0, 2)))
+
+
 # ---- config-4 stress transformation --------------------------------------------
 def stress_transform(hm: HostMesh, level: int, seeds=(1, 2, 3, 4)) -> HostMesh:
     """Jitter interior nodes by U[-0.2h, 0.2h] (h = 2^-level, the leg length),

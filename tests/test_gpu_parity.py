@@ -112,6 +112,70 @@ def test_small_meshes_all_outputs(ctx, mesh_fn):
         hm = O.red_refine(hm)
 
 
+@pytest.mark.parametrize("k,last", [(40, True), (40, False), (700, True), (3000, True), (3000, False)])
+def test_high_valence_fans(ctx, k, last):
+    """Nodes with > 32 occurrences / tiles beyond SMEM take the fallback paths."""
+    hm = G.fan(k, last)
+    args = G.config_fields(2)
+    compare_all(gpu_all(ctx, hm, *args), oracle_all(hm, *args))
+
+
+def test_permuted_node_ids(ctx):
+    """Random node relabelling + element permutation of a refined L-shape."""
+    hm = O.refine_levels(G.lshape_6tri(), 4)
+    perm = np.argsort(G.splitmix64(11, hm.nC), kind="stable")
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(hm.nC)
+    coords = hm.coords[perm]
+    m = capi.HostMesh(coords, inv[hm.elements], inv[hm.dirichlet], inv[hm.neumann])
+    m = capi.HostMesh(m.coords, m.elements[np.argsort(G.splitmix64(12, m.nE), kind="stable")],
+                      m.dirichlet, m.neumann)
+    args = G.config_fields(2)
+    compare_all(gpu_all(ctx, m, *args), oracle_all(m, *args))
+
+
+@pytest.mark.parametrize("name", ["crisscross", "square", "lshape", "stress", "fan", "permuted"])
+def test_refine_topology_equals_sorted_build(ctx, name):
+    """the sort-free topology of the refined mesh is bit-identical
+    to the reference's sort-based build_topology(red_refine(M)) (oracle) and to
+    the device's generic build_topology."""
+    if name == "crisscross":
+        hm = O.refine_levels(G.crisscross_square(), 2)
+    elif name == "square":
+        hm = O.refine_levels(G.square_2tri(), 5)
+    elif name == "lshape":
+        hm = O.refine_levels(G.lshape_6tri(), 4)
+    elif name == "stress":
+        hm = O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 5), 5))
+    elif name == "fan":
+        hm = G.fan(50, True)
+    else:
+        base = O.refine_levels(G.lshape_6tri(), 3)
+        perm = np.argsort(G.splitmix64(21, base.nC), kind="stable")
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(base.nC)
+        hm = capi.HostMesh(base.coords[perm], inv[base.elements][np.argsort(G.splitmix64(22, base.nE))],
+                           inv[base.dirichlet], inv[base.neumann])
+    dm = capi.DeviceMesh.upload(ctx, hm)
+    topo = capi.build_topology(ctx, dm)
+    fine = capi.red_refine(ctx, dm, topo)
+    fast = capi.refine_topology(ctx, dm, topo, fine).download()
+    generic = capi.build_topology(ctx, fine).download()
+    _, ot = O.build_topology(O.red_refine(hm))
+    check_topology(fast, ot.arrays())
+    check_topology(generic, ot.arrays())
+
+
+def test_pipeline_generic_and_fused_agree(ctx):
+    hm = G.lshape_6tri()
+    args = G.config_fields(2)
+    a = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), 4, *args).download()
+    b = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), 4, *args, flags=capi.PIPE_GENERIC_EG).download()
+    check_topology(a["topo"], b["topo"])
+    for k in ["B", "C_row_ptr", "C_col_idx", "C_values", "load", "bd"]:
+        assert np.array_equal(a[k], b[k]), k
+
+
 def test_error_paths_match_reference(ctx):
     tri = G.unit_right_triangle()
     bad = capi.HostMesh(np.vstack([tri.coords, [[1, 1]]]), np.vstack([tri.elements, [[0, 1, 3]]]),
