@@ -73,13 +73,15 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, index: int, period_ms: int = 200):
+        self.index, self.rows, self.proc, self.period = index, [], None, period_ms
 
     def __enter__(self):
+        if self.period <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -254,7 +256,7 @@ def run_ours(args):
     ctx.sync()
     launches0 = ctx.launches
     ctx.profile(True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_ms) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             capi.pipeline(ctx, dm, 1, *fields, flags=flags).release()
@@ -406,6 +408,7 @@ def main():
     ap.add_argument("--ref-level", type=int, default=9)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--generic-eg", action="store_true",
                     help="sort-based edge generation on the refined mesh too (no SURVEY f1 shortcut)")
     args = ap.parse_args()

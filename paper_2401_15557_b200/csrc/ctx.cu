@@ -189,12 +189,19 @@ PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** ou
     }
     ctx->own_stream = true;
   }
-  if (cudaDeviceGetDefaultMemPool(&ctx->pool, device) != cudaSuccess) {
+  // A private stream-ordered pool: freed blocks stay cached across pipeline
+  // runs (release threshold = max), and nothing else in the process (torch,
+  // other libraries) can trim or reconfigure it.
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  if (cudaMemPoolCreate(&ctx->pool, &props) != cudaSuccess) {
     delete ctx;
     cudaGetLastError();
     return PHFEM_ERR_CUDA;
   }
-  uint64_t threshold = UINT64_MAX;  // keep freed blocks cached across pipeline runs
+  uint64_t threshold = UINT64_MAX;
   cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
   if (cudaMalloc((void**)&ctx->derr, sizeof(phfem_dev_errors)) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->herr, sizeof(phfem_dev_errors)) != cudaSuccess) {
@@ -218,6 +225,8 @@ PHFEM_API void phfem_ctx_destroy(phfem_ctx* ctx) {
   cudaFree(ctx->derr);
   cudaFreeHost(ctx->herr);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  cudaStreamSynchronize(nullptr);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 

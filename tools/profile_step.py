@@ -37,8 +37,11 @@ if phases:
         t0 = time.perf_counter()
         topo = tick("build_topology L12", lambda: capi.build_topology(ctx, dm))
         fine = tick("red_refine", lambda: capi.red_refine(ctx, dm, topo))
+        if "--fused" in sys.argv:
+            topo2 = tick("refine_topology L13", lambda: capi.refine_topology(ctx, dm, topo, fine))
+        else:
+            topo2 = tick("build_topology L13", lambda: capi.build_topology(ctx, fine))
         tick("release L12 topo", topo.release)
-        topo2 = tick("build_topology L13", lambda: capi.build_topology(ctx, fine))
         cls = tick("classify_edges", lambda: capi.classify_edges(ctx, topo2, fine))
         nE = fine.m.nE
         bufs = [ctx.alloc(72 * nE) for _ in range(4)]
