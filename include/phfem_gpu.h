@@ -144,6 +144,18 @@ phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* parent,
                                    const phfem_topology* parent_topo, const phfem_mesh* fine,
                                    phfem_topology* out);
 
+/* One refinement level fused: given red_refine's output `fine` of (parent,
+ * parent_topo) and the parent's classification, produce the fine mesh's
+ * topology, classification and coupling matrix C (CSR) in one streaming
+ * pass over the parent edges (fine Neumann edges are the halves of the
+ * parent's).  Bit-identical to build_topology + classify_edges +
+ * assemble_constraint on the fine mesh.                                     */
+typedef struct phfem_csr phfem_csr;
+phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* parent,
+                                const phfem_topology* parent_topo,
+                                const phfem_classification* parent_cls, const phfem_mesh* fine,
+                                phfem_topology* topo, phfem_classification* cls, phfem_csr* C);
+
 /* ---- orientation normalisation (config 4; not in the reference) ----------
  * Swaps v1<->v2 of every element with negative signed area, in place.       */
 phfem_status phfem_orient_ccw(phfem_ctx* ctx, phfem_mesh* mesh);

@@ -142,7 +142,7 @@ EXPORTED = [
     "phfem_cn_rhs", "phfem_cn_plan_destroy", "phfem_pipeline", "phfem_pipeline_release",
     "phfem_pipeline_from_host", "phfem_pipeline_download", "phfem_pipeline_download_bytes",
     "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_ctx_profile", "phfem_ctx_profile_read",
-    "phfem_refine_topology", "phfem_pipeline_ex",
+    "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -206,6 +206,9 @@ def load_library(path: str = LIB_PATH):
         "phfem_ctx_profile": (C.c_int, [vp, C.c_int]),
         "phfem_refine_topology": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_mesh),
                                             P(phfem_topology)]),
+        "phfem_refine_level": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                         P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                         P(phfem_csr)]),
         "phfem_pipeline_ex": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(phfem_coeffs), P(phfem_field),
                                         P(phfem_field), P(phfem_field), dbl, C.c_int, P(phfem_pipeline_out)]),
         "phfem_ctx_profile_read": (C.c_int, [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_int64)]),
@@ -453,6 +456,21 @@ def refine_topology(ctx: Context, parent: DeviceMesh, ptopo: Topology, fine: Dev
     ctx.check(ctx.lib.phfem_refine_topology(ctx.ptr, C.byref(parent.m), C.byref(ptopo.t), C.byref(fine.m),
                                             C.byref(t)))
     return Topology(ctx, t)
+
+
+def refine_level(ctx: Context, parent: DeviceMesh, ptopo: Topology, pcls: Classification,
+                 fine: DeviceMesh):
+    """Fused refined level: (topology, classification, C CSR host arrays) of
+    `fine` = red_refine(parent) from the parent's topology/classification."""
+    t, c, m = phfem_topology(), phfem_classification(), phfem_csr()
+    ctx.check(ctx.lib.phfem_refine_level(ctx.ptr, C.byref(parent.m), C.byref(ptopo.t), C.byref(pcls.c),
+                                         C.byref(fine.m), C.byref(t), C.byref(c), C.byref(m)))
+    try:
+        csr = (ctx.to_host(m.row_ptr, (m.rows + 1,), np.int32), ctx.to_host(m.col_idx, (m.nnz,), np.int32),
+               ctx.to_host(m.values, (m.nnz,), np.float64))
+    finally:
+        ctx.lib.phfem_csr_release(ctx.ptr, C.byref(m))
+    return Topology(ctx, t), Classification(ctx, c), csr
 
 
 def orient_ccw(ctx: Context, mesh: DeviceMesh):

@@ -131,10 +131,12 @@ PHFEM_API void phfem_classification_release(phfem_ctx* ctx, phfem_classification
   c->L = 0;
 }
 
-PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology* topo,
-                                            const phfem_mesh* mesh, phfem_classification* out) {
-  memset(out, 0, sizeof(*out));
-  if (!ctx || !topo || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
+namespace phfem {
+// Boundary pairs -> ids, the Neumann bitmap and the per-block prefixes; with
+// with_retained also retained_pos / retained_edges (else the caller wrote them
+// and allocated out->retained_pos / retained_edges already).
+phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const phfem_mesh* mesh,
+                            phfem_classification* out, bool with_retained) {
   const int E = topo->E, nD = mesh->nD, nN = mesh->nN;
   out->nD = nD;
   out->nN = nN;
@@ -143,8 +145,10 @@ PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology
   const int nwords = (E + 31) / 32;
   PHFEM_TRY(dalloc(ctx, &out->dirichlet_edge_ids, nD));
   PHFEM_TRY(dalloc(ctx, &out->neumann_edge_ids, nN));
-  PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
-  PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
+  if (with_retained) {
+    PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
+    PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
+  }
   PHFEM_TRY(dalloc(ctx, &out->neumann_bits, nwords));
   PHFEM_TRY(dalloc(ctx, &out->block_prefix, 2 * ((int64_t)nblk + 1)));
   PHFEM_CUDA(ctx, cudaMemsetAsync(out->neumann_bits, 0, sizeof(uint32_t) * std::max(nwords, 1),
@@ -162,7 +166,7 @@ PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology
       out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, pre_bnd, pre_neu));
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
-  if (nblk > 0) {
+  if (nblk > 0 && with_retained) {
     PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
                                                          out->retained_pos, out->retained_edges));
   }
@@ -188,4 +192,12 @@ PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology
   out->L = E - (int32_t)(ctx->herr->counters[8] & 0xffffffffu);
   out->flags = ctx->herr->counters[5] ? PHFEM_CLS_DUP_NEUMANN : 0;
   return PHFEM_OK;
+}
+}  // namespace phfem
+
+PHFEM_API phfem_status phfem_classify_edges(phfem_ctx* ctx, const phfem_topology* topo,
+                                            const phfem_mesh* mesh, phfem_classification* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !topo || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
+  return classify_lists(ctx, topo, mesh, out, true);
 }

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/phfem_gpu.h"
@@ -47,6 +48,12 @@ struct phfem_ctx {
   };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> free_events;
+  // size-bucketed cache of freed blocks (stream-ordered reuse on ctx->stream):
+  // repeated pipeline calls get the same blocks back instead of growing /
+  // remapping the pool (which costs tens of ms per call at L13 sizes)
+  std::unordered_map<size_t, std::vector<void*>> cache;
+  std::unordered_map<void*, size_t> block_size;
+  size_t cached_bytes = 0;
 };
 
 namespace phfem {
@@ -81,22 +88,19 @@ phfem_status cuda_fail(phfem_ctx* ctx, cudaError_t e, const char* where);
     if (_s != PHFEM_OK) return _s;      \
   } while (0)
 
+phfem_status raw_alloc(phfem_ctx* ctx, void** p, size_t bytes);
+void raw_free(phfem_ctx* ctx, void* p);
+void cache_flush(phfem_ctx* ctx);
+
 template <typename T>
 phfem_status dalloc(phfem_ctx* ctx, T** p, size_t count) {
-  *p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMallocFromPoolAsync((void**)p, count * sizeof(T), ctx->pool, ctx->stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return set_error(ctx, PHFEM_ERR_OOM, "phfem: device allocation of %zu bytes failed (%s)",
-                     count * sizeof(T), cudaGetErrorString(e));
-  }
-  return PHFEM_OK;
+  return raw_alloc(ctx, (void**)p, count * sizeof(T));
 }
 
 template <typename T>
 void dfree(phfem_ctx* ctx, T*& p) {
-  if (p && ctx) cudaFreeAsync((void*)p, ctx->stream);
+  if (p && ctx) raw_free(ctx, (void*)p);
   p = nullptr;
 }
 

@@ -40,6 +40,59 @@ phfem_status errors_fetch(phfem_ctx* ctx) {
   return PHFEM_OK;
 }
 
+static size_t round_size(size_t bytes) {
+  const size_t g = bytes >= (size_t(1) << 20) ? (size_t(2) << 20) : 512;
+  return (bytes + g - 1) / g * g;
+}
+
+phfem_status raw_alloc(phfem_ctx* ctx, void** p, size_t bytes) {
+  *p = nullptr;
+  const size_t sz = round_size(bytes);
+  auto it = ctx->cache.find(sz);
+  if (it != ctx->cache.end() && !it->second.empty()) {
+    *p = it->second.back();
+    it->second.pop_back();
+    ctx->cached_bytes -= sz;
+    return PHFEM_OK;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(p, sz, ctx->pool, ctx->stream);
+  if (e != cudaSuccess) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    cache_flush(ctx);
+    e = cudaMallocFromPoolAsync(p, sz, ctx->pool, ctx->stream);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return set_error(ctx, PHFEM_ERR_OOM, "phfem: device allocation of %zu bytes failed (%s)", bytes,
+                     cudaGetErrorString(e));
+  }
+  ctx->block_size[*p] = sz;
+  return PHFEM_OK;
+}
+
+void raw_free(phfem_ctx* ctx, void* p) {
+  auto it = ctx->block_size.find(p);
+  if (it == ctx->block_size.end()) {  // not ours: hand back to the stream-ordered pool
+    cudaFreeAsync(p, ctx->stream);
+    return;
+  }
+  ctx->cache[it->second].push_back(p);
+  ctx->cached_bytes += it->second;
+}
+
+void cache_flush(phfem_ctx* ctx) {
+  for (auto& kv : ctx->cache)
+    for (void* q : kv.second) {
+      cudaFreeAsync(q, ctx->stream);
+      ctx->block_size.erase(q);
+    }
+  ctx->cache.clear();
+  ctx->cached_bytes = 0;
+  cudaStreamSynchronize(ctx->stream);
+  cudaMemPoolTrimTo(ctx->pool, 0);
+}
+
 static cudaEvent_t take_event(phfem_ctx* ctx) {
   if (!ctx->free_events.empty()) {
     cudaEvent_t e = ctx->free_events.back();
@@ -217,6 +270,7 @@ PHFEM_API void phfem_ctx_destroy(phfem_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  cache_flush(ctx);
   for (auto& r : ctx->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -248,7 +302,7 @@ PHFEM_API phfem_status phfem_alloc(phfem_ctx* ctx, size_t bytes, void** out) {
 }
 
 PHFEM_API void phfem_free(phfem_ctx* ctx, void* ptr) {
-  if (ptr && ctx) cudaFreeAsync(ptr, ctx->stream);
+  if (ptr && ctx) raw_free(ctx, ptr);
 }
 
 PHFEM_API phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {

@@ -6,11 +6,32 @@
 // build_topology + classify_edges + assemble_operators + the elliptic load
 // b + LN (elliptic.cpp:53-56) and the Dirichlet vector.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace phfem {
+
+// PHFEM_TRACE=1: synchronising per-phase wall-clock trace on stderr (debug only)
+struct Trace {
+  bool on;
+  phfem_ctx* ctx;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit Trace(phfem_ctx* c) : on(getenv("PHFEM_TRACE") != nullptr), ctx(c) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[phfem] %-28s %9.3f ms (t=%9.3f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 
 static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
                                   const phfem_coeffs* c, const phfem_field* f,
@@ -18,30 +39,52 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
                                   phfem_pipeline_out* out) {
   // edge generation on the input mesh (sort-based); every refined mesh gets its
   // topology from the parent's (no sort) unless the generic path is forced
+  Trace tr(ctx);
+  tr("start");
   phfem_topology topo;
   phfem_status st = phfem_build_topology(ctx, &cur, &topo);
+  tr("build_topology");
   if (st != PHFEM_OK) {
     phfem_mesh_release(ctx, &cur);
     return st;
   }
+  bool have_cls_C = false;
   for (int l = 0; l < levels; ++l) {
+    const bool last_fused = (l == levels - 1) && !(flags & PHFEM_PIPE_GENERIC_EG);
+    phfem_classification pcls;
+    memset(&pcls, 0, sizeof pcls);
+    if (last_fused) st = phfem_classify_edges(ctx, &topo, &cur, &pcls);
+    tr("classify parent");
     phfem_mesh next;
-    st = phfem_red_refine(ctx, &cur, &topo, &next);
+    memset(&next, 0, sizeof next);
+    if (st == PHFEM_OK) st = phfem_red_refine(ctx, &cur, &topo, &next);
+    tr("red_refine");
     phfem_topology fine_topo;
+    memset(&fine_topo, 0, sizeof fine_topo);
     if (st == PHFEM_OK) {
-      st = (flags & PHFEM_PIPE_GENERIC_EG) ? phfem_build_topology(ctx, &next, &fine_topo)
-                                           : phfem_refine_topology(ctx, &cur, &topo, &next, &fine_topo);
+      if (flags & PHFEM_PIPE_GENERIC_EG) {
+        st = phfem_build_topology(ctx, &next, &fine_topo);
+      } else if (last_fused) {
+        st = phfem_refine_level(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C);
+        have_cls_C = st == PHFEM_OK;
+      } else {
+        st = phfem_refine_topology(ctx, &cur, &topo, &next, &fine_topo);
+      }
       if (st != PHFEM_OK) phfem_mesh_release(ctx, &next);
     }
+    tr("fine topology");
+    phfem_classification_release(ctx, &pcls);
     phfem_topology_release(ctx, &topo);
     phfem_mesh_release(ctx, &cur);
+    tr("release parent");
     if (st != PHFEM_OK) return st;
     cur = next;
     topo = fine_topo;
   }
   out->mesh = cur;
   out->topo = topo;
-  PHFEM_TRY(phfem_classify_edges(ctx, &out->topo, &out->mesh, &out->cls));
+  if (!have_cls_C) PHFEM_TRY(phfem_classify_edges(ctx, &out->topo, &out->mesh, &out->cls));
+  tr("classify");
   const int64_t nE = out->mesh.nE;
   PHFEM_TRY(dalloc(ctx, &out->B, 9 * nE));
   PHFEM_TRY(dalloc(ctx, &out->D, 9 * nE));
@@ -49,6 +92,7 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   PHFEM_TRY(dalloc(ctx, &out->M0, 9 * nE));
   PHFEM_TRY(dalloc(ctx, &out->load, 3 * nE));
   PHFEM_TRY(dalloc(ctx, &out->bd, std::max(out->cls.L, 1)));
+  tr("alloc outputs");
   PHFEM_TRY(errors_reset(ctx));
   VolArgs a = make_vol_args(&out->mesh);
   a.coeffs = *c;
@@ -61,9 +105,11 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   a.load = out->load;
   a.vec = 1;  // pool allocations are 256-byte aligned
   PHFEM_TRY(launch_volume(ctx, a, true, true));
+  tr("volume+load");
   PHFEM_TRY(neumann_into(ctx, &out->mesh, &out->topo, &out->cls, g, t, out->load, 1, false));
-  PHFEM_TRY(constraint_csr_into(ctx, &out->mesh, &out->topo, &out->cls, &out->C));
+  if (!have_cls_C) PHFEM_TRY(constraint_csr_into(ctx, &out->mesh, &out->topo, &out->cls, &out->C));
   PHFEM_TRY(dirichlet_into(ctx, &out->mesh, &out->topo, &out->cls, uD, t, out->bd));
+  tr("neumann+C+dirichlet");
   PHFEM_TRY(errors_fetch(ctx));
   PHFEM_TRY(volume_errors(ctx, true, true));
   PHFEM_TRY(neu_flux_error(ctx, &out->mesh, &out->topo, &out->cls));

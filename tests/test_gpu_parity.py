@@ -166,6 +166,35 @@ def test_refine_topology_equals_sorted_build(ctx, name):
     check_topology(generic, ot.arrays())
 
 
+@pytest.mark.parametrize("name", ["crisscross", "square", "lshape", "stress", "alldirichlet"])
+def test_refine_level_fused(ctx, name):
+    """Fused refined level (topology + classification + C) == oracle on the fine mesh."""
+    if name == "crisscross":
+        hm = O.refine_levels(G.crisscross_square(), 2)
+    elif name == "square":
+        hm = O.refine_levels(G.square_2tri(), 5)
+    elif name == "lshape":
+        hm = O.refine_levels(G.lshape_6tri(), 4)
+    elif name == "stress":
+        hm = O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 5), 5))
+    else:
+        base = O.refine_levels(G.crisscross_square(), 2)
+        hm = capi.HostMesh(base.coords, base.elements, np.vstack([base.dirichlet, base.neumann]),
+                           np.zeros((0, 2)))
+    dm = capi.DeviceMesh.upload(ctx, hm)
+    topo = capi.build_topology(ctx, dm)
+    cls = capi.classify_edges(ctx, topo, dm)
+    fine = capi.red_refine(ctx, dm, topo)
+    ft, fc, fC = capi.refine_level(ctx, dm, topo, cls, fine)
+    fh = O.red_refine(hm)
+    om, ot = O.build_topology(fh)
+    oc = O.classify_edges(om, ot)
+    check_topology(ft.download(), ot.arrays())
+    check_cls(fc.download(), oc.arrays())
+    for a, b in zip(fC, O.assemble_constraint(om, ot, oc)["csr"]):
+        assert np.array_equal(a, b)
+
+
 def test_pipeline_generic_and_fused_agree(ctx):
     hm = G.lshape_6tri()
     args = G.config_fields(2)
