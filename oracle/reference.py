@@ -1,0 +1,265 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes front end of oracle/_ref/libphfem_ref.so,
+the reference's own hot-path sources (/root/reference/proj/src) compiled
+unmodified against shim/Eigen (see oracle/ref.mk).  Used to pin the C oracle,
+to generate tests/golden and as bench.py's "reference" CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(_HERE, "_ref", "libphfem_ref.so")
+
+import sys as _sys
+_sys.path.insert(0, os.path.dirname(_HERE))
+from paper_2401_15557_b200.capi import HostMesh, phfem_coeffs, phfem_field  # noqa: E402
+
+_lib = None
+
+
+class ReferenceError_(RuntimeError):
+    def __init__(self, status, message):
+        super().__init__(message)
+        self.status = status
+
+
+def available() -> bool:
+    if os.path.exists(LIB):
+        return True
+    if os.path.isdir("/root/reference/proj/src"):
+        try:
+            subprocess.run(["make", "-s", "-j8", "-C", _HERE, "-f", "ref.mk"], check=True)
+        except Exception:
+            return False
+        return os.path.exists(LIB)
+    return False
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError("oracle/_ref/libphfem_ref.so not built (needs /root/reference)")
+        L = C.CDLL(LIB)
+        vp, cp, sz, P = C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER
+        L.ref_mesh_new.restype = vp
+        L.ref_mesh_new.argtypes = [vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int]
+        L.ref_mesh_free.argtypes = [vp]
+        L.ref_mesh_sizes.argtypes = [vp, vp]
+        L.ref_mesh_copy.argtypes = [vp, vp, vp, vp, vp]
+        L.ref_build_topology.argtypes = [vp, P(vp), cp, sz]
+        L.ref_topology_free.argtypes = [vp]
+        L.ref_topology_sizes.argtypes = [vp, vp]
+        L.ref_topology_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.ref_node_pair_to_edge.argtypes = [vp, C.c_int, C.c_int]
+        L.ref_directed_pair_to_element.argtypes = [vp, C.c_int, C.c_int]
+        L.ref_classify_edges.argtypes = [vp, vp, P(vp), cp, sz]
+        L.ref_classification_free.argtypes = [vp]
+        L.ref_classification_sizes.argtypes = [vp, vp]
+        L.ref_classification_copy.argtypes = [vp, vp, vp, vp, vp]
+        L.ref_red_refine.argtypes = [vp, vp, P(vp), cp, sz]
+        L.ref_edge_lengths.argtypes = [vp, vp, vp]
+        L.ref_assemble_volume.argtypes = [vp, P(phfem_coeffs), vp, vp, vp, vp, cp, sz]
+        L.ref_assemble_constraint.argtypes = [vp, vp, vp, P(C.c_int), P(C.c_int), P(C.c_longlong), vp, vp, vp,
+                                              cp, sz]
+        L.ref_assemble_load.argtypes = [vp, P(phfem_field), C.c_double, vp, cp, sz]
+        L.ref_assemble_neumann.argtypes = [vp, vp, vp, P(phfem_field), C.c_double, vp, cp, sz]
+        L.ref_assemble_dirichlet.argtypes = [vp, vp, vp, P(phfem_field), C.c_double, vp, cp, sz]
+        L.ref_cn_rhs.argtypes = [vp, vp, vp, P(phfem_coeffs), P(phfem_field), P(phfem_field), P(phfem_field),
+                                 C.c_double, C.c_int, vp, vp, cp, sz]
+        L.ref_pipeline_seconds.restype = C.c_double
+        L.ref_pipeline_seconds.argtypes = [vp, C.c_int, P(phfem_coeffs), P(phfem_field), P(phfem_field),
+                                           P(phfem_field), P(C.c_longlong)]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(st, err):
+    if st != 0:
+        msg = err.value.decode()
+        if st == 7:
+            raise ValueError(msg)
+        if st == 8:
+            raise IndexError(msg)
+        raise ReferenceError_(st, msg)
+
+
+class RMesh:
+    def __init__(self, hm: HostMesh = None, handle=None):
+        self.h = handle if handle is not None else lib().ref_mesh_new(
+            _p(hm.coords), hm.nC, _p(hm.elements), hm.nE, _p(hm.dirichlet), hm.dirichlet.shape[0],
+            _p(hm.neumann), hm.neumann.shape[0])
+
+    def host(self) -> HostMesh:
+        sz = np.zeros(4, np.int32)
+        lib().ref_mesh_sizes(self.h, _p(sz))
+        c = np.zeros((sz[0], 2))
+        e = np.zeros((sz[1], 3), np.int32)
+        d = np.zeros((sz[2], 2), np.int32)
+        n = np.zeros((sz[3], 2), np.int32)
+        lib().ref_mesh_copy(self.h, _p(c), _p(e), _p(d), _p(n))
+        return HostMesh(c, e, d, n)
+
+    def __del__(self):
+        try:
+            lib().ref_mesh_free(self.h)
+        except Exception:
+            pass
+
+
+class RTopology:
+    def __init__(self, rm: RMesh):
+        self.rm = rm
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        _check(lib().ref_build_topology(rm.h, C.byref(h), err, 512), err)
+        self.h = h.value
+
+    def arrays(self) -> dict:
+        sz = np.zeros(3, np.int32)
+        lib().ref_topology_sizes(self.h, _p(sz))
+        E, ni, nb = (int(x) for x in sz)
+        out = {"edge_nodes": np.zeros((E, 2), np.int32), "edge_elements": np.zeros((E, 2), np.int32),
+               "local_in_tplus": np.zeros(E, np.int32), "local_in_tminus": np.zeros(E, np.int32),
+               "interior_edges": np.zeros(ni, np.int32), "boundary_edges": np.zeros(nb, np.int32)}
+        lib().ref_topology_copy(self.h, *[_p(out[k]) for k in ["edge_nodes", "edge_elements", "local_in_tplus",
+                                                               "local_in_tminus", "interior_edges",
+                                                               "boundary_edges"]])
+        return out
+
+    def node_pair_to_edge(self, k, l):
+        return lib().ref_node_pair_to_edge(self.h, k, l)
+
+    def directed_pair_to_element(self, k, l):
+        return lib().ref_directed_pair_to_element(self.h, k, l)
+
+    def __del__(self):
+        try:
+            lib().ref_topology_free(self.h)
+        except Exception:
+            pass
+
+
+class RClassification:
+    def __init__(self, rt: RTopology, rm: RMesh):
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        _check(lib().ref_classify_edges(rt.h, rm.h, C.byref(h), err, 512), err)
+        self.h = h.value
+
+    @property
+    def L(self):
+        sz = np.zeros(4, np.int32)
+        lib().ref_classification_sizes(self.h, _p(sz))
+        return int(sz[2])
+
+    def arrays(self) -> dict:
+        sz = np.zeros(4, np.int32)
+        lib().ref_classification_sizes(self.h, _p(sz))
+        out = {"dirichlet_edge_ids": np.zeros(sz[0], np.int32), "neumann_edge_ids": np.zeros(sz[1], np.int32),
+               "retained_edges": np.zeros(sz[2], np.int32), "retained_pos": np.zeros(sz[3], np.int32)}
+        lib().ref_classification_copy(self.h, *[_p(out[k]) for k in ["dirichlet_edge_ids", "neumann_edge_ids",
+                                                                     "retained_edges", "retained_pos"]])
+        return out
+
+    def __del__(self):
+        try:
+            lib().ref_classification_free(self.h)
+        except Exception:
+            pass
+
+
+def red_refine(rm: RMesh, rt: RTopology) -> RMesh:
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    _check(lib().ref_red_refine(rm.h, rt.h, C.byref(h), err, 512), err)
+    return RMesh(handle=h.value)
+
+
+def assemble_volume(rm: RMesh, nE: int, coeffs: phfem_coeffs):
+    outs = [np.zeros((nE, 9)) for _ in range(4)]
+    err = C.create_string_buffer(512)
+    _check(lib().ref_assemble_volume(rm.h, C.byref(coeffs), *[_p(o) for o in outs], err, 512), err)
+    return outs
+
+
+def assemble_constraint_csc(rm: RMesh, rt: RTopology, rc: RClassification):
+    rows, cols, nnz = C.c_int(), C.c_int(), C.c_longlong()
+    err = C.create_string_buffer(512)
+    _check(lib().ref_assemble_constraint(rm.h, rt.h, rc.h, C.byref(rows), C.byref(cols), C.byref(nnz),
+                                         None, None, None, err, 512), err)
+    outer = np.zeros(cols.value + 1, np.int32)
+    inner = np.zeros(nnz.value, np.int32)
+    vals = np.zeros(nnz.value)
+    _check(lib().ref_assemble_constraint(rm.h, rt.h, rc.h, C.byref(rows), C.byref(cols), C.byref(nnz),
+                                         _p(outer), _p(inner), _p(vals), err, 512), err)
+    return outer, inner, vals
+
+
+def csc_to_csr(csc, nrows):
+    outer, inner, vals = csc
+    ncols = len(outer) - 1
+    cols = np.repeat(np.arange(ncols, dtype=np.int32), np.diff(outer))
+    order = np.lexsort((cols, inner))  # row-major, columns ascending
+    row_ptr = np.zeros(nrows + 1, np.int32)
+    np.add.at(row_ptr, inner + 1, 1)
+    return np.cumsum(row_ptr).astype(np.int32), cols[order], vals[order]
+
+
+def assemble_load(rm: RMesh, nE: int, f: phfem_field, t=0.0):
+    out = np.zeros(3 * nE)
+    err = C.create_string_buffer(512)
+    _check(lib().ref_assemble_load(rm.h, C.byref(f), t, _p(out), err, 512), err)
+    return out
+
+
+def assemble_neumann(rm, rt, rc, nE, g, t=0.0):
+    out = np.zeros(3 * nE)
+    err = C.create_string_buffer(512)
+    _check(lib().ref_assemble_neumann(rm.h, rt.h, rc.h, C.byref(g), t, _p(out), err, 512), err)
+    return out
+
+
+def assemble_dirichlet(rm, rt, rc, uD, t=0.0):
+    out = np.zeros(max(rc.L, 1))
+    err = C.create_string_buffer(512)
+    _check(lib().ref_assemble_dirichlet(rm.h, rt.h, rc.h, C.byref(uD), t, _p(out), err, 512), err)
+    return out[:rc.L]
+
+
+def cn_rhs(rm, rt, rc, coeffs, f, g, uD, k, n, state):
+    state = np.ascontiguousarray(state, dtype=np.float64)
+    out = np.zeros_like(state)
+    err = C.create_string_buffer(512)
+    _check(lib().ref_cn_rhs(rm.h, rt.h, rc.h, C.byref(coeffs), C.byref(f), C.byref(g), C.byref(uD), k, n,
+                            _p(state), _p(out), err, 512), err)
+    return out
+
+
+def pipeline_seconds(hm: HostMesh, levels: int, coeffs, f, g, uD):
+    rm = RMesh(hm)
+    n = C.c_longlong()
+    s = lib().ref_pipeline_seconds(rm.h, levels, C.byref(coeffs), C.byref(f), C.byref(g), C.byref(uD), C.byref(n))
+    return s, int(n.value)
+
+
+def all_outputs(hm: HostMesh, coeffs, f, g, uD, t=0.0) -> dict:
+    """Everything the reference computes on one mesh (for parity / goldens)."""
+    rm = RMesh(hm)
+    rt = RTopology(rm)
+    rc = RClassification(rt, rm)
+    B, D, M, M0 = assemble_volume(rm, hm.nE, coeffs)
+    csc = assemble_constraint_csc(rm, rt, rc)
+    fine = red_refine(rm, rt).host()
+    return {"topo": rt.arrays(), "cls": rc.arrays(), "B": B, "D": D, "M": M, "M0": M0, "C_csc": csc,
+            "C_csr": csc_to_csr(csc, rc.L), "b": assemble_load(rm, hm.nE, f, t),
+            "ln": assemble_neumann(rm, rt, rc, hm.nE, g, t), "bd": assemble_dirichlet(rm, rt, rc, uD, t),
+            "refined": fine}

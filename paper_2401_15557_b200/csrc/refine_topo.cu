@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kRlEdges) k_rl_emit(RtArgs a, const int32_t* _
   __shared__ int32_t s_rs[kFull ? kRlFine : 1];
   __shared__ int16_t s_ri[kFull ? kRlFine : 1];
   __shared__ double s_len[kFull ? kRlFine : 1];
+  __shared__ int16_t s_owner[kFull ? 4 * kRlFine : 1];
   __shared__ int32_t sm[33];
   __shared__ int32_t s_bpre;
   const int tid = threadIdx.x;
@@ -245,27 +246,28 @@ __global__ void __launch_bounds__(kRlEdges) k_rl_emit(RtArgs a, const int32_t* _
     if (kFull) o.rpos[f] = s_rp[i];
   }
   if (kFull) {
+    // the block's C entries are one contiguous range [K0, K1): map entry -> row
+    // in SMEM, then write entry-parallel (coalesced col / value stores)
     const int R0 = o.base_r[e0], R1 = o.base_r[e_end];
     const int K0 = 4 * R0 - 2 * o.base_br[e0];
     const int K1 = 4 * R1 - 2 * o.base_br[e_end];
-    const int nr = R1 - R0;
-    for (int k = K0 + tid; k < K1; k += kRlEdges) {
-      int lo = 0, hi = nr - 1;  // last retained row starting at or before k
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_rs[mid] <= k) lo = mid;
-        else hi = mid - 1;
-      }
-      const int q = k - s_rs[lo];
-      const int i = s_ri[lo];
+    for (int j = tid; j < R1 - R0; j += kRlEdges) {
+      const int n = s_el[s_ri[j]].y >= 0 ? 4 : 2;
+      const int k0 = s_rs[j] - K0;
+      for (int q = 0; q < n; ++q) s_owner[k0 + q] = (int16_t)j;
+    }
+    __syncthreads();
+    for (int k = tid; k < K1 - K0; k += kRlEdges) {
+      const int j = s_owner[k];
+      const int q = k + K0 - s_rs[j];
+      const int i = s_ri[j];
       const int2 tt = s_el[i];
       const int lt = s_lt[i];
       const int l = q < 2 ? (lt & 0xff) : (lt >> 8);
-      const int qq = q & 1;
-      const int c = qq == 0 ? (l == 0 ? 1 : 0) : (l == 2 ? 1 : 2);  // q-th of {0,1,2} \ {l}
-      const double len = s_len[lo];
-      o.col[k] = 3 * (q < 2 ? tt.x : tt.y) + c;
-      __stcs(o.val + k, q < 2 ? len * 0.5 : -len * 0.5);  // assembly.cpp:160 / :164
+      const int c = (q & 1) == 0 ? (l == 0 ? 1 : 0) : (l == 2 ? 1 : 2);  // q-th of {0,1,2} \ {l}
+      const double len = s_len[j];
+      o.col[K0 + k] = 3 * (q < 2 ? tt.x : tt.y) + c;
+      __stcs(o.val + K0 + k, q < 2 ? len * 0.5 : -len * 0.5);  // assembly.cpp:160 / :164
     }
   }
 }
