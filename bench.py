@@ -146,20 +146,31 @@ def dist_barrier(world):
 
 
 # ---- CPU side -------------------------------------------------------------------
+def cpu_impl():
+    """'reference' = the reference's own sources (oracle/_ref, built from
+    /root/reference against shim/Eigen); 'port' = the C restatement."""
+    from oracle import reference as R
+    return "reference" if os.path.exists(R.LIB) else "port"
+
+
 def cpu_sample_worker(args):
-    level, steps, warmup, q = args
+    level, steps, warmup, kind = args
     from oracle import oracle as O
     from paper_2401_15557_b200 import meshgen as G
-    hm = O.refine_levels(G.square_2tri(), level)
+    hm = O.refine_levels(G.square_2tri(), level)     # input generation, untimed
     fields = G.config_fields(5)
     times = []
     nE = 0
     for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        r = O.pipeline(hm, 1, *fields)
-        dt = time.perf_counter() - t0
-        nE = r["mesh"].nE
-        del r
+        if kind == "reference":
+            from oracle import reference as R
+            dt, nE = R.pipeline_seconds(hm, 1, *fields)
+        else:
+            t0 = time.perf_counter()
+            r = O.pipeline(hm, 1, *fields)
+            dt = time.perf_counter() - t0
+            nE = r["mesh"].nE
+            del r
         if i >= warmup:
             times.append(dt)
     return nE, times
@@ -176,11 +187,15 @@ def cpu_workers_available(per_worker_gb: float) -> int:
     return max(1, min(cores, int(avail_gb * 0.6 / per_worker_gb)))
 
 
-def cpu_baseline_single(level=10):
-    """The oracle port, one core, one bounded sample (L10 -> L11, 8.4 M triangles)."""
-    nE, times = cpu_sample_worker((level, 1, 0, None))
-    return {"value": nE / times[0], "unit": "triangles/s", "cores": 1, "kind": "port",
-            "sample": f"square L{level} -> L{level + 1} pipeline ({nE} triangles), oracle/phfem_oracle.c, "
+def cpu_baseline_single(level=9):
+    """One bounded sample on one core: square L9 -> L10 pipeline (4.2 M triangles)."""
+    kind = cpu_impl()
+    nE, times = cpu_sample_worker((level, 1, 0, kind))
+    what = ("reference sources (oracle/_ref, /root/reference/proj/src via shim/Eigen)" if kind == "reference"
+            else "oracle/phfem_oracle.c (C restatement)")
+    return {"value": nE / times[0], "unit": "triangles/s", "cores": 1, "kind": kind,
+            "sample": f"square L{level} -> L{level + 1} pipeline ({nE} triangles): build_topology, red_refine, "
+                      f"build_topology, classify_edges, B/D/M/M0, C, load+Neumann, Dirichlet; {what}; "
                       f"1 thread, {times[0]:.2f} s"}
 
 
@@ -190,9 +205,10 @@ def run_reference(args):
         return
     import multiprocessing as mp
     level = args.ref_level
+    kind = cpu_impl()
     P = cpu_workers_available(per_worker_gb=1.5)
     with mp.get_context("fork").Pool(P) as pool:
-        res = pool.map(cpu_sample_worker, [(level, args.steps, args.warmup, None)] * P)
+        res = pool.map(cpu_sample_worker, [(level, args.steps, args.warmup, kind)] * P)
     nE = res[0][0]
     per_step = [max(r[1][i] for r in res) for i in range(args.steps)]
     t = statistics.mean(per_step)
@@ -204,10 +220,10 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"config5 pipeline sample: square L{level} -> L{level + 1}, "
                                f"{P} concurrent single-threaded samples", "triangles_per_sample": nE},
-        "cpu_baseline": {"value": value, "unit": "triangles/s", "cores": P, "kind": "port",
-                         "sample": f"{P} x square L{level}->L{level + 1} ({nE} tri each), "
-                                   "oracle/phfem_oracle.c (C restatement of the reference; the reference "
-                                   "itself is single-threaded, so one sample per core)"},
+        "cpu_baseline": {"value": value, "unit": "triangles/s", "cores": P, "kind": kind,
+                         "sample": f"{P} concurrent single-threaded samples (the reference has no threading), "
+                                   f"each square L{level}->L{level + 1} ({nE} tri): build_topology, red_refine, "
+                                   "build_topology, classify_edges, B/D/M/M0, C, load+Neumann, Dirichlet"},
         "e2e": {"value": value, "unit": "triangles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -404,8 +420,8 @@ def main():
     ap.add_argument("--level", type=int, default=13, help="final refinement level (config 5: 13)")
     ap.add_argument("--e2e-level", type=int, default=13)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-level", type=int, default=10)
-    ap.add_argument("--ref-level", type=int, default=9)
+    ap.add_argument("--cpu-level", type=int, default=9)
+    ap.add_argument("--ref-level", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
