@@ -53,17 +53,29 @@ def as_bytes(nC, nE, E, L, nnz):
     return 16 * nC + 324 * nE + 28 * E + 12 * L + 12 * nnz
 
 
-def kernel_bytes(name, s):
-    """Algorithmic bytes of one launch of a kernel (inputs read once, outputs
-    written once) for the final-level sizes s."""
+def kernel_bytes(name, s, p):
+    """Algorithmic bytes of ONE launch of a step kernel (inputs read once,
+    outputs written once).  s = final (L13) sizes, p = parent
+    (L12) sizes.  None for kernels without a model."""
     nC, nE, E, L, nnz = s["nC"], s["nE"], s["E"], s["L"], s["nnz"]
+    pC, pE, pEd = p["nC"], p["nE"], p["E"]
     return {
+        # B, D, M, M0 (4 x 72 B) + load (24 B) written; elements + coords read
         "k_volume": 12 * nE + 16 * nC + 312 * nE,
-        "k_eg_bucket": 24 * nE + 28 * E + 12 * nE + 4 * nC,
-        "k_eg_scatter": 12 * nE + 24 * nE,
-        "k_eg_count": 12 * nE,
-        "k_constraint_csr": 28 * E + 16 * nC + 4 * L + 12 * nnz,
-        "k_cls_retained": E // 8 + 4 * E + 4 * L,
+        # parent build_topology: items in (3 x 8 B / element), edge records out
+        # (edge_nodes, edge_elements, ltp, ltm, list: 28 B), elem_edge 12 B/element
+        "k_eg_tile": 24 * pE + 28 * pEd + 12 * pE,
+        "k_eg_scatter": 12 * pE + 24 * pE,
+        "k_eg_count": 12 * pE,
+        # red_refine without midpoints: elements + elem_edge in, 4 children out
+        "k_refine_elements": 24 * pE + 48 * pE,
+        # fused refined level: parent edge records + elem_edge / opposite-vertex /
+        # coordinate gathers in; fine topology (32 B/edge incl. list slot and
+        # retained_pos), fine elem_edge, node_edge_start + midpoints (20 B per
+        # parent edge), retained list + row_ptr (8 B/row), C entries (12 B) out
+        "k_rl_level_full": (24 * pEd + pEd // 8 + 24 * pE + 16 * pC) +
+                           (32 * E + 12 * nE + 20 * pEd + 8 * L + 12 * nnz),
+        "k_cls_retained": pEd // 8 + 4 * pEd + 4 * pEd,  # parent classification (retained_pos / retained_edges)
     }.get(name)
 
 
@@ -288,17 +300,16 @@ def run_ours(args):
 
     peak, peak_kind = peaks()
     # dominant kernel -> roofline
-    named = {k: v for k, v in prof.items() if kernel_bytes(k, s) is not None}
+    named = {k: v for k, v in prof.items() if kernel_bytes(k, s, s0) is not None}
     dom = max(named, key=lambda k: named[k][0])
     dom_ms, dom_n = named[dom]
-    # final-level launches only: the L12 launch of the same kernel is 4x smaller
-    lvl_bytes = kernel_bytes(dom, s)
-    if dom in ("k_eg_bucket", "k_eg_scatter", "k_eg_count"):
-        small = kernel_bytes(dom, {"nC": s0["nC"], "nE": s0["nE"], "E": s0["E"], "L": 0, "nnz": 0})
-        per_step_bytes = lvl_bytes + small
-    else:
-        per_step_bytes = lvl_bytes * (dom_n // args.steps)
+    per_step_bytes = kernel_bytes(dom, s, s0) * (dom_n // args.steps)
     achieved = per_step_bytes / (dom_ms / args.steps * 1e-3) / 1e9
+    per_kernel = {}
+    for k, (kms, kn) in sorted(named.items(), key=lambda kv: -kv[1][0]):
+        b = kernel_bytes(k, s, s0) * (kn // args.steps)
+        gbs = b / (kms / args.steps * 1e-3) / 1e9
+        per_kernel[k] = {"ms": round(kms / args.steps, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks()[0], 4)}
     step_share = {k: round(v[0] / args.steps / ms_local, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
@@ -321,6 +332,7 @@ def run_ours(args):
         "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(pipeline_gbs, 1),
                               "peak": peak, "frac": round(pipeline_gbs / peak, 4)},
         "kernel_share": step_share,
+        "kernel_roofline": per_kernel,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -209,3 +209,110 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T* total) {
   __syncthreads();
   return res;
 }
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over tiles (single-pass scans of the edge passes).
+// Status word per tile: 2 flag bits (0 = not ready, 1 = aggregate, 2 =
+// inclusive prefix) + two 31-bit payloads.  Tiles are claimed in launch order
+// through an atomic ticket, so every predecessor is running or done.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kPay31 = (1ull << 31) - 1;
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, uint64_t v) {
+  *(volatile unsigned long long*)p = v;
+}
+
+// Decoupled look-back by warp 0 of the CTA owning tile b.  Returns the
+// exclusive (first << 32 | second) prefix of the two payloads.
+// Wide variant: every lane inspects V consecutive predecessors, so one L2
+// round trip covers 32 V tiles — the frontier of inclusive prefixes advances
+// 32 V tiles per round trip instead of 32 (the look-back chain otherwise caps
+// the throughput of kernels with short tiles).
+template <int V>
+__device__ __forceinline__ uint64_t lookback_wide(unsigned long long* status, int b, uint32_t agg_e,
+                                                  uint32_t agg_b) {
+  const unsigned lane = lane_id();
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], (b == 0 ? kFlagPre : kFlagAgg) | ((uint64_t)agg_e << 31) | agg_b);
+  }
+  if (b == 0) return 0;
+  uint64_t ex_e = 0, ex_b = 0;
+  int top = b - 1;
+  while (true) {
+    uint64_t w[V];
+    while (true) {
+      bool ready = true;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int idx = top - (int)lane * V - v;
+        w[v] = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPre;
+        ready = ready && (w[v] >> 62) != 0;
+      }
+      if (__all_sync(0xffffffffu, ready)) break;
+      __nanosleep(32);
+    }
+    int vf = V;  // nearest inclusive prefix among this lane's entries
+#pragma unroll
+    for (int v = V - 1; v >= 0; --v)
+      if ((w[v] >> 62) == 2) vf = v;
+    const unsigned pmask = __ballot_sync(0xffffffffu, vf < V);
+    const int fl = pmask ? __ffs(pmask) - 1 : 32;
+    const int upto = (int)lane < fl ? V - 1 : ((int)lane == fl ? vf : -1);
+    uint64_t ve = 0, vb = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v <= upto) {
+        ve += (w[v] >> 31) & kPay31;
+        vb += w[v] & kPay31;
+      }
+    ex_e += warp_reduce_sum(ve);
+    ex_b += warp_reduce_sum(vb);
+    if (pmask) break;
+    top -= 32 * V;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], kFlagPre | ((ex_e + agg_e) << 31) | (ex_b + agg_b));
+  }
+  return (ex_e << 32) | ex_b;
+}
+
+__device__ __forceinline__ uint64_t eg_lookback(unsigned long long* status, int b, uint32_t agg_e,
+                                                uint32_t agg_b) {
+  const unsigned lane = lane_id();
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], (b == 0 ? kFlagPre : kFlagAgg) | ((uint64_t)agg_e << 31) | agg_b);
+  }
+  if (b == 0) return 0;
+  uint64_t ex_e = 0, ex_b = 0;
+  int top = b - 1;
+  while (true) {
+    const int idx = top - (int)lane;
+    uint64_t w;
+    while (true) {
+      w = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPre;
+      if (!__any_sync(0xffffffffu, (w >> 62) == 0)) break;
+      __nanosleep(32);
+    }
+    const unsigned pmask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+    const bool take = (int)lane <= first_p;
+    const uint64_t ve = take ? ((w >> 31) & kPay31) : 0;
+    const uint64_t vb = take ? (w & kPay31) : 0;
+    ex_e += warp_reduce_sum(ve);
+    ex_b += warp_reduce_sum(vb);
+    if (pmask) break;
+    top -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_volatile_u64(&status[b], kFlagPre | ((ex_e + agg_e) << 31) | (ex_b + agg_b));
+  }
+  return (ex_e << 32) | ex_b;
+}

@@ -120,54 +120,6 @@ struct EgOut {
   int32_t* node_edge_start;
 };
 
-constexpr uint64_t kFlagAgg = 1ull << 62;
-constexpr uint64_t kFlagPre = 2ull << 62;
-constexpr uint64_t kPay31 = (1ull << 31) - 1;
-
-__device__ __forceinline__ uint64_t ld_volatile_u64(const unsigned long long* p) {
-  return *(const volatile unsigned long long*)p;
-}
-__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, uint64_t v) {
-  *(volatile unsigned long long*)p = v;
-}
-
-// Decoupled look-back by warp 0 of the CTA owning bucket b.  Returns the
-// exclusive (edges << 32 | boundary) prefix.
-__device__ __forceinline__ uint64_t eg_lookback(unsigned long long* status, int b, uint32_t agg_e,
-                                                uint32_t agg_b) {
-  const unsigned lane = lane_id();
-  if (lane == 0) {
-    __threadfence();
-    st_volatile_u64(&status[b], (b == 0 ? kFlagPre : kFlagAgg) | ((uint64_t)agg_e << 31) | agg_b);
-  }
-  if (b == 0) return 0;
-  uint64_t ex_e = 0, ex_b = 0;
-  int top = b - 1;
-  while (true) {
-    const int idx = top - (int)lane;
-    uint64_t w;
-    while (true) {
-      w = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPre;
-      if (!__any_sync(0xffffffffu, (w >> 62) == 0)) break;
-      __nanosleep(32);
-    }
-    const unsigned pmask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
-    const int first_p = pmask ? __ffs(pmask) - 1 : 32;
-    const bool take = (int)lane <= first_p;
-    const uint64_t ve = take ? ((w >> 31) & kPay31) : 0;
-    const uint64_t vb = take ? (w & kPay31) : 0;
-    ex_e += warp_reduce_sum(ve);
-    ex_b += warp_reduce_sum(vb);
-    if (pmask) break;
-    top -= 32;
-  }
-  if (lane == 0) {
-    __threadfence();
-    st_volatile_u64(&status[b], kFlagPre | ((ex_e + agg_e) << 31) | (ex_b + agg_b));
-  }
-  return (ex_e << 32) | ex_b;
-}
-
 // One CTA per tile of kTileNodes consecutive max-node ids (= 256 >> bs
 // consecutive buckets).  Item-parallel throughout: counting sort by node,
 // per-segment rank sort (segments are tiny: ~6 occurrences per node), blocked

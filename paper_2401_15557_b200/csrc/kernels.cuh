@@ -86,4 +86,16 @@ phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
                                  const phfem_topology* topo, const phfem_classification* cls,
                                  phfem_csr* out);
 
+// refine.cu / refine_topo.cu internals of the fused pipeline (mid / write_mid:
+// who writes the midpoint nodes of the refined mesh)
+phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                             phfem_mesh* out, bool write_mid);
+phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
+                                  const phfem_topology* ptopo, const phfem_mesh* fine,
+                                  phfem_topology* out, double* mid);
+phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
+                               const phfem_topology* ptopo, const phfem_classification* pcls,
+                               const phfem_mesh* fine, phfem_topology* topo,
+                               phfem_classification* cls, phfem_csr* C, double* mid);
+
 }  // namespace phfem

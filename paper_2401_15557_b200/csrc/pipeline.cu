@@ -57,7 +57,10 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
     tr("classify parent");
     phfem_mesh next;
     memset(&next, 0, sizeof next);
-    if (st == PHFEM_OK) st = phfem_red_refine(ctx, &cur, &topo, &next);
+    // the sort-free paths write the midpoint nodes themselves (coalesced)
+    const bool generic = (flags & PHFEM_PIPE_GENERIC_EG) != 0;
+    if (st == PHFEM_OK) st = red_refine_impl(ctx, &cur, &topo, &next, generic);
+    double* mid = next.coords;  // the level kernels write nodes nc..nc+E-1
     tr("red_refine");
     phfem_topology fine_topo;
     memset(&fine_topo, 0, sizeof fine_topo);
@@ -65,10 +68,10 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
       if (flags & PHFEM_PIPE_GENERIC_EG) {
         st = phfem_build_topology(ctx, &next, &fine_topo);
       } else if (last_fused) {
-        st = phfem_refine_level(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C);
+        st = refine_level_impl(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C, mid);
         have_cls_C = st == PHFEM_OK;
       } else {
-        st = phfem_refine_topology(ctx, &cur, &topo, &next, &fine_topo);
+        st = refine_topology_impl(ctx, &cur, &topo, &next, &fine_topo, mid);
       }
       if (st != PHFEM_OK) phfem_mesh_release(ctx, &next);
     }

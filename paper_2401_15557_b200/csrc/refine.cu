@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(256) k_refine_elements(const double2* __restri
                                                          const int32_t* __restrict__ elements,
                                                          const int32_t* __restrict__ elem_edge,
                                                          int nE, int nC, double2* __restrict__ out_coords,
-                                                         int4* __restrict__ out_elems) {
+                                                         int4* __restrict__ out_elems, int write_mid) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
     const int p0 = __ldg(elements + 3 * m), p1 = __ldg(elements + 3 * m + 1),
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) k_refine_elements(const double2* __restri
     o[1] = make_int4(m2, m1, p1, m0);
     o[2] = make_int4(m2, p2, m1, m0);
     // midpoints 0.5 * (c[a] + c[b]) (refine.cpp:16-19), written once by t_plus
-    if (s0 >= 0 || s1 >= 0 || s2 >= 0) {
+    if (write_mid && (s0 >= 0 || s1 >= 0 || s2 >= 0)) {
       const double2 c0 = __ldg(coords + p0), c1 = __ldg(coords + p1), c2 = __ldg(coords + p2);
       if (s0 >= 0) out_coords[m0] = make_double2(0.5 * (c1.x + c2.x), 0.5 * (c1.y + c2.y));
       if (s1 >= 0) out_coords[m1] = make_double2(0.5 * (c2.x + c0.x), 0.5 * (c2.y + c0.y));
@@ -90,8 +90,11 @@ PHFEM_API void phfem_mesh_release(phfem_ctx* ctx, phfem_mesh* m) {
   m->owned = 0;
 }
 
-PHFEM_API phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh,
-                                        const phfem_topology* topo, phfem_mesh* out) {
+namespace phfem {
+// write_mid = false: the midpoint nodes nc..nc+E-1 are left to the fused
+// refined-level kernel (refine_topo.cu), which writes them coalesced.
+phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                             phfem_mesh* out, bool write_mid) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !mesh || !topo) return PHFEM_ERR_INVALID_ARGUMENT;
   if (topo->nE != mesh->nE || topo->nC != mesh->nC)
@@ -114,7 +117,7 @@ PHFEM_API phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh,
   if (nE > 0) {
     PHFEM_LAUNCH(ctx, "k_refine_elements", k_refine_elements<<<grid_for(nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         (const double2*)mesh->coords, mesh->elements, topo->elem_edge, (int)nE, (int)nC,
-        (double2*)out->coords, (int4*)out->elements));
+        (double2*)out->coords, (int4*)out->elements, write_mid ? 1 : 0));
   }
   const int64_t nb = (int64_t)mesh->nD + mesh->nN;
   if (nb > 0) {
@@ -129,6 +132,12 @@ PHFEM_API phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh,
     }
   }
   return PHFEM_OK;
+}
+}  // namespace phfem
+
+PHFEM_API phfem_status phfem_red_refine(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                        const phfem_topology* topo, phfem_mesh* out) {
+  return red_refine_impl(ctx, mesh, topo, out, true);
 }
 
 PHFEM_API phfem_status phfem_orient_ccw(phfem_ctx* ctx, phfem_mesh* mesh) {

@@ -15,114 +15,57 @@
 // edge_topology.cpp:61-68; tests/test_gpu_parity.py checks it against the
 // oracle's sort-based build_topology.)
 //
-// Two streaming passes over parent edges: count (group sizes) -> scan -> emit.
+// Device algorithm: one main kernel over the parent edges (k_rl_level),
+// one thread per parent edge, 128 edges per tile:
+//   1. coalesced loads of the parent edge record; gathers of elem_edge and the
+//      opposite vertex of t_plus / t_minus (the partner edges of e in each
+//      element sit at the local indices next to ltp / ltm: no search);
+//   2. group size = 2 + #partners < e; one packed block scan gives the
+//      in-tile (fine edges, boundary, Neumann) prefixes; the tile offsets come
+//      from a tiny pre-pass (k_rl_tile_init / k_rl_tile_count: per-tile
+//      totals from the coalesced parent elem_edge, then scans of one int per
+//      tile).  A decoupled look-back was measured slower here: 128-edge
+//      tiles finish faster than the look-back frontier advances;
+//   3. the 4 coordinates every fine-edge length needs (a, b and the two
+//      opposite vertices) are gathered once per parent edge: fine midpoints
+//      are 0.5 (x + y) of parent vertices, so lengths are recomputed from the
+//      parent geometry with the same bits as edge_lengths on the fine mesh
+//      (edge_topology.cpp:179-186) and the midpoint node mu(e) itself is
+//      written coalesced here (refine.cpp:16-19);
+//   4. fine-edge records are staged in SMEM and stored coalesced; with kFull
+//      the retained positions, retained list, CSR rows of C and their
+//      (column, value) entries (assembly.cpp:144-168) are emitted in the
+//      same pass (the fine Neumann edges are the halves of the parent's).
 #include "common.cuh"
 
 namespace phfem {
 
-struct RtArgs {
-  const int32_t* edge_nodes;     // parent
-  const int32_t* edge_elements;  // parent
-  const int32_t* ltp;            // parent
-  const int32_t* ltm;            // parent
-  const int32_t* elem_edge;      // parent
-  const int32_t* boundary;       // parent ascending boundary list
-  int nB;
-  int E;
-  int nc;
-};
+constexpr int kLvT = 128;          // parent edges (= threads) per tile
+constexpr int kLvF = 6 * kLvT;     // fine-edge slots per tile (<= 6 per parent edge)
 
 __device__ __forceinline__ int abs_edge(int s) { return s >= 0 ? s : ~s; }
 
-// partners of e inside parent element m (its other two edges), with the local
-// index of the third edge (the M_k the interior fine edge is opposite to)
-__device__ __forceinline__ void partners_in(const int32_t* __restrict__ elem_edge, int m, int e,
-                                            int pe[2], int pk[2], int ee[3]) {
-  ee[0] = abs_edge(__ldg(elem_edge + 3 * (int64_t)m));
-  ee[1] = abs_edge(__ldg(elem_edge + 3 * (int64_t)m + 1));
-  ee[2] = abs_edge(__ldg(elem_edge + 3 * (int64_t)m + 2));
-  const int i = ee[0] == e ? 0 : (ee[1] == e ? 1 : 2);
-  const int j1 = (i + 1) % 3, j2 = (i + 2) % 3;
-  pe[0] = ee[j1];
-  pk[0] = 3 - i - j1;
-  pe[1] = ee[j2];
-  pk[1] = 3 - i - j2;
-}
-
-// ---------------------------------------------------------------------------
-// Group enumeration: the fine edges whose larger node is mu(e), in canonical
-// order (halves by smaller old node, then interior edges by partner e').
-struct FineEdge {
-  int from, to, tp, lp, tm, lm;
+struct LvArgs {
+  // parent topology
+  const int32_t* edge_nodes;
+  const int32_t* edge_elements;
+  const int32_t* ltp;
+  const int32_t* ltm;
+  const int32_t* elem_edge;
+  // parent mesh
+  const int32_t* elements;
+  const double2* coords;
+  // parent classification (kFull)
+  const uint32_t* neu_bits;
+  int E, nc, Ef, L;
+  // exclusive per-tile prefixes (k_rl_tile_init / k_rl_tile_count + scans):
+  // fine edges, parent boundary edges, parent Neumann edges before the tile
+  const int32_t* tileF;
+  const int32_t* tileB;
+  const int32_t* tileN;
 };
 
-__device__ __forceinline__ int rt_group(const RtArgs& a, int e, int2 el, FineEdge fe[6]) {
-  const int2 ab = reinterpret_cast<const int2*>(a.edge_nodes)[e];
-  const int l = __ldg(a.ltp + e);
-  const int tp = el.x, tm = el.y;
-  const int l2 = tm >= 0 ? __ldg(a.ltm + e) : 0;
-  const int mu = a.nc + e;
-  const int ia = ab.x < ab.y ? 0 : 1;  // the half at the smaller old node comes first
-  fe[ia] = FineEdge{ab.x, mu, 4 * tp + 1 + (l + 1) % 3, 2, tm >= 0 ? 4 * tm + 1 + (l2 + 2) % 3 : -1, 1};
-  fe[1 - ia] = FineEdge{mu, ab.y, 4 * tp + 1 + (l + 2) % 3, 1, tm >= 0 ? 4 * tm + 1 + (l2 + 1) % 3 : -1, 2};
-  int pe[4], pk[4], pm[4], ee[2][3];
-  int np = 0;
-  int q[2], k[2];
-  partners_in(a.elem_edge, tp, e, q, k, ee[0]);
-#pragma unroll
-  for (int t = 0; t < 2; ++t)
-    if (q[t] < e) {
-      pe[np] = q[t];
-      pk[np] = k[t];
-      pm[np] = 0;
-      ++np;
-    }
-  if (tm >= 0) {
-    partners_in(a.elem_edge, tm, e, q, k, ee[1]);
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-      if (q[t] < e) {
-        pe[np] = q[t];
-        pk[np] = k[t];
-        pm[np] = 1;
-        ++np;
-      }
-  }
-  for (int t = 0; t < np; ++t) {
-    int rank = 0;
-    for (int u = 0; u < np; ++u) rank += pe[u] < pe[t];
-    const int m = pm[t] == 0 ? tp : tm;
-    const int kk = pk[t];
-    const int* E3 = ee[pm[t]];
-    fe[2 + rank] = FineEdge{a.nc + E3[(kk + 1) % 3], a.nc + E3[(kk + 2) % 3], 4 * m, kk, 4 * m + 1 + kk, 0};
-  }
-  return 2 + np;
-}
-
-// counts per parent edge: fine edges, retained fine edges, retained boundary fine edges
-__global__ void k_rl_count(RtArgs a, const int32_t* __restrict__ prpos, int32_t* __restrict__ cnt,
-                           int32_t* __restrict__ rcnt, int32_t* __restrict__ brcnt) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int2 el = reinterpret_cast<const int2*>(a.edge_elements)[e];
-    int c = 2;
-    int pe[2], pk[2], ee[3];
-    partners_in(a.elem_edge, el.x, (int)e, pe, pk, ee);
-    c += (pe[0] < e) + (pe[1] < e);
-    if (el.y >= 0) {
-      partners_in(a.elem_edge, el.y, (int)e, pe, pk, ee);
-      c += (pe[0] < e) + (pe[1] < e);
-    }
-    cnt[e] = c;
-    if (rcnt) {
-      const bool neu = prpos[e] < 0;  // halves of a Neumann edge are Neumann
-      rcnt[e] = c - (neu ? 2 : 0);
-      brcnt[e] = (el.y < 0 && !neu) ? 2 : 0;
-    }
-  }
-}
-
-struct RlOut {
+struct LvOut {
   int32_t* edge_nodes;
   int32_t* edge_elements;
   int32_t* ltp;
@@ -131,143 +74,249 @@ struct RlOut {
   int32_t* boundary;
   int32_t* elem_edge;
   int32_t* node_edge_start;
-  // kFull only
-  const double2* fcoords;
-  const int32_t* prpos;
-  const int32_t* base_r;
-  const int32_t* base_br;
+  double2* mid;  // fine coords base (nullable): node nc + e = midpoint of parent edge e
+  // kFull
   int32_t* rpos;
   int32_t* redges;
   int32_t* row_ptr;
   int32_t* col;
   double* val;
-  int L;
 };
 
-constexpr int kRlEdges = 128;              // parent edges per CTA
-constexpr int kRlFine = 6 * kRlEdges;      // max fine edges per CTA
-
-// One CTA per 128 parent edges.  Fine-edge records are staged in SMEM and
-// written back with coalesced stores; in the kFull variant every retained
-// fine edge also gets its retained position and its C row, and the block's C
-// entries (a contiguous range) are produced entry-parallel.
 template <bool kFull>
-__global__ void __launch_bounds__(kRlEdges) k_rl_emit(RtArgs a, const int32_t* __restrict__ base_f,
-                                                       int total, RlOut o) {
-  __shared__ int2 s_en[kRlFine];
-  __shared__ int2 s_el[kRlFine];
-  __shared__ int32_t s_lt[kRlFine];
-  __shared__ int32_t s_rp[kFull ? kRlFine : 1];
-  __shared__ int32_t s_rs[kFull ? kRlFine : 1];
-  __shared__ int16_t s_ri[kFull ? kRlFine : 1];
-  __shared__ double s_len[kFull ? kRlFine : 1];
-  __shared__ int16_t s_owner[kFull ? 4 * kRlFine : 1];
-  __shared__ int32_t sm[33];
-  __shared__ int32_t s_bpre;
-  const int tid = threadIdx.x;
-  const int64_t e0 = (int64_t)blockIdx.x * kRlEdges;
-  const int64_t e = e0 + tid;
-  const bool valid = e < a.E;
-  const int64_t e_end = e0 + kRlEdges < a.E ? e0 + kRlEdges : a.E;
-  int2 el = make_int2(0, 0);
-  if (valid) el = reinterpret_cast<const int2*>(a.edge_elements)[e];
-  const int isB = (valid && el.y < 0) ? 1 : 0;
-  if (tid == 0) {
-    int lo = 0, hi = a.nB;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(a.boundary + mid) < e0) lo = mid + 1;
-      else hi = mid;
-    }
-    s_bpre = lo;
-  }
-  int tot;
-  const int bex = block_exclusive_scan(isB, sm, &tot);
-  const int F0 = base_f[e0];
-  const int nf = base_f[e_end] - F0;
-  if (valid) {
-    const int bpre = s_bpre + bex;  // parent boundary edges before e
-    const int base = base_f[e];
-    o.node_edge_start[a.nc + e] = base;
-    if (e == a.E - 1) o.node_edge_start[a.nc + a.E] = total;
-    FineEdge fe[6];
-    const int cnt = rt_group(a, (int)e, el, fe);
-    int rbase = 0, brbase = 0;
-    bool neu = false;
-    if (kFull) {
-      rbase = o.base_r[e];
-      brbase = o.base_br[e];
-      neu = o.prpos[e] < 0;
-    }
-    const int R0 = kFull ? o.base_r[e0] : 0;
-    int rk = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const int f = base + j;
-      const int i = f - F0;
-      const FineEdge& x = fe[j];
-      s_en[i] = make_int2(x.from, x.to);
-      s_el[i] = make_int2(x.tp, x.tm);
-      s_lt[i] = x.lp | ((x.tm >= 0 ? x.lm : -1) << 8);
-      o.elem_edge[3 * (int64_t)x.tp + x.lp] = f;
-      if (x.tm >= 0) o.elem_edge[3 * (int64_t)x.tm + x.lm] = ~f;
-      const bool fbnd = j < 2 && isB;
-      if (fbnd) o.boundary[2 * bpre + j] = f;
-      else o.interior[f - 2 * bpre - (j >= 2 && isB ? 2 : 0)] = f;
-      if (kFull) {
-        const bool ret = j >= 2 || !neu;
-        int rp = -1;
-        if (ret) {
-          rp = rbase + rk;
-          const int bret = brbase + ((fbnd && j == 1) ? 1 : 0) + ((j >= 2 && isB && !neu) ? 2 : 0);
-          const int rs = 4 * rp - 2 * bret;
-          const double2 pa = __ldg(o.fcoords + x.from), pb = __ldg(o.fcoords + x.to);
-          const double dx = pb.x - pa.x, dy = pb.y - pa.y;
-          const int jr = rp - R0;
-          s_rs[jr] = rs;
-          s_ri[jr] = (int16_t)i;
-          s_len[jr] = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
-          o.row_ptr[rp] = rs;
-          o.redges[rp] = f;
-          if (rp == o.L - 1) o.row_ptr[o.L] = rs + (x.tm >= 0 ? 4 : 2);
-          ++rk;
-        }
-        s_rp[i] = rp;
+struct LvSmem {
+  int2 en[kLvF];
+  int2 el[kLvF];
+  int32_t meta[kLvF];  // lp | (lm + 1) << 2
+  int32_t slot[kLvF];  // interior list index, or ~boundary list index
+  int32_t rp[kFull ? kLvF : 1];
+  int32_t rs[kFull ? kLvF : 1];
+  double len[kFull ? kLvF : 1];
+  int32_t scan[33];
+};
+
+__device__ __forceinline__ double seg_len(double2 p, double2 q) {
+  const double dx = q.x - p.x, dy = q.y - p.y;
+  return sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183 (Eigen norm)
+}
+
+__device__ __forceinline__ double2 midpt(double2 p, double2 q) {
+  return make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));  // refine.cpp:18
+}
+
+// Per-tile totals before the scans.  Group e holds 2 halves plus, for every
+// parent element with sorted edge ids x < y < z, one interior fine edge in
+// group y and two in group z — so the fine-edge count of a tile is
+// 2 (edges in tile) + element contributions, accumulated element-parallel
+// (coalesced elem_edge reads, warp-aggregated atomics).
+__global__ void k_rl_tile_init(int E, int ntiles, const int32_t* __restrict__ boundary, int nB,
+                               const uint32_t* __restrict__ neu_bits, int32_t* __restrict__ tileF,
+                               int32_t* __restrict__ tileB, int32_t* __restrict__ tileN) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+    const int64_t e0 = (int64_t)t * kLvT;
+    const int64_t e1 = e0 + kLvT < E ? e0 + kLvT : E;
+    tileF[t] = 2 * (int)(e1 - e0);
+    auto lower = [&](int64_t key) {  // ascending boundary list
+      int l = 0, r = nB;
+      while (l < r) {
+        const int mid = (l + r) >> 1;
+        if (__ldg(boundary + mid) < key) l = mid + 1;
+        else r = mid;
       }
+      return l;
+    };
+    tileB[t] = lower(e1) - lower(e0);
+    if (neu_bits) {
+      int c = 0;
+      for (int64_t w = e0 >> 5; w < (e1 + 31) >> 5; ++w) c += __popc(__ldg(neu_bits + w));
+      tileN[t] = c;
     }
   }
+}
+
+__device__ __forceinline__ void warp_add(int32_t* ctr, int key, int v) {
+  const unsigned g = __match_any_sync(__activemask(), key);
+  if ((int)lane_id() == __ffs(g) - 1) atomicAdd(ctr + key, v * __popc(g));
+}
+
+__global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE,
+                                int32_t* __restrict__ tileF) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
+    const int x = abs_edge(__ldg(elem_edge + 3 * m)), y = abs_edge(__ldg(elem_edge + 3 * m + 1)),
+              z = abs_edge(__ldg(elem_edge + 3 * m + 2));
+    const int hi = max(x, max(y, z));
+    const int md = max(min(x, y), min(max(x, y), z));
+    warp_add(tileF, md / kLvT, 1);
+    warp_add(tileF, hi / kLvT, 2);
+  }
+}
+
+template <bool kFull>
+__global__ void __launch_bounds__(kLvT) k_rl_level(LvArgs a, LvOut o) {
+  __shared__ LvSmem<kFull> s;
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int64_t e0 = (int64_t)tile * kLvT;
+  const int e = (int)(e0 + tid);
+  const bool valid = e < a.E;
+
+  // 1. the parent edge record (coalesced) and the element gathers
+  int2 ab = make_int2(0, 0), el = make_int2(0, -1);
+  int l = 0, l2 = 0;
+  bool neu = false;
+  if (valid) {
+    ab = reinterpret_cast<const int2*>(a.edge_nodes)[e];
+    el = reinterpret_cast<const int2*>(a.edge_elements)[e];
+    l = __ldg(a.ltp + e);
+    if (kFull) neu = (__ldg(a.neu_bits + (e >> 5)) >> (e & 31)) & 1u;
+  }
+  const bool has_m = valid && el.y >= 0;
+  if (has_m) l2 = __ldg(a.ltm + e);
+  const int tp = el.x, tm = el.y;
+  int P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
+  int vop = 0, vom = 0;
+  if (valid) {
+    P[0] = __ldg(a.elem_edge + 3 * (int64_t)tp);
+    P[1] = __ldg(a.elem_edge + 3 * (int64_t)tp + 1);
+    P[2] = __ldg(a.elem_edge + 3 * (int64_t)tp + 2);
+    vop = __ldg(a.elements + 3 * (int64_t)tp + l);
+  }
+  if (has_m) {
+    Q[0] = __ldg(a.elem_edge + 3 * (int64_t)tm);
+    Q[1] = __ldg(a.elem_edge + 3 * (int64_t)tm + 1);
+    Q[2] = __ldg(a.elem_edge + 3 * (int64_t)tm + 2);
+    vom = __ldg(a.elements + 3 * (int64_t)tm + l2);
+  }
+  double2 ca = make_double2(0.0, 0.0), cb = ca, cop = ca, com = ca;
+  if (valid) {
+    ca = __ldg(a.coords + ab.x);
+    cb = __ldg(a.coords + ab.y);
+    cop = __ldg(a.coords + vop);
+  }
+  if (has_m) com = __ldg(a.coords + vom);
+
+  // 2. group size, tile scan, look-back
+  const int j1 = l == 2 ? 0 : l + 1, j2 = l == 0 ? 2 : l - 1;      // partners in t_plus
+  const int k1 = l2 == 2 ? 0 : l2 + 1, k2 = l2 == 0 ? 2 : l2 - 1;  // partners in t_minus
+  const int q0 = abs_edge(P[j1]), q1 = abs_edge(P[j2]);
+  const int r0 = abs_edge(Q[k1]), r1 = abs_edge(Q[k2]);
+  const bool v0 = valid && q0 < e, v1 = valid && q1 < e;
+  const bool v2 = has_m && r0 < e, v3 = has_m && r1 < e;
+  const bool isB = valid && !has_m;
+  const int cnt = valid ? 2 + v0 + v1 + v2 + v3 : 0;
+  const int packed = cnt | (int)isB << 11 | (int)neu << 20;
+  int tot;
+  const int ex = block_exclusive_scan(packed, s.scan, &tot);
+  const int i0 = ex & 0x7ff;            // first slot of group e in the tile
+  const int exB = (ex >> 11) & 0x1ff;   // parent boundary edges before e in the tile
+  const int exN = ex >> 20;             // parent Neumann edges before e in the tile
+
+  // 3. the group's fine edges into SMEM, with TILE-LOCAL offsets only: the
+  //    global ones are added at store time, so the look-back below overlaps
+  //    nothing but its own latency
+  const int mu = a.nc + e;
+  const double2 me = midpt(ca, cb);
+  if (valid) {
+    if (o.mid) o.mid[mu] = me;
+    auto emit = [&](int j, int from, int to, int tpf, int lp, int tmf, int lm, double len) {
+      const int i = i0 + j;
+      s.en[i] = make_int2(from, to);
+      s.el[i] = make_int2(tpf, tmf);
+      s.meta[i] = lp | (tmf >= 0 ? lm + 1 : 0) << 2;  // local_in_tminus = -1 on the boundary
+      // list slot: boundary list 2 B_e + j, else interior list f - 2 B_e - (2 if isB)
+      s.slot[i] = (j < 2 && isB) ? ~(2 * exB + j) : i - 2 * exB - (isB ? 2 : 0);
+      if (kFull) {
+        int rp = -1;
+        if (j >= 2 || !neu) {
+          rp = i0 - 2 * exN + (neu ? j - 2 : j);
+          const int bret = 2 * (exB - exN) + ((isB && !neu) ? (j == 1 ? 1 : (j >= 2 ? 2 : 0)) : 0);
+          s.rs[i] = 4 * rp - 2 * bret;
+          s.len[i] = len;
+        }
+        s.rp[i] = rp;
+      }
+    };
+    // halves: a -> mu and mu -> b; the one at the smaller old node first
+    const int ia = ab.x < ab.y ? 0 : 1;
+    emit(ia, ab.x, mu, 4 * tp + 1 + j1, 2, has_m ? 4 * tm + 1 + k2 : -1, 1, kFull ? seg_len(ca, me) : 0.0);
+    emit(1 - ia, mu, ab.y, 4 * tp + 1 + j2, 1, has_m ? 4 * tm + 1 + k1 : -1, 2,
+         kFull ? seg_len(me, cb) : 0.0);
+    // interior edges mu(e') - mu(e), e' < e, ascending e'.  Candidate
+    // (partner, element, third local index kk): the edge opposite M_kk of the
+    // element's central child runs M_{kk+1} -> M_{kk+2}.
+    const int rk0 = (v1 && q1 < q0) + (v2 && r0 < q0) + (v3 && r1 < q0);
+    const int rk1 = (v0 && q0 < q1) + (v2 && r0 < q1) + (v3 && r1 < q1);
+    const int rk2 = (v0 && q0 < r0) + (v1 && q1 < r0) + (v3 && r1 < r0);
+    const int rk3 = (v0 && q0 < r1) + (v1 && q1 < r1) + (v2 && r0 < r1);
+    // t_plus vertices: V(l) = cop, V(l+1) = ca, V(l+2) = cb; midpoint of the
+    // edge at local j = 0.5 (V(j+1) + V(j+2)).  t_minus: W(l2) = com,
+    // W(l2+1) = cb, W(l2+2) = ca.
+    if (v0)  // partner at j1, kk = j2: mu(e) -> mu(q0)
+      emit(2 + rk0, mu, a.nc + q0, 4 * tp, j2, 4 * tp + 1 + j2, 0,
+           kFull ? seg_len(me, midpt(cb, cop)) : 0.0);
+    if (v1)  // partner at j2, kk = j1: mu(q1) -> mu(e)
+      emit(2 + rk1, a.nc + q1, mu, 4 * tp, j1, 4 * tp + 1 + j1, 0,
+           kFull ? seg_len(midpt(cop, ca), me) : 0.0);
+    if (v2)  // t_minus partner at k1, kk = k2: mu(e) -> mu(r0)
+      emit(2 + rk2, mu, a.nc + r0, 4 * tm, k2, 4 * tm + 1 + k2, 0,
+           kFull ? seg_len(me, midpt(ca, com)) : 0.0);
+    if (v3)  // t_minus partner at k2, kk = k1: mu(r1) -> mu(e)
+      emit(2 + rk3, a.nc + r1, mu, 4 * tm, k1, 4 * tm + 1 + k1, 0,
+           kFull ? seg_len(midpt(com, cb), me) : 0.0);
+  }
+
+  // 4. global offsets of the tile (precomputed, no look-back)
+  const int F0 = __ldg(a.tileF + tile), B0 = __ldg(a.tileB + tile);
+  const int N0 = kFull ? __ldg(a.tileN + tile) : 0;
   __syncthreads();
-  for (int i = tid; i < nf; i += kRlEdges) {
-    const int f = F0 + i;
-    reinterpret_cast<int2*>(o.edge_nodes)[f] = s_en[i];
-    reinterpret_cast<int2*>(o.edge_elements)[f] = s_el[i];
-    const int lt = s_lt[i];
-    o.ltp[f] = lt & 0xff;
-    o.ltm[f] = lt >> 8;
-    if (kFull) o.rpos[f] = s_rp[i];
+  if (valid) {
+    o.node_edge_start[mu] = F0 + i0;
+    if (e == a.E - 1) o.node_edge_start[mu + 1] = a.Ef;
   }
-  if (kFull) {
-    // the block's C entries are one contiguous range [K0, K1): map entry -> row
-    // in SMEM, then write entry-parallel (coalesced col / value stores)
-    const int R0 = o.base_r[e0], R1 = o.base_r[e_end];
-    const int K0 = 4 * R0 - 2 * o.base_br[e0];
-    const int K1 = 4 * R1 - 2 * o.base_br[e_end];
-    for (int j = tid; j < R1 - R0; j += kRlEdges) {
-      const int n = s_el[s_ri[j]].y >= 0 ? 4 : 2;
-      const int k0 = s_rs[j] - K0;
-      for (int q = 0; q < n; ++q) s_owner[k0 + q] = (int16_t)j;
-    }
-    __syncthreads();
-    for (int k = tid; k < K1 - K0; k += kRlEdges) {
-      const int j = s_owner[k];
-      const int q = k + K0 - s_rs[j];
-      const int i = s_ri[j];
-      const int2 tt = s_el[i];
-      const int lt = s_lt[i];
-      const int l = q < 2 ? (lt & 0xff) : (lt >> 8);
-      const int c = (q & 1) == 0 ? (l == 0 ? 1 : 0) : (l == 2 ? 1 : 2);  // q-th of {0,1,2} \ {l}
-      const double len = s_len[j];
-      o.col[K0 + k] = 3 * (q < 2 ? tt.x : tt.y) + c;
-      __stcs(o.val + K0 + k, q < 2 ? len * 0.5 : -len * 0.5);  // assembly.cpp:160 / :164
+
+  // 5. coalesced stores of the tile's fine edges [F0, F0 + nf)
+  const int nf = tot & 0x7ff;
+  const int off_int = F0 - 2 * B0, off_bnd = 2 * B0;
+  const int off_rp = F0 - 2 * N0, off_rs = 4 * (F0 - N0 - B0);
+  for (int i = tid; i < nf; i += kLvT) {
+    const int f = F0 + i;
+    const int2 en = s.en[i], el2 = s.el[i];
+    const int meta = s.meta[i];
+    const int lp = meta & 3, lm = (meta >> 2) - 1;
+    reinterpret_cast<int2*>(o.edge_nodes)[f] = en;
+    reinterpret_cast<int2*>(o.edge_elements)[f] = el2;
+    o.ltp[f] = lp;
+    o.ltm[f] = lm;
+    const int sl = s.slot[i];
+    if (sl < 0) o.boundary[off_bnd + ~sl] = f;
+    else o.interior[off_int + sl] = f;
+    o.elem_edge[3 * (int64_t)el2.x + lp] = f;
+    if (lm >= 0) o.elem_edge[3 * (int64_t)el2.y + lm] = ~f;
+    if (kFull) {
+      const int rl = s.rp[i];
+      o.rpos[f] = rl < 0 ? -1 : off_rp + rl;
+      if (rl >= 0) {
+        const int rp = off_rp + rl;
+        const int rs = off_rs + s.rs[i];
+        const double len = s.len[i];
+        o.redges[rp] = f;
+        o.row_ptr[rp] = rs;
+        // columns {0,1,2} \ {local}, ascending: T+ DOFs, then T- DOFs
+        const int c0 = lp == 0 ? 1 : 0, c1 = lp == 2 ? 1 : 2;
+        const double vp = len * 0.5;  // assembly.cpp:160
+        *reinterpret_cast<int2*>(o.col + rs) = make_int2(3 * el2.x + c0, 3 * el2.x + c1);
+        __stcs(reinterpret_cast<double2*>(o.val + rs), make_double2(vp, vp));
+        int n = 2;
+        if (lm >= 0) {
+          const int d0 = lm == 0 ? 1 : 0, d1 = lm == 2 ? 1 : 2;
+          const double vm = -len * 0.5;  // assembly.cpp:164
+          *reinterpret_cast<int2*>(o.col + rs + 2) = make_int2(3 * el2.y + d0, 3 * el2.y + d1);
+          __stcs(reinterpret_cast<double2*>(o.val + rs + 2), make_double2(vm, vm));
+          n = 4;
+        }
+        if (rp == a.L - 1) o.row_ptr[a.L] = rs + n;
+      }
     }
   }
 }
@@ -276,9 +325,76 @@ __global__ void __launch_bounds__(kRlEdges) k_rl_emit(RtArgs a, const int32_t* _
 
 using namespace phfem;
 
-PHFEM_API phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* parent,
-                                             const phfem_topology* ptopo, const phfem_mesh* fine,
-                                             phfem_topology* out) {
+namespace phfem {
+
+// Shared host body of phfem_refine_topology / phfem_refine_level.  `mid`
+// (nullable) receives the midpoint coordinates of the fine mesh (nodes
+// nc..nc+E-1) — the fused pipeline lets red_refine skip them.
+static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
+                                     const phfem_topology* ptopo,
+                                     const phfem_classification* pcls, int64_t Ef, int64_t L,
+                                     phfem_topology* topo, phfem_classification* cls, phfem_csr* C,
+                                     double* mid) {
+  const int64_t E = ptopo->E;
+  if (E == 0) return PHFEM_OK;
+  const int64_t ntiles = (E + kLvT - 1) / kLvT;
+  int32_t* tiles = nullptr;
+  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1)));
+  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 3 * (ntiles + 1), ctx->stream));
+  const uint32_t* nbits = pcls ? pcls->neumann_bits : nullptr;
+  PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      (int)E, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN));
+  PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count<<<grid_for(parent->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+      ptopo->elem_edge, parent->nE, tileF));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, nullptr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
+  if (pcls) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, nullptr));
+  LvArgs a;
+  memset(&a, 0, sizeof a);
+  a.edge_nodes = ptopo->edge_nodes;
+  a.edge_elements = ptopo->edge_elements;
+  a.ltp = ptopo->local_in_tplus;
+  a.ltm = ptopo->local_in_tminus;
+  a.elem_edge = ptopo->elem_edge;
+  a.elements = parent->elements;
+  a.coords = (const double2*)parent->coords;
+  a.E = (int)E;
+  a.nc = parent->nC;
+  a.Ef = (int)Ef;
+  a.L = (int)L;
+  a.tileF = tileF;
+  a.tileB = tileB;
+  a.tileN = tileN;
+  LvOut o;
+  memset(&o, 0, sizeof o);
+  o.edge_nodes = topo->edge_nodes;
+  o.edge_elements = topo->edge_elements;
+  o.ltp = topo->local_in_tplus;
+  o.ltm = topo->local_in_tminus;
+  o.interior = topo->interior_edges;
+  o.boundary = topo->boundary_edges;
+  o.elem_edge = topo->elem_edge;
+  o.node_edge_start = topo->node_edge_start;
+  o.mid = (double2*)mid;
+  if (pcls) {
+    a.neu_bits = pcls->neumann_bits;
+    o.rpos = cls->retained_pos;
+    o.redges = cls->retained_edges;
+    o.row_ptr = C->row_ptr;
+    o.col = C->col_idx;
+    o.val = C->values;
+    PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<(unsigned)ntiles, kLvT, 0, ctx->stream>>>(a, o));
+  } else {
+    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)ntiles, kLvT, 0, ctx->stream>>>(a, o));
+  }
+  dfree(ctx, tiles);
+  return PHFEM_OK;
+}
+
+phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
+                                  const phfem_topology* ptopo, const phfem_mesh* fine,
+                                  phfem_topology* out, double* mid) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !parent || !ptopo || !fine) return PHFEM_ERR_INVALID_ARGUMENT;
   if (ptopo->nE != parent->nE || ptopo->nC != parent->nC || fine->nE != 4 * parent->nE ||
@@ -286,12 +402,11 @@ PHFEM_API phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* p
     return set_error(ctx, PHFEM_ERR_MISMATCH, "refine_topology: meshes do not match the topology");
   const int64_t E = ptopo->E, nc = parent->nC;
   // exact count: two halves per parent edge + three interior edges per parent element
-  const int64_t Ef_cap = 2 * E + 3 * (int64_t)parent->nE;
-  if (Ef_cap >= (int64_t(1) << 31))
+  const int64_t Ef = 2 * E + 3 * (int64_t)parent->nE;
+  if (Ef >= (int64_t(1) << 31))
     return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "refine_topology: mesh too large for int ids");
   out->nC = fine->nC;
   out->nE = fine->nE;
-  const int64_t Ef = Ef_cap;  // exact: every half (2 per parent edge) + 3 interior per parent element
   const int64_t nBf = 2 * (int64_t)ptopo->n_boundary;
   PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * Ef));
   PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * Ef));
@@ -302,45 +417,20 @@ PHFEM_API phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* p
   PHFEM_TRY(dalloc(ctx, &out->elem_edge, 3 * (int64_t)fine->nE));
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, (int64_t)fine->nC + 1));
   PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * (nc + 1), ctx->stream));
-  if (E == 0) return PHFEM_OK;
-  RtArgs a{ptopo->edge_nodes, ptopo->edge_elements, ptopo->local_in_tplus, ptopo->local_in_tminus,
-           ptopo->elem_edge, ptopo->boundary_edges, ptopo->n_boundary, (int)E, (int)nc};
-  int32_t* base = nullptr;
-  PHFEM_TRY(dalloc(ctx, &base, E + 1));
-  PHFEM_LAUNCH(ctx, "k_rl_count", k_rl_count<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-      a, nullptr, base, nullptr, nullptr));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(base + E, 0, sizeof(int32_t), ctx->stream));
-  PHFEM_TRY(scan_exclusive_i32(ctx, base, base, E + 1, nullptr));
-  RlOut o;
-  memset(&o, 0, sizeof o);
-  o.edge_nodes = out->edge_nodes;
-  o.edge_elements = out->edge_elements;
-  o.ltp = out->local_in_tplus;
-  o.ltm = out->local_in_tminus;
-  o.interior = out->interior_edges;
-  o.boundary = out->boundary_edges;
-  o.elem_edge = out->elem_edge;
-  o.node_edge_start = out->node_edge_start;
-  PHFEM_LAUNCH(ctx, "k_rl_emit", k_rl_emit<false><<<(unsigned)((E + kRlEdges - 1) / kRlEdges), kRlEdges, 0,
-                                                    ctx->stream>>>(a, base, (int)Ef, o));
-  dfree(ctx, base);
   out->E = (int32_t)Ef;
   out->n_boundary = (int32_t)nBf;
   out->n_interior = (int32_t)(Ef - nBf);
-  return PHFEM_OK;
+  return refine_level_run(ctx, parent, ptopo, nullptr, Ef, 0, out, nullptr, nullptr, mid);
 }
 
-namespace phfem {
 // defined in classify.cu
 phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const phfem_mesh* mesh,
                             phfem_classification* out, bool with_retained);
-}  // namespace phfem
 
-PHFEM_API phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* parent,
-                                          const phfem_topology* ptopo,
-                                          const phfem_classification* pcls,
-                                          const phfem_mesh* fine, phfem_topology* topo,
-                                          phfem_classification* cls, phfem_csr* C) {
+phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
+                               const phfem_topology* ptopo, const phfem_classification* pcls,
+                               const phfem_mesh* fine, phfem_topology* topo,
+                               phfem_classification* cls, phfem_csr* C, double* mid) {
   memset(topo, 0, sizeof(*topo));
   memset(cls, 0, sizeof(*cls));
   memset(C, 0, sizeof(*C));
@@ -380,51 +470,26 @@ PHFEM_API phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* pare
   PHFEM_TRY(dalloc(ctx, &C->values, C->nnz));
   PHFEM_CUDA(ctx, cudaMemsetAsync(topo->node_edge_start, 0, sizeof(int32_t) * (nc + 1), ctx->stream));
   if (L == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
-  if (E > 0) {
-    RtArgs a{ptopo->edge_nodes, ptopo->edge_elements, ptopo->local_in_tplus, ptopo->local_in_tminus,
-             ptopo->elem_edge, ptopo->boundary_edges, ptopo->n_boundary, (int)E, (int)nc};
-    int32_t *bf = nullptr, *br = nullptr, *bb = nullptr;
-    PHFEM_TRY(dalloc(ctx, &bf, E + 1));
-    PHFEM_TRY(dalloc(ctx, &br, E + 1));
-    PHFEM_TRY(dalloc(ctx, &bb, E + 1));
-    PHFEM_LAUNCH(ctx, "k_rl_count", k_rl_count<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        a, pcls->retained_pos, bf, br, bb));
-    PHFEM_CUDA(ctx, cudaMemsetAsync(bf + E, 0, sizeof(int32_t), ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemsetAsync(br + E, 0, sizeof(int32_t), ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemsetAsync(bb + E, 0, sizeof(int32_t), ctx->stream));
-    PHFEM_TRY(scan_exclusive_i32(ctx, bf, bf, E + 1, nullptr));
-    PHFEM_TRY(scan_exclusive_i32(ctx, br, br, E + 1, nullptr));
-    PHFEM_TRY(scan_exclusive_i32(ctx, bb, bb, E + 1, nullptr));
-    RlOut o;
-    memset(&o, 0, sizeof o);
-    o.edge_nodes = topo->edge_nodes;
-    o.edge_elements = topo->edge_elements;
-    o.ltp = topo->local_in_tplus;
-    o.ltm = topo->local_in_tminus;
-    o.interior = topo->interior_edges;
-    o.boundary = topo->boundary_edges;
-    o.elem_edge = topo->elem_edge;
-    o.node_edge_start = topo->node_edge_start;
-    o.fcoords = (const double2*)fine->coords;
-    o.prpos = pcls->retained_pos;
-    o.base_r = br;
-    o.base_br = bb;
-    o.rpos = cls->retained_pos;
-    o.redges = cls->retained_edges;
-    o.row_ptr = C->row_ptr;
-    o.col = C->col_idx;
-    o.val = C->values;
-    o.L = (int)L;
-    PHFEM_LAUNCH(ctx, "k_rl_emit_full", k_rl_emit<true><<<(unsigned)((E + kRlEdges - 1) / kRlEdges), kRlEdges, 0,
-                                                         ctx->stream>>>(a, bf, (int)Ef, o));
-    dfree(ctx, bf);
-    dfree(ctx, br);
-    dfree(ctx, bb);
-  }
+  PHFEM_TRY(refine_level_run(ctx, parent, ptopo, pcls, Ef, L, topo, cls, C, mid));
   // boundary lists -> ids, Neumann bitmap, block prefixes (retained arrays already written)
-  phfem_status st = classify_lists(ctx, topo, fine, cls, false);
-  if (st != PHFEM_OK) return st;
+  PHFEM_TRY(classify_lists(ctx, topo, fine, cls, false));
   if (cls->L != L)
     return set_error(ctx, PHFEM_ERR_MISMATCH, "refine_level: classification does not match the parent's");
   return PHFEM_OK;
+}
+
+}  // namespace phfem
+
+PHFEM_API phfem_status phfem_refine_topology(phfem_ctx* ctx, const phfem_mesh* parent,
+                                             const phfem_topology* ptopo, const phfem_mesh* fine,
+                                             phfem_topology* out) {
+  return refine_topology_impl(ctx, parent, ptopo, fine, out, nullptr);
+}
+
+PHFEM_API phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* parent,
+                                          const phfem_topology* ptopo,
+                                          const phfem_classification* pcls,
+                                          const phfem_mesh* fine, phfem_topology* topo,
+                                          phfem_classification* cls, phfem_csr* C) {
+  return refine_level_impl(ctx, parent, ptopo, pcls, fine, topo, cls, C, nullptr);
 }
