@@ -284,6 +284,14 @@ phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipeline_out* o
 /* bytes phfem_pipeline_download moves for a given `out` and selection */
 int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* out, const phfem_pipeline_host* dst);
 
+/* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
+ * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
+ * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =
+ * max ulp distance of the fast sin from CUDA's sin, out[2] = divisions by 3.0
+ * that differ.  Test infrastructure; no reference counterpart.             */
+phfem_status phfem_selftest_fastmath(phfem_ctx* ctx, int64_t n, uint64_t seed,
+                                     unsigned long long* out);
+
 /* ---- host <-> device helpers for bindings without a CUDA runtime --------- */
 phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
 phfem_status phfem_memcpy_d2h(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);

@@ -20,7 +20,9 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libphfem_b200.so")
+# PHFEM_LIB: an alternative in-tree build of the same library (kernel-variant
+# experiments, tools/variants.sh); the default is the one build() makes
+LIB_PATH = os.environ.get("PHFEM_LIB") or os.path.join(_HERE, "libphfem_b200.so")
 
 # ---- status codes (phfem_status) -------------------------------------------
 OK = 0
@@ -142,7 +144,7 @@ EXPORTED = [
     "phfem_cn_rhs", "phfem_cn_plan_destroy", "phfem_pipeline", "phfem_pipeline_release",
     "phfem_pipeline_from_host", "phfem_pipeline_download", "phfem_pipeline_download_bytes",
     "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_ctx_profile", "phfem_ctx_profile_read",
-    "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level",
+    "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level", "phfem_selftest_fastmath",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -212,6 +214,7 @@ def load_library(path: str = LIB_PATH):
         "phfem_pipeline_ex": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(phfem_coeffs), P(phfem_field),
                                         P(phfem_field), P(phfem_field), dbl, C.c_int, P(phfem_pipeline_out)]),
         "phfem_ctx_profile_read": (C.c_int, [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_int64)]),
+        "phfem_selftest_fastmath": (C.c_int, [vp, i64, C.c_uint64, P(C.c_ulonglong)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -9,6 +9,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "elem.cuh"
 #include "kernels.cuh"
 
 namespace phfem {
@@ -22,6 +23,10 @@ namespace phfem {
 // independently, so stores of one warp overlap the fp64 work of others).
 constexpr int kVolThreads = 128;
 constexpr int kVolWarps = kVolThreads / 32;
+#ifndef PHFEM_VOL_MIN_BLOCKS
+#define PHFEM_VOL_MIN_BLOCKS 6
+#endif
+constexpr int kVolMinBlocks = PHFEM_VOL_MIN_BLOCKS;
 
 __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base, int n_valid,
                                            int per, const double* vals, double* buf, bool vec) {
@@ -43,43 +48,67 @@ __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base,
   }
 }
 
-template <bool kBlocks, bool kLoad>
-__global__ void __launch_bounds__(kVolThreads, 8) k_volume(VolArgs a, phfem_dev_errors* err) {
+template <bool kBlocks, bool kLoad, int FK, int CK>
+__global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a, phfem_dev_errors* err) {
   __shared__ __align__(16) double wbuf[kVolWarps][32 * 9];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* buf = wbuf[warp];
   const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
-  for (int64_t ch = (int64_t)blockIdx.x * kVolWarps + warp; ch < nchunks;
-       ch += (int64_t)gridDim.x * kVolWarps) {
+  const int64_t step = (int64_t)gridDim.x * kVolWarps;
+  // software pipeline: the vertex indices of chunk ch + 2 step and the
+  // coordinates of chunk ch + step are in flight while chunk ch computes
+  auto ld_idx = [&](int64_t c, int& i0, int& i1, int& i2) {
+    const int64_t m = c * 32 + lane;
+    if (c < nchunks && m < a.nE) {
+      i0 = __ldg(a.elements + 3 * m);
+      i1 = __ldg(a.elements + 3 * m + 1);
+      i2 = __ldg(a.elements + 3 * m + 2);
+    } else {
+      i0 = -1;
+    }
+  };
+  auto ld_xy = [&](int i0, int i1, int i2, double2& v0, double2& v1, double2& v2) {
+    if (i0 >= 0) {
+      v0 = __ldg(a.coords + i0);
+      v1 = __ldg(a.coords + i1);
+      v2 = __ldg(a.coords + i2);
+    } else {  // padding lanes: a harmless unit triangle
+      v0 = make_double2(0.0, 0.0);
+      v1 = make_double2(1.0, 0.0);
+      v2 = make_double2(0.0, 1.0);
+    }
+  };
+  int64_t ch = (int64_t)blockIdx.x * kVolWarps + warp;
+  int i0, i1, i2, n0, n1, n2;
+  ld_idx(ch, i0, i1, i2);
+  ld_idx(ch + step, n0, n1, n2);
+  double2 v0, v1, v2;
+  ld_xy(i0, i1, i2, v0, v1, v2);
+  for (; ch < nchunks; ch += step) {
     const int64_t base = ch * 32;
     const int n_valid = (int)((int64_t)a.nE - base < 32 ? (int64_t)a.nE - base : 32);
     const int64_t m = base + lane;
     const bool valid = lane < n_valid;
-    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(1.0, 0.0), v2 = make_double2(0.0, 1.0);
-    if (valid) {
-      const int i0 = __ldg(a.elements + 3 * m), i1 = __ldg(a.elements + 3 * m + 1),
-                i2 = __ldg(a.elements + 3 * m + 2);
-      v0 = __ldg(a.coords + i0);
-      v1 = __ldg(a.coords + i1);
-      v2 = __ldg(a.coords + i2);
-    }
+    // next chunk's coordinates, the one after's indices
+    double2 w0, w1, w2;
+    ld_xy(n0, n1, n2, w0, w1, w2);
+    ld_idx(ch + 2 * step, n0, n1, n2);
     if (kLoad) {
       double bl[3];
-      element_load(v0, v1, v2, &a.f, a.t, bl, valid, m, err);
+      element_load_dev<FK>(v0, v1, v2, a.f, a.t, bl, valid, m, err);
       warp_store(a.load, base, n_valid, 3, bl, buf, a.vec);
     }
     if (kBlocks) {
-      const phfem_geom g = phfem_geometry(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      const phfem_geom g = geometry_dev(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
       if (valid && !(g.t2 > 0.0)) atomicMin(&err->degenerate, (unsigned long long)m);
-      const phfem_coeff_values cv =
-          phfem_coeffs_eval(&a.coeffs, v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      const phfem_coeff_values cv = coeffs_dev<CK>(a.coeffs, v0, v1, v2);
       double x[9];
       if (a.B) {
         phfem_stiffness(&g, &cv, x);
         warp_store(a.B, base, n_valid, 9, x, buf, a.vec);
       }
       if (a.D) {
-        phfem_convection(&g, &cv, x);
+        convection_dev(&g, &cv, x);
         warp_store(a.D, base, n_valid, 9, x, buf, a.vec);
       }
       if (a.M) {
@@ -91,6 +120,9 @@ __global__ void __launch_bounds__(kVolThreads, 8) k_volume(VolArgs a, phfem_dev_
         warp_store(a.M0, base, n_valid, 9, x, buf, a.vec);
       }
     }
+    v0 = w0;
+    v1 = w1;
+    v2 = w2;
   }
 }
 
@@ -99,12 +131,28 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
   const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
   const int grid = (int)std::min<int64_t>((nchunks + kVolWarps - 1) / kVolWarps,
                                           (int64_t)ctx->num_sms * 8 * 4);
-  if (blocks && load)
-    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<true, true><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
-  else if (blocks)
-    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<true, false><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
-  else
-    PHFEM_LAUNCH(ctx, "k_volume", (k_volume<false, true><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)));
+  const int fk = load ? field_kind_spec(a.f) : kKindGeneric;
+  const int ck = a.coeffs.kind == PHFEM_COEFF_CENTROID_POLY ? PHFEM_COEFF_CENTROID_POLY : PHFEM_COEFF_CONST;
+#define PHFEM_VOL(B, L, F, K) \
+  PHFEM_LAUNCH(ctx, "k_volume", (k_volume<B, L, F, K><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)))
+#define PHFEM_VOL_CK(B, L, F)                                                            \
+  do {                                                                                   \
+    if (ck == PHFEM_COEFF_CENTROID_POLY) PHFEM_VOL(B, L, F, PHFEM_COEFF_CENTROID_POLY); \
+    else PHFEM_VOL(B, L, F, PHFEM_COEFF_CONST);                                          \
+  } while (0)
+#define PHFEM_VOL_FK(B, L)                                                               \
+  do {                                                                                   \
+    if (fk == PHFEM_FIELD_SINSIN) PHFEM_VOL_CK(B, L, PHFEM_FIELD_SINSIN);               \
+    else if (fk == PHFEM_FIELD_EXP_SINSIN) PHFEM_VOL_CK(B, L, PHFEM_FIELD_EXP_SINSIN);  \
+    else if (fk == PHFEM_FIELD_ZERO) PHFEM_VOL_CK(B, L, PHFEM_FIELD_ZERO);              \
+    else PHFEM_VOL_CK(B, L, kKindGeneric);                                               \
+  } while (0)
+  if (blocks && load) PHFEM_VOL_FK(true, true);
+  else if (blocks) PHFEM_VOL_CK(true, false, kKindGeneric);
+  else PHFEM_VOL_FK(false, true);
+#undef PHFEM_VOL_FK
+#undef PHFEM_VOL_CK
+#undef PHFEM_VOL
   return PHFEM_OK;
 }
 

@@ -379,3 +379,19 @@ def test_large_refinement_properties(ctx):
     row_ptr = r.ctx.to_host(rp.row_ptr, (r.out.cls.L + 1,), np.int32)
     assert row_ptr[-1] == rp.nnz and (np.diff(row_ptr) >= 2).all()
     r.release()
+
+
+@pytest.mark.gpu
+def test_fastmath_selftest(ctx):
+    """The element kernels divide through one correctly rounded reciprocal per
+    element (csrc/fastmath.cuh, Markstein); the blocks are bit-exact only if
+    that division equals IEEE '/' on every operand — 2^28 random pairs in three
+    families (wide exponents, quotients at binade boundaries, mesh-like
+    geometry) must show zero mismatches.  The fast sin stays within 2 ulp of
+    CUDA's sin."""
+    import ctypes as C
+    out = (C.c_ulonglong * 3)()
+    ctx.check(ctx.lib.phfem_selftest_fastmath(ctx.ptr, 1 << 28, 20241015, out))
+    assert out[0] == 0, f"{out[0]} fast divisions differ from IEEE division"
+    assert out[2] == 0, f"{out[2]} divisions by 3 differ"
+    assert out[1] <= 2, f"sin_fast off by {out[1]} ulp"
