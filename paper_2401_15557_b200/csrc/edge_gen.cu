@@ -120,6 +120,17 @@ struct EgOut {
   int32_t* node_edge_start;
 };
 
+// Edge record of the sort pass (one per unique edge, at a tile-local slot of
+// the tile's item range): {max node, min node, occ_f << 1 | dir, occ_g or -1}
+// — occ = 3 m + slot of the t_plus / t_minus occurrence.
+__device__ __forceinline__ int4 eg_record(int32_t v, int32_t lo, uint64_t f, uint64_t g, bool two,
+                                          int ob) {
+  const uint32_t occ_mask = (uint32_t)((1ull << ob) - 1ull);
+  const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
+  const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
+  return make_int4(v, lo, (int)((occ_f << 1) | (uint32_t)(f & 1ull)), two ? (int)occ_g : -1);
+}
+
 // One CTA per tile of kTileNodes consecutive max-node ids (= 256 >> bs
 // consecutive buckets).  Item-parallel throughout: counting sort by node,
 // per-segment rank sort (segments are tiny: ~6 occurrences per node), blocked
@@ -138,14 +149,14 @@ struct TileSmem {
   int32_t nedge[kTileNodes];
   int32_t sbo[kTileNodes + 1];
   unsigned long long scan[33];
-  unsigned long long prefix;
   int tile;
 };
 
 template <bool kS>
 __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, const EgParams& P,
                                         TileSmem& sm, uint64_t* g1, uint64_t* g2, uint8_t* gnode,
-                                        unsigned long long* status, const EgOut& out,
+                                        int4* __restrict__ rec, int32_t* __restrict__ tileE,
+                                        int32_t* __restrict__ tileB, const EgOut& out,
                                         phfem_dev_errors* err) {
   const int tid = threadIdx.x;
   const int T = blockDim.x;
@@ -229,23 +240,13 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
   unsigned long long agg;
   const unsigned long long ex =
       block_exclusive_scan(((unsigned long long)ne_i << 32) | nb_i, sm.scan, &agg);
-  // per-node first edge (max-node grouping table)
+  // per-node first edge, tile-local (k_eg_emit adds the tile offset)
   const int ne_node = sm.nedge[tid];
   unsigned long long tot2;
   const int nes_local = (int)block_exclusive_scan((unsigned long long)ne_node, sm.scan, &tot2);
-  if (tid < 32) {
-    const uint64_t pre =
-        eg_lookback(status, tile, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
-    if (tid == 0) sm.prefix = pre;
-  }
-  __syncthreads();
-  const uint64_t pre = sm.prefix;
   const int64_t v_me = (int64_t)tile * kTileNodes + tid;
-  if (v_me < P.nC) out.node_edge_start[v_me] = (int32_t)(pre >> 32) + nes_local;
-  int32_t e = (int32_t)((pre >> 32) + (ex >> 32));
-  int32_t bpos = (int32_t)((pre & 0xffffffffu) + (ex & 0xffffffffu));
-  int32_t ipos = e - bpos;
-  const uint32_t occ_mask = (uint32_t)((1ull << P.occ_bits) - 1ull);
+  if (v_me < P.nC) out.node_edge_start[v_me] = nes_local;
+  int32_t e = (int32_t)(ex >> 32);  // tile-local edge index
   for (int p = p0; p < p1; ++p) {
     const int nd = node_of[p];
     const int st = sm.seg[nd], en = st + sm.cnt[nd];
@@ -254,67 +255,24 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
     if (p != st && ((buf2[p - 1] >> lo_shift) & lo_mask) == lo) continue;
     const bool two = p + 1 < en && ((buf2[p + 1] >> lo_shift) & lo_mask) == lo;
     const int32_t v = (int32_t)(tile * kTileNodes + nd);
-    const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
-    const int m_f = (int)(occ_f / 3u);
-    const int l_f = (int)((occ_f % 3u + 2u) % 3u);
-    const bool dir = f & 1ull;
-    reinterpret_cast<int2*>(out.edge_nodes)[e] =
-        dir ? make_int2(v, (int32_t)lo) : make_int2((int32_t)lo, v);
-    out.ltp[e] = l_f;
-    out.elem_edge[3 * (int64_t)m_f + l_f] = e;
-    if (two) {
-      const uint64_t g = buf2[p + 1];
-      const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
-      const int m_g = (int)(occ_g / 3u);
-      const int l_g = (int)((occ_g % 3u + 2u) % 3u);
-      reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
-      out.ltm[e] = l_g;
-      out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
-      out.interior[ipos++] = e;
-    } else {
-      reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
-      out.ltm[e] = -1;
-      out.boundary[bpos++] = e;
-    }
+    rec[s + e] = eg_record(v, (int32_t)lo, f, two ? buf2[p + 1] : 0, two, P.occ_bits);
     ++e;
   }
-  if (tile == P.nb - 1 && tid == 0) {
-    const uint64_t E = (pre >> 32) + (agg >> 32);
-    const uint64_t NBd = (pre & 0xffffffffu) + (agg & 0xffffffffu);
-    err->counters[0] = E;
-    err->counters[1] = E - NBd;
-    err->counters[2] = NBd;
-    out.node_edge_start[P.nC] = (int32_t)E;
+  if (tid == 0) {
+    tileE[tile] = (int32_t)(agg >> 32);
+    tileB[tile] = (int32_t)(agg & 0xffffffffu);
   }
 }
 
-// Fast tile path: after the counting sort by max node, each warp takes its
-// 32 nodes in node-aligned chunks of <= 32 occurrences and sorts a chunk with
-// a register bitonic network on the key (chunk-local node | min node |
-// occurrence).  Partners, run starts and the reference's error checks are
-// then lane-neighbour tests; edge ranks are ballot/popc prefixes, so the
-// emission pass writes consecutive edge ids from consecutive lanes.
-__device__ __forceinline__ void warp_bitonic32(uint64_t& key, uint32_t& pay) {
-  const unsigned lane = lane_id();
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, j);
-      const uint32_t op = __shfl_xor_sync(0xffffffffu, pay, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      const bool take = (lower == up) ? (ok < key) : (ok > key);
-      if (take) {
-        key = ok;
-        pay = op;
-      }
-    }
-  }
-}
-
+// Fast tile path (every node <= 32 occurrences): counting sort by max node,
+// rank sort inside each node segment (each item counts the smaller keys of
+// its segment — ~6 compares on refined meshes, far fewer instructions than a
+// 32-wide bitonic network), then per warp run starts / partners / the
+// reference's error checks as neighbour tests; edge ranks are ballot/popc
+// prefixes, so records of consecutive edges come from consecutive lanes.
 __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items, const EgParams& P,
-                                             TileSmem& sm, unsigned long long* status,
+                                             TileSmem& sm, int4* __restrict__ rec,
+                                             int32_t* __restrict__ tileE, int32_t* __restrict__ tileB,
                                              const EgOut& out, phfem_dev_errors* err) {
   const int tid = threadIdx.x;
   const int T = blockDim.x;
@@ -327,7 +285,6 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   const int ob = P.occ_bits;
   const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
   const uint64_t lokmask = (1ull << (P.lo_bits + P.occ_bits)) - 1ull;
-  const uint32_t occ_mask = (uint32_t)((1ull << ob) - 1ull);
   const unsigned lt = lanemask_lt();
 
   // counting sort by node (histogram already in sm.cnt)
@@ -356,51 +313,49 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   }
   __syncthreads();
 
-  // per warp: node-aligned chunks, sort, counts
+  // rank sort inside each node segment (<= 32 items, ~6 on refined meshes):
+  // key = (min node, occurrence), unique; the reference's stable order
+  for (int p = tid; p < n; p += T) {
+    const uint64_t it = sm.buf1[p];
+    const uint64_t k = (it >> 1) & lokmask;
+    const int nd = sm.node_of[p];
+    const int st = sm.seg[nd], c = sm.cnt[nd];
+    int r = 0;
+    for (int q = st; q < st + c; ++q) r += ((sm.buf1[q] >> 1) & lokmask) < k;
+    sm.buf2[st + r] = it;
+  }
+  __syncthreads();
+  // per warp (its 32 nodes): run starts, partners, the reference's two error
+  // checks (edge_topology.cpp:82-99) as neighbour tests in the sorted segment
   const int cnt_l = sm.cnt[32 * warp + lane];
-  const int incl = warp_inclusive_scan(cnt_l);
-  const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+  const int wtotal = __shfl_sync(0xffffffffu, warp_inclusive_scan(cnt_l), 31);
   const int wbase = sm.seg[32 * warp];
   uint32_t w_ne = 0, w_nb = 0;
-  int cs = 0, base = 0;
-  while (base < wtotal) {
-    const unsigned fits = __ballot_sync(0xffffffffu, lane >= cs && incl - base <= 32);
-    const int ce = 32 - __clz(fits);                    // one past the last node of the chunk
-    const int nitems = __shfl_sync(0xffffffffu, incl, ce - 1) - base;
-    const int pos = wbase + base + lane;
-    const bool valid = lane < nitems;
-    uint64_t key = ~0ull;
-    uint32_t dir = 0;
+  for (int q = 0; q < wtotal; q += 32) {
+    const int pos = wbase + q + lane;
+    const bool valid = q + lane < wtotal;
+    bool start = false, partner = false, third = false;
+    uint64_t f = 0, g = 0;
     int nd = 0;
     if (valid) {
-      const uint64_t it = sm.buf1[pos];
+      f = sm.buf2[pos];
       nd = sm.node_of[pos];
-      key = ((uint64_t)(nd - 32 * warp - cs) << 59) | ((it >> 1) & lokmask);
-      dir = (uint32_t)(it & 1ull);
+      const int st = sm.seg[nd], en = st + sm.cnt[nd];
+      const uint64_t lo = (f >> (ob + 1)) & lomask;
+      start = pos == st || ((sm.buf2[pos - 1] >> (ob + 1)) & lomask) != lo;
+      if (start && pos + 1 < en) {
+        g = sm.buf2[pos + 1];
+        partner = ((g >> (ob + 1)) & lomask) == lo;
+        third = partner && pos + 2 < en && ((sm.buf2[pos + 2] >> (ob + 1)) & lomask) == lo;
+      }
+      if (start && (third || (partner && ((f ^ g) & 1ull) == 0))) {
+        const uint64_t v = (uint64_t)tile * kTileNodes + nd;
+        atomicMin(&err->topo, (v << 33) | (lo << 2) | (third ? 0ull : (2ull | (f & 1ull))));
+      }
+      if (start) atomicAdd(&sm.nedge[nd], 1);
     }
-    warp_bitonic32(key, dir);
-    if (valid) {
-      nd = sm.node_of[pos];  // node grouping is preserved by the sort
-      sm.buf2[pos] = ((key & lokmask) << 1) | dir;
-    }
-    const uint64_t grp = key >> ob;
-    const uint64_t gp = __shfl_up_sync(0xffffffffu, grp, 1);
-    const uint64_t gn = __shfl_down_sync(0xffffffffu, grp, 1);
-    const uint64_t gn2 = __shfl_down_sync(0xffffffffu, grp, 2);
-    const uint32_t dn = __shfl_down_sync(0xffffffffu, dir, 1);
-    const bool start = valid && (lane == 0 || gp != grp);
-    const bool partner = valid && lane + 1 < nitems && gn == grp;
-    const bool third = partner && lane + 2 < nitems && gn2 == grp;
-    if (start && (third || (partner && dn == dir))) {
-      const uint64_t v = (uint64_t)tile * kTileNodes + nd;
-      const uint64_t lo = (key >> ob) & lomask;
-      atomicMin(&err->topo, (v << 33) | (lo << 2) | (third ? 0ull : (2ull | dir)));
-    }
-    if (start) atomicAdd(&sm.nedge[nd], 1);
     w_ne += __popc(__ballot_sync(0xffffffffu, start));
     w_nb += __popc(__ballot_sync(0xffffffffu, start && !partner));
-    base += nitems;
-    cs = ce;
   }
   // CTA totals: per-warp offsets
   __shared__ unsigned long long wsum[kTileThreads / 32];
@@ -414,19 +369,11 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   const int ne_node = sm.nedge[tid];
   unsigned long long tot2;
   const int nes_local = (int)block_exclusive_scan((unsigned long long)ne_node, sm.scan, &tot2);
-  if (tid < 32) {
-    const uint64_t pre =
-        eg_lookback(status, tile, (uint32_t)(agg >> 32), (uint32_t)(agg & 0xffffffffu));
-    if (tid == 0) sm.prefix = pre;
-  }
-  __syncthreads();
-  const uint64_t pre = sm.prefix;
   const int64_t v_me = (int64_t)tile * kTileNodes + tid;
-  if (v_me < P.nC) out.node_edge_start[v_me] = (int32_t)(pre >> 32) + nes_local;
+  if (v_me < P.nC) out.node_edge_start[v_me] = nes_local;  // tile-local
 
-  // emission: consecutive positions, ranks by ballot
-  int32_t e_off = (int32_t)((pre >> 32) + (wex >> 32));
-  int32_t b_off = (int32_t)((pre & 0xffffffffu) + (wex & 0xffffffffu));
+  // records of the tile's edges at tile-local positions (ranks by ballot)
+  int32_t e_off = (int32_t)(wex >> 32);
   for (int q = 0; q < wtotal; q += 32) {
     const int pos = wbase + q + lane;
     const bool valid = q + lane < wtotal;
@@ -445,41 +392,17 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
       }
     }
     const unsigned sb = __ballot_sync(0xffffffffu, start);
-    const unsigned bb = __ballot_sync(0xffffffffu, start && !partner);
     if (start) {
       const int32_t e = e_off + __popc(sb & lt);
       const int32_t v = tile * kTileNodes + nd;
       const int32_t lo = (int32_t)((f >> (ob + 1)) & lomask);
-      const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
-      const int m_f = (int)(occ_f / 3u);
-      const int l_f = (int)((occ_f % 3u + 2u) % 3u);
-      reinterpret_cast<int2*>(out.edge_nodes)[e] = (f & 1ull) ? make_int2(v, lo) : make_int2(lo, v);
-      out.ltp[e] = l_f;
-      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
-      if (partner) {
-        const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
-        const int m_g = (int)(occ_g / 3u);
-        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
-        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
-        out.ltm[e] = l_g;
-        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
-        out.interior[e - (b_off + __popc(bb & lt))] = e;
-      } else {
-        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
-        out.ltm[e] = -1;
-        out.boundary[b_off + __popc(bb & lt)] = e;
-      }
+      rec[s + e] = eg_record(v, lo, f, g, partner, ob);
     }
     e_off += __popc(sb);
-    b_off += __popc(bb);
   }
-  if (tile == P.nb - 1 && tid == 0) {
-    const uint64_t E = (pre >> 32) + (agg >> 32);
-    const uint64_t NBd = (pre & 0xffffffffu) + (agg & 0xffffffffu);
-    err->counters[0] = E;
-    err->counters[1] = E - NBd;
-    err->counters[2] = NBd;
-    out.node_edge_start[P.nC] = (int32_t)E;
+  if (tid == 0) {
+    tileE[tile] = (int32_t)(agg >> 32);
+    tileB[tile] = (int32_t)(agg & 0xffffffffu);
   }
 }
 
@@ -488,13 +411,14 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
                                                           const int32_t* __restrict__ boff,
                                                           int nbuckets, EgParams P, uint64_t* g1,
                                                           uint64_t* g2, uint8_t* gnode,
-                                                          unsigned long long* status,
-                                                          int32_t* ticket, EgOut out,
+                                                          int4* __restrict__ rec,
+                                                          int32_t* __restrict__ tileE,
+                                                          int32_t* __restrict__ tileB, EgOut out,
                                                           phfem_dev_errors* err) {
   extern __shared__ __align__(16) unsigned char smraw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
   const int tid = threadIdx.x;
-  if (tid == 0) sm.tile = atomicAdd(ticket, 1);
+  if (tid == 0) sm.tile = blockIdx.x;
   sm.cnt[tid] = 0;
   sm.nedge[tid] = 0;
   __syncthreads();
@@ -523,15 +447,71 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
     fast = __syncthreads_and(sm.cnt[tid] <= 32);
   }
   if (fast) {
-    eg_tile_fast(items, P, sm, status, out, err);
+    eg_tile_fast(items, P, sm, rec, tileE, tileB, out, err);
     return;
   }
   sm.cnt[tid] = 0;
   __syncthreads();
   if (n <= kTileCap)
-    eg_tile<true>(items, P, sm, g1, g2, gnode, status, out, err);
+    eg_tile<true>(items, P, sm, g1, g2, gnode, rec, tileE, tileB, out, err);
   else
-    eg_tile<false>(items, P, sm, g1, g2, gnode, status, out, err);
+    eg_tile<false>(items, P, sm, g1, g2, gnode, rec, tileE, tileB, out, err);
+}
+
+// E ------------------------------------------------------------------------
+// One CTA per tile: the tile's edge records (consecutive, tile-local) become
+// the final outputs at the scanned tile offsets — coalesced record reads and
+// edge-array writes; ids are canonical because tiles are max-node ranges.
+constexpr int kEmitThreads = kTileNodes;
+__global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict__ rec,
+                                                          const int32_t* __restrict__ boff,
+                                                          int nbuckets, int nsub,
+                                                          const int32_t* __restrict__ tileE,
+                                                          const int32_t* __restrict__ tileB, int nC,
+                                                          EgOut out) {
+  __shared__ int32_t scan[33];
+  const int tile = blockIdx.x;
+  const int64_t s = boff[min(tile * nsub, nbuckets)];
+  const int E0 = tileE[tile], ne = tileE[tile + 1] - E0;
+  const int B0 = tileB[tile];
+  const int64_t vme = (int64_t)tile * kTileNodes + threadIdx.x;
+  if (vme < nC) out.node_edge_start[vme] += E0;
+  if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
+  int bsum = 0;
+  for (int base = 0; base < ne; base += kEmitThreads) {
+    const int i = base + (int)threadIdx.x;
+    const bool valid = i < ne;
+    int4 r = make_int4(0, 0, 0, 0);
+    if (valid) r = rec[s + i];
+    const bool bnd = valid && r.w < 0;
+    int tot;
+    const int bex = block_exclusive_scan((int)bnd, scan, &tot);
+    if (valid) {
+      const int32_t e = E0 + i;
+      const uint32_t z = (uint32_t)r.z;
+      const uint32_t occ_f = z >> 1;
+      const int m_f = (int)(occ_f / 3u);
+      const int l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
+      reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(r.x, r.y) : make_int2(r.y, r.x);
+      out.ltp[e] = l_f;
+      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
+      const int32_t bpos = B0 + bsum + bex;  // boundary edges before e
+      if (!bnd) {
+        const uint32_t occ_g = (uint32_t)r.w;
+        const int m_g = (int)(occ_g / 3u);
+        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
+        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
+        out.ltm[e] = l_g;
+        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+        out.interior[e - bpos] = e;
+      } else {
+        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
+        out.ltm[e] = -1;
+        out.boundary[bpos] = e;
+      }
+    }
+    bsum += tot;
+  }
 }
 
 __global__ void k_eg_tile_max(const int32_t* __restrict__ boff, int nbuckets, int nsub, int ntiles,
@@ -600,16 +580,15 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   }
 
   PHFEM_TRY(errors_reset(ctx));
-  int32_t *bcount = nullptr, *boff = nullptr, *ticket = nullptr;
-  unsigned long long* status = nullptr;
+  int32_t *bcount = nullptr, *boff = nullptr, *tiles = nullptr;
+  const int ntiles_h = (int)((nC + kTileNodes - 1) / kTileNodes);
   PHFEM_TRY(dalloc(ctx, &bcount, (int64_t)P.nb + 1));
   PHFEM_TRY(dalloc(ctx, &boff, (int64_t)P.nb + 1));
-  PHFEM_TRY(dalloc(ctx, &status, (P.nC + 255) / 256 + 1));
-  PHFEM_TRY(dalloc(ctx, &ticket, 1));
+  PHFEM_TRY(dalloc(ctx, &tiles, 2 * ((int64_t)ntiles_h + 1)));
+  int32_t* tileE = tiles;
+  int32_t* tileB = tiles + ntiles_h + 1;
   PHFEM_CUDA(ctx, cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (P.nb + 1), ctx->stream));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ((P.nC + 255) / 256 + 1),
-                                  ctx->stream));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 2 * (ntiles_h + 1), ctx->stream));
 
   const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
   const int nsub = kTileNodes >> P.bs;
@@ -624,7 +603,7 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   PHFEM_TRY(errors_fetch(ctx));
   if (ctx->herr->misc != ~0ull) {
     const long long m = (long long)ctx->herr->misc;
-    dfree(ctx, bcount); dfree(ctx, boff); dfree(ctx, status); dfree(ctx, ticket);
+    dfree(ctx, bcount); dfree(ctx, boff); dfree(ctx, tiles);
     return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE,
                      "build_topology: element %lld has a node index outside 1..%lld", m + 1,
                      (long long)nC);
@@ -634,7 +613,9 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   uint64_t* items = nullptr;
   uint64_t *g1 = nullptr, *g2 = nullptr;
   uint8_t* gnode = nullptr;
+  int4* rec = nullptr;
   PHFEM_TRY(dalloc(ctx, &items, nd));
+  PHFEM_TRY(dalloc(ctx, &rec, nd));
   if (max_tile > kTileCap) {  // some tile does not fit SMEM: global scratch
     PHFEM_TRY(dalloc(ctx, &g1, nd));
     PHFEM_TRY(dalloc(ctx, &g2, nd));
@@ -653,15 +634,24 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
     attr_set = true;
   }
   PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
-      items, boff, P.nb, PT, g1, g2, gnode, status, ticket, o, ctx->derr));
+      items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileE, tileE, (int64_t)ntiles + 1, nullptr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, (int64_t)ntiles + 1, nullptr));
+  PHFEM_LAUNCH(ctx, "k_eg_emit", k_eg_emit<<<ntiles, kEmitThreads, 0, ctx->stream>>>(
+      rec, boff, P.nb, nsub, tileE, tileB, (int)nC, o));
+  // totals ride back with the error words (low 32 bits of counters 0 / 2)
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[0], tileE + ntiles, sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[2], tileB + ntiles, sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
   dfree(ctx, items);
+  dfree(ctx, rec);
   dfree(ctx, g1);
   dfree(ctx, g2);
   dfree(ctx, gnode);
   dfree(ctx, bcount);
   dfree(ctx, boff);
-  dfree(ctx, status);
-  dfree(ctx, ticket);
+  dfree(ctx, tiles);
   PHFEM_TRY(errors_fetch(ctx));
   const uint64_t te = ctx->herr->topo;
   if (te != ~0ull) {
@@ -679,8 +669,8 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
                      "build_topology: non-manifold edge (%lld,%lld) shared by more than two elements",
                      lo + 1, hi + 1);
   }
-  out->E = (int32_t)ctx->herr->counters[0];
-  out->n_interior = (int32_t)ctx->herr->counters[1];
-  out->n_boundary = (int32_t)ctx->herr->counters[2];
+  out->E = (int32_t)(ctx->herr->counters[0] & 0xffffffffu);
+  out->n_boundary = (int32_t)(ctx->herr->counters[2] & 0xffffffffu);
+  out->n_interior = out->E - out->n_boundary;
   return PHFEM_OK;
 }
