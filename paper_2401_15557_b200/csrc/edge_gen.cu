@@ -121,14 +121,17 @@ struct EgOut {
 };
 
 // Edge record of the sort pass (one per unique edge, at a tile-local slot of
-// the tile's item range): {max node, min node, occ_f << 1 | dir, occ_g or -1}
-// — occ = 3 m + slot of the t_plus / t_minus occurrence.
-__device__ __forceinline__ int4 eg_record(int32_t v, int32_t lo, uint64_t f, uint64_t g, bool two,
-                                          int ob) {
+// the tile's item range): {local max node | boundary edges before it in the
+// tile << 8, min node, occ_f << 1 | dir, occ_g or -1} — occ = 3 m + slot of
+// the t_plus / t_minus occurrence.  Carrying the tile-local boundary prefix
+// lets the emit pass run one record per thread with no scan.
+__device__ __forceinline__ int4 eg_record(int nd, int bloc, int32_t lo, uint64_t f, uint64_t g,
+                                          bool two, int ob) {
   const uint32_t occ_mask = (uint32_t)((1ull << ob) - 1ull);
   const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
   const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
-  return make_int4(v, lo, (int)((occ_f << 1) | (uint32_t)(f & 1ull)), two ? (int)occ_g : -1);
+  return make_int4(nd | bloc << 8, lo, (int)((occ_f << 1) | (uint32_t)(f & 1ull)),
+                   two ? (int)occ_g : -1);
 }
 
 // One CTA per tile of kTileNodes consecutive max-node ids (= 256 >> bs
@@ -247,6 +250,7 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
   const int64_t v_me = (int64_t)tile * kTileNodes + tid;
   if (v_me < P.nC) out.node_edge_start[v_me] = nes_local;
   int32_t e = (int32_t)(ex >> 32);  // tile-local edge index
+  int32_t bl = (int32_t)(ex & 0xffffffffu);  // tile-local boundary edges before it
   for (int p = p0; p < p1; ++p) {
     const int nd = node_of[p];
     const int st = sm.seg[nd], en = st + sm.cnt[nd];
@@ -254,9 +258,9 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
     const uint64_t lo = (f >> lo_shift) & lo_mask;
     if (p != st && ((buf2[p - 1] >> lo_shift) & lo_mask) == lo) continue;
     const bool two = p + 1 < en && ((buf2[p + 1] >> lo_shift) & lo_mask) == lo;
-    const int32_t v = (int32_t)(tile * kTileNodes + nd);
-    rec[s + e] = eg_record(v, (int32_t)lo, f, two ? buf2[p + 1] : 0, two, P.occ_bits);
+    rec[s + e] = eg_record(nd, bl, (int32_t)lo, f, two ? buf2[p + 1] : 0, two, P.occ_bits);
     ++e;
+    bl += !two;
   }
   if (tid == 0) {
     tileE[tile] = (int32_t)(agg >> 32);
@@ -284,7 +288,6 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   const int shift = P.total_bits;
   const int ob = P.occ_bits;
   const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
-  const uint64_t lokmask = (1ull << (P.lo_bits + P.occ_bits)) - 1ull;
   const unsigned lt = lanemask_lt();
 
   // counting sort by node (histogram already in sm.cnt)
@@ -315,13 +318,14 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
 
   // rank sort inside each node segment (<= 32 items, ~6 on refined meshes):
   // key = (min node, occurrence), unique; the reference's stable order
+  // (items of one segment share the max-node bits and differ in (min, occ),
+  // so the raw 64-bit items compare in key order)
   for (int p = tid; p < n; p += T) {
     const uint64_t it = sm.buf1[p];
-    const uint64_t k = (it >> 1) & lokmask;
     const int nd = sm.node_of[p];
     const int st = sm.seg[nd], c = sm.cnt[nd];
     int r = 0;
-    for (int q = st; q < st + c; ++q) r += ((sm.buf1[q] >> 1) & lokmask) < k;
+    for (int q = st; q < st + c; ++q) r += sm.buf1[q] < it;
     sm.buf2[st + r] = it;
   }
   __syncthreads();
@@ -374,6 +378,7 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
 
   // records of the tile's edges at tile-local positions (ranks by ballot)
   int32_t e_off = (int32_t)(wex >> 32);
+  int32_t b_off = (int32_t)(wex & 0xffffffffu);
   for (int q = 0; q < wtotal; q += 32) {
     const int pos = wbase + q + lane;
     const bool valid = q + lane < wtotal;
@@ -392,13 +397,14 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
       }
     }
     const unsigned sb = __ballot_sync(0xffffffffu, start);
+    const unsigned bb = __ballot_sync(0xffffffffu, start && !partner);
     if (start) {
       const int32_t e = e_off + __popc(sb & lt);
-      const int32_t v = tile * kTileNodes + nd;
       const int32_t lo = (int32_t)((f >> (ob + 1)) & lomask);
-      rec[s + e] = eg_record(v, lo, f, g, partner, ob);
+      rec[s + e] = eg_record(nd, b_off + __popc(bb & lt), lo, f, g, partner, ob);
     }
     e_off += __popc(sb);
+    b_off += __popc(bb);
   }
   if (tid == 0) {
     tileE[tile] = (int32_t)(agg >> 32);
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
   __syncthreads();
   const int64_t s = sm.sbo[0];
   const int n = sm.sbo[nsub] - (int)s;
-  bool fast = n <= kTileCap && P.lo_bits + P.occ_bits <= 59;
+  bool fast = n <= kTileCap;
   if (fast) {  // histogram by node; the fast path needs every node <= 32 occurrences
     for (int p = tid; p < n; p += blockDim.x) {
       const uint64_t it = __ldg(items + s + p);
@@ -442,7 +448,13 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
         }
         sub = lo;
       }
-      atomicAdd(&sm.cnt[(sub << P.bs) | (int)(it >> P.total_bits)], 1);
+      const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
+#ifdef PHFEM_EG_HIST_MATCH
+      const unsigned g = __match_any_sync(__activemask(), nd);
+      if ((int)lane_id() == __ffs(g) - 1) atomicAdd(&sm.cnt[nd], __popc(g));
+#else
+      atomicAdd(&sm.cnt[nd], 1);
+#endif
     }
     fast = __syncthreads_and(sm.cnt[tid] <= 32);
   }
@@ -469,7 +481,6 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
                                                           const int32_t* __restrict__ tileE,
                                                           const int32_t* __restrict__ tileB, int nC,
                                                           EgOut out) {
-  __shared__ int32_t scan[33];
   const int tile = blockIdx.x;
   const int64_t s = boff[min(tile * nsub, nbuckets)];
   const int E0 = tileE[tile], ne = tileE[tile + 1] - E0;
@@ -477,27 +488,32 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
   const int64_t vme = (int64_t)tile * kTileNodes + threadIdx.x;
   if (vme < nC) out.node_edge_start[vme] += E0;
   if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
-  int bsum = 0;
-  for (int base = 0; base < ne; base += kEmitThreads) {
-    const int i = base + (int)threadIdx.x;
-    const bool valid = i < ne;
-    int4 r = make_int4(0, 0, 0, 0);
-    if (valid) r = rec[s + i];
-    const bool bnd = valid && r.w < 0;
-    int tot;
-    const int bex = block_exclusive_scan((int)bnd, scan, &tot);
-    if (valid) {
+  // one record per thread, 4 in flight: no scan (records carry their
+  // tile-local boundary prefix)
+  const int64_t vbase = (int64_t)tile * kTileNodes;
+  for (int i0 = threadIdx.x; i0 < ne; i0 += 4 * kEmitThreads) {
+    int4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kEmitThreads;
+      if (i < ne) r[u] = rec[s + i];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kEmitThreads;
+      if (i >= ne) break;
       const int32_t e = E0 + i;
-      const uint32_t z = (uint32_t)r.z;
+      const int32_t v = (int32_t)(vbase + (r[u].x & 0xff));
+      const int32_t bpos = B0 + (r[u].x >> 8);  // boundary edges before e
+      const uint32_t z = (uint32_t)r[u].z;
       const uint32_t occ_f = z >> 1;
       const int m_f = (int)(occ_f / 3u);
       const int l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
-      reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(r.x, r.y) : make_int2(r.y, r.x);
+      reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(v, r[u].y) : make_int2(r[u].y, v);
       out.ltp[e] = l_f;
       out.elem_edge[3 * (int64_t)m_f + l_f] = e;
-      const int32_t bpos = B0 + bsum + bex;  // boundary edges before e
-      if (!bnd) {
-        const uint32_t occ_g = (uint32_t)r.w;
+      if (r[u].w >= 0) {
+        const uint32_t occ_g = (uint32_t)r[u].w;
         const int m_g = (int)(occ_g / 3u);
         const int l_g = (int)((occ_g % 3u + 2u) % 3u);
         reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
@@ -510,7 +526,6 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
         out.boundary[bpos] = e;
       }
     }
-    bsum += tot;
   }
 }
 

@@ -87,10 +87,10 @@ template <bool kFull>
 struct LvSmem {
   int2 en[kLvF];
   int2 el[kLvF];
-  int32_t meta[kLvF];  // lp | (lm + 1) << 2
-  int32_t slot[kLvF];  // interior list index, or ~boundary list index
-  int32_t rp[kFull ? kLvF : 1];
-  int32_t rs[kFull ? kLvF : 1];
+  // tile-local list slot << 8 | lp | (lm + 1) << 2; the slot is the interior
+  // list index, or ~(boundary list index) — both offsets are added at store time
+  int32_t ms[kLvF];
+  int32_t rr[kFull ? kLvF : 1];  // retained: local row << 16 | local row start; else -1
   double len[kFull ? kLvF : 1];
   int32_t scan[33];
 };
@@ -152,8 +152,11 @@ __global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE,
   }
 }
 
+#ifndef PHFEM_LV_MIN_BLOCKS
+#define PHFEM_LV_MIN_BLOCKS 7
+#endif
 template <bool kFull>
-__global__ void __launch_bounds__(kLvT) k_rl_level(LvArgs a, LvOut o) {
+__global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a, LvOut o) {
   __shared__ LvSmem<kFull> s;
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
@@ -223,18 +226,18 @@ __global__ void __launch_bounds__(kLvT) k_rl_level(LvArgs a, LvOut o) {
       const int i = i0 + j;
       s.en[i] = make_int2(from, to);
       s.el[i] = make_int2(tpf, tmf);
-      s.meta[i] = lp | (tmf >= 0 ? lm + 1 : 0) << 2;  // local_in_tminus = -1 on the boundary
       // list slot: boundary list 2 B_e + j, else interior list f - 2 B_e - (2 if isB)
-      s.slot[i] = (j < 2 && isB) ? ~(2 * exB + j) : i - 2 * exB - (isB ? 2 : 0);
+      const int slot = (j < 2 && isB) ? ~(2 * exB + j) : i - 2 * exB - (isB ? 2 : 0);
+      s.ms[i] = slot * 256 | lp | (tmf >= 0 ? lm + 1 : 0) << 2;  // local_in_tminus = -1 on the boundary
       if (kFull) {
-        int rp = -1;
+        int rr = -1;
         if (j >= 2 || !neu) {
-          rp = i0 - 2 * exN + (neu ? j - 2 : j);
+          const int rp = i0 - 2 * exN + (neu ? j - 2 : j);
           const int bret = 2 * (exB - exN) + ((isB && !neu) ? (j == 1 ? 1 : (j >= 2 ? 2 : 0)) : 0);
-          s.rs[i] = 4 * rp - 2 * bret;
+          rr = rp << 16 | (4 * rp - 2 * bret);  // both in [0, 4 kLvF)
           s.len[i] = len;
         }
-        s.rp[i] = rp;
+        s.rr[i] = rr;
       }
     };
     // halves: a -> mu and mu -> b; the one at the smaller old node first
@@ -282,23 +285,23 @@ __global__ void __launch_bounds__(kLvT) k_rl_level(LvArgs a, LvOut o) {
   for (int i = tid; i < nf; i += kLvT) {
     const int f = F0 + i;
     const int2 en = s.en[i], el2 = s.el[i];
-    const int meta = s.meta[i];
-    const int lp = meta & 3, lm = (meta >> 2) - 1;
+    const int ms = s.ms[i];
+    const int lp = ms & 3, lm = ((ms >> 2) & 3) - 1;
     reinterpret_cast<int2*>(o.edge_nodes)[f] = en;
     reinterpret_cast<int2*>(o.edge_elements)[f] = el2;
     o.ltp[f] = lp;
     o.ltm[f] = lm;
-    const int sl = s.slot[i];
+    const int sl = ms >> 8;  // arithmetic shift: boundary slots stay negative
     if (sl < 0) o.boundary[off_bnd + ~sl] = f;
     else o.interior[off_int + sl] = f;
     o.elem_edge[3 * (int64_t)el2.x + lp] = f;
     if (lm >= 0) o.elem_edge[3 * (int64_t)el2.y + lm] = ~f;
     if (kFull) {
-      const int rl = s.rp[i];
-      o.rpos[f] = rl < 0 ? -1 : off_rp + rl;
-      if (rl >= 0) {
-        const int rp = off_rp + rl;
-        const int rs = off_rs + s.rs[i];
+      const int rr = s.rr[i];
+      o.rpos[f] = rr < 0 ? -1 : off_rp + (rr >> 16);
+      if (rr >= 0) {
+        const int rp = off_rp + (rr >> 16);
+        const int rs = off_rs + (rr & 0xffff);
         const double len = s.len[i];
         o.redges[rp] = f;
         o.row_ptr[rp] = rs;
