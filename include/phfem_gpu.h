@@ -284,6 +284,57 @@ phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipeline_out* o
 /* bytes phfem_pipeline_download moves for a given `out` and selection */
 int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* out, const phfem_pipeline_host* dst);
 
+/* ---- support of the C++ drop-in layer (paper_2401_15557_b200/dropin, see
+ * INTEGRATION.md): host-built reference objects -> device, the reference's
+ * lookup tables, and the std::function field path ------------------------
+ *
+ * A topology whose edge_nodes / edge_elements / local_in_tplus /
+ * local_in_tminus / interior / boundary arrays (and E, n_interior,
+ * n_boundary) the caller filled in device memory gets elem_edge and
+ * node_edge_start computed and is checked against the mesh: every element
+ * slot covered exactly once by an edge with the element's own vertex pair
+ * (else PHFEM_ERR_MISMATCH, the reference's "topology does not match mesh",
+ * refine.cpp:21-25), edges in canonical (max, min) order.                  */
+phfem_status phfem_topology_derive(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_topology* topo);
+
+/* EdgeTopology::pair_offsets / pair_entries / directed_offsets /
+ * directed_entries (edge_topology.hpp:38-44; built at edge_topology.cpp:
+ * 117-140): CSR by smaller node of (larger node, edge id), ids ascending;
+ * CSR by initial node of (end node, element), emission (element) order.
+ * Device buffers: offsets [nC+1], pair_entries [E][2], directed_entries
+ * [3nE][2].                                                                 */
+phfem_status phfem_topology_tables(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                   const phfem_topology* topo, int32_t* pair_offsets,
+                                   int32_t* pair_entries, int32_t* directed_offsets,
+                                   int32_t* directed_entries);
+
+/* edge_lengths (edge_topology.hpp:67; edge_topology.cpp:179-186) -> out[E] */
+phfem_status phfem_edge_lengths(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                                double* out);
+
+/* Sample points of the reference's std::function fields, which cannot run on
+ * the device.  LOAD: [3nE][2] edge midpoints per element (assembly.cpp:36);
+ * NEUMANN: [nN][4] (midpoint, outward unit normal) in Neumann-list order
+ * (:211-215); DIRICHLET: [nD][2] midpoints in Dirichlet-list order (:236).
+ * The caller evaluates f / g / u_D there and passes the values to:          */
+#define PHFEM_POINTS_LOAD 0
+#define PHFEM_POINTS_NEUMANN 1
+#define PHFEM_POINTS_DIRICHLET 2
+phfem_status phfem_field_points(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                                const phfem_classification* cls, int which, double* out);
+/* assemble_load / assemble_neumann / assemble_dirichlet with the field given
+ * as sampled values (same kernels, same operation order, same errors).      */
+phfem_status phfem_assemble_load_sampled(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                         const double* samples, double* out);
+phfem_status phfem_assemble_neumann_sampled(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                            const phfem_topology* topo,
+                                            const phfem_classification* cls,
+                                            const double* samples, double* out, int accumulate);
+phfem_status phfem_assemble_dirichlet_sampled(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                              const phfem_topology* topo,
+                                              const phfem_classification* cls,
+                                              const double* samples, double* out);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

@@ -297,3 +297,15 @@ def pipeline(hm: HostMesh, levels: int, coeffs, f, g, uD, t: float = 0.0) -> dic
     bd = assemble_dirichlet(om, topo, cls, uD, t)
     return {"mesh": hm, "topo": topo.arrays(), "cls": cls.arrays(), "C_csr": Cm["csr"],
             "C_csc": Cm["csc"], "B": B, "D": D, "M": M, "M0": M0, "load": b + ln, "bd": bd}
+
+
+def all_outputs(hm: HostMesh, coeffs, f, g, uD, t: float = 0.0) -> dict:
+    """Every hot-path output on one mesh, keyed like reference.all_outputs
+    (the parity tests compare the two dicts entry by entry)."""
+    om, ot = build_topology(hm)
+    oc = classify_edges(om, ot)
+    B, D, M, M0 = assemble_volume(hm, coeffs)
+    Cm = assemble_constraint(om, ot, oc)
+    return {"topo": ot.arrays(), "cls": oc.arrays(), "B": B, "D": D, "M": M, "M0": M0, "C_csc": Cm["csc"],
+            "C_csr": Cm["csr"], "b": assemble_load(hm, f, t), "ln": assemble_neumann(om, ot, oc, g, t),
+            "bd": assemble_dirichlet(om, ot, oc, uD, t), "refined": red_refine(hm, ot)}

@@ -13,6 +13,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(_HERE, "_ref", "libphfem_ref.so")
+# the same extern "C" runner linked against the C++ drop-in layer instead of
+# the reference's edge_topology / refine / assembly TUs (oracle/dropin.mk)
+DROPIN_LIB = os.path.join(_HERE, "_ref", "dropin", "libphfem_dropin_runner.so")
 
 import sys as _sys
 _sys.path.insert(0, os.path.dirname(_HERE))
@@ -37,6 +40,14 @@ def available() -> bool:
             return False
         return os.path.exists(LIB)
     return False
+
+
+def use_library(path: str) -> None:
+    """Point every function of this module at another build of the runner
+    (LIB = the reference's sources, DROPIN_LIB = the drop-in layer)."""
+    global _lib, LIB
+    LIB = path
+    _lib = None
 
 
 def lib():

@@ -145,6 +145,8 @@ EXPORTED = [
     "phfem_pipeline_from_host", "phfem_pipeline_download", "phfem_pipeline_download_bytes",
     "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_ctx_profile", "phfem_ctx_profile_read",
     "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level", "phfem_selftest_fastmath",
+    "phfem_topology_derive", "phfem_topology_tables", "phfem_field_points", "phfem_edge_lengths",
+    "phfem_assemble_load_sampled", "phfem_assemble_neumann_sampled", "phfem_assemble_dirichlet_sampled",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -215,6 +217,16 @@ def load_library(path: str = LIB_PATH):
                                         P(phfem_field), P(phfem_field), dbl, C.c_int, P(phfem_pipeline_out)]),
         "phfem_ctx_profile_read": (C.c_int, [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_int64)]),
         "phfem_selftest_fastmath": (C.c_int, [vp, i64, C.c_uint64, P(C.c_ulonglong)]),
+        "phfem_topology_derive": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology)]),
+        "phfem_topology_tables": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), vp, vp, vp, vp]),
+        "phfem_field_points": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                         C.c_int, vp]),
+        "phfem_assemble_load_sampled": (C.c_int, [vp, P(phfem_mesh), vp, vp]),
+        "phfem_edge_lengths": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), vp]),
+        "phfem_assemble_neumann_sampled": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology),
+                                                     P(phfem_classification), vp, vp, C.c_int]),
+        "phfem_assemble_dirichlet_sampled": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology),
+                                                       P(phfem_classification), vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a
     ld_idx(ch + 2 * step, n0, n1, n2);
     if (kLoad) {
       double bl[3];
-      element_load_dev<FK>(v0, v1, v2, a.f, a.t, bl, valid, m, err);
+      element_load_dev<FK>(v0, v1, v2, a.f, a.t, bl, valid, m, err, a.samples);
       warp_store(a.load, base, n_valid, 3, bl, buf, a.vec);
     }
     if (kBlocks) {
@@ -131,7 +131,7 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
   const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
   const int grid = (int)std::min<int64_t>((nchunks + kVolWarps - 1) / kVolWarps,
                                           (int64_t)ctx->num_sms * 8 * 4);
-  const int fk = load ? field_kind_spec(a.f) : kKindGeneric;
+  const int fk = !load ? kKindGeneric : (a.samples ? kKindSamples : field_kind_spec(a.f));
   const int ck = a.coeffs.kind == PHFEM_COEFF_CENTROID_POLY ? PHFEM_COEFF_CENTROID_POLY : PHFEM_COEFF_CONST;
 #define PHFEM_VOL(B, L, F, K) \
   PHFEM_LAUNCH(ctx, "k_volume", (k_volume<B, L, F, K><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)))
@@ -145,6 +145,7 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
     if (fk == PHFEM_FIELD_SINSIN) PHFEM_VOL_CK(B, L, PHFEM_FIELD_SINSIN);               \
     else if (fk == PHFEM_FIELD_EXP_SINSIN) PHFEM_VOL_CK(B, L, PHFEM_FIELD_EXP_SINSIN);  \
     else if (fk == PHFEM_FIELD_ZERO) PHFEM_VOL_CK(B, L, PHFEM_FIELD_ZERO);              \
+    else if (fk == kKindSamples) PHFEM_VOL_CK(B, L, kKindSamples);                       \
     else PHFEM_VOL_CK(B, L, kKindGeneric);                                               \
   } while (0)
   if (blocks && load) PHFEM_VOL_FK(true, true);
@@ -373,7 +374,7 @@ __device__ __forceinline__ void neu_entry(const NeuArgs& a, int64_t i, double t,
   const double dx = pb.x - pa.x, dy = pb.y - pa.y;
   const double length = sqrt(dx * dx + dy * dy);
   const double nx = dy / length, ny = -dx / length;
-  const double g = phfem_flux_eval(&a.g, midx, midy, nx, ny, t);
+  const double g = a.samples ? a.samples[i] : phfem_flux_eval(&a.g, midx, midy, nx, ny, t);
   if (!isfinite(g)) atomicMin(&err->flux_nan, (unsigned long long)i);
   const int led = a.ltp[e];
   const double lg = length * g;
@@ -442,7 +443,8 @@ void neu_table_free(phfem_ctx* ctx, NeuTable* tab) {
 
 phfem_status neu_table_eval(phfem_ctx* ctx, const NeuTable* tab, const phfem_mesh* mesh,
                             const phfem_topology* topo, const phfem_classification* cls,
-                            const phfem_field* g, double t, double* vals) {
+                            const phfem_field* g, double t, double* vals,
+                            const double* samples) {
   if (tab->nN == 0) return PHFEM_OK;
   NeuArgs a;
   a.coords = (const double2*)mesh->coords;
@@ -452,6 +454,7 @@ phfem_status neu_table_eval(phfem_ctx* ctx, const NeuTable* tab, const phfem_mes
   a.slot_of = tab->slot_of;
   a.nN = tab->nN;
   a.g = *g;
+  a.samples = samples;
   a.vals = vals;
   PHFEM_CUDA(ctx, cudaMemsetAsync(vals, 0, sizeof(double) * 3 * tab->cap, ctx->stream));
   PHFEM_LAUNCH(ctx, "k_neu_values", k_neu_values<<<tab->seq ? 1 : grid_for(tab->nN, 256, ctx->num_sms * 4), tab->seq ? 1 : 256, 0,
@@ -478,12 +481,12 @@ phfem_status neu_flux_error(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_
 
 phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                           const phfem_classification* cls, const phfem_field* g, double t,
-                          double* out, int accumulate, bool check) {
+                          double* out, int accumulate, bool check, const double* samples) {
   if (cls->nN == 0) return PHFEM_OK;
   NeuTable tab;
   PHFEM_TRY(neu_table_build(ctx, topo, cls, &tab));
   if (check) PHFEM_TRY(errors_reset(ctx));
-  PHFEM_TRY(neu_table_eval(ctx, &tab, mesh, topo, cls, g, t, tab.vals));
+  PHFEM_TRY(neu_table_eval(ctx, &tab, mesh, topo, cls, g, t, tab.vals, samples));
   PHFEM_LAUNCH(ctx, "k_neu_apply", k_neu_apply<<<grid_for(tab.cap, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
       tab.keys, tab.vals, tab.cap, out, accumulate));
   neu_table_free(ctx, &tab);
@@ -498,7 +501,7 @@ phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_to
 __global__ void k_dirichlet(const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
                             const int32_t* __restrict__ dir_ids, int nD,
                             const int32_t* __restrict__ rpos, phfem_field uD, double t,
-                            double* __restrict__ out) {
+                            double* __restrict__ out, const double* __restrict__ samples) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nD;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int e = dir_ids[i];
@@ -509,19 +512,20 @@ __global__ void k_dirichlet(const double2* __restrict__ coords, const int32_t* _
     const double midx = 0.5 * (pa.x + pb.x), midy = 0.5 * (pa.y + pb.y);
     const double dx = pb.x - pa.x, dy = pb.y - pa.y;
     const double length = sqrt(dx * dx + dy * dy);
-    out[pos] = -length * phfem_field_eval(&uD, midx, midy, t);  // assembly.cpp:239
+    const double u = samples ? samples[i] : phfem_field_eval(&uD, midx, midy, t);
+    out[pos] = -length * u;  // assembly.cpp:239
   }
 }
 
 phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                             const phfem_classification* cls, const phfem_field* uD, double t,
-                            double* out) {
+                            double* out, const double* samples) {
   if (cls->L > 0)
     PHFEM_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * cls->L, ctx->stream));
   if (cls->nD == 0) return PHFEM_OK;
   PHFEM_LAUNCH(ctx, "k_dirichlet", k_dirichlet<<<grid_for(cls->nD, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
       (const double2*)mesh->coords, topo->edge_nodes, cls->dirichlet_edge_ids, cls->nD,
-      cls->retained_pos, *uD, t, out));
+      cls->retained_pos, *uD, t, out, samples));
   return PHFEM_OK;
 }
 

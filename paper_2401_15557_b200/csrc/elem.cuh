@@ -15,6 +15,7 @@
 namespace phfem {
 
 constexpr int kKindGeneric = -1;
+constexpr int kKindSamples = -2;  // field values sampled on the host (drop-in std::function path)
 
 // phfem_geometry (assembly.cpp:17-27) with one reciprocal for the 6 divisions
 __device__ __forceinline__ phfem_geom geometry_dev(double x0, double y0, double x1, double y1,
@@ -105,14 +106,16 @@ __device__ __forceinline__ void convection_dev(const phfem_geom* g, const phfem_
 template <int FK>
 __device__ __forceinline__ void element_load_dev(double2 v0, double2 v1, double2 v2,
                                                  const phfem_field& f, double t, double bl[3],
-                                                 bool valid, int64_t m, phfem_dev_errors* err) {
+                                                 bool valid, int64_t m, phfem_dev_errors* err,
+                                                 const double* __restrict__ samples = nullptr) {
   const double mx[3] = {0.5 * (v1.x + v2.x), 0.5 * (v2.x + v0.x), 0.5 * (v0.x + v1.x)};
   const double my[3] = {0.5 * (v1.y + v2.y), 0.5 * (v2.y + v0.y), 0.5 * (v0.y + v1.y)};
   const double area = 0.5 * ((v1.x - v0.x) * (v2.y - v0.y) - (v1.y - v0.y) * (v2.x - v0.x));
   double fm[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    fm[i] = field_dev<FK>(f, mx[i], my[i], t);
+    if (FK == kKindSamples) fm[i] = valid ? samples[3 * m + i] : 0.0;
+    else fm[i] = field_dev<FK>(f, mx[i], my[i], t);
     if (valid && !isfinite(fm[i])) atomicMin(&err->load_nan, (unsigned long long)m);
   }
   const double w = div3(area) * 0.5;

@@ -19,6 +19,7 @@ struct VolArgs {
   double* M;
   double* M0;
   double* load;
+  const double* samples;  // host-sampled field values [3nE] (kind kKindSamples), else null
 };
 
 VolArgs make_vol_args(const phfem_mesh* mesh);
@@ -58,6 +59,7 @@ struct NeuArgs {
   const int32_t* slot_of;
   int nN;
   phfem_field g;
+  const double* samples;  // host-sampled flux values [nN] (drop-in std::function path), else null
   double* vals;
 };
 
@@ -73,15 +75,16 @@ phfem_status neu_table_build(phfem_ctx* ctx, const phfem_topology* topo,
 void neu_table_free(phfem_ctx* ctx, NeuTable* tab);
 phfem_status neu_table_eval(phfem_ctx* ctx, const NeuTable* tab, const phfem_mesh* mesh,
                             const phfem_topology* topo, const phfem_classification* cls,
-                            const phfem_field* g, double t, double* vals);
+                            const phfem_field* g, double t, double* vals,
+                            const double* samples = nullptr);
 phfem_status neu_flux_error(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                             const phfem_classification* cls);
 phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                           const phfem_classification* cls, const phfem_field* g, double t,
-                          double* out, int accumulate, bool check);
+                          double* out, int accumulate, bool check, const double* samples = nullptr);
 phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                             const phfem_classification* cls, const phfem_field* uD, double t,
-                            double* out);
+                            double* out, const double* samples = nullptr);
 phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
                                  const phfem_topology* topo, const phfem_classification* cls,
                                  phfem_csr* out);

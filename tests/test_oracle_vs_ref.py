@@ -30,13 +30,7 @@ CASES = meshes()
 
 
 def oracle_outputs(hm, coeffs, f, g, uD, t=0.0):
-    om, ot = O.build_topology(hm)
-    oc = O.classify_edges(om, ot)
-    B, D, M, M0 = O.assemble_volume(hm, coeffs)
-    C = O.assemble_constraint(om, ot, oc)
-    return {"topo": ot.arrays(), "cls": oc.arrays(), "B": B, "D": D, "M": M, "M0": M0, "C_csc": C["csc"],
-            "C_csr": C["csr"], "b": O.assemble_load(hm, f, t), "ln": O.assemble_neumann(om, ot, oc, g, t),
-            "bd": O.assemble_dirichlet(om, ot, oc, uD, t), "refined": O.red_refine(hm, ot)}
+    return O.all_outputs(hm, coeffs, f, g, uD, t)
 
 
 @pytest.mark.parametrize("name,hm", CASES, ids=[c[0] for c in CASES])
