@@ -335,6 +335,63 @@ phfem_status phfem_assemble_dirichlet_sampled(phfem_ctx* ctx, const phfem_mesh* 
                                               const phfem_classification* cls,
                                               const double* samples, double* out);
 
+/* ---- multi-GPU (host orchestration paper_2401_15557_b200/dist.py)
+ * Elements are split into contiguous ranges, max nodes into contiguous key
+ * ranges (so every rank owns a contiguous range of canonical edge ids).
+ * Not in the reference (single-threaded); the concatenation of the ranks'
+ * outputs equals the single-GPU outputs bit for bit.
+ *
+ * Directed occurrences of elements [elo, ehi) as records {max, min, 3m+s,
+ * dir}, grouped by the rank owning the max node (splits [W+1], device):
+ * counts[W] always; with send != NULL also offsets[W+1] and the records. */
+phfem_status phfem_dist_occurrences(phfem_ctx* ctx, const int32_t* elements, int32_t elo,
+                                    int32_t ehi, const int32_t* splits, int32_t W, int32_t* counts,
+                                    int32_t* offsets, int32_t* send);
+/* red_refine of the rank's elements (local arrays [n][3] + their elem_edge):
+ * children 4m..4m+3 (refine.cpp:28-37) -> children[4n][3]; the midpoints of
+ * a range of edges (refine.cpp:16-19) -> out[E][2] (all-gathered by dist.py) */
+phfem_status phfem_dist_children(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                 int32_t n, int32_t nC, int32_t* children);
+phfem_status phfem_dist_midpoints(phfem_ctx* ctx, const double* coords, const int32_t* edge_nodes,
+                                  int32_t E, double* out);
+/* build_topology of the records of one max-node range [node_lo, node_hi):
+ * out gets the range's edges (rank-local ids, global node / element ids),
+ * node_edge_start for the range's nodes; pairs[2E][2] the (element slot
+ * 3m+l, edge or ~edge) of every occurrence (slot -1 = none) instead of
+ * elem_edge.                                                                */
+phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n, int32_t node_lo,
+                              int32_t node_hi, int32_t nC_all, int32_t nE_all, phfem_topology* out,
+                              int32_t* pairs);
+/* pairs -> global edge ids (+E0) routed to the element owner (esplits[W+1]);
+ * the receiver writes them into its elem_edge ([3(ehi-elo)]).              */
+phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pairs, int64_t n, int32_t E0,
+                                    const int32_t* esplits, int32_t W, int32_t* counts,
+                                    int32_t* offsets, int32_t* send);
+phfem_status phfem_dist_apply_pairs(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t elo,
+                                    int32_t* elem_edge);
+/* a[i] += off (only_nonneg: where a[i] >= 0) — re-basing local ids         */
+phfem_status phfem_dist_add_offset(phfem_ctx* ctx, int32_t* a, int64_t n, int32_t off,
+                                   int only_nonneg);
+/* boundary pairs (global list, positions list_base..) whose max node this
+ * rank owns -> global edge ids (else -1); the first error as (position << 2
+ * | 0 not an edge / 1 interior) via atomicMin on *err (init ~0).            */
+phfem_status phfem_dist_resolve(phfem_ctx* ctx, const phfem_topology* part, int32_t node_lo,
+                                int32_t E0, const int32_t* pairs, int32_t n, int32_t list_base,
+                                int32_t* ids, unsigned long long* err);
+/* classification of the rank's edges from the global Dirichlet / Neumann id
+ * lists: rank-local retained_pos / retained_edges / id lists / bitmap.      */
+phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                 const int32_t* dir_ids, int32_t nD, const int32_t* neu_ids,
+                                 int32_t nN, phfem_classification* out);
+/* Neumann edges: the owner writes rows {a, b, t_plus, led} of table[nN][4]
+ * (others zero; a sum all-reduce completes it), then every rank adds the
+ * Neumann load of its elements [elo, ehi) to its local load vector.         */
+phfem_status phfem_dist_neumann_table(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                      const int32_t* neu_ids, int32_t nN, int32_t* table);
+phfem_status phfem_dist_neumann_apply(phfem_ctx* ctx, const phfem_mesh* mesh, const int32_t* table,
+                                      int32_t nN, int32_t dup, int32_t elo, int32_t ehi,
+                                      const phfem_field* g, double t, double* load_local);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

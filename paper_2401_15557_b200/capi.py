@@ -147,6 +147,9 @@ EXPORTED = [
     "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level", "phfem_selftest_fastmath",
     "phfem_topology_derive", "phfem_topology_tables", "phfem_field_points", "phfem_edge_lengths",
     "phfem_assemble_load_sampled", "phfem_assemble_neumann_sampled", "phfem_assemble_dirichlet_sampled",
+    "phfem_dist_occurrences", "phfem_dist_dedup", "phfem_dist_route_pairs", "phfem_dist_apply_pairs",
+    "phfem_dist_add_offset", "phfem_dist_resolve", "phfem_dist_classify", "phfem_dist_neumann_table",
+    "phfem_dist_neumann_apply", "phfem_dist_children", "phfem_dist_midpoints",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -223,6 +226,19 @@ def load_library(path: str = LIB_PATH):
                                          C.c_int, vp]),
         "phfem_assemble_load_sampled": (C.c_int, [vp, P(phfem_mesh), vp, vp]),
         "phfem_edge_lengths": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), vp]),
+        "phfem_dist_occurrences": (C.c_int, [vp, vp, i32, i32, vp, i32, vp, vp, vp]),
+        "phfem_dist_children": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+        "phfem_dist_midpoints": (C.c_int, [vp, vp, vp, i32, vp]),
+        "phfem_dist_dedup": (C.c_int, [vp, vp, i64, i32, i32, i32, i32, P(phfem_topology), vp]),
+        "phfem_dist_route_pairs": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp]),
+        "phfem_dist_apply_pairs": (C.c_int, [vp, vp, i64, i32, vp]),
+        "phfem_dist_add_offset": (C.c_int, [vp, vp, i64, i32, C.c_int]),
+        "phfem_dist_resolve": (C.c_int, [vp, P(phfem_topology), i32, i32, vp, i32, i32, vp, vp]),
+        "phfem_dist_classify": (C.c_int, [vp, P(phfem_topology), i32, vp, i32, vp, i32,
+                                          P(phfem_classification)]),
+        "phfem_dist_neumann_table": (C.c_int, [vp, P(phfem_topology), i32, vp, i32, vp]),
+        "phfem_dist_neumann_apply": (C.c_int, [vp, P(phfem_mesh), vp, i32, i32, i32, i32, P(phfem_field),
+                                               dbl, vp]),
         "phfem_assemble_neumann_sampled": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology),
                                                      P(phfem_classification), vp, vp, C.c_int]),
         "phfem_assemble_dirichlet_sampled": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology),

@@ -132,6 +132,25 @@ PHFEM_API void phfem_classification_release(phfem_ctx* ctx, phfem_classification
 }
 
 namespace phfem {
+// per-1024-edge-block (boundary, Neumann) prefixes from the Neumann bitmap and
+// the ascending boundary list; with_retained also retained_pos / _edges
+static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topology* topo,
+                                              phfem_classification* out, int nblk,
+                                              bool with_retained) {
+  const int E = topo->E;
+  int32_t* pre_bnd = out->block_prefix;
+  int32_t* pre_neu = out->block_prefix + nblk + 1;
+  PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
+      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, pre_bnd, pre_neu));
+  PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
+  PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
+  if (nblk > 0 && with_retained) {
+    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
+                                                         out->retained_pos, out->retained_edges));
+  }
+  return PHFEM_OK;
+}
+
 // Boundary pairs -> ids, the Neumann bitmap and the per-block prefixes; with
 // with_retained also retained_pos / retained_edges (else the caller wrote them
 // and allocated out->retained_pos / retained_edges already).
@@ -160,18 +179,9 @@ phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const ph
         topo->edge_elements, topo->nC, out->dirichlet_edge_ids, out->neumann_edge_ids,
         out->neumann_bits, ctx->derr));
   }
-  int32_t* pre_bnd = out->block_prefix;
-  int32_t* pre_neu = out->block_prefix + nblk + 1;
-  PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
-      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, pre_bnd, pre_neu));
-  PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
-  PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
-  if (nblk > 0 && with_retained) {
-    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
-                                                         out->retained_pos, out->retained_edges));
-  }
+  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, with_retained));
   // total Neumann count rides back with the error words (one sync)
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[8], pre_neu + nblk, sizeof(int32_t),
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[8], out->block_prefix + nblk + 1 + nblk, sizeof(int32_t),
                                   cudaMemcpyDeviceToDevice, ctx->stream));
   PHFEM_TRY(errors_fetch(ctx));
   const uint64_t ce = ctx->herr->classify;
@@ -191,6 +201,26 @@ phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const ph
   }
   out->L = E - (int32_t)(ctx->herr->counters[8] & 0xffffffffu);
   out->flags = ctx->herr->counters[5] ? PHFEM_CLS_DUP_NEUMANN : 0;
+  return PHFEM_OK;
+}
+}  // namespace phfem
+
+namespace phfem {
+// Distributed ranks (dist.cu): the Neumann bitmap and the owned id lists are
+// set; block prefixes, retained_pos / retained_edges and L follow.
+phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo,
+                                      phfem_classification* out) {
+  const int E = topo->E;
+  const int nblk = (E + kEdgeBlock - 1) / kEdgeBlock;
+  PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
+  PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
+  PHFEM_TRY(dalloc(ctx, &out->block_prefix, 2 * ((int64_t)nblk + 1)));
+  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, true));
+  int32_t nneu = 0;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&nneu, out->block_prefix + nblk + 1 + nblk, sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  out->L = E - nneu;
   return PHFEM_OK;
 }
 }  // namespace phfem

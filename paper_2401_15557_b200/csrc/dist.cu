@@ -1,0 +1,434 @@
+// dist.cu — device side of the multi-GPU pipeline (host side in
+// paper_2401_15557_b200/dist.py).  Elements are partitioned by contiguous
+// ranges, nodes (and so edges, which are grouped by max node) by contiguous
+// key ranges.  Per-element work needs no communication; the edge dedup is one
+// key-range all-to-all of directed occurrences, a local sort (the single-GPU
+// tile machinery of edge_gen.cu, phfem_dist_dedup) and a reverse all-to-all
+// of (element slot, edge id) pairs.  The kernels here produce and consume the
+// exchange buffers and re-base rank-local ids to global ones, so the
+// concatenation of the ranks' outputs is bit-identical to the single-GPU run.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace phfem {
+
+__device__ __forceinline__ int dest_of(const int32_t* __restrict__ splits, int W, int v) {
+  int lo = 0, hi = W;  // last r with splits[r] <= v
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(splits + mid) <= v) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// directed occurrences of elements [elo, ehi) (elements: the rank's local
+// array): slot s of element m is v_s -> v_{s+1} (edge_topology.cpp:61-68);
+// record {max, min, 3m+s, dir}
+__global__ void k_dist_occ(const int32_t* __restrict__ elements, int elo, int ehi,
+                           const int32_t* __restrict__ splits, int W, int32_t* __restrict__ cnt,
+                           int32_t* __restrict__ cursor, int4* __restrict__ send) {
+  const int64_t n = 3 * (int64_t)(ehi - elo);
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    int a = 0, b = 0, d = -1;
+    int64_t occ = 0;
+    if (valid) {
+      const int64_t ml = i / 3;
+      const int s = (int)(i % 3);
+      occ = 3 * (elo + ml) + s;
+      a = elements[3 * ml + s];
+      b = elements[3 * ml + (s + 1) % 3];
+      d = dest_of(splits, W, max(a, b));
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(grp) - 1;
+    if (!send) {
+      if (valid && (int)lane_id() == leader) atomicAdd(&cnt[d], __popc(grp));
+      continue;
+    }
+    int base = 0;
+    if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[d], __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid)
+      send[base + __popc(grp & lanemask_lt())] = make_int4(max(a, b), min(a, b), (int)occ, a > b ? 1 : 0);
+  }
+}
+
+// pairs (slot 3m+l, local edge or ~local edge) -> global edge ids, routed to
+// the element owner; slot < 0 marks "no t_minus"
+__global__ void k_dist_pairs(const int2* __restrict__ pairs, int64_t n, int E0,
+                             const int32_t* __restrict__ esplits, int W, int32_t* __restrict__ cnt,
+                             int32_t* __restrict__ cursor, int2* __restrict__ send) {
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int2 p = make_int2(-1, 0);
+    if (i < n) p = pairs[i];
+    const bool valid = p.x >= 0;
+    const int d = valid ? dest_of(esplits, W, p.x / 3) : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(grp) - 1;
+    if (!send) {
+      if (valid && (int)lane_id() == leader) atomicAdd(&cnt[d], __popc(grp));
+      continue;
+    }
+    int base = 0;
+    if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[d], __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) {
+      const int v = p.y >= 0 ? p.y + E0 : ~(~p.y + E0);
+      send[base + __popc(grp & lanemask_lt())] = make_int2(p.x, v);
+    }
+  }
+}
+
+__global__ void k_dist_apply(const int2* __restrict__ recv, int64_t n, int elo,
+                             int32_t* __restrict__ elem_edge) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 p = recv[i];
+    elem_edge[p.x - 3 * (int64_t)elo] = p.y;
+  }
+}
+
+__global__ void k_add_offset(int32_t* __restrict__ a, int64_t n, int32_t off, int only_nonneg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = a[i];
+    if (!only_nonneg || v >= 0) a[i] = v + off;
+  }
+}
+
+// boundary pairs whose max node lies in [nlo, nhi): global id, or the
+// reference's errors (edge_topology.cpp:151-157) keyed by list position
+__global__ void k_dist_resolve(const int32_t* __restrict__ pairs, int n, int list,
+                               const int32_t* __restrict__ nes, const int32_t* __restrict__ edge_nodes,
+                               const int32_t* __restrict__ edge_elements, int nlo, int nhi, int E0,
+                               int32_t* __restrict__ ids, unsigned long long* __restrict__ err) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = pairs[2 * i], b = pairs[2 * i + 1];
+    const int hi = max(a, b), lo = min(a, b);
+    ids[i] = -1;
+    if (hi < nlo || hi >= nhi) continue;
+    int e = -1;
+    if (lo >= 0) {
+      // edges of max node hi (ascending min); nes holds global ids (re-based)
+      const int end = nes[hi - nlo + 1] - E0;
+      int l = nes[hi - nlo] - E0, r = end;
+      while (l < r) {
+        const int mid = (l + r) >> 1;
+        const int x = edge_nodes[2 * mid], y = edge_nodes[2 * mid + 1];
+        if (min(x, y) < lo) l = mid + 1;
+        else r = mid;
+      }
+      if (l < end && min(edge_nodes[2 * l], edge_nodes[2 * l + 1]) == lo) e = l;
+    }
+    // error key: (global list position << 2) | code (0 not an edge, 1 interior)
+    const unsigned long long pos = (unsigned long long)(list + i);
+    if (e < 0) atomicMin(err, pos << 2);
+    else if (edge_elements[2 * e + 1] >= 0) atomicMin(err, (pos << 2) | 1ull);
+    else ids[i] = E0 + e;
+  }
+}
+
+// Neumann flags of the local edges from the global Neumann id list
+__global__ void k_dist_neu_bits(const int32_t* __restrict__ neu_ids, int nN, int E0, int E,
+                                uint32_t* __restrict__ bits, unsigned long long* __restrict__ dup) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nN; i += gridDim.x * blockDim.x) {
+    const int e = neu_ids[i] - E0;
+    if (e < 0 || e >= E) continue;
+    const uint32_t bit = 1u << (e & 31);
+    if (atomicOr(&bits[e >> 5], bit) & bit) *dup = 1;
+  }
+}
+
+// local ids of the listed edges in [E0, E0 + E), list order kept
+__global__ void k_dist_local_ids(const int32_t* __restrict__ ids, int n, int E0, int E,
+                                 int32_t* __restrict__ flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int e = ids[i] - E0;
+    flag[i] = (e >= 0 && e < E) ? 1 : 0;
+  }
+}
+__global__ void k_dist_compact(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
+                               int n, int E0, int E, int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int e = ids[i] - E0;
+    if (e >= 0 && e < E) out[pos[i]] = e;
+  }
+}
+
+// Neumann edge table rows {a, b, t_plus, led} for the local Neumann edges
+__global__ void k_dist_neu_table(const int32_t* __restrict__ neu_ids, int nN, int E0, int E,
+                                 const int32_t* __restrict__ edge_nodes,
+                                 const int32_t* __restrict__ edge_elements,
+                                 const int32_t* __restrict__ ltp, int32_t* __restrict__ table) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nN; i += gridDim.x * blockDim.x) {
+    const int e = neu_ids[i] - E0;
+    if (e < 0 || e >= E) continue;
+    table[4 * i] = edge_nodes[2 * e];
+    table[4 * i + 1] = edge_nodes[2 * e + 1];
+    table[4 * i + 2] = edge_elements[2 * e];
+    table[4 * i + 3] = ltp[e];
+  }
+}
+
+// mini topology of the Neumann edges whose t_plus element is local: edge i
+// of the table keeps id i; the Neumann list is the owned positions in order
+__global__ void k_dist_neu_mini(const int32_t* __restrict__ table, int nN, int elo, int ehi,
+                                int32_t* __restrict__ en, int32_t* __restrict__ el,
+                                int32_t* __restrict__ ltp, int32_t* __restrict__ flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nN; i += gridDim.x * blockDim.x) {
+    en[2 * i] = table[4 * i];
+    en[2 * i + 1] = table[4 * i + 1];
+    el[2 * i] = table[4 * i + 2] - elo;  // local element: the load array is local
+    el[2 * i + 1] = -1;
+    ltp[i] = table[4 * i + 3];
+    flag[i] = (table[4 * i + 2] >= elo && table[4 * i + 2] < ehi) ? 1 : 0;
+  }
+}
+__global__ void k_dist_iota_compact(const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
+                                    int n, int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = i;
+}
+
+// midpoints 0.5 (c[a] + c[b]) of a range of edges (refine.cpp:16-19)
+__global__ void k_dist_midpoints(const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
+                                 int E, double2* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pa = coords[edge_nodes[2 * e]], pb = coords[edge_nodes[2 * e + 1]];
+    out[e] = make_double2(0.5 * (pa.x + pb.x), 0.5 * (pa.y + pb.y));
+  }
+}
+
+// children 4m..4m+3 of the local elements (refine.cpp:28-37)
+__global__ void k_dist_children(const int32_t* __restrict__ elements, const int32_t* __restrict__ elem_edge,
+                                int n, int nc, int4* __restrict__ out) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int p0 = elements[3 * m], p1 = elements[3 * m + 1], p2 = elements[3 * m + 2];
+    const int s0 = elem_edge[3 * m], s1 = elem_edge[3 * m + 1], s2 = elem_edge[3 * m + 2];
+    const int m0 = nc + (s0 >= 0 ? s0 : ~s0), m1 = nc + (s1 >= 0 ? s1 : ~s1), m2 = nc + (s2 >= 0 ? s2 : ~s2);
+    int4* o = out + 3 * m;
+    o[0] = make_int4(m0, m1, m2, p0);
+    o[1] = make_int4(m2, m1, p1, m0);
+    o[2] = make_int4(m2, p2, m1, m0);
+  }
+}
+
+}  // namespace phfem
+
+using namespace phfem;
+
+PHFEM_API phfem_status phfem_dist_midpoints(phfem_ctx* ctx, const double* coords,
+                                            const int32_t* edge_nodes, int32_t E, double* out) {
+  if (!ctx || (E && (!coords || !edge_nodes || !out))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (E > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_midpoints", k_dist_midpoints<<<grid_for(E, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        (const double2*)coords, edge_nodes, E, (double2*)out));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_children(phfem_ctx* ctx, const int32_t* elements,
+                                           const int32_t* elem_edge, int32_t n, int32_t nC,
+                                           int32_t* children) {
+  if (!ctx || (n && (!elements || !elem_edge || !children))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_children", k_dist_children<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        elements, elem_edge, n, nC, reinterpret_cast<int4*>(children)));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_occurrences(phfem_ctx* ctx, const int32_t* elements, int32_t elo,
+                                              int32_t ehi, const int32_t* splits, int32_t W,
+                                              int32_t* counts, int32_t* offsets, int32_t* send) {
+  if (!ctx || !splits || !counts || W < 1 || elo < 0 || ehi < elo || (ehi > elo && !elements))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
+  const int64_t n = 3 * (int64_t)(ehi - elo);
+  const int grid = grid_for(n, 256, ctx->num_sms * 8);
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, 256, 0, ctx->stream>>>(
+        elements, elo, ehi, splits, W, counts, nullptr, nullptr));
+  if (!send) return PHFEM_OK;
+  if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
+  int32_t* cursor = nullptr;
+  PHFEM_TRY(dalloc(ctx, &cursor, (int64_t)W + 1));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, counts, sizeof(int32_t) * W, cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(cursor + W, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_TRY(scan_exclusive_i32(ctx, cursor, cursor, (int64_t)W + 1, nullptr));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, 256, 0, ctx->stream>>>(
+        elements, elo, ehi, splits, W, nullptr, cursor, reinterpret_cast<int4*>(send)));
+  dfree(ctx, cursor);
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pairs, int64_t n,
+                                              int32_t E0, const int32_t* esplits, int32_t W,
+                                              int32_t* counts, int32_t* offsets, int32_t* send) {
+  if (!ctx || (!pairs && n) || !esplits || !counts || W < 1) return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
+  const int grid = grid_for(n, 256, ctx->num_sms * 8);
+  const int2* p2 = reinterpret_cast<const int2*>(pairs);
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, 256, 0, ctx->stream>>>(
+        p2, n, E0, esplits, W, counts, nullptr, nullptr));
+  if (!send) return PHFEM_OK;
+  if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
+  int32_t* cursor = nullptr;
+  PHFEM_TRY(dalloc(ctx, &cursor, (int64_t)W + 1));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, counts, sizeof(int32_t) * W, cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(cursor + W, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_TRY(scan_exclusive_i32(ctx, cursor, cursor, (int64_t)W + 1, nullptr));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, 256, 0, ctx->stream>>>(
+        p2, n, E0, esplits, W, nullptr, cursor, reinterpret_cast<int2*>(send)));
+  dfree(ctx, cursor);
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_apply_pairs(phfem_ctx* ctx, const int32_t* recv, int64_t n,
+                                              int32_t elo, int32_t* elem_edge) {
+  if (!ctx || (n && (!recv || !elem_edge))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_apply", k_dist_apply<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const int2*>(recv), n, elo, elem_edge));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_add_offset(phfem_ctx* ctx, int32_t* a, int64_t n, int32_t off,
+                                             int only_nonneg) {
+  if (!ctx || (n && !a)) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0 && off != 0)
+    PHFEM_LAUNCH(ctx, "k_add_offset", k_add_offset<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        a, n, off, only_nonneg));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_resolve(phfem_ctx* ctx, const phfem_topology* part,
+                                          int32_t node_lo, int32_t E0, const int32_t* pairs,
+                                          int32_t n, int32_t list_base, int32_t* ids,
+                                          unsigned long long* err) {
+  if (!ctx || !part || (n && (!pairs || !ids || !err))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_resolve", k_dist_resolve<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        pairs, n, list_base, part->node_edge_start, part->edge_nodes, part->edge_elements, node_lo,
+        node_lo + part->nC, E0, ids, err));
+  return PHFEM_OK;
+}
+
+namespace phfem {
+phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo,
+                                      phfem_classification* out);
+}
+
+PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                           const int32_t* dir_ids, int32_t nD,
+                                           const int32_t* neu_ids, int32_t nN,
+                                           phfem_classification* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !part) return PHFEM_ERR_INVALID_ARGUMENT;
+  const int E = part->E;
+  const int nwords = (E + 31) / 32;
+  out->E = E;
+  PHFEM_TRY(dalloc(ctx, &out->neumann_bits, nwords));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->neumann_bits, 0, sizeof(uint32_t) * std::max(nwords, 1), ctx->stream));
+  unsigned long long* dup = nullptr;
+  PHFEM_TRY(dalloc(ctx, &dup, 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(dup, 0, sizeof(unsigned long long), ctx->stream));
+  if (nN > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_neu_bits", k_dist_neu_bits<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        neu_ids, nN, E0, E, out->neumann_bits, dup));
+  // local Dirichlet / Neumann id lists (owned entries, list order)
+  auto compact = [&](const int32_t* ids, int n, int32_t** dst, int32_t* count) -> phfem_status {
+    int32_t* flag = nullptr;
+    PHFEM_TRY(dalloc(ctx, &flag, (int64_t)n + 1));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int32_t) * (n + 1), ctx->stream));
+    if (n > 0)
+      PHFEM_LAUNCH(ctx, "k_dist_local_ids", k_dist_local_ids<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+          ids, n, E0, E, flag));
+    PHFEM_TRY(scan_exclusive_i32(ctx, flag, flag, (int64_t)n + 1, nullptr));
+    int32_t c = 0;
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&c, flag + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    PHFEM_TRY(dalloc(ctx, dst, c));
+    if (n > 0)
+      PHFEM_LAUNCH(ctx, "k_dist_compact", k_dist_compact<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+          ids, flag, n, E0, E, *dst));
+    *count = c;
+    dfree(ctx, flag);
+    return PHFEM_OK;
+  };
+  PHFEM_TRY(compact(dir_ids, nD, &out->dirichlet_edge_ids, &out->nD));
+  PHFEM_TRY(compact(neu_ids, nN, &out->neumann_edge_ids, &out->nN));
+  unsigned long long hdup = 0;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&hdup, dup, sizeof hdup, cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, dup);
+  out->flags = hdup ? PHFEM_CLS_DUP_NEUMANN : 0;
+  return classify_lists_from_bits(ctx, part, out);
+}
+
+PHFEM_API phfem_status phfem_dist_neumann_table(phfem_ctx* ctx, const phfem_topology* part,
+                                                int32_t E0, const int32_t* neu_ids, int32_t nN,
+                                                int32_t* table) {
+  if (!ctx || !part || (nN && (!neu_ids || !table))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (nN == 0) return PHFEM_OK;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(table, 0, sizeof(int32_t) * 4 * (int64_t)nN, ctx->stream));
+  PHFEM_LAUNCH(ctx, "k_dist_neu_table", k_dist_neu_table<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      neu_ids, nN, E0, part->E, part->edge_nodes, part->edge_elements, part->local_in_tplus, table));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_neumann_apply(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                                const int32_t* table, int32_t nN, int32_t dup,
+                                                int32_t elo, int32_t ehi, const phfem_field* g,
+                                                double t, double* load_local) {
+  if (!ctx || !mesh || !g || (nN && (!table || !load_local))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (nN == 0) return PHFEM_OK;
+  phfem_topology mt;
+  memset(&mt, 0, sizeof mt);
+  phfem_classification mc;
+  memset(&mc, 0, sizeof mc);
+  int32_t *flag = nullptr, *pos = nullptr;
+  PHFEM_TRY(dalloc(ctx, &mt.edge_nodes, 2 * (int64_t)nN));
+  PHFEM_TRY(dalloc(ctx, &mt.edge_elements, 2 * (int64_t)nN));
+  PHFEM_TRY(dalloc(ctx, &mt.local_in_tplus, nN));
+  PHFEM_TRY(dalloc(ctx, &flag, nN));
+  PHFEM_TRY(dalloc(ctx, &pos, (int64_t)nN + 1));
+  PHFEM_LAUNCH(ctx, "k_dist_neu_mini", k_dist_neu_mini<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+      table, nN, elo, ehi, mt.edge_nodes, mt.edge_elements, mt.local_in_tplus, flag));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(pos, flag, sizeof(int32_t) * nN, cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(pos + nN, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_TRY(scan_exclusive_i32(ctx, pos, pos, (int64_t)nN + 1, nullptr));
+  int32_t c = 0;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&c, pos + nN, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  phfem_status st = PHFEM_OK;
+  if (c > 0) {
+    PHFEM_TRY(dalloc(ctx, &mc.neumann_edge_ids, c));
+    PHFEM_LAUNCH(ctx, "k_dist_iota_compact", k_dist_iota_compact<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        flag, pos, nN, mc.neumann_edge_ids));
+    mt.E = nN;
+    mc.nN = c;
+    mc.E = nN;
+    mc.flags = dup ? PHFEM_CLS_DUP_NEUMANN : 0;
+    // coordinates global, load array and the mini topology's elements local
+    st = neumann_into(ctx, mesh, &mt, &mc, g, t, load_local, 1, true);
+    dfree(ctx, mc.neumann_edge_ids);
+  }
+  dfree(ctx, flag);
+  dfree(ctx, pos);
+  dfree(ctx, mt.edge_nodes);
+  dfree(ctx, mt.edge_elements);
+  dfree(ctx, mt.local_in_tplus);
+  return st;
+}

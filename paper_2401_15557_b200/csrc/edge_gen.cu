@@ -27,9 +27,10 @@
 namespace phfem {
 
 struct EgParams {
-  int32_t nC, nE;
+  int32_t nC, nE;  // nodes of the key range (local), elements of the mesh
   int lo_bits, occ_bits, total_bits, bs;
   int nb;
+  int32_t node_base;  // first max node of the range (0 for a whole mesh)
 };
 
 static int bits_for(int64_t max_value) {  // bits to represent 0..max_value
@@ -108,6 +109,52 @@ __global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ 
   }
 }
 
+// A'/C' for the distributed dedup: the occurrences arrive as records
+// {max node, min node, occurrence 3m+s, dir} of one max-node key range
+// (dist.py's key-range all-to-all) instead of being read from elements.
+__global__ void __launch_bounds__(256) k_rec_count(const int4* __restrict__ recs, int64_t n,
+                                                   EgParams P, int32_t* __restrict__ bcount,
+                                                   phfem_dev_errors* err) {
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    bool ok = i < n;
+    int hl = 0;
+    if (ok) {
+      const int4 r = recs[i];
+      hl = r.x - P.node_base;
+      if (hl < 0 || hl >= P.nC) {
+        atomicMin(&err->misc, (unsigned long long)i);
+        ok = false;
+      }
+    }
+    const unsigned key = ok ? ((unsigned)hl >> P.bs) : 0xffffffffu;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (ok && lane_id() == (unsigned)(__ffs(grp) - 1)) atomicAdd(&bcount[key], __popc(grp));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rec_scatter(const int4* __restrict__ recs, int64_t n,
+                                                     EgParams P, int32_t* __restrict__ cursor,
+                                                     uint64_t* __restrict__ items) {
+  const uint32_t hl_mask = (1u << P.bs) - 1u;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    int4 r = make_int4(0, 0, 0, 0);
+    if (valid) r = recs[i];
+    const int hl = r.x - P.node_base;
+    const unsigned key = valid ? ((unsigned)hl >> P.bs) : 0xffffffffu;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid)
+      items[base + __popc(grp & lanemask_lt())] =
+          eg_pack(P, (uint32_t)hl & hl_mask, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w);
+  }
+}
+
 // D ------------------------------------------------------------------------
 struct EgOut {
   int32_t* edge_nodes;
@@ -118,6 +165,8 @@ struct EgOut {
   int32_t* boundary;
   int32_t* elem_edge;
   int32_t* node_edge_start;
+  int2* pairs;  // non-null: (slot 3m+l, edge or ~edge) per occurrence instead of elem_edge
+  int32_t node_base;
 };
 
 // Edge record of the sort pass (one per unique edge, at a tile-local slot of
@@ -233,7 +282,7 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
     int len = 1;
     while (p + len < en && ((buf2[p + len] >> lo_shift) & lo_mask) == lo) ++len;
     if (len > 2 || (len == 2 && ((f ^ buf2[p + 1]) & 1ull) == 0)) {
-      const uint64_t v = (uint64_t)tile * kTileNodes + nd;
+      const uint64_t v = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + nd;
       atomicMin(&err->topo, (v << 33) | (lo << 2) | (len > 2 ? 0ull : (2ull | (f & 1ull))));
     }
     ++ne_i;
@@ -353,7 +402,7 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
         third = partner && pos + 2 < en && ((sm.buf2[pos + 2] >> (ob + 1)) & lomask) == lo;
       }
       if (start && (third || (partner && ((f ^ g) & 1ull) == 0))) {
-        const uint64_t v = (uint64_t)tile * kTileNodes + nd;
+        const uint64_t v = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + nd;
         atomicMin(&err->topo, (v << 33) | (lo << 2) | (third ? 0ull : (2ull | (f & 1ull))));
       }
       if (start) atomicAdd(&sm.nedge[nd], 1);
@@ -490,7 +539,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
   if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
   // one record per thread, 4 in flight: no scan (records carry their
   // tile-local boundary prefix)
-  const int64_t vbase = (int64_t)tile * kTileNodes;
+  const int64_t vbase = (int64_t)out.node_base + (int64_t)tile * kTileNodes;
   for (int i0 = threadIdx.x; i0 < ne; i0 += 4 * kEmitThreads) {
     int4 r[4];
 #pragma unroll
@@ -511,18 +560,21 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
       const int l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
       reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(v, r[u].y) : make_int2(r[u].y, v);
       out.ltp[e] = l_f;
-      out.elem_edge[3 * (int64_t)m_f + l_f] = e;
+      if (out.pairs) out.pairs[2 * (int64_t)e] = make_int2(3 * m_f + l_f, e);
+      else out.elem_edge[3 * (int64_t)m_f + l_f] = e;
       if (r[u].w >= 0) {
         const uint32_t occ_g = (uint32_t)r[u].w;
         const int m_g = (int)(occ_g / 3u);
         const int l_g = (int)((occ_g % 3u + 2u) % 3u);
         reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
         out.ltm[e] = l_g;
-        out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+        if (out.pairs) out.pairs[2 * (int64_t)e + 1] = make_int2(3 * m_g + l_g, ~e);
+        else out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
         out.interior[e - bpos] = e;
       } else {
         reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
         out.ltm[e] = -1;
+        if (out.pairs) out.pairs[2 * (int64_t)e + 1] = make_int2(-1, 0);
         out.boundary[bpos] = e;
       }
     }
@@ -556,31 +608,17 @@ PHFEM_API void phfem_topology_release(phfem_ctx* ctx, phfem_topology* t) {
   t->E = t->n_interior = t->n_boundary = 0;
 }
 
-PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* mesh,
-                                            phfem_topology* out) {
-  memset(out, 0, sizeof(*out));
-  if (!ctx || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
-  if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "set device");
-  const int64_t nE = mesh->nE, nC = mesh->nC;
-  if (nE < 0 || nC < 0 || 3 * nE >= (int64_t(1) << 31))
-    return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: mesh too large for int ids");
-  out->nC = (int32_t)nC;
-  out->nE = (int32_t)nE;
+namespace phfem {
 
-  EgParams P;
-  P.nC = (int32_t)nC;
-  P.nE = (int32_t)nE;
-  P.lo_bits = bits_for(std::max<int64_t>(nC - 1, 1));
-  P.occ_bits = bits_for(std::max<int64_t>(3 * nE - 1, 1));
-  P.total_bits = P.lo_bits + P.occ_bits + 1;
-  P.bs = std::min(8, 64 - P.total_bits);
-  if (P.bs < 1) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: ids too wide");
-  const int NB = 1 << P.bs;
-  P.nb = (int)((nC + NB - 1) / NB);
-  if (P.nb < 1) P.nb = 1;
-  const int64_t nd = 3 * nE;
+// Sort -> records -> emit over nd occurrences of one max-node key range
+// (the whole mesh for build_topology, one rank's range for the distributed
+// dedup).  source(kind, ...) launches the histogram (kind 0) or the scatter
+// (kind 1) of the occurrences into the bucket array.
+template <typename Source>
+static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source source,
+                            phfem_topology* out, int2* pairs, const char* who) {
+  const int64_t nC = P.nC;
   const int64_t cap_e = std::max<int64_t>(nd, 1);
-
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
   PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * cap_e));
   PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * cap_e));
@@ -588,27 +626,25 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   PHFEM_TRY(dalloc(ctx, &out->local_in_tminus, cap_e));
   PHFEM_TRY(dalloc(ctx, &out->interior_edges, cap_e / 2 + 1));
   PHFEM_TRY(dalloc(ctx, &out->boundary_edges, cap_e));
-  PHFEM_TRY(dalloc(ctx, &out->elem_edge, cap_e));
-  if (nE == 0) {
+  if (!pairs) PHFEM_TRY(dalloc(ctx, &out->elem_edge, cap_e));
+  if (nd == 0) {
     PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * (nC + 1), ctx->stream));
     return PHFEM_OK;
   }
 
   PHFEM_TRY(errors_reset(ctx));
   int32_t *bcount = nullptr, *boff = nullptr, *tiles = nullptr;
-  const int ntiles_h = (int)((nC + kTileNodes - 1) / kTileNodes);
+  const int ntiles = (int)((nC + kTileNodes - 1) / kTileNodes);
   PHFEM_TRY(dalloc(ctx, &bcount, (int64_t)P.nb + 1));
   PHFEM_TRY(dalloc(ctx, &boff, (int64_t)P.nb + 1));
-  PHFEM_TRY(dalloc(ctx, &tiles, 2 * ((int64_t)ntiles_h + 1)));
+  PHFEM_TRY(dalloc(ctx, &tiles, 2 * ((int64_t)ntiles + 1)));
   int32_t* tileE = tiles;
-  int32_t* tileB = tiles + ntiles_h + 1;
+  int32_t* tileB = tiles + ntiles + 1;
   PHFEM_CUDA(ctx, cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (P.nb + 1), ctx->stream));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 2 * (ntiles_h + 1), ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 2 * (ntiles + 1), ctx->stream));
 
-  const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
   const int nsub = kTileNodes >> P.bs;
-  const int ntiles = (int)((nC + kTileNodes - 1) / kTileNodes);
-  PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, bcount, ctx->derr));
+  PHFEM_TRY(source(0, bcount, (uint64_t*)nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
   PHFEM_LAUNCH(ctx, "k_eg_tile_max", k_eg_tile_max<<<grid_for(ntiles, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
       boff, P.nb, nsub, ntiles, ctx->derr));
@@ -619,6 +655,9 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   if (ctx->herr->misc != ~0ull) {
     const long long m = (long long)ctx->herr->misc;
     dfree(ctx, bcount); dfree(ctx, boff); dfree(ctx, tiles);
+    phfem_topology_release(ctx, out);
+    if (pairs)
+      return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE, "%s: occurrence %lld outside the key range", who, m);
     return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE,
                      "build_topology: element %lld has a node index outside 1..%lld", m + 1,
                      (long long)nC);
@@ -636,10 +675,11 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
     PHFEM_TRY(dalloc(ctx, &g2, nd));
     PHFEM_TRY(dalloc(ctx, &gnode, nd));
   }
-  PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, cursor, items));
+  PHFEM_TRY(source(1, cursor, items));
 
   EgOut o{out->edge_nodes, out->edge_elements, out->local_in_tplus, out->local_in_tminus,
-          out->interior_edges, out->boundary_edges, out->elem_edge, out->node_edge_start};
+          out->interior_edges, out->boundary_edges, out->elem_edge, out->node_edge_start,
+          pairs, P.node_base};
   EgParams PT = P;
   PT.nb = ntiles;
   const size_t smem = sizeof(TileSmem);
@@ -688,4 +728,68 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   out->n_boundary = (int32_t)(ctx->herr->counters[2] & 0xffffffffu);
   out->n_interior = out->E - out->n_boundary;
   return PHFEM_OK;
+}
+
+static phfem_status eg_params(phfem_ctx* ctx, int64_t nC_range, int64_t nC_all, int64_t nE_all,
+                              int32_t node_base, EgParams* P) {
+  P->nC = (int32_t)nC_range;
+  P->nE = (int32_t)nE_all;
+  P->node_base = node_base;
+  P->lo_bits = bits_for(std::max<int64_t>(nC_all - 1, 1));
+  P->occ_bits = bits_for(std::max<int64_t>(3 * nE_all - 1, 1));
+  P->total_bits = P->lo_bits + P->occ_bits + 1;
+  P->bs = std::min(8, 64 - P->total_bits);
+  if (P->bs < 1) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: ids too wide");
+  const int NB = 1 << P->bs;
+  P->nb = (int)((nC_range + NB - 1) / NB);
+  if (P->nb < 1) P->nb = 1;
+  return PHFEM_OK;
+}
+
+}  // namespace phfem
+
+PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                            phfem_topology* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !mesh) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "set device");
+  const int64_t nE = mesh->nE, nC = mesh->nC;
+  if (nE < 0 || nC < 0 || 3 * nE >= (int64_t(1) << 31))
+    return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: mesh too large for int ids");
+  out->nC = (int32_t)nC;
+  out->nE = (int32_t)nE;
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, nC, nC, nE, 0, &P));
+  const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
+  auto source = [&](int kind, int32_t* counts, uint64_t* items) -> phfem_status {
+    if (kind == 0)
+      PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, counts, ctx->derr));
+    else
+      PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, counts, items));
+    return PHFEM_OK;
+  };
+  return eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology");
+}
+
+PHFEM_API phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n,
+                                        int32_t node_lo, int32_t node_hi, int32_t nC_all,
+                                        int32_t nE_all, phfem_topology* out, int32_t* pairs) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || (!recs && n) || !pairs || node_lo < 0 || node_hi < node_lo || node_hi > nC_all ||
+      3 * (int64_t)nE_all >= (int64_t(1) << 31))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  out->nC = node_hi - node_lo;
+  out->nE = nE_all;
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, (int64_t)node_hi - node_lo, nC_all, nE_all, node_lo, &P));
+  const int grid_r = grid_for(n, 256, ctx->num_sms * 8);
+  const int4* r4 = reinterpret_cast<const int4*>(recs);
+  auto source = [&](int kind, int32_t* counts, uint64_t* items) -> phfem_status {
+    if (kind == 0)
+      PHFEM_LAUNCH(ctx, "k_rec_count", k_rec_count<<<grid_r, 256, 0, ctx->stream>>>(r4, n, P, counts, ctx->derr));
+    else
+      PHFEM_LAUNCH(ctx, "k_rec_scatter", k_rec_scatter<<<grid_r, 256, 0, ctx->stream>>>(r4, n, P, counts, items));
+    return PHFEM_OK;
+  };
+  return eg_core(ctx, P, n, source, out, reinterpret_cast<int2*>(pairs), "dist_dedup");
 }

@@ -1,0 +1,490 @@
+"""Multi-GPU edge generation -> red refinement -> assembly.
+
+One rank per GPU.  Elements are partitioned into contiguous ranges (their
+children keep the partition: the children of [a, b) are [4a, 4b),
+refine.cpp:28-37); max nodes into contiguous key ranges, so every rank owns a
+contiguous range of canonical edge ids.  Per-element work (blocks, load,
+children of the own elements) needs no communication.  The exchanges:
+
+  edge dedup     key-range all-to-all of the directed occurrences, a local
+                 sort (phfem_dist_dedup: the single-GPU tile kernels), an
+                 all-gather of the per-rank edge counts (global ids), and a
+                 reverse all-to-all of (element slot, edge id) pairs;
+  refinement     midpoints of the owned edges, all-gathered (coordinates stay
+                 replicated); boundary lists bisected from the resolved ids;
+  boundary data  all-reduce of the boundary-pair ids and of the Neumann edge
+                 table (both O(sqrt N)).
+
+The concatenation of the ranks' outputs is bit-identical to the single-GPU
+pipeline (tests/test_dist.py): numbering depends only on keys, t_plus only on
+element ids.
+
+The orchestration runs phase by phase over the rank states this process
+owns: one under torchrun (TorchComm: NCCL on GPUs, gloo on CPU) or W
+emulated ranks in one process (LocalComm) — the latter runs the real kernels
+of W ranks on one GPU one after another, never concurrently, so no rank ever
+waits on another.  Per-rank operations come from a backend: CudaRankOps (the
+product: C-ABI kernels); the CPU tests plug in a numpy restatement
+(tests/dist_cpu_backend.py) to exercise the exchanges with gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+import torch
+
+from . import capi
+
+NO_ERROR = -1  # int64 view of the uint64 ~0 the kernels start from (all-reduced as unsigned below)
+
+
+# ---- communication ------------------------------------------------------------------
+class TorchComm:
+    """torch.distributed: this process is one rank (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = dist.get_world_size()
+        self.ranks = [dist.get_rank()]
+
+    def all_reduce(self, ts: list, op: str):
+        o = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}[op]
+        self.dist.all_reduce(ts[0], op=o)
+
+    def all_gather(self, ts: list) -> list:
+        out = [torch.empty_like(ts[0]) for _ in range(self.world)]
+        self.dist.all_gather(out, ts[0])
+        return [out]
+
+    def all_to_all_v(self, sends: list, counts: list) -> list:
+        send, sc = sends[0], [int(c) for c in counts[0]]
+        sct = torch.tensor(sc, dtype=torch.int64, device=send.device)
+        rct = torch.empty_like(sct)
+        self.dist.all_to_all_single(rct, sct)
+        rc = [int(x) for x in rct.tolist()]
+        recv = torch.empty((sum(rc),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=rc, input_split_sizes=sc)
+        return [recv]
+
+
+class LocalComm:
+    """W ranks emulated in one process (their states are processed in turn)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def all_reduce(self, ts: list, op: str):
+        acc = ts[0].clone()
+        for t in ts[1:]:
+            acc = acc + t if op == "sum" else (torch.maximum(acc, t) if op == "max" else torch.minimum(acc, t))
+        for t in ts:
+            t.copy_(acc)
+
+    def all_gather(self, ts: list) -> list:
+        return [[t.clone() for t in ts] for _ in ts]
+
+    def all_to_all_v(self, sends: list, counts: list) -> list:
+        offs = [np.concatenate([[0], np.cumsum([int(c) for c in cs])]).astype(np.int64) for cs in counts]
+        return [torch.cat([sends[s][offs[s][d]:offs[s][d + 1]] for s in range(self.world)], 0)
+                for d in range(self.world)]
+
+
+def balanced_splits(hist: np.ndarray, bins: np.ndarray, world: int) -> np.ndarray:
+    """Key-range boundaries (node ids, W+1 entries) at histogram-bin edges with
+    about equal occurrence counts per rank."""
+    cum = np.concatenate([[0], np.cumsum(hist.astype(np.int64))])
+    out = [int(bins[0])]
+    for r in range(1, world):
+        k = int(np.searchsorted(cum, cum[-1] * r / world))
+        out.append(max(out[-1], int(bins[min(k, len(bins) - 1)])))
+    out.append(int(bins[-1]))
+    return np.asarray(out, dtype=np.int32)
+
+
+def element_splits(nE: int, world: int) -> np.ndarray:
+    return np.asarray([nE * r // world for r in range(world + 1)], dtype=np.int32)
+
+
+# ---- CUDA backend -------------------------------------------------------------------
+class CudaRankOps:
+    """One rank's operations through the C ABI.  Exchange buffers are torch
+    tensors on the rank's device; the ctx must run on torch's current stream
+    (dist.py passes it) so kernels and collectives are stream-ordered."""
+
+    def __init__(self, ctx: capi.Context, device):
+        self.ctx, self.lib, self.dev = ctx, ctx.lib, torch.device(device)
+
+    def _ck(self, st):
+        self.ctx.check(st)
+
+    @staticmethod
+    def p(t):
+        return C.c_void_p(t.data_ptr()) if t is not None and t.numel() else None
+
+    def empty(self, shape, dtype=torch.int32):
+        return torch.empty(shape, dtype=dtype, device=self.dev)
+
+    def as_tensor(self, a, dtype=torch.int32):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(device=self.dev, dtype=dtype)
+
+    def mesh_view(self, coords, nC, elements, nE_local, nE_cols):
+        """phfem_mesh over replicated coordinates and the rank's elements;
+        nE_cols = global element count (columns of C are 3 m, m global)."""
+        m = capi.phfem_mesh()
+        m.coords, m.elements = coords.data_ptr(), (elements.data_ptr() if elements.numel() else None)
+        m.nC, m.nE, m.nD, m.nN = nC, nE_local, 0, 0
+        m.owned = 0
+        self._cols = nE_cols
+        return m
+
+    # -- edge dedup -------------------------------------------------------------------
+    def occurrences(self, elements, elo, ehi, splits, pack: bool):
+        W = splits.numel() - 1
+        cnt = self.empty(W)
+        if not pack:
+            self._ck(self.lib.phfem_dist_occurrences(self.ctx.ptr, self.p(elements), elo, ehi, self.p(splits), W,
+                                                     self.p(cnt), None, None))
+            return cnt
+        off = self.empty(W + 1)
+        send = self.empty((max(3 * (ehi - elo), 1), 4))
+        self._ck(self.lib.phfem_dist_occurrences(self.ctx.ptr, self.p(elements), elo, ehi, self.p(splits), W,
+                                                 self.p(cnt), self.p(off), self.p(send)))
+        return send[:3 * (ehi - elo)], cnt.tolist()
+
+    def dedup(self, recv, nlo, nhi, nC, nE):
+        n = recv.shape[0]
+        pairs = self.empty((max(2 * n, 1), 2))
+        t = capi.phfem_topology()
+        self._ck(self.lib.phfem_dist_dedup(self.ctx.ptr, self.p(recv), n, nlo, nhi, nC, nE, C.byref(t),
+                                           self.p(pairs)))
+        self.part = capi.Topology(self.ctx, t)
+        self.pairs = pairs[:2 * t.E]
+        return int(t.E), int(t.n_boundary)
+
+    def route_pairs(self, E0, esplits):
+        W = esplits.numel() - 1
+        cnt, off = self.empty(W), self.empty(W + 1)
+        send = self.empty((max(self.pairs.shape[0], 1), 2))
+        self._ck(self.lib.phfem_dist_route_pairs(self.ctx.ptr, self.p(self.pairs), self.pairs.shape[0], E0,
+                                                 self.p(esplits), W, self.p(cnt), self.p(off), self.p(send)))
+        c = cnt.tolist()
+        return send[:sum(c)], c
+
+    def apply_pairs(self, recv, elo, ehi):
+        ee = self.empty((ehi - elo, 3))
+        self._ck(self.lib.phfem_dist_apply_pairs(self.ctx.ptr, self.p(recv), recv.shape[0], elo, self.p(ee)))
+        return ee
+
+    def rebase(self, ptr, n, off, only_nonneg=0):
+        self._ck(self.lib.phfem_dist_add_offset(self.ctx.ptr, C.c_void_p(ptr), n, off, only_nonneg))
+
+    def rebase_part(self, E0):
+        t = self.part.t
+        for ptr, n in ((t.interior_edges, t.n_interior), (t.boundary_edges, t.n_boundary),
+                       (t.node_edge_start, t.nC + 1)):
+            if n:
+                self.rebase(ptr, n, E0)
+
+    def resolve(self, pairs, list_base, nlo, E0):
+        n = pairs.shape[0]
+        ids = torch.full((max(n, 1),), -1, dtype=torch.int32, device=self.dev)
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        if n:
+            self._ck(self.lib.phfem_dist_resolve(self.ctx.ptr, C.byref(self.part.t), nlo, E0, self.p(pairs), n,
+                                                 list_base, self.p(ids), self.p(err)))
+        return ids[:n], err
+
+    # -- refinement -----------------------------------------------------------------
+    def midpoints(self, coords):
+        t = self.part.t
+        out = self.empty((max(t.E, 1), 2), torch.float64)
+        self._ck(self.lib.phfem_dist_midpoints(self.ctx.ptr, self.p(coords), C.c_void_p(t.edge_nodes), t.E,
+                                               self.p(out)))
+        return out[:t.E]
+
+    def children(self, elements, elem_edge, nC):
+        n = elements.shape[0]
+        out = self.empty((max(4 * n, 1), 3))
+        self._ck(self.lib.phfem_dist_children(self.ctx.ptr, self.p(elements), self.p(elem_edge), n, nC,
+                                              self.p(out)))
+        return out[:4 * n]
+
+    # -- classification, C, boundary vectors, blocks ------------------------------------------
+    def classify(self, dir_ids_local, neu_ids_local):
+        c = capi.phfem_classification()
+        self._ck(self.lib.phfem_dist_classify(self.ctx.ptr, C.byref(self.part.t), 0, self.p(dir_ids_local),
+                                              dir_ids_local.numel(), self.p(neu_ids_local), neu_ids_local.numel(),
+                                              C.byref(c)))
+        self.cls = capi.Classification(self.ctx, c)
+        return int(c.L)
+
+    def constraint(self, mview):
+        m = capi.phfem_csr()
+        mv = capi.phfem_mesh()
+        C.memmove(C.byref(mv), C.byref(mview), C.sizeof(mv))
+        mv.nE = self._cols
+        self._ck(self.lib.phfem_assemble_constraint(self.ctx.ptr, C.byref(mv), C.byref(self.part.t),
+                                                    C.byref(self.cls.c), C.byref(m)))
+        self.csr = m
+        return m
+
+    def dirichlet(self, mview, uD, t):
+        bd = self.empty((max(self.cls.c.L, 1),), torch.float64)
+        self._ck(self.lib.phfem_assemble_dirichlet(self.ctx.ptr, C.byref(mview), C.byref(self.part.t),
+                                                   C.byref(self.cls.c), C.byref(uD), t, self.p(bd)))
+        return bd[:self.cls.c.L]
+
+    def volume(self, mview, coeffs, f, t):
+        n = mview.nE
+        out = {k: self.empty((max(n, 1), 9), torch.float64) for k in ("B", "D", "M", "M0")}
+        self._ck(self.lib.phfem_assemble_volume(self.ctx.ptr, C.byref(mview), C.byref(coeffs), self.p(out["B"]),
+                                                self.p(out["D"]), self.p(out["M"]), self.p(out["M0"])))
+        load = self.empty((max(n, 1), 3), torch.float64)
+        self._ck(self.lib.phfem_assemble_load(self.ctx.ptr, C.byref(mview), C.byref(f), t, self.p(load)))
+        out = {k: v[:n] for k, v in out.items()}
+        out["load"] = load[:n]
+        return out
+
+    def neumann_table(self, neu_ids_local, nN_all, positions):
+        """rows {a, b, t_plus, led} of the owned Neumann edges at their global
+        list positions (others zero)."""
+        table = torch.zeros((max(nN_all, 1), 4), dtype=torch.int32, device=self.dev)
+        if nN_all:
+            full = torch.full((nN_all,), -1, dtype=torch.int32, device=self.dev)
+            full[positions] = neu_ids_local
+            self._ck(self.lib.phfem_dist_neumann_table(self.ctx.ptr, C.byref(self.part.t), 0, self.p(full), nN_all,
+                                                       self.p(table)))
+        return table[:nN_all]
+
+    def neumann_apply(self, mview, table, dup, elo, ehi, g, t, load):
+        self._ck(self.lib.phfem_dist_neumann_apply(self.ctx.ptr, C.byref(mview), self.p(table), table.shape[0],
+                                                   1 if dup else 0, elo, ehi, C.byref(g), t, self.p(load)))
+
+    # -- results -----------------------------------------------------------------------------------
+    def part_arrays(self) -> dict:
+        d = self.part.download()
+        d.pop("elem_edge", None)
+        return d
+
+    def cls_arrays(self) -> dict:
+        return self.cls.download()
+
+    def csr_arrays(self):
+        m, x = self.csr, self.ctx
+        return (x.to_host(m.row_ptr, (m.rows + 1,), np.int32), x.to_host(m.col_idx, (m.nnz,), np.int32),
+                x.to_host(m.values, (m.nnz,), np.float64))
+
+    def release(self):
+        if getattr(self, "csr", None) is not None:
+            self.lib.phfem_csr_release(self.ctx.ptr, C.byref(self.csr))
+            self.csr = None
+        for a in ("cls", "part"):
+            o = getattr(self, a, None)
+            if o is not None:
+                o.release()
+                setattr(self, a, None)
+
+
+# ---- one rank's state -------------------------------------------------------------------
+@dataclass
+class RankState:
+    rank: int
+    ops: object
+    coords: torch.Tensor        # replicated [nC][2] fp64
+    elements: torch.Tensor      # own elements [n][3] int32
+    elo: int
+    ehi: int
+    dirichlet: torch.Tensor     # replicated boundary lists [nD][2], [nN][2]
+    neumann: torch.Tensor
+
+
+def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: np.ndarray,
+                     nbins: int = 4096):
+    """Distributed build_topology.  Returns the key-range splits, per-state
+    (E0, B0) and the global (E, n_boundary); each ops holds its part (global
+    ids) and each state gets its elem_edge."""
+    W = comm.world
+    nb = max(1, min(nbins, nC))
+    bins = np.asarray([nC * i // nb for i in range(nb + 1)], dtype=np.int32)
+    # coarse histogram of max nodes -> balanced key ranges (identical on every rank)
+    hists = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(bins), pack=False) for s in states]
+    comm.all_reduce(hists, "sum")
+    splits = balanced_splits(hists[0].cpu().numpy(), bins, W)
+    # forward all-to-all of the occurrences, local dedup
+    packed = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(splits), pack=True) for s in states]
+    recvs = comm.all_to_all_v([p[0] for p in packed], [p[1] for p in packed])
+    eb = []
+    for s, rv in zip(states, recvs):
+        r = s.rank
+        E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE)
+        eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
+    gath = comm.all_gather(eb)
+    per = []
+    for s, g in zip(states, gath):
+        allc = torch.stack(g).cpu().numpy()
+        E0, B0 = int(allc[:s.rank, 0].sum()), int(allc[:s.rank, 1].sum())
+        per.append((E0, B0))
+        s.ops.rebase_part(E0)
+    Etot, Btot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
+    # reverse all-to-all: (element slot, global edge id) to the element owners
+    routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits)) for s, (E0, _) in zip(states, per)]
+    recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
+    for s, rv in zip(states, recvs):
+        s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
+    return splits, per, (Etot, Btot)
+
+
+def _resolve(states, comm, splits, per, nD, nN):
+    """Global boundary-pair ids (every rank) + the reference's first error."""
+    ids = []
+    errs = []
+    for s, (E0, _) in zip(states, per):
+        pairs = torch.cat([s.dirichlet, s.neumann], 0).reshape(-1, 2).contiguous()
+        i, e = s.ops.resolve(pairs, 0, int(splits[s.rank]), E0)
+        ids.append(i.to(torch.int64))
+        errs.append(e)
+    if nD + nN:
+        comm.all_reduce(ids, "max")
+        # ~0 (no error) is -1 as int64: shift to make "no error" the largest
+        shifted = [torch.where(e == -1, torch.full_like(e, 2 ** 62), e) for e in errs]
+        comm.all_reduce(shifted, "min")
+        key = int(shifted[0].item())
+        if key != 2 ** 62:
+            pos, interior = key >> 2, key & 1
+            s = states[0]
+            is_d = pos < nD
+            pr = (s.dirichlet[pos] if is_d else s.neumann[pos - nD]).tolist()
+            what = "dirichlet" if is_d else "neumann"
+            raise RuntimeError(f"{what} pair ({pr[0] + 1},{pr[1] + 1}) " +
+                               ("resolves to an interior edge" if interior else "is not an edge"))
+    return ids
+
+
+def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels: int, coeffs, f, g, uD,
+                         t: float = 0.0):
+    """[edge generation -> red refinement] x levels -> edge generation ->
+    classification -> B, D, M, M0, load = b + LN, C (CSR rows), bD; every rank
+    keeps its slices (collect() gathers them for tests)."""
+    W = comm.world
+    # element ranges: the input split, x4 per refinement (children of [a,b) are [4a,4b))
+    esplits = element_splits(nE, W)
+    for _ in range(levels):
+        splits, per, (Etot, _) = _edge_generation(states, comm, nC, nE, esplits)
+        nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
+        ids = _resolve(states, comm, splits, per, nD, nN)
+        # replicated fine coordinates: old nodes + all-gathered midpoints (edge order)
+        mids = [s.ops.midpoints(s.coords) for s in states]
+        counts = [torch.tensor([m.shape[0]], dtype=torch.int64, device=m.device) for m in mids]
+        cg = comm.all_gather(counts)
+        Emax = max(1, max(int(torch.stack(c).max().item()) for c in cg))
+        padded = [torch.cat([m, m.new_zeros((Emax - m.shape[0], 2))], 0) for m in mids]
+        gm = comm.all_gather(padded)
+        for s, parts, c in zip(states, gm, cg):
+            sizes = [int(x.item()) for x in c]
+            newc = torch.cat([s.coords] + [p[:n] for p, n in zip(parts, sizes)], 0)
+            kids = s.ops.children(s.elements, s.elem_edge, nC)
+            bd_ids = ids[states.index(s)]
+            # bisect the boundary lists (refine.cpp:39-50): (a, mid), (mid, b)
+            def bisect(pairs, eid):
+                if pairs.shape[0] == 0:
+                    return pairs
+                mid = (eid + nC).to(pairs.dtype)
+                return torch.stack([pairs[:, 0], mid, mid, pairs[:, 1]], 1).reshape(-1, 2).contiguous()
+            s.dirichlet = bisect(s.dirichlet, bd_ids[:nD])
+            s.neumann = bisect(s.neumann, bd_ids[nD:])
+            s.ops.release()
+            s.coords, s.elements = newc.contiguous(), kids
+            s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
+        nC, nE = nC + Etot, 4 * nE
+        esplits = 4 * esplits
+    # final level
+    splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
+    nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
+    ids = _resolve(states, comm, splits, per, nD, nN)
+    Ls = []
+    for s, (E0, _), i in zip(states, per, ids):
+        dl = i[:nD] - E0
+        nl = i[nD:] - E0
+        E_r = s.ops.part.t.E
+        s.dir_local = dl[(dl >= 0) & (dl < E_r) & (i[:nD] >= 0)].to(torch.int32).contiguous()
+        own_n = (nl >= 0) & (nl < E_r) & (i[nD:] >= 0)
+        s.neu_pos = torch.nonzero(own_n).flatten()
+        s.neu_local = nl[own_n].to(torch.int32).contiguous()
+        Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local)], dtype=torch.int64,
+                               device=s.coords.device))
+    gl = comm.all_gather(Ls)
+    results = []
+    for s, (E0, B0), g_ in zip(states, per, gl):
+        L_all = torch.stack(g_).flatten().cpu().numpy()
+        R0 = int(L_all[:s.rank].sum())
+        N0 = E0 - R0                      # Neumann edges before the rank
+        nnz0 = 4 * R0 - 2 * (B0 - N0)     # retained boundary rows hold 2 entries
+        mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
+        s.ops.constraint(mview)
+        s.bd = s.ops.dirichlet(mview, uD, t)
+        c = s.ops.cls.c
+        s.ops.rebase(c.retained_pos, c.E, R0, 1)
+        s.ops.rebase(c.retained_edges, c.L, E0)
+        s.ops.rebase(s.ops.csr.row_ptr, s.ops.csr.rows + 1, nnz0)
+        s.E0, s.R0 = E0, R0
+        s.blocks = s.ops.volume(mview, coeffs, f, t)
+        s.mview = mview
+    # Neumann: owners publish {a, b, t_plus, led}; element owners add b + LN
+    all_neu = ids[0][nD:]
+    dup = bool(nN) and int(torch.unique(all_neu).numel()) < nN
+    tables = [s.ops.neumann_table(s.neu_local, nN, s.neu_pos) for s in states]
+    if nN:
+        comm.all_reduce(tables, "sum")
+    for s, tb in zip(states, tables):
+        s.ops.neumann_apply(s.mview, tb, dup, s.elo, s.ehi, g, t, s.blocks["load"])
+    return states, nC, nE
+
+
+def collect(states: List[RankState]) -> dict:
+    """Rank slices of the emulated ranks concatenated (tests)."""
+    out = {}
+    parts = [s.ops.part_arrays() for s in states]
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "interior_edges",
+              "boundary_edges"):
+        out[k] = np.concatenate([p[k] for p in parts])
+    out["node_edge_start"] = np.concatenate([p["node_edge_start"][:-1] for p in parts] +
+                                            [parts[-1]["node_edge_start"][-1:]])
+    out["elem_edge"] = np.concatenate([s.elem_edge.cpu().numpy() for s in states])
+    cls = [s.ops.cls_arrays() for s in states]
+    out["retained_pos"] = np.concatenate([c["retained_pos"] for c in cls])
+    out["retained_edges"] = np.concatenate([c["retained_edges"] for c in cls])
+    csr = [s.ops.csr_arrays() for s in states]
+    out["C_row_ptr"] = np.concatenate([c[0][:-1] for c in csr] + [csr[-1][0][-1:]])
+    out["C_col_idx"] = np.concatenate([c[1] for c in csr])
+    out["C_values"] = np.concatenate([c[2] for c in csr])
+    out["bd"] = np.concatenate([s.bd.cpu().numpy() for s in states])
+    for k in ("B", "D", "M", "M0", "load"):
+        out[k] = np.concatenate([s.blocks[k].cpu().numpy().reshape(-1) for s in states])
+    out["coords"] = states[0].coords.cpu().numpy()
+    out["elements"] = np.concatenate([s.elements.cpu().numpy() for s in states])
+    out["dirichlet"] = states[0].dirichlet.cpu().numpy()
+    out["neumann"] = states[0].neumann.cpu().numpy()
+    return out
+
+
+def make_states(hm: capi.HostMesh, comm, ops_factory) -> List[RankState]:
+    """Replicated input mesh, element ranges split evenly; ops_factory(rank)
+    gives the backend of a rank (its device)."""
+    es = element_splits(hm.nE, comm.world)
+    states = []
+    for r in comm.ranks:
+        ops = ops_factory(r)
+        dev = ops.dev
+        states.append(RankState(
+            rank=r, ops=ops,
+            coords=torch.as_tensor(hm.coords).to(dev).contiguous(),
+            elements=torch.as_tensor(hm.elements[es[r]:es[r + 1]]).to(dev).contiguous(),
+            elo=int(es[r]), ehi=int(es[r + 1]),
+            dirichlet=torch.as_tensor(hm.dirichlet).to(dev).contiguous(),
+            neumann=torch.as_tensor(hm.neumann).to(dev).contiguous()))
+    return states

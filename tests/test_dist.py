@@ -1,0 +1,72 @@
+"""Multi-GPU path (paper_2401_15557_b200/dist.py).
+
+* gpu: W ranks emulated in one process on one B200 (LocalComm: the real
+  kernels of every rank run one after another, never waiting on each other)
+  must reproduce the single-GPU pipeline BIT FOR BIT after concatenating the
+  rank slices — topology, element->edge map, classification, C in CSR, bD,
+  blocks and load — for W = 1..4 and refinement in the loop.
+* not gpu: the same orchestration with 2 gloo processes on CPU and the numpy
+  restatement of the per-rank operations (tests/dist_cpu_backend.py) against
+  the C oracle — the exchange logic (key ranges, all-to-alls, id re-basing,
+  boundary-pair resolution, Neumann table) under a real process group.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2401_15557_b200 import meshgen as G
+
+CASES = [("crisscross-L1", lambda: O.refine_levels(G.crisscross_square(), 1), 1),
+         ("square-L3", lambda: O.refine_levels(G.square_2tri(), 3), 1),
+         ("lshape-L2", lambda: O.refine_levels(G.lshape_6tri(), 2), 1),
+         ("lshape-L3-nolevel", lambda: O.refine_levels(G.lshape_6tri(), 3), 0),
+         ("stress-L3", lambda: O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 3), 3)), 1),
+         ("fan-30", lambda: G.fan(30, True), 1)]
+
+
+def check_equal(d, ref):
+    r = ref
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "interior_edges",
+              "boundary_edges", "node_edge_start", "elem_edge"):
+        assert np.array_equal(d[k].reshape(-1), r["topo"][k].reshape(-1)), k
+    for k in ("retained_pos", "retained_edges"):
+        assert np.array_equal(d[k], r["cls"][k]), k
+    for k in ("C_row_ptr", "C_col_idx", "C_values", "bd"):
+        assert np.array_equal(d[k], r[k]), k
+    for k in ("B", "D", "M", "M0", "load"):
+        assert np.array_equal(d[k], r[k].reshape(-1)), k
+    assert np.array_equal(d["coords"], r["mesh"].coords)
+    assert np.array_equal(d["elements"], r["mesh"].elements)
+    assert np.array_equal(d["dirichlet"], r["mesh"].dirichlet)
+    assert np.array_equal(d["neumann"], r["mesh"].neumann)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [1, 2, 3, 4])
+@pytest.mark.parametrize("name,make,levels", CASES, ids=[c[0] for c in CASES])
+def test_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels):
+    import torch
+    from paper_2401_15557_b200 import capi, dist
+    hm = make()
+    args = G.config_fields(2)
+    ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args, flags=capi.PIPE_GENERIC_EG).download()
+    tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    comm = dist.LocalComm(W)
+    states = dist.make_states(hm, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *args)
+    check_equal(dist.collect(states), ref)
+
+
+@pytest.mark.gpu
+def test_emulated_ranks_boundary_errors(ctx):
+    import torch
+    from paper_2401_15557_b200 import capi, dist
+    cc = G.crisscross_square()
+    bad = capi.HostMesh(cc.coords, cc.elements, np.vstack([cc.dirichlet, [[4, 0]]]), cc.neumann)
+    tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    comm = dist.LocalComm(2)
+    states = dist.make_states(bad, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
+    with pytest.raises(RuntimeError, match="resolves to an interior edge"):
+        dist.distributed_pipeline(states, comm, bad.nC, bad.nE, 0, *G.config_fields(2))
