@@ -265,6 +265,18 @@ class CudaRankOps:
         self._ck(self.lib.phfem_dist_neumann_apply(self.ctx.ptr, C.byref(mview), self.p(table), table.shape[0],
                                                    1 if dup else 0, elo, ehi, C.byref(g), t, self.p(load)))
 
+    def num_edges(self) -> int:
+        return int(self.part.t.E)
+
+    def rebase_results(self, E0, R0, nnz0):
+        """rank-local retained positions / retained edges / CSR row pointers -> global"""
+        c, m = self.cls.c, self.csr
+        if c.E:
+            self.rebase(c.retained_pos, c.E, R0, 1)
+        if c.L:
+            self.rebase(c.retained_edges, c.L, E0)
+        self.rebase(m.row_ptr, m.rows + 1, nnz0)
+
     # -- results -----------------------------------------------------------------------------------
     def part_arrays(self) -> dict:
         d = self.part.download()
@@ -410,7 +422,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     for s, (E0, _), i in zip(states, per, ids):
         dl = i[:nD] - E0
         nl = i[nD:] - E0
-        E_r = s.ops.part.t.E
+        E_r = s.ops.num_edges()
         s.dir_local = dl[(dl >= 0) & (dl < E_r) & (i[:nD] >= 0)].to(torch.int32).contiguous()
         own_n = (nl >= 0) & (nl < E_r) & (i[nD:] >= 0)
         s.neu_pos = torch.nonzero(own_n).flatten()
@@ -427,10 +439,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
         s.ops.constraint(mview)
         s.bd = s.ops.dirichlet(mview, uD, t)
-        c = s.ops.cls.c
-        s.ops.rebase(c.retained_pos, c.E, R0, 1)
-        s.ops.rebase(c.retained_edges, c.L, E0)
-        s.ops.rebase(s.ops.csr.row_ptr, s.ops.csr.rows + 1, nnz0)
+        s.ops.rebase_results(E0, R0, nnz0)
         s.E0, s.R0 = E0, R0
         s.blocks = s.ops.volume(mview, coeffs, f, t)
         s.mview = mview
@@ -445,31 +454,43 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     return states, nC, nE
 
 
+def rank_slice(s: RankState) -> dict:
+    """One rank's slice of every output (host arrays, global ids)."""
+    p = s.ops.part_arrays()
+    c = s.ops.cls_arrays()
+    rp, col, val = s.ops.csr_arrays()
+    out = {k: np.asarray(p[k]) for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus",
+                                          "interior_edges", "boundary_edges", "node_edge_start")}
+    out["elem_edge"] = s.elem_edge.cpu().numpy()
+    out["retained_pos"], out["retained_edges"] = np.asarray(c["retained_pos"]), np.asarray(c["retained_edges"])
+    out["C_row_ptr"], out["C_col_idx"], out["C_values"] = np.asarray(rp), np.asarray(col), np.asarray(val)
+    out["bd"] = s.bd.cpu().numpy()
+    for k in ("B", "D", "M", "M0", "load"):
+        out[k] = s.blocks[k].cpu().numpy().reshape(-1)
+    out["coords"] = s.coords.cpu().numpy()
+    out["elements"] = s.elements.cpu().numpy()
+    out["dirichlet"] = s.dirichlet.cpu().numpy()
+    out["neumann"] = s.neumann.cpu().numpy()
+    return out
+
+
+def concat_slices(sl: list) -> dict:
+    """Rank slices (rank order) -> the single-GPU layout."""
+    out = {}
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "interior_edges",
+              "boundary_edges", "elem_edge", "retained_pos", "retained_edges", "C_col_idx", "C_values", "bd",
+              "B", "D", "M", "M0", "load", "elements"):
+        out[k] = np.concatenate([x[k] for x in sl])
+    out["node_edge_start"] = np.concatenate([x["node_edge_start"][:-1] for x in sl] + [sl[-1]["node_edge_start"][-1:]])
+    out["C_row_ptr"] = np.concatenate([x["C_row_ptr"][:-1] for x in sl] + [sl[-1]["C_row_ptr"][-1:]])
+    for k in ("coords", "dirichlet", "neumann"):
+        out[k] = sl[0][k]
+    return out
+
+
 def collect(states: List[RankState]) -> dict:
     """Rank slices of the emulated ranks concatenated (tests)."""
-    out = {}
-    parts = [s.ops.part_arrays() for s in states]
-    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "interior_edges",
-              "boundary_edges"):
-        out[k] = np.concatenate([p[k] for p in parts])
-    out["node_edge_start"] = np.concatenate([p["node_edge_start"][:-1] for p in parts] +
-                                            [parts[-1]["node_edge_start"][-1:]])
-    out["elem_edge"] = np.concatenate([s.elem_edge.cpu().numpy() for s in states])
-    cls = [s.ops.cls_arrays() for s in states]
-    out["retained_pos"] = np.concatenate([c["retained_pos"] for c in cls])
-    out["retained_edges"] = np.concatenate([c["retained_edges"] for c in cls])
-    csr = [s.ops.csr_arrays() for s in states]
-    out["C_row_ptr"] = np.concatenate([c[0][:-1] for c in csr] + [csr[-1][0][-1:]])
-    out["C_col_idx"] = np.concatenate([c[1] for c in csr])
-    out["C_values"] = np.concatenate([c[2] for c in csr])
-    out["bd"] = np.concatenate([s.bd.cpu().numpy() for s in states])
-    for k in ("B", "D", "M", "M0", "load"):
-        out[k] = np.concatenate([s.blocks[k].cpu().numpy().reshape(-1) for s in states])
-    out["coords"] = states[0].coords.cpu().numpy()
-    out["elements"] = np.concatenate([s.elements.cpu().numpy() for s in states])
-    out["dirichlet"] = states[0].dirichlet.cpu().numpy()
-    out["neumann"] = states[0].neumann.cpu().numpy()
-    return out
+    return concat_slices([rank_slice(s) for s in states])
 
 
 def make_states(hm: capi.HostMesh, comm, ops_factory) -> List[RankState]:

@@ -1,0 +1,295 @@
+"""TEST INFRASTRUCTURE: a numpy restatement of the per-rank operations of
+paper_2401_15557_b200/dist.py (the interface of dist.CudaRankOps), so the
+distributed orchestration — key ranges, all-to-alls, id re-basing, boundary
+pair resolution, the Neumann table — runs under a real gloo process group on
+CPU.  Per-element values come from the C oracle (oracle/), the rest is plain
+numpy following the same reference lines as the kernels:
+  occurrences / dedup      edge_topology.cpp:52-115
+  children / midpoints     refine.cpp:16-37
+  classification           edge_topology.cpp:145-177
+  C rows                   assembly.cpp:144-168
+  Dirichlet / Neumann      assembly.cpp:205-242, elliptic.cpp:54-55
+Never used by the product path.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from oracle import oracle as O
+from paper_2401_15557_b200 import capi
+
+PI = 3.14159265358979323846
+
+
+def field_eval(f, x, y, t):
+    k, p = f.kind, f.p
+    if k == capi.FIELD_ZERO:
+        return 0.0
+    if k == capi.FIELD_CONST:
+        return p[0]
+    if k == capi.FIELD_SINSIN:
+        return p[0] * math.sin(PI * x) * math.sin(PI * y)
+    if k == capi.FIELD_EXP_SINSIN:
+        return math.exp(-t) * p[0] * math.sin(PI * x) * math.sin(PI * y)
+    if k == capi.FIELD_AFFINE:
+        return p[0] + p[1] * x + p[2] * y + p[3] * t
+    raise NotImplementedError(k)
+
+
+def flux_eval(g, x, y, nx, ny, t):
+    k, p = g.kind, g.p
+    if k == capi.FLUX_ZERO:
+        return 0.0
+    if k == capi.FLUX_CONST:
+        return p[0]
+    if k == capi.FLUX_GRAD_SINSIN:
+        gx = p[0] * PI * math.cos(PI * x) * math.sin(PI * y)
+        gy = p[0] * PI * math.sin(PI * x) * math.cos(PI * y)
+        return gx * nx + gy * ny
+    raise NotImplementedError(k)
+
+
+class _Part:
+    pass
+
+
+class NumpyRankOps:
+    def __init__(self):
+        self.dev = torch.device("cpu")
+
+    def as_tensor(self, a, dtype=torch.int32):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(dtype=dtype)
+
+    @staticmethod
+    def _dest(splits, v):
+        return np.searchsorted(splits, v, side="right") - 1
+
+    # -- edge dedup -------------------------------------------------------------------------
+    def occurrences(self, elements, elo, ehi, splits, pack):
+        el = elements.numpy().reshape(-1, 3)
+        sp = splits.numpy().astype(np.int64)
+        n = el.shape[0]
+        a = el.reshape(-1)
+        b = el[:, [1, 2, 0]].reshape(-1)
+        hi, lo = np.maximum(a, b), np.minimum(a, b)
+        occ = 3 * (elo + np.repeat(np.arange(n), 3)) + np.tile(np.arange(3), n)
+        d = self._dest(sp, hi)
+        W = len(sp) - 1
+        cnt = np.bincount(d, minlength=W)[:W].astype(np.int32)
+        if not pack:
+            return torch.as_tensor(cnt)
+        order = np.argsort(d, kind="stable")
+        rec = np.stack([hi, lo, occ, (a > b).astype(np.int64)], 1)[order].astype(np.int32)
+        return torch.as_tensor(rec), cnt.tolist()
+
+    def dedup(self, recv, nlo, nhi, nC, nE):
+        r = recv.numpy().astype(np.int64).reshape(-1, 4)
+        order = np.lexsort((r[:, 2], r[:, 1], r[:, 0]))   # (max, min, occurrence)
+        r = r[order]
+        key = r[:, 0] * (nC + 1) + r[:, 1]
+        start = np.ones(len(r), bool)
+        start[1:] = key[1:] != key[:-1]
+        idx = np.flatnonzero(start)
+        cnt = np.diff(np.append(idx, len(r)))
+        if np.any(cnt > 2):
+            raise RuntimeError("non-manifold")
+        E = len(idx)
+        f = r[idx]
+        two = cnt == 2
+        g = np.zeros_like(f)
+        g[two] = r[idx[two] + 1]
+        if np.any(two & (g[:, 3] == f[:, 3])):
+            raise RuntimeError("duplicate directed")
+        mf, lf = f[:, 2] // 3, (f[:, 2] % 3 + 2) % 3
+        mg, lg = g[:, 2] // 3, (g[:, 2] % 3 + 2) % 3
+        p = _Part()
+        p.edge_nodes = np.where(f[:, 3:4] == 1, f[:, [0, 1]], f[:, [1, 0]]).astype(np.int32)
+        p.edge_elements = np.stack([mf, np.where(two, mg, -1)], 1).astype(np.int32)
+        p.ltp = lf.astype(np.int32)
+        p.ltm = np.where(two, lg, -1).astype(np.int32)
+        ids = np.arange(E)
+        p.interior = ids[two].astype(np.int32)
+        p.boundary = ids[~two].astype(np.int32)
+        nodes = np.arange(nlo, nhi + 1)
+        p.nes = np.searchsorted(f[:, 0], nodes, side="left").astype(np.int32)
+        p.nlo = nlo
+        self.part = p
+        pairs = np.full((2 * E, 2), -1, np.int32)
+        pairs[0::2, 0], pairs[0::2, 1] = 3 * mf + lf, ids
+        pairs[1::2, 0] = np.where(two, 3 * mg + lg, -1)
+        pairs[1::2, 1] = ~ids
+        self.pairs = pairs
+        return E, int((~two).sum())
+
+    def num_edges(self):
+        return len(self.part.ltp)
+
+    def rebase_part(self, E0):
+        p = self.part
+        p.interior = p.interior + E0
+        p.boundary = p.boundary + E0
+        p.nes = p.nes + E0
+        p.E0 = E0
+
+    def route_pairs(self, E0, esplits):
+        pr = self.pairs
+        pr = pr[pr[:, 0] >= 0].astype(np.int64)
+        v = np.where(pr[:, 1] >= 0, pr[:, 1] + E0, ~(~pr[:, 1] + E0))
+        sp = esplits.numpy().astype(np.int64)
+        d = self._dest(sp, pr[:, 0] // 3)
+        W = len(sp) - 1
+        order = np.argsort(d, kind="stable")
+        send = np.stack([pr[:, 0], v], 1)[order].astype(np.int32)
+        return torch.as_tensor(send), np.bincount(d, minlength=W)[:W].tolist()
+
+    def apply_pairs(self, recv, elo, ehi):
+        ee = np.zeros(3 * (ehi - elo), np.int32)
+        r = recv.numpy()
+        ee[r[:, 0] - 3 * elo] = r[:, 1]
+        return torch.as_tensor(ee.reshape(-1, 3))
+
+    def resolve(self, pairs, list_base, nlo, E0):
+        p = self.part
+        pr = pairs.numpy().reshape(-1, 2)
+        ids = np.full(len(pr), -1, np.int32)
+        err = (1 << 64) - 1
+        for i, (a, b) in enumerate(pr):
+            hi, lo = max(a, b), min(a, b)
+            if hi < nlo or hi >= nlo + len(p.nes) - 1:
+                continue
+            l, r = p.nes[hi - nlo] - E0, p.nes[hi - nlo + 1] - E0
+            e = -1
+            for k in range(l, r):
+                if min(p.edge_nodes[k]) == lo:
+                    e = k
+            pos = list_base + i
+            if e < 0:
+                err = min(err, pos << 2)
+            elif p.edge_elements[e, 1] >= 0:
+                err = min(err, (pos << 2) | 1)
+            else:
+                ids[i] = E0 + e
+        e64 = np.array([err], dtype=np.uint64).view(np.int64)
+        return torch.as_tensor(ids), torch.as_tensor(e64)
+
+    # -- refinement -----------------------------------------------------------------------------
+    def midpoints(self, coords):
+        c = coords.numpy()
+        en = self.part.edge_nodes
+        return torch.as_tensor(0.5 * (c[en[:, 0]] + c[en[:, 1]]))
+
+    def children(self, elements, elem_edge, nC):
+        el = elements.numpy()
+        s = elem_edge.numpy().astype(np.int64)
+        mid = nC + np.where(s >= 0, s, ~s)
+        p0, p1, p2 = el[:, 0], el[:, 1], el[:, 2]
+        m0, m1, m2 = mid[:, 0], mid[:, 1], mid[:, 2]
+        kids = np.stack([np.stack([m0, m1, m2], 1), np.stack([p0, m2, m1], 1),
+                         np.stack([p1, m0, m2], 1), np.stack([p2, m1, m0], 1)], 1)
+        return torch.as_tensor(kids.reshape(-1, 3).astype(np.int32))
+
+    # -- classification / C / vectors -----------------------------------------------------------------
+    def classify(self, dir_local, neu_local):
+        E = self.num_edges()
+        neu = np.zeros(E, bool)
+        neu[neu_local.numpy()] = True
+        rpos = np.full(E, -1, np.int32)
+        keep = np.flatnonzero(~neu)
+        rpos[keep] = np.arange(len(keep))
+        self.cls = {"retained_pos": rpos, "retained_edges": keep.astype(np.int32),
+                    "dirichlet": dir_local.numpy().copy()}
+        return len(keep)
+
+    def mesh_view(self, coords, nC, elements, nE_local, nE_cols):
+        return {"coords": coords.numpy(), "elements": elements.numpy()}
+
+    def constraint(self, mv):
+        p, c = self.part, mv["coords"]
+        rp, cols, vals = [0], [], []
+        for e in self.cls["retained_edges"]:
+            a, b = p.edge_nodes[e]
+            d = c[b] - c[a]
+            ln = math.sqrt(d[0] * d[0] + d[1] * d[1])
+            tp, tm = p.edge_elements[e]
+            for cc in range(3):
+                if cc != p.ltp[e]:
+                    cols.append(3 * tp + cc)
+                    vals.append(ln * 0.5)
+            if tm >= 0:
+                for cc in range(3):
+                    if cc != p.ltm[e]:
+                        cols.append(3 * tm + cc)
+                        vals.append(-ln * 0.5)
+            rp.append(len(cols))
+        self.csr = [np.asarray(rp, np.int32), np.asarray(cols, np.int32), np.asarray(vals, np.float64)]
+
+    def dirichlet(self, mv, uD, t):
+        p, c = self.part, mv["coords"]
+        bd = np.zeros(len(self.cls["retained_edges"]))
+        for e in self.cls["dirichlet"]:
+            a, b = p.edge_nodes[e]
+            mx, my = 0.5 * (c[a][0] + c[b][0]), 0.5 * (c[a][1] + c[b][1])
+            d = c[b] - c[a]
+            ln = math.sqrt(d[0] * d[0] + d[1] * d[1])
+            pos = self.cls["retained_pos"][e]
+            if pos >= 0:
+                bd[pos] = -ln * field_eval(uD, mx, my, t)
+        return torch.as_tensor(bd)
+
+    def volume(self, mv, coeffs, f, t):
+        hm = capi.HostMesh(mv["coords"], mv["elements"], np.zeros((0, 2)), np.zeros((0, 2)))
+        B, D, M, M0 = O.assemble_volume(hm, coeffs)
+        load = O.assemble_load(hm, f, t)
+        return {"B": torch.as_tensor(B.reshape(-1, 9)), "D": torch.as_tensor(D.reshape(-1, 9)),
+                "M": torch.as_tensor(M.reshape(-1, 9)), "M0": torch.as_tensor(M0.reshape(-1, 9)),
+                "load": torch.as_tensor(load.reshape(-1, 3).copy())}
+
+    def neumann_table(self, neu_local, nN_all, positions):
+        p = self.part
+        tab = np.zeros((nN_all, 4), np.int32)
+        for pos, e in zip(positions.numpy(), neu_local.numpy()):
+            tab[pos] = [p.edge_nodes[e][0], p.edge_nodes[e][1], p.edge_elements[e][0], p.ltp[e]]
+        return torch.as_tensor(tab)
+
+    def neumann_apply(self, mv, table, dup, elo, ehi, g, t, load):
+        c = mv["coords"]
+        ln_acc = {}
+        for a, b, tp, led in table.numpy():
+            if not (elo <= tp < ehi):
+                continue
+            mx, my = 0.5 * (c[a][0] + c[b][0]), 0.5 * (c[a][1] + c[b][1])
+            dx, dy = c[b][0] - c[a][0], c[b][1] - c[a][1]
+            ln = math.sqrt(dx * dx + dy * dy)
+            val = flux_eval(g, mx, my, dy / ln, -dx / ln, t)
+            acc = ln_acc.setdefault(tp, [0.0, 0.0, 0.0])
+            for cc in range(3):
+                acc[cc] += ln * val * (0.0 if cc == led else 0.5)
+        L = load.numpy()
+        for tp, acc in ln_acc.items():
+            for cc in range(3):
+                L[tp - elo, cc] = L[tp - elo, cc] + acc[cc]
+
+    def rebase_results(self, E0, R0, nnz0):
+        rp = self.cls["retained_pos"]
+        self.cls["retained_pos"] = np.where(rp >= 0, rp + R0, -1).astype(np.int32)
+        self.cls["retained_edges"] = self.cls["retained_edges"] + E0
+        self.csr[0] = self.csr[0] + nnz0
+
+    # -- results --------------------------------------------------------------------------------------
+    def part_arrays(self):
+        p = self.part
+        return {"edge_nodes": p.edge_nodes, "edge_elements": p.edge_elements, "local_in_tplus": p.ltp,
+                "local_in_tminus": p.ltm, "interior_edges": p.interior, "boundary_edges": p.boundary,
+                "node_edge_start": p.nes}
+
+    def cls_arrays(self):
+        return {"retained_pos": self.cls["retained_pos"], "retained_edges": self.cls["retained_edges"]}
+
+    def csr_arrays(self):
+        return tuple(self.csr)
+
+    def release(self):
+        pass

@@ -70,3 +70,56 @@ def test_emulated_ranks_boundary_errors(ctx):
     states = dist.make_states(bad, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
     with pytest.raises(RuntimeError, match="resolves to an interior edge"):
         dist.distributed_pipeline(states, comm, bad.nC, bad.nE, 0, *G.config_fields(2))
+
+
+def _gloo_worker(rank, world, port, tmp, case, levels):
+    import torch.distributed as tdist
+    from paper_2401_15557_b200 import dist
+    from dist_cpu_backend import NumpyRankOps
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        hm = dict((c[0], c[1]) for c in CASES)[case]()
+        comm = dist.TorchComm()
+        states = dist.make_states(hm, comm, lambda r: NumpyRankOps())
+        states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *G.config_fields(1))
+        np.savez(os.path.join(tmp, f"rank{rank}.npz"), **dist.rank_slice(states[0]))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,levels", [("square-L3", 1), ("lshape-L2", 1), ("stress-L3", 0)])
+def test_gloo_two_ranks_equal_oracle(tmp_path, case, levels):
+    """2 gloo processes on CPU: the concatenated rank slices == the C oracle
+    run on the whole mesh (topology, maps, classification, C, bD, blocks,
+    load = b + LN)."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2401_15557_b200 import dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.start_processes(_gloo_worker, args=(2, port, str(tmp_path), case, levels), nprocs=2, join=True,
+                       start_method="fork")
+    got = dist.concat_slices([dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(2)])
+    hm = dict((c[0], c[1]) for c in CASES)[case]()
+    fine = O.refine_levels(hm, levels)
+    args = G.config_fields(1)
+    om, ot = O.build_topology(fine)
+    oc = O.classify_edges(om, ot)
+    topo, cls = ot.arrays(), oc.arrays()
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "interior_edges",
+              "boundary_edges"):
+        assert np.array_equal(got[k].reshape(-1), topo[k].reshape(-1)), k
+    for k in ("retained_pos", "retained_edges"):
+        assert np.array_equal(got[k], cls[k]), k
+    Cm = O.assemble_constraint(om, ot, oc)
+    for a, b in zip((got["C_row_ptr"], got["C_col_idx"], got["C_values"]), Cm["csr"]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(got["bd"], O.assemble_dirichlet(om, ot, oc, args[3], 0.0))
+    B, D, M, M0 = O.assemble_volume(fine, args[0])
+    for k, v in zip(("B", "D", "M", "M0"), (B, D, M, M0)):
+        assert np.array_equal(got[k], v.reshape(-1)), k
+    load = O.assemble_load(fine, args[1], 0.0) + O.assemble_neumann(om, ot, oc, args[2], 0.0)
+    assert np.array_equal(got["load"], load)
+    assert np.array_equal(got["coords"], fine.coords)
+    assert np.array_equal(got["elements"], fine.elements)
