@@ -255,9 +255,90 @@ def build_input(ctx, level):
     return dm
 
 
+def run_ours_sharded(args, rank, world, local):
+    """N > 1: the same step (L12 resident -> L13 outputs) sharded over the
+    ranks (paper_2401_15557_b200/dist.py): element ranges,
+    key-range all-to-all edge dedup over NCCL, replicated midpoints.  Every
+    rank keeps its slices; value = total L13 triangles / max-over-ranks time."""
+    import torch
+    from paper_2401_15557_b200 import capi, dist, meshgen as G
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = capi.Context(local, stream=torch.cuda.current_stream(dev).cuda_stream)
+    fields = G.config_fields(5)
+    hm = build_input(ctx, args.level - 1).download()   # L12 input (untimed), replicated
+    comm = dist.TorchComm()
+    es = dist.element_splits(hm.nE, world)
+    inp = dict(coords=torch.as_tensor(hm.coords).to(dev), elements=torch.as_tensor(hm.elements[es[rank]:es[rank + 1]]).to(dev),
+               dirichlet=torch.as_tensor(hm.dirichlet).to(dev), neumann=torch.as_tensor(hm.neumann).to(dev))
+    ops = dist.CudaRankOps(ctx, dev)
+
+    def step():
+        st = [dist.RankState(rank=rank, ops=ops, coords=inp["coords"], elements=inp["elements"],
+                             elo=int(es[rank]), ehi=int(es[rank + 1]), dirichlet=inp["dirichlet"],
+                             neumann=inp["neumann"])]
+        st, nC, nE = dist.distributed_pipeline(st, comm, hm.nC, hm.nE, 1, *fields)
+        n_own = st[0].ehi - st[0].elo
+        step.stats = st[0].stats
+        ops.release()
+        return nC, nE, n_own
+
+    for _ in range(args.warmup):
+        nC, nE, n_own = step()
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist_barrier(world)
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    with ClockSampler(local, args.clock_ms) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            nC, nE, n_own = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = dist_max(ms_local, world)
+    dist_barrier(world)
+    launches = (ctx.launches - launches0) // args.steps
+    value = nE / (ms * 1e-3)
+    peak, peak_kind = peaks()
+    # whole-job compulsory bytes of the workload (as N = 1) against N x peak
+    nE0, nC0 = hm.nE, hm.nC
+    E0 = nC - nC0                          # one midpoint per parent edge
+    E1, L1, nnz1 = step.stats["E"], step.stats["L"], step.stats["nnz"]
+    compulsory = (eg_bytes(nE0, E0) + rf_bytes(nC0, nE0, E0) + eg_bytes(nE, E1) +
+                  as_bytes(nC, nE, E1, L1, nnz1))
+    gbs = compulsory / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "triangles/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} ({nE} triangles): "
+                               "EG+RF+EG+AS, config-2 coefficients, sharded",
+                   "parallelism": f"element-range x key-range sharding over {world} GPUs (NCCL all-to-all)",
+                   "refined_edge_generation": "sort-based key-range dedup (generic)",
+                   "triangles": nE, "own_triangles_rank0": n_own, "l2": "inputs larger than L2 (no flush)"},
+        "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
+                              "peak": peak * world, "peak_kind": peak_kind, "frac": round(gbs / (peak * world), 4)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args):
     from paper_2401_15557_b200 import capi, meshgen as G
     rank, world, local = dist_init(args.gpus)
+    if (world > 1 and not args.replicas) or args.sharded:
+        if world == 1:  # --sharded at N = 1: a one-rank NCCL group (exercises the collectives)
+            import torch
+            import torch.distributed as tdist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            torch.cuda.set_device(local)
+            tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        return run_ours_sharded(args, rank, world, local)
     ctx = capi.Context(local)
     fields = G.config_fields(5)
     dm = build_input(ctx, args.level - 1)          # L12 input, resident in HBM
@@ -437,6 +518,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (multi-GPU) pipeline even at N = 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent single-GPU replicas instead of the sharded pipeline")
     ap.add_argument("--generic-eg", action="store_true",
                     help="sort-based edge generation on the refined mesh too (no SURVEY f1 shortcut)")
     args = ap.parse_args()

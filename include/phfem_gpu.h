@@ -56,7 +56,8 @@ typedef struct phfem_ctx phfem_ctx;
 
 /* ---- context ------------------------------------------------------------- */
 int phfem_abi_version(void);
-/* stream: a cudaStream_t (NULL = a new non-blocking stream owned by the ctx). */
+/* stream: a cudaStream_t (NULL = a new non-blocking stream owned by the ctx;
+ * pass cudaStreamLegacy (0x1) for the legacy default stream). */
 phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** out);
 void phfem_ctx_destroy(phfem_ctx* ctx);
 const char* phfem_ctx_message(const phfem_ctx* ctx);

@@ -273,7 +273,11 @@ class Context:
     def __init__(self, device: int = 0, stream: Optional[int] = None):
         self.lib = load_library()
         self.ptr = C.c_void_p()
-        st = self.lib.phfem_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(self.ptr))
+        # stream None: the ctx creates its own non-blocking stream.  An explicit
+        # handle 0 is torch's legacy default stream: pass cudaStreamLegacy (0x1),
+        # because a null handle would make the ctx create its own (unordered) one.
+        handle = None if stream is None else C.c_void_p(stream if stream != 0 else 1)
+        st = self.lib.phfem_ctx_create(device, handle, C.byref(self.ptr))
         if st != OK:
             raise PhfemError(st, f"phfem_ctx_create failed with status {st} (no usable sm_100 device?)")
         self.device = device

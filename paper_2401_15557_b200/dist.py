@@ -434,6 +434,8 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     for s, (E0, B0), g_ in zip(states, per, gl):
         L_all = torch.stack(g_).flatten().cpu().numpy()
         R0 = int(L_all[:s.rank].sum())
+        s.stats = {"E": Etot, "n_boundary": Btot, "L": int(L_all.sum()),
+                   "nnz": 4 * int(L_all.sum()) - 2 * (Btot - (Etot - int(L_all.sum())))}
         N0 = E0 - R0                      # Neumann edges before the rank
         nnz0 = 4 * R0 - 2 * (B0 - N0)     # retained boundary rows hold 2 entries
         mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
