@@ -24,65 +24,79 @@ __device__ __forceinline__ int dest_of(const int32_t* __restrict__ splits, int W
   return lo;
 }
 
+// Routing by destination with block-level aggregation: every thread owns
+// kRouteK items; destinations are counted in SMEM (W <= kMaxDest), one
+// global atomic per (block, destination) reserves the block's ranges, items
+// go to base[d] + SMEM rank.  (A per-warp global atomic serialised on one
+// counter at W = 1-8 and dominated the step.)  Order inside a destination is
+// irrelevant: the receiver sorts.
+constexpr int kRouteThreads = 256;
+constexpr int kRouteK = 8;
+constexpr int kMaxDest = 4097;  // also the coarse histogram's bins
+
+template <typename Item, typename Fn>
+__device__ __forceinline__ void route_block(int64_t n, int W, Fn item_of, int32_t* __restrict__ cnt,
+                                            int32_t* __restrict__ cursor, Item* __restrict__ send) {
+  __shared__ int32_t s_cnt[kMaxDest];
+  __shared__ int32_t s_base[kMaxDest];
+  const int64_t chunk = (int64_t)kRouteThreads * kRouteK;
+  for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < n; c0 += (int64_t)gridDim.x * chunk) {
+    for (int d = threadIdx.x; d < W; d += blockDim.x) s_cnt[d] = 0;
+    __syncthreads();
+    Item it[kRouteK];
+    int dst[kRouteK], rk[kRouteK];
+#pragma unroll
+    for (int k = 0; k < kRouteK; ++k) {
+      const int64_t i = c0 + (int64_t)k * kRouteThreads + threadIdx.x;
+      dst[k] = -1;
+      if (i < n) dst[k] = item_of(i, it[k]);
+      rk[k] = dst[k] >= 0 ? atomicAdd(&s_cnt[dst[k]], 1) : 0;
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < W; d += blockDim.x) {
+      const int c = s_cnt[d];
+      if (c) {
+        if (send) s_base[d] = atomicAdd(&cursor[d], c);
+        else atomicAdd(&cnt[d], c);
+      }
+    }
+    if (send) {
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kRouteK; ++k)
+        if (dst[k] >= 0) send[s_base[dst[k]] + rk[k]] = it[k];
+    }
+    __syncthreads();
+  }
+}
+
 // directed occurrences of elements [elo, ehi) (elements: the rank's local
 // array): slot s of element m is v_s -> v_{s+1} (edge_topology.cpp:61-68);
-// record {max, min, 3m+s, dir}
-__global__ void k_dist_occ(const int32_t* __restrict__ elements, int elo, int ehi,
+// record {max, min, 3m+s, dir}, routed to the owner of the max node
+__global__ void __launch_bounds__(kRouteThreads) k_dist_occ(const int32_t* __restrict__ elements, int elo, int ehi,
                            const int32_t* __restrict__ splits, int W, int32_t* __restrict__ cnt,
                            int32_t* __restrict__ cursor, int4* __restrict__ send) {
   const int64_t n = 3 * (int64_t)(ehi - elo);
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = i0 + threadIdx.x;
-    const bool valid = i < n;
-    int a = 0, b = 0, d = -1;
-    int64_t occ = 0;
-    if (valid) {
-      const int64_t ml = i / 3;
-      const int s = (int)(i % 3);
-      occ = 3 * (elo + ml) + s;
-      a = elements[3 * ml + s];
-      b = elements[3 * ml + (s + 1) % 3];
-      d = dest_of(splits, W, max(a, b));
-    }
-    const unsigned grp = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(grp) - 1;
-    if (!send) {
-      if (valid && (int)lane_id() == leader) atomicAdd(&cnt[d], __popc(grp));
-      continue;
-    }
-    int base = 0;
-    if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[d], __popc(grp));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (valid)
-      send[base + __popc(grp & lanemask_lt())] = make_int4(max(a, b), min(a, b), (int)occ, a > b ? 1 : 0);
-  }
+  route_block<int4>(n, W, [&](int64_t i, int4& r) {
+    const int64_t ml = i / 3;
+    const int s = (int)(i - 3 * ml);
+    const int a = elements[3 * ml + s], b = elements[3 * ml + (s == 2 ? 0 : s + 1)];
+    r = make_int4(max(a, b), min(a, b), (int)(3 * (elo + ml) + s), a > b ? 1 : 0);
+    return dest_of(splits, W, r.x);
+  }, cnt, cursor, send);
 }
 
 // pairs (slot 3m+l, local edge or ~local edge) -> global edge ids, routed to
 // the element owner; slot < 0 marks "no t_minus"
-__global__ void k_dist_pairs(const int2* __restrict__ pairs, int64_t n, int E0,
+__global__ void __launch_bounds__(kRouteThreads) k_dist_pairs(const int2* __restrict__ pairs, int64_t n, int E0,
                              const int32_t* __restrict__ esplits, int W, int32_t* __restrict__ cnt,
                              int32_t* __restrict__ cursor, int2* __restrict__ send) {
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = i0 + threadIdx.x;
-    int2 p = make_int2(-1, 0);
-    if (i < n) p = pairs[i];
-    const bool valid = p.x >= 0;
-    const int d = valid ? dest_of(esplits, W, p.x / 3) : -1;
-    const unsigned grp = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(grp) - 1;
-    if (!send) {
-      if (valid && (int)lane_id() == leader) atomicAdd(&cnt[d], __popc(grp));
-      continue;
-    }
-    int base = 0;
-    if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[d], __popc(grp));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (valid) {
-      const int v = p.y >= 0 ? p.y + E0 : ~(~p.y + E0);
-      send[base + __popc(grp & lanemask_lt())] = make_int2(p.x, v);
-    }
-  }
+  route_block<int2>(n, W, [&](int64_t i, int2& q) {
+    const int2 p = pairs[i];
+    if (p.x < 0) return -1;
+    q = make_int2(p.x, p.y >= 0 ? p.y + E0 : ~(~p.y + E0));
+    return dest_of(esplits, W, p.x / 3);
+  }, cnt, cursor, send);
 }
 
 __global__ void k_dist_apply(const int2* __restrict__ recv, int64_t n, int elo,
@@ -251,9 +265,10 @@ PHFEM_API phfem_status phfem_dist_occurrences(phfem_ctx* ctx, const int32_t* ele
     return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
   const int64_t n = 3 * (int64_t)(ehi - elo);
-  const int grid = grid_for(n, 256, ctx->num_sms * 8);
+  if (W >= kMaxDest) return PHFEM_ERR_INVALID_ARGUMENT;
+  const int grid = grid_for(n, kRouteThreads * kRouteK, ctx->num_sms * 8);
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, kRouteThreads, 0, ctx->stream>>>(
         elements, elo, ehi, splits, W, counts, nullptr, nullptr));
   if (!send) return PHFEM_OK;
   if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
@@ -264,7 +279,7 @@ PHFEM_API phfem_status phfem_dist_occurrences(phfem_ctx* ctx, const int32_t* ele
   PHFEM_TRY(scan_exclusive_i32(ctx, cursor, cursor, (int64_t)W + 1, nullptr));
   PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH(ctx, "k_dist_occ", k_dist_occ<<<grid, kRouteThreads, 0, ctx->stream>>>(
         elements, elo, ehi, splits, W, nullptr, cursor, reinterpret_cast<int4*>(send)));
   dfree(ctx, cursor);
   return PHFEM_OK;
@@ -275,10 +290,11 @@ PHFEM_API phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pai
                                               int32_t* counts, int32_t* offsets, int32_t* send) {
   if (!ctx || (!pairs && n) || !esplits || !counts || W < 1) return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
-  const int grid = grid_for(n, 256, ctx->num_sms * 8);
+  if (W >= kMaxDest) return PHFEM_ERR_INVALID_ARGUMENT;
+  const int grid = grid_for(n, kRouteThreads * kRouteK, ctx->num_sms * 8);
   const int2* p2 = reinterpret_cast<const int2*>(pairs);
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, kRouteThreads, 0, ctx->stream>>>(
         p2, n, E0, esplits, W, counts, nullptr, nullptr));
   if (!send) return PHFEM_OK;
   if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
@@ -289,7 +305,7 @@ PHFEM_API phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pai
   PHFEM_TRY(scan_exclusive_i32(ctx, cursor, cursor, (int64_t)W + 1, nullptr));
   PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, kRouteThreads, 0, ctx->stream>>>(
         p2, n, E0, esplits, W, nullptr, cursor, reinterpret_cast<int2*>(send)));
   dfree(ctx, cursor);
   return PHFEM_OK;

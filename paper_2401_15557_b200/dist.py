@@ -38,6 +38,32 @@ import torch
 
 from . import capi
 
+import os as _os
+import time as _time
+
+
+class _Trace:
+    """PHFEM_DIST_TRACE=1: synchronising per-phase wall times (debug only)."""
+
+    def __init__(self, states):
+        self.on = _os.environ.get("PHFEM_DIST_TRACE") is not None
+        self.t = _time.perf_counter()
+        self.dev = states[0].coords.device if states else None
+        self.rows = []
+
+    def __call__(self, what):
+        if not self.on:
+            return
+        if self.dev is not None and self.dev.type == "cuda":
+            torch.cuda.synchronize(self.dev)
+        now = _time.perf_counter()
+        self.rows.append((what, (now - self.t) * 1e3))
+        self.t = now
+
+    def dump(self):
+        if self.on:
+            print("[dist] " + "  ".join(f"{w}={ms:.2f}" for w, ms in self.rows), flush=True)
+
 NO_ERROR = -1  # int64 view of the uint64 ~0 the kernels start from (all-reduced as unsigned below)
 
 
@@ -316,25 +342,30 @@ class RankState:
 
 
 def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: np.ndarray,
-                     nbins: int = 4096):
+                     nbins_per_rank: int = 64):
     """Distributed build_topology.  Returns the key-range splits, per-state
     (E0, B0) and the global (E, n_boundary); each ops holds its part (global
     ids) and each state gets its elem_edge."""
     W = comm.world
-    nb = max(1, min(nbins, nC))
+    tr = getattr(comm, "trace", None) or (lambda w: None)
+    nb = max(1, min(nbins_per_rank * W, 4096, nC))  # key ranges balanced to ~1/64 of a share
     bins = np.asarray([nC * i // nb for i in range(nb + 1)], dtype=np.int32)
     # coarse histogram of max nodes -> balanced key ranges (identical on every rank)
     hists = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(bins), pack=False) for s in states]
     comm.all_reduce(hists, "sum")
     splits = balanced_splits(hists[0].cpu().numpy(), bins, W)
+    tr("hist")
     # forward all-to-all of the occurrences, local dedup
     packed = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(splits), pack=True) for s in states]
+    tr("pack")
     recvs = comm.all_to_all_v([p[0] for p in packed], [p[1] for p in packed])
+    tr("a2a")
     eb = []
     for s, rv in zip(states, recvs):
         r = s.rank
         E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE)
         eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
+    tr("dedup")
     gath = comm.all_gather(eb)
     per = []
     for s, g in zip(states, gath):
@@ -346,8 +377,10 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
     # reverse all-to-all: (element slot, global edge id) to the element owners
     routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits)) for s, (E0, _) in zip(states, per)]
     recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
+    tr("route")
     for s, rv in zip(states, recvs):
         s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
+    tr("pairs")
     return splits, per, (Etot, Btot)
 
 
@@ -383,12 +416,14 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     classification -> B, D, M, M0, load = b + LN, C (CSR rows), bD; every rank
     keeps its slices (collect() gathers them for tests)."""
     W = comm.world
+    tr = comm.trace = _Trace(states)
     # element ranges: the input split, x4 per refinement (children of [a,b) are [4a,4b))
     esplits = element_splits(nE, W)
     for _ in range(levels):
         splits, per, (Etot, _) = _edge_generation(states, comm, nC, nE, esplits)
         nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
         ids = _resolve(states, comm, splits, per, nD, nN)
+        tr("resolve")
         # replicated fine coordinates: old nodes + all-gathered midpoints (edge order)
         mids = [s.ops.midpoints(s.coords) for s in states]
         counts = [torch.tensor([m.shape[0]], dtype=torch.int64, device=m.device) for m in mids]
@@ -414,6 +449,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
             s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
         nC, nE = nC + Etot, 4 * nE
         esplits = 4 * esplits
+        tr("refine")
     # final level
     splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
     nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
@@ -429,6 +465,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         s.neu_local = nl[own_n].to(torch.int32).contiguous()
         Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local)], dtype=torch.int64,
                                device=s.coords.device))
+    tr("classify")
     gl = comm.all_gather(Ls)
     results = []
     for s, (E0, B0), g_ in zip(states, per, gl):
@@ -445,6 +482,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         s.E0, s.R0 = E0, R0
         s.blocks = s.ops.volume(mview, coeffs, f, t)
         s.mview = mview
+    tr("C+bd+volume")
     # Neumann: owners publish {a, b, t_plus, led}; element owners add b + LN
     all_neu = ids[0][nD:]
     dup = bool(nN) and int(torch.unique(all_neu).numel()) < nN
@@ -453,6 +491,9 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         comm.all_reduce(tables, "sum")
     for s, tb in zip(states, tables):
         s.ops.neumann_apply(s.mview, tb, dup, s.elo, s.ehi, g, t, s.blocks["load"])
+    tr("neumann")
+    tr.dump()
+    comm.trace = None
     return states, nC, nE
 
 
