@@ -198,6 +198,24 @@ phfem_status phfem_constraint_csc(phfem_ctx* ctx, const phfem_mesh* mesh,
                                   phfem_csc* out);
 void phfem_csc_release(phfem_ctx* ctx, phfem_csc* m);
 
+/* ---- generic COO -> CSC and the solve's operators ---------
+ * SparseMatrix::from_triplets (sparse.hpp:55; sparse.cpp:30-97) on device
+ * triplets [n]: first out-of-range entry -> PHFEM_ERR_OUT_OF_RANGE with the
+ * reference's message; a strictly (row, col)-increasing buffer is stored
+ * as-is, otherwise runs are summed in insertion order from 0.0; Eigen
+ * ColMajor CSC out (library-owned, phfem_csc_release).  n < 2^31.          */
+phfem_status phfem_from_triplets(phfem_ctx* ctx, int32_t rows, int32_t cols, const int32_t* ri,
+                                 const int32_t* ci, const double* v, int64_t n, phfem_csc* out);
+/* build_saddle_matrix (elliptic.hpp; elliptic.cpp:22-36): [[B+D+M, -C'],
+ * [-C, 0]] from the device blocks ([nE][9]) and C in CSC.                  */
+phfem_status phfem_saddle_matrix(phfem_ctx* ctx, int32_t nE, const double* B, const double* D,
+                                 const double* M, const phfem_csc* C, phfem_csc* out);
+/* step_matrix (parabolic.cpp:21-37): [[M0 + sign k/2 (B+D+M), -sign k/2 C'],
+ * [-sign/2 C, 0]]; step_matrices = sign +1 (M_plus) and -1 (M_minus).       */
+phfem_status phfem_step_matrix(phfem_ctx* ctx, int32_t nE, const double* B, const double* D,
+                               const double* M, const double* M0, const phfem_csc* C, double k,
+                               double sign, phfem_csc* out);
+
 /* ---- load vectors --------------------------------------------------------
  * assemble_load (assembly.hpp:84; assembly.cpp:179-203) -> out[3nE]          */
 phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_field* f,

@@ -309,3 +309,43 @@ def all_outputs(hm: HostMesh, coeffs, f, g, uD, t: float = 0.0) -> dict:
     return {"topo": ot.arrays(), "cls": oc.arrays(), "B": B, "D": D, "M": M, "M0": M0, "C_csc": Cm["csc"],
             "C_csr": Cm["csr"], "b": assemble_load(hm, f, t), "ln": assemble_neumann(om, ot, oc, g, t),
             "bd": assemble_dirichlet(om, ot, oc, uD, t), "refined": red_refine(hm, ot)}
+
+
+def from_triplets(rows: int, cols: int, ri, ci, v):
+    """SparseMatrix::from_triplets (sparse.cpp:30-97) -> (outer, inner, values)."""
+    ri = np.ascontiguousarray(ri, dtype=np.int32)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = orc_sparse()
+    err = C.create_string_buffer(512)
+    L = lib()
+    L.orc_from_triplets.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                    C.POINTER(orc_sparse), C.c_char_p, C.c_size_t]
+    _check(L.orc_from_triplets(rows, cols, _ptr(ri), _ptr(ci), _ptr(v), len(v), C.byref(out), err, 512), err)
+    r = (_arr(out.ptr, cols + 1, np.int32), _arr(out.idx, out.nnz, np.int32), _arr(out.val, out.nnz, np.float64))
+    L.orc_sparse_free(C.byref(out))
+    return r
+
+
+def operator_matrix(B, D, M, M0, C_csc, nE: int, L: int, which: int, k: float = 0.0):
+    """build_saddle_matrix (which 0, elliptic.cpp:22-36) / step_matrix sign +1
+    (which 1) / -1 (which 2) (parabolic.cpp:21-37): triplets in the
+    reference's append order -> from_triplets.  Blocks [nE][9] column-major."""
+    N = 3 * nE
+    Bf, Df, Mf = (np.asarray(x, np.float64).reshape(-1) for x in (B, D, M))
+    kk = (Bf + Df) + Mf
+    if which == 0:
+        top, s_ct, s_c = kk, -1.0, -1.0
+    else:
+        sign = 1.0 if which == 1 else -1.0
+        top = np.asarray(M0, np.float64).reshape(-1) + (sign * (k / 2.0)) * kk
+        s_ct, s_c = -sign * (k / 2.0), -sign * 0.5
+    t = np.arange(9 * nE)
+    e, q = t // 9, t % 9
+    ri_b, ci_b = 3 * e + q % 3, 3 * e + q // 3
+    outer, inner, val = C_csc
+    cols = np.repeat(np.arange(N), np.diff(outer))
+    ri = np.concatenate([ri_b, cols, N + inner])
+    ci = np.concatenate([ci_b, N + inner, cols])
+    v = np.concatenate([1.0 * top, s_ct * val, s_c * val])
+    return from_triplets(N + L, N + L, ri, ci, v)

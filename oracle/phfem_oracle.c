@@ -706,3 +706,95 @@ int orc_cn_rhs(const orc_mesh* mesh, const orc_topology* topo, const orc_classif
   orc_sparse_free(&C);
   return st;
 }
+
+
+/* ---- SparseMatrix::from_triplets (proj/src/sparse.cpp:30-97) ---------------
+ * Index check with the first offending entry (:14-27); a buffer already in
+ * strictly increasing (row, col) order is stored as-is (:41-45, :53);
+ * otherwise a stable sort by (row, col) and left-to-right run sums starting
+ * from 0.0 (:55-76); then the compressed-column fill, rows ascending in each
+ * column (:80-96).  The stable sort is a merge sort of the entry indices.   */
+static const int32_t* g_ri;
+static const int32_t* g_ci;
+
+static int trip_less(int64_t a, int64_t b) {
+  if (g_ri[a] != g_ri[b]) return g_ri[a] < g_ri[b];
+  return g_ci[a] < g_ci[b];
+}
+
+static void merge_sort_idx(int64_t* a, int64_t* tmp, int64_t n) {
+  if (n < 2) return;
+  const int64_t h = n / 2;
+  merge_sort_idx(a, tmp, h);
+  merge_sort_idx(a + h, tmp, n - h);
+  int64_t i = 0, j = h, k = 0;
+  while (i < h && j < n) tmp[k++] = trip_less(a[j], a[i]) ? a[j++] : a[i++];  /* stable */
+  while (i < h) tmp[k++] = a[i++];
+  while (j < n) tmp[k++] = a[j++];
+  memcpy(a, tmp, sizeof(int64_t) * (size_t)n);
+}
+
+int orc_from_triplets(int32_t rows, int32_t cols, const int32_t* ri, const int32_t* ci,
+                      const double* v, int64_t n, orc_sparse* out, char* err, size_t errlen) {
+  memset(out, 0, sizeof(*out));
+  for (int64_t k = 0; k < n; ++k)
+    if (ri[k] < 0 || ri[k] >= rows || ci[k] < 0 || ci[k] >= cols) {
+      snprintf(err, errlen, "TripletBuffer: entry %lld at (%d,%d) outside %dx%d", (long long)k, ri[k],
+               ci[k], rows, cols);
+      return 8; /* std::out_of_range */
+    }
+  g_ri = ri;
+  g_ci = ci;
+  int sorted_unique = 1;
+  for (int64_t k = 1; k < n && sorted_unique; ++k)
+    if (!trip_less(k - 1, k)) sorted_unique = 0;
+  int32_t* mi = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int32_t* mj = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  double* mv = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+  int64_t nnz = 0;
+  if (sorted_unique) {
+    for (int64_t k = 0; k < n; ++k) {
+      mi[k] = ri[k];
+      mj[k] = ci[k];
+      mv[k] = v[k];
+    }
+    nnz = n;
+  } else {
+    int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    for (int64_t k = 0; k < n; ++k) perm[k] = k;
+    merge_sort_idx(perm, tmp, n);
+    int64_t k = 0;
+    while (k < n) {
+      const int32_t i = ri[perm[k]], j = ci[perm[k]];
+      double sum = 0.0;
+      while (k < n && ri[perm[k]] == i && ci[perm[k]] == j) sum += v[perm[k++]];
+      mi[nnz] = i;
+      mj[nnz] = j;
+      mv[nnz] = sum;
+      ++nnz;
+    }
+    free(perm);
+    free(tmp);
+  }
+  out->rows = rows;
+  out->cols = cols;
+  out->nnz = nnz;
+  out->ptr = (int32_t*)calloc((size_t)cols + 1, sizeof(int32_t));
+  out->idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nnz ? nnz : 1));
+  out->val = (double*)malloc(sizeof(double) * (size_t)(nnz ? nnz : 1));
+  for (int64_t e = 0; e < nnz; ++e) ++out->ptr[mj[e] + 1];
+  for (int32_t c2 = 0; c2 < cols; ++c2) out->ptr[c2 + 1] += out->ptr[c2];
+  int32_t* cursor = (int32_t*)malloc(sizeof(int32_t) * (size_t)(cols ? cols : 1));
+  memcpy(cursor, out->ptr, sizeof(int32_t) * (size_t)cols);
+  for (int64_t e = 0; e < nnz; ++e) {
+    const int32_t p = cursor[mj[e]]++;
+    out->idx[p] = mi[e];
+    out->val[p] = mv[e];
+  }
+  free(cursor);
+  free(mi);
+  free(mj);
+  free(mv);
+  return 0;
+}

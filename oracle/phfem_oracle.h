@@ -81,6 +81,9 @@ int orc_node_pair_to_edge(const orc_topology* t, int k, int l);
 int orc_directed_pair_to_element(const orc_topology* t, int k, int l);
 
 int orc_build_topology(const orc_mesh* mesh, orc_topology* out, char* err, size_t errlen);
+/* SparseMatrix::from_triplets (sparse.cpp:30-97) -> Eigen ColMajor CSC       */
+int orc_from_triplets(int32_t rows, int32_t cols, const int32_t* ri, const int32_t* ci,
+                      const double* v, int64_t n, orc_sparse* out, char* err, size_t errlen);
 int orc_classify_edges(const orc_topology* topo, const orc_mesh* mesh, orc_classification* out,
                        char* err, size_t errlen);
 int orc_edge_lengths(const orc_mesh* mesh, const orc_topology* topo, double* out);

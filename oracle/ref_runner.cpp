@@ -298,6 +298,47 @@ int ref_cn_rhs(const void* mp, const void* tp, const void* cp, const phfem_coeff
   })
 }
 
+// SparseMatrix::from_triplets on a raw buffer: sizes first (outer may be NULL)
+int ref_from_triplets(int rows, int cols, const int* ri, const int* ci, const double* v, long long n,
+                      long long* nnz, int* outer, int* inner, double* vals, char* err, size_t errlen) {
+  REF_TRY({
+    TripletBuffer buf(rows, cols);
+    for (long long k = 0; k < n; ++k) buf.add(ri[k], ci[k], v[k]);
+    const SparseMatrix m = SparseMatrix::from_triplets(buf);
+    const auto& e = m.eigen();
+    *nnz = m.nonzeros();
+    if (outer) {
+      std::memcpy(outer, e.outerIndexPtr(), sizeof(int) * (size_t)(e.outerSize() + 1));
+      std::memcpy(inner, e.innerIndexPtr(), sizeof(int) * (size_t)e.nonZeros());
+      std::memcpy(vals, e.valuePtr(), sizeof(double) * (size_t)e.nonZeros());
+    }
+  })
+}
+
+// build_saddle_matrix (which = 0) / step_matrices(k).first (1) / .second (2)
+// of assemble_operators with constant coefficients: sizes first
+int ref_operator_matrix(const void* mp, const void* tp, const void* cp, const phfem_coeffs* c,
+                        int which, double k, int* dim, long long* nnz, int* outer, int* inner,
+                        double* vals, char* err, size_t errlen) {
+  REF_TRY({
+    const std::array<Vec2, 3> dummy = {Vec2(0, 0), Vec2(1, 0), Vec2(0, 1)};
+    const GlobalOperators ops =
+        assemble_operators(*static_cast<const Mesh*>(mp), *static_cast<const EdgeTopology*>(tp),
+                           *static_cast<const EdgeClassification*>(cp), coeffs_of(c, dummy));
+    SparseMatrix m;
+    if (which == 0) m = build_saddle_matrix(ops);
+    else m = which == 1 ? step_matrices(ops, k).first : step_matrices(ops, k).second;
+    const auto& e = m.eigen();
+    *dim = m.rows();
+    *nnz = m.nonzeros();
+    if (outer) {
+      std::memcpy(outer, e.outerIndexPtr(), sizeof(int) * (size_t)(e.outerSize() + 1));
+      std::memcpy(inner, e.innerIndexPtr(), sizeof(int) * (size_t)e.nonZeros());
+      std::memcpy(vals, e.valuePtr(), sizeof(double) * (size_t)e.nonZeros());
+    }
+  })
+}
+
 // CPU baseline: one bench step on the reference — build_topology, red_refine,
 // build_topology, classify_edges, B/D/M/M0, C, load + Neumann, Dirichlet.
 // Returns wall seconds; the produced triangle count in *n_out.

@@ -274,3 +274,41 @@ def all_outputs(hm: HostMesh, coeffs, f, g, uD, t=0.0) -> dict:
             "C_csr": csc_to_csr(csc, rc.L), "b": assemble_load(rm, hm.nE, f, t),
             "ln": assemble_neumann(rm, rt, rc, hm.nE, g, t), "bd": assemble_dirichlet(rm, rt, rc, uD, t),
             "refined": fine}
+
+
+def from_triplets(rows, cols, ri, ci, v):
+    ri = np.ascontiguousarray(ri, dtype=np.int32)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    L = lib()
+    L.ref_from_triplets.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t]
+    nnz = C.c_longlong()
+    err = C.create_string_buffer(512)
+    _check(L.ref_from_triplets(rows, cols, _p(ri), _p(ci), _p(v), len(v), C.byref(nnz), None, None, None,
+                               err, 512), err)
+    outer = np.zeros(cols + 1, np.int32)
+    inner = np.zeros(max(nnz.value, 1), np.int32)
+    vals = np.zeros(max(nnz.value, 1), np.float64)
+    _check(L.ref_from_triplets(rows, cols, _p(ri), _p(ci), _p(v), len(v), C.byref(nnz), _p(outer), _p(inner),
+                               _p(vals), err, 512), err)
+    return outer, inner[:nnz.value], vals[:nnz.value]
+
+
+def operator_matrix(rm, rt, rc, coeffs, which: int, k: float = 0.0):
+    """build_saddle_matrix (0) / step_matrices(k).first (1) / .second (2)."""
+    L = lib()
+    L.ref_operator_matrix.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p,
+                                      C.c_size_t]
+    dim = C.c_int()
+    nnz = C.c_longlong()
+    err = C.create_string_buffer(512)
+    _check(L.ref_operator_matrix(rm.h, rt.h, rc.h, C.byref(coeffs), which, k, C.byref(dim), C.byref(nnz), None,
+                                 None, None, err, 512), err)
+    outer = np.zeros(dim.value + 1, np.int32)
+    inner = np.zeros(nnz.value, np.int32)
+    vals = np.zeros(nnz.value, np.float64)
+    _check(L.ref_operator_matrix(rm.h, rt.h, rc.h, C.byref(coeffs), which, k, C.byref(dim), C.byref(nnz),
+                                 _p(outer), _p(inner), _p(vals), err, 512), err)
+    return outer, inner, vals

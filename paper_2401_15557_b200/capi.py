@@ -150,6 +150,7 @@ EXPORTED = [
     "phfem_dist_occurrences", "phfem_dist_dedup", "phfem_dist_route_pairs", "phfem_dist_apply_pairs",
     "phfem_dist_add_offset", "phfem_dist_resolve", "phfem_dist_classify", "phfem_dist_neumann_table",
     "phfem_dist_neumann_apply", "phfem_dist_children", "phfem_dist_midpoints",
+    "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -228,6 +229,9 @@ def load_library(path: str = LIB_PATH):
         "phfem_edge_lengths": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), vp]),
         "phfem_dist_occurrences": (C.c_int, [vp, vp, i32, i32, vp, i32, vp, vp, vp]),
         "phfem_dist_children": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+        "phfem_from_triplets": (C.c_int, [vp, i32, i32, vp, vp, vp, i64, P(phfem_csc)]),
+        "phfem_saddle_matrix": (C.c_int, [vp, i32, vp, vp, vp, P(phfem_csc), P(phfem_csc)]),
+        "phfem_step_matrix": (C.c_int, [vp, i32, vp, vp, vp, vp, P(phfem_csc), dbl, dbl, P(phfem_csc)]),
         "phfem_dist_midpoints": (C.c_int, [vp, vp, vp, i32, vp]),
         "phfem_dist_dedup": (C.c_int, [vp, vp, i64, i32, i32, i32, i32, P(phfem_topology), vp]),
         "phfem_dist_route_pairs": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp]),
