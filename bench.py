@@ -418,6 +418,8 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
 
+    if rank == 0 and world == 1 and not args.no_cn:
+        line["cn_rhs"] = run_cn_rhs(ctx, args)
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(ctx, args, fields)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -426,6 +428,51 @@ def run_ours(args):
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_cn_rhs(ctx, args):
+    """BASELINE config 3 (secondary line): square L11 (8.4 M triangles), B/D/M/M0
+    and C assembled once, then the Crank-Nicolson right-hand side for 100 steps
+    (k = 1e-3), state W ~ U[-1,1] (seed 5), solve excluded.  Bytes per step:
+    SURVEY §8(d) recompute-from-geometry variant 16 nC + 75 nE + 4 E + 16 L."""
+    import torch
+    from paper_2401_15557_b200 import capi, meshgen as G
+    coeffs, f, g, uD = G.config_fields(3)
+    dm = build_input(ctx, args.cn_level)
+    topo = capi.build_topology(ctx, dm)
+    cls = capi.classify_edges(ctx, topo, dm)
+    plan = capi.CNPlan(ctx, dm, topo, cls, coeffs, f, g, uD, 1e-3)
+    n_state = plan.n_state
+    W = G.uniform_pm1(5, n_state)
+    dW = ctx.to_device(W)
+    dr = ctx.alloc(8 * n_state)
+    for n in range(3):
+        plan.rhs_device(n, dW, dr)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.sync()
+    steps = 100
+    e0.record(stream)
+    for n in range(steps):
+        plan.rhs_device(n, dW, dr)
+    e1.record(stream)
+    ctx.sync()
+    ms = e0.elapsed_time(e1) / steps
+    nC, nE, E, L = dm.m.nC, dm.m.nE, topo.E, cls.L
+    bytes_step = 16 * nC + 75 * nE + 4 * E + 16 * L
+    peak, kind = peaks()
+    gbs = bytes_step / (ms * 1e-3) / 1e9
+    plan.close()
+    ctx.free(dW)
+    ctx.free(dr)
+    cls.release()
+    topo.release()
+    dm.release()
+    return {"workload": f"config3: square L{args.cn_level} ({nE} triangles), 100 CN right-hand sides, k=1e-3",
+            "ms_per_step": round(ms, 4), "triangles_per_s": nE / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "algorithmic_bytes_per_step": bytes_step,
+                         "peak_kind": kind}}
 
 
 def run_e2e(ctx, args, fields):
@@ -517,6 +564,8 @@ def main():
     ap.add_argument("--ref-level", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cn", action="store_true", help="skip the config-3 CN right-hand-side line")
+    ap.add_argument("--cn-level", type=int, default=11)
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) pipeline even at N = 1")

@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "elem.cuh"
 #include "kernels.cuh"
 
 struct phfem_cn_plan {
@@ -63,6 +64,9 @@ struct CnArgs {
 };
 
 constexpr int kCnThreads = 128;
+#ifndef PHFEM_CN_MIN_BLOCKS
+#define PHFEM_CN_MIN_BLOCKS 1
+#endif
 
 __device__ __forceinline__ int neu_lookup(const int32_t* __restrict__ keys, int cap, int m) {
   if (cap == 0) return -1;
@@ -75,7 +79,24 @@ __device__ __forceinline__ int neu_lookup(const int32_t* __restrict__ keys, int 
   }
 }
 
-__global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const double* __restrict__ W,
+// sin(pi x) sin(pi y) at the 3 midpoints is shared by t_n and t_{n+1}: the
+// EXP_SINSIN specialisation evaluates it once, then exp(-t) p0 * sx * sy for
+// both times in the formula's own order (phfem_fields.h).
+template <int FK>
+__device__ __forceinline__ void field_pair(const phfem_field& f, double x, double y, double t0,
+                                           double t1, double e0, double e1, double& f0, double& f1) {
+  if (FK == PHFEM_FIELD_EXP_SINSIN) {
+    const double sx = sin_fast(PHFEM_PI * x), sy = sin_fast(PHFEM_PI * y);
+    f0 = e0 * sx * sy;
+    f1 = e1 * sx * sy;
+  } else {
+    f0 = field_dev<FK>(f, x, y, t0);
+    f1 = field_dev<FK>(f, x, y, t1);
+  }
+}
+
+template <int FK, int CK>
+__global__ void __launch_bounds__(kCnThreads, PHFEM_CN_MIN_BLOCKS) k_cn_elements(CnArgs a, const double* __restrict__ W,
                                                             double* __restrict__ rhs) {
   __shared__ __align__(16) double tile[kCnThreads * 3];
   const int64_t ntiles = ((int64_t)a.nE + kCnThreads - 1) / kCnThreads;
@@ -90,10 +111,28 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const doub
                         __ldg(a.elements + 3 * m + 2)};
       const double2 v[3] = {__ldg(a.coords + t[0]), __ldg(a.coords + t[1]), __ldg(a.coords + t[2])};
       const double U[3] = {W[3 * m], W[3 * m + 1], W[3 * m + 2]};
-      const phfem_coeff_values cv =
-          phfem_coeffs_eval(&a.c, v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y);
-      double b[9], d[9], mm[9], m0[9];
-      phfem_local_blocks(v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y, &cv, b, d, mm, m0);
+      const phfem_coeff_values cv = coeffs_dev<CK>(a.c, v[0], v[1], v[2]);
+      // the M_minus top block is formed entry by entry below (no 4 x 9 block
+      // arrays in registers): the same expressions as phfem_stiffness /
+      // convection_dev / phfem_mass / phfem_unit_mass, so the same bits
+      const phfem_geom g = geometry_dev(v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y);
+      double rx[3], ry[3], dj[3];
+      const double a3 = div3(g.area);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        rx[i] = cv.a00 * g.gx[i] + cv.a01 * g.gy[i];
+        ry[i] = cv.a10 * g.gx[i] + cv.a11 * g.gy[i];
+        dj[i] = a3 * (cv.px * g.gx[i] + cv.py * g.gy[i]);
+      }
+      const double md = cv.delta * g.area * (1.0 / 6.0), mo = cv.delta * g.area * (1.0 / 12.0);
+      const double ud = g.area * (1.0 / 6.0), uo = g.area * (1.0 / 12.0);
+      auto top = [&](int i, int j) {  // M0(i,j) + s ((B(i,j) + D(i,j)) + M(i,j))
+        const int lo = i < j ? i : j, hi = i < j ? j : i;  // B from the upper triangle
+        const double bij = g.area * (rx[lo] * g.gx[hi] + ry[lo] * g.gy[hi]);
+        const double mij = i == j ? md : mo;
+        const double m0ij = i == j ? ud : uo;
+        return m0ij + a.s_top * ((bij + dj[j]) + mij);
+      };
 
       // edges of m: id, orientation, multiplier row, length
       int e[3], rp[3];
@@ -125,15 +164,14 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const doub
         const double area =
             0.5 * ((v[1].x - v[0].x) * (v[2].y - v[0].y) - (v[1].y - v[0].y) * (v[2].x - v[0].x));
         double f0[3], f1[3];
+        const double e0 = exp(-a.t0) * a.f.p[0], e1 = exp(-a.t1) * a.f.p[0];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) field_pair<FK>(a.f, mx[i], my[i], a.t0, a.t1, e0, e1, f0[i], f1[i]);
+        const double w = div3(area) * 0.5;  // area / 3.0 * 0.5 (assembly.cpp:199)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          f0[i] = phfem_field_eval(&a.f, mx[i], my[i], a.t0);
-          f1[i] = phfem_field_eval(&a.f, mx[i], my[i], a.t1);
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          b0[i] = 0.0 + area / 3.0 * 0.5 * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
-          b1[i] = 0.0 + area / 3.0 * 0.5 * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
+          b0[i] = 0.0 + w * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
+          b1[i] = 0.0 + w * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
         }
         const int slot = neu_lookup(a.neu_keys, a.neu_cap, (int)m);
         if (slot >= 0) {
@@ -150,11 +188,7 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const doub
       for (int i = 0; i < 3; ++i) {
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int q = 3 * j + i;
-          const double top = m0[q] + a.s_top * ((b[q] + d[q]) + mm[q]);
-          acc += (0.0 + 1.0 * top) * U[j];
-        }
+        for (int j = 0; j < 3; ++j) acc += (0.0 + 1.0 * top(i, j)) * U[j];
         int ka = (i + 1) % 3, kb = (i + 2) % 3;  // edges with R[k][i] != 0
         if (rp[kb] >= 0 && (rp[ka] < 0 || rp[kb] < rp[ka])) {
           const int x = ka;
@@ -166,31 +200,6 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const doub
         out3[i] = acc + a.kh * (((b0[i] + l0[i]) + b1[i]) + l1[i]);
       }
 
-      // multiplier rows of the retained edges m owns as t_plus
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        if (!plus[k] || rp[k] < 0) continue;
-        const double cp = 0.0 + a.s_c * (len[k] * 0.5);
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (c != k) acc += cp * U[c];
-        const int tm = a.edge_elements[2 * e[k] + 1];
-        double bdsum = 0.0 + 0.0;
-        if (tm >= 0) {
-          const int ledtn = a.ltm[e[k]];
-          const double cm = 0.0 + a.s_c * (-len[k] * 0.5);
-          for (int c = 0; c < 3; ++c)
-            if (c != ledtn) acc += cm * W[3 * (int64_t)tm + c];
-        } else if ((a.dir_bits[e[k] >> 5] >> (e[k] & 31)) & 1u) {
-          const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
-          const double midx = 0.5 * (pa.x + pb.x), midy = 0.5 * (pa.y + pb.y);
-          const double bd0 = -len[k] * phfem_field_eval(&a.uD, midx, midy, a.t0);
-          const double bd1 = -len[k] * phfem_field_eval(&a.uD, midx, midy, a.t1);
-          bdsum = bd0 + bd1;
-        }
-        rhs[a.N + rp[k]] = acc + 0.5 * bdsum;
-      }
     }
     // coalesced store of the primal rows
     __syncthreads();
@@ -207,6 +216,45 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_elements(CnArgs a, const doub
     } else {
       for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = tile[i];
     }
+  }
+}
+
+// Multiplier rows, one thread per edge (the retained ones write): row l of
+// M_minus W is 0.0 + sum over the row's columns ascending — T+ DOFs, then T-
+// DOFs (t_plus < t_minus) — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor
+// SpMV, from_triplets' 0.0 +), then + 0.5 (bD^n + bD^{n+1}) (parabolic.cpp:103).
+__global__ void __launch_bounds__(256) k_cn_edges(CnArgs a, const int32_t* __restrict__ edge_nodes,
+                                                   const int32_t* __restrict__ ltp, int E,
+                                                   const double* __restrict__ W, double* __restrict__ rhs) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int rp = a.rpos[e];
+    if (rp < 0) continue;
+    const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+    const int2 el = reinterpret_cast<const int2*>(a.edge_elements)[e];
+    const double2 pa = __ldg(a.coords + ab.x), pb = __ldg(a.coords + ab.y);
+    const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+    const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+    const int l = ltp[e];
+    const double cp = 0.0 + a.s_c * (len * 0.5);  // assembly.cpp:160
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (c != l) acc += cp * W[3 * (int64_t)el.x + c];
+    double bdsum = 0.0 + 0.0;
+    if (el.y >= 0) {
+      const int l2 = a.ltm[e];
+      const double cm = 0.0 + a.s_c * (-len * 0.5);  // assembly.cpp:164
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (c != l2) acc += cm * W[3 * (int64_t)el.y + c];
+    } else if ((a.dir_bits[e >> 5] >> (e & 31)) & 1u) {
+      const double midx = 0.5 * (pa.x + pb.x), midy = 0.5 * (pa.y + pb.y);
+      const double bd0 = -len * phfem_field_eval(&a.uD, midx, midy, a.t0);  // assembly.cpp:239
+      const double bd1 = -len * phfem_field_eval(&a.uD, midx, midy, a.t1);
+      bdsum = bd0 + bd1;
+    }
+    rhs[a.N + rp] = acc + 0.5 * bdsum;
   }
 }
 
@@ -314,7 +362,25 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
   if (a.nE > 0) {
     const int64_t ntiles = ((int64_t)a.nE + kCnThreads - 1) / kCnThreads;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 16);
-    PHFEM_LAUNCH(ctx, "k_cn_elements", k_cn_elements<<<grid, kCnThreads, 0, ctx->stream>>>(a, state, rhs));
+    const int fk = (a.f.kind == PHFEM_FIELD_EXP_SINSIN || a.f.kind == PHFEM_FIELD_SINSIN ||
+                    a.f.kind == PHFEM_FIELD_ZERO) ? a.f.kind : kKindGeneric;
+    const bool cp = a.c.kind == PHFEM_COEFF_CENTROID_POLY;
+#define PHFEM_CN(F)                                                                                   \
+  do {                                                                                                \
+    if (cp)                                                                                           \
+      PHFEM_LAUNCH(ctx, "k_cn_elements", (k_cn_elements<F, PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, state, rhs))); \
+    else                                                                                              \
+      PHFEM_LAUNCH(ctx, "k_cn_elements", (k_cn_elements<F, PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, state, rhs))); \
+  } while (0)
+    if (fk == PHFEM_FIELD_EXP_SINSIN) PHFEM_CN(PHFEM_FIELD_EXP_SINSIN);
+    else if (fk == PHFEM_FIELD_SINSIN) PHFEM_CN(PHFEM_FIELD_SINSIN);
+    else if (fk == PHFEM_FIELD_ZERO) PHFEM_CN(PHFEM_FIELD_ZERO);
+    else PHFEM_CN(kKindGeneric);
+#undef PHFEM_CN
+  }
+  if (p->topo.E > 0) {
+    PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->topo.E, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        a, p->topo.edge_nodes, p->topo.local_in_tplus, p->topo.E, state, rhs));
   }
   return PHFEM_OK;
 }
