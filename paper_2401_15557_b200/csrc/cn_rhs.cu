@@ -19,6 +19,7 @@
 // DOFs: ascending columns), including the Dirichlet data.  Neumann data enter
 // through the per-element table of assemble.cu, evaluated once per step.
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 #include "elem.cuh"
@@ -35,6 +36,12 @@ struct phfem_cn_plan {
   double* neu_vals0 = nullptr;  // [cap][3] LN at t_n
   double* neu_vals1 = nullptr;  // [cap][3] LN at t_{n+1}
   uint32_t* dir_bits = nullptr; // Dirichlet edge bitmap
+  // stored-operator path (sin-sin / zero loads): the time-independent parts of
+  // every element, computed once by k_cn_pre with the assembly's expressions
+  double* top = nullptr;  // [nE][9] M_minus top-block entries as stored: 0.0 + (M0 + s((B+D)+M))
+  double* cpl = nullptr;  // [nE][3] C' entries of the element's edge slots: 0.0 + s_ct (+-|E|/2)
+  double* lw = nullptr;   // [nE] load weight (|T|/3) * 0.5
+  double* sxy = nullptr;  // [nE][3][2] sin(pi x), sin(pi y) at the edge midpoints
 };
 
 namespace phfem {
@@ -219,6 +226,159 @@ __global__ void __launch_bounds__(kCnThreads, PHFEM_CN_MIN_BLOCKS) k_cn_elements
   }
 }
 
+// ---- stored-operator path ---------------------------------------------------------
+// Once per plan: everything of an element that does not depend on t or W.
+template <int CK>
+__global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restrict__ top,
+                                                        double* __restrict__ cpl, double* __restrict__ lw,
+                                                        double* __restrict__ sxy) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < a.nE;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v[3] = {a.coords[a.elements[3 * m]], a.coords[a.elements[3 * m + 1]],
+                          a.coords[a.elements[3 * m + 2]]};
+    const phfem_coeff_values cv = coeffs_dev<CK>(a.c, v[0], v[1], v[2]);
+    const phfem_geom g = geometry_dev(v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y);
+    const double a3 = div3(g.area);
+    double rx[3], ry[3], dj[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      rx[i] = cv.a00 * g.gx[i] + cv.a01 * g.gy[i];
+      ry[i] = cv.a10 * g.gx[i] + cv.a11 * g.gy[i];
+      dj[i] = a3 * (cv.px * g.gx[i] + cv.py * g.gy[i]);
+    }
+    const double md = cv.delta * g.area * (1.0 / 6.0), mo = cv.delta * g.area * (1.0 / 12.0);
+    const double ud = g.area * (1.0 / 6.0), uo = g.area * (1.0 / 12.0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int lo = i < j ? i : j, hi = i < j ? j : i;  // B from the upper triangle
+        const double bij = g.area * (rx[lo] * g.gx[hi] + ry[lo] * g.gy[hi]);
+        const double t = (i == j ? ud : uo) + a.s_top * ((bij + dj[j]) + (i == j ? md : mo));
+        top[9 * m + 3 * j + i] = 0.0 + 1.0 * t;  // from_triplets stores 0.0 + value
+      }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
+      const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+      const double len = sqrt(dx * dx + dy * dy);
+      const bool plus = a.elem_edge[3 * m + k] >= 0;
+      cpl[3 * m + k] = 0.0 + a.s_ct * (plus ? len * 0.5 : -len * 0.5);  // assembly.cpp:160,164
+      const double mx = 0.5 * (pa.x + pb.x), my = 0.5 * (pa.y + pb.y);
+      sxy[6 * m + 2 * k] = sin_fast(PHFEM_PI * mx);
+      sxy[6 * m + 2 * k + 1] = sin_fast(PHFEM_PI * my);
+    }
+    const double area = 0.5 * ((v[1].x - v[0].x) * (v[2].y - v[0].y) - (v[1].y - v[0].y) * (v[2].x - v[0].x));
+    lw[m] = div3(area) * 0.5;
+  }
+}
+
+// warp-cooperative coalesced load of a per-element record of `per` doubles
+// for the warp's 32 consecutive elements into SMEM (stride `per`)
+__device__ __forceinline__ void warp_load(const double* __restrict__ g, int64_t base, int n_valid, int per,
+                                          double* buf) {
+  const int lane = threadIdx.x & 31;
+  const int count = n_valid * per;
+  const double* src = g + base * per;
+  for (int i = lane; i < count; i += 32) buf[i] = __ldg(src + i);
+  __syncwarp();
+}
+
+// Per step: c = exp(-t) p0 (exp-sin-sin) or p0 (sin-sin); f = (c sx) sy in the
+// formula's own order; the stored blocks replace all geometry.
+__global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, const double* __restrict__ top,
+                                                          const double* __restrict__ cpl,
+                                                          const double* __restrict__ lw,
+                                                          const double* __restrict__ sxy, double c0,
+                                                          double c1, const double* __restrict__ W,
+                                                          double* __restrict__ rhs) {
+  __shared__ __align__(16) double sbuf[kCnThreads / 32][32 * 9];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* buf = sbuf[warp];
+  const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
+  for (int64_t ch = (int64_t)blockIdx.x * (kCnThreads / 32) + warp; ch < nchunks;
+       ch += (int64_t)gridDim.x * (kCnThreads / 32)) {
+    const int64_t base = ch * 32;
+    const int n_valid = (int)((int64_t)a.nE - base < 32 ? (int64_t)a.nE - base : 32);
+    const int64_t m = base + lane;
+    const bool valid = lane < n_valid;
+    // stored top block (72 B / element)
+    __syncwarp();
+    warp_load(top, base, n_valid, 9, buf);
+    double T[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) T[q] = valid ? buf[9 * lane + q] : 0.0;
+    __syncwarp();
+    warp_load(sxy, base, n_valid, 6, buf);
+    double sx[3], sy[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      sx[k] = valid ? buf[6 * lane + 2 * k] : 0.0;
+      sy[k] = valid ? buf[6 * lane + 2 * k + 1] : 0.0;
+    }
+    __syncwarp();
+    warp_load(cpl, base, n_valid, 3, buf);
+    double cv3[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cv3[k] = valid ? buf[3 * lane + k] : 0.0;
+    __syncwarp();
+    warp_load(W, base, n_valid, 3, buf);  // U of the warp's elements
+    double out3[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+      const double U[3] = {buf[3 * lane], buf[3 * lane + 1], buf[3 * lane + 2]};
+      int rp[3];
+      double lam[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int s = __ldg(a.elem_edge + 3 * m + k);
+        rp[k] = __ldg(a.rpos + (s >= 0 ? s : ~s));
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) lam[k] = rp[k] >= 0 ? W[a.N + rp[k]] : 0.0;
+      const double w = __ldg(lw + m);
+      double f0[3], f1[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        f0[i] = c0 * sx[i] * sy[i];
+        f1[i] = c1 * sx[i] * sy[i];
+      }
+      double l0[3] = {0.0, 0.0, 0.0}, l1[3] = {0.0, 0.0, 0.0};
+      const int slot = neu_lookup(a.neu_keys, a.neu_cap, (int)m);
+      if (slot >= 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          l0[i] = a.neu0[3 * slot + i];
+          l1[i] = a.neu1[3 * slot + i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) acc += T[3 * j + i] * U[j];
+        int ka = (i + 1) % 3, kb = (i + 2) % 3;  // edges with R[k][i] != 0, ascending rows
+        if (rp[kb] >= 0 && (rp[ka] < 0 || rp[kb] < rp[ka])) {
+          const int x = ka;
+          ka = kb;
+          kb = x;
+        }
+        if (rp[ka] >= 0) acc += cv3[ka] * lam[ka];
+        if (rp[kb] >= 0) acc += cv3[kb] * lam[kb];
+        const double b0 = 0.0 + w * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
+        const double b1 = 0.0 + w * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
+        out3[i] = acc + a.kh * (((b0 + l0[i]) + b1) + l1[i]);
+      }
+    }
+    // coalesced store through the warp's SMEM slice
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 3; ++i) buf[3 * lane + i] = out3[i];
+    __syncwarp();
+    double* dst = rhs + base * 3;
+    for (int i = lane; i < n_valid * 3; i += 32) dst[i] = buf[i];
+  }
+}
+
 // Multiplier rows, one thread per edge (the retained ones write): row l of
 // M_minus W is 0.0 + sum over the row's columns ascending — T+ DOFs, then T-
 // DOFs (t_plus < t_minus) — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor
@@ -308,6 +468,35 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
     }
     if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
   }
+  const bool sinsin = f->kind == PHFEM_FIELD_SINSIN || f->kind == PHFEM_FIELD_EXP_SINSIN ||
+                      f->kind == PHFEM_FIELD_ZERO;
+  if (st == PHFEM_OK && sinsin && mesh->nE > 0) {
+    const int64_t nE = mesh->nE;
+    st = dalloc(ctx, &p->top, 9 * nE);
+    if (st == PHFEM_OK) st = dalloc(ctx, &p->cpl, 3 * nE);
+    if (st == PHFEM_OK) st = dalloc(ctx, &p->lw, nE);
+    if (st == PHFEM_OK) st = dalloc(ctx, &p->sxy, 6 * nE);
+    if (st == PHFEM_OK) {
+      CnArgs a;
+      memset(&a, 0, sizeof a);
+      a.coords = (const double2*)mesh->coords;
+      a.elements = mesh->elements;
+      a.elem_edge = topo->elem_edge;
+      a.nE = mesh->nE;
+      a.c = *c;
+      const double sign = -1.0;
+      a.s_top = sign * (k / 2.0);
+      a.s_ct = -sign * (k / 2.0);
+      const int grid = grid_for(nE, kCnThreads, ctx->num_sms * 16);
+      KTimer kt(ctx, "k_cn_pre");
+      if (c->kind == PHFEM_COEFF_CENTROID_POLY)
+        k_cn_pre<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy);
+      else
+        k_cn_pre<PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy);
+      ctx->launches++;
+      if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
+    }
+  }
   if (st != PHFEM_OK) {
     phfem_cn_plan_destroy(ctx, p);
     return st;
@@ -322,6 +511,10 @@ PHFEM_API void phfem_cn_plan_destroy(phfem_ctx* ctx, phfem_cn_plan* p) {
   dfree(ctx, p->neu_vals0);
   dfree(ctx, p->neu_vals1);
   dfree(ctx, p->dir_bits);
+  dfree(ctx, p->top);
+  dfree(ctx, p->cpl);
+  dfree(ctx, p->lw);
+  dfree(ctx, p->sxy);
   delete p;
 }
 
@@ -359,7 +552,20 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
   a.t0 = t0;
   a.t1 = t1;
   a.vec = (((uintptr_t)rhs) & 15u) == 0;
-  if (a.nE > 0) {
+  if (a.nE > 0 && p->top) {
+    // c = exp(-t) p0 / p0 / 0: the leading factor of the sin-sin formulas
+    double c0 = 0.0, c1 = 0.0;
+    if (a.f.kind == PHFEM_FIELD_EXP_SINSIN) {
+      c0 = std::exp(-t0) * a.f.p[0];
+      c1 = std::exp(-t1) * a.f.p[0];
+    } else if (a.f.kind == PHFEM_FIELD_SINSIN) {
+      c0 = c1 = a.f.p[0];
+    }
+    const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
+    const int grid = (int)std::min<int64_t>((nchunks + 3) / 4, (int64_t)ctx->num_sms * 16);
+    PHFEM_LAUNCH(ctx, "k_cn_stored", k_cn_stored<<<grid, kCnThreads, 0, ctx->stream>>>(
+        a, p->top, p->cpl, p->lw, p->sxy, c0, c1, state, rhs));
+  } else if (a.nE > 0) {
     const int64_t ntiles = ((int64_t)a.nE + kCnThreads - 1) / kCnThreads;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 16);
     const int fk = (a.f.kind == PHFEM_FIELD_EXP_SINSIN || a.f.kind == PHFEM_FIELD_SINSIN ||

@@ -1,3 +1,2 @@
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k cn_rhs > gpurun_out/cn_tests.log 2>&1; echo exit $? >> gpurun_out/cn_tests.log
 python tools/_cn_var.py > gpurun_out/cnvar.log 2>&1
-for v in cn6 cn8; do PHFEM_LIB=paper_2401_15557_b200/variants/libphfem_b200_$v.so python tools/_cn_var.py >> gpurun_out/cnvar.log 2>&1; done
