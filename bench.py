@@ -505,6 +505,7 @@ def run_e2e(ctx, args, fields):
             C.byref(fields[3]), 0.0, C.byref(out)))
         if dst is not None:
             ctx.check(lib.phfem_pipeline_download(ctx.ptr, C.byref(out), C.byref(dst)))
+            run_once.wire = int(lib.phfem_pipeline_download_bytes(C.byref(out), C.byref(dst)))
         lib.phfem_pipeline_release(ctx.ptr, C.byref(out))
 
     # sizes -> pinned destination buffers
@@ -546,9 +547,13 @@ def run_e2e(ctx, args, fields):
     for _ in range(steps):
         run_once(dst)
     dt = (time.perf_counter() - t0) / steps
+    wire = run_once.wire
     return {"value": nE_final / dt, "unit": "triangles/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": need, "ms_per_step": dt * 1e3, "steps": steps,
-            "note": "phfem_pipeline_from_host + phfem_pipeline_download (every output) with pinned host buffers"}
+            "d2h_bytes_per_step": wire, "delivered_bytes_per_step": need, "ms_per_step": dt * 1e3,
+            "steps": steps,
+            "note": "phfem_pipeline_from_host + phfem_pipeline_download (every output, reference layouts, "
+                    "in pinned host buffers; compact PCIe encodings of the blocks / C / locals expanded "
+                    "on the host)"}
 
 
 def main():

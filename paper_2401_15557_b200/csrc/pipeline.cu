@@ -195,64 +195,4 @@ PHFEM_API phfem_status phfem_pipeline_from_host(phfem_ctx* ctx, const double* co
   return st;
 }
 
-namespace {
-struct Piece {
-  void* dst;
-  const void* src;
-  size_t bytes;
-};
-}  // namespace
-
-static int collect_pieces(const phfem_pipeline_out* o, const phfem_pipeline_host* d, Piece* p) {
-  int n = 0;
-  auto add = [&](void* dst, const void* src, size_t bytes) {
-    if (dst && bytes) p[n++] = Piece{dst, src, bytes};
-  };
-  const size_t nC = o->mesh.nC, nE = o->mesh.nE, E = o->topo.E, L = o->cls.L;
-  add(d->coords, o->mesh.coords, 16 * nC);
-  add(d->elements, o->mesh.elements, 12 * nE);
-  add(d->dirichlet, o->mesh.dirichlet, 8 * (size_t)o->mesh.nD);
-  add(d->neumann, o->mesh.neumann, 8 * (size_t)o->mesh.nN);
-  add(d->edge_nodes, o->topo.edge_nodes, 8 * E);
-  add(d->edge_elements, o->topo.edge_elements, 8 * E);
-  add(d->local_in_tplus, o->topo.local_in_tplus, 4 * E);
-  add(d->local_in_tminus, o->topo.local_in_tminus, 4 * E);
-  add(d->interior_edges, o->topo.interior_edges, 4 * (size_t)o->topo.n_interior);
-  add(d->boundary_edges, o->topo.boundary_edges, 4 * (size_t)o->topo.n_boundary);
-  add(d->elem_edge, o->topo.elem_edge, 12 * nE);
-  add(d->dirichlet_edge_ids, o->cls.dirichlet_edge_ids, 4 * (size_t)o->cls.nD);
-  add(d->neumann_edge_ids, o->cls.neumann_edge_ids, 4 * (size_t)o->cls.nN);
-  add(d->retained_edges, o->cls.retained_edges, 4 * L);
-  add(d->retained_pos, o->cls.retained_pos, 4 * E);
-  add(d->C_row_ptr, o->C.row_ptr, 4 * (L + 1));
-  add(d->C_col_idx, o->C.col_idx, 4 * (size_t)o->C.nnz);
-  add(d->C_values, o->C.values, 8 * (size_t)o->C.nnz);
-  add(d->B, o->B, 72 * nE);
-  add(d->D, o->D, 72 * nE);
-  add(d->M, o->M, 72 * nE);
-  add(d->M0, o->M0, 72 * nE);
-  add(d->load, o->load, 24 * nE);
-  add(d->bd, o->bd, 8 * L);
-  return n;
-}
-
-PHFEM_API int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* out,
-                                                const phfem_pipeline_host* dst) {
-  Piece p[32];
-  const int n = collect_pieces(out, dst, p);
-  int64_t total = 0;
-  for (int i = 0; i < n; ++i) total += (int64_t)p[i].bytes;
-  return total;
-}
-
-PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipeline_out* out,
-                                               const phfem_pipeline_host* dst) {
-  if (!ctx || !out || !dst) return PHFEM_ERR_INVALID_ARGUMENT;
-  Piece p[32];
-  const int n = collect_pieces(out, dst, p);
-  for (int i = 0; i < n; ++i)
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(p[i].dst, p[i].src, p[i].bytes, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return PHFEM_OK;
-}
+// phfem_pipeline_download / _download_bytes: download.cu

@@ -395,3 +395,43 @@ def test_fastmath_selftest(ctx):
     assert out[0] == 0, f"{out[0]} fast divisions differ from IEEE division"
     assert out[2] == 0, f"{out[2]} divisions by 3 differ"
     assert out[1] <= 2, f"sin_fast off by {out[1]} ulp"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["square-L4-1", "lshape-L3-1", "crisscross-L2-0"])
+def test_host_buffer_pipeline_equals_device_outputs(ctx, case):
+    """phfem_pipeline_from_host + phfem_pipeline_download (the drop-in / e2e
+    path: compact PCIe encodings expanded on the host) reproduce every device
+    output bit for bit, for full and partial selections of outputs."""
+    import ctypes as Cc
+    name, lv, levels = case.rsplit("-", 2)[0], int(case.split("-")[1][1:]), int(case.rsplit("-", 1)[1])
+    base = {"square": G.square_2tri, "lshape": G.lshape_6tri, "crisscross": G.crisscross_square}[name.split("-")[0]]
+    hm = O.refine_levels(base(), lv)
+    args = G.config_fields(2 if name != "crisscross" else 1)
+    ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args).download()
+    out = capi.phfem_pipeline_out()
+    ctx.check(ctx.lib.phfem_pipeline_from_host(
+        ctx.ptr, hm.coords.ctypes.data_as(Cc.c_void_p), hm.elements.ctypes.data_as(Cc.c_void_p),
+        hm.dirichlet.ctypes.data_as(Cc.c_void_p), hm.neumann.ctypes.data_as(Cc.c_void_p), hm.nC, hm.nE,
+        len(hm.dirichlet), len(hm.neumann), levels, Cc.byref(args[0]), Cc.byref(args[1]), Cc.byref(args[2]),
+        Cc.byref(args[3]), 0.0, Cc.byref(out)))
+    o = out
+    shapes = {"coords": ((o.mesh.nC, 2), np.float64), "elements": ((o.mesh.nE, 3), np.int32),
+              "edge_nodes": ((o.topo.E, 2), np.int32), "edge_elements": ((o.topo.E, 2), np.int32),
+              "local_in_tplus": ((o.topo.E,), np.int32), "local_in_tminus": ((o.topo.E,), np.int32),
+              "elem_edge": ((o.mesh.nE, 3), np.int32), "retained_edges": ((o.cls.L,), np.int32),
+              "retained_pos": ((o.topo.E,), np.int32), "C_row_ptr": ((o.cls.L + 1,), np.int32),
+              "C_col_idx": ((o.C.nnz,), np.int32), "C_values": ((o.C.nnz,), np.float64),
+              "B": ((o.mesh.nE, 9), np.float64), "D": ((o.mesh.nE, 9), np.float64),
+              "M": ((o.mesh.nE, 9), np.float64), "M0": ((o.mesh.nE, 9), np.float64),
+              "load": ((3 * o.mesh.nE,), np.float64), "bd": ((o.cls.L,), np.float64)}
+    for sel in (list(shapes), ["B", "M0", "C_values", "local_in_tminus", "load"]):
+        bufs = {k: np.full(shapes[k][0], -7, dtype=shapes[k][1]) for k in sel}
+        dst = capi.phfem_pipeline_host(**{k: bufs[k].ctypes.data for k in sel})
+        ctx.check(ctx.lib.phfem_pipeline_download(ctx.ptr, Cc.byref(out), Cc.byref(dst)))
+        want = {"coords": ref["mesh"].coords, "elements": ref["mesh"].elements, **ref["topo"], **ref["cls"],
+                **{k: ref[k] for k in ("C_row_ptr", "C_col_idx", "C_values", "B", "D", "M", "M0", "load", "bd")}}
+        for k in sel:
+            a, b = bufs[k].reshape(-1), np.asarray(want[k]).reshape(-1)
+            assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8)), k
+    ctx.lib.phfem_pipeline_release(ctx.ptr, Cc.byref(out))
