@@ -112,12 +112,26 @@ __device__ __forceinline__ void element_load_dev(double2 v0, double2 v1, double2
   const double my[3] = {0.5 * (v1.y + v2.y), 0.5 * (v2.y + v0.y), 0.5 * (v0.y + v1.y)};
   const double area = 0.5 * ((v1.x - v0.x) * (v2.y - v0.y) - (v1.y - v0.y) * (v2.x - v0.x));
   double fm[3];
+  if (FK == PHFEM_FIELD_SINSIN || FK == PHFEM_FIELD_EXP_SINSIN) {
+    // one range check for the element's 6 sines instead of one branch each
+    bool ok = true;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    if (FK == kKindSamples) fm[i] = valid ? samples[3 * m + i] : 0.0;
-    else fm[i] = field_dev<FK>(f, mx[i], my[i], t);
-    if (valid && !isfinite(fm[i])) atomicMin(&err->load_nan, (unsigned long long)m);
+    for (int i = 0; i < 3; ++i) ok = ok && sin_fast_ok(PHFEM_PI * mx[i]) && sin_fast_ok(PHFEM_PI * my[i]);
+    const double c = FK == PHFEM_FIELD_EXP_SINSIN ? exp(-t) * f.p[0] : f.p[0];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      fm[i] = ok ? c * sin_fast_core(PHFEM_PI * mx[i]) * sin_fast_core(PHFEM_PI * my[i])
+                 : field_dev<FK>(f, mx[i], my[i], t);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (FK == kKindSamples) fm[i] = valid ? samples[3 * m + i] : 0.0;
+      else fm[i] = field_dev<FK>(f, mx[i], my[i], t);
+    }
   }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (valid && !isfinite(fm[i])) atomicMin(&err->load_nan, (unsigned long long)m);
   const double w = div3(area) * 0.5;
 #pragma unroll
   for (int i = 0; i < 3; ++i) bl[i] = 0.0 + w * (fm[(i + 1) % 3] + fm[(i + 2) % 3]);
