@@ -242,6 +242,16 @@ def run_reference(args):
 
 
 # ---- GPU side ---------------------------------------------------------------------
+def ncu_traffic(level, kernel):
+    """Per-launch DRAM bytes of `kernel` at `level` from the committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(f"L{level}:{kernel}")
+    except (OSError, ValueError):
+        return None
+
+
 def build_input(ctx, level):
     from paper_2401_15557_b200 import capi, meshgen as G
     dm = capi.DeviceMesh.upload(ctx, G.square_2tri())
@@ -392,8 +402,11 @@ def run_ours(args):
         gbs = b / (kms / args.steps * 1e-3) / 1e9
         per_kernel[k] = {"ms": round(kms / args.steps, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks()[0], 4)}
     step_share = {k: round(v[0] / args.steps / ms_local, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    traffic = ncu_traffic(args.level, dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "algorithmic_bytes_per_step": per_step_bytes,
                 "kernel_ms_per_step": round(dom_ms / args.steps, 4)}
     pipeline_gbs = compulsory / (ms_local * 1e-3) / 1e9
@@ -434,7 +447,8 @@ def run_cn_rhs(ctx, args):
     """BASELINE config 3 (secondary line): square L11 (8.4 M triangles), B/D/M/M0
     and C assembled once, then the Crank-Nicolson right-hand side for 100 steps
     (k = 1e-3), state W ~ U[-1,1] (seed 5), solve excluded.  Bytes per step:
-    SURVEY §8(d) recompute-from-geometry variant 16 nC + 75 nE + 4 E + 16 L."""
+    SURVEY §8(d) stored-operator variant 16 nC + 147 nE + 4 E + 16 L (the
+    recompute-from-geometry figure 16 nC + 75 nE + 4 E + 16 L is reported too)."""
     import torch
     from paper_2401_15557_b200 import capi, meshgen as G
     coeffs, f, g, uD = G.config_fields(3)
@@ -459,7 +473,8 @@ def run_cn_rhs(ctx, args):
     ctx.sync()
     ms = e0.elapsed_time(e1) / steps
     nC, nE, E, L = dm.m.nC, dm.m.nE, topo.E, cls.L
-    bytes_step = 16 * nC + 75 * nE + 4 * E + 16 * L
+    bytes_recompute = 16 * nC + 75 * nE + 4 * E + 16 * L
+    bytes_step = bytes_recompute + 72 * nE   # stored-operator variant
     peak, kind = peaks()
     gbs = bytes_step / (ms * 1e-3) / 1e9
     plan.close()
@@ -472,6 +487,10 @@ def run_cn_rhs(ctx, args):
             "ms_per_step": round(ms, 4), "triangles_per_s": nE / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gbs / peak, 4), "algorithmic_bytes_per_step": bytes_step,
+                         "variant": "stored operator: 16 nC + 147 nE + 4 E + 16 L (SURVEY §8(d) "
+                                    "recompute bytes + the 72 nE stored top block)",
+                         "recompute_variant_bytes": bytes_recompute,
+                         "traffic": (ncu_traffic(args.cn_level, "cn_rhs_step") or {}).get("bytes"),
                          "peak_kind": kind}}
 
 

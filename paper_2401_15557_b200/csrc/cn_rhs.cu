@@ -10,17 +10,25 @@
 // from_triplets.  Eigen's column-major SpMV accumulates each row from 0 in
 // ascending column order.
 //
-// Device version: ONE element pass per step.  Element m recomputes its
-// M_minus block from the geometry (the same expressions as the assembly, so
-// the same bits — 72 bytes/element of stored blocks are never read), adds its
-// coupling terms in ascending multiplier order, evaluates f at the three edge
-// midpoints at t_n and t_{n+1}, and — for every edge it owns as t_plus — also
-// produces that edge's multiplier row (its own DOFs first, then the t_minus
-// DOFs: ascending columns), including the Dirichlet data.  Neumann data enter
-// through the per-element table of assemble.cu, evaluated once per step.
+// Device version.  The plan (phfem_cn_plan_create) stores, once, everything of
+// an element that depends on neither t nor W — the M_minus top block as
+// from_triplets stores it, the coupling entries, the load weight, sin(pi x) and
+// sin(pi y) at the three edge midpoints (sin-sin loads), the multiplier row of
+// each edge slot — and one record per multiplier row (T+ / T- DOF bases and
+// locals, |E|/2), all computed with the assembly's own expressions.  Per step:
+//   * k_cn_tma: the primal rows, one thread per element; the element records
+//     and U stream through a 4-stage SMEM ring filled by cp.async.bulk (TMA),
+//     the Lambda gathers run two tiles ahead of the arithmetic;
+//   * k_cn_rows: the multiplier rows from the row records (coalesced), U of
+//     T+ / T- gathered;
+//   * k_cn_edges over the Dirichlet list only (the rows with u_D data);
+//   * Neumann data through the per-element table of assemble.cu.
+// Other load kinds take k_cn_elements (geometry recomputed every step) +
+// k_cn_edges over all edges.
 #include <algorithm>
 #include <cmath>
 
+#include "bulk.cuh"
 #include "common.cuh"
 #include "elem.cuh"
 #include "kernels.cuh"
@@ -42,6 +50,12 @@ struct phfem_cn_plan {
   double* cpl = nullptr;  // [nE][3] C' entries of the element's edge slots: 0.0 + s_ct (+-|E|/2)
   double* lw = nullptr;   // [nE] load weight (|T|/3) * 0.5
   double* sxy = nullptr;  // [nE][3][2] sin(pi x), sin(pi y) at the edge midpoints
+  int32_t* rp3 = nullptr; // [nE][3] multiplier row of each edge slot, -1 if not retained
+  // multiplier rows, one record per retained edge l (row order): T+ as
+  // 4 t_plus + local, T- as 4 t_minus + local (kRowBnd / kRowDir on the
+  // boundary), and |E| * 0.5
+  uint2* rowt = nullptr;
+  double* rowh = nullptr;
 };
 
 namespace phfem {
@@ -231,7 +245,7 @@ __global__ void __launch_bounds__(kCnThreads, PHFEM_CN_MIN_BLOCKS) k_cn_elements
 template <int CK>
 __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restrict__ top,
                                                         double* __restrict__ cpl, double* __restrict__ lw,
-                                                        double* __restrict__ sxy) {
+                                                        double* __restrict__ sxy, int32_t* __restrict__ rp3) {
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < a.nE;
        m += (int64_t)gridDim.x * blockDim.x) {
     const double2 v[3] = {a.coords[a.elements[3 * m]], a.coords[a.elements[3 * m + 1]],
@@ -262,8 +276,10 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restr
       const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
       const double dx = pb.x - pa.x, dy = pb.y - pa.y;
       const double len = sqrt(dx * dx + dy * dy);
-      const bool plus = a.elem_edge[3 * m + k] >= 0;
+      const int se = a.elem_edge[3 * m + k];
+      const bool plus = se >= 0;
       cpl[3 * m + k] = 0.0 + a.s_ct * (plus ? len * 0.5 : -len * 0.5);  // assembly.cpp:160,164
+      rp3[3 * m + k] = a.rpos[plus ? se : ~se];
       const double mx = 0.5 * (pa.x + pb.x), my = 0.5 * (pa.y + pb.y);
       sxy[6 * m + 2 * k] = sin_fast(PHFEM_PI * mx);
       sxy[6 * m + 2 * k + 1] = sin_fast(PHFEM_PI * my);
@@ -273,43 +289,115 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restr
   }
 }
 
-// warp-cooperative coalesced load of a per-element record of `per` doubles
-// for the warp's 32 consecutive elements into SMEM (stride `per`)
-__device__ __forceinline__ void warp_load(const double* __restrict__ g, int64_t base, int n_valid, int per,
-                                          double* buf) {
+constexpr uint32_t kRowBnd = 0xffffffffu;  // boundary edge, no Dirichlet data
+constexpr uint32_t kRowDir = 0xfffffffeu;  // Dirichlet edge: row written by k_cn_edges
+
+// Once per plan: the record of every multiplier row (row order = retained order)
+__global__ void k_cn_rows_pre(CnArgs a, const int32_t* __restrict__ edge_nodes,
+                              const int32_t* __restrict__ ltp, int E, uint2* __restrict__ rowt,
+                              double* __restrict__ rowh) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int rp = a.rpos[e];
+    if (rp < 0) continue;
+    const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+    const int2 el = reinterpret_cast<const int2*>(a.edge_elements)[e];
+    const double2 pa = a.coords[ab.x], pb = a.coords[ab.y];
+    const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+    const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+    uint32_t y;
+    if (el.y >= 0) y = 4u * (uint32_t)el.y + (uint32_t)a.ltm[e];
+    else y = ((a.dir_bits[e >> 5] >> (e & 31)) & 1u) ? kRowDir : kRowBnd;
+    rowt[rp] = make_uint2(4u * (uint32_t)el.x + (uint32_t)ltp[e], y);
+    rowh[rp] = len * 0.5;
+  }
+}
+
+// Primal rows 3m+i of one element from its stored record (shared by the TMA
+// and the plain-load kernels: one expression, one set of bits).
+__device__ __forceinline__ void cn_primal(const CnArgs& a, int64_t m, const double (&T)[9],
+                                          const double (&sx)[3], const double (&sy)[3],
+                                          const double (&cv3)[3], const double (&U)[3], double w,
+                                          const int (&rp)[3], const double (&lam)[3], double c0,
+                                          double c1, double (&out3)[3]) {
+  double f0[3], f1[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    f0[i] = c0 * sx[i] * sy[i];
+    f1[i] = c1 * sx[i] * sy[i];
+  }
+  double l0[3] = {0.0, 0.0, 0.0}, l1[3] = {0.0, 0.0, 0.0};
+  // LN data only on elements with a Neumann edge, i.e. a non-retained one
+  // (retained = non-Neumann, edge_topology.cpp:165-173): no probe otherwise
+  const int slot = (rp[0] < 0 || rp[1] < 0 || rp[2] < 0) ? neu_lookup(a.neu_keys, a.neu_cap, (int)m) : -1;
+  if (slot >= 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      l0[i] = a.neu0[3 * slot + i];
+      l1[i] = a.neu1[3 * slot + i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc += T[3 * j + i] * U[j];
+    int ka = (i + 1) % 3, kb = (i + 2) % 3;  // edges with R[k][i] != 0, ascending rows
+    if (rp[kb] >= 0 && (rp[ka] < 0 || rp[kb] < rp[ka])) {
+      const int x = ka;
+      ka = kb;
+      kb = x;
+    }
+    if (rp[ka] >= 0) acc += cv3[ka] * lam[ka];
+    if (rp[kb] >= 0) acc += cv3[kb] * lam[kb];
+    const double b0 = 0.0 + w * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
+    const double b1 = 0.0 + w * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
+    out3[i] = acc + a.kh * (((b0 + l0[i]) + b1) + l1[i]);
+  }
+}
+
+struct CnStored {
+  const double* top;
+  const double* cpl;
+  const double* lw;
+  const double* sxy;
+  const int32_t* rp3;
+};
+
+// warp-cooperative coalesced load of a per-element record of `per` elements
+// of T for the warp's 32 consecutive elements into SMEM (stride `per`)
+template <typename T>
+__device__ __forceinline__ void warp_load(const T* __restrict__ g, int64_t base, int n_valid, int per,
+                                          T* buf) {
   const int lane = threadIdx.x & 31;
   const int count = n_valid * per;
-  const double* src = g + base * per;
+  const T* src = g + base * per;
   for (int i = lane; i < count; i += 32) buf[i] = __ldg(src + i);
   __syncwarp();
 }
 
-// Per step: c = exp(-t) p0 (exp-sin-sin) or p0 (sin-sin); f = (c sx) sy in the
-// formula's own order; the stored blocks replace all geometry.
-__global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, const double* __restrict__ top,
-                                                          const double* __restrict__ cpl,
-                                                          const double* __restrict__ lw,
-                                                          const double* __restrict__ sxy, double c0,
+// Plain-load variant: elements [m0, nE) by warps of 32 (the tail tile of the
+// TMA kernel, or everything when the state / rhs are not 16-byte aligned).
+__global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, CnStored st, int64_t m0, double c0,
                                                           double c1, const double* __restrict__ W,
                                                           double* __restrict__ rhs) {
   __shared__ __align__(16) double sbuf[kCnThreads / 32][32 * 9];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* buf = sbuf[warp];
-  const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
+  const int64_t nchunks = ((int64_t)a.nE - m0 + 31) / 32;
   for (int64_t ch = (int64_t)blockIdx.x * (kCnThreads / 32) + warp; ch < nchunks;
        ch += (int64_t)gridDim.x * (kCnThreads / 32)) {
-    const int64_t base = ch * 32;
+    const int64_t base = m0 + ch * 32;
     const int n_valid = (int)((int64_t)a.nE - base < 32 ? (int64_t)a.nE - base : 32);
     const int64_t m = base + lane;
     const bool valid = lane < n_valid;
-    // stored top block (72 B / element)
     __syncwarp();
-    warp_load(top, base, n_valid, 9, buf);
+    warp_load(st.top, base, n_valid, 9, buf);
     double T[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) T[q] = valid ? buf[9 * lane + q] : 0.0;
     __syncwarp();
-    warp_load(sxy, base, n_valid, 6, buf);
+    warp_load(st.sxy, base, n_valid, 6, buf);
     double sx[3], sy[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -317,7 +405,7 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, const double
       sy[k] = valid ? buf[6 * lane + 2 * k + 1] : 0.0;
     }
     __syncwarp();
-    warp_load(cpl, base, n_valid, 3, buf);
+    warp_load(st.cpl, base, n_valid, 3, buf);
     double cv3[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) cv3[k] = valid ? buf[3 * lane + k] : 0.0;
@@ -329,45 +417,10 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, const double
       int rp[3];
       double lam[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int s = __ldg(a.elem_edge + 3 * m + k);
-        rp[k] = __ldg(a.rpos + (s >= 0 ? s : ~s));
-      }
+      for (int k = 0; k < 3; ++k) rp[k] = __ldg(st.rp3 + 3 * m + k);
 #pragma unroll
       for (int k = 0; k < 3; ++k) lam[k] = rp[k] >= 0 ? W[a.N + rp[k]] : 0.0;
-      const double w = __ldg(lw + m);
-      double f0[3], f1[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        f0[i] = c0 * sx[i] * sy[i];
-        f1[i] = c1 * sx[i] * sy[i];
-      }
-      double l0[3] = {0.0, 0.0, 0.0}, l1[3] = {0.0, 0.0, 0.0};
-      const int slot = neu_lookup(a.neu_keys, a.neu_cap, (int)m);
-      if (slot >= 0) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          l0[i] = a.neu0[3 * slot + i];
-          l1[i] = a.neu1[3 * slot + i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) acc += T[3 * j + i] * U[j];
-        int ka = (i + 1) % 3, kb = (i + 2) % 3;  // edges with R[k][i] != 0, ascending rows
-        if (rp[kb] >= 0 && (rp[ka] < 0 || rp[kb] < rp[ka])) {
-          const int x = ka;
-          ka = kb;
-          kb = x;
-        }
-        if (rp[ka] >= 0) acc += cv3[ka] * lam[ka];
-        if (rp[kb] >= 0) acc += cv3[kb] * lam[kb];
-        const double b0 = 0.0 + w * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
-        const double b1 = 0.0 + w * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
-        out3[i] = acc + a.kh * (((b0 + l0[i]) + b1) + l1[i]);
-      }
+      cn_primal(a, m, T, sx, sy, cv3, U, __ldg(st.lw + m), rp, lam, c0, c1, out3);
     }
     // coalesced store through the warp's SMEM slice
     __syncwarp();
@@ -379,15 +432,153 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, const double
   }
 }
 
+// TMA variant over the full 128-element tiles: one elected thread streams each
+// tile's stored record (top, sin table, coupling, U, load weight, rows: 188
+// bytes / element) into a kCnStages-deep SMEM ring with cp.async.bulk
+// (evict-first), completion on one mbarrier per stage; the threads read their
+// element's record from SMEM (odd strides / 16-byte pairs: conflict-free) and
+// only the Lambda and Neumann lookups stay as gathers.
+constexpr int kCnTile = 128;
+constexpr int kCnStages = 4;
+struct CnStage {
+  double top[9 * kCnTile];
+  double sxy[6 * kCnTile];
+  double cpl[3 * kCnTile];
+  double U[3 * kCnTile];
+  double lw[kCnTile];
+  int32_t rp[3 * kCnTile];
+};
+static_assert(sizeof(CnStage) % 16 == 0, "bulk copies need 16-byte granules");
+constexpr size_t kCnTmaSmem = kCnStages * sizeof(CnStage) + 3 * kCnTile * sizeof(double) +
+                              kCnStages * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(kCnTile) k_cn_tma(CnArgs a, CnStored st, int64_t ntiles, double c0,
+                                                     double c1, const double* __restrict__ W,
+                                                     double* __restrict__ rhs) {
+  extern __shared__ __align__(128) unsigned char cn_smem[];
+  CnStage* stg = reinterpret_cast<CnStage*>(cn_smem);
+  double* outb = reinterpret_cast<double*>(cn_smem + kCnStages * sizeof(CnStage));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(outb + 3 * kCnTile);
+  const int tid = threadIdx.x;
+  const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int64_t i) {
+    const int s = (int)(i % kCnStages);
+    const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
+    mbar_expect_tx(&bar[s], (unsigned)sizeof(CnStage));
+    bulk_load(stg[s].top, st.top + 9 * base, 9 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].sxy, st.sxy + 6 * base, 6 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].cpl, st.cpl + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].U, W + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].lw, st.lw + base, kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].rp, st.rp3 + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kCnStages; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+    pol = policy_evict_first();
+    for (int64_t i = 0; i < my && i < kCnStages; ++i) issue(i);
+  }
+  __syncthreads();
+  // the Lambda gathers run two tiles ahead of the arithmetic (their rows come
+  // with the tile's stage), so their latency overlaps two tiles of work
+  int rpq[2][3];
+  double lamq[2][3];
+  auto gather = [&](int64_t j, int (&rp)[3], double (&lam)[3]) {
+    const int sj = (int)(j % kCnStages);
+    mbar_wait(&bar[sj], (unsigned)((j / kCnStages) & 1));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) rp[k] = stg[sj].rp[3 * tid + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) lam[k] = rp[k] >= 0 ? __ldg(W + a.N + rp[k]) : 0.0;
+  };
+#pragma unroll
+  for (int d = 0; d < 2; ++d)
+    if (d < my) gather(d, rpq[d], lamq[d]);
+  for (int64_t i = 0; i < my; ++i) {
+    const int s = (int)(i % kCnStages);
+    const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
+    const int64_t m = base + tid;
+    const CnStage& S = stg[s];
+    int rp[3];
+    double lam[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      rp[k] = rpq[0][k];
+      lam[k] = lamq[0][k];
+      rpq[0][k] = rpq[1][k];
+      lamq[0][k] = lamq[1][k];
+    }
+    if (i + 2 < my) gather(i + 2, rpq[1], lamq[1]);
+    double T[9], sx[3], sy[3], cv3[3];
+    const double U[3] = {S.U[3 * tid], S.U[3 * tid + 1], S.U[3 * tid + 2]};
+#pragma unroll
+    for (int q = 0; q < 9; ++q) T[q] = S.top[9 * tid + q];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double2 p = reinterpret_cast<const double2*>(S.sxy)[3 * tid + k];
+      sx[k] = p.x;
+      sy[k] = p.y;
+      cv3[k] = S.cpl[3 * tid + k];
+    }
+    const double w = S.lw[tid];
+    double out3[3];
+    cn_primal(a, m, T, sx, sy, cv3, U, w, rp, lam, c0, c1, out3);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) outb[3 * tid + q] = out3[q];
+    __syncthreads();  // stage s consumed, tile results staged
+    if (tid == 0 && i + kCnStages < my) issue(i + kCnStages);
+    const double2* s2 = reinterpret_cast<const double2*>(outb);
+    double2* d2 = reinterpret_cast<double2*>(rhs + 3 * base);
+    for (int q = tid; q < 3 * kCnTile / 2; q += kCnTile) __stcs(d2 + q, s2[q]);
+    __syncthreads();  // outb free for the next tile
+  }
+}
+
+// Multiplier rows from the stored row records (coalesced), except the
+// Dirichlet ones: row l = 0.0 + sum over ascending columns — T+ DOFs, then T-
+// DOFs — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor SpMV, from_triplets'
+// 0.0 +), + 0.5 (0.0 + 0.0) (parabolic.cpp:103 with no Dirichlet data).
+__global__ void __launch_bounds__(256) k_cn_rows(const uint2* __restrict__ rowt, const double* __restrict__ rowh,
+                                                  int L, double s_c, const double* __restrict__ W,
+                                                  double* __restrict__ rhs_rows) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 r = __ldcs(rowt + l);
+    if (r.y == kRowDir) continue;
+    const double h = __ldcs(rowh + l);
+    const double cp = 0.0 + s_c * h;  // assembly.cpp:160
+    const int64_t p = 3 * (int64_t)(r.x >> 2);
+    const int lp = (int)(r.x & 3u);
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (c != lp) acc += cp * __ldg(W + p + c);
+    if (r.y != kRowBnd) {
+      const int64_t q = 3 * (int64_t)(r.y >> 2);
+      const int lm = (int)(r.y & 3u);
+      const double cm = 0.0 + s_c * (-h);  // assembly.cpp:164: -len * 0.5 = -(len * 0.5)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (c != lm) acc += cm * __ldg(W + q + c);
+    }
+    const double bdsum = 0.0 + 0.0;
+    __stcs(rhs_rows + l, acc + 0.5 * bdsum);
+  }
+}
+
 // Multiplier rows, one thread per edge (the retained ones write): row l of
 // M_minus W is 0.0 + sum over the row's columns ascending — T+ DOFs, then T-
 // DOFs (t_plus < t_minus) — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor
 // SpMV, from_triplets' 0.0 +), then + 0.5 (bD^n + bD^{n+1}) (parabolic.cpp:103).
+// With `ids` the edges are ids[0..E) (the Dirichlet list of the stored path).
 __global__ void __launch_bounds__(256) k_cn_edges(CnArgs a, const int32_t* __restrict__ edge_nodes,
                                                    const int32_t* __restrict__ ltp, int E,
+                                                   const int32_t* __restrict__ ids,
                                                    const double* __restrict__ W, double* __restrict__ rhs) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = ids ? ids[i] : i;
     const int rp = a.rpos[e];
     if (rp < 0) continue;
     const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
@@ -476,24 +667,44 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
     if (st == PHFEM_OK) st = dalloc(ctx, &p->cpl, 3 * nE);
     if (st == PHFEM_OK) st = dalloc(ctx, &p->lw, nE);
     if (st == PHFEM_OK) st = dalloc(ctx, &p->sxy, 6 * nE);
+    if (st == PHFEM_OK) st = dalloc(ctx, &p->rp3, 3 * nE);
+    if (st == PHFEM_OK && cls->L > 0) st = dalloc(ctx, &p->rowt, (int64_t)cls->L);
+    if (st == PHFEM_OK && cls->L > 0) st = dalloc(ctx, &p->rowh, (int64_t)cls->L);
     if (st == PHFEM_OK) {
       CnArgs a;
       memset(&a, 0, sizeof a);
       a.coords = (const double2*)mesh->coords;
       a.elements = mesh->elements;
       a.elem_edge = topo->elem_edge;
+      a.edge_elements = topo->edge_elements;
+      a.ltm = topo->local_in_tminus;
+      a.rpos = cls->retained_pos;
+      a.dir_bits = p->dir_bits;
       a.nE = mesh->nE;
       a.c = *c;
       const double sign = -1.0;
       a.s_top = sign * (k / 2.0);
       a.s_ct = -sign * (k / 2.0);
       const int grid = grid_for(nE, kCnThreads, ctx->num_sms * 16);
-      KTimer kt(ctx, "k_cn_pre");
-      if (c->kind == PHFEM_COEFF_CENTROID_POLY)
-        k_cn_pre<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy);
-      else
-        k_cn_pre<PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy);
-      ctx->launches++;
+      {
+        KTimer kt(ctx, "k_cn_pre");
+        if (c->kind == PHFEM_COEFF_CENTROID_POLY)
+          k_cn_pre<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy, p->rp3);
+        else
+          k_cn_pre<PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy, p->rp3);
+        ctx->launches++;
+      }
+      if (cls->L > 0) {
+        KTimer kt(ctx, "k_cn_rows_pre");
+        k_cn_rows_pre<<<grid_for(topo->E, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+            a, topo->edge_nodes, topo->local_in_tplus, topo->E, p->rowt, p->rowh);
+        ctx->launches++;
+      }
+      static bool attr_set = false;  // per process; the attribute is per function
+      if (!attr_set) {
+        cudaFuncSetAttribute(k_cn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCnTmaSmem);
+        attr_set = true;
+      }
       if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
     }
   }
@@ -515,6 +726,9 @@ PHFEM_API void phfem_cn_plan_destroy(phfem_ctx* ctx, phfem_cn_plan* p) {
   dfree(ctx, p->cpl);
   dfree(ctx, p->lw);
   dfree(ctx, p->sxy);
+  dfree(ctx, p->rp3);
+  dfree(ctx, p->rowt);
+  dfree(ctx, p->rowh);
   delete p;
 }
 
@@ -561,10 +775,31 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     } else if (a.f.kind == PHFEM_FIELD_SINSIN) {
       c0 = c1 = a.f.p[0];
     }
-    const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
-    const int grid = (int)std::min<int64_t>((nchunks + 3) / 4, (int64_t)ctx->num_sms * 16);
-    PHFEM_LAUNCH(ctx, "k_cn_stored", k_cn_stored<<<grid, kCnThreads, 0, ctx->stream>>>(
-        a, p->top, p->cpl, p->lw, p->sxy, c0, c1, state, rhs));
+    const CnStored st{p->top, p->cpl, p->lw, p->sxy, p->rp3};
+    // TMA over the full tiles when the state and rhs allow 16-byte bulk copies
+    const bool tma = ((((uintptr_t)state) | ((uintptr_t)rhs)) & 15u) == 0;
+    const int64_t nfull = tma ? (int64_t)a.nE / kCnTile : 0;
+    if (nfull > 0) {
+      const int grid = (int)std::min<int64_t>(nfull, (int64_t)ctx->num_sms * 2);
+      PHFEM_LAUNCH(ctx, "k_cn_tma", k_cn_tma<<<grid, kCnTile, kCnTmaSmem, ctx->stream>>>(
+          a, st, nfull, c0, c1, state, rhs));
+    }
+    const int64_t m0 = nfull * kCnTile;
+    if (m0 < a.nE) {
+      const int64_t nchunks = ((int64_t)a.nE - m0 + 31) / 32;
+      const int grid = (int)std::min<int64_t>((nchunks + 3) / 4, (int64_t)ctx->num_sms * 16);
+      PHFEM_LAUNCH(ctx, "k_cn_stored", k_cn_stored<<<grid, kCnThreads, 0, ctx->stream>>>(
+          a, st, m0, c0, c1, state, rhs));
+    }
+    // (measured: running the rows on a side stream next to the element pass
+    // gains nothing — both are DRAM-bound)
+    if (p->cls.L > 0)
+      PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          p->rowt, p->rowh, p->cls.L, a.s_c, state, rhs + a.N));
+    if (p->cls.nD > 0)
+      PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->cls.nD, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+          a, p->topo.edge_nodes, p->topo.local_in_tplus, p->cls.nD, p->cls.dirichlet_edge_ids, state, rhs));
+    return PHFEM_OK;
   } else if (a.nE > 0) {
     const int64_t ntiles = ((int64_t)a.nE + kCnThreads - 1) / kCnThreads;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 16);
@@ -586,7 +821,7 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
   }
   if (p->topo.E > 0) {
     PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->topo.E, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        a, p->topo.edge_nodes, p->topo.local_in_tplus, p->topo.E, state, rhs));
+        a, p->topo.edge_nodes, p->topo.local_in_tplus, p->topo.E, nullptr, state, rhs));
   }
   return PHFEM_OK;
 }

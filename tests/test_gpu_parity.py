@@ -353,6 +353,35 @@ def test_cn_rhs_with_boundary_data(ctx):
         rel_close(plan.rhs(n, W), O.cn_rhs(om, ot, oc, coeffs, f, g, uD, 0.125, n, W), floor=1e-300)
 
 
+@pytest.mark.parametrize("aligned", [True, False])
+def test_cn_rhs_tail_tile_and_unaligned_state(ctx, aligned):
+    """832 triangles = 6.5 TMA tiles (bulk-copy tiles + the plain-load tail),
+    Dirichlet data on the ring; unaligned state / rhs pointers take the
+    plain-load kernel for every element.  Same bits either way."""
+    hm = O.refine_levels(G.fan(13), 3)
+    coeffs, f, g, _ = G.config_fields(3)
+    uD = capi.field(capi.FIELD_AFFINE, 0.5, 1.0, -2.0, 3.0)
+    om, ot = O.build_topology(hm)
+    oc = O.classify_edges(om, ot)
+    n_state = 3 * hm.nE + oc.L
+    W = G.uniform_pm1(11, n_state)
+    dm = capi.DeviceMesh.upload(ctx, hm)
+    topo = capi.build_topology(ctx, dm)
+    cls = capi.classify_edges(ctx, topo, dm)
+    plan = capi.CNPlan(ctx, dm, topo, cls, coeffs, f, g, uD, 1e-3)
+    off = 0 if aligned else 1
+    s = ctx.to_device(np.concatenate([np.zeros(off), W]))
+    r = ctx.alloc(8 * (n_state + off))
+    try:
+        for n in (0, 7):
+            plan.rhs_device(n, s + 8 * off, r + 8 * off)
+            rg = ctx.to_host(r + 8 * off, (n_state,), np.float64)
+            rel_close(rg, O.cn_rhs(om, ot, oc, coeffs, f, g, uD, 1e-3, n, W), floor=1e-300)
+    finally:
+        ctx.free(s)
+        ctx.free(r)
+
+
 # ------------------------------------------------------------------ large sizes
 def test_large_refinement_properties(ctx):
     """Square L11 (8.4 M triangles, config 3's mesh) on the device only:

@@ -1,3 +1,5 @@
+"""CN RHS per-kernel times (ctx event profile) at config 3 (L11); with
+--once it runs 3 steps only (for ncu captures)."""
 import sys
 sys.path.insert(0, '.')
 import bench
@@ -13,4 +15,11 @@ dW = ctx.to_device(W); dr = ctx.alloc(8 * plan.n_state)
 for n in range(3):
     plan.rhs_device(n, dW, dr)
 ctx.sync()
+if "--once" not in sys.argv:
+    ctx.profile(True)
+    for n in range(20):
+        plan.rhs_device(n, dW, dr)
+    ctx.sync()
+    for k, (ms, cnt) in sorted(ctx.profile_read().items(), key=lambda kv: -kv[1][0]):
+        print(f"{k:24s} {ms / 20:.4f} ms/step  ({cnt // 20} launches/step)")
 print("ok")
