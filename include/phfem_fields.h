@@ -215,6 +215,150 @@ PHFEM_HD double phfem_local_blocks(double x0, double y0, double x1, double y1, d
   return g.t2;
 }
 
+/*
+ * ---- manufactured problems (verification) ----------------
+ * The exact solution u and its gradient, for the error norms and the exact
+ * multiplier (analysis.cpp:26-95).  The two registry problems restate
+ * problems.cpp:85-150 in the lambdas' own operation order; SINSIN is the
+ * config-1 solution u = sin(pi x) sin(pi y) behind FLUX_GRAD_SINSIN (not in
+ * the reference's registry).
+ */
+enum phfem_problem_kind {
+  PHFEM_PROBLEM_ELLIPTIC_POLY = 1,  /* u = mu(x) mu(y), mu(s) = s - s s          */
+  PHFEM_PROBLEM_PARABOLIC_POLY = 2, /* u = t mu(x) mu(y)                         */
+  PHFEM_PROBLEM_SINSIN = 3          /* u = sin(pi x) sin(pi y)                   */
+};
+
+typedef struct phfem_problem {
+  int32_t kind;
+  int32_t reserved;
+  phfem_coeffs coeffs; /* problem.coeffs (constant): A, p for exact_multiplier */
+} phfem_problem;
+
+PHFEM_HD double phfem_mu(double s) { return s - s * s; }      /* problems.cpp:91 */
+PHFEM_HD double phfem_dmu(double s) { return 1.0 - 2.0 * s; } /* problems.cpp:92 */
+
+PHFEM_HD double phfem_problem_u(const phfem_problem* p, double x, double y, double t) {
+  switch (p->kind) {
+    case PHFEM_PROBLEM_ELLIPTIC_POLY: return phfem_mu(x) * phfem_mu(y);
+    case PHFEM_PROBLEM_PARABOLIC_POLY: return t * phfem_mu(x) * phfem_mu(y);
+    case PHFEM_PROBLEM_SINSIN: return sin(PHFEM_PI * x) * sin(PHFEM_PI * y);
+    default: return 0.0;
+  }
+}
+
+PHFEM_HD void phfem_problem_grad(const phfem_problem* p, double x, double y, double t, double* gx,
+                                 double* gy) {
+  switch (p->kind) {
+    case PHFEM_PROBLEM_ELLIPTIC_POLY:
+      *gx = phfem_dmu(x) * phfem_mu(y);
+      *gy = phfem_mu(x) * phfem_dmu(y);
+      return;
+    case PHFEM_PROBLEM_PARABOLIC_POLY:
+      *gx = t * phfem_dmu(x) * phfem_mu(y);
+      *gy = t * phfem_mu(x) * phfem_dmu(y);
+      return;
+    case PHFEM_PROBLEM_SINSIN:
+      *gx = PHFEM_PI * cos(PHFEM_PI * x) * sin(PHFEM_PI * y);
+      *gy = PHFEM_PI * sin(PHFEM_PI * x) * cos(PHFEM_PI * y);
+      return;
+    default:
+      *gx = 0.0;
+      *gy = 0.0;
+  }
+}
+
+/* The 25-point Duffy rule of quadrature.cpp:9-53 (TriangleQuadrature::
+ * default_rule): barycentric points b[q][3], weights w[q] summing to 1.     */
+typedef struct phfem_quad_rule {
+  double b[25][3];
+  double w[25];
+} phfem_quad_rule;
+
+PHFEM_HD void phfem_default_rule(phfem_quad_rule* r) {
+  const double a = sqrt(5.0 - 2.0 * sqrt(10.0 / 7.0)) / 3.0;
+  const double bb = sqrt(5.0 + 2.0 * sqrt(10.0 / 7.0)) / 3.0;
+  const double wa = (322.0 + 13.0 * sqrt(70.0)) / 900.0;
+  const double wb = (322.0 - 13.0 * sqrt(70.0)) / 900.0;
+  const double xs[5] = {-bb, -a, 0.0, a, bb};
+  const double ws[5] = {wb, wa, 128.0 / 225.0, wa, wb};
+  double gx[5], gw[5];
+  for (int i = 0; i < 5; ++i) {
+    gx[i] = 0.5 * (xs[i] + 1.0);
+    gw[i] = 0.5 * ws[i];
+  }
+  for (int i = 0; i < 5; ++i)
+    for (int j = 0; j < 5; ++j) {
+      const double xi = gx[i], eta = gx[j];
+      const double x = xi, y = eta * (1.0 - xi);
+      r->b[5 * i + j][0] = 1.0 - x - y;
+      r->b[5 * i + j][1] = x;
+      r->b[5 * i + j][2] = y;
+      r->w[5 * i + j] = 2.0 * gw[i] * gw[j] * (1.0 - xi);
+    }
+}
+
+/* Per-element terms of error_l2 (analysis.cpp:62-80: area * sum_q w (u - uh)^2)
+ * and error_h1 (analysis.cpp:44-58: TriangleQuadrature::integrate of
+ * |grad u - grad uh|^2, quadrature.hpp:25-35).                              */
+PHFEM_HD double phfem_l2_term(const phfem_problem* p, const phfem_quad_rule* r, double x0,
+                              double y0, double x1, double y1, double x2, double y2, double u0,
+                              double u1, double u2, double t) {
+  const double area = 0.5 * ((x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0));
+  double local = 0.0;
+  for (int q = 0; q < 25; ++q) {
+    const double* bc = r->b[q];
+    const double x = bc[0] * x0 + bc[1] * x1 + bc[2] * x2;
+    const double y = bc[0] * y0 + bc[1] * y1 + bc[2] * y2;
+    const double uh = bc[0] * u0 + bc[1] * u1 + bc[2] * u2;
+    const double diff = phfem_problem_u(p, x, y, t) - uh;
+    local += r->w[q] * diff * diff;
+  }
+  return area * local;
+}
+
+PHFEM_HD double phfem_h1_term(const phfem_problem* p, const phfem_quad_rule* r, double x0,
+                              double y0, double x1, double y1, double x2, double y2, double u0,
+                              double u1, double u2, double t) {
+  /* barycentric_gradients (analysis.cpp:16-21): Vec2(...) / twice_area */
+  const double t2 = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
+  const double g0x = (y1 - y2) / t2, g0y = (x2 - x1) / t2;
+  const double g1x = (y2 - y0) / t2, g1y = (x0 - x2) / t2;
+  const double g2x = (y0 - y1) / t2, g2y = (x1 - x0) / t2;
+  const double ghx = 0.0 + u0 * g0x + u1 * g1x + u2 * g2x; /* grad_h += U_i * grads[i] */
+  const double ghy = 0.0 + u0 * g0y + u1 * g1y + u2 * g2y;
+  const double area = 0.5 * ((x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0));
+  double sum = 0.0;
+  for (int q = 0; q < 25; ++q) {
+    const double* bc = r->b[q];
+    const double x = bc[0] * x0 + bc[1] * x1 + bc[2] * x2;
+    const double y = bc[0] * y0 + bc[1] * y1 + bc[2] * y2;
+    double gx, gy;
+    phfem_problem_grad(p, x, y, t, &gx, &gy);
+    const double dx = gx - ghx, dy = gy - ghy;
+    sum += r->w[q] * (dx * dx + dy * dy);
+  }
+  return area * sum;
+}
+
+/* exact_multiplier value of edge (a -> b) (analysis.cpp:26-39 with
+ * edge_normal, edge_topology.cpp:188-192): (A grad u + u p) . nu at the
+ * midpoint, nu = (dy, -dx) / |d|.                                           */
+PHFEM_HD double phfem_exact_multiplier_value(const phfem_problem* p, double ax, double ay,
+                                             double bx, double by, double t) {
+  const double mx = 0.5 * (ax + bx), my = 0.5 * (ay + by);
+  const double dx = bx - ax, dy = by - ay;
+  const double n = sqrt(dx * dx + dy * dy);
+  const double nux = dy / n, nuy = -dx / n;
+  double gx, gy;
+  phfem_problem_grad(p, mx, my, t, &gx, &gy);
+  const double u = phfem_problem_u(p, mx, my, t);
+  const double* c = p->coeffs.p; /* A = [[c0, c1], [c2, c3]], p = (c4, c5) */
+  const double sx = (c[0] * gx + c[1] * gy) + u * c[4];
+  const double sy = (c[2] * gx + c[3] * gy) + u * c[5];
+  return sx * nux + sy * nuy;
+}
+
 #ifdef __cplusplus
 }
 #endif

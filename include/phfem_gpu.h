@@ -49,7 +49,8 @@ typedef enum phfem_status {
   PHFEM_ERR_MISMATCH = 9,           /* runtime_error     assembly.cpp:148-149; refine.cpp:23 */
   PHFEM_ERR_OOM = 10,
   PHFEM_ERR_CUDA = 11,
-  PHFEM_ERR_NO_DEVICE = 12
+  PHFEM_ERR_NO_DEVICE = 12,
+  PHFEM_ERR_RUNTIME = 13            /* runtime_error (other) analysis.cpp:96      */
 } phfem_status;
 
 typedef struct phfem_ctx phfem_ctx;
@@ -410,6 +411,42 @@ phfem_status phfem_dist_neumann_table(phfem_ctx* ctx, const phfem_topology* part
 phfem_status phfem_dist_neumann_apply(phfem_ctx* ctx, const phfem_mesh* mesh, const int32_t* table,
                                       int32_t nN, int32_t dup, int32_t elo, int32_t ehi,
                                       const phfem_field* g, double t, double* load_local);
+
+/* ---- verification around the solve (csrc/verify.cu) ------
+ * Values bit-identical to the reference's; the two error norms sum their
+ * per-element terms in a fixed device tree instead of element order (the
+ * optional `terms` [nE] output is bit-identical, the norm agrees to
+ * rounding).  Scalar results are returned through host pointers (the call
+ * synchronises the ctx stream).
+ * ||C U + bD||_inf (tools/main.cpp:205-207); bd may be NULL (no addition).  */
+phfem_status phfem_constraint_residual(phfem_ctx* ctx, const phfem_csr* C, const double* primal,
+                                       const double* bd, double* out);
+/* exact_multiplier (analysis.hpp; analysis.cpp:26-39) -> out[L]; the problem's
+ * coefficients must be PHFEM_COEFF_CONST (ProblemCoefficients).            */
+phfem_status phfem_exact_multiplier(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                    const phfem_topology* topo, const phfem_classification* cls,
+                                    const phfem_problem* problem, double t, double* out);
+/* error_l2 / error_h1 (analysis.cpp:41-80) of primal[3nE] at time t.        */
+phfem_status phfem_error_l2(phfem_ctx* ctx, const phfem_mesh* mesh, const double* primal,
+                            const phfem_problem* problem, double t, double* out, double* terms);
+phfem_status phfem_error_h1(phfem_ctx* ctx, const phfem_mesh* mesh, const double* primal,
+                            const phfem_problem* problem, double t, double* out, double* terms);
+/* error_multiplier(exact, discrete, C, B) (analysis.cpp:82-98): C from the
+ * classification (assemble_constraint), B the stiffness blocks [nE][9];
+ * sizes differ or != L -> INVALID_ARGUMENT "size mismatch"; no B_ii > 0 ->
+ * RUNTIME "all diagonal entries of B vanish".                               */
+phfem_status phfem_error_multiplier(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                    const phfem_topology* topo, const phfem_classification* cls,
+                                    const double* B, const double* exact, const double* discrete,
+                                    int64_t n_exact, int64_t n_discrete, double* out);
+/* hybrid_midpoint_traces (analysis.cpp:113-125) -> out[E].                  */
+phfem_status phfem_midpoint_traces(phfem_ctx* ctx, const phfem_topology* topo,
+                                   const double* primal, double* out);
+/* CSC -> CSR (columns ascending per row; library-owned, phfem_csr_release)
+ * and y = A x with Eigen's ColMajor SpMV bits (each y_i summed from 0.0 over
+ * ascending columns) — e.g. M_minus W on phfem_step_matrix's output.        */
+phfem_status phfem_csc_to_csr(phfem_ctx* ctx, const phfem_csc* A, phfem_csr* out);
+phfem_status phfem_csr_spmv(phfem_ctx* ctx, const phfem_csr* A, const double* x, double* y);
 
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'

@@ -18,7 +18,7 @@ LIB = os.path.join(_HERE, "_build", "libphfem_oracle.so")
 
 import sys as _sys
 _sys.path.insert(0, os.path.dirname(_HERE))
-from paper_2401_15557_b200.capi import HostMesh, phfem_coeffs, phfem_field  # noqa: E402
+from paper_2401_15557_b200.capi import HostMesh, phfem_coeffs, phfem_field, phfem_problem  # noqa: E402
 
 
 class orc_mesh(C.Structure):
@@ -84,6 +84,14 @@ def lib():
         L.orc_edge_lengths.argtypes = [P(orc_mesh), P(orc_topology), vp]
         L.orc_node_pair_to_edge.argtypes = [P(orc_topology), C.c_int, C.c_int]
         L.orc_directed_pair_to_element.argtypes = [P(orc_topology), C.c_int, C.c_int]
+        L.orc_constraint_residual.argtypes = [P(orc_sparse), vp, vp, P(C.c_double)]
+        L.orc_exact_multiplier.argtypes = [P(orc_mesh), P(orc_topology), P(orc_classification),
+                                           P(phfem_problem), C.c_double, vp]
+        L.orc_error_l2.argtypes = [P(orc_mesh), vp, P(phfem_problem), C.c_double, P(C.c_double), vp]
+        L.orc_error_h1.argtypes = [P(orc_mesh), vp, P(phfem_problem), C.c_double, P(C.c_double), vp]
+        L.orc_error_multiplier.argtypes = [P(orc_sparse), vp, vp, vp, C.c_int64, C.c_int64, P(C.c_double), cp, sz]
+        L.orc_midpoint_traces.argtypes = [P(orc_topology), vp, vp]
+        L.orc_csc_spmv.argtypes = [P(orc_sparse), vp, vp]
         for n in ["orc_topology_free", "orc_classification_free", "orc_sparse_free", "orc_mesh_free"]:
             getattr(L, n).restype = None
         L.orc_topology_free.argtypes = [P(orc_topology)]
@@ -349,3 +357,68 @@ def operator_matrix(B, D, M, M0, C_csc, nE: int, L: int, which: int, k: float = 
     ci = np.concatenate([ci_b, N + inner, cols])
     v = np.concatenate([1.0 * top, s_ct * val, s_c * val])
     return from_triplets(N + L, N + L, ri, ci, v)
+
+
+# ---- verification around the solve ---------------------------
+class _CSC:
+    """orc_sparse view of an Eigen ColMajor CSC (outer, inner, values) tuple."""
+
+    def __init__(self, csc, rows: int, cols: int):
+        self.keep = [np.ascontiguousarray(csc[0], dtype=np.int32), np.ascontiguousarray(csc[1], dtype=np.int32),
+                     np.ascontiguousarray(csc[2], dtype=np.float64)]
+        self.s = orc_sparse(rows, cols, len(self.keep[2]), _ptr(self.keep[0]), _ptr(self.keep[1]),
+                            _ptr(self.keep[2]))
+
+
+def constraint_residual(C_csc, L: int, N: int, primal, bd=None) -> float:
+    """||C U + bD||_inf (tools/main.cpp:205-207)."""
+    cs = _CSC(C_csc, L, N)
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    b = None if bd is None else np.ascontiguousarray(bd, dtype=np.float64)
+    out = C.c_double()
+    lib().orc_constraint_residual(C.byref(cs.s), _ptr(U), None if b is None else _ptr(b), C.byref(out))
+    return out.value
+
+
+def exact_multiplier(om: OMesh, topo: OTopology, cls: OClassification, prob, t: float = 0.0):
+    out = np.zeros(cls.L)
+    lib().orc_exact_multiplier(C.byref(om.m), C.byref(topo.t), C.byref(cls.c), C.byref(prob), t, _ptr(out))
+    return out
+
+
+def error_norm(hm: HostMesh, primal, prob, t: float = 0.0, h1: bool = False):
+    """(norm, per-element terms) of error_h1 / error_l2 (analysis.cpp:41-80)."""
+    om = OMesh(hm)
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    terms = np.zeros(hm.nE)
+    out = C.c_double()
+    fn = lib().orc_error_h1 if h1 else lib().orc_error_l2
+    fn(C.byref(om.m), _ptr(U), C.byref(prob), t, C.byref(out), _ptr(terms))
+    return out.value, terms
+
+
+def error_multiplier(C_csc, L: int, N: int, B, exact, discrete) -> float:
+    cs = _CSC(C_csc, L, N)
+    Bv = np.ascontiguousarray(B, dtype=np.float64)
+    ex = np.ascontiguousarray(exact, dtype=np.float64)
+    di = np.ascontiguousarray(discrete, dtype=np.float64)
+    out = C.c_double()
+    err = C.create_string_buffer(512)
+    _check(lib().orc_error_multiplier(C.byref(cs.s), _ptr(Bv), _ptr(ex), _ptr(di), len(ex), len(di),
+                                      C.byref(out), err, 512), err)
+    return out.value
+
+
+def midpoint_traces(topo: OTopology, primal):
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    out = np.zeros(topo.t.E)
+    lib().orc_midpoint_traces(C.byref(topo.t), _ptr(U), _ptr(out))
+    return out
+
+
+def csc_spmv(A_csc, rows: int, cols: int, x):
+    cs = _CSC(A_csc, rows, cols)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(rows)
+    lib().orc_csc_spmv(C.byref(cs.s), _ptr(xx), _ptr(y))
+    return y

@@ -798,3 +798,127 @@ int orc_from_triplets(int32_t rows, int32_t cols, const int32_t* ri, const int32
   free(mv);
   return 0;
 }
+
+/* ======================================================================
+ * Verification around the solve.
+ * ====================================================================== */
+
+/* ||C U + bD||_inf (tools/main.cpp:205-207): the ColMajor SpMV of the CSC C
+ * (res = 0; res[i] += a_ij U_j, columns ascending), + bD, lpNorm<Infinity>. */
+int orc_constraint_residual(const orc_sparse* csc, const double* U, const double* bd, double* out) {
+  const int L = csc->rows;
+  double* res = (double*)xcalloc((size_t)L + 1, sizeof(double));
+  for (int j = 0; j < csc->cols; ++j) {
+    const double xj = U[j];
+    for (int p = csc->ptr[j]; p < csc->ptr[j + 1]; ++p) res[csc->idx[p]] += csc->val[p] * xj;
+  }
+  double worst = 0.0;
+  for (int l = 0; l < L; ++l) {
+    const double r = bd ? res[l] + bd[l] : res[l];
+    const double a = fabs(r);
+    if (a > worst || a != a) worst = a;
+  }
+  free(res);
+  *out = worst;
+  return PHFEM_OK;
+}
+
+/* exact_multiplier (analysis.cpp:26-39): for each retained edge, in edge
+ * order, (A grad u + u p) . nu at the midpoint (phfem_fields.h formula). */
+int orc_exact_multiplier(const orc_mesh* mesh, const orc_topology* topo,
+                         const orc_classification* cls, const phfem_problem* p, double t,
+                         double* out) {
+  for (int k = 0; k < cls->L; ++k) {
+    const int e = cls->retained_edges[k];
+    const int a = topo->edge_nodes[2 * e], b = topo->edge_nodes[2 * e + 1];
+    out[cls->retained_pos[e]] =
+        phfem_exact_multiplier_value(p, mesh->coords[2 * a], mesh->coords[2 * a + 1],
+                                     mesh->coords[2 * b], mesh->coords[2 * b + 1], t);
+  }
+  return PHFEM_OK;
+}
+
+/* error_l2 / error_h1 (analysis.cpp:41-80): sum of the per-element terms in
+ * element order, then sqrt.  terms (nullable) receives every term. */
+static int error_norm(const orc_mesh* mesh, const double* U, const phfem_problem* p, double t,
+                      double* out, double* terms, int h1) {
+  phfem_quad_rule rule;
+  phfem_default_rule(&rule);
+  double sum = 0.0;
+  for (int m = 0; m < mesh->nE; ++m) {
+    const int* tv = mesh->elements + 3 * m;
+    const double* c = mesh->coords;
+    const double x0 = c[2 * tv[0]], y0 = c[2 * tv[0] + 1], x1 = c[2 * tv[1]], y1 = c[2 * tv[1] + 1];
+    const double x2 = c[2 * tv[2]], y2 = c[2 * tv[2] + 1];
+    const double term = h1 ? phfem_h1_term(p, &rule, x0, y0, x1, y1, x2, y2, U[3 * m], U[3 * m + 1],
+                                           U[3 * m + 2], t)
+                           : phfem_l2_term(p, &rule, x0, y0, x1, y1, x2, y2, U[3 * m], U[3 * m + 1],
+                                           U[3 * m + 2], t);
+    if (terms) terms[m] = term;
+    sum += term;
+  }
+  *out = sqrt(sum);
+  return PHFEM_OK;
+}
+
+int orc_error_l2(const orc_mesh* mesh, const double* U, const phfem_problem* p, double t,
+                 double* out, double* terms) {
+  return error_norm(mesh, U, p, t, out, terms, 0);
+}
+
+int orc_error_h1(const orc_mesh* mesh, const double* U, const phfem_problem* p, double t,
+                 double* out, double* terms) {
+  return error_norm(mesh, U, p, t, out, terms, 1);
+}
+
+/* error_multiplier (analysis.cpp:82-98): w = C' (exact - discrete) through
+ * the CSC columns (rows ascending, from 0), max |w_i| / sqrt(B_ii) over the
+ * B_ii > 0 (B = stiffness blocks [nE][9], diagonal at 9m + 4i). */
+int orc_error_multiplier(const orc_sparse* csc, const double* B, const double* exact,
+                         const double* discrete, int64_t n_exact, int64_t n_discrete, double* out,
+                         char* err, size_t errlen) {
+  if (n_exact != n_discrete || n_exact != csc->rows) {
+    SETERR("error_multiplier: size mismatch");
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  }
+  double worst = 0.0;
+  int any = 0;
+  for (int j = 0; j < csc->cols; ++j) {
+    double w = 0.0;
+    for (int p = csc->ptr[j]; p < csc->ptr[j + 1]; ++p) {
+      const int l = csc->idx[p];
+      w += csc->val[p] * (exact[l] - discrete[l]);
+    }
+    const double diag = B[9 * (size_t)(j / 3) + 4 * (j % 3)];
+    if (diag <= 0.0) continue;
+    any = 1;
+    const double r = fabs(w) / sqrt(diag);
+    if (worst < r) worst = r; /* std::max(worst, r) */
+  }
+  if (!any) {
+    SETERR("error_multiplier: all diagonal entries of B vanish");
+    return PHFEM_ERR_RUNTIME;
+  }
+  *out = worst;
+  return PHFEM_OK;
+}
+
+/* hybrid_midpoint_traces (analysis.cpp:113-125) */
+int orc_midpoint_traces(const orc_topology* topo, const double* U, double* out) {
+  for (int e = 0; e < topo->E; ++e) {
+    const int m = topo->edge_elements[2 * e];
+    const int led = topo->local_in_tplus[e];
+    out[e] = 0.5 * (U[3 * m + (led + 1) % 3] + U[3 * m + (led + 2) % 3]);
+  }
+  return PHFEM_OK;
+}
+
+/* y = A x, Eigen ColMajor sparse x dense (res = 0; res[i] += a_ij x_j) */
+int orc_csc_spmv(const orc_sparse* csc, const double* x, double* y) {
+  for (int i = 0; i < csc->rows; ++i) y[i] = 0.0;
+  for (int j = 0; j < csc->cols; ++j) {
+    const double xj = x[j];
+    for (int p = csc->ptr[j]; p < csc->ptr[j + 1]; ++p) y[csc->idx[p]] += csc->val[p] * xj;
+  }
+  return PHFEM_OK;
+}

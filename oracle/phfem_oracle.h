@@ -110,6 +110,21 @@ int orc_cn_rhs(const orc_mesh* mesh, const orc_topology* topo, const orc_classif
                const phfem_field* uD, double k, int n, const double* state, double* rhs,
                char* err, size_t errlen);
 
+/* ---- verification around the solve ---------------------- */
+int orc_constraint_residual(const orc_sparse* csc, const double* U, const double* bd, double* out);
+int orc_exact_multiplier(const orc_mesh* mesh, const orc_topology* topo,
+                         const orc_classification* cls, const phfem_problem* p, double t,
+                         double* out);
+int orc_error_l2(const orc_mesh* mesh, const double* U, const phfem_problem* p, double t,
+                 double* out, double* terms);
+int orc_error_h1(const orc_mesh* mesh, const double* U, const phfem_problem* p, double t,
+                 double* out, double* terms);
+int orc_error_multiplier(const orc_sparse* csc, const double* B, const double* exact,
+                         const double* discrete, int64_t n_exact, int64_t n_discrete, double* out,
+                         char* err, size_t errlen);
+int orc_midpoint_traces(const orc_topology* topo, const double* U, double* out);
+int orc_csc_spmv(const orc_sparse* csc, const double* x, double* y);
+
 #ifdef __cplusplus
 }
 #endif

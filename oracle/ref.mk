@@ -9,7 +9,7 @@ REF      ?= /root/reference/proj
 OUT      := _ref
 CXXFLAGS ?= -std=c++20 -O3 -DNDEBUG -ffp-contract=off -fPIC -w
 INCS     := -I../shim -I$(REF)/include
-SRCS     := mesh edge_topology refine sparse assembly parabolic elliptic
+SRCS     := mesh edge_topology refine sparse assembly parabolic elliptic analysis problems quadrature
 OBJS     := $(SRCS:%=$(OUT)/%.o) $(OUT)/ref_runner.o
 
 all: $(OUT)/libphfem_ref.so

@@ -2,7 +2,7 @@
 //
 // extern "C" front end over the reference's OWN hot-path sources
 // (/root/reference/proj/src/{mesh,edge_topology,refine,sparse,assembly,
-// parabolic,elliptic}.cpp, compiled unmodified against shim/Eigen by
+// parabolic,elliptic,analysis,problems,quadrature}.cpp, compiled unmodified against shim/Eigen by
 // oracle/ref.mk into oracle/_ref/libphfem_ref.so).  Used to pin the C oracle
 // (tests/test_oracle_vs_ref.py), to generate tests/golden, and as the
 // "reference" CPU baseline of bench.py.  Never linked by the product.
@@ -13,11 +13,13 @@
 #include <string>
 #include <vector>
 
+#include "phfem/analysis.hpp"
 #include "phfem/assembly.hpp"
 #include "phfem/edge_topology.hpp"
 #include "phfem/elliptic.hpp"
 #include "phfem/mesh.hpp"
 #include "phfem/parabolic.hpp"
+#include "phfem/problems.hpp"
 #include "phfem/refine.hpp"
 #include "phfem/sparse.hpp"
 
@@ -362,6 +364,97 @@ double ref_pipeline_seconds(const void* mp, int levels, const phfem_coeffs* c, c
     *n_out = -1;
   }
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- verification around the solve (analysis.cpp; tools/main.cpp:205-207),
+// with the reference's OWN registry problems ("elliptic-poly",
+// "parabolic-poly", problems.cpp) ----------------------------------------------
+int ref_error_norms(const void* mp, const char* problem, const double* primal, double t, double* l2,
+                    double* h1, char* err, size_t errlen) {
+  const Mesh& mesh = *static_cast<const Mesh*>(mp);
+  REF_TRY({
+    const ManufacturedProblem& p = find_problem(problem);
+    DiscreteSolution sol;
+    sol.primal = Eigen::VectorXd(3 * mesh.element_count());
+    for (int i = 0; i < 3 * mesh.element_count(); ++i) sol.primal[i] = primal[i];
+    *l2 = error_l2(mesh, sol, p, t);
+    *h1 = error_h1(mesh, sol, p, t);
+  })
+}
+
+int ref_exact_multiplier(const void* mp, const void* tp, const void* cp, const char* problem, double t,
+                         double* out, char* err, size_t errlen) {
+  REF_TRY({
+    const Eigen::VectorXd k =
+        exact_multiplier(*static_cast<const Mesh*>(mp), *static_cast<const EdgeTopology*>(tp),
+                         *static_cast<const EdgeClassification*>(cp), find_problem(problem), t);
+    std::memcpy(out, k.data(), sizeof(double) * (size_t)k.size());
+  })
+}
+
+// error_multiplier(exact, discrete, constraint, stiffness): constraint =
+// assemble_constraint, stiffness = the block-diagonal matrix of the given
+// blocks B [nE][9] (column-major, as assemble_block_diagonal stores them)
+int ref_error_multiplier(const void* mp, const void* tp, const void* cp, const double* B,
+                         const double* exact, const double* discrete, int n_exact, int n_discrete,
+                         double* out, char* err, size_t errlen) {
+  REF_TRY({
+    const Mesh& mesh = *static_cast<const Mesh*>(mp);
+    const int ne = mesh.element_count();
+    const SparseMatrix Cm = assemble_constraint(mesh, *static_cast<const EdgeTopology*>(tp),
+                                                *static_cast<const EdgeClassification*>(cp));
+    TripletBuffer buf(3 * ne, 3 * ne);
+    for (int m = 0; m < ne; ++m)
+      for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) buf.add(3 * m + i, 3 * m + j, B[9 * (size_t)m + 3 * j + i]);
+    const SparseMatrix stiffness = SparseMatrix::from_triplets(buf);
+    Eigen::VectorXd ex(n_exact), di(n_discrete);
+    for (int i = 0; i < n_exact; ++i) ex[i] = exact[i];
+    for (int i = 0; i < n_discrete; ++i) di[i] = discrete[i];
+    *out = error_multiplier(ex, di, Cm, stiffness);
+  })
+}
+
+int ref_midpoint_traces(const void* tp, const double* primal, int n, double* out) {
+  Eigen::VectorXd U(n);
+  for (int i = 0; i < n; ++i) U[i] = primal[i];
+  const Eigen::VectorXd tr = hybrid_midpoint_traces(*static_cast<const EdgeTopology*>(tp), U);
+  std::memcpy(out, tr.data(), sizeof(double) * (size_t)tr.size());
+  return 0;
+}
+
+// the CLI's residual check: (C U + bD(t)).lpNorm<Infinity>() (main.cpp:205-207)
+int ref_constraint_residual(const void* mp, const void* tp, const void* cp, const phfem_field* uD,
+                            double t, const double* primal, double* out, char* err, size_t errlen) {
+  const Mesh& mesh = *static_cast<const Mesh*>(mp);
+  const EdgeTopology& topo = *static_cast<const EdgeTopology*>(tp);
+  const EdgeClassification& cls = *static_cast<const EdgeClassification*>(cp);
+  REF_TRY({
+    const SparseMatrix Cm = assemble_constraint(mesh, topo, cls);
+    const Eigen::VectorXd bd = assemble_dirichlet(mesh, topo, cls, scalar(uD), t);
+    Eigen::VectorXd U(3 * mesh.element_count());
+    for (int i = 0; i < 3 * mesh.element_count(); ++i) U[i] = primal[i];
+    *out = (Cm.eigen() * U + bd).lpNorm<Eigen::Infinity>();
+  })
+}
+
+// y = A x for A = build_saddle_matrix (which 0) / step_matrices(k).first (1) /
+// .second (2) with constant coefficients (Eigen ColMajor SpMV)
+int ref_operator_spmv(const void* mp, const void* tp, const void* cp, const phfem_coeffs* c, int which,
+                      double k, const double* x, double* y, char* err, size_t errlen) {
+  REF_TRY({
+    const std::array<Vec2, 3> dummy = {Vec2(0, 0), Vec2(1, 0), Vec2(0, 1)};
+    const GlobalOperators ops =
+        assemble_operators(*static_cast<const Mesh*>(mp), *static_cast<const EdgeTopology*>(tp),
+                           *static_cast<const EdgeClassification*>(cp), coeffs_of(c, dummy));
+    SparseMatrix m;
+    if (which == 0) m = build_saddle_matrix(ops);
+    else m = which == 1 ? step_matrices(ops, k).first : step_matrices(ops, k).second;
+    Eigen::VectorXd xv(m.rows());
+    for (int i = 0; i < m.rows(); ++i) xv[i] = x[i];
+    const Eigen::VectorXd r = m.eigen() * xv;
+    std::memcpy(y, r.data(), sizeof(double) * (size_t)r.size());
+  })
 }
 
 }  // extern "C"

@@ -312,3 +312,69 @@ def operator_matrix(rm, rt, rc, coeffs, which: int, k: float = 0.0):
     _check(L.ref_operator_matrix(rm.h, rt.h, rc.h, C.byref(coeffs), which, k, C.byref(dim), C.byref(nnz),
                                  _p(outer), _p(inner), _p(vals), err, 512), err)
     return outer, inner, vals
+
+
+# ---- verification around the solve (analysis.cpp; tools/main.cpp:205-207) ----
+_vp, _cp, _sz, _dbl = C.c_void_p, C.c_char_p, C.c_size_t, C.c_double
+
+
+def error_norms(rm: RMesh, problem: str, primal, t: float = 0.0):
+    """(error_l2, error_h1) with the reference's registry problem `problem`."""
+    L = lib()
+    L.ref_error_norms.argtypes = [_vp, _cp, _vp, _dbl, C.POINTER(_dbl), C.POINTER(_dbl), _cp, _sz]
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    l2, h1 = _dbl(), _dbl()
+    err = C.create_string_buffer(512)
+    _check(L.ref_error_norms(rm.h, problem.encode(), _p(U), t, C.byref(l2), C.byref(h1), err, 512), err)
+    return l2.value, h1.value
+
+
+def exact_multiplier(rm, rt, rc, problem: str, L_: int, t: float = 0.0):
+    L = lib()
+    L.ref_exact_multiplier.argtypes = [_vp, _vp, _vp, _cp, _dbl, _vp, _cp, _sz]
+    out = np.zeros(L_)
+    err = C.create_string_buffer(512)
+    _check(L.ref_exact_multiplier(rm.h, rt.h, rc.h, problem.encode(), t, _p(out), err, 512), err)
+    return out
+
+
+def error_multiplier(rm, rt, rc, B, exact, discrete) -> float:
+    L = lib()
+    L.ref_error_multiplier.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(_dbl), _cp, _sz]
+    ex = np.ascontiguousarray(exact, dtype=np.float64)
+    di = np.ascontiguousarray(discrete, dtype=np.float64)
+    out = _dbl()
+    err = C.create_string_buffer(512)
+    Bv = np.ascontiguousarray(B, dtype=np.float64)
+    _check(L.ref_error_multiplier(rm.h, rt.h, rc.h, _p(Bv), _p(ex), _p(di), len(ex), len(di),
+                                  C.byref(out), err, 512), err)
+    return out.value
+
+
+def midpoint_traces(rt, primal, E: int):
+    L = lib()
+    L.ref_midpoint_traces.argtypes = [_vp, _vp, C.c_int, _vp]
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    out = np.zeros(E)
+    L.ref_midpoint_traces(rt.h, _p(U), len(U), _p(out))
+    return out
+
+
+def constraint_residual(rm, rt, rc, uD, t, primal) -> float:
+    L = lib()
+    L.ref_constraint_residual.argtypes = [_vp, _vp, _vp, _vp, _dbl, _vp, C.POINTER(_dbl), _cp, _sz]
+    U = np.ascontiguousarray(primal, dtype=np.float64)
+    out = _dbl()
+    err = C.create_string_buffer(512)
+    _check(L.ref_constraint_residual(rm.h, rt.h, rc.h, C.byref(uD), t, _p(U), C.byref(out), err, 512), err)
+    return out.value
+
+
+def operator_spmv(rm, rt, rc, coeffs, which: int, k: float, x):
+    L = lib()
+    L.ref_operator_spmv.argtypes = [_vp, _vp, _vp, _vp, C.c_int, _dbl, _vp, _vp, _cp, _sz]
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(len(xx))
+    err = C.create_string_buffer(512)
+    _check(L.ref_operator_spmv(rm.h, rt.h, rc.h, C.byref(coeffs), which, k, _p(xx), _p(y), err, 512), err)
+    return y

@@ -38,11 +38,13 @@ ERR_MISMATCH = 9
 ERR_OOM = 10
 ERR_CUDA = 11
 ERR_NO_DEVICE = 12
+ERR_RUNTIME = 13
 
 # ---- field / coefficient kinds (phfem_fields.h) ------------------------------
 FIELD_ZERO, FIELD_CONST, FIELD_SINSIN, FIELD_EXP_SINSIN, FIELD_AFFINE, FIELD_SIN3X, FIELD_NAN = range(7)
 FLUX_ZERO, FLUX_CONST, FLUX_GRAD_SINSIN, FLUX_VEC_KAT = range(4)
 COEFF_CONST, COEFF_CENTROID_POLY = range(2)
+PROBLEM_ELLIPTIC_POLY, PROBLEM_PARABOLIC_POLY, PROBLEM_SINSIN = 1, 2, 3
 
 
 class phfem_field(C.Structure):
@@ -51,6 +53,22 @@ class phfem_field(C.Structure):
 
 class phfem_coeffs(C.Structure):
     _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("p", C.c_double * 8)]
+
+
+class phfem_problem(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("coeffs", phfem_coeffs)]
+
+
+def problem(kind: int, coeffs: "phfem_coeffs | None" = None) -> phfem_problem:
+    """Manufactured problem descriptor (phfem_fields.h).  The registry problems
+    (problems.cpp:85-150) carry A = I, p = (1, 1), delta = 1; SINSIN (config 1)
+    A = I, p = 0, delta = 0."""
+    pr = phfem_problem()
+    pr.kind = kind
+    if coeffs is None:
+        coeffs = (coeffs_const(p=(1.0, 1.0), delta=1.0) if kind != PROBLEM_SINSIN else coeffs_const())
+    pr.coeffs = coeffs
+    return pr
 
 
 def field(kind: int, *params: float) -> phfem_field:
@@ -151,6 +169,8 @@ EXPORTED = [
     "phfem_dist_add_offset", "phfem_dist_resolve", "phfem_dist_classify", "phfem_dist_neumann_table",
     "phfem_dist_neumann_apply", "phfem_dist_children", "phfem_dist_midpoints",
     "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
+    "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
+    "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -247,6 +267,16 @@ def load_library(path: str = LIB_PATH):
                                                      P(phfem_classification), vp, vp, C.c_int]),
         "phfem_assemble_dirichlet_sampled": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology),
                                                        P(phfem_classification), vp, vp]),
+        "phfem_constraint_residual": (C.c_int, [vp, P(phfem_csr), vp, vp, P(dbl)]),
+        "phfem_exact_multiplier": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                             P(phfem_problem), dbl, vp]),
+        "phfem_error_l2": (C.c_int, [vp, P(phfem_mesh), vp, P(phfem_problem), dbl, P(dbl), vp]),
+        "phfem_error_h1": (C.c_int, [vp, P(phfem_mesh), vp, P(phfem_problem), dbl, P(dbl), vp]),
+        "phfem_error_multiplier": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                             vp, vp, vp, i64, i64, P(dbl)]),
+        "phfem_midpoint_traces": (C.c_int, [vp, P(phfem_topology), vp, vp]),
+        "phfem_csc_to_csr": (C.c_int, [vp, P(phfem_csc), P(phfem_csr)]),
+        "phfem_csr_spmv": (C.c_int, [vp, P(phfem_csr), vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -584,6 +614,81 @@ def constraint_csc(ctx: Context, mesh: DeviceMesh, topo: Topology, cls: Classifi
                 ctx.to_host(m.values, (m.nnz,), np.float64))
     finally:
         ctx.lib.phfem_csc_release(ctx.ptr, C.byref(m))
+
+
+# ---- verification around the solve (csrc/verify.cu) ----------
+def exact_multiplier(ctx: Context, mesh: DeviceMesh, topo: Topology, cls: Classification,
+                     prob: phfem_problem, t: float = 0.0) -> np.ndarray:
+    p = ctx.alloc(8 * max(cls.L, 1))
+    try:
+        ctx.check(ctx.lib.phfem_exact_multiplier(ctx.ptr, C.byref(mesh.m), C.byref(topo.t), C.byref(cls.c),
+                                                 C.byref(prob), t, C.c_void_p(p)))
+        return ctx.to_host(p, (cls.L,), np.float64)
+    finally:
+        ctx.free(p)
+
+
+def error_norm(ctx: Context, mesh: DeviceMesh, primal: np.ndarray, prob: phfem_problem, t: float = 0.0,
+               h1: bool = False):
+    """(error_h1 or error_l2, per-element terms) of a host primal vector."""
+    nE = mesh.m.nE
+    U = ctx.to_device(np.ascontiguousarray(primal, dtype=np.float64))
+    terms = ctx.alloc(8 * max(nE, 1))
+    out = C.c_double()
+    try:
+        fn = ctx.lib.phfem_error_h1 if h1 else ctx.lib.phfem_error_l2
+        ctx.check(fn(ctx.ptr, C.byref(mesh.m), C.c_void_p(U), C.byref(prob), t, C.byref(out), C.c_void_p(terms)))
+        return out.value, ctx.to_host(terms, (nE,), np.float64)
+    finally:
+        ctx.free(U)
+        ctx.free(terms)
+
+
+def error_multiplier(ctx: Context, mesh: DeviceMesh, topo: Topology, cls: Classification, B: np.ndarray,
+                     exact: np.ndarray, discrete: np.ndarray) -> float:
+    dB = ctx.to_device(np.ascontiguousarray(B, dtype=np.float64))
+    de = ctx.to_device(np.ascontiguousarray(exact, dtype=np.float64))
+    dd = ctx.to_device(np.ascontiguousarray(discrete, dtype=np.float64))
+    out = C.c_double()
+    try:
+        ctx.check(ctx.lib.phfem_error_multiplier(ctx.ptr, C.byref(mesh.m), C.byref(topo.t), C.byref(cls.c),
+                                                 C.c_void_p(dB), C.c_void_p(de), C.c_void_p(dd), len(exact),
+                                                 len(discrete), C.byref(out)))
+        return out.value
+    finally:
+        for p in (dB, de, dd):
+            ctx.free(p)
+
+
+def midpoint_traces(ctx: Context, topo: Topology, primal: np.ndarray) -> np.ndarray:
+    U = ctx.to_device(np.ascontiguousarray(primal, dtype=np.float64))
+    out = ctx.alloc(8 * max(topo.E, 1))
+    try:
+        ctx.check(ctx.lib.phfem_midpoint_traces(ctx.ptr, C.byref(topo.t), C.c_void_p(U), C.c_void_p(out)))
+        return ctx.to_host(out, (topo.E,), np.float64)
+    finally:
+        ctx.free(U)
+        ctx.free(out)
+
+
+def constraint_residual(ctx: Context, mesh: DeviceMesh, topo: Topology, cls: Classification,
+                        primal: np.ndarray, bd: Optional[np.ndarray]) -> float:
+    """||C U + bD||_inf with C assembled on the device (assemble_constraint)."""
+    m = phfem_csr()
+    ctx.check(ctx.lib.phfem_assemble_constraint(ctx.ptr, C.byref(mesh.m), C.byref(topo.t), C.byref(cls.c),
+                                                C.byref(m)))
+    U = ctx.to_device(np.ascontiguousarray(primal, dtype=np.float64))
+    b = ctx.to_device(np.ascontiguousarray(bd, dtype=np.float64)) if bd is not None else 0
+    out = C.c_double()
+    try:
+        ctx.check(ctx.lib.phfem_constraint_residual(ctx.ptr, C.byref(m), C.c_void_p(U), C.c_void_p(b or None),
+                                                    C.byref(out)))
+        return out.value
+    finally:
+        ctx.lib.phfem_csr_release(ctx.ptr, C.byref(m))
+        ctx.free(U)
+        if b:
+            ctx.free(b)
 
 
 class CNPlan:
