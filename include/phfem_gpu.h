@@ -448,6 +448,33 @@ phfem_status phfem_midpoint_traces(phfem_ctx* ctx, const phfem_topology* topo,
 phfem_status phfem_csc_to_csr(phfem_ctx* ctx, const phfem_csc* A, phfem_csr* out);
 phfem_status phfem_csr_spmv(phfem_ctx* ctx, const phfem_csr* A, const double* x, double* y);
 
+/* ---- on-disk formats (csrc/io.cu) --------------------------
+ * load_mesh (mesh.hpp; mesh.cpp:114-150) from the four text files' bytes
+ * (dirichlet / neumann may be empty) -> a library-owned device mesh, with the
+ * reference's validation order and messages (PHFEM_ERR_RUNTIME, 1-based
+ * rows); boundary pairs normalised to their element-cycle direction.
+ * load_mesh_dir reads DIR/{coordinates,elements,dirichlet,neumann}.dat (the
+ * last two optional, "cannot open DIR/name" otherwise).                    */
+phfem_status phfem_mesh_load_text(phfem_ctx* ctx, const char* coordinates, size_t coordinates_len,
+                                  const char* elements, size_t elements_len, const char* dirichlet,
+                                  size_t dirichlet_len, const char* neumann, size_t neumann_len,
+                                  phfem_mesh* out);
+phfem_status phfem_mesh_load_dir(phfem_ctx* ctx, const char* dir, phfem_mesh* out);
+/* save_mesh (mesh.cpp:170-180): which 0 coordinates ("%.17g %.17g"), 1
+ * elements, 2 dirichlet, 3 neumann (1-based ids) -> *out (malloc'd, free with
+ * phfem_text_free), *len bytes.  save_mesh_dir writes the files.           */
+phfem_status phfem_mesh_format(phfem_ctx* ctx, const phfem_mesh* mesh, int which, char** out,
+                               size_t* len);
+void phfem_text_free(char* text);
+phfem_status phfem_mesh_save_dir(phfem_ctx* ctx, const phfem_mesh* mesh, const char* dir);
+/* The CLI's topology CSV (tools/main.cpp:302-323): header, then per edge
+ * "e,a,b,t_plus,t_minus,led,led_tn,length" (1-based, 0 for no t_minus,
+ * length "%.10g").                                                          */
+phfem_status phfem_topology_csv(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
+                                char** out, size_t* len);
+phfem_status phfem_topology_csv_file(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                     const phfem_topology* topo, const char* path);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

@@ -23,6 +23,6 @@ $(OUT)/ref_runner.o: ref_runner.cpp ../include/phfem_fields.h $(wildcard ../shim
 	$(CXX) $(CXXFLAGS) $(INCS) -c $< -o $@
 
 $(OUT)/libphfem_ref.so: $(OBJS)
-	$(CXX) -shared -o $@ $(OBJS)
+	$(CXX) -shared -Wl,-Bsymbolic -Wl,--exclude-libs,ALL -o $@ $(OBJS)
 
 .PHONY: all

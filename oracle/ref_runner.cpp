@@ -7,6 +7,8 @@
 // (tests/test_oracle_vs_ref.py), to generate tests/golden, and as the
 // "reference" CPU baseline of bench.py.  Never linked by the product.
 #include <chrono>
+#include <cstdio>
+#include <sstream>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -454,6 +456,50 @@ int ref_operator_spmv(const void* mp, const void* tp, const void* cp, const phfe
     for (int i = 0; i < m.rows(); ++i) xv[i] = x[i];
     const Eigen::VectorXd r = m.eigen() * xv;
     std::memcpy(y, r.data(), sizeof(double) * (size_t)r.size());
+  })
+}
+
+// ---- on-disk formats: load_mesh / save_mesh (mesh.cpp:114-180) on in-memory
+// streams, and the CLI's topology CSV (tools/main.cpp:302-323) restated with
+// the reference's build_topology / edge_lengths and its fmt ("%.10g") --------
+int ref_load_mesh_text(const char* c, size_t nc, const char* e, size_t ne, const char* d, size_t nd,
+                       const char* n, size_t nn, void** out, char* err, size_t errlen) {
+  REF_TRY({
+    std::istringstream cs(std::string(c, nc)), es(std::string(e, ne)), ds(std::string(d, nd)),
+        ns(std::string(n, nn));
+    *out = new Mesh(load_mesh(cs, es, ds, ns));
+  })
+}
+
+// which: 0 coordinates, 1 elements, 2 dirichlet, 3 neumann; buf NULL -> size
+int ref_save_mesh_text(const void* mp, int which, char* buf, size_t cap, size_t* len) {
+  std::ostringstream s[4];
+  save_mesh(*static_cast<const Mesh*>(mp), s[0], s[1], s[2], s[3]);
+  const std::string t = s[which].str();
+  *len = t.size();
+  if (buf && cap >= t.size()) std::memcpy(buf, t.data(), t.size());
+  return 0;
+}
+
+int ref_topology_csv(const void* mp, char* buf, size_t cap, size_t* len, char* err, size_t errlen) {
+  const Mesh& mesh = *static_cast<const Mesh*>(mp);
+  REF_TRY({
+    const EdgeTopology topo = build_topology(mesh);
+    const std::vector<double> lengths = edge_lengths(mesh, topo);
+    std::ostringstream out;
+    out << "edge,node_start,node_end,t_plus,t_minus,led,led_tn,length\n";
+    for (int e = 0; e < topo.edge_count(); ++e) {
+      const auto& [a, b] = topo.edge_nodes[e];
+      const auto& [tp, tm] = topo.edge_elements[e];
+      char f[64];
+      std::snprintf(f, sizeof f, "%.10g", lengths[e]);
+      out << e + 1 << ',' << a + 1 << ',' << b + 1 << ',' << tp + 1 << ',' << tm + 1 << ','
+          << topo.local_in_tplus[e] + 1 << ',' << (tm >= 0 ? topo.local_in_tminus[e] + 1 : 0) << ','
+          << f << '\n';
+    }
+    const std::string t = out.str();
+    *len = t.size();
+    if (buf && cap >= t.size()) std::memcpy(buf, t.data(), t.size());
   })
 }
 

@@ -378,3 +378,38 @@ def operator_spmv(rm, rt, rc, coeffs, which: int, k: float, x):
     err = C.create_string_buffer(512)
     _check(L.ref_operator_spmv(rm.h, rt.h, rc.h, C.byref(coeffs), which, k, _p(xx), _p(y), err, 512), err)
     return y
+
+
+# ---- on-disk formats (mesh.cpp:114-180; tools/main.cpp:302-323) ---------------
+def load_mesh_text(coordinates: bytes, elements: bytes, dirichlet: bytes = b"", neumann: bytes = b"") -> RMesh:
+    L = lib()
+    L.ref_load_mesh_text.argtypes = [_cp, _sz, _cp, _sz, _cp, _sz, _cp, _sz, C.POINTER(_vp), _cp, _sz]
+    h = _vp()
+    err = C.create_string_buffer(1024)
+    _check(L.ref_load_mesh_text(coordinates, len(coordinates), elements, len(elements), dirichlet, len(dirichlet),
+                                neumann, len(neumann), C.byref(h), err, 1024), err)
+    return RMesh(handle=h.value)
+
+
+def save_mesh_text(rm: RMesh) -> tuple:
+    L = lib()
+    L.ref_save_mesh_text.argtypes = [_vp, C.c_int, _vp, _sz, C.POINTER(_sz)]
+    out = []
+    for which in range(4):
+        n = _sz()
+        L.ref_save_mesh_text(rm.h, which, None, 0, C.byref(n))
+        buf = C.create_string_buffer(max(n.value, 1))
+        L.ref_save_mesh_text(rm.h, which, buf, n.value, C.byref(n))
+        out.append(buf.raw[:n.value])
+    return tuple(out)
+
+
+def topology_csv(rm: RMesh) -> bytes:
+    L = lib()
+    L.ref_topology_csv.argtypes = [_vp, _vp, _sz, C.POINTER(_sz), _cp, _sz]
+    n = _sz()
+    err = C.create_string_buffer(512)
+    _check(L.ref_topology_csv(rm.h, None, 0, C.byref(n), err, 512), err)
+    buf = C.create_string_buffer(max(n.value, 1))
+    _check(L.ref_topology_csv(rm.h, buf, n.value, C.byref(n), err, 512), err)
+    return buf.raw[:n.value]

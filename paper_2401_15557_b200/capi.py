@@ -171,6 +171,8 @@ EXPORTED = [
     "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
     "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
+    "phfem_mesh_load_text", "phfem_mesh_load_dir", "phfem_mesh_format", "phfem_mesh_save_dir",
+    "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -277,6 +279,14 @@ def load_library(path: str = LIB_PATH):
         "phfem_midpoint_traces": (C.c_int, [vp, P(phfem_topology), vp, vp]),
         "phfem_csc_to_csr": (C.c_int, [vp, P(phfem_csc), P(phfem_csr)]),
         "phfem_csr_spmv": (C.c_int, [vp, P(phfem_csr), vp, vp]),
+        "phfem_mesh_load_text": (C.c_int, [vp, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.c_char_p,
+                                           C.c_size_t, C.c_char_p, C.c_size_t, P(phfem_mesh)]),
+        "phfem_mesh_load_dir": (C.c_int, [vp, C.c_char_p, P(phfem_mesh)]),
+        "phfem_mesh_format": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(vp), P(C.c_size_t)]),
+        "phfem_text_free": (None, [vp]),
+        "phfem_mesh_save_dir": (C.c_int, [vp, P(phfem_mesh), C.c_char_p]),
+        "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
+        "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -614,6 +624,51 @@ def constraint_csc(ctx: Context, mesh: DeviceMesh, topo: Topology, cls: Classifi
                 ctx.to_host(m.values, (m.nnz,), np.float64))
     finally:
         ctx.lib.phfem_csc_release(ctx.ptr, C.byref(m))
+
+
+# ---- on-disk formats (csrc/io.cu) ------------------------------
+def load_mesh_text(ctx: Context, coordinates: bytes, elements: bytes, dirichlet: bytes = b"",
+                   neumann: bytes = b"") -> "DeviceMesh":
+    """load_mesh (mesh.cpp:114-150) of the four files' contents."""
+    m = phfem_mesh()
+    ctx.check(ctx.lib.phfem_mesh_load_text(ctx.ptr, coordinates, len(coordinates), elements, len(elements),
+                                           dirichlet, len(dirichlet), neumann, len(neumann), C.byref(m)))
+    return DeviceMesh(ctx, m)
+
+
+def load_mesh_dir(ctx: Context, path: str) -> "DeviceMesh":
+    m = phfem_mesh()
+    ctx.check(ctx.lib.phfem_mesh_load_dir(ctx.ptr, path.encode(), C.byref(m)))
+    return DeviceMesh(ctx, m)
+
+
+def save_mesh_text(ctx: Context, mesh: "DeviceMesh") -> tuple:
+    """save_mesh (mesh.cpp:170-180): (coordinates, elements, dirichlet, neumann) bytes."""
+    out = []
+    for which in range(4):
+        p, n = C.c_void_p(), C.c_size_t()
+        ctx.check(ctx.lib.phfem_mesh_format(ctx.ptr, C.byref(mesh.m), which, C.byref(p), C.byref(n)))
+        out.append(_take_text(ctx, p, n))
+    return tuple(out)
+
+
+def _take_text(ctx: Context, p, n) -> bytes:
+    try:
+        # (string_at takes a C int size: texts pass 2 GB at L12)
+        return (C.c_char * n.value).from_address(p.value).raw if n.value else b""
+    finally:
+        ctx.lib.phfem_text_free(p)
+
+
+def save_mesh_dir(ctx: Context, mesh: "DeviceMesh", path: str):
+    ctx.check(ctx.lib.phfem_mesh_save_dir(ctx.ptr, C.byref(mesh.m), path.encode()))
+
+
+def topology_csv(ctx: Context, mesh: "DeviceMesh", topo: "Topology") -> bytes:
+    """The CLI's topology CSV (tools/main.cpp:302-323)."""
+    p, n = C.c_void_p(), C.c_size_t()
+    ctx.check(ctx.lib.phfem_topology_csv(ctx.ptr, C.byref(mesh.m), C.byref(topo.t), C.byref(p), C.byref(n)))
+    return _take_text(ctx, p, n)
 
 
 # ---- verification around the solve (SURVEY §8(f4); csrc/verify.cu) ----------
