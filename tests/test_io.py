@@ -3,7 +3,7 @@
 
 The checker is the reference itself: its own mesh.cpp (load_mesh on
 istringstreams, save_mesh on ostringstreams) and edge_topology.cpp compiled
-in oracle/_ref.  not gpu: committed fixtures (tests/golden/io_golden.npz,
+in oracle/_ref.  not gpu: committed fixtures (tests/golden/io/io_golden.npz,
 made by tools/make_golden_io.py from the reference) are reproduced by the
 reference build.  gpu: csrc/io.cu against the reference — parsed arrays bit
 for bit, written text byte for byte, and every validation error with the
@@ -19,7 +19,7 @@ from oracle import reference as R
 from paper_2401_15557_b200 import capi, meshgen as G
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-GOLDEN = os.path.join(HERE, "golden", "io_golden.npz")
+GOLDEN = os.path.join(HERE, "golden", "io", "io_golden.npz")
 needs_ref = pytest.mark.skipif(not R.available(), reason="reference build unavailable")
 
 

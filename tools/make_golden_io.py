@@ -1,4 +1,4 @@
-"""Generate tests/golden/io_golden.npz from the REFERENCE build (oracle/_ref):
+"""Generate tests/golden/io/io_golden.npz from the REFERENCE build (oracle/_ref):
 save_mesh text and the CLI's topology CSV of the test meshes, and load_mesh's
 result (arrays or exception text) for every case of tests/test_io.py.
 Run in the container that has /root/reference (the fixture is committed)."""
@@ -26,5 +26,5 @@ for name, c, e, d, n in T.CASES:
     else:
         for k, x in enumerate(T.arrays(hm)):
             out[f"case_{name}_{k}"] = x
-np.savez_compressed(os.path.join(ROOT, "tests", "golden", "io_golden.npz"), **out)
+np.savez_compressed(os.path.join(ROOT, "tests", "golden", "io", "io_golden.npz"), **out)
 print(len(out), "arrays")
