@@ -269,7 +269,8 @@ def run_ours_sharded(args, rank, world, local):
     """N > 1: the same step (L12 resident -> L13 outputs) sharded over the
     ranks (paper_2401_15557_b200/dist.py): element ranges,
     key-range all-to-all edge dedup over NCCL, replicated midpoints.  Every
-    rank keeps its slices; value = total L13 triangles / max-over-ranks time."""
+    rank keeps its slices; value = total L13 triangles / max-over-ranks time.
+    The refined level is built sort-free from the parent's topology."""
     import torch
     from paper_2401_15557_b200 import capi, dist, meshgen as G
     torch.cuda.set_device(local)
@@ -295,6 +296,12 @@ def run_ours_sharded(args, rank, world, local):
 
     for _ in range(args.warmup):
         nC, nE, n_own = step()
+    if os.environ.get("PHFEM_DIST_KPROF"):  # per-kernel times of one step (debug)
+        ctx.profile(True)
+        step()
+        for k, (kms, kn) in sorted(ctx.profile_read().items(), key=lambda kv: -kv[1][0])[:25]:
+            print(f"[kprof] {k:28s} {kms:8.3f} ms  x{kn}", file=sys.stderr, flush=True)
+        ctx.profile(False)
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist_barrier(world)
@@ -326,7 +333,9 @@ def run_ours_sharded(args, rank, world, local):
         "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} ({nE} triangles): "
                                "EG+RF+EG+AS, config-2 coefficients, sharded",
                    "parallelism": f"element-range x key-range sharding over {world} GPUs (NCCL all-to-all)",
-                   "refined_edge_generation": "sort-based key-range dedup (generic)",
+                   "refined_edge_generation": "input level: key-range all-to-all dedup; refined level: "
+                                              "from the parent topology (SURVEY f1, all-gathered parent "
+                                              "elem_edge / elements, no occurrence exchange)",
                    "triangles": nE, "own_triangles_rank0": n_own, "l2": "inputs larger than L2 (no flush)"},
         "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
                               "peak": peak * world, "peak_kind": peak_kind, "frac": round(gbs / (peak * world), 4)},

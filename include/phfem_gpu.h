@@ -218,7 +218,12 @@ phfem_status phfem_step_matrix(phfem_ctx* ctx, int32_t nE, const double* B, cons
                                double sign, phfem_csc* out);
 
 /* ---- load vectors --------------------------------------------------------
- * assemble_load (assembly.hpp:84; assembly.cpp:179-203) -> out[3nE]          */
+ * assemble_volume_operators + assemble_load (assembly.cpp:120-142, 179-203)
+ * fused in one element pass: identical values, one read of the mesh.       */
+phfem_status phfem_assemble_volume_load(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                        const phfem_coeffs* c, const phfem_field* f, double t,
+                                        double* B, double* D, double* M, double* M0, double* load);
+/* assemble_load (assembly.hpp:84; assembly.cpp:179-203) -> out[3nE]         */
 phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_field* f,
                                  double t, double* out);
 /* assemble_neumann (assembly.hpp:87-89; assembly.cpp:205-228).
@@ -383,10 +388,13 @@ phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n, in
                               int32_t node_hi, int32_t nC_all, int32_t nE_all, phfem_topology* out,
                               int32_t* pairs);
 /* pairs -> global edge ids (+E0) routed to the element owner (esplits[W+1]);
- * the receiver writes them into its elem_edge ([3(ehi-elo)]).              */
+ * the receiver writes them into its elem_edge ([3(ehi-elo)]).  Pairs of the
+ * caller's own elements [self_lo, self_hi) are written to self_elem_edge
+ * directly and not sent (self_lo = self_hi: route everything).            */
 phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pairs, int64_t n, int32_t E0,
                                     const int32_t* esplits, int32_t W, int32_t* counts,
-                                    int32_t* offsets, int32_t* send);
+                                    int32_t* offsets, int32_t* send, int32_t self_lo,
+                                    int32_t self_hi, int32_t* self_elem_edge);
 phfem_status phfem_dist_apply_pairs(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t elo,
                                     int32_t* elem_edge);
 /* a[i] += off (only_nonneg: where a[i] >= 0) — re-basing local ids         */
@@ -398,8 +406,10 @@ phfem_status phfem_dist_add_offset(phfem_ctx* ctx, int32_t* a, int64_t n, int32_
 phfem_status phfem_dist_resolve(phfem_ctx* ctx, const phfem_topology* part, int32_t node_lo,
                                 int32_t E0, const int32_t* pairs, int32_t n, int32_t list_base,
                                 int32_t* ids, unsigned long long* err);
-/* classification of the rank's edges from the global Dirichlet / Neumann id
- * lists: rank-local retained_pos / retained_edges / id lists / bitmap.      */
+/* classification of the rank's edges from its Dirichlet / Neumann edges
+ * (LOCAL ids, list order): rank-local retained_pos / retained_edges / id
+ * lists / bitmap.  E0 = global id of the part's first edge (the part's
+ * boundary list holds global ids after phfem_dist_add_offset).              */
 phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
                                  const int32_t* dir_ids, int32_t nD, const int32_t* neu_ids,
                                  int32_t nN, phfem_classification* out);
@@ -474,6 +484,20 @@ phfem_status phfem_topology_csv(phfem_ctx* ctx, const phfem_mesh* mesh, const ph
                                 char** out, size_t* len);
 phfem_status phfem_topology_csv_file(phfem_ctx* ctx, const phfem_mesh* mesh,
                                      const phfem_topology* topo, const char* path);
+
+/* Distributed refined level (§8(e) with SURVEY f1): the rank's part of the
+ * fine topology straight from its parent part `ppart` (parent edges
+ * [E0p, E0p + ppart->E), lists with global ids) and the all-gathered parent
+ * elem_edge / elements — no sort, no occurrence exchange.  Fine node range
+ * [node_lo, node_hi) with node_hi = nc + E0p + E; local fine ids (re-base as
+ * for phfem_dist_dedup); *pairs_out (ctx memory, 2 x out->E int2, free with
+ * phfem_free) = (fine slot, f / ~f) per fine edge for
+ * phfem_dist_route_pairs; mids (nullable, [E][2]) = the rank's midpoints.   */
+phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                     const int32_t* elem_edge_all, const int32_t* elements_all,
+                                     int32_t nE_all, const double* coords, int32_t nc,
+                                     int32_t node_lo, int32_t node_hi, phfem_topology* out,
+                                     int32_t** pairs_out, double* mids);
 
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'

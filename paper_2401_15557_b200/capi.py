@@ -172,7 +172,8 @@ EXPORTED = [
     "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
     "phfem_mesh_load_text", "phfem_mesh_load_dir", "phfem_mesh_format", "phfem_mesh_save_dir",
-    "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free",
+    "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free", "phfem_dist_refine_level",
+    "phfem_assemble_volume_load",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -256,7 +257,7 @@ def load_library(path: str = LIB_PATH):
         "phfem_step_matrix": (C.c_int, [vp, i32, vp, vp, vp, vp, P(phfem_csc), dbl, dbl, P(phfem_csc)]),
         "phfem_dist_midpoints": (C.c_int, [vp, vp, vp, i32, vp]),
         "phfem_dist_dedup": (C.c_int, [vp, vp, i64, i32, i32, i32, i32, P(phfem_topology), vp]),
-        "phfem_dist_route_pairs": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp]),
+        "phfem_dist_route_pairs": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp, i32, i32, vp]),
         "phfem_dist_apply_pairs": (C.c_int, [vp, vp, i64, i32, vp]),
         "phfem_dist_add_offset": (C.c_int, [vp, vp, i64, i32, C.c_int]),
         "phfem_dist_resolve": (C.c_int, [vp, P(phfem_topology), i32, i32, vp, i32, i32, vp, vp]),
@@ -284,6 +285,10 @@ def load_library(path: str = LIB_PATH):
         "phfem_mesh_load_dir": (C.c_int, [vp, C.c_char_p, P(phfem_mesh)]),
         "phfem_mesh_format": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(vp), P(C.c_size_t)]),
         "phfem_text_free": (None, [vp]),
+        "phfem_assemble_volume_load": (C.c_int, [vp, P(phfem_mesh), P(phfem_coeffs), P(phfem_field), dbl,
+                                                 vp, vp, vp, vp, vp]),
+        "phfem_dist_refine_level": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, vp, i32, i32, i32,
+                                              P(phfem_topology), P(vp), vp]),
         "phfem_mesh_save_dir": (C.c_int, [vp, P(phfem_mesh), C.c_char_p]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),

@@ -591,6 +591,29 @@ PHFEM_API phfem_status phfem_assemble_volume(phfem_ctx* ctx, const phfem_mesh* m
   return volume_errors(ctx, true, false);
 }
 
+// assemble_volume_operators + assemble_load in one element pass (the fused
+// k_volume of the pipeline): same values as the two calls, one read of the mesh
+PHFEM_API phfem_status phfem_assemble_volume_load(phfem_ctx* ctx, const phfem_mesh* mesh,
+                                                  const phfem_coeffs* c, const phfem_field* f, double t,
+                                                  double* B, double* D, double* M, double* M0,
+                                                  double* load) {
+  if (!ctx || !mesh || !c || !f || (!load && mesh->nE)) return PHFEM_ERR_INVALID_ARGUMENT;
+  VolArgs a = make_vol_args(mesh);
+  a.coeffs = *c;
+  a.B = B;
+  a.D = D;
+  a.M = M;
+  a.M0 = M0;
+  a.f = *f;
+  a.t = t;
+  a.load = load;
+  a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0) && aligned16(load);
+  PHFEM_TRY(errors_reset(ctx));
+  PHFEM_TRY(launch_volume(ctx, a, true, true));
+  PHFEM_TRY(errors_fetch(ctx));
+  return volume_errors(ctx, true, true);
+}
+
 PHFEM_API phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh,
                                            const phfem_field* f, double t, double* out) {
   if (!ctx || !mesh || !f || (!out && mesh->nE)) return PHFEM_ERR_INVALID_ARGUMENT;

@@ -49,9 +49,10 @@ __global__ void k_cls_pairs(const int32_t* __restrict__ dir_pairs, int nD,
 }
 
 // One thread per 1024-edge block: Neumann count (bitmap popcount) and boundary
-// count (two lower_bounds into the ascending boundary list).
+// count (two lower_bounds into the ascending boundary list, whose ids start at
+// `base`: 0, or the global id of a rank part's first edge).
 __global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
-                                   const int32_t* __restrict__ boundary, int nB, int E, int nblk,
+                                   const int32_t* __restrict__ boundary, int nB, int E, int nblk, int base,
                                    int32_t* __restrict__ cnt_bnd, int32_t* __restrict__ cnt_neu) {
   const int blk = blockIdx.x * blockDim.x + threadIdx.x;
   if (blk > nblk) return;
@@ -72,7 +73,7 @@ __global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
     }
     return l;
   };
-  cnt_bnd[blk] = lower(min(E, (blk + 1) * kEdgeBlock)) - lower(blk * kEdgeBlock);
+  cnt_bnd[blk] = lower(base + min(E, (blk + 1) * kEdgeBlock)) - lower(base + blk * kEdgeBlock);
   cnt_neu[blk] = nn;
 }
 
@@ -136,12 +137,12 @@ namespace phfem {
 // the ascending boundary list; with_retained also retained_pos / _edges
 static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topology* topo,
                                               phfem_classification* out, int nblk,
-                                              bool with_retained) {
+                                              bool with_retained, int bnd_base = 0) {
   const int E = topo->E;
   int32_t* pre_bnd = out->block_prefix;
   int32_t* pre_neu = out->block_prefix + nblk + 1;
   PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
-      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, pre_bnd, pre_neu));
+      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, bnd_base, pre_bnd, pre_neu));
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
   if (nblk > 0 && with_retained) {
@@ -209,13 +210,13 @@ namespace phfem {
 // Distributed ranks (dist.cu): the Neumann bitmap and the owned id lists are
 // set; block prefixes, retained_pos / retained_edges and L follow.
 phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo,
-                                      phfem_classification* out) {
+                                      phfem_classification* out, int bnd_base) {
   const int E = topo->E;
   const int nblk = (E + kEdgeBlock - 1) / kEdgeBlock;
   PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
   PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
   PHFEM_TRY(dalloc(ctx, &out->block_prefix, 2 * ((int64_t)nblk + 1)));
-  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, true));
+  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, true, bnd_base));
   int32_t nneu = 0;
   PHFEM_CUDA(ctx, cudaMemcpyAsync(&nneu, out->block_prefix + nblk + 1 + nblk, sizeof(int32_t),
                                   cudaMemcpyDeviceToHost, ctx->stream));

@@ -87,15 +87,23 @@ __global__ void __launch_bounds__(kRouteThreads) k_dist_occ(const int32_t* __res
 }
 
 // pairs (slot 3m+l, local edge or ~local edge) -> global edge ids, routed to
-// the element owner; slot < 0 marks "no t_minus"
+// the element owner; slot < 0 marks "no t_minus".  Pairs of the own element
+// range [3 lo, 3 hi) (self_lo < self_hi) are applied to self_ee directly (no
+// send, no exchange).
 __global__ void __launch_bounds__(kRouteThreads) k_dist_pairs(const int2* __restrict__ pairs, int64_t n, int E0,
                              const int32_t* __restrict__ esplits, int W, int32_t* __restrict__ cnt,
-                             int32_t* __restrict__ cursor, int2* __restrict__ send) {
+                             int32_t* __restrict__ cursor, int2* __restrict__ send, int self_lo,
+                             int self_hi, int32_t* __restrict__ self_ee) {
   route_block<int2>(n, W, [&](int64_t i, int2& q) {
     const int2 p = pairs[i];
     if (p.x < 0) return -1;
     q = make_int2(p.x, p.y >= 0 ? p.y + E0 : ~(~p.y + E0));
-    return dest_of(esplits, W, p.x / 3);
+    const int m = p.x / 3;
+    if (m >= self_lo && m < self_hi) {
+      if (send) self_ee[p.x - 3 * (int64_t)self_lo] = q.y;  // (once: in the scatter pass)
+      return -1;
+    }
+    return dest_of(esplits, W, m);
   }, cnt, cursor, send);
 }
 
@@ -287,15 +295,17 @@ PHFEM_API phfem_status phfem_dist_occurrences(phfem_ctx* ctx, const int32_t* ele
 
 PHFEM_API phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pairs, int64_t n,
                                               int32_t E0, const int32_t* esplits, int32_t W,
-                                              int32_t* counts, int32_t* offsets, int32_t* send) {
+                                              int32_t* counts, int32_t* offsets, int32_t* send,
+                                              int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge) {
   if (!ctx || (!pairs && n) || !esplits || !counts || W < 1) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (self_lo < self_hi && !self_elem_edge) return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
   if (W >= kMaxDest) return PHFEM_ERR_INVALID_ARGUMENT;
   const int grid = grid_for(n, kRouteThreads * kRouteK, ctx->num_sms * 8);
   const int2* p2 = reinterpret_cast<const int2*>(pairs);
   if (n > 0)
     PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, kRouteThreads, 0, ctx->stream>>>(
-        p2, n, E0, esplits, W, counts, nullptr, nullptr));
+        p2, n, E0, esplits, W, counts, nullptr, nullptr, self_lo, self_hi, self_elem_edge));
   if (!send) return PHFEM_OK;
   if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
   int32_t* cursor = nullptr;
@@ -306,7 +316,8 @@ PHFEM_API phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pai
   PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
   if (n > 0)
     PHFEM_LAUNCH(ctx, "k_dist_pairs", k_dist_pairs<<<grid, kRouteThreads, 0, ctx->stream>>>(
-        p2, n, E0, esplits, W, nullptr, cursor, reinterpret_cast<int2*>(send)));
+        p2, n, E0, esplits, W, nullptr, cursor, reinterpret_cast<int2*>(send), self_lo, self_hi,
+        self_elem_edge));
   dfree(ctx, cursor);
   return PHFEM_OK;
 }
@@ -342,10 +353,12 @@ PHFEM_API phfem_status phfem_dist_resolve(phfem_ctx* ctx, const phfem_topology* 
 }
 
 namespace phfem {
-phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo,
-                                      phfem_classification* out);
+phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo, phfem_classification* out,
+                                      int bnd_base);
 }
 
+// dir_ids / neu_ids: the rank's edges, LOCAL ids; E0 = global id of the
+// part's first edge (its boundary list holds global ids after re-basing).
 PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
                                            const int32_t* dir_ids, int32_t nD,
                                            const int32_t* neu_ids, int32_t nN,
@@ -362,7 +375,7 @@ PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology*
   PHFEM_CUDA(ctx, cudaMemsetAsync(dup, 0, sizeof(unsigned long long), ctx->stream));
   if (nN > 0)
     PHFEM_LAUNCH(ctx, "k_dist_neu_bits", k_dist_neu_bits<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
-        neu_ids, nN, E0, E, out->neumann_bits, dup));
+        neu_ids, nN, 0, E, out->neumann_bits, dup));
   // local Dirichlet / Neumann id lists (owned entries, list order)
   auto compact = [&](const int32_t* ids, int n, int32_t** dst, int32_t* count) -> phfem_status {
     int32_t* flag = nullptr;
@@ -370,7 +383,7 @@ PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology*
     PHFEM_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int32_t) * (n + 1), ctx->stream));
     if (n > 0)
       PHFEM_LAUNCH(ctx, "k_dist_local_ids", k_dist_local_ids<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
-          ids, n, E0, E, flag));
+          ids, n, 0, E, flag));
     PHFEM_TRY(scan_exclusive_i32(ctx, flag, flag, (int64_t)n + 1, nullptr));
     int32_t c = 0;
     PHFEM_CUDA(ctx, cudaMemcpyAsync(&c, flag + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -378,7 +391,7 @@ PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology*
     PHFEM_TRY(dalloc(ctx, dst, c));
     if (n > 0)
       PHFEM_LAUNCH(ctx, "k_dist_compact", k_dist_compact<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
-          ids, flag, n, E0, E, *dst));
+          ids, flag, n, 0, E, *dst));
     *count = c;
     dfree(ctx, flag);
     return PHFEM_OK;
@@ -390,7 +403,7 @@ PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology*
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   dfree(ctx, dup);
   out->flags = hdup ? PHFEM_CLS_DUP_NEUMANN : 0;
-  return classify_lists_from_bits(ctx, part, out);
+  return classify_lists_from_bits(ctx, part, out, E0);
 }
 
 PHFEM_API phfem_status phfem_dist_neumann_table(phfem_ctx* ctx, const phfem_topology* part,

@@ -58,6 +58,10 @@ struct LvArgs {
   // parent classification (kFull)
   const uint32_t* neu_bits;
   int E, nc, Ef, L;
+  // distributed level (phfem_dist_refine_level): the parent edge arrays hold
+  // edges [eb, eb + E) at local indices; node_edge_start covers the fine node
+  // range from nlo.  Both 0 on one GPU.
+  int eb, nlo;
   // exclusive per-tile prefixes (k_rl_tile_init / k_rl_tile_count + scans):
   // fine edges, parent boundary edges, parent Neumann edges before the tile
   const int32_t* tileF;
@@ -74,7 +78,9 @@ struct LvOut {
   int32_t* boundary;
   int32_t* elem_edge;
   int32_t* node_edge_start;
-  double2* mid;  // fine coords base (nullable): node nc + e = midpoint of parent edge e
+  double2* mid;  // nullable: mid[nc + e - mid_base] = midpoint of parent edge e
+  int64_t mid_base;
+  int2* pairs;   // distributed level: (slot 3m+l, f / ~f) per fine edge instead of elem_edge
   // kFull
   int32_t* rpos;
   int32_t* redges;
@@ -109,13 +115,14 @@ __device__ __forceinline__ double2 midpt(double2 p, double2 q) {
 // group y and two in group z — so the fine-edge count of a tile is
 // 2 (edges in tile) + element contributions, accumulated element-parallel
 // (coalesced elem_edge reads, warp-aggregated atomics).
-__global__ void k_rl_tile_init(int E, int ntiles, const int32_t* __restrict__ boundary, int nB,
+__global__ void k_rl_tile_init(int E, int eb, int ntiles, const int32_t* __restrict__ boundary, int nB,
                                const uint32_t* __restrict__ neu_bits, int32_t* __restrict__ tileF,
                                int32_t* __restrict__ tileB, int32_t* __restrict__ tileN) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
-    const int64_t e0 = (int64_t)t * kLvT;
-    const int64_t e1 = e0 + kLvT < E ? e0 + kLvT : E;
-    tileF[t] = 2 * (int)(e1 - e0);
+    const int64_t l0 = (int64_t)t * kLvT;
+    const int64_t l1 = l0 + kLvT < E ? l0 + kLvT : E;
+    const int64_t e0 = eb + l0, e1 = eb + l1;  // global parent edge ids of the tile
+    tileF[t] = 2 * (int)(l1 - l0);
     auto lower = [&](int64_t key) {  // ascending boundary list
       int l = 0, r = nB;
       while (l < r) {
@@ -139,16 +146,17 @@ __device__ __forceinline__ void warp_add(int32_t* ctr, int key, int v) {
   if ((int)lane_id() == __ffs(g) - 1) atomicAdd(ctr + key, v * __popc(g));
 }
 
-__global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE,
+// (eb, E): only the groups of parent edges [eb, eb + E) count (a rank's range)
+__global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE, int eb, int E,
                                 int32_t* __restrict__ tileF) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
     const int x = abs_edge(__ldg(elem_edge + 3 * m)), y = abs_edge(__ldg(elem_edge + 3 * m + 1)),
               z = abs_edge(__ldg(elem_edge + 3 * m + 2));
-    const int hi = max(x, max(y, z));
-    const int md = max(min(x, y), min(max(x, y), z));
-    warp_add(tileF, md / kLvT, 1);
-    warp_add(tileF, hi / kLvT, 2);
+    const int hi = max(x, max(y, z)) - eb;
+    const int md = max(min(x, y), min(max(x, y), z)) - eb;
+    if (md >= 0 && md < E) warp_add(tileF, md / kLvT, 1);
+    if (hi >= 0 && hi < E) warp_add(tileF, hi / kLvT, 2);
   }
 }
 
@@ -161,21 +169,22 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
   const int64_t e0 = (int64_t)tile * kLvT;
-  const int e = (int)(e0 + tid);
-  const bool valid = e < a.E;
+  const int le = (int)(e0 + tid);  // index into the parent edge arrays
+  const int e = a.eb + le;         // global parent edge id
+  const bool valid = le < a.E;
 
   // 1. the parent edge record (coalesced) and the element gathers
   int2 ab = make_int2(0, 0), el = make_int2(0, -1);
   int l = 0, l2 = 0;
   bool neu = false;
   if (valid) {
-    ab = reinterpret_cast<const int2*>(a.edge_nodes)[e];
-    el = reinterpret_cast<const int2*>(a.edge_elements)[e];
-    l = __ldg(a.ltp + e);
+    ab = reinterpret_cast<const int2*>(a.edge_nodes)[le];
+    el = reinterpret_cast<const int2*>(a.edge_elements)[le];
+    l = __ldg(a.ltp + le);
     if (kFull) neu = (__ldg(a.neu_bits + (e >> 5)) >> (e & 31)) & 1u;
   }
   const bool has_m = valid && el.y >= 0;
-  if (has_m) l2 = __ldg(a.ltm + e);
+  if (has_m) l2 = __ldg(a.ltm + le);
   const int tp = el.x, tm = el.y;
   int P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
   int vop = 0, vom = 0;
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   const int mu = a.nc + e;
   const double2 me = midpt(ca, cb);
   if (valid) {
-    if (o.mid) o.mid[mu] = me;
+    if (o.mid) o.mid[mu - o.mid_base] = me;
     auto emit = [&](int j, int from, int to, int tpf, int lp, int tmf, int lm, double len) {
       const int i = i0 + j;
       s.en[i] = make_int2(from, to);
@@ -274,8 +283,8 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   const int N0 = kFull ? __ldg(a.tileN + tile) : 0;
   __syncthreads();
   if (valid) {
-    o.node_edge_start[mu] = F0 + i0;
-    if (e == a.E - 1) o.node_edge_start[mu + 1] = a.Ef;
+    o.node_edge_start[mu - a.nlo] = F0 + i0;
+    if (le == a.E - 1) o.node_edge_start[mu - a.nlo + 1] = a.Ef;
   }
 
   // 5. coalesced stores of the tile's fine edges [F0, F0 + nf)
@@ -294,8 +303,13 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
     const int sl = ms >> 8;  // arithmetic shift: boundary slots stay negative
     if (sl < 0) o.boundary[off_bnd + ~sl] = f;
     else o.interior[off_int + sl] = f;
-    o.elem_edge[3 * (int64_t)el2.x + lp] = f;
-    if (lm >= 0) o.elem_edge[3 * (int64_t)el2.y + lm] = ~f;
+    if (o.pairs) {  // distributed: to the owners of the fine elements (coalesced)
+      o.pairs[2 * (int64_t)f] = make_int2(3 * el2.x + lp, f);
+      o.pairs[2 * (int64_t)f + 1] = lm >= 0 ? make_int2(3 * el2.y + lm, ~f) : make_int2(-1, 0);
+    } else {
+      o.elem_edge[3 * (int64_t)el2.x + lp] = f;
+      if (lm >= 0) o.elem_edge[3 * (int64_t)el2.y + lm] = ~f;
+    }
     if (kFull) {
       const int rr = s.rr[i];
       o.rpos[f] = rr < 0 ? -1 : off_rp + (rr >> 16);
@@ -347,9 +361,9 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
   PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 3 * (ntiles + 1), ctx->stream));
   const uint32_t* nbits = pcls ? pcls->neumann_bits : nullptr;
   PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-      (int)E, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN));
+      (int)E, 0, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN));
   PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count<<<grid_for(parent->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-      ptopo->elem_edge, parent->nE, tileF));
+      ptopo->elem_edge, parent->nE, 0, (int)E, tileF));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
   if (pcls) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, nullptr));
@@ -495,4 +509,93 @@ PHFEM_API phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* pare
                                           const phfem_mesh* fine, phfem_topology* topo,
                                           phfem_classification* cls, phfem_csr* C) {
   return refine_level_impl(ctx, parent, ptopo, pcls, fine, topo, cls, C, nullptr);
+}
+
+// Distributed refined level (SURVEY §8(e) + f1): this rank's part of the fine
+// topology from its parent part (edges [E0p, E0p + E) with local arrays and
+// global-id lists) and the all-gathered parent elem_edge / elements, no sort
+// and no occurrence exchange.  Fine edges of the rank are its groups, in
+// order (local ids); the fine elem_edge entries leave as (slot, f / ~f) pairs
+// for the element owners (phfem_dist_route_pairs).  node range [node_lo,
+// node_hi) must end at nc + E0p + E (the rank's last midpoint node).
+PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                               const int32_t* elem_edge_all, const int32_t* elements_all,
+                                               int32_t nE_all, const double* coords, int32_t nc,
+                                               int32_t node_lo, int32_t node_hi, phfem_topology* out,
+                                               int32_t** pairs_out, double* mids) {
+  if (!ctx || !ppart || !out || !pairs_out) return PHFEM_ERR_INVALID_ARGUMENT;
+  memset(out, 0, sizeof(*out));
+  *pairs_out = nullptr;
+  const int64_t E = ppart->E;
+  if ((E > 0 && (!elem_edge_all || !elements_all || !coords)) || E0p < 0 || node_lo < 0 ||
+      node_hi < node_lo || (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) ||
+      (E > 0 && node_lo > nc + E0p) || 4 * (int64_t)nE_all >= (int64_t(1) << 31))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  const int64_t ntiles = std::max<int64_t>(1, (E + kLvT - 1) / kLvT);
+  int32_t* tiles = nullptr;
+  PHFEM_TRY(dalloc(ctx, &tiles, 2 * (ntiles + 1) + 1));
+  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *total = tiles + 2 * (ntiles + 1);
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (2 * (ntiles + 1) + 1), ctx->stream));
+  if (E > 0) {
+    PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, nullptr, tileF, tileB, nullptr));
+    PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count<<<grid_for(nE_all, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        elem_edge_all, nE_all, E0p, (int)E, tileF));
+  }
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
+  int32_t Ef = 0;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&Ef, total, sizeof Ef, cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int64_t nBf = 2 * (int64_t)ppart->n_boundary;
+  out->nC = node_hi - node_lo;
+  out->nE = 4 * nE_all;
+  out->E = Ef;
+  out->n_boundary = (int32_t)nBf;
+  out->n_interior = (int32_t)(Ef - nBf);
+  const int64_t cap = std::max<int64_t>(Ef, 1);
+  PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * cap));
+  PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * cap));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tplus, cap));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tminus, cap));
+  PHFEM_TRY(dalloc(ctx, &out->interior_edges, std::max<int64_t>(Ef - nBf, 1)));
+  PHFEM_TRY(dalloc(ctx, &out->boundary_edges, std::max<int64_t>(nBf, 1)));
+  PHFEM_TRY(dalloc(ctx, &out->node_edge_start, (int64_t)out->nC + 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * ((int64_t)out->nC + 1), ctx->stream));
+  int32_t* pairs = nullptr;
+  PHFEM_TRY(dalloc(ctx, &pairs, 4 * cap));
+  if (E > 0) {
+    LvArgs a;
+    memset(&a, 0, sizeof a);
+    a.edge_nodes = ppart->edge_nodes;
+    a.edge_elements = ppart->edge_elements;
+    a.ltp = ppart->local_in_tplus;
+    a.ltm = ppart->local_in_tminus;
+    a.elem_edge = elem_edge_all;
+    a.elements = elements_all;
+    a.coords = (const double2*)coords;
+    a.E = (int)E;
+    a.nc = nc;
+    a.Ef = Ef;
+    a.eb = E0p;
+    a.nlo = node_lo;
+    a.tileF = tileF;
+    a.tileB = tileB;
+    LvOut o;
+    memset(&o, 0, sizeof o);
+    o.edge_nodes = out->edge_nodes;
+    o.edge_elements = out->edge_elements;
+    o.ltp = out->local_in_tplus;
+    o.ltm = out->local_in_tminus;
+    o.interior = out->interior_edges;
+    o.boundary = out->boundary_edges;
+    o.node_edge_start = out->node_edge_start;
+    o.mid = (double2*)mids;
+    o.mid_base = (int64_t)nc + E0p;
+    o.pairs = reinterpret_cast<int2*>(pairs);
+    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)((E + kLvT - 1) / kLvT), kLvT, 0, ctx->stream>>>(a, o));
+  }
+  dfree(ctx, tiles);
+  *pairs_out = pairs;
+  return PHFEM_OK;
 }

@@ -190,19 +190,45 @@ class CudaRankOps:
                                            self.p(pairs)))
         self.part = capi.Topology(self.ctx, t)
         self.pairs = pairs[:2 * t.E]
+        self._pairs = (pairs.data_ptr(), 2 * int(t.E), False)
         return int(t.E), int(t.n_boundary)
 
-    def route_pairs(self, E0, esplits):
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all):
+        """The rank's part of the refined topology from its parent part (sort
+        free, phfem_dist_refine_level); returns (E, n_boundary, midpoints)."""
+        t = capi.phfem_topology()
+        pairs = C.c_void_p()
+        pt = self.part.t
+        Ep = int(pt.E)  # (the parent part is released below)
+        mids = self.empty((max(Ep, 1), 2), torch.float64)
+        self._ck(self.lib.phfem_dist_refine_level(self.ctx.ptr, C.byref(pt), E0p, self.p(ee_all), self.p(el_all),
+                                                  nE_all, self.p(coords), nc, nlo, nhi, C.byref(t), C.byref(pairs),
+                                                  self.p(mids)))
+        self.part.release()
+        self.part = capi.Topology(self.ctx, t)
+        self._pairs = (pairs.value, 2 * int(t.E), True)
+        return int(t.E), int(t.n_boundary), mids[:Ep]
+
+    def route_pairs(self, E0, esplits, elo, ehi):
+        """Pairs of the own (destination-level) elements [elo, ehi) go straight
+        into the next elem_edge; the rest is packed by owner for the exchange."""
         W = esplits.numel() - 1
+        ptr, n, owned = self._pairs
         cnt, off = self.empty(W), self.empty(W + 1)
-        send = self.empty((max(self.pairs.shape[0], 1), 2))
-        self._ck(self.lib.phfem_dist_route_pairs(self.ctx.ptr, self.p(self.pairs), self.pairs.shape[0], E0,
-                                                 self.p(esplits), W, self.p(cnt), self.p(off), self.p(send)))
+        send = self.empty((max(n, 1), 2))
+        self._ee_next = self.empty((ehi - elo, 3))
+        self._ck(self.lib.phfem_dist_route_pairs(self.ctx.ptr, C.c_void_p(ptr) if n else None, n, E0,
+                                                 self.p(esplits), W, self.p(cnt), self.p(off), self.p(send), elo, ehi,
+                                                 self.p(self._ee_next)))
+        if owned:
+            self.ctx.free(ptr)
+        self._pairs = (0, 0, False)
+        self.pairs = None
         c = cnt.tolist()
         return send[:sum(c)], c
 
     def apply_pairs(self, recv, elo, ehi):
-        ee = self.empty((ehi - elo, 3))
+        ee, self._ee_next = self._ee_next, None
         self._ck(self.lib.phfem_dist_apply_pairs(self.ctx.ptr, self.p(recv), recv.shape[0], elo, self.p(ee)))
         return ee
 
@@ -241,9 +267,9 @@ class CudaRankOps:
         return out[:4 * n]
 
     # -- classification, C, boundary vectors, blocks ------------------------------------------
-    def classify(self, dir_ids_local, neu_ids_local):
+    def classify(self, dir_ids_local, neu_ids_local, E0):
         c = capi.phfem_classification()
-        self._ck(self.lib.phfem_dist_classify(self.ctx.ptr, C.byref(self.part.t), 0, self.p(dir_ids_local),
+        self._ck(self.lib.phfem_dist_classify(self.ctx.ptr, C.byref(self.part.t), E0, self.p(dir_ids_local),
                                               dir_ids_local.numel(), self.p(neu_ids_local), neu_ids_local.numel(),
                                               C.byref(c)))
         self.cls = capi.Classification(self.ctx, c)
@@ -268,10 +294,10 @@ class CudaRankOps:
     def volume(self, mview, coeffs, f, t):
         n = mview.nE
         out = {k: self.empty((max(n, 1), 9), torch.float64) for k in ("B", "D", "M", "M0")}
-        self._ck(self.lib.phfem_assemble_volume(self.ctx.ptr, C.byref(mview), C.byref(coeffs), self.p(out["B"]),
-                                                self.p(out["D"]), self.p(out["M"]), self.p(out["M0"])))
         load = self.empty((max(n, 1), 3), torch.float64)
-        self._ck(self.lib.phfem_assemble_load(self.ctx.ptr, C.byref(mview), C.byref(f), t, self.p(load)))
+        self._ck(self.lib.phfem_assemble_volume_load(self.ctx.ptr, C.byref(mview), C.byref(coeffs), C.byref(f), t,
+                                                     self.p(out["B"]), self.p(out["D"]), self.p(out["M"]),
+                                                     self.p(out["M0"]), self.p(load)))
         out = {k: v[:n] for k, v in out.items()}
         out["load"] = load[:n]
         return out
@@ -375,7 +401,7 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
         s.ops.rebase_part(E0)
     Etot, Btot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
     # reverse all-to-all: (element slot, global edge id) to the element owners
-    routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits)) for s, (E0, _) in zip(states, per)]
+    routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits), s.elo, s.ehi) for s, (E0, _) in zip(states, per)]
     recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
     tr("route")
     for s, rv in zip(states, recvs):
@@ -410,48 +436,118 @@ def _resolve(states, comm, splits, per, nD, nN):
     return ids
 
 
+def _gather_rows(comm, ts: list) -> list:
+    """All-gather of per-rank row blocks of different lengths -> the full
+    array (rank order) on every rank."""
+    if comm.world == 1:
+        return [t.contiguous() for t in ts]
+    counts = [torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device) for t in ts]
+    cg = comm.all_gather(counts)
+    nmax = max(1, max(int(torch.stack(c).max().item()) for c in cg))
+    padded = [torch.cat([t, t.new_zeros((nmax - t.shape[0],) + tuple(t.shape[1:]))], 0) for t in ts]
+    gm = comm.all_gather(padded)
+    return [torch.cat([p[:int(n.item())] for p, n in zip(parts, c)], 0).contiguous() for parts, c in zip(gm, cg)]
+
+
+def _bisect(pairs, eid, nC):
+    """refine.cpp:39-50: boundary pair (a, b) of edge e -> (a, mid), (mid, b)"""
+    if pairs.shape[0] == 0:
+        return pairs
+    mid = (eid + nC).to(pairs.dtype)
+    return torch.stack([pairs[:, 0], mid, mid, pairs[:, 1]], 1).reshape(-1, 2).contiguous()
+
+
+def _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids):
+    """One refinement with the refined topology left to the next (sort-based)
+    edge generation: midpoints of the owned edges, all-gathered."""
+    mids = _gather_rows(comm, [s.ops.midpoints(s.coords) for s in states])
+    for s, m, i in zip(states, mids, ids):
+        kids = s.ops.children(s.elements, s.elem_edge, nC)
+        s.dirichlet, s.neumann = _bisect(s.dirichlet, i[:nD], nC), _bisect(s.neumann, i[nD:], nC)
+        s.ops.release()
+        s.coords, s.elements = torch.cat([s.coords, m], 0).contiguous(), kids
+        s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
+
+
+def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD, nN, ids):
+    """One refinement with the fine topology straight from the parent's
+    (phfem_dist_refine_level): the parent elem_edge / elements are
+    all-gathered (12 + 12 B per element), every rank builds the groups of its
+    own parent edges (fine node range [nC + E0, nC + E0 + E_r); rank 0 also
+    holds the old nodes, which start no fine edge), the fine elem_edge goes
+    to the element owners as pairs.  Returns the fine (splits, per, totals)."""
+    tr = getattr(comm, "trace", None) or (lambda w: None)
+    ee_all = _gather_rows(comm, [s.elem_edge for s in states])
+    el_all = _gather_rows(comm, [s.elements for s in states])
+    tr("gather")
+    # fine node ranges from every rank's parent edge offset
+    fsplits = np.asarray([0] + [nC + e for e in _all_E0(states, comm, per)[1:]] + [nC + Etot], dtype=np.int64)
+    counts, mids = [], []
+    for s, (E0, _), ea, la in zip(states, per, ee_all, el_all):
+        r = s.rank
+        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE)
+        counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
+        mids.append(m)
+    tr("level")
+    gath = comm.all_gather(counts)
+    fper = []
+    for s, gc in zip(states, gath):
+        allc = torch.stack(gc).cpu().numpy()
+        E0f, B0f = int(allc[:s.rank, 0].sum()), int(allc[:s.rank, 1].sum())
+        fper.append((E0f, B0f))
+        s.ops.rebase_part(E0f)
+    Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
+    fes = 4 * esplits
+    routed = [s.ops.route_pairs(E0f, s.ops.as_tensor(fes), 4 * s.elo, 4 * s.ehi) for s, (E0f, _) in zip(states, fper)]
+    recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
+    tr("route")
+    gm = _gather_rows(comm, mids)
+    for s, rv, m, i in zip(states, recvs, gm, ids):
+        kids = s.ops.children(s.elements, s.elem_edge, nC)   # parent elem_edge of the own elements
+        s.dirichlet, s.neumann = _bisect(s.dirichlet, i[:nD], nC), _bisect(s.neumann, i[nD:], nC)
+        s.coords, s.elements = torch.cat([s.coords, m], 0).contiguous(), kids
+        s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
+        s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
+    tr("refine")
+    return fsplits.astype(np.int32), fper, (Ef_tot, Bf_tot)
+
+
+def _all_E0(states, comm, per) -> list:
+    """E0 of every rank (each rank knows only its own from `per`)."""
+    ts = [torch.tensor([E0], dtype=torch.int64, device=s.coords.device) for s, (E0, _) in zip(states, per)]
+    g = comm.all_gather(ts)[0]
+    return [int(x.item()) for x in g]
+
+
 def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels: int, coeffs, f, g, uD,
-                         t: float = 0.0):
-    """[edge generation -> red refinement] x levels -> edge generation ->
+                         t: float = 0.0, sort_free: bool = True):
+    """edge generation -> [red refinement + refined topology] x levels ->
     classification -> B, D, M, M0, load = b + LN, C (CSR rows), bD; every rank
-    keeps its slices (collect() gathers them for tests)."""
+    keeps its slices (collect() gathers them for tests).  sort_free: refined
+    levels get their topology from the parent's (phfem_dist_refine_level);
+    otherwise every level repeats the occurrence exchange + sort."""
     W = comm.world
     tr = comm.trace = _Trace(states)
     # element ranges: the input split, x4 per refinement (children of [a,b) are [4a,4b))
     esplits = element_splits(nE, W)
+    splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
     for _ in range(levels):
-        splits, per, (Etot, _) = _edge_generation(states, comm, nC, nE, esplits)
         nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
         ids = _resolve(states, comm, splits, per, nD, nN)
         tr("resolve")
-        # replicated fine coordinates: old nodes + all-gathered midpoints (edge order)
-        mids = [s.ops.midpoints(s.coords) for s in states]
-        counts = [torch.tensor([m.shape[0]], dtype=torch.int64, device=m.device) for m in mids]
-        cg = comm.all_gather(counts)
-        Emax = max(1, max(int(torch.stack(c).max().item()) for c in cg))
-        padded = [torch.cat([m, m.new_zeros((Emax - m.shape[0], 2))], 0) for m in mids]
-        gm = comm.all_gather(padded)
-        for s, parts, c in zip(states, gm, cg):
-            sizes = [int(x.item()) for x in c]
-            newc = torch.cat([s.coords] + [p[:n] for p, n in zip(parts, sizes)], 0)
-            kids = s.ops.children(s.elements, s.elem_edge, nC)
-            bd_ids = ids[states.index(s)]
-            # bisect the boundary lists (refine.cpp:39-50): (a, mid), (mid, b)
-            def bisect(pairs, eid):
-                if pairs.shape[0] == 0:
-                    return pairs
-                mid = (eid + nC).to(pairs.dtype)
-                return torch.stack([pairs[:, 0], mid, mid, pairs[:, 1]], 1).reshape(-1, 2).contiguous()
-            s.dirichlet = bisect(s.dirichlet, bd_ids[:nD])
-            s.neumann = bisect(s.neumann, bd_ids[nD:])
-            s.ops.release()
-            s.coords, s.elements = newc.contiguous(), kids
-            s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
+        if sort_free:
+            splits, per, (Etot_f, Btot_f) = _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot,
+                                                              esplits, nD, nN, ids)
+        else:
+            _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids)
         nC, nE = nC + Etot, 4 * nE
         esplits = 4 * esplits
+        if sort_free:
+            Etot, Btot = Etot_f, Btot_f
+        else:
+            splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
         tr("refine")
     # final level
-    splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
     nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
     ids = _resolve(states, comm, splits, per, nD, nN)
     Ls = []
@@ -463,7 +559,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         own_n = (nl >= 0) & (nl < E_r) & (i[nD:] >= 0)
         s.neu_pos = torch.nonzero(own_n).flatten()
         s.neu_local = nl[own_n].to(torch.int32).contiguous()
-        Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local)], dtype=torch.int64,
+        Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local, E0)], dtype=torch.int64,
                                device=s.coords.device))
     tr("classify")
     gl = comm.all_gather(Ls)

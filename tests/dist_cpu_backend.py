@@ -6,6 +6,9 @@ CPU.  Per-element values come from the C oracle (oracle/), the rest is plain
 numpy following the same reference lines as the kernels:
   occurrences / dedup      edge_topology.cpp:52-115
   children / midpoints     refine.cpp:16-37
+  refined level            SURVEY §8(f1) closed form (refine.cpp:28-37 +
+                           edge_topology.cpp:59-113), the groups of the
+                           rank's own parent edges
   classification           edge_topology.cpp:145-177
   C rows                   assembly.cpp:144-168
   Dirichlet / Neumann      assembly.cpp:205-242, elliptic.cpp:54-55
@@ -124,6 +127,67 @@ class NumpyRankOps:
         self.pairs = pairs
         return E, int((~two).sum())
 
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all):
+        """Groups of the own parent edges e: the two halves (the one at the
+        smaller old node first), then the interior edges mu(e') - mu(e) for the
+        partners e' < e of e's elements, ascending e'."""
+        p = self.part
+        ee = ee_all.numpy().reshape(-1, 3).astype(np.int64)
+        ee = np.where(ee >= 0, ee, ~ee)
+        c = coords.numpy()
+        E = len(p.ltp)
+        rows, isb = [], []
+        nes = np.zeros(nhi - nlo + 1, np.int32)
+        mids = np.zeros((E, 2))
+        for le in range(E):
+            e = E0p + le
+            a, b = (int(x) for x in p.edge_nodes[le])
+            tp, tm = (int(x) for x in p.edge_elements[le])
+            l = int(p.ltp[le])
+            l2 = int(p.ltm[le]) if tm >= 0 else 0
+            mu = nc + e
+            nes[mu - nlo] = len(rows)
+            mids[le] = [0.5 * (c[a][0] + c[b][0]), 0.5 * (c[a][1] + c[b][1])]
+            j1, j2, k1, k2 = (l + 1) % 3, (l + 2) % 3, (l2 + 1) % 3, (l2 + 2) % 3
+            h1 = (a, mu, 4 * tp + 1 + j1, 2, 4 * tm + 1 + k2 if tm >= 0 else -1, 1 if tm >= 0 else -1)
+            h2 = (mu, b, 4 * tp + 1 + j2, 1, 4 * tm + 1 + k1 if tm >= 0 else -1, 2 if tm >= 0 else -1)
+            halves = [h1, h2] if a < b else [h2, h1]
+            cand = []
+            q0, q1 = int(ee[tp][j1]), int(ee[tp][j2])
+            if q0 < e:
+                cand.append((q0, (mu, nc + q0, 4 * tp, j2, 4 * tp + 1 + j2, 0)))
+            if q1 < e:
+                cand.append((q1, (nc + q1, mu, 4 * tp, j1, 4 * tp + 1 + j1, 0)))
+            if tm >= 0:
+                r0, r1 = int(ee[tm][k1]), int(ee[tm][k2])
+                if r0 < e:
+                    cand.append((r0, (mu, nc + r0, 4 * tm, k2, 4 * tm + 1 + k2, 0)))
+                if r1 < e:
+                    cand.append((r1, (nc + r1, mu, 4 * tm, k1, 4 * tm + 1 + k1, 0)))
+            group = halves + [x for _, x in sorted(cand)]
+            rows += group
+            isb += [tm < 0, tm < 0] + [False] * (len(group) - 2)
+        if E:
+            nes[nhi - nlo] = len(rows)
+        r = np.asarray(rows, np.int64).reshape(-1, 6)
+        Ef = len(r)
+        q = _Part()
+        q.edge_nodes = r[:, 0:2].astype(np.int32)
+        q.edge_elements = r[:, [2, 4]].astype(np.int32)
+        q.ltp = r[:, 3].astype(np.int32)
+        q.ltm = r[:, 5].astype(np.int32)
+        ids = np.arange(Ef)
+        b = np.asarray(isb, bool)
+        q.interior, q.boundary = ids[~b].astype(np.int32), ids[b].astype(np.int32)
+        q.nes, q.nlo = nes, nlo
+        self.part = q
+        pairs = np.full((2 * Ef, 2), -1, np.int32)
+        pairs[0::2, 0], pairs[0::2, 1] = 3 * r[:, 2] + r[:, 3], ids
+        pairs[1::2, 0] = np.where(r[:, 4] >= 0, 3 * r[:, 4] + r[:, 5], -1)
+        pairs[1::2, 1] = ~ids
+        self.pairs = pairs
+        return Ef, int(b.sum()), torch.as_tensor(mids)
+
     def num_edges(self):
         return len(self.part.ltp)
 
@@ -134,7 +198,7 @@ class NumpyRankOps:
         p.nes = p.nes + E0
         p.E0 = E0
 
-    def route_pairs(self, E0, esplits):
+    def route_pairs(self, E0, esplits, elo=0, ehi=0):
         pr = self.pairs
         pr = pr[pr[:, 0] >= 0].astype(np.int64)
         v = np.where(pr[:, 1] >= 0, pr[:, 1] + E0, ~(~pr[:, 1] + E0))
@@ -192,7 +256,7 @@ class NumpyRankOps:
         return torch.as_tensor(kids.reshape(-1, 3).astype(np.int32))
 
     # -- classification / C / vectors -----------------------------------------------------------------
-    def classify(self, dir_local, neu_local):
+    def classify(self, dir_local, neu_local, E0=0):
         E = self.num_edges()
         neu = np.zeros(E, bool)
         neu[neu_local.numpy()] = True

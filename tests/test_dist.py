@@ -23,7 +23,9 @@ CASES = [("crisscross-L1", lambda: O.refine_levels(G.crisscross_square(), 1), 1)
          ("lshape-L2", lambda: O.refine_levels(G.lshape_6tri(), 2), 1),
          ("lshape-L3-nolevel", lambda: O.refine_levels(G.lshape_6tri(), 3), 0),
          ("stress-L3", lambda: O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 3), 3)), 1),
-         ("fan-30", lambda: G.fan(30, True), 1)]
+         ("fan-30", lambda: G.fan(30, True), 1),
+         ("crisscross-L1-2levels", lambda: O.refine_levels(G.crisscross_square(), 1), 2),
+         ("lshape-L1-3levels", lambda: O.refine_levels(G.lshape_6tri(), 1), 3)]
 
 
 def check_equal(d, ref):
@@ -46,16 +48,19 @@ def check_equal(d, ref):
 @pytest.mark.gpu
 @pytest.mark.parametrize("W", [1, 2, 3, 4])
 @pytest.mark.parametrize("name,make,levels", CASES, ids=[c[0] for c in CASES])
-def test_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels):
+@pytest.mark.parametrize("sort_free", [True, False], ids=["sortfree", "sorted"])
+def test_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels, sort_free):
     import torch
     from paper_2401_15557_b200 import capi, dist
+    if not sort_free and (levels > 1 or W == 3):
+        pytest.skip("sorted-level path: covered by the other cases")
     hm = make()
     args = G.config_fields(2)
     ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args, flags=capi.PIPE_GENERIC_EG).download()
     tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
     comm = dist.LocalComm(W)
     states = dist.make_states(hm, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
-    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *args)
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *args, sort_free=sort_free)
     check_equal(dist.collect(states), ref)
 
 
@@ -87,7 +92,8 @@ def _gloo_worker(rank, world, port, tmp, case, levels):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,levels", [("square-L3", 1), ("lshape-L2", 1), ("stress-L3", 0)])
+@pytest.mark.parametrize("case,levels", [("square-L3", 1), ("lshape-L2", 1), ("stress-L3", 0),
+                                         ("crisscross-L1-2levels", 2), ("lshape-L1-3levels", 3)])
 def test_gloo_two_ranks_equal_oracle(tmp_path, case, levels):
     """2 gloo processes on CPU: the concatenated rank slices == the C oracle
     run on the whole mesh (topology, maps, classification, C, bD, blocks,
