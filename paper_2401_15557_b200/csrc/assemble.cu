@@ -169,112 +169,97 @@ VolArgs make_vol_args(const phfem_mesh* mesh) {
 }
 
 // ---------------------------------------------------------------------------
-// C in CSR: one CTA per 1024 consecutive edges, 4 edges per thread (vector
-// loads of the SoA edge arrays, 8 independent coordinate gathers in flight).
-// Row pointers come from the per-block boundary / Neumann prefixes of
-// classify_edges plus an in-block scan (a retained boundary row holds 2
-// entries, an interior row 4).  The block's (col, value) range is contiguous
-// in the output, so it is staged in SMEM and written with coalesced stores.
-constexpr int kCsrEdges = 1024;
-constexpr int kCsrThreads = 256;
+// C in CSR (assembly.cpp:144-168).  Row pointers come from the per-block
+// boundary / Neumann prefixes of classify_edges (a retained boundary row
+// holds 2 entries, an interior row 4).
+constexpr int kCsrEdges = 1024;  // the classification's prefix block
 
-__global__ void __launch_bounds__(kCsrThreads) k_constraint_csr(
+// Warp-staged: a CTA of 8 warps owns the 1024-edge block of the
+// classification's prefixes, each warp 4 chunks of 32 consecutive edges
+// (coalesced 4-byte loads per chunk).  Row starts k = 4 rp - 2 (retained
+// boundary rows before) from the block prefixes + ballot counts.  A chunk's
+// entries are contiguous: they go out as "pairs" — (3t + c0, 3t + c1) with
+// one value, the T+ pair then the T- pair of a row — staged per warp as
+// 16-byte records (<= 2-way SMEM conflicts) and stored as int2 / double2 by
+// consecutive lanes (the previous layout staged 4 entries per thread at
+// stride 4, a 16- to 32-way bank conflict on every staging store).
+constexpr int kCsr2Warps = 8;
+struct CsrPair {
+  int2 col;
+  double val;
+};
+
+__global__ void __launch_bounds__(32 * kCsr2Warps) k_constraint_csr2(
     const double2* __restrict__ coords, const int32_t* __restrict__ edge_nodes,
     const int32_t* __restrict__ edge_elements, const int32_t* __restrict__ ltp,
     const int32_t* __restrict__ ltm, const int32_t* __restrict__ rpos,
     const int32_t* __restrict__ pre_bnd, const int32_t* __restrict__ pre_neu, int E, int L,
     int32_t* __restrict__ row_ptr, int32_t* __restrict__ col, double* __restrict__ val) {
-  __shared__ int32_t sm[33];
-  extern __shared__ __align__(16) unsigned char csr_smem[];
-  double* sval = reinterpret_cast<double*>(csr_smem);              // [4 * kCsrEdges]
-  int32_t* scol = reinterpret_cast<int32_t*>(sval + 4 * kCsrEdges);  // [4 * kCsrEdges]
+  __shared__ CsrPair stage[kCsr2Warps][64];
+  __shared__ int32_t wcnt[kCsr2Warps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x;
-  const int64_t e0 = (int64_t)blk * kCsrEdges + 4 * threadIdx.x;
-  int rp[4], tp[4], tm[4], lp[4], lm[4], a[4], b[4];
-  if (e0 + 3 < E) {
-    const int4 r4 = *reinterpret_cast<const int4*>(rpos + e0);
-    const int4 el0 = *reinterpret_cast<const int4*>(edge_elements + 2 * e0);
-    const int4 el1 = *reinterpret_cast<const int4*>(edge_elements + 2 * e0 + 4);
-    const int4 en0 = *reinterpret_cast<const int4*>(edge_nodes + 2 * e0);
-    const int4 en1 = *reinterpret_cast<const int4*>(edge_nodes + 2 * e0 + 4);
-    const int4 p4 = *reinterpret_cast<const int4*>(ltp + e0);
-    const int4 m4 = *reinterpret_cast<const int4*>(ltm + e0);
-    rp[0] = r4.x; rp[1] = r4.y; rp[2] = r4.z; rp[3] = r4.w;
-    tp[0] = el0.x; tm[0] = el0.y; tp[1] = el0.z; tm[1] = el0.w;
-    tp[2] = el1.x; tm[2] = el1.y; tp[3] = el1.z; tm[3] = el1.w;
-    a[0] = en0.x; b[0] = en0.y; a[1] = en0.z; b[1] = en0.w;
-    a[2] = en1.x; b[2] = en1.y; a[3] = en1.z; b[3] = en1.w;
-    lp[0] = p4.x; lp[1] = p4.y; lp[2] = p4.z; lp[3] = p4.w;
-    lm[0] = m4.x; lm[1] = m4.y; lm[2] = m4.z; lm[3] = m4.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t e = e0 + q;
-      const bool ok = e < E;
-      rp[q] = ok ? rpos[e] : -1;
-      tp[q] = ok ? edge_elements[2 * e] : 0;
-      tm[q] = ok ? edge_elements[2 * e + 1] : -1;
-      a[q] = ok ? edge_nodes[2 * e] : 0;
-      b[q] = ok ? edge_nodes[2 * e + 1] : 0;
-      lp[q] = ok ? ltp[e] : 0;
-      lm[q] = ok ? ltm[e] : 0;
-    }
-  }
+  const int64_t eb = (int64_t)blk * kCsrEdges + warp * 128;
+  int rp[4], tp[4], tm[4], lp[4], lm[4];
   double len[4];
+  unsigned rbm[4];
+  int c_before[4];
+  int own = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    len[q] = 0.0;
-    if (rp[q] >= 0) {
-      const double2 pa = __ldg(coords + a[q]), pb = __ldg(coords + b[q]);
+  for (int j = 0; j < 4; ++j) {
+    const int64_t e = eb + 32 * j + lane;
+    const bool ok = e < E;
+    rp[j] = ok ? __ldg(rpos + e) : -1;
+    const int2 el = ok ? reinterpret_cast<const int2*>(edge_elements)[e] : make_int2(0, -1);
+    tp[j] = el.x;
+    tm[j] = el.y;
+    lp[j] = ok ? __ldg(ltp + e) : 0;
+    lm[j] = ok ? __ldg(ltm + e) : 0;
+    len[j] = 0.0;
+    if (rp[j] >= 0) {
+      const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+      const double2 pa = __ldg(coords + ab.x), pb = __ldg(coords + ab.y);
       const double dx = pb.x - pa.x, dy = pb.y - pa.y;
-      len[q] = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+      len[j] = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
     }
+    rbm[j] = __ballot_sync(0xffffffffu, rp[j] >= 0 && tm[j] < 0);
+    c_before[j] = own;
+    own += __popc(rbm[j]);
   }
-  int rb = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) rb += (rp[q] >= 0 && tm[q] < 0);
-  int tot;
-  int bret = block_exclusive_scan(rb, sm, &tot) + pre_bnd[blk] - pre_neu[blk];
-  const int64_t eb = (int64_t)blk * kCsrEdges;
-  const int R0 = (int)eb - pre_neu[blk];                  // retained rows before the block
-  const int k_first = 4 * R0 - 2 * (pre_bnd[blk] - pre_neu[blk]);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (rp[q] < 0) continue;
-    const int k = 4 * rp[q] - 2 * bret;
-    row_ptr[rp[q]] = k;
-    int loc = k - k_first;
-    const double vp = len[q] * 0.5;   // lengths[e] * kR[led][c]    (assembly.cpp:160)
-    const double vm = -len[q] * 0.5;  // -lengths[e] * kR[ledtn][c] (assembly.cpp:164)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      if (c != lp[q]) {
-        scol[loc] = 3 * tp[q] + c;
-        sval[loc] = vp;
-        ++loc;
-      }
-    if (tm[q] >= 0) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        if (c != lm[q]) {
-          scol[loc] = 3 * tm[q] + c;
-          sval[loc] = vm;
-          ++loc;
-        }
-    } else {
-      ++bret;
-    }
-    if (rp[q] == L - 1) row_ptr[L] = k_first + loc;
-  }
+  if (lane == 0) wcnt[warp] = own;
   __syncthreads();
-  // block's entries: retained rows R0 .. R0 + nret - 1
-  const int nblock = (int)((int64_t)E - eb < kCsrEdges ? (int64_t)E - eb : kCsrEdges);
-  const int nret = nblock - (pre_neu[blk + 1] - pre_neu[blk]);
-  const int nbret = tot;
-  const int count = 4 * nret - 2 * nbret;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) {
-    col[k_first + i] = scol[i];
-    __stcs(val + k_first + i, sval[i]);
+  int wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += wcnt[w];
+  const int base_b = pre_bnd[blk] - pre_neu[blk] + wpre;  // retained boundary rows before the warp
+  CsrPair* st = stage[warp];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int bret = base_b + c_before[j] + __popc(rbm[j] & lanemask_lt());
+    const bool ret = rp[j] >= 0;
+    const int k = 4 * rp[j] - 2 * bret;
+    const int kmin = __reduce_min_sync(0xffffffffu, ret ? k : 0x7fffffff);
+    if (kmin == 0x7fffffff) continue;  // no retained edge in the chunk
+    const int n = ret ? (tm[j] >= 0 ? 4 : 2) : 0;
+    if (ret) {
+      row_ptr[rp[j]] = k;
+      if (rp[j] == L - 1) row_ptr[L] = k + n;
+      const int q = (k - kmin) >> 1;
+      const int c0 = lp[j] == 0 ? 1 : 0, c1 = lp[j] == 2 ? 1 : 2;
+      st[q] = CsrPair{make_int2(3 * tp[j] + c0, 3 * tp[j] + c1), len[j] * 0.5};  // assembly.cpp:160
+      if (tm[j] >= 0) {
+        const int d0 = lm[j] == 0 ? 1 : 0, d1 = lm[j] == 2 ? 1 : 2;
+        st[q + 1] = CsrPair{make_int2(3 * tm[j] + d0, 3 * tm[j] + d1), -len[j] * 0.5};  // :164
+      }
+    }
+    const int kend = __reduce_max_sync(0xffffffffu, ret ? k + n : 0);
+    const int npairs = (kend - kmin) >> 1;
+    __syncwarp();
+    for (int p = lane; p < npairs; p += 32) {
+      const CsrPair r = st[p];
+      *reinterpret_cast<int2*>(col + kmin + 2 * p) = r.col;
+      __stcs(reinterpret_cast<double2*>(val + kmin + 2 * p), make_double2(r.val, r.val));
+    }
+    __syncwarp();
   }
 }
 
@@ -546,13 +531,8 @@ phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
     PHFEM_CUDA(ctx, cudaMemsetAsync(out->row_ptr, 0, sizeof(int32_t), ctx->stream));
     return PHFEM_OK;
   }
-  const int smem = 4 * kCsrEdges * (int)(sizeof(double) + sizeof(int32_t));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_constraint_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  PHFEM_LAUNCH(ctx, "k_constraint_csr", k_constraint_csr<<<nblk, kCsrThreads, smem, ctx->stream>>>(
+  // col / val pairs need 8 / 16-byte alignment: true for pool allocations
+  PHFEM_LAUNCH(ctx, "k_constraint_csr", k_constraint_csr2<<<nblk, 32 * kCsr2Warps, 0, ctx->stream>>>(
       (const double2*)mesh->coords, topo->edge_nodes, topo->edge_elements, topo->local_in_tplus,
       topo->local_in_tminus, cls->retained_pos, cls->block_prefix, cls->block_prefix + nblk + 1, E,
       L, out->row_ptr, out->col_idx, out->values));
