@@ -440,16 +440,56 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
 
+    if rank == 0 and world == 1 and not args.no_given:
+        dm.release()
+        dm = None
+        line["config5_given_mesh"] = run_given(ctx, args, fields)
     if rank == 0 and world == 1 and not args.no_cn:
         line["cn_rhs"] = run_cn_rhs(ctx, args)
     if rank == 0 and world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(ctx, args, fields)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_single(args.cpu_level)
-    dm.release()
+    if dm is not None:
+        dm.release()
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_given(ctx, args, fields):
+    """SURVEY §8(d)'s reading of config 5: the L13 mesh GIVEN (no parent, so
+    the sort-based edge generation) -> classification -> C -> blocks / load /
+    bD; same metric, compulsory bytes eg_bytes + as_bytes (72.3 GB @ L13)."""
+    import torch
+    from paper_2401_15557_b200 import capi
+    dm = build_input(ctx, args.level)
+    r = capi.pipeline(ctx, dm, 0, *fields)
+    o = r.out
+    s = {"nC": o.mesh.nC, "nE": o.mesh.nE, "E": o.topo.E, "L": o.cls.L, "nnz": o.C.nnz}
+    r.release()
+    for _ in range(max(1, args.warmup - 1)):
+        capi.pipeline(ctx, dm, 0, *fields).release()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.sync()
+    steps = max(3, args.steps)
+    e0.record(stream)
+    for _ in range(steps):
+        capi.pipeline(ctx, dm, 0, *fields).release()
+    e1.record(stream)
+    ctx.sync()
+    ms = e0.elapsed_time(e1) / steps
+    dm.release()
+    compulsory = eg_bytes(s["nE"], s["E"]) + as_bytes(s["nC"], s["nE"], s["E"], s["L"], s["nnz"])
+    peak, kind = peaks()
+    gbs = compulsory / (ms * 1e-3) / 1e9
+    return {"workload": f"config5 as SURVEY 8(d) reads it: square L{args.level} mesh given "
+                        f"({s['nE']} triangles): EG (sort-based: no parent) + classification + C + "
+                        "B/D/M/M0/load/bD, config-2 coefficients",
+            "ms_per_step": round(ms, 3), "value": s["nE"] / (ms * 1e-3), "unit": "triangles/s", "steps": steps,
+            "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
+                                  "peak": peak, "peak_kind": kind, "frac": round(gbs / peak, 4)}}
 
 
 def run_cn_rhs(ctx, args):
@@ -598,6 +638,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cn", action="store_true", help="skip the config-3 CN right-hand-side line")
+    ap.add_argument("--no-given", action="store_true", help="skip the given-L13-mesh (EG + AS) line")
     ap.add_argument("--cn-level", type=int, default=11)
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--sharded", action="store_true",
