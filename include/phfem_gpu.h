@@ -492,12 +492,18 @@ phfem_status phfem_topology_csv_file(phfem_ctx* ctx, const phfem_mesh* mesh,
  * [node_lo, node_hi) with node_hi = nc + E0p + E; local fine ids (re-base as
  * for phfem_dist_dedup); *pairs_out (ctx memory, 2 x out->E int2, free with
  * phfem_free) = (fine slot, f / ~f) per fine edge for
- * phfem_dist_route_pairs; mids (nullable, [E][2]) = the rank's midpoints.   */
+ * phfem_dist_route_pairs; mids (nullable, [E][2]) = the rank's midpoints.
+ * C (nullable): also the rank's rows of the fine C in CSR (local rows and
+ * row pointers, global columns; re-base by the rank's row / nnz offsets),
+ * fused as on one GPU, from the parent Neumann edges neu_parent_ids (global
+ * ids, all ranks' list).                                                   */
 phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
                                      const int32_t* elem_edge_all, const int32_t* elements_all,
                                      int32_t nE_all, const double* coords, int32_t nc,
-                                     int32_t node_lo, int32_t node_hi, phfem_topology* out,
-                                     int32_t** pairs_out, double* mids);
+                                     int32_t node_lo, int32_t node_hi,
+                                     const int32_t* neu_parent_ids, int32_t nN_parent,
+                                     phfem_topology* out, int32_t** pairs_out, double* mids,
+                                     phfem_csr* C);
 
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'

@@ -288,7 +288,7 @@ def load_library(path: str = LIB_PATH):
         "phfem_assemble_volume_load": (C.c_int, [vp, P(phfem_mesh), P(phfem_coeffs), P(phfem_field), dbl,
                                                  vp, vp, vp, vp, vp]),
         "phfem_dist_refine_level": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, vp, i32, i32, i32,
-                                              P(phfem_topology), P(vp), vp]),
+                                              vp, i32, P(phfem_topology), P(vp), vp, P(phfem_csr)]),
         "phfem_mesh_save_dir": (C.c_int, [vp, P(phfem_mesh), C.c_char_p]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),

@@ -133,9 +133,9 @@ __global__ void k_rl_tile_init(int E, int eb, int ntiles, const int32_t* __restr
       return l;
     };
     tileB[t] = lower(e1) - lower(e0);
-    if (neu_bits) {
+    if (neu_bits) {  // bitmap over the local edge index
       int c = 0;
-      for (int64_t w = e0 >> 5; w < (e1 + 31) >> 5; ++w) c += __popc(__ldg(neu_bits + w));
+      for (int64_t w = l0 >> 5; w < (l1 + 31) >> 5; ++w) c += __popc(__ldg(neu_bits + w));
       tileN[t] = c;
     }
   }
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
     ab = reinterpret_cast<const int2*>(a.edge_nodes)[le];
     el = reinterpret_cast<const int2*>(a.edge_elements)[le];
     l = __ldg(a.ltp + le);
-    if (kFull) neu = (__ldg(a.neu_bits + (e >> 5)) >> (e & 31)) & 1u;
+    if (kFull) neu = (__ldg(a.neu_bits + (le >> 5)) >> (le & 31)) & 1u;
   }
   const bool has_m = valid && el.y >= 0;
   if (has_m) l2 = __ldg(a.ltm + le);
@@ -312,12 +312,12 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
     }
     if (kFull) {
       const int rr = s.rr[i];
-      o.rpos[f] = rr < 0 ? -1 : off_rp + (rr >> 16);
+      if (o.rpos) o.rpos[f] = rr < 0 ? -1 : off_rp + (rr >> 16);
       if (rr >= 0) {
         const int rp = off_rp + (rr >> 16);
         const int rs = off_rs + (rr & 0xffff);
         const double len = s.len[i];
-        o.redges[rp] = f;
+        if (o.redges) o.redges[rp] = f;
         o.row_ptr[rp] = rs;
         // columns {0,1,2} \ {local}, ascending: T+ DOFs, then T- DOFs
         const int c0 = lp == 0 ? 1 : 0, c1 = lp == 2 ? 1 : 2;
@@ -518,35 +518,59 @@ PHFEM_API phfem_status phfem_refine_level(phfem_ctx* ctx, const phfem_mesh* pare
 // order (local ids); the fine elem_edge entries leave as (slot, f / ~f) pairs
 // for the element owners (phfem_dist_route_pairs).  node range [node_lo,
 // node_hi) must end at nc + E0p + E (the rank's last midpoint node).
+// parent Neumann ids (global) -> bitmap over the rank's local parent edges
+__global__ void k_rl_neu_bits(const int32_t* __restrict__ ids, int n, int E0, int E, uint32_t* __restrict__ bits) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int e = ids[i] - E0;
+    if (e >= 0 && e < E) atomicOr(&bits[e >> 5], 1u << (e & 31));
+  }
+}
+
 PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
                                                const int32_t* elem_edge_all, const int32_t* elements_all,
                                                int32_t nE_all, const double* coords, int32_t nc,
-                                               int32_t node_lo, int32_t node_hi, phfem_topology* out,
-                                               int32_t** pairs_out, double* mids) {
+                                               int32_t node_lo, int32_t node_hi,
+                                               const int32_t* neu_parent_ids, int32_t nN_parent,
+                                               phfem_topology* out, int32_t** pairs_out, double* mids,
+                                               phfem_csr* C) {
   if (!ctx || !ppart || !out || !pairs_out) return PHFEM_ERR_INVALID_ARGUMENT;
   memset(out, 0, sizeof(*out));
+  if (C) memset(C, 0, sizeof(*C));
   *pairs_out = nullptr;
+  if (nN_parent > 0 && !neu_parent_ids) return PHFEM_ERR_INVALID_ARGUMENT;
   const int64_t E = ppart->E;
   if ((E > 0 && (!elem_edge_all || !elements_all || !coords)) || E0p < 0 || node_lo < 0 ||
       node_hi < node_lo || (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) ||
       (E > 0 && node_lo > nc + E0p) || 4 * (int64_t)nE_all >= (int64_t(1) << 31))
     return PHFEM_ERR_INVALID_ARGUMENT;
   const int64_t ntiles = std::max<int64_t>(1, (E + kLvT - 1) / kLvT);
+  const int64_t nwords = std::max<int64_t>(1, (E + 31) / 32);
   int32_t* tiles = nullptr;
-  PHFEM_TRY(dalloc(ctx, &tiles, 2 * (ntiles + 1) + 1));
-  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *total = tiles + 2 * (ntiles + 1);
-  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (2 * (ntiles + 1) + 1), ctx->stream));
+  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1) + 2));
+  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
+  int32_t* total = tiles + 3 * (ntiles + 1);  // [0] fine edges, [1] parent Neumann edges
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 2), ctx->stream));
+  uint32_t* nbits = nullptr;
+  if (C) {  // the fused variant: classification bits of the owned parent edges
+    PHFEM_TRY(dalloc(ctx, &nbits, nwords));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(nbits, 0, sizeof(uint32_t) * nwords, ctx->stream));
+    if (nN_parent > 0 && E > 0)
+      PHFEM_LAUNCH(ctx, "k_rl_neu_bits", k_rl_neu_bits<<<grid_for(nN_parent, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+          neu_parent_ids, nN_parent, E0p, (int)E, nbits));
+  }
   if (E > 0) {
     PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, nullptr, tileF, tileB, nullptr));
+        (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, nbits, tileF, tileB, tileN));
     PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count<<<grid_for(nE_all, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         elem_edge_all, nE_all, E0p, (int)E, tileF));
   }
   PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
-  int32_t Ef = 0;
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(&Ef, total, sizeof Ef, cudaMemcpyDeviceToHost, ctx->stream));
+  if (C) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, total + 1));
+  int32_t hcnt[2] = {0, 0};
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(hcnt, total, sizeof hcnt, cudaMemcpyDeviceToHost, ctx->stream));
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int32_t Ef = hcnt[0];
   const int64_t nBf = 2 * (int64_t)ppart->n_boundary;
   out->nC = node_hi - node_lo;
   out->nE = 4 * nE_all;
@@ -564,6 +588,19 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
   PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * ((int64_t)out->nC + 1), ctx->stream));
   int32_t* pairs = nullptr;
   PHFEM_TRY(dalloc(ctx, &pairs, 4 * cap));
+  int64_t Lr = 0;
+  if (C) {  // rows: fine edges minus the halves of Neumann parent edges (refine_level_impl)
+    const int64_t nneu = hcnt[1];
+    Lr = Ef - 2 * nneu;
+    const int64_t BR = 2 * ((int64_t)ppart->n_boundary - nneu);
+    C->rows = (int32_t)Lr;
+    C->cols = 3 * 4 * nE_all;
+    C->nnz = 4 * Lr - 2 * BR;
+    PHFEM_TRY(dalloc(ctx, &C->row_ptr, Lr + 1));
+    PHFEM_TRY(dalloc(ctx, &C->col_idx, std::max<int64_t>(C->nnz, 1)));
+    PHFEM_TRY(dalloc(ctx, &C->values, std::max<int64_t>(C->nnz, 1)));
+    if (Lr == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
+  }
   if (E > 0) {
     LvArgs a;
     memset(&a, 0, sizeof a);
@@ -593,8 +630,20 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
     o.mid = (double2*)mids;
     o.mid_base = (int64_t)nc + E0p;
     o.pairs = reinterpret_cast<int2*>(pairs);
-    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)((E + kLvT - 1) / kLvT), kLvT, 0, ctx->stream>>>(a, o));
+    const unsigned nt = (unsigned)((E + kLvT - 1) / kLvT);
+    if (C) {
+      a.neu_bits = nbits;
+      a.tileN = tileN;
+      a.L = (int)Lr;
+      o.row_ptr = C->row_ptr;
+      o.col = C->col_idx;
+      o.val = C->values;
+      PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<nt, kLvT, 0, ctx->stream>>>(a, o));
+    } else {
+      PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<nt, kLvT, 0, ctx->stream>>>(a, o));
+    }
   }
+  dfree(ctx, nbits);
   dfree(ctx, tiles);
   *pairs_out = pairs;
   return PHFEM_OK;

@@ -193,17 +193,24 @@ class CudaRankOps:
         self._pairs = (pairs.data_ptr(), 2 * int(t.E), False)
         return int(t.E), int(t.n_boundary)
 
-    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all):
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None):
         """The rank's part of the refined topology from its parent part (sort
-        free, phfem_dist_refine_level); returns (E, n_boundary, midpoints)."""
+        free, phfem_dist_refine_level); returns (E, n_boundary, midpoints).
+        neu_parent (global parent Neumann ids): also the rank's C rows, fused."""
         t = capi.phfem_topology()
         pairs = C.c_void_p()
         pt = self.part.t
         Ep = int(pt.E)  # (the parent part is released below)
         mids = self.empty((max(Ep, 1), 2), torch.float64)
+        csr = capi.phfem_csr() if neu_parent is not None else None
+        nN = 0 if neu_parent is None else int(neu_parent.numel())
         self._ck(self.lib.phfem_dist_refine_level(self.ctx.ptr, C.byref(pt), E0p, self.p(ee_all), self.p(el_all),
-                                                  nE_all, self.p(coords), nc, nlo, nhi, C.byref(t), C.byref(pairs),
-                                                  self.p(mids)))
+                                                  nE_all, self.p(coords), nc, nlo, nhi,
+                                                  self.p(neu_parent) if nN else None, nN, C.byref(t),
+                                                  C.byref(pairs), self.p(mids),
+                                                  C.byref(csr) if csr is not None else None))
+        if csr is not None:
+            self.csr = csr
         self.part.release()
         self.part = capi.Topology(self.ctx, t)
         self._pairs = (pairs.value, 2 * int(t.E), True)
@@ -276,6 +283,8 @@ class CudaRankOps:
         return int(c.L)
 
     def constraint(self, mview):
+        if getattr(self, "csr", None) is not None:  # fused into the refined level
+            return self.csr
         m = capi.phfem_csr()
         mv = capi.phfem_mesh()
         C.memmove(C.byref(mv), C.byref(mview), C.sizeof(mv))
@@ -469,7 +478,7 @@ def _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids):
         s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
 
 
-def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD, nN, ids):
+def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD, nN, ids, fused_c=False):
     """One refinement with the fine topology straight from the parent's
     (phfem_dist_refine_level): the parent elem_edge / elements are
     all-gathered (12 + 12 B per element), every rank builds the groups of its
@@ -483,9 +492,10 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     # fine node ranges from every rank's parent edge offset
     fsplits = np.asarray([0] + [nC + e for e in _all_E0(states, comm, per)[1:]] + [nC + Etot], dtype=np.int64)
     counts, mids = [], []
-    for s, (E0, _), ea, la in zip(states, per, ee_all, el_all):
+    for s, (E0, _), ea, la, i in zip(states, per, ee_all, el_all, ids):
         r = s.rank
-        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE)
+        neu = i[nD:].to(torch.int32).contiguous() if fused_c else None
+        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, neu)
         counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
         mids.append(m)
     tr("level")
@@ -531,13 +541,14 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     # element ranges: the input split, x4 per refinement (children of [a,b) are [4a,4b))
     esplits = element_splits(nE, W)
     splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
-    for _ in range(levels):
+    for lvl in range(levels):
         nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
         ids = _resolve(states, comm, splits, per, nD, nN)
         tr("resolve")
         if sort_free:
+            # the last level also produces C's rows (fused, from the parent Neumann edges)
             splits, per, (Etot_f, Btot_f) = _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot,
-                                                              esplits, nD, nN, ids)
+                                                              esplits, nD, nN, ids, fused_c=lvl == levels - 1)
         else:
             _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids)
         nC, nE = nC + Etot, 4 * nE

@@ -127,7 +127,7 @@ class NumpyRankOps:
         self.pairs = pairs
         return E, int((~two).sum())
 
-    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all):
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None):
         """Groups of the own parent edges e: the two halves (the one at the
         smaller old node first), then the interior edges mu(e') - mu(e) for the
         partners e' < e of e's elements, ascending e'."""
