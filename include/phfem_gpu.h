@@ -484,6 +484,13 @@ phfem_status phfem_topology_csv(phfem_ctx* ctx, const phfem_mesh* mesh, const ph
                                 char** out, size_t* len);
 phfem_status phfem_topology_csv_file(phfem_ctx* ctx, const phfem_mesh* mesh,
                                      const phfem_topology* topo, const char* path);
+/* printf("%.<precision>g") of n device doubles on the device (the formatter
+ * behind the two calls above; precision 1..17): out = n 32-byte slots,
+ * lens = bytes used per slot.  Test entry point.                           */
+phfem_status phfem_format_g(phfem_ctx* ctx, const double* vals, int64_t n, int precision,
+                            char* out, int32_t* lens);
+/* the same formatter on the host (out >= 32 bytes): returns the length.     */
+int phfem_format_g_host(double v, int precision, char* out);
 
 /* Distributed refined level (§8(e) with SURVEY f1): the rank's part of the
  * fine topology straight from its parent part `ppart` (parent edges

@@ -173,7 +173,7 @@ EXPORTED = [
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
     "phfem_mesh_load_text", "phfem_mesh_load_dir", "phfem_mesh_format", "phfem_mesh_save_dir",
     "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free", "phfem_dist_refine_level",
-    "phfem_assemble_volume_load",
+    "phfem_assemble_volume_load", "phfem_format_g", "phfem_format_g_host",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -285,6 +285,8 @@ def load_library(path: str = LIB_PATH):
         "phfem_mesh_load_dir": (C.c_int, [vp, C.c_char_p, P(phfem_mesh)]),
         "phfem_mesh_format": (C.c_int, [vp, P(phfem_mesh), C.c_int, P(vp), P(C.c_size_t)]),
         "phfem_text_free": (None, [vp]),
+        "phfem_format_g": (C.c_int, [vp, vp, i64, C.c_int, vp, vp]),
+        "phfem_format_g_host": (C.c_int, [dbl, C.c_int, C.c_char_p]),
         "phfem_assemble_volume_load": (C.c_int, [vp, P(phfem_mesh), P(phfem_coeffs), P(phfem_field), dbl,
                                                  vp, vp, vp, vp, vp]),
         "phfem_dist_refine_level": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, vp, i32, i32, i32,

@@ -12,16 +12,21 @@
 // strtol semantics incl. sign and 64-bit overflow), the signed-area check of
 // each element fused into the same pass, and the boundary-pair normalisation
 // against the element cycles as one streaming pass over the elements with a
-// small hash set of the pairs.  The element file is also FORMATTED on the
-// device (lengths, 64-bit scan, digits).  Floating-point text needs exact
-// decimal <-> binary conversion: it runs on host threads through
-// std::from_chars / std::to_chars (correctly rounded; to_chars(general, 17) is
-// specified as printf("%.17g")); any token outside the plain decimal grammar
-// or whose value is not a normal number goes through std::stod itself, so
-// hex floats, inf/nan and ERANGE behave exactly as in the reference.  The first
+// small hash set of the pairs.  All output text is FORMATTED on the device
+// (line lengths, 64-bit scan, bytes, one copy back): ids, and the
+// coordinates / CSV lengths through fmt.cuh's exact "%.<P>g" (128-bit
+// scaling, big-integer fallback; byte-identical to glibc's printf).  Parsing
+// floating-point text (exact decimal -> binary) runs on host threads through
+// std::from_chars (correctly rounded like strtod); any token outside the plain
+// decimal grammar or whose value is not a normal number goes through
+// std::stod itself, so hex floats, inf/nan and ERANGE behave exactly as in
+// the reference.  The first
 // error in the reference's order (file, row, check) is found as a minimum
 // over per-row keys; its message is rebuilt on the host from the text.
 #include <cub/device/device_scan.cuh>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cerrno>
@@ -37,6 +42,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fmt.cuh"
 
 namespace phfem {
 
@@ -267,6 +273,80 @@ __global__ void k_fmt_write(const int32_t* __restrict__ ids, int64_t rows, const
       *p++ = j + 1 < K ? ' ' : '\n';
     }
   }
+}
+
+// "%.17g %.17g\n" per node (save_mesh / format_g17, mesh.cpp:95-99, 172-173)
+__global__ void k_fmt_coords_len(const double* __restrict__ xy, int64_t rows, int64_t* __restrict__ len) {
+  char buf[32];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    len[r] = fmt_g(xy[2 * r], 17, buf) + fmt_g(xy[2 * r + 1], 17, buf) + 2;
+}
+
+__global__ void k_fmt_coords_write(const double* __restrict__ xy, int64_t rows, const int64_t* __restrict__ off,
+                                   char* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    char* p = out + off[r];
+    p += fmt_g(xy[2 * r], 17, p);
+    *p++ = ' ';
+    p += fmt_g(xy[2 * r + 1], 17, p);
+    *p = '\n';
+  }
+}
+
+// the CLI's topology CSV row (tools/main.cpp:315-318): 1-based ids, 0 for no
+// t_minus, fmt(length) = "%.10g"
+__device__ __forceinline__ int put_uint(char* p, uint32_t v) {
+  const int d = ndigits(v);
+  for (int q = d - 1; q >= 0; --q) {
+    p[q] = (char)('0' + v % 10);
+    v /= 10;
+  }
+  return d;
+}
+
+template <bool kWrite>
+__global__ void k_fmt_csv(const int32_t* __restrict__ edge_nodes, const int32_t* __restrict__ edge_elements,
+                          const int32_t* __restrict__ ltp, const int32_t* __restrict__ ltm,
+                          const double2* __restrict__ coords, int64_t E, int64_t* __restrict__ len_off,
+                          char* __restrict__ out) {
+  char buf[96];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int2 ab = reinterpret_cast<const int2*>(edge_nodes)[e];
+    const int2 el = reinterpret_cast<const int2*>(edge_elements)[e];
+    const double2 pa = coords[ab.x], pb = coords[ab.y];
+    const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+    const double len = sqrt(dx * dx + dy * dy);  // edge_lengths, edge_topology.cpp:183
+    char* p = kWrite ? out + len_off[e] : buf;
+    char* q = p;
+    q += put_uint(q, (uint32_t)(e + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(ab.x + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(ab.y + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(el.x + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(el.y + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(ltp[e] + 1));
+    *q++ = ',';
+    q += put_uint(q, (uint32_t)(el.y >= 0 ? ltm[e] + 1 : 0));
+    *q++ = ',';
+    q += fmt_g(len, 10, q);
+    *q++ = '\n';
+    if (!kWrite) len_off[e] = q - p;
+  }
+}
+
+// test entry: "%.<P>g" of n device doubles into 32-byte slots + lengths
+__global__ void k_fmt_g_test(const double* __restrict__ v, int64_t n, int P, char* __restrict__ out,
+                             int32_t* __restrict__ lens) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lens[i] = fmt_g(v[i], P, out + 32 * i);
 }
 
 // ---------------------------------------------------------------- host side
@@ -599,118 +679,184 @@ static phfem_status load_text(phfem_ctx* ctx, const char* c, size_t nc, const ch
   return PHFEM_OK;
 }
 
-static bool read_file(const std::string& path, std::string* s) {
-  FILE* f = fopen(path.c_str(), "rb");
-  if (!f) return false;
-  s->clear();
-  if (fseek(f, 0, SEEK_END) == 0) {
-    const long sz = ftell(f);
-    if (sz > 0) {
-      s->resize((size_t)sz);
-      fseek(f, 0, SEEK_SET);
-      const size_t got = fread(&(*s)[0], 1, (size_t)sz, f);
-      s->resize(got);
-    }
+// whole file into malloc'd memory (no zero fill), large files by parallel pread
+struct FileBuf {
+  char* p = nullptr;
+  size_t n = 0;
+  ~FileBuf() { free(p); }
+};
+
+static bool read_file(const std::string& path, FileBuf* b) {
+  const int fd = open(path.c_str(), O_RDONLY);
+  if (fd < 0) return false;
+  struct stat st;
+  if (fstat(fd, &st) != 0) {
+    close(fd);
+    return false;
   }
-  fclose(f);
+  const size_t sz = (size_t)st.st_size;
+  b->p = (char*)malloc(sz ? sz : 1);
+  if (!b->p) {
+    close(fd);
+    return false;
+  }
+  const int T = sz < (size_t(64) << 20) ? 1 : std::min(8, io_threads());
+  std::vector<size_t> got((size_t)T, 0);
+  parallel_for(T, [&](int t) {
+    size_t a = sz * t / T;
+    const size_t e = sz * (t + 1) / T;
+    while (a < e) {
+      const ssize_t r = pread(fd, b->p + a, e - a, (off_t)a);
+      if (r <= 0) break;
+      a += (size_t)r;
+      got[t] += (size_t)r;
+    }
+  });
+  close(fd);
+  size_t total = 0;
+  for (size_t g : got) total += g;
+  b->n = total;  // (a short read ends the text there, like the stream would)
   return true;
 }
 
 // ---- formatting --------------------------------------------------------------
-// Text produced in per-thread chunks (uninitialised buffers), then either
-// written in order or gathered into one malloc'd buffer by parallel copies.
-struct Chunk {
-  std::unique_ptr<char[]> p;
-  size_t n = 0;
-};
+// Device -> pageable host copy of a large buffer: through a cached pinned
+// ring (2 x 32 MB per ctx and thread), the host threads copying chunk i - 1
+// out (first touch of the destination pages included) while the copy engine
+// brings chunk i — a plain pageable copy into fresh memory ran at ~2 GB/s.
+static phfem_status d2h_large(phfem_ctx* ctx, char* dst, const char* src, size_t bytes) {
+  constexpr size_t kCh = size_t(32) << 20;
+  if (bytes <= kCh) {
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PHFEM_OK;
+  }
+  struct Ring {
+    phfem_ctx* ctx;
+    char* buf;
+    cudaEvent_t ev[2];
+  };
+  static thread_local std::vector<Ring> rings;
+  Ring* r = nullptr;
+  for (auto& x : rings)
+    if (x.ctx == ctx) r = &x;
+  if (!r) {
+    Ring x{ctx, nullptr, {nullptr, nullptr}};
+    PHFEM_CUDA(ctx, cudaHostAlloc((void**)&x.buf, 2 * kCh, cudaHostAllocDefault));
+    for (auto& e : x.ev) PHFEM_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    rings.push_back(x);
+    r = &rings.back();
+  }
+  const size_t nch = (bytes + kCh - 1) / kCh;
+  const int T = std::min(8, io_threads());
+  auto drain = [&](size_t i) -> phfem_status {
+    PHFEM_CUDA(ctx, cudaEventSynchronize(r->ev[i & 1]));
+    const size_t off = i * kCh, n = std::min(kCh, bytes - off);
+    const char* slot = r->buf + (i & 1) * kCh;
+    parallel_for(T, [&](int t) {
+      const size_t a = n * t / T, b = n * (t + 1) / T;
+      memcpy(dst + off + a, slot + a, b - a);
+    });
+    return PHFEM_OK;
+  };
+  for (size_t i = 0; i < nch; ++i) {
+    const size_t off = i * kCh, n = std::min(kCh, bytes - off);
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(r->buf + (i & 1) * kCh, src + off, n, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaEventRecord(r->ev[i & 1], ctx->stream));
+    if (i > 0) PHFEM_TRY(drain(i - 1));  // (slot (i+1)&1 is free once chunk i-1 is out)
+  }
+  return drain(nch - 1);
+}
+
+// Text: one malloc'd buffer (handed to the caller as is by the *_format /
+// *_csv entry points; free with phfem_text_free), the optional header first.
 struct Text {
-  std::string head;  // small prefix (CSV header)
-  std::vector<Chunk> parts;
-  size_t size() const {
-    size_t s = head.size();
-    for (const auto& c : parts) s += c.n;
-    return s;
-  }
-  char* gather() const {  // malloc'd (free with phfem_text_free)
-    const size_t n = size();
-    char* out = (char*)malloc(n ? n : 1);
-    if (!out) return nullptr;
-    memcpy(out, head.data(), head.size());
-    std::vector<size_t> off(parts.size() + 1, head.size());
-    for (size_t i = 0; i < parts.size(); ++i) off[i + 1] = off[i] + parts[i].n;
-    parallel_for((int)parts.size(), [&](int i) { memcpy(out + off[i], parts[i].p.get(), parts[i].n); });
-    return out;
+  std::string head;
+  char* buf = nullptr;
+  size_t n = 0;
+  Text() = default;
+  Text(const Text&) = delete;
+  Text& operator=(const Text&) = delete;
+  ~Text() { free(buf); }
+  char* release() {
+    char* p = buf;
+    buf = nullptr;
+    return p;
   }
 };
-template <int K>
-static phfem_status format_index_rows(phfem_ctx* ctx, const int32_t* ids, int64_t rows, Text* out) {
-  out->parts.clear();
-  if (rows == 0) return PHFEM_OK;
+
+// Device text: line lengths (int64), one 64-bit scan, the bytes, one D2H.
+template <class LenFn, class WriteFn>
+static phfem_status device_text(phfem_ctx* ctx, int64_t rows, LenFn launch_len, WriteFn launch_write, Text* out) {
+  free(out->buf);
+  out->buf = nullptr;
+  out->n = 0;
+  const size_t hn = out->head.size();
+  int64_t total = 0;
+  char* d = nullptr;
   int64_t* len = nullptr;
   int64_t* off = nullptr;
-  PHFEM_TRY(dalloc(ctx, &len, rows + 1));
-  PHFEM_TRY(dalloc(ctx, &off, rows + 1));
-  const int g = grid_for(rows, 256, ctx->num_sms * 8);
-  PHFEM_LAUNCH(ctx, "k_fmt_len", k_fmt_len<K><<<g, 256, 0, ctx->stream>>>(ids, rows, len));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(len + rows, 0, sizeof(int64_t), ctx->stream));
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, len, off, (int)(rows + 1), ctx->stream);
-  void* tmp = nullptr;
-  PHFEM_TRY(raw_alloc(ctx, &tmp, tb));
-  PHFEM_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, len, off, (int)(rows + 1), ctx->stream));
-  ctx->launches++;
-  raw_free(ctx, tmp);
-  int64_t total = 0;
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(&total, off + rows, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
-  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  char* d = nullptr;
-  PHFEM_TRY(dalloc(ctx, &d, total));
-  PHFEM_LAUNCH(ctx, "k_fmt_write", k_fmt_write<K><<<g, 256, 0, ctx->stream>>>(ids, rows, off, d));
-  out->parts.resize(1);
-  out->parts[0].p.reset(new char[(size_t)total + 1]);
-  out->parts[0].n = (size_t)total;
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(out->parts[0].p.get(), d, (size_t)total, cudaMemcpyDeviceToHost, ctx->stream));
-  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (rows > 0) {
+    PHFEM_TRY(dalloc(ctx, &len, rows + 1));
+    PHFEM_TRY(dalloc(ctx, &off, rows + 1));
+    PHFEM_TRY(launch_len(len));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(len + rows, 0, sizeof(int64_t), ctx->stream));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, len, off, (int)(rows + 1), ctx->stream);
+    void* tmp = nullptr;
+    PHFEM_TRY(raw_alloc(ctx, &tmp, tb));
+    PHFEM_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, len, off, (int)(rows + 1), ctx->stream));
+    ctx->launches++;
+    raw_free(ctx, tmp);
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&total, off + rows, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    PHFEM_TRY(dalloc(ctx, &d, std::max<int64_t>(total, 1)));
+    PHFEM_TRY(launch_write(off, d));
+  }
+  out->buf = (char*)malloc(hn + (size_t)total + 1);
+  if (!out->buf) return set_error(ctx, PHFEM_ERR_OOM, "out of host memory (%zu bytes)", hn + (size_t)total);
+  memcpy(out->buf, out->head.data(), hn);
+  out->n = hn + (size_t)total;
+  if (total > 0) PHFEM_TRY(d2h_large(ctx, out->buf + hn, d, (size_t)total));
   dfree(ctx, d);
   dfree(ctx, len);
   dfree(ctx, off);
   return PHFEM_OK;
 }
 
-// format_g17 (mesh.cpp:95-99): "%.17g %.17g\n" per node, host threads
-static void format_coords(const std::vector<double>& xy, Text* out) {
-  const size_t rows = xy.size() / 2;
-  const int T = rows < 65536 ? 1 : 4 * io_threads();
-  out->parts.clear();
-  out->parts.resize((size_t)T);
-  parallel_for(std::min(T, io_threads()), [&](int w) {
-    for (int t = w; t < T; t += std::min(T, io_threads())) {
-      const size_t r0 = rows * (size_t)t / T, r1 = rows * (size_t)(t + 1) / T;
-      Chunk& c = out->parts[t];
-      c.p.reset(new char[(r1 - r0) * 50 + 1]);
-      char* p = c.p.get();
-      for (size_t r = r0; r < r1; ++r) {
-        p = std::to_chars(p, p + 25, xy[2 * r], std::chars_format::general, 17).ptr;
-        *p++ = ' ';
-        p = std::to_chars(p, p + 25, xy[2 * r + 1], std::chars_format::general, 17).ptr;
-        *p++ = '\n';
-      }
-      c.n = (size_t)(p - c.p.get());
-    }
-  });
+template <int K>
+static phfem_status format_index_rows(phfem_ctx* ctx, const int32_t* ids, int64_t rows, Text* out) {
+  const int g = grid_for(rows, 256, ctx->num_sms * 8);
+  return device_text(
+      ctx, rows,
+      [&](int64_t* len) -> phfem_status {
+        PHFEM_LAUNCH(ctx, "k_fmt_len", k_fmt_len<K><<<g, 256, 0, ctx->stream>>>(ids, rows, len));
+        return PHFEM_OK;
+      },
+      [&](const int64_t* off, char* d) -> phfem_status {
+        PHFEM_LAUNCH(ctx, "k_fmt_write", k_fmt_write<K><<<g, 256, 0, ctx->stream>>>(ids, rows, off, d));
+        return PHFEM_OK;
+      },
+      out);
 }
 
 static phfem_status mesh_text(phfem_ctx* ctx, const phfem_mesh* m, int which, Text* out) {
   switch (which) {
-    case 0: {
-      std::vector<double> xy(2 * (size_t)m->nC);
-      if (m->nC > 0) {
-        PHFEM_CUDA(ctx, cudaMemcpyAsync(xy.data(), m->coords, sizeof(double) * xy.size(), cudaMemcpyDeviceToHost,
-                                        ctx->stream));
-        PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-      }
-      format_coords(xy, out);
-      return PHFEM_OK;
+    case 0: {  // format_g17 (mesh.cpp:95-99) on the device (fmt.cuh, exact)
+      const int64_t rows = m->nC;
+      const int g = grid_for(rows, 256, ctx->num_sms * 8);
+      return device_text(
+          ctx, rows,
+          [&](int64_t* len) -> phfem_status {
+            PHFEM_LAUNCH(ctx, "k_fmt_coords_len", k_fmt_coords_len<<<g, 256, 0, ctx->stream>>>(m->coords, rows, len));
+            return PHFEM_OK;
+          },
+          [&](const int64_t* off, char* d) -> phfem_status {
+            PHFEM_LAUNCH(ctx, "k_fmt_coords_write", k_fmt_coords_write<<<g, 256, 0, ctx->stream>>>(m->coords, rows,
+                                                                                              off, d));
+            return PHFEM_OK;
+          },
+          out);
     }
     case 1: return format_index_rows<3>(ctx, m->elements, m->nE, out);
     case 2: return format_index_rows<2>(ctx, m->dirichlet, m->nD, out);
@@ -719,69 +865,41 @@ static phfem_status mesh_text(phfem_ctx* ctx, const phfem_mesh* m, int which, Te
   }
 }
 
-// tools/main.cpp:302-323 (cmd_topology): header + one row per edge, lengths
-// from edge_lengths (device, bit-identical) in fmt = "%.10g"
+// tools/main.cpp:302-323 (cmd_topology): header + one row per edge on the
+// device (lengths as edge_lengths computes them, "%.10g" exact)
 static phfem_status topology_csv(phfem_ctx* ctx, const phfem_mesh* m, const phfem_topology* t, Text* out) {
   const int64_t E = t->E;
-  std::vector<int32_t> en(2 * E), el(2 * E), lp(E), lm(E);
-  std::vector<double> len(E);
-  if (E > 0) {
-    double* dl = nullptr;
-    PHFEM_TRY(dalloc(ctx, &dl, E));
-    PHFEM_TRY(phfem_edge_lengths(ctx, m, t, dl));
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(len.data(), dl, 8 * E, cudaMemcpyDeviceToHost, ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(en.data(), t->edge_nodes, 8 * E, cudaMemcpyDeviceToHost, ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(el.data(), t->edge_elements, 8 * E, cudaMemcpyDeviceToHost, ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(lp.data(), t->local_in_tplus, 4 * E, cudaMemcpyDeviceToHost, ctx->stream));
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(lm.data(), t->local_in_tminus, 4 * E, cudaMemcpyDeviceToHost, ctx->stream));
-    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    dfree(ctx, dl);
-  }
-  const int T = E < 65536 ? 1 : 4 * io_threads();
-  const int W = std::min(T, io_threads());
-  out->parts.clear();
-  out->parts.resize((size_t)T);
-  parallel_for(W, [&](int w) {
-   for (int th = w; th < T; th += W) {
-    const int64_t e0 = E * th / T, e1 = E * (th + 1) / T;
-    Chunk& c = out->parts[th];
-    c.p.reset(new char[(size_t)(e1 - e0) * 96 + 1]);
-    char* p = c.p.get();
-    auto put = [&](long long v, char sep) {
-      p = std::to_chars(p, p + 24, v).ptr;
-      *p++ = sep;
-    };
-    for (int64_t e = e0; e < e1; ++e) {
-      const int tm = el[2 * e + 1];
-      put(e + 1, ',');
-      put(en[2 * e] + 1, ',');
-      put(en[2 * e + 1] + 1, ',');
-      put(el[2 * e] + 1, ',');
-      put(tm + 1, ',');
-      put(lp[e] + 1, ',');
-      put(tm >= 0 ? lm[e] + 1 : 0, ',');
-      p = std::to_chars(p, p + 32, len[e], std::chars_format::general, 10).ptr;
-      *p++ = '\n';
-    }
-    c.n = (size_t)(p - c.p.get());
-   }
-  });
+  const int g = grid_for(E, 256, ctx->num_sms * 8);
+  const double2* c = (const double2*)m->coords;
   out->head = "edge,node_start,node_end,t_plus,t_minus,led,led_tn,length\n";
+  PHFEM_TRY(device_text(
+      ctx, E,
+      [&](int64_t* len) -> phfem_status {
+        PHFEM_LAUNCH(ctx, "k_fmt_csv", (k_fmt_csv<false><<<g, 256, 0, ctx->stream>>>(
+            t->edge_nodes, t->edge_elements, t->local_in_tplus, t->local_in_tminus, c, E, len, nullptr)));
+        return PHFEM_OK;
+      },
+      [&](const int64_t* off, char* d) -> phfem_status {
+        PHFEM_LAUNCH(ctx, "k_fmt_csv", (k_fmt_csv<true><<<g, 256, 0, ctx->stream>>>(
+            t->edge_nodes, t->edge_elements, t->local_in_tplus, t->local_in_tminus, c, E,
+            const_cast<int64_t*>(off), d)));
+        return PHFEM_OK;
+      },
+      out));
   return PHFEM_OK;
 }
 
-static phfem_status to_buffer(phfem_ctx* ctx, const Text& t, char** out, size_t* len) {
-  *len = t.size();
-  *out = t.gather();
-  if (!*out) return set_error(ctx, PHFEM_ERR_OOM, "out of host memory (%zu bytes)", *len);
+static phfem_status to_buffer(phfem_ctx* ctx, Text& t, char** out, size_t* len) {
+  (void)ctx;
+  *len = t.n;
+  *out = t.release();
   return PHFEM_OK;
 }
 
 static phfem_status write_file(phfem_ctx* ctx, const std::string& path, const Text& t) {
   FILE* f = fopen(path.c_str(), "wb");
   if (!f) return set_error(ctx, PHFEM_ERR_RUNTIME, "cannot write %s", path.c_str());
-  bool ok = fwrite(t.head.data(), 1, t.head.size(), f) == t.head.size();
-  for (const auto& c : t.parts) ok = ok && fwrite(c.p.get(), 1, c.n, f) == c.n;
+  bool ok = t.n == 0 || fwrite(t.buf, 1, t.n, f) == t.n;
   ok = (fclose(f) == 0) && ok;
   if (!ok) return set_error(ctx, PHFEM_ERR_RUNTIME, "cannot write %s", path.c_str());
   return PHFEM_OK;
@@ -806,13 +924,13 @@ PHFEM_API phfem_status phfem_mesh_load_dir(phfem_ctx* ctx, const char* dir, phfe
   if (!ctx || !dir || !out) return PHFEM_ERR_INVALID_ARGUMENT;
   memset(out, 0, sizeof(*out));
   const std::string d(dir);
-  std::string c, e, di, ne;
+  FileBuf c, e, di, ne;
   if (!read_file(d + "/coordinates.dat", &c))
     return set_error(ctx, PHFEM_ERR_RUNTIME, "cannot open %s/coordinates.dat", dir);
   if (!read_file(d + "/elements.dat", &e)) return set_error(ctx, PHFEM_ERR_RUNTIME, "cannot open %s/elements.dat", dir);
   read_file(d + "/dirichlet.dat", &di);  // optional (mesh.cpp:162-163)
   read_file(d + "/neumann.dat", &ne);
-  return load_text(ctx, c.data(), c.size(), e.data(), e.size(), di.data(), di.size(), ne.data(), ne.size(), out);
+  return load_text(ctx, c.p, c.n, e.p, e.n, di.p, di.n, ne.p, ne.n, out);
 }
 
 PHFEM_API phfem_status phfem_mesh_format(phfem_ctx* ctx, const phfem_mesh* mesh, int which, char** out,
@@ -859,4 +977,22 @@ PHFEM_API phfem_status phfem_topology_csv_file(phfem_ctx* ctx, const phfem_mesh*
   Text s;
   PHFEM_TRY(topology_csv(ctx, mesh, topo, &s));
   return write_file(ctx, path, s);
+}
+
+// test entry: "%.<precision>g" of n device doubles into 32-byte slots (device)
+PHFEM_API phfem_status phfem_format_g(phfem_ctx* ctx, const double* vals, int64_t n, int precision, char* out,
+                                      int32_t* lens) {
+  if (!ctx || precision < 1 || precision > 17 || (n > 0 && (!vals || !out || !lens)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_fmt_g_test", k_fmt_g_test<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        vals, n, precision, out, lens));
+  return PHFEM_OK;
+}
+
+// the same formatter on the host (no device needed): the CPU tests pin it to
+// glibc's printf over millions of doubles; the kernels run this very code
+PHFEM_API int phfem_format_g_host(double v, int precision, char* out) {
+  if (precision < 1 || precision > 17 || !out) return -1;
+  return fmt_g(v, precision, out);
 }

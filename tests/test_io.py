@@ -171,3 +171,68 @@ def test_gpu_io_large_round_trip(ctx):
     back = capi.load_mesh_text(ctx, *text).download()
     same_mesh(back, R.load_mesh_text(*text).host())
     assert np.array_equal(back.coords, hm.coords) and np.array_equal(back.elements, hm.elements)
+
+
+# ---- the device "%.<P>g" formatter against glibc's printf ---------------------
+def _fmt_cases():
+    import struct
+    rng = np.random.default_rng(17)
+    bits = rng.integers(0, 2**63, 200000, dtype=np.uint64) | (rng.integers(0, 2, 200000, dtype=np.uint64) << 63)
+    v = bits.view(np.float64)
+    special = [0.0, -0.0, 1.0, -1.0, 0.1, 0.5, 1e-5, 1e-4, 9.9999e-5, 123456789012345678.0, 1e16, 1e17,
+               9.999999999999999e16, 1e22, 1e23, 5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+               1125899906842624.5, 2.0**60, 2.0**64, 0.3, 2.0 / 3.0, float("inf"), -float("inf"), float("nan"),
+               -float("nan"), 1.5, 2.5, 0.125, 1e-310, 4.35e-320, 999999999.5, 99999.999999999999]
+    # exact ties at 17 and 10 digits: k / 2 with 17 / 10 significant digits before the .5
+    ties = [float(k) + 0.5 for k in (1125899906842624, 1125899906842623, 99999999.0, 123456789.0)]
+    grid = [m * 10.0 ** k for k in range(-30, 31) for m in (1.0, 0.5, 0.25, 0.999999, 7.0)]
+    uni = list(rng.uniform(-2.0, 2.0, 20000)) + list(np.ldexp(rng.uniform(0.5, 1.0, 2000), rng.integers(-1074, 1024, 2000)))
+    return np.concatenate([v, np.array(special + ties + grid + uni, dtype=np.float64)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [17, 10, 1, 6, 15, 16])
+def test_gpu_format_g_equals_glibc(ctx, prec):
+    import ctypes as C
+    libc = C.CDLL(None)
+    vals = _fmt_cases()
+    n = len(vals)
+    dv = ctx.to_device(vals)
+    out = ctx.alloc(32 * n)
+    lens = ctx.alloc(4 * n)
+    ctx.check(ctx.lib.phfem_format_g(ctx.ptr, C.c_void_p(dv), n, prec, C.c_void_p(out), C.c_void_p(lens)))
+    txt = ctx.to_host(out, (n, 32), np.uint8)
+    ln = ctx.to_host(lens, (n,), np.int32)
+    for p in (dv, out, lens):
+        ctx.free(p)
+    buf = C.create_string_buffer(64)
+    fmt = f"%.{prec}g".encode()
+    bad = []
+    for i in range(n):
+        libc.snprintf(buf, 64, fmt, C.c_double(vals[i]))
+        if bytes(txt[i, :ln[i]]) != buf.value:
+            bad.append((vals[i], bytes(txt[i, :ln[i]]), buf.value))
+            if len(bad) > 5:
+                break
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("prec", [17, 10, 1, 6, 15, 16])
+def test_format_g_host_equals_glibc(prec):
+    """The formatter the kernels use (fmt.cuh), run on the host: the same
+    bytes as glibc's printf("%.Pg") for random bit patterns, subnormals,
+    powers of ten and their neighbours, exact ties, infinities and NaNs."""
+    import ctypes as C
+    lib = capi.load_library()
+    libc = C.CDLL(None)
+    buf, out = C.create_string_buffer(64), C.create_string_buffer(64)
+    fmt = f"%.{prec}g".encode()
+    bad = []
+    for v in _fmt_cases()[::4]:
+        libc.snprintf(buf, 64, fmt, C.c_double(v))
+        n = lib.phfem_format_g_host(float(v), prec, out)
+        if out.raw[:n] != buf.value:
+            bad.append((v, out.raw[:n], buf.value))
+            if len(bad) > 5:
+                break
+    assert not bad, bad

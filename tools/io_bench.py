@@ -35,9 +35,14 @@ for lv, is_ref in ((level, False), (ref_level, True)):
     tl, m2 = timed(lambda: capi.load_mesh_text(ctx, *text), 2)
     topo = capi.build_topology(ctx, m2)
     tc, csv = timed(lambda: capi.topology_csv(ctx, m2, topo), 2)
+    import tempfile
+    with tempfile.TemporaryDirectory(dir="/dev/shm" if os.path.isdir("/dev/shm") else None) as td:
+        tsd, _ = timed(lambda: capi.save_mesh_dir(ctx, dm, td), 2)
+        tld, _ = timed(lambda: capi.load_mesh_dir(ctx, td), 2)
     print(f"device L{lv}: {nE} triangles, text {nbytes / 1e9:.2f} GB: save {ts:.3f} s "
           f"({nE / ts / 1e6:.1f} M tri/s), load {tl:.3f} s ({nE / tl / 1e6:.1f} M tri/s), "
-          f"topology CSV {len(csv) / 1e9:.2f} GB in {tc:.3f} s", flush=True)
+          f"topology CSV {len(csv) / 1e9:.2f} GB in {tc:.3f} s (Python bytes); files in /dev/shm: "
+          f"save_mesh_dir {tsd:.3f} s, load_mesh_dir {tld:.3f} s", flush=True)
     if is_ref and R.available():
         t0 = time.perf_counter()
         rm = R.load_mesh_text(*text)
