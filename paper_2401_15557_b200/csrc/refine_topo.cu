@@ -40,7 +40,10 @@
 
 namespace phfem {
 
-constexpr int kLvT = 128;          // parent edges (= threads) per tile
+#ifndef PHFEM_LV_TILE
+#define PHFEM_LV_TILE 128
+#endif
+constexpr int kLvT = PHFEM_LV_TILE;  // parent edges (= threads) per tile
 constexpr int kLvF = 6 * kLvT;     // fine-edge slots per tile (<= 6 per parent edge)
 
 __device__ __forceinline__ int abs_edge(int s) { return s >= 0 ? s : ~s; }
@@ -165,7 +168,8 @@ __global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE, i
 #endif
 template <bool kFull>
 __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a, LvOut o) {
-  __shared__ LvSmem<kFull> s;
+  extern __shared__ __align__(16) unsigned char lv_smem[];  // dynamic: tiles may exceed 48 KB
+  LvSmem<kFull>& s = *reinterpret_cast<LvSmem<kFull>*>(lv_smem);
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
   const int64_t e0 = (int64_t)tile * kLvT;
@@ -338,6 +342,18 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   }
 }
 
+// dynamic SMEM of the level kernel (opt-in above 48 KB, set once per variant)
+template <bool kFull>
+static size_t lv_smem_bytes() {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_rl_level<kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(LvSmem<kFull>));
+    set = true;
+  }
+  return sizeof(LvSmem<kFull>);
+}
+
 }  // namespace phfem
 
 using namespace phfem;
@@ -401,9 +417,9 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
     o.row_ptr = C->row_ptr;
     o.col = C->col_idx;
     o.val = C->values;
-    PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<(unsigned)ntiles, kLvT, 0, ctx->stream>>>(a, o));
+    PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<(unsigned)ntiles, kLvT, lv_smem_bytes<true>(), ctx->stream>>>(a, o));
   } else {
-    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)ntiles, kLvT, 0, ctx->stream>>>(a, o));
+    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)ntiles, kLvT, lv_smem_bytes<false>(), ctx->stream>>>(a, o));
   }
   dfree(ctx, tiles);
   return PHFEM_OK;
@@ -638,9 +654,9 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
       o.row_ptr = C->row_ptr;
       o.col = C->col_idx;
       o.val = C->values;
-      PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<nt, kLvT, 0, ctx->stream>>>(a, o));
+      PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<nt, kLvT, lv_smem_bytes<true>(), ctx->stream>>>(a, o));
     } else {
-      PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<nt, kLvT, 0, ctx->stream>>>(a, o));
+      PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<nt, kLvT, lv_smem_bytes<false>(), ctx->stream>>>(a, o));
     }
   }
   dfree(ctx, nbits);
