@@ -192,9 +192,10 @@ constexpr int kTileThreads = 256;
 constexpr int kTileCap = 10 * kTileNodes;  // items kept in SMEM (10 per node)
 
 struct TileSmem {
-  uint64_t buf1[kTileCap];
+  uint64_t buf1[kTileCap + 4];  // + 4 all-ones keys: the rank loop reads past the last segment
   uint64_t buf2[kTileCap];
   uint8_t node_of[kTileCap];
+  uint8_t fl[kTileCap];  // fast path: run start (bit 0) / has a partner (bit 1) per sorted item
   int32_t cnt[kTileNodes];
   int32_t seg[kTileNodes];
   int32_t cur[kTileNodes];
@@ -363,18 +364,24 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
     sm.buf1[pos] = it;
     sm.node_of[pos] = (uint8_t)nd;
   }
+  if (tid < 4) sm.buf1[n + tid] = ~0ull;
   __syncthreads();
 
   // rank sort inside each node segment (<= 32 items, ~6 on refined meshes):
   // key = (min node, occurrence), unique; the reference's stable order
   // (items of one segment share the max-node bits and differ in (min, occ),
-  // so the raw 64-bit items compare in key order)
+  // so the raw 64-bit items compare in key order).  Four branch-free masked
+  // compares per trip (reads past the segment stay inside the tile or hit
+  // the padding; the mask drops them — the next sub-bucket's keys restart
+  // at node 0, so they are not simply larger).
   for (int p = tid; p < n; p += T) {
     const uint64_t it = sm.buf1[p];
     const int nd = sm.node_of[p];
-    const int st = sm.seg[nd], c = sm.cnt[nd];
+    const int st = sm.seg[nd], end = st + sm.cnt[nd];
     int r = 0;
-    for (int q = st; q < st + c; ++q) r += sm.buf1[q] < it;
+    for (int q = st; q < end; q += 4)
+      r += (int)(sm.buf1[q] < it) + (int)((q + 1 < end) & (sm.buf1[q + 1] < it)) +
+           (int)((q + 2 < end) & (sm.buf1[q + 2] < it)) + (int)((q + 3 < end) & (sm.buf1[q + 3] < it));
     sm.buf2[st + r] = it;
   }
   __syncthreads();
@@ -406,6 +413,7 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
         atomicMin(&err->topo, (v << 33) | (lo << 2) | (third ? 0ull : (2ull | (f & 1ull))));
       }
       if (start) atomicAdd(&sm.nedge[nd], 1);
+      sm.fl[pos] = (uint8_t)(start | (partner << 1));
     }
     w_ne += __popc(__ballot_sync(0xffffffffu, start));
     w_nb += __popc(__ballot_sync(0xffffffffu, start && !partner));
@@ -431,19 +439,14 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   for (int q = 0; q < wtotal; q += 32) {
     const int pos = wbase + q + lane;
     const bool valid = q + lane < wtotal;
-    bool start = false, partner = false;
+    const int fl = valid ? sm.fl[pos] : 0;  // from the detection pass
+    const bool start = fl & 1, partner = fl & 2;
     uint64_t f = 0, g = 0;
     int nd = 0;
-    if (valid) {
+    if (start) {
       f = sm.buf2[pos];
       nd = sm.node_of[pos];
-      const int st = sm.seg[nd], en = st + sm.cnt[nd];
-      const uint64_t lo = (f >> (ob + 1)) & lomask;
-      start = pos == st || ((sm.buf2[pos - 1] >> (ob + 1)) & lomask) != lo;
-      if (start && pos + 1 < en) {
-        g = sm.buf2[pos + 1];
-        partner = ((g >> (ob + 1)) & lomask) == lo;
-      }
+      if (partner) g = sm.buf2[pos + 1];
     }
     const unsigned sb = __ballot_sync(0xffffffffu, start);
     const unsigned bb = __ballot_sync(0xffffffffu, start && !partner);
