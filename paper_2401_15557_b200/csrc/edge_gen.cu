@@ -324,10 +324,13 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
 // 32-wide bitonic network), then per warp run starts / partners / the
 // reference's error checks as neighbour tests; edge ranks are ballot/popc
 // prefixes, so records of consecutive edges come from consecutive lanes.
+constexpr int kTilePer = kTileCap / kTileThreads;  // items per thread in the fast path
+
 __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items, const EgParams& P,
                                              TileSmem& sm, int4* __restrict__ rec,
                                              int32_t* __restrict__ tileE, int32_t* __restrict__ tileB,
-                                             const EgOut& out, phfem_dev_errors* err) {
+                                             const EgOut& out, phfem_dev_errors* err,
+                                             const uint64_t (&itr)[kTilePer], const int (&ndr)[kTilePer]) {
   const int tid = threadIdx.x;
   const int T = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -335,7 +338,6 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   const int nsub = kTileNodes >> P.bs;
   const int64_t s = sm.sbo[0];
   const int n = sm.sbo[nsub] - (int)s;
-  const int shift = P.total_bits;
   const int ob = P.occ_bits;
   const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
   const unsigned lt = lanemask_lt();
@@ -347,22 +349,14 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   sm.seg[tid] = st_me;
   sm.cur[tid] = st_me;
   __syncthreads();
-  for (int p = tid; p < n; p += T) {
-    const uint64_t it = __ldg(items + s + p);
-    int sub = 0;
-    if (nsub > 1) {
-      int lo = 0, hi = nsub - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sm.sbo[mid] - s <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      sub = lo;
+  // scatter the items the histogram pass kept in registers
+#pragma unroll
+  for (int k = 0; k < kTilePer; ++k) {
+    if (tid + k * T < n) {
+      const int pos = atomicAdd(&sm.cur[ndr[k]], 1);
+      sm.buf1[pos] = itr[k];
+      sm.node_of[pos] = (uint8_t)ndr[k];
     }
-    const int nd = (sub << P.bs) | (int)(it >> shift);
-    const int pos = atomicAdd(&sm.cur[nd], 1);
-    sm.buf1[pos] = it;
-    sm.node_of[pos] = (uint8_t)nd;
   }
   if (tid < 4) sm.buf1[n + tid] = ~0ull;
   __syncthreads();
@@ -487,31 +481,39 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
   const int64_t s = sm.sbo[0];
   const int n = sm.sbo[nsub] - (int)s;
   bool fast = n <= kTileCap;
-  if (fast) {  // histogram by node; the fast path needs every node <= 32 occurrences
-    for (int p = tid; p < n; p += blockDim.x) {
-      const uint64_t it = __ldg(items + s + p);
-      int sub = 0;
-      if (nsub > 1) {
-        int lo = 0, hi = nsub - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sm.sbo[mid] - s <= p) lo = mid;
-          else hi = mid - 1;
+  // fast path: every item loaded once into registers (all loads in flight
+  // together), histogram by node; it needs every node <= 32 occurrences
+  uint64_t itr[kTilePer];
+  int ndr[kTilePer];
+  if (fast) {
+#pragma unroll
+    for (int k = 0; k < kTilePer; ++k) {
+      const int p = tid + k * kTileThreads;
+      itr[k] = p < n ? __ldg(items + s + p) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < kTilePer; ++k) {
+      const int p = tid + k * kTileThreads;
+      ndr[k] = 0;
+      if (p < n) {
+        int sub = 0;
+        if (nsub > 1) {
+          int lo = 0, hi = nsub - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.sbo[mid] - s <= p) lo = mid;
+            else hi = mid - 1;
+          }
+          sub = lo;
         }
-        sub = lo;
+        ndr[k] = (sub << P.bs) | (int)(itr[k] >> P.total_bits);
+        atomicAdd(&sm.cnt[ndr[k]], 1);
       }
-      const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
-#ifdef PHFEM_EG_HIST_MATCH
-      const unsigned g = __match_any_sync(__activemask(), nd);
-      if ((int)lane_id() == __ffs(g) - 1) atomicAdd(&sm.cnt[nd], __popc(g));
-#else
-      atomicAdd(&sm.cnt[nd], 1);
-#endif
     }
     fast = __syncthreads_and(sm.cnt[tid] <= 32);
   }
   if (fast) {
-    eg_tile_fast(items, P, sm, rec, tileE, tileB, out, err);
+    eg_tile_fast(items, P, sm, rec, tileE, tileB, out, err, itr, ndr);
     return;
   }
   sm.cnt[tid] = 0;
