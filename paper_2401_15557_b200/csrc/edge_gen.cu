@@ -167,7 +167,52 @@ struct EgOut {
   int32_t* node_edge_start;
   int2* pairs;  // non-null: (slot 3m+l, edge or ~edge) per occurrence instead of elem_edge
   int32_t node_base;
+  // fused classification + C (sort-built final topology, pipeline): the
+  // Neumann pairs as a hash set of (min << 32 | max) keys; retained_pos /
+  // retained_edges / C rows written by the emit pass
+  const unsigned long long* neu_keys;
+  int neu_cap;
+  int32_t* tileN;  // Neumann edges per tile (tile pass), then their prefixes
+  int32_t* rpos;
+  int32_t* redges;
+  int32_t* row_ptr;
+  int32_t* col;
+  double* val;
+  const double2* coords;
+  int L;
 };
+
+__device__ __forceinline__ uint32_t neu_pair_hash(unsigned long long key, int cap) {
+  return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32) & (uint32_t)(cap - 1);
+}
+
+// is (lo, hi) a Neumann pair (either direction in the mesh's list)?
+__device__ __forceinline__ bool neu_pair_has(const EgOut& o, int lo, int hi) {
+  if (!o.neu_keys) return false;
+  const unsigned long long key = (unsigned long long)(uint32_t)lo << 32 | (uint32_t)hi;
+  uint32_t h = neu_pair_hash(key, o.neu_cap);
+  while (true) {
+    const unsigned long long k = o.neu_keys[h];
+    if (k == key) return true;
+    if (k == ~0ull) return false;
+    h = (h + 1) & (uint32_t)(o.neu_cap - 1);
+  }
+}
+
+__global__ void k_neu_pair_insert(const int32_t* __restrict__ pairs, int n, int cap,
+                                  unsigned long long* __restrict__ keys) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = pairs[2 * i], b = pairs[2 * i + 1];
+    const unsigned long long key =
+        (unsigned long long)(uint32_t)min(a, b) << 32 | (uint32_t)max(a, b);
+    uint32_t h = neu_pair_hash(key, cap);
+    while (true) {
+      const unsigned long long prev = atomicCAS(keys + h, ~0ull, key);
+      if (prev == ~0ull || prev == key) break;
+      h = (h + 1) & (uint32_t)(cap - 1);
+    }
+  }
+}
 
 // Edge record of the sort pass (one per unique edge, at a tile-local slot of
 // the tile's item range): {local max node | boundary edges before it in the
@@ -175,12 +220,12 @@ struct EgOut {
 // the t_plus / t_minus occurrence.  Carrying the tile-local boundary prefix
 // lets the emit pass run one record per thread with no scan.
 __device__ __forceinline__ int4 eg_record(int nd, int bloc, int32_t lo, uint64_t f, uint64_t g,
-                                          bool two, int ob) {
+                                          bool two, int ob, bool neu = false) {
   const uint32_t occ_mask = (uint32_t)((1ull << ob) - 1ull);
   const uint32_t occ_f = (uint32_t)(f >> 1) & occ_mask;
   const uint32_t occ_g = (uint32_t)(g >> 1) & occ_mask;
   return make_int4(nd | bloc << 8, lo, (int)((occ_f << 1) | (uint32_t)(f & 1ull)),
-                   two ? (int)occ_g : -1);
+                   two ? (int)occ_g : (neu ? -2 : -1));  // -2: a Neumann boundary edge
 }
 
 // One CTA per tile of kTileNodes consecutive max-node ids (= 256 >> bs
@@ -308,7 +353,10 @@ __device__ __forceinline__ void eg_tile(const uint64_t* __restrict__ items, cons
     const uint64_t lo = (f >> lo_shift) & lo_mask;
     if (p != st && ((buf2[p - 1] >> lo_shift) & lo_mask) == lo) continue;
     const bool two = p + 1 < en && ((buf2[p + 1] >> lo_shift) & lo_mask) == lo;
-    rec[s + e] = eg_record(nd, bl, (int32_t)lo, f, two ? buf2[p + 1] : 0, two, P.occ_bits);
+    const bool neu =
+        !two && out.neu_keys && neu_pair_has(out, (int)lo, P.node_base + tile * kTileNodes + nd);
+    if (neu) atomicAdd(&out.tileN[tile], 1);
+    rec[s + e] = eg_record(nd, bl, (int32_t)lo, f, two ? buf2[p + 1] : 0, two, P.occ_bits, neu);
     ++e;
     bl += !two;
   }
@@ -447,7 +495,9 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
     if (start) {
       const int32_t e = e_off + __popc(sb & lt);
       const int32_t lo = (int32_t)((f >> (ob + 1)) & lomask);
-      rec[s + e] = eg_record(nd, b_off + __popc(bb & lt), lo, f, g, partner, ob);
+      const bool neu = !partner && out.neu_keys && neu_pair_has(out, lo, P.node_base + tile * kTileNodes + nd);
+      if (neu) atomicAdd(&out.tileN[tile], 1);
+      rec[s + e] = eg_record(nd, b_off + __popc(bb & lt), lo, f, g, partner, ob, neu);
     }
     e_off += __popc(sb);
     b_off += __popc(bb);
@@ -543,14 +593,35 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
   if (vme < nC) out.node_edge_start[vme] += E0;
   if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
   // one record per thread, 4 in flight: no scan (records carry their
-  // tile-local boundary prefix)
+  // tile-local boundary prefix); the fused classification + C also needs
+  // the Neumann edges before each record: one packed block scan per trip
   const int64_t vbase = (int64_t)out.node_base + (int64_t)tile * kTileNodes;
-  for (int i0 = threadIdx.x; i0 < ne; i0 += 4 * kEmitThreads) {
+  const bool fused = out.rpos != nullptr;
+  __shared__ unsigned long long nscan[33];
+  int nrun = fused ? out.tileN[tile] : 0;  // Neumann edges before the trip (global)
+  for (int i00 = 0; i00 < ne; i00 += 4 * kEmitThreads) {
+    const int i0 = i00 + threadIdx.x;
     int4 r[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = i0 + u * kEmitThreads;
       if (i < ne) r[u] = rec[s + i];
+    }
+    int nb4[4] = {0, 0, 0, 0};  // Neumann edges before each of the thread's records
+    if (fused) {
+      unsigned long long f = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * kEmitThreads < ne && r[u].w == -2) f |= 1ull << (16 * u);
+      unsigned long long tot;
+      const unsigned long long ex = block_exclusive_scan(f, nscan, &tot);
+      int base = nrun;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        nb4[u] = base + (int)((ex >> (16 * u)) & 0xffff);
+        base += (int)((tot >> (16 * u)) & 0xffff);
+      }
+      nrun = base;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -581,6 +652,39 @@ __global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict
         out.ltm[e] = -1;
         if (out.pairs) out.pairs[2 * (int64_t)e + 1] = make_int2(-1, 0);
         out.boundary[bpos] = e;
+      }
+      if (fused) {  // classify_edges + assemble_constraint (edge_topology.cpp:165-173; assembly.cpp:144-168)
+        const bool neu = r[u].w == -2;
+        const int nl = nb4[u];
+        if (neu) {
+          out.rpos[e] = -1;
+        } else {
+          const int rp = e - nl;
+          const int rs = 4 * rp - 2 * (bpos - nl);  // retained boundary rows hold 2 entries
+          out.rpos[e] = rp;
+          out.redges[rp] = e;
+          out.row_ptr[rp] = rs;
+          const int a = (z & 1u) ? v : r[u].y, b = (z & 1u) ? r[u].y : v;
+          const double2 pa = out.coords[a], pb = out.coords[b];
+          const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+          const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
+          const int c0 = l_f == 0 ? 1 : 0, c1 = l_f == 2 ? 1 : 2;
+          const double vp = len * 0.5;  // assembly.cpp:160
+          *reinterpret_cast<int2*>(out.col + rs) = make_int2(3 * m_f + c0, 3 * m_f + c1);
+          __stcs(reinterpret_cast<double2*>(out.val + rs), make_double2(vp, vp));
+          int nn = 2;
+          if (r[u].w >= 0) {
+            const uint32_t occ_g = (uint32_t)r[u].w;
+            const int m_g = (int)(occ_g / 3u);
+            const int l_g = (int)((occ_g % 3u + 2u) % 3u);
+            const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
+            const double vm = -len * 0.5;  // assembly.cpp:164
+            *reinterpret_cast<int2*>(out.col + rs + 2) = make_int2(3 * m_g + d0, 3 * m_g + d1);
+            __stcs(reinterpret_cast<double2*>(out.val + rs + 2), make_double2(vm, vm));
+            nn = 4;
+          }
+          if (rp == out.L - 1) out.row_ptr[out.L] = rs + nn;
+        }
       }
     }
   }
@@ -619,9 +723,21 @@ namespace phfem {
 // (the whole mesh for build_topology, one rank's range for the distributed
 // dedup).  source(kind, ...) launches the histogram (kind 0) or the scatter
 // (kind 1) of the occurrences into the bucket array.
+// Fused classification + C of a sort-built topology (pipeline_impl): the
+// Neumann pairs' hash set in, retained arrays and C (CSR) out.
+struct EgFuse {
+  const unsigned long long* keys;
+  int cap;
+  const double* coords;
+  phfem_classification* cls;  // retained_pos / retained_edges allocated here, L set
+  phfem_csr* C;
+  int32_t nE;                 // elements (columns of C = 3 nE)
+};
+
 template <typename Source>
 static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source source,
-                            phfem_topology* out, int2* pairs, const char* who) {
+                            phfem_topology* out, int2* pairs, const char* who,
+                            const EgFuse* fuse = nullptr) {
   const int64_t nC = P.nC;
   const int64_t cap_e = std::max<int64_t>(nd, 1);
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
@@ -682,9 +798,27 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   }
   PHFEM_TRY(source(1, cursor, items));
 
-  EgOut o{out->edge_nodes, out->edge_elements, out->local_in_tplus, out->local_in_tminus,
-          out->interior_edges, out->boundary_edges, out->elem_edge, out->node_edge_start,
-          pairs, P.node_base};
+  EgOut o;
+  memset(&o, 0, sizeof o);
+  o.edge_nodes = out->edge_nodes;
+  o.edge_elements = out->edge_elements;
+  o.ltp = out->local_in_tplus;
+  o.ltm = out->local_in_tminus;
+  o.interior = out->interior_edges;
+  o.boundary = out->boundary_edges;
+  o.elem_edge = out->elem_edge;
+  o.node_edge_start = out->node_edge_start;
+  o.pairs = pairs;
+  o.node_base = P.node_base;
+  int32_t* tileN = nullptr;
+  if (fuse) {
+    PHFEM_TRY(dalloc(ctx, &tileN, (int64_t)ntiles + 2));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(tileN, 0, sizeof(int32_t) * (ntiles + 2), ctx->stream));
+    o.neu_keys = fuse->keys;
+    o.neu_cap = fuse->cap;
+    o.tileN = tileN;
+    o.coords = (const double2*)fuse->coords;
+  }
   EgParams PT = P;
   PT.nb = ntiles;
   const size_t smem = sizeof(TileSmem);
@@ -697,6 +831,35 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
       items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileE, tileE, (int64_t)ntiles + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, (int64_t)ntiles + 1, nullptr));
+  if (fuse) {  // sizes of the classification / C before the emit pass writes them
+    PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, (int64_t)ntiles + 1, nullptr));
+    int32_t h[3] = {0, 0, 0};
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[0], tileE + ntiles, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[1], tileB + ntiles, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[2], tileN + ntiles, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const int64_t E = h[0], nB = h[1], nneu = h[2];
+    const int64_t L = E - nneu;
+    phfem_classification* cls = fuse->cls;
+    phfem_csr* C = fuse->C;
+    cls->E = (int32_t)E;
+    cls->L = (int32_t)L;
+    PHFEM_TRY(dalloc(ctx, &cls->retained_pos, std::max<int64_t>(E, 1)));
+    PHFEM_TRY(dalloc(ctx, &cls->retained_edges, std::max<int64_t>(L, 1)));
+    C->rows = (int32_t)L;
+    C->cols = 3 * fuse->nE;
+    C->nnz = 4 * L - 2 * (nB - nneu);
+    PHFEM_TRY(dalloc(ctx, &C->row_ptr, L + 1));
+    PHFEM_TRY(dalloc(ctx, &C->col_idx, std::max<int64_t>(C->nnz, 1)));
+    PHFEM_TRY(dalloc(ctx, &C->values, std::max<int64_t>(C->nnz, 1)));
+    if (L == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
+    o.rpos = cls->retained_pos;
+    o.redges = cls->retained_edges;
+    o.row_ptr = C->row_ptr;
+    o.col = C->col_idx;
+    o.val = C->values;
+    o.L = (int)L;
+  }
   PHFEM_LAUNCH(ctx, "k_eg_emit", k_eg_emit<<<ntiles, kEmitThreads, 0, ctx->stream>>>(
       rec, boff, P.nb, nsub, tileE, tileB, (int)nC, o));
   // totals ride back with the error words (low 32 bits of counters 0 / 2)
@@ -712,6 +875,7 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   dfree(ctx, bcount);
   dfree(ctx, boff);
   dfree(ctx, tiles);
+  dfree(ctx, tileN);
   PHFEM_TRY(errors_fetch(ctx));
   const uint64_t te = ctx->herr->topo;
   if (te != ~0ull) {
@@ -798,3 +962,51 @@ PHFEM_API phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int
   };
   return eg_core(ctx, P, n, source, out, reinterpret_cast<int2*>(pairs), "dist_dedup");
 }
+
+namespace phfem {
+phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const phfem_mesh* mesh,
+                            phfem_classification* out, bool with_retained);
+
+// build_topology + classify_edges + assemble_constraint of a mesh in one
+// edge-generation pass (pipeline_impl's final, sort-built level): the emit
+// pass writes retained_pos / retained_edges and C's rows; classify_lists then
+// resolves the boundary pairs (the reference's errors) and must agree on L.
+phfem_status build_topology_fused(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_topology* out,
+                                  phfem_classification* cls, phfem_csr* C) {
+  memset(out, 0, sizeof(*out));
+  memset(cls, 0, sizeof(*cls));
+  memset(C, 0, sizeof(*C));
+  const int64_t nE = mesh->nE, nC = mesh->nC;
+  if (nE < 0 || nC < 0 || 3 * nE >= (int64_t(1) << 31))
+    return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: mesh too large for int ids");
+  out->nC = (int32_t)nC;
+  out->nE = (int32_t)nE;
+  int cap = 64;
+  while (cap < 2 * mesh->nN) cap <<= 1;
+  unsigned long long* keys = nullptr;
+  PHFEM_TRY(dalloc(ctx, &keys, cap));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(keys, 0xff, sizeof(unsigned long long) * cap, ctx->stream));
+  if (mesh->nN > 0)
+    PHFEM_LAUNCH(ctx, "k_neu_pair_insert", k_neu_pair_insert<<<grid_for(mesh->nN, 256, ctx->num_sms), 256, 0,
+                                                                ctx->stream>>>(mesh->neumann, mesh->nN, cap, keys));
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, nC, nC, nE, 0, &P));
+  const int grid_e = grid_for(nE, 256, ctx->num_sms * 8);
+  auto source = [&](int kind, int32_t* counts, uint64_t* items) -> phfem_status {
+    if (kind == 0)
+      PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, counts, ctx->derr));
+    else
+      PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, counts, items));
+    return PHFEM_OK;
+  };
+  EgFuse fuse{keys, cap, mesh->coords, cls, C, (int32_t)nE};
+  phfem_status st = eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology", &fuse);
+  dfree(ctx, keys);
+  if (st != PHFEM_OK) return st;
+  const int32_t L = cls->L;
+  PHFEM_TRY(classify_lists(ctx, out, mesh, cls, false));
+  if (cls->L != L)
+    return set_error(ctx, PHFEM_ERR_MISMATCH, "build_topology: fused classification disagrees (%d vs %d)", L, cls->L);
+  return PHFEM_OK;
+}
+}  // namespace phfem

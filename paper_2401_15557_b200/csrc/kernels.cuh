@@ -96,6 +96,9 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
 phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                   const phfem_topology* ptopo, const phfem_mesh* fine,
                                   phfem_topology* out, double* mid);
+// build_topology + classify_edges + assemble_constraint in one edge pass (edge_gen.cu)
+phfem_status build_topology_fused(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_topology* out,
+                                  phfem_classification* cls, phfem_csr* C);
 phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                const phfem_topology* ptopo, const phfem_classification* pcls,
                                const phfem_mesh* fine, phfem_topology* topo,

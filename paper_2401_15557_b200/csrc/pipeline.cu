@@ -42,13 +42,19 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   Trace tr(ctx);
   tr("start");
   phfem_topology topo;
-  phfem_status st = phfem_build_topology(ctx, &cur, &topo);
+  bool have_cls_C = false;
+  phfem_status st;
+  if (levels == 0) {  // the given mesh is the final one: classification + C fused into its edge pass
+    st = build_topology_fused(ctx, &cur, &topo, &out->cls, &out->C);
+    have_cls_C = st == PHFEM_OK;
+  } else {
+    st = phfem_build_topology(ctx, &cur, &topo);
+  }
   tr("build_topology");
   if (st != PHFEM_OK) {
     phfem_mesh_release(ctx, &cur);
     return st;
   }
-  bool have_cls_C = false;
   for (int l = 0; l < levels; ++l) {
     const bool last_fused = (l == levels - 1) && !(flags & PHFEM_PIPE_GENERIC_EG);
     phfem_classification pcls;
@@ -66,7 +72,12 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
     memset(&fine_topo, 0, sizeof fine_topo);
     if (st == PHFEM_OK) {
       if (flags & PHFEM_PIPE_GENERIC_EG) {
-        st = phfem_build_topology(ctx, &next, &fine_topo);
+        if (l == levels - 1) {  // final level, sort-built: classification + C fused too
+          st = build_topology_fused(ctx, &next, &fine_topo, &out->cls, &out->C);
+          have_cls_C = st == PHFEM_OK;
+        } else {
+          st = phfem_build_topology(ctx, &next, &fine_topo);
+        }
       } else if (last_fused) {
         st = refine_level_impl(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C, mid);
         have_cls_C = st == PHFEM_OK;
