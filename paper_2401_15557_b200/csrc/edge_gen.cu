@@ -579,7 +579,10 @@ __global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __rest
 // the final outputs at the scanned tile offsets — coalesced record reads and
 // edge-array writes; ids are canonical because tiles are max-node ranges.
 constexpr int kEmitThreads = kTileNodes;
-__global__ void __launch_bounds__(kEmitThreads) k_eg_emit(const int4* __restrict__ rec,
+#ifndef PHFEM_EMIT_MIN_BLOCKS
+#define PHFEM_EMIT_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit(const int4* __restrict__ rec,
                                                           const int32_t* __restrict__ boff,
                                                           int nbuckets, int nsub,
                                                           const int32_t* __restrict__ tileE,
