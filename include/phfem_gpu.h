@@ -387,6 +387,14 @@ phfem_status phfem_dist_midpoints(phfem_ctx* ctx, const double* coords, const in
 phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n, int32_t node_lo,
                               int32_t node_hi, int32_t nC_all, int32_t nE_all, phfem_topology* out,
                               int32_t* pairs);
+/* The same with the rank's own element range [self_lo, self_hi): their
+ * entries go straight into self_elem_edge ([self_hi - self_lo][3], LOCAL ids
+ * e / ~e: re-base with phfem_dist_add_offset(..., 2)); pairs then holds only
+ * the *n_pairs entries of other ranks' elements (compact, any order).       */
+phfem_status phfem_dist_dedup_ex(phfem_ctx* ctx, const int32_t* recs, int64_t n, int32_t node_lo,
+                                 int32_t node_hi, int32_t nC_all, int32_t nE_all, int32_t self_lo,
+                                 int32_t self_hi, int32_t* self_elem_edge, phfem_topology* out,
+                                 int32_t* pairs, int64_t* n_pairs);
 /* pairs -> global edge ids (+E0) routed to the element owner (esplits[W+1]);
  * the receiver writes them into its elem_edge ([3(ehi-elo)]).  Pairs of the
  * caller's own elements [self_lo, self_hi) are written to self_elem_edge
@@ -397,7 +405,8 @@ phfem_status phfem_dist_route_pairs(phfem_ctx* ctx, const int32_t* pairs, int64_
                                     int32_t self_hi, int32_t* self_elem_edge);
 phfem_status phfem_dist_apply_pairs(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t elo,
                                     int32_t* elem_edge);
-/* a[i] += off (only_nonneg: where a[i] >= 0) — re-basing local ids         */
+/* a[i] += off (only_nonneg 1: where a[i] >= 0; 2: signed ids e / ~e, i.e.
+ * e + off or ~(~a[i] + off)) — re-basing local ids                          */
 phfem_status phfem_dist_add_offset(phfem_ctx* ctx, int32_t* a, int64_t n, int32_t off,
                                    int only_nonneg);
 /* boundary pairs (global list, positions list_base..) whose max node this
@@ -511,6 +520,20 @@ phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart
                                      const int32_t* neu_parent_ids, int32_t nN_parent,
                                      phfem_topology* out, int32_t** pairs_out, double* mids,
                                      phfem_csr* C);
+/* The same with the rank's own FINE element range [self_lo, self_hi): their
+ * elem_edge entries are written straight into self_elem_edge
+ * ([self_hi - self_lo][3], LOCAL ids f / ~f: re-base with
+ * phfem_dist_add_offset(..., 2) once the rank's fine edge offset is known);
+ * *pairs_out then holds only the *n_pairs pairs of other ranks' elements
+ * (compact, any order) for phfem_dist_route_pairs.                          */
+phfem_status phfem_dist_refine_level_ex(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                        const int32_t* elem_edge_all, const int32_t* elements_all,
+                                        int32_t nE_all, const double* coords, int32_t nc,
+                                        int32_t node_lo, int32_t node_hi,
+                                        const int32_t* neu_parent_ids, int32_t nN_parent,
+                                        int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge,
+                                        phfem_topology* out, int32_t** pairs_out, int64_t* n_pairs,
+                                        double* mids, phfem_csr* C);
 
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'

@@ -173,7 +173,8 @@ EXPORTED = [
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
     "phfem_mesh_load_text", "phfem_mesh_load_dir", "phfem_mesh_format", "phfem_mesh_save_dir",
     "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free", "phfem_dist_refine_level",
-    "phfem_assemble_volume_load", "phfem_format_g", "phfem_format_g_host",
+    "phfem_assemble_volume_load", "phfem_format_g", "phfem_format_g_host", "phfem_dist_refine_level_ex",
+    "phfem_dist_dedup_ex",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -291,6 +292,11 @@ def load_library(path: str = LIB_PATH):
                                                  vp, vp, vp, vp, vp]),
         "phfem_dist_refine_level": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, vp, i32, i32, i32,
                                               vp, i32, P(phfem_topology), P(vp), vp, P(phfem_csr)]),
+        "phfem_dist_dedup_ex": (C.c_int, [vp, vp, i64, i32, i32, i32, i32, i32, i32, vp, P(phfem_topology),
+                                          vp, P(i64)]),
+        "phfem_dist_refine_level_ex": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, vp, i32, i32, i32,
+                                                 vp, i32, i32, i32, vp, P(phfem_topology), P(vp), P(i64), vp,
+                                                 P(phfem_csr)]),
         "phfem_mesh_save_dir": (C.c_int, [vp, P(phfem_mesh), C.c_char_p]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),

@@ -45,12 +45,20 @@ __device__ __forceinline__ void route_block(int64_t n, int W, Fn item_of, int32_
     __syncthreads();
     Item it[kRouteK];
     int dst[kRouteK], rk[kRouteK];
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < kRouteK; ++k) {
       const int64_t i = c0 + (int64_t)k * kRouteThreads + threadIdx.x;
       dst[k] = -1;
       if (i < n) dst[k] = item_of(i, it[k]);
-      rk[k] = dst[k] >= 0 ? atomicAdd(&s_cnt[dst[k]], 1) : 0;
+      // warp-aggregated: one SMEM atomic per (warp, destination) — with few
+      // destinations every lane would otherwise hit the same counter
+      const unsigned peers = __match_any_sync(0xffffffffu, dst[k]);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (lane == leader && dst[k] >= 0) base = atomicAdd(&s_cnt[dst[k]], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      rk[k] = base + __popc(peers & ((1u << lane) - 1u));
     }
     __syncthreads();
     for (int d = threadIdx.x; d < W; d += blockDim.x) {
@@ -120,7 +128,8 @@ __global__ void k_add_offset(int32_t* __restrict__ a, int64_t n, int32_t off, in
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = a[i];
-    if (!only_nonneg || v >= 0) a[i] = v + off;
+    if (only_nonneg == 2) a[i] = v >= 0 ? v + off : v - off;  // signed ids e / ~e
+    else if (!only_nonneg || v >= 0) a[i] = v + off;
   }
 }
 

@@ -166,6 +166,11 @@ struct EgOut {
   int32_t* elem_edge;
   int32_t* node_edge_start;
   int2* pairs;  // non-null: (slot 3m+l, edge or ~edge) per occurrence instead of elem_edge
+  // with pairs: slots [self_lo3, self_hi3) of the rank's own elements go to
+  // self_ee directly, only the others are appended to pairs (count npairs)
+  int32_t* self_ee;
+  int64_t self_lo3, self_hi3;
+  int32_t* npairs;
   int32_t node_base;
   // fused classification + C (sort-built final topology, pipeline): the
   // Neumann pairs as a hash set of (min << 32 | max) keys; retained_pos /
@@ -181,6 +186,28 @@ struct EgOut {
   const double2* coords;
   int L;
 };
+
+// the elem_edge entries of edge e: slot s0 <- e (T+), s1 <- ~e (T-; s1 < 0: none)
+__device__ __forceinline__ void eg_slots(const EgOut& o, int32_t e, int64_t s0, int64_t s1) {
+  if (o.self_ee) {
+    const bool own0 = s0 >= o.self_lo3 && s0 < o.self_hi3;
+    const bool own1 = s1 < 0 || (s1 >= o.self_lo3 && s1 < o.self_hi3);
+    if (own0) o.self_ee[s0 - o.self_lo3] = e;
+    if (s1 >= 0 && own1) o.self_ee[s1 - o.self_lo3] = ~e;
+    const int k = (own0 ? 0 : 1) + (own1 ? 0 : 1);
+    if (k) {
+      int at = atomicAdd(o.npairs, k);
+      if (!own0) o.pairs[at++] = make_int2((int)s0, e);
+      if (!own1) o.pairs[at] = make_int2((int)s1, ~e);
+    }
+  } else if (o.pairs) {
+    o.pairs[2 * (int64_t)e] = make_int2((int)s0, e);
+    o.pairs[2 * (int64_t)e + 1] = s1 >= 0 ? make_int2((int)s1, ~e) : make_int2(-1, 0);
+  } else {
+    o.elem_edge[s0] = e;
+    if (s1 >= 0) o.elem_edge[s1] = ~e;
+  }
+}
 
 __device__ __forceinline__ uint32_t neu_pair_hash(unsigned long long key, int cap) {
   return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32) & (uint32_t)(cap - 1);
@@ -639,21 +666,18 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
       const int l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
       reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(v, r[u].y) : make_int2(r[u].y, v);
       out.ltp[e] = l_f;
-      if (out.pairs) out.pairs[2 * (int64_t)e] = make_int2(3 * m_f + l_f, e);
-      else out.elem_edge[3 * (int64_t)m_f + l_f] = e;
       if (r[u].w >= 0) {
         const uint32_t occ_g = (uint32_t)r[u].w;
         const int m_g = (int)(occ_g / 3u);
         const int l_g = (int)((occ_g % 3u + 2u) % 3u);
         reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
         out.ltm[e] = l_g;
-        if (out.pairs) out.pairs[2 * (int64_t)e + 1] = make_int2(3 * m_g + l_g, ~e);
-        else out.elem_edge[3 * (int64_t)m_g + l_g] = ~e;
+        eg_slots(out, e, 3 * (int64_t)m_f + l_f, 3 * (int64_t)m_g + l_g);
         out.interior[e - bpos] = e;
       } else {
         reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
         out.ltm[e] = -1;
-        if (out.pairs) out.pairs[2 * (int64_t)e + 1] = make_int2(-1, 0);
+        eg_slots(out, e, 3 * (int64_t)m_f + l_f, -1);
         out.boundary[bpos] = e;
       }
       if (fused) {  // classify_edges + assemble_constraint (edge_topology.cpp:165-173; assembly.cpp:144-168)
@@ -737,10 +761,17 @@ struct EgFuse {
   int32_t nE;                 // elements (columns of C = 3 nE)
 };
 
+// the rank's own element slots of a distributed dedup (eg_slots)
+struct EgOwn {
+  int32_t* ee;
+  int64_t lo3, hi3;
+  int32_t* npairs;  // device counter, zeroed by the caller
+};
+
 template <typename Source>
 static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source source,
                             phfem_topology* out, int2* pairs, const char* who,
-                            const EgFuse* fuse = nullptr) {
+                            const EgFuse* fuse = nullptr, const EgOwn* own = nullptr) {
   const int64_t nC = P.nC;
   const int64_t cap_e = std::max<int64_t>(nd, 1);
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
@@ -812,6 +843,12 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   o.elem_edge = out->elem_edge;
   o.node_edge_start = out->node_edge_start;
   o.pairs = pairs;
+  if (own) {
+    o.self_ee = own->ee;
+    o.self_lo3 = own->lo3;
+    o.self_hi3 = own->hi3;
+    o.npairs = own->npairs;
+  }
   o.node_base = P.node_base;
   int32_t* tileN = nullptr;
   if (fuse) {
@@ -943,13 +980,18 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
   return eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology");
 }
 
-PHFEM_API phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n,
-                                        int32_t node_lo, int32_t node_hi, int32_t nC_all,
-                                        int32_t nE_all, phfem_topology* out, int32_t* pairs) {
+PHFEM_API phfem_status phfem_dist_dedup_ex(phfem_ctx* ctx, const int32_t* recs, int64_t n,
+                                           int32_t node_lo, int32_t node_hi, int32_t nC_all,
+                                           int32_t nE_all, int32_t self_lo, int32_t self_hi,
+                                           int32_t* self_elem_edge, phfem_topology* out, int32_t* pairs,
+                                           int64_t* n_pairs) {
   memset(out, 0, sizeof(*out));
   if (!ctx || (!recs && n) || !pairs || node_lo < 0 || node_hi < node_lo || node_hi > nC_all ||
       3 * (int64_t)nE_all >= (int64_t(1) << 31))
     return PHFEM_ERR_INVALID_ARGUMENT;
+  if (self_elem_edge && (self_lo < 0 || self_hi < self_lo || self_hi > nE_all || !n_pairs))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n_pairs) *n_pairs = 0;
   out->nC = node_hi - node_lo;
   out->nE = nE_all;
   EgParams P;
@@ -963,7 +1005,30 @@ PHFEM_API phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int
       PHFEM_LAUNCH(ctx, "k_rec_scatter", k_rec_scatter<<<grid_r, 256, 0, ctx->stream>>>(r4, n, P, counts, items));
     return PHFEM_OK;
   };
-  return eg_core(ctx, P, n, source, out, reinterpret_cast<int2*>(pairs), "dist_dedup");
+  if (!self_elem_edge) {
+    PHFEM_TRY(eg_core(ctx, P, n, source, out, reinterpret_cast<int2*>(pairs), "dist_dedup"));
+    if (n_pairs) *n_pairs = 2 * (int64_t)out->E;
+    return PHFEM_OK;
+  }
+  EgOwn own{self_elem_edge, 3 * (int64_t)self_lo, 3 * (int64_t)self_hi, nullptr};
+  PHFEM_TRY(dalloc(ctx, &own.npairs, 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(own.npairs, 0, sizeof(int32_t), ctx->stream));
+  phfem_status st = eg_core(ctx, P, n, source, out, reinterpret_cast<int2*>(pairs), "dist_dedup", nullptr, &own);
+  int32_t np = 0;
+  if (st == PHFEM_OK) {
+    if (cudaMemcpyAsync(&np, own.npairs, sizeof np, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      st = cuda_fail(ctx, cudaGetLastError(), "dist_dedup: pair count");
+  }
+  dfree(ctx, own.npairs);
+  *n_pairs = np;
+  return st;
+}
+
+PHFEM_API phfem_status phfem_dist_dedup(phfem_ctx* ctx, const int32_t* recs, int64_t n,
+                                        int32_t node_lo, int32_t node_hi, int32_t nC_all,
+                                        int32_t nE_all, phfem_topology* out, int32_t* pairs) {
+  return phfem_dist_dedup_ex(ctx, recs, n, node_lo, node_hi, nC_all, nE_all, 0, 0, nullptr, out, pairs, nullptr);
 }
 
 namespace phfem {

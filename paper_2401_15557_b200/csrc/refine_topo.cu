@@ -84,6 +84,11 @@ struct LvOut {
   double2* mid;  // nullable: mid[nc + e - mid_base] = midpoint of parent edge e
   int64_t mid_base;
   int2* pairs;   // distributed level: (slot 3m+l, f / ~f) per fine edge instead of elem_edge
+  // distributed level with an own range: slots [self_lo3, self_hi3) go to
+  // self_ee directly (local f / ~f); only the others are appended to pairs
+  int32_t* self_ee;
+  int64_t self_lo3, self_hi3;
+  int32_t* npairs;
   // kFull
   int32_t* rpos;
   int32_t* redges;
@@ -307,7 +312,20 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
     const int sl = ms >> 8;  // arithmetic shift: boundary slots stay negative
     if (sl < 0) o.boundary[off_bnd + ~sl] = f;
     else o.interior[off_int + sl] = f;
-    if (o.pairs) {  // distributed: to the owners of the fine elements (coalesced)
+    if (o.self_ee) {  // distributed, own fine elements written in place
+      const int64_t s0 = 3 * (int64_t)el2.x + lp;
+      const int64_t s1 = lm >= 0 ? 3 * (int64_t)el2.y + lm : -1;
+      const bool own0 = s0 >= o.self_lo3 && s0 < o.self_hi3;
+      const bool own1 = s1 < 0 || (s1 >= o.self_lo3 && s1 < o.self_hi3);
+      if (own0) o.self_ee[s0 - o.self_lo3] = f;
+      if (s1 >= 0 && own1) o.self_ee[s1 - o.self_lo3] = ~f;
+      const int k = (own0 ? 0 : 1) + (own1 ? 0 : 1);
+      if (k) {  // to the owners of the other fine elements
+        int at = atomicAdd(o.npairs, k);
+        if (!own0) o.pairs[at++] = make_int2((int)s0, f);
+        if (!own1) o.pairs[at] = make_int2((int)s1, ~f);
+      }
+    } else if (o.pairs) {  // distributed: to the owners of the fine elements (coalesced)
       o.pairs[2 * (int64_t)f] = make_int2(3 * el2.x + lp, f);
       o.pairs[2 * (int64_t)f + 1] = lm >= 0 ? make_int2(3 * el2.y + lm, ~f) : make_int2(-1, 0);
     } else {
@@ -542,14 +560,19 @@ __global__ void k_rl_neu_bits(const int32_t* __restrict__ ids, int n, int E0, in
   }
 }
 
-PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
-                                               const int32_t* elem_edge_all, const int32_t* elements_all,
-                                               int32_t nE_all, const double* coords, int32_t nc,
-                                               int32_t node_lo, int32_t node_hi,
-                                               const int32_t* neu_parent_ids, int32_t nN_parent,
-                                               phfem_topology* out, int32_t** pairs_out, double* mids,
-                                               phfem_csr* C) {
+PHFEM_API phfem_status phfem_dist_refine_level_ex(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                                  const int32_t* elem_edge_all, const int32_t* elements_all,
+                                                  int32_t nE_all, const double* coords, int32_t nc,
+                                                  int32_t node_lo, int32_t node_hi,
+                                                  const int32_t* neu_parent_ids, int32_t nN_parent,
+                                                  int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge,
+                                                  phfem_topology* out, int32_t** pairs_out, int64_t* n_pairs,
+                                                  double* mids, phfem_csr* C) {
   if (!ctx || !ppart || !out || !pairs_out) return PHFEM_ERR_INVALID_ARGUMENT;
+  const bool own = self_elem_edge != nullptr;
+  if (own && (self_lo < 0 || self_hi < self_lo || (int64_t)self_hi > 4 * (int64_t)nE_all || !n_pairs))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n_pairs) *n_pairs = 0;
   memset(out, 0, sizeof(*out));
   if (C) memset(C, 0, sizeof(*C));
   *pairs_out = nullptr;
@@ -562,10 +585,10 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
   const int64_t ntiles = std::max<int64_t>(1, (E + kLvT - 1) / kLvT);
   const int64_t nwords = std::max<int64_t>(1, (E + 31) / 32);
   int32_t* tiles = nullptr;
-  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1) + 2));
+  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1) + 3));
   int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
   int32_t* total = tiles + 3 * (ntiles + 1);  // [0] fine edges, [1] parent Neumann edges
-  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 2), ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 3), ctx->stream));
   uint32_t* nbits = nullptr;
   if (C) {  // the fused variant: classification bits of the owned parent edges
     PHFEM_TRY(dalloc(ctx, &nbits, nwords));
@@ -646,6 +669,12 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
     o.mid = (double2*)mids;
     o.mid_base = (int64_t)nc + E0p;
     o.pairs = reinterpret_cast<int2*>(pairs);
+    if (own) {
+      o.self_ee = self_elem_edge;
+      o.self_lo3 = 3 * (int64_t)self_lo;
+      o.self_hi3 = 3 * (int64_t)self_hi;
+      o.npairs = total + 2;
+    }
     const unsigned nt = (unsigned)((E + kLvT - 1) / kLvT);
     if (C) {
       a.neu_bits = nbits;
@@ -659,8 +688,28 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
       PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<nt, kLvT, lv_smem_bytes<false>(), ctx->stream>>>(a, o));
     }
   }
+  if (own) {  // the count of pairs for other ranks
+    int32_t np = 0;
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(&np, total + 2, sizeof np, cudaMemcpyDeviceToHost, ctx->stream));
+    PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *n_pairs = np;
+  } else if (n_pairs) {
+    *n_pairs = 2 * (int64_t)Ef;
+  }
   dfree(ctx, nbits);
   dfree(ctx, tiles);
   *pairs_out = pairs;
   return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                               const int32_t* elem_edge_all, const int32_t* elements_all,
+                                               int32_t nE_all, const double* coords, int32_t nc,
+                                               int32_t node_lo, int32_t node_hi,
+                                               const int32_t* neu_parent_ids, int32_t nN_parent,
+                                               phfem_topology* out, int32_t** pairs_out, double* mids,
+                                               phfem_csr* C) {
+  return phfem_dist_refine_level_ex(ctx, ppart, E0p, elem_edge_all, elements_all, nE_all, coords, nc, node_lo,
+                                    node_hi, neu_parent_ids, nN_parent, 0, 0, nullptr, out, pairs_out, nullptr,
+                                    mids, C);
 }

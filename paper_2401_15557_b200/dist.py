@@ -144,6 +144,7 @@ class CudaRankOps:
 
     def __init__(self, ctx: capi.Context, device):
         self.ctx, self.lib, self.dev = ctx, ctx.lib, torch.device(device)
+        self._ee_next = None  # the next level's elem_edge of the own elements
 
     def _ck(self, st):
         self.ctx.check(st)
@@ -182,38 +183,54 @@ class CudaRankOps:
                                                  self.p(cnt), self.p(off), self.p(send)))
         return send[:3 * (ehi - elo)], cnt.tolist()
 
-    def dedup(self, recv, nlo, nhi, nC, nE):
+    def dedup(self, recv, nlo, nhi, nC, nE, own_range=None):
+        """own_range = the rank's elements [lo, hi): their elem_edge entries are
+        written in place (local ids, re-based in route_pairs); only the other
+        ranks' entries leave as pairs."""
         n = recv.shape[0]
         pairs = self.empty((max(2 * n, 1), 2))
         t = capi.phfem_topology()
-        self._ck(self.lib.phfem_dist_dedup(self.ctx.ptr, self.p(recv), n, nlo, nhi, nC, nE, C.byref(t),
-                                           self.p(pairs)))
+        npairs = C.c_int64(0)
+        lo, hi = own_range if own_range is not None else (0, 0)
+        ee = self.empty((max(hi - lo, 1), 3)) if own_range is not None else None
+        self._ck(self.lib.phfem_dist_dedup_ex(self.ctx.ptr, self.p(recv), n, nlo, nhi, nC, nE, lo, hi,
+                                              self.p(ee) if ee is not None else None, C.byref(t), self.p(pairs),
+                                              C.byref(npairs)))
         self.part = capi.Topology(self.ctx, t)
-        self.pairs = pairs[:2 * t.E]
-        self._pairs = (pairs.data_ptr(), 2 * int(t.E), False)
+        self.pairs = pairs[:int(npairs.value)]
+        self._pairs = (pairs.data_ptr(), int(npairs.value), False)
+        self._ee_next = ee[:hi - lo] if ee is not None else None
         return int(t.E), int(t.n_boundary)
 
-    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None):
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None, fine_range=None):
         """The rank's part of the refined topology from its parent part (sort
-        free, phfem_dist_refine_level); returns (E, n_boundary, midpoints).
-        neu_parent (global parent Neumann ids): also the rank's C rows, fused."""
+        free, phfem_dist_refine_level_ex); returns (E, n_boundary, midpoints).
+        neu_parent (global parent Neumann ids): also the rank's C rows, fused.
+        fine_range = the rank's fine elements [lo, hi): their elem_edge entries
+        are written in place (local ids, re-based in route_pairs), only the
+        other ranks' entries leave as pairs."""
         t = capi.phfem_topology()
         pairs = C.c_void_p()
+        npairs = C.c_int64(0)
         pt = self.part.t
         Ep = int(pt.E)  # (the parent part is released below)
         mids = self.empty((max(Ep, 1), 2), torch.float64)
         csr = capi.phfem_csr() if neu_parent is not None else None
         nN = 0 if neu_parent is None else int(neu_parent.numel())
-        self._ck(self.lib.phfem_dist_refine_level(self.ctx.ptr, C.byref(pt), E0p, self.p(ee_all), self.p(el_all),
-                                                  nE_all, self.p(coords), nc, nlo, nhi,
-                                                  self.p(neu_parent) if nN else None, nN, C.byref(t),
-                                                  C.byref(pairs), self.p(mids),
-                                                  C.byref(csr) if csr is not None else None))
+        lo, hi = fine_range if fine_range is not None else (0, 0)
+        ee = self.empty((max(hi - lo, 1), 3)) if fine_range is not None else None
+        self._ck(self.lib.phfem_dist_refine_level_ex(self.ctx.ptr, C.byref(pt), E0p, self.p(ee_all),
+                                                     self.p(el_all), nE_all, self.p(coords), nc, nlo, nhi,
+                                                     self.p(neu_parent) if nN else None, nN, lo, hi,
+                                                     self.p(ee) if ee is not None else None, C.byref(t),
+                                                     C.byref(pairs), C.byref(npairs), self.p(mids),
+                                                     C.byref(csr) if csr is not None else None))
         if csr is not None:
             self.csr = csr
         self.part.release()
         self.part = capi.Topology(self.ctx, t)
-        self._pairs = (pairs.value, 2 * int(t.E), True)
+        self._pairs = (pairs.value, int(npairs.value), True)
+        self._ee_next = ee[:hi - lo] if ee is not None else None
         return int(t.E), int(t.n_boundary), mids[:Ep]
 
     def route_pairs(self, E0, esplits, elo, ehi):
@@ -223,7 +240,10 @@ class CudaRankOps:
         ptr, n, owned = self._pairs
         cnt, off = self.empty(W), self.empty(W + 1)
         send = self.empty((max(n, 1), 2))
-        self._ee_next = self.empty((ehi - elo, 3))
+        if self._ee_next is None:
+            self._ee_next = self.empty((ehi - elo, 3))
+        elif E0 and ehi > elo:  # written in place by the level kernel with local ids
+            self.rebase(self._ee_next.data_ptr(), 3 * (ehi - elo), E0, 2)
         self._ck(self.lib.phfem_dist_route_pairs(self.ctx.ptr, C.c_void_p(ptr) if n else None, n, E0,
                                                  self.p(esplits), W, self.p(cnt), self.p(off), self.p(send), elo, ehi,
                                                  self.p(self._ee_next)))
@@ -386,7 +406,12 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
     nb = max(1, min(nbins_per_rank * W, 4096, nC))  # key ranges balanced to ~1/64 of a share
     bins = np.asarray([nC * i // nb for i in range(nb + 1)], dtype=np.int32)
     # coarse histogram of max nodes -> balanced key ranges (identical on every rank)
-    hists = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(bins), pack=False) for s in states]
+    # the key ranges only balance the work (no output depends on them): a
+    # 1/8 sample of the own elements is enough for the coarse histogram
+    S = 8 if nE >= (1 << 20) else 1
+    smp = [s.elements[::S].contiguous() if S > 1 else s.elements for s in states]
+    hists = [s.ops.occurrences(e, 0, int(e.shape[0]), s.ops.as_tensor(bins), pack=False)
+             for s, e in zip(states, smp)]
     comm.all_reduce(hists, "sum")
     splits = balanced_splits(hists[0].cpu().numpy(), bins, W)
     tr("hist")
@@ -398,7 +423,7 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
     eb = []
     for s, rv in zip(states, recvs):
         r = s.rank
-        E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE)
+        E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE, own_range=(s.elo, s.ehi))
         eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
     tr("dedup")
     gath = comm.all_gather(eb)
@@ -495,7 +520,8 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     for s, (E0, _), ea, la, i in zip(states, per, ee_all, el_all, ids):
         r = s.rank
         neu = i[nD:].to(torch.int32).contiguous() if fused_c else None
-        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, neu)
+        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, neu,
+                                       fine_range=(4 * s.elo, 4 * s.ehi))
         counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
         mids.append(m)
     tr("level")

@@ -88,7 +88,7 @@ class NumpyRankOps:
         rec = np.stack([hi, lo, occ, (a > b).astype(np.int64)], 1)[order].astype(np.int32)
         return torch.as_tensor(rec), cnt.tolist()
 
-    def dedup(self, recv, nlo, nhi, nC, nE):
+    def dedup(self, recv, nlo, nhi, nC, nE, own_range=None):
         r = recv.numpy().astype(np.int64).reshape(-1, 4)
         order = np.lexsort((r[:, 2], r[:, 1], r[:, 0]))   # (max, min, occurrence)
         r = r[order]
@@ -127,7 +127,7 @@ class NumpyRankOps:
         self.pairs = pairs
         return E, int((~two).sum())
 
-    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None):
+    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None, fine_range=None):
         """Groups of the own parent edges e: the two halves (the one at the
         smaller old node first), then the interior edges mu(e') - mu(e) for the
         partners e' < e of e's elements, ascending e'."""
