@@ -36,6 +36,10 @@
 //      the retained positions, retained list, CSR rows of C and their
 //      (column, value) entries (assembly.cpp:144-168) are emitted in the
 //      same pass (the fine Neumann edges are the halves of the parent's).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace phfem {
@@ -171,57 +175,97 @@ __global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE, i
 #ifndef PHFEM_LV_MIN_BLOCKS
 #define PHFEM_LV_MIN_BLOCKS 7
 #endif
+// stage 1: the parent edge record (coalesced)
+struct LvRec {
+  int2 ab, el;
+  int l, l2;
+  bool neu;
+};
+// stage 2: the gathers of the two parent elements (edges, opposite vertices)
+struct LvGat {
+  int P[3], Q[3];
+  int vop, vom;
+};
+// stage 3: the four parent coordinates
+struct LvCrd {
+  double2 ca, cb, cop, com;
+};
+
 template <bool kFull>
-__global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a, LvOut o) {
-  extern __shared__ __align__(16) unsigned char lv_smem[];  // dynamic: tiles may exceed 48 KB
-  LvSmem<kFull>& s = *reinterpret_cast<LvSmem<kFull>*>(lv_smem);
+__device__ __forceinline__ LvRec lv_load_rec(const LvArgs& a, int le) {
+  LvRec r;
+  r.ab = make_int2(0, 0);
+  r.el = make_int2(0, -1);
+  r.l = r.l2 = 0;
+  r.neu = false;
+  if (le < a.E) {
+    r.ab = reinterpret_cast<const int2*>(a.edge_nodes)[le];
+    r.el = reinterpret_cast<const int2*>(a.edge_elements)[le];
+    r.l = __ldg(a.ltp + le);
+    r.l2 = __ldg(a.ltm + le);  // -1 on the boundary
+    if (kFull) r.neu = (__ldg(a.neu_bits + (le >> 5)) >> (le & 31)) & 1u;
+  }
+  return r;
+}
+
+__device__ __forceinline__ LvGat lv_load_gat(const LvArgs& a, const LvRec& r, bool valid) {
+  LvGat g;
+  g.P[0] = g.P[1] = g.P[2] = g.Q[0] = g.Q[1] = g.Q[2] = 0;
+  g.vop = g.vom = 0;
+  if (valid) {
+    const int tp = r.el.x;
+    g.P[0] = __ldg(a.elem_edge + 3 * (int64_t)tp);
+    g.P[1] = __ldg(a.elem_edge + 3 * (int64_t)tp + 1);
+    g.P[2] = __ldg(a.elem_edge + 3 * (int64_t)tp + 2);
+    g.vop = __ldg(a.elements + 3 * (int64_t)tp + r.l);
+  }
+  if (valid && r.el.y >= 0) {
+    const int tm = r.el.y;
+    g.Q[0] = __ldg(a.elem_edge + 3 * (int64_t)tm);
+    g.Q[1] = __ldg(a.elem_edge + 3 * (int64_t)tm + 1);
+    g.Q[2] = __ldg(a.elem_edge + 3 * (int64_t)tm + 2);
+    g.vom = __ldg(a.elements + 3 * (int64_t)tm + r.l2);
+  }
+  return g;
+}
+
+__device__ __forceinline__ LvCrd lv_load_crd(const LvArgs& a, const LvRec& r, const LvGat& g, bool valid) {
+  LvCrd c;
+  c.ca = c.cb = c.cop = c.com = make_double2(0.0, 0.0);
+  if (valid) {
+    c.ca = __ldg(a.coords + r.ab.x);
+    c.cb = __ldg(a.coords + r.ab.y);
+    c.cop = __ldg(a.coords + g.vop);
+  }
+  if (valid && r.el.y >= 0) c.com = __ldg(a.coords + g.vom);
+  return c;
+}
+
+// One tile of 128 parent edges from its three load stages: group sizes, the
+// packed block scan, fine edges into SMEM, coalesced stores.
+template <bool kFull>
+__device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<kFull>& s, int tile,
+                                        const LvRec& r, const LvGat& g, const LvCrd& c) {
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
   const int64_t e0 = (int64_t)tile * kLvT;
   const int le = (int)(e0 + tid);  // index into the parent edge arrays
   const int e = a.eb + le;         // global parent edge id
   const bool valid = le < a.E;
-
-  // 1. the parent edge record (coalesced) and the element gathers
-  int2 ab = make_int2(0, 0), el = make_int2(0, -1);
-  int l = 0, l2 = 0;
-  bool neu = false;
-  if (valid) {
-    ab = reinterpret_cast<const int2*>(a.edge_nodes)[le];
-    el = reinterpret_cast<const int2*>(a.edge_elements)[le];
-    l = __ldg(a.ltp + le);
-    if (kFull) neu = (__ldg(a.neu_bits + (le >> 5)) >> (le & 31)) & 1u;
-  }
-  const bool has_m = valid && el.y >= 0;
-  if (has_m) l2 = __ldg(a.ltm + le);
-  const int tp = el.x, tm = el.y;
-  int P[3] = {0, 0, 0}, Q[3] = {0, 0, 0};
-  int vop = 0, vom = 0;
-  if (valid) {
-    P[0] = __ldg(a.elem_edge + 3 * (int64_t)tp);
-    P[1] = __ldg(a.elem_edge + 3 * (int64_t)tp + 1);
-    P[2] = __ldg(a.elem_edge + 3 * (int64_t)tp + 2);
-    vop = __ldg(a.elements + 3 * (int64_t)tp + l);
-  }
-  if (has_m) {
-    Q[0] = __ldg(a.elem_edge + 3 * (int64_t)tm);
-    Q[1] = __ldg(a.elem_edge + 3 * (int64_t)tm + 1);
-    Q[2] = __ldg(a.elem_edge + 3 * (int64_t)tm + 2);
-    vom = __ldg(a.elements + 3 * (int64_t)tm + l2);
-  }
-  double2 ca = make_double2(0.0, 0.0), cb = ca, cop = ca, com = ca;
-  if (valid) {
-    ca = __ldg(a.coords + ab.x);
-    cb = __ldg(a.coords + ab.y);
-    cop = __ldg(a.coords + vop);
-  }
-  if (has_m) com = __ldg(a.coords + vom);
+  const int2 ab = r.ab;
+  const int l = r.l;
+  const bool neu = r.neu;
+  const bool has_m = valid && r.el.y >= 0;
+  const int l2 = has_m ? r.l2 : 0;
+  const int tp = r.el.x, tm = r.el.y;
+  const double2 ca = c.ca, cb = c.cb, cop = c.cop, com = c.com;
 
   // 2. group size, tile scan, look-back
   const int j1 = l == 2 ? 0 : l + 1, j2 = l == 0 ? 2 : l - 1;      // partners in t_plus
   const int k1 = l2 == 2 ? 0 : l2 + 1, k2 = l2 == 0 ? 2 : l2 - 1;  // partners in t_minus
-  const int q0 = abs_edge(P[j1]), q1 = abs_edge(P[j2]);
-  const int r0 = abs_edge(Q[k1]), r1 = abs_edge(Q[k2]);
+  // (selects, not indexing: keeps the gathered edges in registers)
+  auto pick = [](const int (&v)[3], int i) { return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]); };
+  const int q0 = abs_edge(pick(g.P, j1)), q1 = abs_edge(pick(g.P, j2));
+  const int r0 = abs_edge(pick(g.Q, k1)), r1 = abs_edge(pick(g.Q, k2));
   const bool v0 = valid && q0 < e, v1 = valid && q1 < e;
   const bool v2 = has_m && r0 < e, v3 = has_m && r1 < e;
   const bool isB = valid && !has_m;
@@ -360,7 +404,20 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   }
 }
 
-// dynamic SMEM of the level kernel (opt-in above 48 KB, set once per variant)
+// One tile per CTA: the three load stages back to back.
+template <bool kFull>
+__global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a, LvOut o) {
+  extern __shared__ __align__(16) unsigned char lv_smem[];  // dynamic: tiles may exceed 48 KB
+  LvSmem<kFull>& s = *reinterpret_cast<LvSmem<kFull>*>(lv_smem);
+  const int le = blockIdx.x * kLvT + threadIdx.x;
+  const bool valid = le < a.E;
+  const LvRec r = lv_load_rec<kFull>(a, le);
+  const LvGat g = lv_load_gat(a, r, valid);
+  const LvCrd c = lv_load_crd(a, r, g, valid);
+  lv_tile<kFull>(a, o, s, blockIdx.x, r, g, c);
+}
+
+// dynamic SMEM of the level kernels (opt-in above 48 KB, set once per variant)
 template <bool kFull>
 static size_t lv_smem_bytes() {
   static bool set = false;
@@ -370,6 +427,17 @@ static size_t lv_smem_bytes() {
     set = true;
   }
   return sizeof(LvSmem<kFull>);
+}
+
+// The level kernel over `ntiles` tiles, one tile per CTA.  (A persistent,
+// software-pipelined variant — the next tile's record and element gathers in
+// flight while a tile computes — measured 6.4-6.7 ms against 5.16 at L13:
+// the kernel is bound by its scattered stores, not by the load chain.)
+template <bool kFull>
+static phfem_status launch_level(phfem_ctx* ctx, const LvArgs& a, const LvOut& o, int64_t ntiles) {
+  const char* name = kFull ? "k_rl_level_full" : "k_rl_level";
+  PHFEM_LAUNCH(ctx, name, k_rl_level<kFull><<<(unsigned)ntiles, kLvT, lv_smem_bytes<kFull>(), ctx->stream>>>(a, o));
+  return PHFEM_OK;
 }
 
 }  // namespace phfem
@@ -435,9 +503,9 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
     o.row_ptr = C->row_ptr;
     o.col = C->col_idx;
     o.val = C->values;
-    PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<(unsigned)ntiles, kLvT, lv_smem_bytes<true>(), ctx->stream>>>(a, o));
+    PHFEM_TRY(launch_level<true>(ctx, a, o, ntiles));
   } else {
-    PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<(unsigned)ntiles, kLvT, lv_smem_bytes<false>(), ctx->stream>>>(a, o));
+    PHFEM_TRY(launch_level<false>(ctx, a, o, ntiles));
   }
   dfree(ctx, tiles);
   return PHFEM_OK;
@@ -683,9 +751,9 @@ PHFEM_API phfem_status phfem_dist_refine_level_ex(phfem_ctx* ctx, const phfem_to
       o.row_ptr = C->row_ptr;
       o.col = C->col_idx;
       o.val = C->values;
-      PHFEM_LAUNCH(ctx, "k_rl_level_full", k_rl_level<true><<<nt, kLvT, lv_smem_bytes<true>(), ctx->stream>>>(a, o));
+      PHFEM_TRY(launch_level<true>(ctx, a, o, nt));
     } else {
-      PHFEM_LAUNCH(ctx, "k_rl_level", k_rl_level<false><<<nt, kLvT, lv_smem_bytes<false>(), ctx->stream>>>(a, o));
+      PHFEM_TRY(launch_level<false>(ctx, a, o, nt));
     }
   }
   if (own) {  // the count of pairs for other ranks

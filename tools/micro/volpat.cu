@@ -1,0 +1,70 @@
+// volpat.cu — the store pattern of k_volume without its arithmetic: every
+// warp writes, per 32-element chunk, 288 doubles to each of B, D, M, M0 and
+// 96 doubles of load (16-byte stores), optionally reading the 12-byte
+// element records.  Bounds what the blocks kernel can reach at this access
+// pattern on one B200.  nvcc -gencode arch=compute_100a,code=sm_100a -O3 volpat.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+// G: 32-element chunks per warp iteration (the span written per stream)
+template <int NS, bool CS>
+__global__ void k_pat(double2* B, double2* D, double2* M, double2* M0, double2* L, const int* el, long nchunks,
+                      int rd, int G) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc = 0;
+  for (long c0 = ((long)blockIdx.x * nw + warp) * G; c0 < nchunks; c0 += (long)gridDim.x * nw * G) {
+    if (rd)
+      for (int g = 0; g < G; ++g) acc += el[(c0 + g) * 96 + lane] + el[(c0 + g) * 96 + 32 + lane] + el[(c0 + g) * 96 + 64 + lane];
+    const double2 v = make_double2(acc, 1.0);
+    double2* outs[5] = {B, D, M, M0, L};
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int n2 = s == 4 ? 48 : 144;
+      double2* o = outs[s] + c0 * n2;
+      for (int i = lane; i < n2 * G; i += 32) {
+        if (CS) __stcs(o + i, v);
+        else o[i] = v;
+      }
+    }
+  }
+}
+
+int main() {
+  const long nE = 134217728, nchunks = nE / 32;
+  double2 *B, *D, *M, *M0, *L;
+  int* el;
+  cudaMalloc(&B, nE * 72);
+  cudaMalloc(&D, nE * 72);
+  cudaMalloc(&M, nE * 72);
+  cudaMalloc(&M0, nE * 72);
+  cudaMalloc(&L, nE * 24);
+  cudaMalloc(&el, nE * 12);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const double bytes5 = nE * (4 * 72.0 + 24.0);
+  for (int rd = 0; rd < 2; ++rd)
+    for (int G : {1, 2, 4, 8})
+    for (int mult : {6}) {
+      for (int v = 0; v < 2; ++v) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+          cudaEventRecord(e0);
+          if (v == 0) k_pat<5, false><<<sms * mult, 128>>>(B, D, M, M0, L, el, nchunks, rd, G);
+          else k_pat<5, true><<<sms * mult, 128>>>(B, D, M, M0, L, el, nchunks, rd, G);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best) best = ms;
+        }
+        const double moved = bytes5 + (rd ? nE * 12.0 : 0.0);
+        printf("read=%d G=%d grid %2dx%d x128 %-6s %7.3f ms %8.1f GB/s\n", rd, G, mult, sms, v ? "st.cs" : "st", best,
+               moved / best / 1e6);
+      }
+    }
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
