@@ -91,17 +91,20 @@ phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
 
 // refine.cu / refine_topo.cu internals of the fused pipeline (mid / write_mid:
 // who writes the midpoint nodes of the refined mesh)
+// defer_elements: the children rows are left to the refined-level pass
+// (write_elems below), which writes them together with the fine elem_edge
 phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
-                             phfem_mesh* out, bool write_mid);
+                             phfem_mesh* out, bool write_mid, bool defer_elements = false);
 phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                   const phfem_topology* ptopo, const phfem_mesh* fine,
-                                  phfem_topology* out, double* mid);
+                                  phfem_topology* out, double* mid, bool write_elems = false);
 // build_topology + classify_edges + assemble_constraint in one edge pass (edge_gen.cu)
 phfem_status build_topology_fused(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_topology* out,
                                   phfem_classification* cls, phfem_csr* C);
 phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                const phfem_topology* ptopo, const phfem_classification* pcls,
                                const phfem_mesh* fine, phfem_topology* topo,
-                               phfem_classification* cls, phfem_csr* C, double* mid);
+                               phfem_classification* cls, phfem_csr* C, double* mid,
+                               bool write_elems = false);
 
 }  // namespace phfem

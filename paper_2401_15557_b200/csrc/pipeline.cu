@@ -65,7 +65,8 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
     memset(&next, 0, sizeof next);
     // the sort-free paths write the midpoint nodes themselves (coalesced)
     const bool generic = (flags & PHFEM_PIPE_GENERIC_EG) != 0;
-    if (st == PHFEM_OK) st = red_refine_impl(ctx, &cur, &topo, &next, generic);
+    // sort-free levels: children rows + fine elem_edge come from the level pass
+    if (st == PHFEM_OK) st = red_refine_impl(ctx, &cur, &topo, &next, generic, !generic);
     double* mid = next.coords;  // the level kernels write nodes nc..nc+E-1
     tr("red_refine");
     phfem_topology fine_topo;
@@ -79,10 +80,10 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
           st = phfem_build_topology(ctx, &next, &fine_topo);
         }
       } else if (last_fused) {
-        st = refine_level_impl(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C, mid);
+        st = refine_level_impl(ctx, &cur, &topo, &pcls, &next, &fine_topo, &out->cls, &out->C, mid, true);
         have_cls_C = st == PHFEM_OK;
       } else {
-        st = refine_topology_impl(ctx, &cur, &topo, &next, &fine_topo, mid);
+        st = refine_topology_impl(ctx, &cur, &topo, &next, &fine_topo, mid, true);
       }
       if (st != PHFEM_OK) phfem_mesh_release(ctx, &next);
     }

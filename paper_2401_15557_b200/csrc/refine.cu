@@ -7,6 +7,7 @@
 // gathered) vertices, and the four children of parent m are stored as 48
 // contiguous bytes (rows 4m..4m+3).
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace phfem {
 
@@ -94,7 +95,7 @@ namespace phfem {
 // write_mid = false: the midpoint nodes nc..nc+E-1 are left to the fused
 // refined-level kernel (refine_topo.cu), which writes them coalesced.
 phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
-                             phfem_mesh* out, bool write_mid) {
+                             phfem_mesh* out, bool write_mid, bool defer_elements) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !mesh || !topo) return PHFEM_ERR_INVALID_ARGUMENT;
   if (topo->nE != mesh->nE || topo->nC != mesh->nC)
@@ -114,7 +115,7 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
   if (nC > 0)
     PHFEM_CUDA(ctx, cudaMemcpyAsync(out->coords, mesh->coords, sizeof(double) * 2 * nC,
                                     cudaMemcpyDeviceToDevice, ctx->stream));
-  if (nE > 0) {
+  if (nE > 0 && !defer_elements) {
     PHFEM_LAUNCH(ctx, "k_refine_elements", k_refine_elements<<<grid_for(nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         (const double2*)mesh->coords, mesh->elements, topo->elem_edge, (int)nE, (int)nC,
         (double2*)out->coords, (int4*)out->elements, write_mid ? 1 : 0));

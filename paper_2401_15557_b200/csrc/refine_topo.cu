@@ -41,6 +41,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace phfem {
 
@@ -83,8 +84,12 @@ struct LvOut {
   int32_t* ltm;
   int32_t* interior;
   int32_t* boundary;
-  int32_t* elem_edge;
+  int32_t* elem_edge;  // nullable: with rk the element pass (k_refine_children) writes it
   int32_t* node_edge_start;
+  // per parent edge e: the in-group ranks of its interior fine edges, 2 bits
+  // each (partner at j1 / j2 of t_plus, k1 / k2 of t_minus) — all the
+  // element pass needs besides the group starts
+  uint8_t* rk;
   double2* mid;  // nullable: mid[nc + e - mid_base] = midpoint of parent edge e
   int64_t mid_base;
   int2* pairs;   // distributed level: (slot 3m+l, f / ~f) per fine edge instead of elem_edge
@@ -314,6 +319,7 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
     const int rk1 = (v0 && q0 < q1) + (v2 && r0 < q1) + (v3 && r1 < q1);
     const int rk2 = (v0 && q0 < r0) + (v1 && q1 < r0) + (v3 && r1 < r0);
     const int rk3 = (v0 && q0 < r1) + (v1 && q1 < r1) + (v2 && r0 < r1);
+    if (o.rk) o.rk[le] = (uint8_t)(rk0 | rk1 << 2 | rk2 << 4 | rk3 << 6);
     // t_plus vertices: V(l) = cop, V(l+1) = ca, V(l+2) = cb; midpoint of the
     // edge at local j = 0.5 (V(j+1) + V(j+2)).  t_minus: W(l2) = com,
     // W(l2+1) = cb, W(l2+2) = ca.
@@ -372,7 +378,7 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
     } else if (o.pairs) {  // distributed: to the owners of the fine elements (coalesced)
       o.pairs[2 * (int64_t)f] = make_int2(3 * el2.x + lp, f);
       o.pairs[2 * (int64_t)f + 1] = lm >= 0 ? make_int2(3 * el2.y + lm, ~f) : make_int2(-1, 0);
-    } else {
+    } else if (o.elem_edge) {
       o.elem_edge[3 * (int64_t)el2.x + lp] = f;
       if (lm >= 0) o.elem_edge[3 * (int64_t)el2.y + lm] = ~f;
     }
@@ -417,6 +423,66 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   lv_tile<kFull>(a, o, s, blockIdx.x, r, g, c);
 }
 
+// Children rows AND their elem_edge, one thread per parent element, after the
+// level kernel (coalesced 48-byte rows instead of two scattered 4-byte
+// elem_edge stores per fine edge).  Parent m = (P0, P1, P2) with edges e_j
+// opposite P_j (sign s_j: m is t_plus of e_j), group starts G_j, M_j = nc + e_j:
+//   * half of e_j at its endpoint v: G_j + (v == min of e_j's endpoints ? 0 : 1)
+//     (group order: the half at the smaller old node first);
+//   * interior edge I_k (opposite M_k, between M_{k+1} and M_{k+2}): group of
+//     E' = max(e_{k+1}, e_{k+2}), position 2 + the rank the level kernel
+//     stored for the partner e_min = min(e_{k+1}, e_{k+2}) of E';
+//   * child 4m = (M0, M1, M2): (I_0, I_1, I_2), its t_plus;
+//     child 4m+1+k = (P_k, M_{k+2}, M_{k+1}): (~I_k, half of e_{k+1} at P_k,
+//     half of e_{k+2} at P_k), each half signed by s of its parent edge
+//   (refine.cpp:33-36; the same ids as the scattered stores of k_rl_level).
+__global__ void __launch_bounds__(256) k_refine_children(const int32_t* __restrict__ elements,
+                                                         const int32_t* __restrict__ elem_edge,
+                                                         const int32_t* __restrict__ nes,
+                                                         const uint8_t* __restrict__ rk, int nE, int nc,
+                                                         int4* __restrict__ out_elems,
+                                                         int4* __restrict__ out_ee) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
+    int P[3], sg[3], e[3], G[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      P[j] = __ldg(elements + 3 * m + j);
+      sg[j] = __ldg(elem_edge + 3 * m + j);
+      e[j] = abs_edge(sg[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[j] = __ldg(nes + nc + e[j]);
+    int I[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int jA = k == 2 ? 0 : k + 1, jB = k == 0 ? 2 : k - 1;
+      const bool aBig = e[jA] > e[jB];
+      const int jE = aBig ? jA : jB, jm = aBig ? jB : jA;
+      const int r = __ldg(rk + e[jE]);
+      // partner slot of e_min seen from E': next local index (j1 / k1) or the one after (j2 / k2)
+      const bool next = jm == (jE == 2 ? 0 : jE + 1);
+      const int field = (sg[jE] >= 0 ? 0 : 2) + (next ? 0 : 1);
+      I[k] = G[jE] + 2 + ((r >> (2 * field)) & 3);
+    }
+    // half of e_j at vertex v, signed
+    auto half = [&](int j, int v) {
+      const int a = P[j == 2 ? 0 : j + 1], b = P[j == 0 ? 2 : j - 1];
+      const int id = G[j] + (v == min(a, b) ? 0 : 1);
+      return sg[j] >= 0 ? id : ~id;
+    };
+    const int M0 = nc + e[0], M1 = nc + e[1], M2 = nc + e[2];
+    int4* o = out_elems + 3 * m;
+    o[0] = make_int4(M0, M1, M2, P[0]);
+    o[1] = make_int4(M2, M1, P[1], M0);
+    o[2] = make_int4(M2, P[2], M1, M0);
+    int4* q = out_ee + 3 * m;
+    q[0] = make_int4(I[0], I[1], I[2], ~I[0]);
+    q[1] = make_int4(half(1, P[0]), half(2, P[0]), ~I[1], half(2, P[1]));
+    q[2] = make_int4(half(0, P[1]), ~I[2], half(0, P[2]), half(1, P[2]));
+  }
+}
+
 // dynamic SMEM of the level kernels (opt-in above 48 KB, set once per variant)
 template <bool kFull>
 static size_t lv_smem_bytes() {
@@ -453,7 +519,7 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
                                      const phfem_topology* ptopo,
                                      const phfem_classification* pcls, int64_t Ef, int64_t L,
                                      phfem_topology* topo, phfem_classification* cls, phfem_csr* C,
-                                     double* mid) {
+                                     double* mid, const phfem_mesh* fine, bool write_elems) {
   const int64_t E = ptopo->E;
   if (E == 0) return PHFEM_OK;
   const int64_t ntiles = (E + kLvT - 1) / kLvT;
@@ -496,6 +562,12 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
   o.elem_edge = topo->elem_edge;
   o.node_edge_start = topo->node_edge_start;
   o.mid = (double2*)mid;
+  uint8_t* rk = nullptr;
+  if (write_elems) {  // children rows + fine elem_edge by the element pass below
+    PHFEM_TRY(dalloc(ctx, &rk, E));
+    o.rk = rk;
+    o.elem_edge = nullptr;
+  }
   if (pcls) {
     a.neu_bits = pcls->neumann_bits;
     o.rpos = cls->retained_pos;
@@ -507,13 +579,18 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
   } else {
     PHFEM_TRY(launch_level<false>(ctx, a, o, ntiles));
   }
+  if (write_elems && parent->nE > 0)
+    PHFEM_LAUNCH(ctx, "k_refine_children", k_refine_children<<<grid_for(parent->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        parent->elements, ptopo->elem_edge, topo->node_edge_start, rk, parent->nE, parent->nC,
+        (int4*)fine->elements, (int4*)topo->elem_edge));
+  dfree(ctx, rk);
   dfree(ctx, tiles);
   return PHFEM_OK;
 }
 
 phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                   const phfem_topology* ptopo, const phfem_mesh* fine,
-                                  phfem_topology* out, double* mid) {
+                                  phfem_topology* out, double* mid, bool write_elems) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !parent || !ptopo || !fine) return PHFEM_ERR_INVALID_ARGUMENT;
   if (ptopo->nE != parent->nE || ptopo->nC != parent->nC || fine->nE != 4 * parent->nE ||
@@ -539,7 +616,7 @@ phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
   out->E = (int32_t)Ef;
   out->n_boundary = (int32_t)nBf;
   out->n_interior = (int32_t)(Ef - nBf);
-  return refine_level_run(ctx, parent, ptopo, nullptr, Ef, 0, out, nullptr, nullptr, mid);
+  return refine_level_run(ctx, parent, ptopo, nullptr, Ef, 0, out, nullptr, nullptr, mid, fine, write_elems);
 }
 
 // defined in classify.cu
@@ -549,7 +626,8 @@ phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const ph
 phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                const phfem_topology* ptopo, const phfem_classification* pcls,
                                const phfem_mesh* fine, phfem_topology* topo,
-                               phfem_classification* cls, phfem_csr* C, double* mid) {
+                               phfem_classification* cls, phfem_csr* C, double* mid,
+                               bool write_elems) {
   memset(topo, 0, sizeof(*topo));
   memset(cls, 0, sizeof(*cls));
   memset(C, 0, sizeof(*C));
@@ -589,7 +667,7 @@ phfem_status refine_level_impl(phfem_ctx* ctx, const phfem_mesh* parent,
   PHFEM_TRY(dalloc(ctx, &C->values, C->nnz));
   PHFEM_CUDA(ctx, cudaMemsetAsync(topo->node_edge_start, 0, sizeof(int32_t) * (nc + 1), ctx->stream));
   if (L == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
-  PHFEM_TRY(refine_level_run(ctx, parent, ptopo, pcls, Ef, L, topo, cls, C, mid));
+  PHFEM_TRY(refine_level_run(ctx, parent, ptopo, pcls, Ef, L, topo, cls, C, mid, fine, write_elems));
   // boundary lists -> ids, Neumann bitmap, block prefixes (retained arrays already written)
   PHFEM_TRY(classify_lists(ctx, topo, fine, cls, false));
   if (cls->L != L)
