@@ -655,10 +655,16 @@ def main():
     ap.add_argument("--generic-eg", action="store_true",
                     help="sort-based edge generation on the refined mesh too (no SURVEY f1 shortcut)")
     args = ap.parse_args()
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args)
+        else:
+            run_ours(args)
+    finally:
+        if "torch.distributed" in sys.modules:
+            import torch.distributed as tdist
+            if tdist.is_available() and tdist.is_initialized():
+                tdist.destroy_process_group()
 
 
 if __name__ == "__main__":
