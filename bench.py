@@ -71,10 +71,13 @@ def kernel_bytes(name, s, p):
         "k_refine_elements": 24 * pE + 48 * pE,
         # fused refined level: parent edge records + elem_edge / opposite-vertex /
         # coordinate gathers in; fine topology (32 B/edge incl. list slot and
-        # retained_pos), fine elem_edge, node_edge_start + midpoints (20 B per
+        # retained_pos), node_edge_start + midpoints + partner ranks (21 B per
         # parent edge), retained list + row_ptr (8 B/row), C entries (12 B) out
         "k_rl_level_full": (24 * pEd + pEd // 8 + 24 * pE + 16 * pC) +
-                           (32 * E + 12 * nE + 20 * pEd + 8 * L + 12 * nnz),
+                           (32 * E + 21 * pEd + 8 * L + 12 * nnz),
+        # element pass: parent elements + elem_edge in, group starts + ranks
+        # gathered (5 B per parent edge), children rows + fine elem_edge out
+        "k_refine_children": 24 * pE + 5 * pEd + 96 * pE,
         "k_cls_retained": pEd // 8 + 4 * pEd + 4 * pEd,  # parent classification (retained_pos / retained_edges)
     }.get(name)
 
