@@ -338,6 +338,16 @@ PHFEM_API int phfem_ctx_profile_read(phfem_ctx* ctx, int max_names, const char**
     return -1;
   }
   int n = 0;
+  if (getenv("PHFEM_PROF_TIMELINE") && !ctx->recs.empty()) {  // debug: per-launch start / gap
+    float prev_end = 0.f;
+    for (auto& r : ctx->recs) {
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, ctx->recs[0].a, r.a);
+      cudaEventElapsedTime(&t1, ctx->recs[0].a, r.b);
+      fprintf(stderr, "[timeline] %-22s start %9.3f  dur %8.3f  gap %7.3f ms\n", r.name, t0, t1 - t0, t0 - prev_end);
+      prev_end = t1;
+    }
+  }
   for (auto& r : ctx->recs) {
     float t = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);

@@ -6,6 +6,26 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+__device__ __forceinline__ void st256(double2* p, double2 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.x), "d"(v.y)
+               : "memory");
+}
+
+// 256-bit stores (STG.256): the same pattern with half the store instructions
+__global__ void k_pat256(double2* B, double2* D, double2* M, double2* M0, double2* L, long nchunks) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long c0 = (long)blockIdx.x * nw + warp; c0 < nchunks; c0 += (long)gridDim.x * nw) {
+    const double2 v = make_double2((double)c0, 1.0);
+    double2* outs[5] = {B, D, M, M0, L};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int n4 = s == 4 ? 24 : 72;  // 32-byte units per chunk
+      double2* o = outs[s] + c0 * 2 * n4;
+      for (int i = lane; i < n4; i += 32) st256(o + 2 * i, v);
+    }
+  }
+}
+
 // G: 32-element chunks per warp iteration (the span written per stream)
 template <int NS, bool CS>
 __global__ void k_pat(double2* B, double2* D, double2* M, double2* M0, double2* L, const int* el, long nchunks,
@@ -65,6 +85,19 @@ int main() {
                moved / best / 1e6);
       }
     }
+  for (int mult : {4, 6, 8}) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(e0);
+      k_pat256<<<sms * mult, 128>>>(B, D, M, M0, L, nchunks);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("st.256 grid %2dx%d x128 %7.3f ms %8.1f GB/s\n", mult, sms, best, bytes5 / best / 1e6);
+  }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
