@@ -35,7 +35,13 @@
 //   4. fine-edge records are staged in SMEM and stored coalesced; with kFull
 //      the retained positions, retained list, CSR rows of C and their
 //      (column, value) entries (assembly.cpp:144-168) are emitted in the
-//      same pass (the fine Neumann edges are the halves of the parent's).
+//      same pass (the fine Neumann edges are the halves of the parent's);
+//   5. the fine elem_edge is NOT scattered from here (two 4-byte stores per
+//      fine edge bounded the kernel): one rank byte per parent edge goes
+//      out instead, and k_refine_children (one thread per parent element)
+//      writes the children rows and their elem_edge as coalesced rows from
+//      the group starts and those ranks.  The distributed variant keeps the
+//      per-fine-edge stores (own elements in place, others as pairs).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
