@@ -7,7 +7,12 @@
 //     134-140: 13 doubles per element cross the bus instead of 36;
 //   * C's values are +-|E|/2 per row and its pattern follows from the edge
 //     arrays (assembly.cpp:144-168): one double per row crosses the bus;
-//   * local_in_tplus / local_in_tminus travel as one byte per edge.
+//   * local_in_tplus / local_in_tminus travel as one byte per edge;
+//   * interior_edges, retained_edges, retained_pos and bD do not travel at
+//     all: they follow from the (small) boundary, Neumann and Dirichlet id
+//     lists (edge_topology.cpp:104-113, 165-173: ascending complements and
+//     running positions; assembly.cpp:230-242: bD is zero outside the
+//     Dirichlet rows, whose values come along gathered).
 // A device pack kernel writes the compact form, chunks of it are copied into
 // a pinned staging buffer (kept in the ctx), and host threads expand each
 // chunk into the caller's buffers as soon as its copy event fires, while the
@@ -15,6 +20,7 @@
 // The expansion only copies bits, so the host buffers equal the device
 // outputs exactly.
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -64,6 +70,15 @@ __global__ void k_pack_locals(const int32_t* __restrict__ ltp, const int32_t* __
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x)
     out[e] = (uint8_t)(ltp[e] | (ltm[e] + 1) << 2);
+}
+
+// bD at the Dirichlet rows (list order; rows of Neumann edges give 0, unused)
+__global__ void k_pack_bd(const double* __restrict__ bd, const int32_t* __restrict__ rpos,
+                          const int32_t* __restrict__ dir_ids, int n, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = rpos[dir_ids[i]];
+    out[i] = r >= 0 ? bd[r] : 0.0;
+  }
 }
 
 struct HostPool {
@@ -129,17 +144,18 @@ PHFEM_API int64_t phfem_pipeline_download_bytes(const phfem_pipeline_out* o,
   add(d->edge_nodes, 8 * E);
   add(d->edge_elements, 8 * E);
   if (d->local_in_tplus || d->local_in_tminus) b += E;
-  add(d->interior_edges, 4 * (int64_t)o->topo.n_interior);
   add(d->boundary_edges, 4 * (int64_t)o->topo.n_boundary);
+  // interior / retained arrays and bD are derived on the host from id lists
+  if (d->interior_edges) b += 4 * (int64_t)o->topo.n_boundary;
+  if (d->retained_pos || d->retained_edges || d->bd || d->C_row_ptr || d->C_col_idx || d->C_values)
+    b += 4 * (int64_t)o->cls.nN;
+  if (d->bd) b += 12 * (int64_t)o->cls.nD;
   add(d->elem_edge, 12 * nE);
   add(d->dirichlet_edge_ids, 4 * (int64_t)o->cls.nD);
   add(d->neumann_edge_ids, 4 * (int64_t)o->cls.nN);
-  add(d->retained_edges, 4 * L);
-  add(d->retained_pos, 4 * E);
   if (d->C_row_ptr || d->C_col_idx || d->C_values) b += 8 * L;
   if (d->B || d->D || d->M || d->M0) b += 104 * nE;
   add(d->load, 24 * nE);
-  add(d->bd, 8 * L);
   return b;
 }
 
@@ -170,6 +186,28 @@ PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipel
     tmp_re.resize(L);
     h_re = tmp_re.data();
   }
+  // the id lists the host derives interior / retained arrays and bD from
+  const bool want_bd = d->bd != nullptr;
+  const bool need_neu = d->retained_pos || h_re || want_bd;
+  const int64_t nB = o->topo.n_boundary, nNc = o->cls.nN, nDc = o->cls.nD;
+  std::vector<int32_t> hb(d->interior_edges ? nB : 0), hn(need_neu ? nNc : 0), hd(want_bd ? nDc : 0);
+  std::vector<double> hbv(want_bd ? nDc : 0);
+  if (!hb.empty())
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(hb.data(), o->topo.boundary_edges, 4 * hb.size(), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+  if (!hn.empty())
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(hn.data(), o->cls.neumann_edge_ids, 4 * hn.size(), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+  double* dbv = nullptr;
+  if (!hd.empty()) {
+    PHFEM_TRY(dalloc(ctx, &dbv, nDc));
+    PHFEM_LAUNCH(ctx, "k_pack_bd", k_pack_bd<<<grid_for(nDc, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        o->bd, o->cls.retained_pos, o->cls.dirichlet_edge_ids, (int)nDc, dbv));
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(hd.data(), o->cls.dirichlet_edge_ids, 4 * hd.size(), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(hbv.data(), dbv, 8 * hbv.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (!hb.empty() || !hn.empty() || !hd.empty()) PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   const int64_t CH = int64_t(1) << 22;  // elements per block chunk (416 MB compact)
   const int64_t nchunks = want_blocks ? (nE + CH - 1) / CH : 0;
   const size_t bytes_blocks = want_blocks ? (size_t)104 * nE : 0;
@@ -214,26 +252,20 @@ PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipel
     if (dst && bytes) p[np++] = Piece{dst, src, bytes};
   };
   add(h_el, o->topo.edge_elements, 8 * (size_t)E);
-  add(h_re, o->cls.retained_edges, 4 * (size_t)L);
-  PHFEM_CUDA(ctx, cudaEventRecord(ev[nchunks], ctx->stream));  // C inputs ready after these two
-  const int np_c = 2;
   for (int i = 0; i < np; ++i)
     PHFEM_CUDA(ctx, cudaMemcpyAsync(p[i].dst, p[i].src, p[i].bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  (void)np_c;
+  PHFEM_CUDA(ctx, cudaEventRecord(ev[nchunks], ctx->stream));  // C inputs ready
   np = 0;
   add(d->coords, o->mesh.coords, 16 * (size_t)nC);
   add(d->elements, o->mesh.elements, 12 * (size_t)nE);
   add(d->dirichlet, o->mesh.dirichlet, 8 * (size_t)o->mesh.nD);
   add(d->neumann, o->mesh.neumann, 8 * (size_t)o->mesh.nN);
   add(d->edge_nodes, o->topo.edge_nodes, 8 * (size_t)E);
-  add(d->interior_edges, o->topo.interior_edges, 4 * (size_t)o->topo.n_interior);
   add(d->boundary_edges, o->topo.boundary_edges, 4 * (size_t)o->topo.n_boundary);
   add(d->elem_edge, o->topo.elem_edge, 12 * (size_t)nE);
   add(d->dirichlet_edge_ids, o->cls.dirichlet_edge_ids, 4 * (size_t)o->cls.nD);
   add(d->neumann_edge_ids, o->cls.neumann_edge_ids, 4 * (size_t)o->cls.nN);
-  add(d->retained_pos, o->cls.retained_pos, 4 * (size_t)E);
   add(d->load, o->load, 24 * (size_t)nE);
-  add(d->bd, o->bd, 8 * (size_t)L);
   for (int i = 0; i < np; ++i)
     PHFEM_CUDA(ctx, cudaMemcpyAsync(p[i].dst, p[i].src, p[i].bytes, cudaMemcpyDeviceToHost, ctx->stream));
 
@@ -291,6 +323,56 @@ PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipel
   }
   _mm_sfence();
   tick("blocks expanded");
+  // retained set = edges minus the (sorted, unique) Neumann ids: retained_edges
+  // ascending, retained_pos the running position (edge_topology.cpp:165-173)
+  std::sort(hn.begin(), hn.end());
+  hn.erase(std::unique(hn.begin(), hn.end()), hn.end());
+  auto below = [](const std::vector<int32_t>& v, int64_t x) {  // #entries < x
+    return (int64_t)(std::lower_bound(v.begin(), v.end(), (int32_t)std::min<int64_t>(x, INT32_MAX)) - v.begin());
+  };
+  if (h_re || d->retained_pos) {
+    int32_t* rpos = d->retained_pos;
+    pool.run(E, [&](int64_t a, int64_t b) {
+      int64_t k = below(hn, a), q = a - k;
+      for (int64_t e = a; e < b; ++e) {
+        // non-temporal stores: written once, never read back here
+        if (k < (int64_t)hn.size() && hn[k] == e) {
+          if (rpos) _mm_stream_si32(rpos + e, -1);
+          ++k;
+        } else {
+          if (h_re) _mm_stream_si32(h_re + q, (int)e);
+          if (rpos) _mm_stream_si32(rpos + e, (int)q);
+          ++q;
+        }
+      }
+      _mm_sfence();
+    });
+  }
+  if (d->interior_edges) {  // ascending complement of the boundary list (edge_topology.cpp:104-113)
+    int32_t* in = d->interior_edges;
+    pool.run(E, [&](int64_t a, int64_t b) {
+      int64_t k = below(hb, a), q = a - k;
+      for (int64_t e = a; e < b; ++e) {
+        if (k < (int64_t)hb.size() && hb[k] == e) ++k;
+        else _mm_stream_si32(in + q++, (int)e);
+      }
+      _mm_sfence();
+    });
+  }
+  if (want_bd) {  // zero outside the Dirichlet rows (assembly.cpp:230-242)
+    double* bd = d->bd;
+    pool.run(L, [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) _mm_stream_si64(reinterpret_cast<long long*>(bd + i), 0);
+      _mm_sfence();
+    });
+    for (int64_t i = 0; i < nDc; ++i) {
+      const int64_t e = hd[i];
+      const int64_t k = below(hn, e);
+      if (k < (int64_t)hn.size() && hn[k] == e) continue;  // a Neumann edge has no row
+      bd[e - k] = hbv[i];
+    }
+  }
+  tick("lists derived");
   PHFEM_CUDA(ctx, cudaEventSynchronize(ev[nchunks]));
   tick("C inputs arrived");
   if (want_loc) {
@@ -365,5 +447,6 @@ PHFEM_API phfem_status phfem_pipeline_download(phfem_ctx* ctx, const phfem_pipel
   dfree(ctx, dpk);
   dfree(ctx, dcv);
   dfree(ctx, dloc);
+  dfree(ctx, dbv);
   return PHFEM_OK;
 }
