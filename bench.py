@@ -100,6 +100,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: wait for its first row, then
+            # keep only the rows sampled while the timed region runs
+            t_end = time.time() + 5.0
+            while not self.rows and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -110,6 +116,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            t_end = time.time() + 1.0  # a region shorter than the period: take the next row
+            while not self.rows and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -650,7 +659,7 @@ def main():
     ap.add_argument("--no-cn", action="store_true", help="skip the config-3 CN right-hand-side line")
     ap.add_argument("--no-given", action="store_true", help="skip the given-L13-mesh (EG + AS) line")
     ap.add_argument("--cn-level", type=int, default=11)
-    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0 = off)")
+    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) pipeline even at N = 1")
     ap.add_argument("--replicas", action="store_true",
