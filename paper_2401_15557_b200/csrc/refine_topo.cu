@@ -448,44 +448,60 @@ __global__ void __launch_bounds__(256) k_refine_children(const int32_t* __restri
                                                          const uint8_t* __restrict__ rk, int nE, int nc,
                                                          int4* __restrict__ out_elems,
                                                          int4* __restrict__ out_ee) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
-    int P[3], sg[3], e[3], G[3];
+  // rows staged per warp in SMEM, then stored as contiguous 512-byte warp
+  // writes (a direct per-thread 48-byte row leaves every sector half written
+  // per instruction: twice the L2 write transactions)
+  __shared__ int4 stage[8][2][96];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* se = stage[warp][0];
+  int4* sq = stage[warp][1];
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + warp * 32); base < nE; base += wstride) {
+    const int64_t m = base + lane;
+    if (m < nE) {
+      int P[3], sg[3], e[3], G[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      P[j] = __ldg(elements + 3 * m + j);
-      sg[j] = __ldg(elem_edge + 3 * m + j);
-      e[j] = abs_edge(sg[j]);
+      for (int j = 0; j < 3; ++j) {
+        P[j] = __ldg(elements + 3 * m + j);
+        sg[j] = __ldg(elem_edge + 3 * m + j);
+        e[j] = abs_edge(sg[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) G[j] = __ldg(nes + nc + e[j]);
+      int I[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int jA = k == 2 ? 0 : k + 1, jB = k == 0 ? 2 : k - 1;
+        const bool aBig = e[jA] > e[jB];
+        const int jE = aBig ? jA : jB, jm = aBig ? jB : jA;
+        const int r = __ldg(rk + e[jE]);
+        // partner slot of e_min seen from E': next local index (j1 / k1) or the one after (j2 / k2)
+        const bool next = jm == (jE == 2 ? 0 : jE + 1);
+        const int field = (sg[jE] >= 0 ? 0 : 2) + (next ? 0 : 1);
+        I[k] = G[jE] + 2 + ((r >> (2 * field)) & 3);
+      }
+      // half of e_j at vertex v, signed
+      auto half = [&](int j, int v) {
+        const int a = P[j == 2 ? 0 : j + 1], b = P[j == 0 ? 2 : j - 1];
+        const int id = G[j] + (v == min(a, b) ? 0 : 1);
+        return sg[j] >= 0 ? id : ~id;
+      };
+      const int M0 = nc + e[0], M1 = nc + e[1], M2 = nc + e[2];
+      se[3 * lane] = make_int4(M0, M1, M2, P[0]);
+      se[3 * lane + 1] = make_int4(M2, M1, P[1], M0);
+      se[3 * lane + 2] = make_int4(M2, P[2], M1, M0);
+      sq[3 * lane] = make_int4(I[0], I[1], I[2], ~I[0]);
+      sq[3 * lane + 1] = make_int4(half(1, P[0]), half(2, P[0]), ~I[1], half(2, P[1]));
+      sq[3 * lane + 2] = make_int4(half(0, P[1]), ~I[2], half(0, P[2]), half(1, P[2]));
     }
-#pragma unroll
-    for (int j = 0; j < 3; ++j) G[j] = __ldg(nes + nc + e[j]);
-    int I[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int jA = k == 2 ? 0 : k + 1, jB = k == 0 ? 2 : k - 1;
-      const bool aBig = e[jA] > e[jB];
-      const int jE = aBig ? jA : jB, jm = aBig ? jB : jA;
-      const int r = __ldg(rk + e[jE]);
-      // partner slot of e_min seen from E': next local index (j1 / k1) or the one after (j2 / k2)
-      const bool next = jm == (jE == 2 ? 0 : jE + 1);
-      const int field = (sg[jE] >= 0 ? 0 : 2) + (next ? 0 : 1);
-      I[k] = G[jE] + 2 + ((r >> (2 * field)) & 3);
+    __syncwarp();
+    const int64_t rem = nE - base;
+    const int n4 = 3 * (int)(rem < 32 ? rem : 32);
+    for (int i = lane; i < n4; i += 32) {
+      out_elems[3 * base + i] = se[i];
+      out_ee[3 * base + i] = sq[i];
     }
-    // half of e_j at vertex v, signed
-    auto half = [&](int j, int v) {
-      const int a = P[j == 2 ? 0 : j + 1], b = P[j == 0 ? 2 : j - 1];
-      const int id = G[j] + (v == min(a, b) ? 0 : 1);
-      return sg[j] >= 0 ? id : ~id;
-    };
-    const int M0 = nc + e[0], M1 = nc + e[1], M2 = nc + e[2];
-    int4* o = out_elems + 3 * m;
-    o[0] = make_int4(M0, M1, M2, P[0]);
-    o[1] = make_int4(M2, M1, P[1], M0);
-    o[2] = make_int4(M2, P[2], M1, M0);
-    int4* q = out_ee + 3 * m;
-    q[0] = make_int4(I[0], I[1], I[2], ~I[0]);
-    q[1] = make_int4(half(1, P[0]), half(2, P[0]), ~I[1], half(2, P[1]));
-    q[2] = make_int4(half(0, P[1]), ~I[2], half(0, P[2]), half(1, P[2]));
+    __syncwarp();
   }
 }
 
