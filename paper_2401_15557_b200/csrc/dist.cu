@@ -238,17 +238,29 @@ __global__ void k_dist_midpoints(const double2* __restrict__ coords, const int32
 }
 
 // children 4m..4m+3 of the local elements (refine.cpp:28-37)
-__global__ void k_dist_children(const int32_t* __restrict__ elements, const int32_t* __restrict__ elem_edge,
-                                int n, int nc, int4* __restrict__ out) {
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int p0 = elements[3 * m], p1 = elements[3 * m + 1], p2 = elements[3 * m + 2];
-    const int s0 = elem_edge[3 * m], s1 = elem_edge[3 * m + 1], s2 = elem_edge[3 * m + 2];
-    const int m0 = nc + (s0 >= 0 ? s0 : ~s0), m1 = nc + (s1 >= 0 ? s1 : ~s1), m2 = nc + (s2 >= 0 ? s2 : ~s2);
-    int4* o = out + 3 * m;
-    o[0] = make_int4(m0, m1, m2, p0);
-    o[1] = make_int4(m2, m1, p1, m0);
-    o[2] = make_int4(m2, p2, m1, m0);
+__global__ void __launch_bounds__(256) k_dist_children(const int32_t* __restrict__ elements,
+                                                       const int32_t* __restrict__ elem_edge, int n, int nc,
+                                                       int4* __restrict__ out) {
+  // rows staged per warp, stored as contiguous 512-byte warp writes (as k_refine_children)
+  __shared__ int4 stage[8][96];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* so = stage[warp];
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + warp * 32; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = base + lane;
+    if (m < n) {
+      const int p0 = elements[3 * m], p1 = elements[3 * m + 1], p2 = elements[3 * m + 2];
+      const int s0 = elem_edge[3 * m], s1 = elem_edge[3 * m + 1], s2 = elem_edge[3 * m + 2];
+      const int m0 = nc + (s0 >= 0 ? s0 : ~s0), m1 = nc + (s1 >= 0 ? s1 : ~s1), m2 = nc + (s2 >= 0 ? s2 : ~s2);
+      so[3 * lane] = make_int4(m0, m1, m2, p0);
+      so[3 * lane + 1] = make_int4(m2, m1, p1, m0);
+      so[3 * lane + 2] = make_int4(m2, p2, m1, m0);
+    }
+    __syncwarp();
+    const int64_t rem = n - base;
+    const int n4 = 3 * (int)(rem < 32 ? rem : 32);
+    for (int i = lane; i < n4; i += 32) out[3 * base + i] = so[i];
+    __syncwarp();
   }
 }
 

@@ -16,27 +16,38 @@ __global__ void __launch_bounds__(256) k_refine_elements(const double2* __restri
                                                          const int32_t* __restrict__ elem_edge,
                                                          int nE, int nC, double2* __restrict__ out_coords,
                                                          int4* __restrict__ out_elems, int write_mid) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
-    const int p0 = __ldg(elements + 3 * m), p1 = __ldg(elements + 3 * m + 1),
-              p2 = __ldg(elements + 3 * m + 2);
-    const int s0 = __ldg(elem_edge + 3 * m), s1 = __ldg(elem_edge + 3 * m + 1),
-              s2 = __ldg(elem_edge + 3 * m + 2);
-    const int m0 = nC + (s0 >= 0 ? s0 : ~s0);  // midpoint opposite p0
-    const int m1 = nC + (s1 >= 0 ? s1 : ~s1);
-    const int m2 = nC + (s2 >= 0 ? s2 : ~s2);
-    // children rows 4m..4m+3 (refine.cpp:33-36): (M0,M1,M2),(P0,M2,M1),(P1,M0,M2),(P2,M1,M0)
-    int4* o = out_elems + 3 * m;
-    o[0] = make_int4(m0, m1, m2, p0);
-    o[1] = make_int4(m2, m1, p1, m0);
-    o[2] = make_int4(m2, p2, m1, m0);
-    // midpoints 0.5 * (c[a] + c[b]) (refine.cpp:16-19), written once by t_plus
-    if (write_mid && (s0 >= 0 || s1 >= 0 || s2 >= 0)) {
-      const double2 c0 = __ldg(coords + p0), c1 = __ldg(coords + p1), c2 = __ldg(coords + p2);
-      if (s0 >= 0) out_coords[m0] = make_double2(0.5 * (c1.x + c2.x), 0.5 * (c1.y + c2.y));
-      if (s1 >= 0) out_coords[m1] = make_double2(0.5 * (c2.x + c0.x), 0.5 * (c2.y + c0.y));
-      if (s2 >= 0) out_coords[m2] = make_double2(0.5 * (c0.x + c1.x), 0.5 * (c0.y + c1.y));
+  // children rows staged per warp, stored as contiguous 512-byte warp writes
+  __shared__ int4 stage[8][96];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* so = stage[warp];
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + warp * 32; base < nE;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = base + lane;
+    if (m < nE) {
+      const int p0 = __ldg(elements + 3 * m), p1 = __ldg(elements + 3 * m + 1),
+                p2 = __ldg(elements + 3 * m + 2);
+      const int s0 = __ldg(elem_edge + 3 * m), s1 = __ldg(elem_edge + 3 * m + 1),
+                s2 = __ldg(elem_edge + 3 * m + 2);
+      const int m0 = nC + (s0 >= 0 ? s0 : ~s0);  // midpoint opposite p0
+      const int m1 = nC + (s1 >= 0 ? s1 : ~s1);
+      const int m2 = nC + (s2 >= 0 ? s2 : ~s2);
+      // children rows 4m..4m+3 (refine.cpp:33-36): (M0,M1,M2),(P0,M2,M1),(P1,M0,M2),(P2,M1,M0)
+      so[3 * lane] = make_int4(m0, m1, m2, p0);
+      so[3 * lane + 1] = make_int4(m2, m1, p1, m0);
+      so[3 * lane + 2] = make_int4(m2, p2, m1, m0);
+      // midpoints 0.5 * (c[a] + c[b]) (refine.cpp:16-19), written once by t_plus
+      if (write_mid && (s0 >= 0 || s1 >= 0 || s2 >= 0)) {
+        const double2 c0 = __ldg(coords + p0), c1 = __ldg(coords + p1), c2 = __ldg(coords + p2);
+        if (s0 >= 0) out_coords[m0] = make_double2(0.5 * (c1.x + c2.x), 0.5 * (c1.y + c2.y));
+        if (s1 >= 0) out_coords[m1] = make_double2(0.5 * (c2.x + c0.x), 0.5 * (c2.y + c0.y));
+        if (s2 >= 0) out_coords[m2] = make_double2(0.5 * (c0.x + c1.x), 0.5 * (c0.y + c1.y));
+      }
     }
+    __syncwarp();
+    const int64_t rem = nE - base;
+    const int n4 = 3 * (int)(rem < 32 ? rem : 32);
+    for (int i = lane; i < n4; i += 32) out_elems[3 * base + i] = so[i];
+    __syncwarp();
   }
 }
 
