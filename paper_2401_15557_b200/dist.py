@@ -132,6 +132,12 @@ def balanced_splits(hist: np.ndarray, bins: np.ndarray, world: int) -> np.ndarra
     return np.asarray(out, dtype=np.int32)
 
 
+# coarse key-range histogram over every HIST_SAMPLE-th element of meshes with
+# at least HIST_SAMPLE_MIN_ELEMENTS elements (module constants: tests force it)
+HIST_SAMPLE = 8
+HIST_SAMPLE_MIN_ELEMENTS = 1 << 20
+
+
 def element_splits(nE: int, world: int) -> np.ndarray:
     return np.asarray([nE * r // world for r in range(world + 1)], dtype=np.int32)
 
@@ -408,7 +414,7 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
     # coarse histogram of max nodes -> balanced key ranges (identical on every rank)
     # the key ranges only balance the work (no output depends on them): a
     # 1/8 sample of the own elements is enough for the coarse histogram
-    S = 8 if nE >= (1 << 20) else 1
+    S = HIST_SAMPLE if nE >= HIST_SAMPLE_MIN_ELEMENTS else 1
     smp = [s.elements[::S].contiguous() if S > 1 else s.elements for s in states]
     hists = [s.ops.occurrences(e, 0, int(e.shape[0]), s.ops.as_tensor(bins), pack=False)
              for s, e in zip(states, smp)]

@@ -129,3 +129,25 @@ def test_gloo_two_ranks_equal_oracle(tmp_path, case, levels):
     assert np.array_equal(got["load"], load)
     assert np.array_equal(got["coords"], fine.coords)
     assert np.array_equal(got["elements"], fine.elements)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_sampled_key_histogram_local_ranks(monkeypatch, W):
+    """The key ranges come from a SAMPLED coarse histogram on large meshes
+    (dist.HIST_SAMPLE); forced on a small mesh here: W emulated NumPy ranks
+    (one process, LocalComm) still reproduce the C oracle bit for bit — the
+    ranges only balance work."""
+    from paper_2401_15557_b200 import dist
+    from dist_cpu_backend import NumpyRankOps
+    monkeypatch.setattr(dist, "HIST_SAMPLE", 3)
+    monkeypatch.setattr(dist, "HIST_SAMPLE_MIN_ELEMENTS", 0)
+    hm = O.refine_levels(G.lshape_6tri(), 2)
+    comm = dist.LocalComm(W)
+    states = dist.make_states(hm, comm, lambda r: NumpyRankOps())
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, 1, *G.config_fields(1))
+    got = dist.collect(states)
+    fine = O.refine_levels(hm, 1)
+    om, ot = O.build_topology(fine)
+    topo = ot.arrays()
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "elem_edge"):
+        assert np.array_equal(np.asarray(got[k]).reshape(-1), topo[k].reshape(-1)), k
