@@ -211,8 +211,9 @@ def cpu_workers_available(per_worker_gb: float) -> int:
     return max(1, min(cores, int(avail_gb * 0.6 / per_worker_gb)))
 
 
-def cpu_baseline_single(level=9):
-    """One bounded sample on one core: square L9 -> L10 pipeline (4.2 M triangles)."""
+def cpu_baseline_single(level=11):
+    """One bounded sample on one core (about 10-30 s of CPU work): square
+    L11 -> L12 pipeline (33.5 M triangles) by default."""
     kind = cpu_impl()
     nE, times = cpu_sample_worker((level, 1, 0, kind))
     what = ("reference sources (oracle/_ref, /root/reference/proj/src via shim/Eigen)" if kind == "reference"
@@ -652,7 +653,7 @@ def main():
     ap.add_argument("--level", type=int, default=13, help="final refinement level (config 5: 13)")
     ap.add_argument("--e2e-level", type=int, default=13)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-level", type=int, default=9)
+    ap.add_argument("--cpu-level", type=int, default=11)
     ap.add_argument("--ref-level", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
