@@ -5,7 +5,7 @@
  * Plain pointers and sizes only (no torch, no Eigen, no C++ types), so it can
  * be bound from C++, ctypes, cgo or JNI.  Every entry point replaces one
  * reference C++ function from /root/reference/proj/include/phfem (cited per
- * function); the C++ drop-in layer in include/phfem/*.hpp re-exposes the
+ * function); the C++ drop-in layer in include/phfem/ headers re-exposes the
  * reference signatures on top of this ABI.
  *
  * Conventions
