@@ -442,16 +442,33 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   // so the raw 64-bit items compare in key order).  Four branch-free masked
   // compares per trip (reads past the segment stay inside the tile or hit
   // the padding; the mask drops them — the next sub-bucket's keys restart
-  // at node 0, so they are not simply larger).
-  for (int p = tid; p < n; p += T) {
-    const uint64_t it = sm.buf1[p];
-    const int nd = sm.node_of[p];
-    const int st = sm.seg[nd], end = st + sm.cnt[nd];
-    int r = 0;
-    for (int q = st; q < end; q += 4)
-      r += (int)(sm.buf1[q] < it) + (int)((q + 1 < end) & (sm.buf1[q + 1] < it)) +
-           (int)((q + 2 < end) & (sm.buf1[q + 2] < it)) + (int)((q + 3 < end) & (sm.buf1[q + 3] < it));
-    sm.buf2[st + r] = it;
+  // at node 0, so they are not simply larger).  With one sub-bucket per tile
+  // (bs = 8: every mesh up to 2^56 packed bits, L13 included) the item's top
+  // bits ARE the tile node, so everything past the segment — the next nodes'
+  // items or the ~0 padding — compares larger and the masks are dropped (the
+  // masked compares were a quarter of the kernel's instructions at L12).
+  if (nsub == 1) {
+    for (int p = tid; p < n; p += T) {
+      const uint64_t it = sm.buf1[p];
+      const int nd = sm.node_of[p];
+      const int st = sm.seg[nd], end = st + sm.cnt[nd];
+      int r = 0;
+      for (int q = st; q < end; q += 4)
+        r += (int)(sm.buf1[q] < it) + (int)(sm.buf1[q + 1] < it) + (int)(sm.buf1[q + 2] < it) +
+             (int)(sm.buf1[q + 3] < it);
+      sm.buf2[st + r] = it;
+    }
+  } else {
+    for (int p = tid; p < n; p += T) {
+      const uint64_t it = sm.buf1[p];
+      const int nd = sm.node_of[p];
+      const int st = sm.seg[nd], end = st + sm.cnt[nd];
+      int r = 0;
+      for (int q = st; q < end; q += 4)
+        r += (int)(sm.buf1[q] < it) + (int)((q + 1 < end) & (sm.buf1[q + 1] < it)) +
+             (int)((q + 2 < end) & (sm.buf1[q + 2] < it)) + (int)((q + 3 < end) & (sm.buf1[q + 3] < it));
+      sm.buf2[st + r] = it;
+    }
   }
   __syncthreads();
   // per warp (its 32 nodes): run starts, partners, the reference's two error
