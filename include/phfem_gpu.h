@@ -69,6 +69,12 @@ phfem_status phfem_alloc(phfem_ctx* ctx, size_t bytes, void** out);
 void phfem_free(phfem_ctx* ctx, void* ptr);
 /* number of kernels this ctx launched so far (bench evidence) */
 int64_t phfem_ctx_launches(const phfem_ctx* ctx);
+/* Test knob: cap the edge pass's bucket width (bits of max node per bucket,
+ * 1..8; default 8, or env PHFEM_EG_MAX_BS at ctx creation).  A cap below 8
+ * makes every 256-node tile span several buckets (the multi-sub-bucket tile
+ * path that meshes with > 56 packed key bits, e.g. the L13 square, take).
+ * Outputs do not depend on it.                                              */
+phfem_status phfem_ctx_set_eg_max_bs(phfem_ctx* ctx, int max_bs);
 /* Per-launch CUDA-event timing on the ctx stream.  enable != 0 clears the
  * records and starts recording an event pair around every kernel launch;
  * read synchronises and returns the number of distinct kernel names with the

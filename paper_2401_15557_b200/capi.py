@@ -154,7 +154,7 @@ class phfem_pipeline_host(C.Structure):
 EXPORTED = [
     "phfem_abi_version", "phfem_ctx_create", "phfem_ctx_destroy", "phfem_ctx_message",
     "phfem_ctx_stream", "phfem_ctx_sync", "phfem_alloc", "phfem_free", "phfem_ctx_launches",
-    "phfem_mesh_release", "phfem_build_topology", "phfem_topology_release",
+    "phfem_ctx_set_eg_max_bs", "phfem_mesh_release", "phfem_build_topology", "phfem_topology_release",
     "phfem_classify_edges", "phfem_classification_release", "phfem_red_refine",
     "phfem_orient_ccw", "phfem_assemble_volume", "phfem_assemble_constraint",
     "phfem_csr_release", "phfem_constraint_csc", "phfem_csc_release", "phfem_assemble_load",
@@ -201,6 +201,7 @@ def load_library(path: str = LIB_PATH):
         "phfem_alloc": (C.c_int, [vp, C.c_size_t, P(vp)]),
         "phfem_free": (None, [vp, vp]),
         "phfem_ctx_launches": (i64, [vp]),
+        "phfem_ctx_set_eg_max_bs": (C.c_int, [vp, C.c_int]),
         "phfem_mesh_release": (None, [vp, P(phfem_mesh)]),
         "phfem_build_topology": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology)]),
         "phfem_topology_release": (None, [vp, P(phfem_topology)]),
@@ -364,6 +365,11 @@ class Context:
         if k < 0:
             raise PhfemError(ERR_CUDA, "phfem_ctx_profile_read failed")
         return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(k)}
+
+    def set_eg_max_bs(self, bs: int):
+        """Test knob: cap the edge pass's bucket width (1..8, default 8) so
+        small meshes take the multi-sub-bucket tile path (outputs unchanged)."""
+        self.check(self.lib.phfem_ctx_set_eg_max_bs(self.ptr, int(bs)))
 
     @property
     def stream(self) -> int:

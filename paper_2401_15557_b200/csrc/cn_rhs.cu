@@ -700,12 +700,8 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
             a, topo->edge_nodes, topo->local_in_tplus, topo->E, p->rowt, p->rowh);
         ctx->launches++;
       }
-      static bool attr_set = false;  // per process; the attribute is per function
-      if (!attr_set) {
-        cudaFuncSetAttribute(k_cn_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCnTmaSmem);
-        attr_set = true;
-      }
       if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
+      if (st == PHFEM_OK) st = smem_optin(ctx, (const void*)k_cn_tma, kCnTmaSmem, "k_cn_tma smem opt-in");
     }
   }
   if (st != PHFEM_OK) {

@@ -54,6 +54,14 @@ struct phfem_ctx {
   std::unordered_map<size_t, std::vector<void*>> cache;
   std::unordered_map<void*, size_t> block_size;
   size_t cached_bytes = 0;
+  // dynamic-SMEM opt-ins already applied on this ctx's device (kernel ->
+  // bytes); cudaFuncSetAttribute is per device, so the cache lives here
+  std::unordered_map<const void*, size_t> smem_optin;
+  // upper bound on the edge pass's bucket width bs (bits of max node per
+  // bucket; 8 = a tile is one bucket when the packed item leaves 8 bits).
+  // Lowered only to exercise the multi-sub-bucket tile path on small meshes
+  // (env PHFEM_EG_MAX_BS at ctx creation, or phfem_ctx_set_eg_max_bs)
+  int eg_max_bs = 8;
 };
 
 namespace phfem {
@@ -89,6 +97,10 @@ phfem_status cuda_fail(phfem_ctx* ctx, cudaError_t e, const char* where);
   } while (0)
 
 phfem_status raw_alloc(phfem_ctx* ctx, void** p, size_t bytes);
+
+// Opt a kernel into `bytes` of dynamic shared memory on the ctx's device
+// (needed above 48 KB); applied once per (ctx, kernel), errors reported.
+phfem_status smem_optin(phfem_ctx* ctx, const void* fn, size_t bytes, const char* name);
 void raw_free(phfem_ctx* ctx, void* p);
 void cache_flush(phfem_ctx* ctx);
 

@@ -1,5 +1,6 @@
 // ctx.cu — context, stream-ordered memory, error plumbing and the device-wide
 // scan used by the edge / classification passes.
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -37,6 +38,17 @@ phfem_status errors_fetch(phfem_ctx* ctx) {
   PHFEM_CUDA(ctx, cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(phfem_dev_errors),
                                   cudaMemcpyDeviceToHost, ctx->stream));
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PHFEM_OK;
+}
+
+phfem_status smem_optin(phfem_ctx* ctx, const void* fn, size_t bytes, const char* name) {
+  auto it = ctx->smem_optin.find(fn);
+  if (it != ctx->smem_optin.end() && it->second >= bytes) return PHFEM_OK;
+  if (bytes > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, name);
+  }
+  ctx->smem_optin[fn] = bytes;
   return PHFEM_OK;
 }
 
@@ -232,6 +244,10 @@ PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** ou
       return PHFEM_ERR_NO_DEVICE;  // sm_100a code only
     }
   }
+  if (const char* bs = getenv("PHFEM_EG_MAX_BS")) {
+    const int v = atoi(bs);
+    if (v >= 1 && v <= 8) ctx->eg_max_bs = v;
+  }
   if (stream) {
     ctx->stream = (cudaStream_t)stream;
   } else {
@@ -291,6 +307,12 @@ PHFEM_API const char* phfem_ctx_message(const phfem_ctx* ctx) {
 PHFEM_API void* phfem_ctx_stream(const phfem_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 PHFEM_API int64_t phfem_ctx_launches(const phfem_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+PHFEM_API phfem_status phfem_ctx_set_eg_max_bs(phfem_ctx* ctx, int max_bs) {
+  if (!ctx || max_bs < 1 || max_bs > 8) return PHFEM_ERR_INVALID_ARGUMENT;
+  ctx->eg_max_bs = max_bs;
+  return PHFEM_OK;
+}
 
 PHFEM_API phfem_status phfem_ctx_sync(phfem_ctx* ctx) {
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -6,20 +6,28 @@
 // occurrence of a run is t_plus, ids are handed out in canonical order.
 //
 // Device algorithm (2 global passes over the occurrences):
-//   A  k_eg_count    histogram of occurrences per bucket of 2^bs consecutive
-//                    max-node ids (warp-aggregated atomics)
-//   B  scan          bucket offsets
-//   C  k_eg_scatter  each occurrence packed into one 64-bit item
-//                      [max-node low bits | min node | occurrence index | dir]
-//                    and scattered into its bucket (warp-aggregated cursor)
-//   D  k_eg_bucket   one CTA per bucket: counting sort by max node in SMEM,
-//                    per-node insertion sort of the packed items (the packed
-//                    value orders by (max, min, occurrence) = the reference's
-//                    stable order), run detection with the reference's two
-//                    error checks, and a decoupled look-back over buckets that
-//                    carries (edges, boundary edges) so every CTA writes its
-//                    final edge ids, interior/boundary list slots, the
-//                    element->edge map and the max-node grouping table directly.
+//   A  k_eg_count     histogram of occurrences per bucket of 2^bs consecutive
+//                     max-node ids (warp-aggregated atomics)
+//   B  scan           bucket offsets; k_eg_tile_max = the largest tile (does
+//                     every 256-node tile fit in SMEM?)
+//   C  k_eg_scatter   each occurrence packed into one 64-bit item
+//                       [max-node low bits | min node | occurrence index | dir]
+//                     and scattered into its bucket (warp-aggregated cursor)
+//   D  k_eg_tile      one CTA per tile of 256 max nodes (256 >> bs buckets):
+//                     counting sort by max node in SMEM, rank sort inside each
+//                     node's segment (the packed value orders by (max, min,
+//                     occurrence) = the reference's stable order), run
+//                     detection with the reference's two error checks, one
+//                     16-byte record per edge at a tile-local slot (carrying
+//                     the tile-local boundary prefix) and per-tile edge /
+//                     boundary / Neumann counts.  Fast path (tile in SMEM,
+//                     every node <= 32 occurrences) and a general path
+//                     (global scratch for oversized tiles or segments).
+//   E  scans          of the per-tile counts (no look-back: tiny arrays)
+//   F  k_eg_emit      one CTA per tile: records -> edge_nodes, edge_elements,
+//                     local indices, interior / boundary list slots, elem_edge,
+//                     node_edge_start at the scanned tile offsets; on a fused
+//                     final level also retained_pos / retained_edges and C.
 #include <algorithm>
 
 #include "common.cuh"
@@ -439,34 +447,31 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   // rank sort inside each node segment (<= 32 items, ~6 on refined meshes):
   // key = (min node, occurrence), unique; the reference's stable order
   // (items of one segment share the max-node bits and differ in (min, occ),
-  // so the raw 64-bit items compare in key order).  Four branch-free masked
-  // compares per trip (reads past the segment stay inside the tile or hit
-  // the padding; the mask drops them — the next sub-bucket's keys restart
-  // at node 0, so they are not simply larger).  With one sub-bucket per tile
-  // (bs = 8: every mesh up to 2^56 packed bits, L13 included) the item's top
-  // bits ARE the tile node, so everything past the segment — the next nodes'
-  // items or the ~0 padding — compares larger and the masks are dropped (the
-  // masked compares were a quarter of the kernel's instructions at L12).
-  if (nsub == 1) {
-    for (int p = tid; p < n; p += T) {
-      const uint64_t it = sm.buf1[p];
-      const int nd = sm.node_of[p];
+  // so the raw 64-bit items compare in key order).  Each thread ranks the
+  // items it holds in registers; four compares per trip read up to 3 items
+  // past the segment.  Those are larger — the next nodes' items carry larger
+  // max-node bits, the tile ends in ~0 padding — unless the next sub-bucket
+  // starts within them: its keys restart at node 0.  Only such segments
+  // (tiles of several sub-buckets, bs < 8: e.g. the L13 square's 57-bit
+  // items give bs = 7) take the masked compares.
+  const int hb = (1 << P.bs) - 1;
+#pragma unroll
+  for (int k = 0; k < kTilePer; ++k) {
+    if (tid + k * T < n) {
+      const uint64_t it = itr[k];
+      const int nd = ndr[k];
       const int st = sm.seg[nd], end = st + sm.cnt[nd];
+      const int sub_end = (nd | hb) + 1 < kTileNodes ? sm.seg[(nd | hb) + 1] : 0x7fffffff;
       int r = 0;
-      for (int q = st; q < end; q += 4)
-        r += (int)(sm.buf1[q] < it) + (int)(sm.buf1[q + 1] < it) + (int)(sm.buf1[q + 2] < it) +
-             (int)(sm.buf1[q + 3] < it);
-      sm.buf2[st + r] = it;
-    }
-  } else {
-    for (int p = tid; p < n; p += T) {
-      const uint64_t it = sm.buf1[p];
-      const int nd = sm.node_of[p];
-      const int st = sm.seg[nd], end = st + sm.cnt[nd];
-      int r = 0;
-      for (int q = st; q < end; q += 4)
-        r += (int)(sm.buf1[q] < it) + (int)((q + 1 < end) & (sm.buf1[q + 1] < it)) +
-             (int)((q + 2 < end) & (sm.buf1[q + 2] < it)) + (int)((q + 3 < end) & (sm.buf1[q + 3] < it));
+      if (end + 3 <= sub_end) {
+        for (int q = st; q < end; q += 4)
+          r += (int)(sm.buf1[q] < it) + (int)(sm.buf1[q + 1] < it) + (int)(sm.buf1[q + 2] < it) +
+               (int)(sm.buf1[q + 3] < it);
+      } else {
+        for (int q = st; q < end; q += 4)
+          r += (int)(sm.buf1[q] < it) + (int)((q + 1 < end) & (sm.buf1[q + 1] < it)) +
+               (int)((q + 2 < end) & (sm.buf1[q + 2] < it)) + (int)((q + 3 < end) & (sm.buf1[q + 3] < it));
+      }
       sm.buf2[st + r] = it;
     }
   }
@@ -879,11 +884,7 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   EgParams PT = P;
   PT.nb = ntiles;
   const size_t smem = sizeof(TileSmem);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_eg_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile, smem, "k_eg_tile smem opt-in"));
   PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
       items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileE, tileE, (int64_t)ntiles + 1, nullptr));
@@ -964,7 +965,7 @@ static phfem_status eg_params(phfem_ctx* ctx, int64_t nC_range, int64_t nC_all, 
   P->lo_bits = bits_for(std::max<int64_t>(nC_all - 1, 1));
   P->occ_bits = bits_for(std::max<int64_t>(3 * nE_all - 1, 1));
   P->total_bits = P->lo_bits + P->occ_bits + 1;
-  P->bs = std::min(8, 64 - P->total_bits);
+  P->bs = std::min(ctx->eg_max_bs, 64 - P->total_bits);
   if (P->bs < 1) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "build_topology: ids too wide");
   const int NB = 1 << P->bs;
   P->nb = (int)((nC_range + NB - 1) / NB);

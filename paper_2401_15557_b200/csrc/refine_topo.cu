@@ -505,16 +505,11 @@ __global__ void __launch_bounds__(256) k_refine_children(const int32_t* __restri
   }
 }
 
-// dynamic SMEM of the level kernels (opt-in above 48 KB, set once per variant)
+// dynamic SMEM of the level kernels (opt-in above 48 KB, per ctx device)
 template <bool kFull>
-static size_t lv_smem_bytes() {
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_rl_level<kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(LvSmem<kFull>));
-    set = true;
-  }
-  return sizeof(LvSmem<kFull>);
+static phfem_status lv_smem_bytes(phfem_ctx* ctx, size_t* bytes) {
+  *bytes = sizeof(LvSmem<kFull>);
+  return smem_optin(ctx, (const void*)k_rl_level<kFull>, *bytes, "k_rl_level smem opt-in");
 }
 
 // The level kernel over `ntiles` tiles, one tile per CTA.  (A persistent,
@@ -524,7 +519,9 @@ static size_t lv_smem_bytes() {
 template <bool kFull>
 static phfem_status launch_level(phfem_ctx* ctx, const LvArgs& a, const LvOut& o, int64_t ntiles) {
   const char* name = kFull ? "k_rl_level_full" : "k_rl_level";
-  PHFEM_LAUNCH(ctx, name, k_rl_level<kFull><<<(unsigned)ntiles, kLvT, lv_smem_bytes<kFull>(), ctx->stream>>>(a, o));
+  size_t smem = 0;
+  PHFEM_TRY(lv_smem_bytes<kFull>(ctx, &smem));
+  PHFEM_LAUNCH(ctx, name, k_rl_level<kFull><<<(unsigned)ntiles, kLvT, smem, ctx->stream>>>(a, o));
   return PHFEM_OK;
 }
 
