@@ -113,6 +113,14 @@ def _arr(ptr, n, dtype):
     return np.ctypeslib.as_array((ct * n).from_address(ptr)).copy()
 
 
+def _view(ptr, n, dtype):
+    """No-copy numpy view of oracle-owned C memory (valid while its owner lives)."""
+    if n == 0 or not ptr:
+        return np.zeros(0, dtype=dtype)
+    ct = {np.int32: C.c_int32, np.float64: C.c_double}[dtype]
+    return np.ctypeslib.as_array((ct * n).from_address(ptr))
+
+
 def _check(st, err):
     if st != 0:
         msg = err.value.decode()
@@ -152,6 +160,20 @@ class OTopology:
             "node_edge_start": _arr(t.node_edge_start, t.nC + 1, np.int32),
         }
 
+    def views(self) -> dict:
+        """arrays() without the copies (large meshes): views of the C buffers."""
+        t = self.t
+        return {
+            "edge_nodes": _view(t.edge_nodes, 2 * t.E, np.int32).reshape(-1, 2),
+            "edge_elements": _view(t.edge_elements, 2 * t.E, np.int32).reshape(-1, 2),
+            "local_in_tplus": _view(t.local_in_tplus, t.E, np.int32),
+            "local_in_tminus": _view(t.local_in_tminus, t.E, np.int32),
+            "interior_edges": _view(t.interior_edges, t.n_interior, np.int32),
+            "boundary_edges": _view(t.boundary_edges, t.n_boundary, np.int32),
+            "elem_edge": _view(t.elem_edge, 3 * t.nE, np.int32).reshape(-1, 3),
+            "node_edge_start": _view(t.node_edge_start, t.nC + 1, np.int32),
+        }
+
     def node_pair_to_edge(self, k, l):
         return lib().orc_node_pair_to_edge(C.byref(self.t), k, l)
 
@@ -182,6 +204,15 @@ class OClassification:
             "neumann_edge_ids": _arr(c.neumann_edge_ids, c.nN, np.int32),
             "retained_edges": _arr(c.retained_edges, c.L, np.int32),
             "retained_pos": _arr(c.retained_pos, c.E, np.int32),
+        }
+
+    def views(self) -> dict:
+        c = self.c
+        return {
+            "dirichlet_edge_ids": _view(c.dirichlet_edge_ids, c.nD, np.int32),
+            "neumann_edge_ids": _view(c.neumann_edge_ids, c.nN, np.int32),
+            "retained_edges": _view(c.retained_edges, c.L, np.int32),
+            "retained_pos": _view(c.retained_pos, c.E, np.int32),
         }
 
     def __del__(self):
@@ -234,6 +265,26 @@ def assemble_volume(hm: HostMesh, coeffs: phfem_coeffs):
     err = C.create_string_buffer(512)
     _check(lib().orc_assemble_volume(C.byref(om.m), C.byref(coeffs), *[_ptr(o) for o in outs], err, 512), err)
     return outs
+
+
+class OCsr:
+    """C in CSR as oracle-owned C memory (no copies): .ptr / .idx / .val views."""
+
+    def __init__(self, om: OMesh, topo: OTopology, cls: OClassification):
+        self.s = orc_sparse()
+        err = C.create_string_buffer(512)
+        _check(lib().orc_assemble_constraint(C.byref(om.m), C.byref(topo.t), C.byref(cls.c), C.byref(self.s),
+                                             None, err, 512), err)
+        s = self.s
+        self.ptr = _view(s.ptr, s.rows + 1, np.int32)
+        self.idx = _view(s.idx, s.nnz, np.int32)
+        self.val = _view(s.val, s.nnz, np.float64)
+
+    def __del__(self):
+        try:
+            lib().orc_sparse_free(C.byref(self.s))
+        except Exception:
+            pass
 
 
 def assemble_constraint(om: OMesh, topo: OTopology, cls: OClassification):
