@@ -62,9 +62,12 @@ def kernel_bytes(name, s, p):
     return {
         # B, D, M, M0 (4 x 72 B) + load (24 B) written; elements + coords read
         "k_volume": 12 * nE + 16 * nC + 312 * nE,
-        # parent build_topology: items in (3 x 8 B / element), edge records out
-        # (edge_nodes, edge_elements, ltp, ltm, list: 28 B), elem_edge 12 B/element
-        "k_eg_tile": 24 * pE + 28 * pEd + 12 * pE,
+        # parent build_topology, sort pass: packed items in (3 x 8 B / element),
+        # one 16-B edge record per edge + node_edge_start (4 B / node) out
+        "k_eg_tile": 24 * pE + 16 * pEd + 4 * pC,
+        # emit pass: records in; edge_nodes, edge_elements, ltp, ltm, list slot
+        # (28 B / edge) + elem_edge (12 B / element) out
+        "k_eg_emit": 16 * pEd + 28 * pEd + 12 * pE,
         "k_eg_scatter": 12 * pE + 24 * pE,
         "k_eg_count": 12 * pE,
         # red_refine without midpoints: elements + elem_edge in, 4 children out
@@ -231,6 +234,9 @@ def run_reference(args):
     import multiprocessing as mp
     level = args.ref_level
     kind = cpu_impl()
+    if kind == "reference":     # load oracle/_ref in the parent: the forked workers inherit the mapping
+        from oracle import reference as R
+        R.lib()
     P = cpu_workers_available(per_worker_gb=1.5)
     with mp.get_context("fork").Pool(P) as pool:
         res = pool.map(cpu_sample_worker, [(level, args.steps, args.warmup, kind)] * P)
@@ -362,6 +368,8 @@ def run_ours_sharded(args, rank, world, local):
 def run_ours(args):
     from paper_2401_15557_b200 import capi, meshgen as G
     rank, world, local = dist_init(args.gpus)
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world}")
     if (world > 1 and not args.replicas) or args.sharded:
         if world == 1:  # --sharded at N = 1: a one-rank NCCL group (exercises the collectives)
             import torch
@@ -644,6 +652,44 @@ def run_e2e(ctx, args, fields):
                     "on the host)"}
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` (N > 1, no torchrun around it): start the N
+    ranks ourselves — one process per GPU, the driver's own launch form — and
+    return their exit code.  Rank 0 prints the one JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # NCCL's init lines show nranks / NVLS
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank harness alone (rendezvous, barrier, device
+    max-over-ranks timing, rank 0's JSON line) over gloo on the CPU, no
+    kernels — checks that `bench.py --gpus N` really starts N ranks."""
+    import torch
+    import torch.distributed as tdist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        tdist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        tdist.barrier()
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "triangles/s", "n_gpus": world,
+                          "dry_run": True, "max_over_ranks": float(t.item()), "steps": args.steps,
+                          "warmup": args.warmup}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -667,7 +713,13 @@ def main():
                     help="N > 1: N independent single-GPU replicas instead of the sharded pipeline")
     ap.add_argument("--generic-eg", action="store_true",
                     help="sort-based edge generation on the refined mesh too (no SURVEY f1 shortcut)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank launch / timing harness only (gloo, CPU, no kernels)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch_under_torchrun(args))
+    if args.dry_run:
+        return run_dry(args)
     try:
         if args.impl == "reference":
             run_reference(args)
