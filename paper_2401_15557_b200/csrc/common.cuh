@@ -146,6 +146,13 @@ inline int grid_for(int64_t n, int block, int max_blocks) {
 phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
                                 int32_t* total_dev);
 
+// Stable LSD radix sort of (key, u32 value) pairs over key bits [0, end_bit)
+// (radix_sort.cu; hand-written, no library sort).  Inputs are not modified.
+phfem_status radix_sort_pairs_u64(phfem_ctx* ctx, const uint64_t* kin, uint64_t* kout, const uint32_t* vin,
+                                  uint32_t* vout, int64_t n, int end_bit);
+phfem_status radix_sort_pairs_u32(phfem_ctx* ctx, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
+                                  uint32_t* vout, int64_t n, int end_bit);
+
 }  // namespace phfem
 
 // ---------------------------------------------------------------------------

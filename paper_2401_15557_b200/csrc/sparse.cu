@@ -12,14 +12,12 @@
 //   * otherwise entries are ordered by (row, col), ties by insertion, and each
 //     run is summed left to right from 0.0;
 //   * output is Eigen's ColMajor CSC, rows ascending inside a column.
-// Device algorithm: one stable LSD radix sort (CUB) of the column-major key
-// col * rows + row with the entry index as payload — stable, so runs keep
-// insertion order and come out in CSC order directly — then run starts by
-// neighbour compare, a scan for run ids, one thread per run summing its
-// (short) run sequentially in the reference's order, and the column pointer
-// array from the run columns.
-#include <cub/device/device_radix_sort.cuh>
-
+// Device algorithm: one stable LSD radix sort (radix_sort.cu, hand-written)
+// of the column-major key col * rows + row with the entry index as payload —
+// stable, so runs keep insertion order and come out in CSC order directly —
+// then run starts by neighbour compare, a scan for run ids, one thread per
+// run summing its (short) run sequentially in the reference's order (the
+// segmented run-sum), and the column pointer array from the run columns.
 #include <algorithm>
 
 #include "common.cuh"
@@ -136,14 +134,7 @@ phfem_status from_triplets_impl(phfem_ctx* ctx, int rows, int cols, const int32_
   int end_bit = 1;
   const unsigned long long maxkey = (unsigned long long)rows * (unsigned long long)cols;
   while (end_bit < 64 && (1ull << end_bit) < maxkey) ++end_bit;
-  size_t temp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, k0, k1, i0, i1, (int)n, 0, end_bit, ctx->stream);
-  void* temp = nullptr;
-  PHFEM_TRY(raw_alloc(ctx, &temp, temp_bytes));
-  PHFEM_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k0, k1, i0, i1, (int)n, 0, end_bit,
-                                                  ctx->stream));
-  ctx->launches++;
-  raw_free(ctx, temp);
+  PHFEM_TRY(radix_sort_pairs_u64(ctx, k0, k1, i0, i1, n, end_bit));
   dfree(ctx, k0);
   dfree(ctx, i0);
   int32_t* pos = nullptr;

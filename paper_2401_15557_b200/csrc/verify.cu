@@ -13,7 +13,6 @@
 // element order, the device in a fixed tree (deterministic, run to run); the
 // terms themselves are bit-identical (optional per-element output), the sum
 // agrees to rounding.  Max-reductions (residual, error_multiplier) are exact.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -394,15 +393,9 @@ PHFEM_API phfem_status phfem_csc_to_csr(phfem_ctx* ctx, const phfem_csc* A, phfe
   PHFEM_TRY(scan_exclusive_i32(ctx, out->row_ptr, out->row_ptr, (int64_t)A->rows + 1, nullptr));
   int end_bit = 1;
   while (end_bit < 31 && (1ll << end_bit) < (long long)A->rows) ++end_bit;
-  size_t temp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, A->inner, k1, i0, i1, (int)n, 0, end_bit, ctx->stream);
-  void* temp = nullptr;
-  PHFEM_TRY(raw_alloc(ctx, &temp, temp_bytes));
   // stable LSD radix sort by row: entries of a row keep the CSC (column) order
-  PHFEM_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, temp_bytes, A->inner, k1, i0, i1, (int)n, 0, end_bit,
-                                                  ctx->stream));
-  ctx->launches++;
-  raw_free(ctx, temp);
+  PHFEM_TRY(radix_sort_pairs_u32(ctx, reinterpret_cast<const uint32_t*>(A->inner), reinterpret_cast<uint32_t*>(k1),
+                                 reinterpret_cast<const uint32_t*>(i0), reinterpret_cast<uint32_t*>(i1), n, end_bit));
   PHFEM_LAUNCH(ctx, "k_csr_gather", k_csr_gather<<<grid, 256, 0, ctx->stream>>>(i1, colp, A->values, n,
                                                                                 out->col_idx, out->values));
   dfree(ctx, colp);

@@ -145,3 +145,60 @@ def test_gpu_operator_matrices(ctx, name, make, which):
                                             C.byref(out)))
     same(host_csc(ctx, out), want)
     ctx.lib.phfem_csc_release(ctx.ptr, C.byref(out))
+
+
+def big_buffers():
+    """Multi-tile, multi-digit inputs for the hand-written radix sort
+    (csrc/radix_sort.cu): heavy duplicates (stability decides the run sums),
+    wide keys (5 digit passes), one hot column, reversed order."""
+    rng = np.random.default_rng(2024)
+    out = []
+    n = 3_000_000
+    out.append(("dups-3M", 3000, 2500, rng.integers(0, 3000, n).astype(np.int32),
+                rng.integers(0, 2500, n).astype(np.int32), rng.standard_normal(n)))
+    n = 2_000_000
+    out.append(("wide-2M", 1 << 20, 1 << 20, rng.integers(0, 1 << 20, n).astype(np.int32),
+                rng.integers(0, 1 << 20, n).astype(np.int32), rng.standard_normal(n)))
+    n = 500_000
+    out.append(("hot-column", 100_000, 64, rng.integers(0, 100_000, n).astype(np.int32),
+                np.where(rng.random(n) < 0.9, 7, rng.integers(0, 64, n)).astype(np.int32), rng.standard_normal(n)))
+    r = np.repeat(np.arange(999, -1, -1, dtype=np.int32), 700)
+    c = np.tile(np.arange(699, -1, -1, dtype=np.int32), 1000)
+    out.append(("reversed-unique", 1000, 700, r, c, rng.standard_normal(r.size)))
+    return out
+
+
+BIG = big_buffers()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,rows,cols,ri,ci,v", BIG, ids=[b[0] for b in BIG])
+def test_gpu_from_triplets_large(ctx, name, rows, cols, ri, ci, v):
+    out = capi.phfem_csc()
+    ctx.check(ctx.lib.phfem_from_triplets(ctx.ptr, rows, cols, C.c_void_p(ctx.to_device(ri)),
+                                          C.c_void_p(ctx.to_device(ci)), C.c_void_p(ctx.to_device(v)), len(v),
+                                          C.byref(out)))
+    same(host_csc(ctx, out), O.from_triplets(rows, cols, ri, ci, v))
+    ctx.lib.phfem_csc_release(ctx.ptr, C.byref(out))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", [0, 2])
+def test_gpu_operator_matrices_L9(ctx, which):
+    """Saddle / CN step matrix of the square at L9 (524,288 triangles, ~11 M
+    triplets, 3 digit passes): the device-resident inputs of the excluded solve."""
+    hm = O.refine_levels(G.square_2tri(), 9)
+    coeffs = capi.coeffs_const(((2.0, 0.3), (0.3, 1.0)), (1.0, -0.5), 0.7)
+    om, ot, oc, (B, D, M, M0), Ccsc = operator_case(hm, coeffs)
+    want = O.operator_matrix(B, D, M, M0, Ccsc, hm.nE, oc.L, which, 1e-3)
+    dB, dD, dM, dM0 = (ctx.to_device(np.ascontiguousarray(x, np.float64)) for x in (B, D, M, M0))
+    Cd = dev_csc(ctx, (*Ccsc, oc.L, 3 * hm.nE))
+    out = capi.phfem_csc()
+    if which == 0:
+        ctx.check(ctx.lib.phfem_saddle_matrix(ctx.ptr, hm.nE, C.c_void_p(dB), C.c_void_p(dD), C.c_void_p(dM),
+                                              C.byref(Cd), C.byref(out)))
+    else:
+        ctx.check(ctx.lib.phfem_step_matrix(ctx.ptr, hm.nE, C.c_void_p(dB), C.c_void_p(dD), C.c_void_p(dM),
+                                            C.c_void_p(dM0), C.byref(Cd), 1e-3, -1.0, C.byref(out)))  # M_minus
+    same(host_csc(ctx, out), want)
+    ctx.lib.phfem_csc_release(ctx.ptr, C.byref(out))
