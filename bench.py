@@ -465,6 +465,9 @@ def run_ours(args):
         dm.release()
         dm = None
         line["config5_given_mesh"] = run_given(ctx, args, fields)
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["config4_stress"] = run_config4(ctx, args, G.config_fields(4))
+        line["config2_lshape"] = run_config2(ctx, args)
     if rank == 0 and world == 1 and not args.no_cn:
         line["cn_rhs"] = run_cn_rhs(ctx, args)
     if rank == 0 and world == 1 and not args.no_e2e:
@@ -509,6 +512,135 @@ def run_given(ctx, args, fields):
                         f"({s['nE']} triangles): EG (sort-based: no parent) + classification + C + "
                         "B/D/M/M0/load/bD, config-2 coefficients",
             "ms_per_step": round(ms, 3), "value": s["nE"] / (ms * 1e-3), "unit": "triangles/s", "steps": steps,
+            "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
+                                  "peak": peak, "peak_kind": kind, "frac": round(gbs / peak, 4)}}
+
+
+def step_events(ctx, steps, before, step):
+    """Per-step CUDA events on the ctx stream around `step` (`before` runs
+    outside the events, e.g. restoring an input the step modifies).
+    Returns the mean ms per step."""
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    ctx.sync()
+    for i in range(steps):
+        before()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    ctx.sync()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps
+
+
+def config4_input(ctx, level):
+    """Config 4's stress mesh at `level` (the square refined on the device,
+    then jittered U[-0.2h, 0.2h] (seed 1), permuted (2), rotated (3) and
+    flipped (4) on the host — input generation, untimed) uploaded raw; plus a
+    device copy of the raw elements to restore before every step (the
+    normalisation rewrites them in place)."""
+    from paper_2401_15557_b200 import capi, meshgen as G
+    base = build_input(ctx, level)
+    hm = base.download()
+    base.release()
+    raw = G.stress_transform(hm, level)
+    dm = capi.DeviceMesh.upload(ctx, raw)
+    keep = ctx.to_device(raw.elements)
+    nflip = int((G.signed_area2(raw) < 0).sum())
+    return dm, keep, nflip
+
+
+def run_config4(ctx, args, fields4):
+    """BASELINE config 4: jittered / permuted / rotated / flipped L12 stress
+    mesh -> orientation normalisation (a18) -> build_topology(L12) ->
+    red_refine -> L13 topology + classification + C -> B/D/M/M0/load/bD with
+    config-2 coefficients.  Compulsory bytes: the normalisation (elements read,
+    coordinates read once, flipped rows rewritten) + the config-5 step's."""
+    import ctypes as C
+    from paper_2401_15557_b200 import capi
+    dm, keep, nflip = config4_input(ctx, args.level - 1)
+    nE0, nC0 = dm.m.nE, dm.m.nC
+    restore = lambda: ctx.check(ctx.lib.phfem_memcpy_d2d(ctx.ptr, C.c_void_p(dm.m.elements), C.c_void_p(keep),
+                                                          12 * nE0))
+
+    def step():
+        capi.orient_ccw(ctx, dm)
+        capi.pipeline(ctx, dm, 1, *fields4).release()
+    # sizes (one untimed step)
+    restore()
+    capi.orient_ccw(ctx, dm)
+    r = capi.pipeline(ctx, dm, 1, *fields4)
+    o = r.out
+    s = {"nC": o.mesh.nC, "nE": o.mesh.nE, "E": o.topo.E, "L": o.cls.L, "nnz": o.C.nnz}
+    r.release()
+    t0 = capi.build_topology(ctx, dm)
+    E0 = t0.E
+    t0.release()
+    for _ in range(max(1, args.warmup - 1)):
+        restore()
+        step()
+    steps = max(3, args.steps)
+    ms = step_events(ctx, steps, restore, step)
+    ctx.free(keep)
+    dm.release()
+    normalise = 12 * nE0 + 16 * nC0 + 12 * nflip
+    compulsory = (normalise + eg_bytes(nE0, E0) + rf_bytes(nC0, nE0, E0) + eg_bytes(s["nE"], s["E"]) +
+                  as_bytes(s["nC"], s["nE"], s["E"], s["L"], s["nnz"]))
+    peak, kind = peaks()
+    gbs = compulsory / (ms * 1e-3) / 1e9
+    return {"workload": f"config4: stress square L{args.level - 1} ({nE0} triangles; jitter U[-0.2h,0.2h] seed 1, "
+                        f"permuted seed 2, rotated seed 3, {nflip} flipped seed 4) -> normalise -> EG -> RF -> "
+                        f"L{args.level} EG + AS ({s['nE']} triangles), config-2 coefficients",
+            "ms_per_step": round(ms, 3), "value": s["nE"] / (ms * 1e-3), "unit": "triangles/s", "steps": steps,
+            "l2": "inputs larger than L2 (no flush); raw elements restored outside the per-step events",
+            "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
+                                  "peak": peak, "peak_kind": kind, "frac": round(gbs / peak, 4)},
+            "ncu": ncu_traffic(args.level, "config4_sectors")}
+
+
+def run_config2(ctx, args):
+    """BASELINE config 2: the 6-triangle L-shape refined 10 times on the device
+    (Σ10 (EG + RF) + EG + AS) -> 6,291,456 triangles, per-element
+    A(x_c), delta(x_c), p = (0.1, -0.1).  Compulsory bytes summed over the levels."""
+    from paper_2401_15557_b200 import capi, meshgen as G
+    fields = G.config_fields(2)
+    levels = 10
+    dm = capi.DeviceMesh.upload(ctx, G.lshape_6tri())
+    # per-level sizes for the byte count (untimed)
+    compulsory = 0
+    cur = capi.DeviceMesh.upload(ctx, G.lshape_6tri())
+    for _ in range(levels):
+        t = capi.build_topology(ctx, cur)
+        compulsory += eg_bytes(cur.m.nE, t.E) + rf_bytes(cur.m.nC, cur.m.nE, t.E)
+        nxt = capi.red_refine(ctx, cur, t)
+        t.release()
+        cur.release()
+        cur = nxt
+    cur.release()
+    r = capi.pipeline(ctx, dm, levels, *fields)
+    o = r.out
+    s = {"nC": o.mesh.nC, "nE": o.mesh.nE, "E": o.topo.E, "L": o.cls.L, "nnz": o.C.nnz}
+    r.release()
+    compulsory += eg_bytes(s["nE"], s["E"]) + as_bytes(s["nC"], s["nE"], s["E"], s["L"], s["nnz"])
+    step = lambda: capi.pipeline(ctx, dm, levels, *fields).release()
+    for _ in range(max(1, args.warmup)):
+        step()
+    import torch
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+    it = [0]
+
+    def before():
+        it[0] += 1
+        flush.fill_(it[0] & 0xff)
+    ms = step_events(ctx, max(10, args.steps), before, step)
+    del flush
+    dm.release()
+    peak, kind = peaks()
+    gbs = compulsory / (ms * 1e-3) / 1e9
+    return {"workload": f"config2: L-shape 6 triangles -> 10 refinements ({s['nE']} triangles): "
+                        "sum of 10 x (EG + RF) + EG + AS, config-2 coefficients",
+            "ms_per_step": round(ms, 3), "value": s["nE"] / (ms * 1e-3), "unit": "triangles/s",
+            "steps": max(10, args.steps), "l2": "flushed between steps (512 MB write outside the per-step events)",
             "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
                                   "peak": peak, "peak_kind": kind, "frac": round(gbs / peak, 4)}}
 
@@ -706,6 +838,7 @@ def main():
     ap.add_argument("--no-cn", action="store_true", help="skip the config-3 CN right-hand-side line")
     ap.add_argument("--no-given", action="store_true", help="skip the given-L13-mesh (EG + AS) line")
     ap.add_argument("--cn-level", type=int, default=11)
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-4 / config-2 lines")
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) pipeline even at N = 1")

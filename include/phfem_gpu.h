@@ -552,6 +552,8 @@ phfem_status phfem_selftest_fastmath(phfem_ctx* ctx, int64_t n, uint64_t seed,
 /* ---- host <-> device helpers for bindings without a CUDA runtime --------- */
 phfem_status phfem_memcpy_h2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
 phfem_status phfem_memcpy_d2h(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* device -> device, asynchronous on the ctx stream */
+phfem_status phfem_memcpy_d2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
 
 #ifdef __cplusplus
 }

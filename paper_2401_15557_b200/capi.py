@@ -161,7 +161,7 @@ EXPORTED = [
     "phfem_assemble_neumann", "phfem_assemble_dirichlet", "phfem_cn_plan_create",
     "phfem_cn_rhs", "phfem_cn_plan_destroy", "phfem_pipeline", "phfem_pipeline_release",
     "phfem_pipeline_from_host", "phfem_pipeline_download", "phfem_pipeline_download_bytes",
-    "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_ctx_profile", "phfem_ctx_profile_read",
+    "phfem_memcpy_h2d", "phfem_memcpy_d2h", "phfem_memcpy_d2d", "phfem_ctx_profile", "phfem_ctx_profile_read",
     "phfem_refine_topology", "phfem_pipeline_ex", "phfem_refine_level", "phfem_selftest_fastmath",
     "phfem_topology_derive", "phfem_topology_tables", "phfem_field_points", "phfem_edge_lengths",
     "phfem_assemble_load_sampled", "phfem_assemble_neumann_sampled", "phfem_assemble_dirichlet_sampled",
@@ -236,6 +236,7 @@ def load_library(path: str = LIB_PATH):
         "phfem_pipeline_download_bytes": (i64, [P(phfem_pipeline_out), P(phfem_pipeline_host)]),
         "phfem_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_size_t]),
         "phfem_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_size_t]),
+        "phfem_memcpy_d2d": (C.c_int, [vp, vp, vp, C.c_size_t]),
         "phfem_ctx_profile": (C.c_int, [vp, C.c_int]),
         "phfem_refine_topology": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_mesh),
                                             P(phfem_topology)]),

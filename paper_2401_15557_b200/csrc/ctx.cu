@@ -341,6 +341,12 @@ PHFEM_API phfem_status phfem_memcpy_d2h(phfem_ctx* ctx, void* dst, const void* s
   return PHFEM_OK;
 }
 
+PHFEM_API phfem_status phfem_memcpy_d2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PHFEM_OK;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return PHFEM_OK;
+}
+
 PHFEM_API phfem_status phfem_ctx_profile(phfem_ctx* ctx, int enable) {
   if (!ctx) return PHFEM_ERR_INVALID_ARGUMENT;
   for (auto& r : ctx->recs) {
