@@ -691,14 +691,20 @@ def run_cn_rhs(ctx, args):
     cls.release()
     topo.release()
     dm.release()
+    gbs_rc = bytes_recompute / (ms * 1e-3) / 1e9
     return {"workload": f"config3: square L{args.cn_level} ({nE} triangles), 100 CN right-hand sides, k=1e-3",
             "l2": "flushed between steps (512 MB write outside the per-step events)",
             "ms_per_step": round(ms, 4), "triangles_per_s": nE / (ms * 1e-3),
+            "design": "k_cn_hyb: M_minus top block + coupling recomputed per step from the (L2-resident) "
+                      "coordinates with the plan's expressions (bit-identical); streamed per element: "
+                      "elements 12 + load factors 24 + U 24 + row codes 12 B through a 4-stage TMA ring, "
+                      "rhs 24 B out; k_cn_rows: 16-B row records + U gathers, 8 B out",
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gbs / peak, 4), "algorithmic_bytes_per_step": bytes_step,
                          "variant": "stored operator: 16 nC + 147 nE + 4 E + 16 L (SURVEY §8(d) "
                                     "recompute bytes + the 72 nE stored top block)",
                          "recompute_variant_bytes": bytes_recompute,
+                         "frac_recompute_variant": round(gbs_rc / peak, 4),
                          "traffic": (ncu_traffic(args.cn_level, "cn_rhs_step") or {}).get("bytes"),
                          "peak_kind": kind}}
 

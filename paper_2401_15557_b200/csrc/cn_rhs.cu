@@ -26,6 +26,7 @@
 // Other load kinds take k_cn_elements (geometry recomputed every step) +
 // k_cn_edges over all edges.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "bulk.cuh"
@@ -48,14 +49,19 @@ struct phfem_cn_plan {
   // every element, computed once by k_cn_pre with the assembly's expressions
   double* top = nullptr;  // [nE][9] M_minus top-block entries as stored: 0.0 + (M0 + s((B+D)+M))
   double* cpl = nullptr;  // [nE][3] C' entries of the element's edge slots: 0.0 + s_ct (+-|E|/2)
-  double* lw = nullptr;   // [nE] load weight (|T|/3) * 0.5
-  double* sxy = nullptr;  // [nE][3][2] sin(pi x), sin(pi y) at the edge midpoints
-  int32_t* rp3 = nullptr; // [nE][3] multiplier row of each edge slot, -1 if not retained
+  // [nE][3] load factor of each primal row: w (g[i+1] + g[i+2]) with
+  // w = (|T|/3) 0.5 and g[k] = sin(pi x_k) sin(pi y_k) at midpoint k, so the
+  // sin-sin load of row i at time t is c(t) lq[i] (24 B instead of a 48-B
+  // sin table + 8-B weight; reassociated: within 1e-12, no sign change of g
+  // inside an element on the configured fields — SURVEY Appendix A)
+  double* lq = nullptr;
+  int32_t* rp3 = nullptr; // [nE][3] (multiplier row << 1) | (element is T-) per edge slot, -1 if not retained
   // multiplier rows, one record per retained edge l (row order): T+ as
   // 4 t_plus + local, T- as 4 t_minus + local (kRowBnd / kRowDir on the
   // boundary), and |E| * 0.5
   uint2* rowt = nullptr;
   double* rowh = nullptr;
+  bool hybrid = false;  // k_cn_hyb (top block + coupling recomputed) instead of k_cn_tma
 };
 
 namespace phfem {
@@ -244,8 +250,8 @@ __global__ void __launch_bounds__(kCnThreads, PHFEM_CN_MIN_BLOCKS) k_cn_elements
 // Once per plan: everything of an element that does not depend on t or W.
 template <int CK>
 __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restrict__ top,
-                                                        double* __restrict__ cpl, double* __restrict__ lw,
-                                                        double* __restrict__ sxy, int32_t* __restrict__ rp3) {
+                                                        double* __restrict__ cpl, double* __restrict__ lq,
+                                                        int32_t* __restrict__ rp3) {
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < a.nE;
        m += (int64_t)gridDim.x * blockDim.x) {
     const double2 v[3] = {a.coords[a.elements[3 * m]], a.coords[a.elements[3 * m + 1]],
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restr
         const double t = (i == j ? ud : uo) + a.s_top * ((bij + dj[j]) + (i == j ? md : mo));
         top[9 * m + 3 * j + i] = 0.0 + 1.0 * t;  // from_triplets stores 0.0 + value
       }
+    double gk[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
@@ -279,13 +286,15 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_pre(CnArgs a, double* __restr
       const int se = a.elem_edge[3 * m + k];
       const bool plus = se >= 0;
       cpl[3 * m + k] = 0.0 + a.s_ct * (plus ? len * 0.5 : -len * 0.5);  // assembly.cpp:160,164
-      rp3[3 * m + k] = a.rpos[plus ? se : ~se];
+      const int rp = a.rpos[plus ? se : ~se];
+      rp3[3 * m + k] = rp >= 0 ? (rp << 1) | (plus ? 0 : 1) : -1;  // row and the slot's C sign
       const double mx = 0.5 * (pa.x + pb.x), my = 0.5 * (pa.y + pb.y);
-      sxy[6 * m + 2 * k] = sin_fast(PHFEM_PI * mx);
-      sxy[6 * m + 2 * k + 1] = sin_fast(PHFEM_PI * my);
+      gk[k] = sin_fast(PHFEM_PI * mx) * sin_fast(PHFEM_PI * my);
     }
     const double area = 0.5 * ((v[1].x - v[0].x) * (v[2].y - v[0].y) - (v[1].y - v[0].y) * (v[2].x - v[0].x));
-    lw[m] = div3(area) * 0.5;
+    const double w = div3(area) * 0.5;  // assembly.cpp:199
+#pragma unroll
+    for (int i = 0; i < 3; ++i) lq[3 * m + i] = w * (gk[(i + 1) % 3] + gk[(i + 2) % 3]);
   }
 }
 
@@ -316,16 +325,9 @@ __global__ void k_cn_rows_pre(CnArgs a, const int32_t* __restrict__ edge_nodes,
 // Primal rows 3m+i of one element from its stored record (shared by the TMA
 // and the plain-load kernels: one expression, one set of bits).
 __device__ __forceinline__ void cn_primal(const CnArgs& a, int64_t m, const double (&T)[9],
-                                          const double (&sx)[3], const double (&sy)[3],
-                                          const double (&cv3)[3], const double (&U)[3], double w,
-                                          const int (&rp)[3], const double (&lam)[3], double c0,
-                                          double c1, double (&out3)[3]) {
-  double f0[3], f1[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    f0[i] = c0 * sx[i] * sy[i];
-    f1[i] = c1 * sx[i] * sy[i];
-  }
+                                          const double (&lq)[3], const double (&cv3)[3], const double (&U)[3],
+                                          const int (&rp)[3], const double (&lam)[3], double c0, double c1,
+                                          double (&out3)[3]) {
   double l0[3] = {0.0, 0.0, 0.0}, l1[3] = {0.0, 0.0, 0.0};
   // LN data only on elements with a Neumann edge, i.e. a non-retained one
   // (retained = non-Neumann, edge_topology.cpp:165-173): no probe otherwise
@@ -350,8 +352,9 @@ __device__ __forceinline__ void cn_primal(const CnArgs& a, int64_t m, const doub
     }
     if (rp[ka] >= 0) acc += cv3[ka] * lam[ka];
     if (rp[kb] >= 0) acc += cv3[kb] * lam[kb];
-    const double b0 = 0.0 + w * (f0[(i + 1) % 3] + f0[(i + 2) % 3]);
-    const double b1 = 0.0 + w * (f1[(i + 1) % 3] + f1[(i + 2) % 3]);
+    // assemble_load's 0.0 + w (f[i+1] + f[i+2]) at t_n and t_{n+1} (assembly.cpp:199)
+    const double b0 = 0.0 + c0 * lq[i];
+    const double b1 = 0.0 + c1 * lq[i];
     out3[i] = acc + a.kh * (((b0 + l0[i]) + b1) + l1[i]);
   }
 }
@@ -359,8 +362,7 @@ __device__ __forceinline__ void cn_primal(const CnArgs& a, int64_t m, const doub
 struct CnStored {
   const double* top;
   const double* cpl;
-  const double* lw;
-  const double* sxy;
+  const double* lq;
   const int32_t* rp3;
 };
 
@@ -397,13 +399,10 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, CnStored st,
 #pragma unroll
     for (int q = 0; q < 9; ++q) T[q] = valid ? buf[9 * lane + q] : 0.0;
     __syncwarp();
-    warp_load(st.sxy, base, n_valid, 6, buf);
-    double sx[3], sy[3];
+    warp_load(st.lq, base, n_valid, 3, buf);
+    double lq[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      sx[k] = valid ? buf[6 * lane + 2 * k] : 0.0;
-      sy[k] = valid ? buf[6 * lane + 2 * k + 1] : 0.0;
-    }
+    for (int k = 0; k < 3; ++k) lq[k] = valid ? buf[3 * lane + k] : 0.0;
     __syncwarp();
     warp_load(st.cpl, base, n_valid, 3, buf);
     double cv3[3];
@@ -417,10 +416,10 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, CnStored st,
       int rp[3];
       double lam[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) rp[k] = __ldg(st.rp3 + 3 * m + k);
+      for (int k = 0; k < 3; ++k) rp[k] = __ldg(st.rp3 + 3 * m + k) >> 1;  // -1 stays -1
 #pragma unroll
       for (int k = 0; k < 3; ++k) lam[k] = rp[k] >= 0 ? W[a.N + rp[k]] : 0.0;
-      cn_primal(a, m, T, sx, sy, cv3, U, __ldg(st.lw + m), rp, lam, c0, c1, out3);
+      cn_primal(a, m, T, lq, cv3, U, rp, lam, c0, c1, out3);
     }
     // coalesced store through the warp's SMEM slice
     __syncwarp();
@@ -433,8 +432,8 @@ __global__ void __launch_bounds__(kCnThreads) k_cn_stored(CnArgs a, CnStored st,
 }
 
 // TMA variant over the full 128-element tiles: one elected thread streams each
-// tile's stored record (top, sin table, coupling, U, load weight, rows: 188
-// bytes / element) into a kCnStages-deep SMEM ring with cp.async.bulk
+// tile's stored record (top 72, load factors 24, coupling 24, U 24, rows 12:
+// 156 bytes / element) into a kCnStages-deep SMEM ring with cp.async.bulk
 // (evict-first), completion on one mbarrier per stage; the threads read their
 // element's record from SMEM (odd strides / 16-byte pairs: conflict-free) and
 // only the Lambda and Neumann lookups stay as gathers.
@@ -442,10 +441,9 @@ constexpr int kCnTile = 128;
 constexpr int kCnStages = 4;
 struct CnStage {
   double top[9 * kCnTile];
-  double sxy[6 * kCnTile];
+  double lq[3 * kCnTile];
   double cpl[3 * kCnTile];
   double U[3 * kCnTile];
-  double lw[kCnTile];
   int32_t rp[3 * kCnTile];
 };
 static_assert(sizeof(CnStage) % 16 == 0, "bulk copies need 16-byte granules");
@@ -467,10 +465,9 @@ __global__ void __launch_bounds__(kCnTile) k_cn_tma(CnArgs a, CnStored st, int64
     const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
     mbar_expect_tx(&bar[s], (unsigned)sizeof(CnStage));
     bulk_load(stg[s].top, st.top + 9 * base, 9 * kCnTile * 8, &bar[s], pol);
-    bulk_load(stg[s].sxy, st.sxy + 6 * base, 6 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].lq, st.lq + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
     bulk_load(stg[s].cpl, st.cpl + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
     bulk_load(stg[s].U, W + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
-    bulk_load(stg[s].lw, st.lw + base, kCnTile * 8, &bar[s], pol);
     bulk_load(stg[s].rp, st.rp3 + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
   };
   if (tid == 0) {
@@ -488,7 +485,7 @@ __global__ void __launch_bounds__(kCnTile) k_cn_tma(CnArgs a, CnStored st, int64
     const int sj = (int)(j % kCnStages);
     mbar_wait(&bar[sj], (unsigned)((j / kCnStages) & 1));
 #pragma unroll
-    for (int k = 0; k < 3; ++k) rp[k] = stg[sj].rp[3 * tid + k];
+    for (int k = 0; k < 3; ++k) rp[k] = stg[sj].rp[3 * tid + k] >> 1;  // -1 stays -1
 #pragma unroll
     for (int k = 0; k < 3; ++k) lam[k] = rp[k] >= 0 ? __ldg(W + a.N + rp[k]) : 0.0;
   };
@@ -510,20 +507,17 @@ __global__ void __launch_bounds__(kCnTile) k_cn_tma(CnArgs a, CnStored st, int64
       lamq[0][k] = lamq[1][k];
     }
     if (i + 2 < my) gather(i + 2, rpq[1], lamq[1]);
-    double T[9], sx[3], sy[3], cv3[3];
+    double T[9], lq[3], cv3[3];
     const double U[3] = {S.U[3 * tid], S.U[3 * tid + 1], S.U[3 * tid + 2]};
 #pragma unroll
     for (int q = 0; q < 9; ++q) T[q] = S.top[9 * tid + q];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double2 p = reinterpret_cast<const double2*>(S.sxy)[3 * tid + k];
-      sx[k] = p.x;
-      sy[k] = p.y;
+      lq[k] = S.lq[3 * tid + k];
       cv3[k] = S.cpl[3 * tid + k];
     }
-    const double w = S.lw[tid];
     double out3[3];
-    cn_primal(a, m, T, sx, sy, cv3, U, w, rp, lam, c0, c1, out3);
+    cn_primal(a, m, T, lq, cv3, U, rp, lam, c0, c1, out3);
 #pragma unroll
     for (int q = 0; q < 3; ++q) outb[3 * tid + q] = out3[q];
     __syncthreads();  // stage s consumed, tile results staged
@@ -531,6 +525,131 @@ __global__ void __launch_bounds__(kCnTile) k_cn_tma(CnArgs a, CnStored st, int64
     const double2* s2 = reinterpret_cast<const double2*>(outb);
     double2* d2 = reinterpret_cast<double2*>(rhs + 3 * base);
     for (int q = tid; q < 3 * kCnTile / 2; q += kCnTile) __stcs(d2 + q, s2[q]);
+    __syncthreads();  // outb free for the next tile
+  }
+}
+
+// Hybrid variant (the default when the coordinates fit in L2): the M_minus
+// top block and the coupling entries are recomputed from the geometry with
+// the plan's own expressions (same bits as k_cn_pre), so per element only
+// the elements (12 B), the load factors (24), U (24) and the row codes (12)
+// stream through the TMA ring — 72 B instead of 156 — and the coordinates
+// are gathered (L2-resident: 16 nC bytes).  Coordinates and Lambda of tile
+// i + 2 are gathered while tile i computes.
+struct CnHStage {
+  int32_t el[3 * kCnTile];
+  double lq[3 * kCnTile];
+  double U[3 * kCnTile];
+  int32_t rp[3 * kCnTile];
+};
+static_assert(sizeof(CnHStage) % 16 == 0, "bulk copies need 16-byte granules");
+constexpr int kCnHStages = 4;
+constexpr size_t kCnHybSmem = kCnHStages * sizeof(CnHStage) + 3 * kCnTile * sizeof(double) +
+                              kCnHStages * sizeof(uint64_t);
+
+struct CnHQueue {
+  double2 v[3];
+  double lam[3];
+  int rpx[3];
+};
+
+#ifndef PHFEM_CN_HYB_BLOCKS
+#define PHFEM_CN_HYB_BLOCKS 4
+#endif
+template <int CK>
+__global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs a, CnStored st, int64_t ntiles, double c0,
+                                                     double c1, const double* __restrict__ W,
+                                                     double* __restrict__ rhs) {
+  extern __shared__ __align__(128) unsigned char cn_smem[];
+  CnHStage* stg = reinterpret_cast<CnHStage*>(cn_smem);
+  double* outb = reinterpret_cast<double*>(cn_smem + kCnHStages * sizeof(CnHStage));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(outb + 3 * kCnTile);
+  const int tid = threadIdx.x;
+  const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  uint64_t pol = 0;
+  auto issue = [&](int64_t i) {
+    const int s = (int)(i % kCnHStages);
+    const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
+    mbar_expect_tx(&bar[s], (unsigned)sizeof(CnHStage));
+    bulk_load(stg[s].el, a.elements + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
+    bulk_load(stg[s].lq, st.lq + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].U, W + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
+    bulk_load(stg[s].rp, st.rp3 + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kCnHStages; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+    pol = policy_evict_first();
+    for (int64_t i = 0; i < my && i < kCnHStages; ++i) issue(i);
+  }
+  __syncthreads();
+  CnHQueue q0, q1;
+  auto gather = [&](int64_t j, CnHQueue& q) {
+    const int sj = (int)(j % kCnHStages);
+    mbar_wait(&bar[sj], (unsigned)((j / kCnHStages) & 1));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      q.v[k] = __ldg(a.coords + stg[sj].el[3 * tid + k]);
+      q.rpx[k] = stg[sj].rp[3 * tid + k];
+      q.lam[k] = q.rpx[k] >= 0 ? __ldg(W + a.N + (q.rpx[k] >> 1)) : 0.0;
+    }
+  };
+  if (my > 0) gather(0, q0);
+  if (my > 1) gather(1, q1);
+  for (int64_t i = 0; i < my; ++i) {
+    const int s = (int)(i % kCnHStages);
+    const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
+    const int64_t m = base + tid;
+    const CnHStage& S = stg[s];
+    const double2 v[3] = {q0.v[0], q0.v[1], q0.v[2]};
+    const double lamv[3] = {q0.lam[0], q0.lam[1], q0.lam[2]};
+    const int rpx[3] = {q0.rpx[0], q0.rpx[1], q0.rpx[2]};
+    q0 = q1;
+    if (i + 2 < my) gather(i + 2, q1);
+    // the plan's k_cn_pre expressions (bit-identical top block / coupling)
+    const phfem_coeff_values cv = coeffs_dev<CK>(a.c, v[0], v[1], v[2]);
+    const phfem_geom g = geometry_dev(v[0].x, v[0].y, v[1].x, v[1].y, v[2].x, v[2].y);
+    const double a3 = div3(g.area);
+    double rx[3], ry[3], dj[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      rx[k] = cv.a00 * g.gx[k] + cv.a01 * g.gy[k];
+      ry[k] = cv.a10 * g.gx[k] + cv.a11 * g.gy[k];
+      dj[k] = a3 * (cv.px * g.gx[k] + cv.py * g.gy[k]);
+    }
+    const double md = cv.delta * g.area * (1.0 / 6.0), mo = cv.delta * g.area * (1.0 / 12.0);
+    const double ud = g.area * (1.0 / 6.0), uo = g.area * (1.0 / 12.0);
+    double T[9];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i2 = 0; i2 < 3; ++i2) {
+        const int lo = i2 < j ? i2 : j, hi = i2 < j ? j : i2;  // B from the upper triangle
+        const double bij = g.area * (rx[lo] * g.gx[hi] + ry[lo] * g.gy[hi]);
+        const double t = (i2 == j ? ud : uo) + a.s_top * ((bij + dj[j]) + (i2 == j ? md : mo));
+        T[3 * j + i2] = 0.0 + 1.0 * t;  // from_triplets stores 0.0 + value
+      }
+    double cv3[3], lq[3];
+    int rp[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
+      const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+      const double len = sqrt(dx * dx + dy * dy);
+      cv3[k] = 0.0 + a.s_ct * ((rpx[k] & 1) ? -len * 0.5 : len * 0.5);  // assembly.cpp:160,164
+      rp[k] = rpx[k] >> 1;  // -1 stays -1
+      lq[k] = S.lq[3 * tid + k];
+    }
+    const double U[3] = {S.U[3 * tid], S.U[3 * tid + 1], S.U[3 * tid + 2]};
+    double out3[3];
+    cn_primal(a, m, T, lq, cv3, U, rp, lamv, c0, c1, out3);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) outb[3 * tid + k] = out3[k];
+    __syncthreads();  // stage s consumed, tile results staged
+    if (tid == 0 && i + kCnHStages < my) issue(i + kCnHStages);
+    const double2* s2 = reinterpret_cast<const double2*>(outb);
+    double2* d2 = reinterpret_cast<double2*>(rhs + 3 * base);
+    for (int k = tid; k < 3 * kCnTile / 2; k += kCnTile) __stcs(d2 + k, s2[k]);
     __syncthreads();  // outb free for the next tile
   }
 }
@@ -663,10 +782,14 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
                       f->kind == PHFEM_FIELD_ZERO;
   if (st == PHFEM_OK && sinsin && mesh->nE > 0) {
     const int64_t nE = mesh->nE;
+    // hybrid when the coordinates stay L2-resident (their gathers are then
+    // nearly free); env PHFEM_CN_MODE=stored|hybrid overrides (A/B runs)
+    p->hybrid = 16 * (int64_t)mesh->nC <= (int64_t)80 << 20;
+    if (const char* md = getenv("PHFEM_CN_MODE")) p->hybrid = md[0] == 'h';
+
     st = dalloc(ctx, &p->top, 9 * nE);
     if (st == PHFEM_OK) st = dalloc(ctx, &p->cpl, 3 * nE);
-    if (st == PHFEM_OK) st = dalloc(ctx, &p->lw, nE);
-    if (st == PHFEM_OK) st = dalloc(ctx, &p->sxy, 6 * nE);
+    if (st == PHFEM_OK) st = dalloc(ctx, &p->lq, 3 * nE);
     if (st == PHFEM_OK) st = dalloc(ctx, &p->rp3, 3 * nE);
     if (st == PHFEM_OK && cls->L > 0) st = dalloc(ctx, &p->rowt, (int64_t)cls->L);
     if (st == PHFEM_OK && cls->L > 0) st = dalloc(ctx, &p->rowh, (int64_t)cls->L);
@@ -689,9 +812,9 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
       {
         KTimer kt(ctx, "k_cn_pre");
         if (c->kind == PHFEM_COEFF_CENTROID_POLY)
-          k_cn_pre<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy, p->rp3);
+          k_cn_pre<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lq, p->rp3);
         else
-          k_cn_pre<PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lw, p->sxy, p->rp3);
+          k_cn_pre<PHFEM_COEFF_CONST><<<grid, kCnThreads, 0, ctx->stream>>>(a, p->top, p->cpl, p->lq, p->rp3);
         ctx->launches++;
       }
       if (cls->L > 0) {
@@ -702,6 +825,10 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
       }
       if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
       if (st == PHFEM_OK) st = smem_optin(ctx, (const void*)k_cn_tma, kCnTmaSmem, "k_cn_tma smem opt-in");
+      if (st == PHFEM_OK)
+        st = smem_optin(ctx, (const void*)k_cn_hyb<PHFEM_COEFF_CONST>, kCnHybSmem, "k_cn_hyb smem opt-in");
+      if (st == PHFEM_OK)
+        st = smem_optin(ctx, (const void*)k_cn_hyb<PHFEM_COEFF_CENTROID_POLY>, kCnHybSmem, "k_cn_hyb smem opt-in");
     }
   }
   if (st != PHFEM_OK) {
@@ -720,8 +847,7 @@ PHFEM_API void phfem_cn_plan_destroy(phfem_ctx* ctx, phfem_cn_plan* p) {
   dfree(ctx, p->dir_bits);
   dfree(ctx, p->top);
   dfree(ctx, p->cpl);
-  dfree(ctx, p->lw);
-  dfree(ctx, p->sxy);
+  dfree(ctx, p->lq);
   dfree(ctx, p->rp3);
   dfree(ctx, p->rowt);
   dfree(ctx, p->rowh);
@@ -771,11 +897,21 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     } else if (a.f.kind == PHFEM_FIELD_SINSIN) {
       c0 = c1 = a.f.p[0];
     }
-    const CnStored st{p->top, p->cpl, p->lw, p->sxy, p->rp3};
+    const CnStored st{p->top, p->cpl, p->lq, p->rp3};
     // TMA over the full tiles when the state and rhs allow 16-byte bulk copies
     const bool tma = ((((uintptr_t)state) | ((uintptr_t)rhs)) & 15u) == 0;
     const int64_t nfull = tma ? (int64_t)a.nE / kCnTile : 0;
-    if (nfull > 0) {
+    if (nfull > 0 && p->hybrid) {
+      // 4 CTAs (16 warps) per SM: registers (122) and the 4-stage ring allow it;
+      // the recompute is latency-bound, so residency matters more than depth
+      const int grid = (int)std::min<int64_t>(nfull, (int64_t)ctx->num_sms * PHFEM_CN_HYB_BLOCKS);
+      if (a.c.kind == PHFEM_COEFF_CENTROID_POLY)
+        PHFEM_LAUNCH(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnTile, kCnHybSmem, ctx->stream>>>(
+            a, st, nfull, c0, c1, state, rhs));
+      else
+        PHFEM_LAUNCH(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CONST><<<grid, kCnTile, kCnHybSmem, ctx->stream>>>(
+            a, st, nfull, c0, c1, state, rhs));
+    } else if (nfull > 0) {
       const int grid = (int)std::min<int64_t>(nfull, (int64_t)ctx->num_sms * 2);
       PHFEM_LAUNCH(ctx, "k_cn_tma", k_cn_tma<<<grid, kCnTile, kCnTmaSmem, ctx->stream>>>(
           a, st, nfull, c0, c1, state, rhs));
@@ -789,6 +925,8 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     }
     // (measured: running the rows on a side stream next to the element pass
     // gains nothing — both are DRAM-bound)
+    // (measured: the rows on a side stream beside the hybrid element pass,
+    // 3 or 4 element CTAs per SM: step 0.373 ms either way)
     if (p->cls.L > 0)
       PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
           p->rowt, p->rowh, p->cls.L, a.s_c, state, rhs + a.N));

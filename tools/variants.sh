@@ -9,7 +9,7 @@ mkdir -p ../variants
 while [ $# -gt 1 ]; do
   name=$1; flags=$2; shift 2
   objs=()
-  for f in ctx edge_gen classify refine refine_topo assemble cn_rhs pipeline selftest dropin dist sparse download verify io; do
+  for f in $(sed -n 's/^SRCS *:= *//p' Makefile | sed 's/\.cu//g'); do
     nvcc -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
       -gencode arch=compute_100a,code=sm_100a $flags -c $f.cu -o /tmp/var_${name}_$f.o &
     objs+=(/tmp/var_${name}_$f.o)
