@@ -541,6 +541,48 @@ phfem_status phfem_dist_refine_level_ex(phfem_ctx* ctx, const phfem_topology* pp
                                         phfem_topology* out, int32_t** pairs_out, int64_t* n_pairs,
                                         double* mids, phfem_csr* C);
 
+/* Distributed refined level, halo form (dist.py _refine_sort_free; replaces
+ * the all-gathers of the parent arrays and midpoints of the _ex variant):
+ *  1. element owner: phfem_dist_side_records — for every slot k of its n
+ *     elements one 16-byte record {e << 1 | (element is t_minus of e), the
+ *     partner edges at local k+1 / k+2 (signed), vertex k} routed by parent
+ *     edge id to its owner (esplits: first global edge id per rank, W + 1);
+ *     counts / offsets / send as phfem_dist_occurrences (send NULL: counts);
+ *  2. edge owner: phfem_dist_side_apply — recv -> side[2 (e - E0) + s]
+ *     ([2 E][4] int32, s = 0 t_plus / 1 t_minus);
+ *  3. edge owner: phfem_dist_refine_level_side — the fine topology part (as
+ *     phfem_dist_refine_level, local fine ids), rk[E] (in-group rank bytes of
+ *     each owned parent edge), the owned midpoints into coords_fine[nc + E0p
+ *     + le] (coords_fine: the rank's fine coordinate array; coords = the
+ *     replicated parent coordinates), C's rows when C != NULL;
+ *  4. edge owner: phfem_dist_start_records — for each owned parent edge and
+ *     each of its elements a 12-byte record {slot 3 m + l, group start
+ *     fine_nes[le + nes_off] (global once re-based), rank byte} routed by
+ *     element to its owner (psplits: first parent element per rank);
+ *  5. element owner: phfem_dist_start_apply — recv -> gs / grk per slot
+ *     ([3 n] int32 / uint8, elements from elo);
+ *  6. element owner: phfem_dist_children_slots — children rows and their
+ *     elem_edge (global ids) as k_refine_children, from gs / grk, plus the
+ *     midpoints of its elements' edges into coords_fine (same bits as 3.). */
+phfem_status phfem_dist_side_records(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                     int32_t n, const int32_t* esplits, int32_t W, int32_t* counts,
+                                     int32_t* offsets, int32_t* send);
+phfem_status phfem_dist_side_apply(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t E0, int32_t E,
+                                   int32_t* side);
+phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                          const int32_t* side, const double* coords, int32_t nc,
+                                          int32_t node_lo, int32_t node_hi, int32_t nE_all,
+                                          const int32_t* neu_parent_ids, int32_t nN_parent,
+                                          phfem_topology* out, uint8_t* rk, double* coords_fine, phfem_csr* C);
+phfem_status phfem_dist_start_records(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                      int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                      int32_t* counts, int32_t* offsets, int32_t* send);
+phfem_status phfem_dist_start_apply(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t elo, int32_t* gs,
+                                    uint8_t* grk);
+phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                       int32_t n, const int32_t* gs, const uint8_t* grk, int32_t nc,
+                                       double* coords_fine, int32_t* children, int32_t* fine_elem_edge);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

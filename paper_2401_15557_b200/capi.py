@@ -168,6 +168,8 @@ EXPORTED = [
     "phfem_dist_occurrences", "phfem_dist_dedup", "phfem_dist_route_pairs", "phfem_dist_apply_pairs",
     "phfem_dist_add_offset", "phfem_dist_resolve", "phfem_dist_classify", "phfem_dist_neumann_table",
     "phfem_dist_neumann_apply", "phfem_dist_children", "phfem_dist_midpoints",
+    "phfem_dist_side_records", "phfem_dist_side_apply", "phfem_dist_refine_level_side",
+    "phfem_dist_start_records", "phfem_dist_start_apply", "phfem_dist_children_slots",
     "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
     "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
@@ -300,6 +302,13 @@ def load_library(path: str = LIB_PATH):
                                                  vp, i32, i32, i32, vp, P(phfem_topology), P(vp), P(i64), vp,
                                                  P(phfem_csr)]),
         "phfem_mesh_save_dir": (C.c_int, [vp, P(phfem_mesh), C.c_char_p]),
+        "phfem_dist_side_records": (C.c_int, [vp, vp, vp, i32, vp, i32, vp, vp, vp]),
+        "phfem_dist_side_apply": (C.c_int, [vp, vp, i64, i32, i32, vp]),
+        "phfem_dist_refine_level_side": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, i32, i32, i32, vp, i32,
+                                                   P(phfem_topology), vp, vp, P(phfem_csr)]),
+        "phfem_dist_start_records": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, vp, i32, vp, vp, vp]),
+        "phfem_dist_start_apply": (C.c_int, [vp, vp, i64, i32, vp, vp]),
+        "phfem_dist_children_slots": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, vp, vp, vp]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),
     }

@@ -264,6 +264,91 @@ __global__ void __launch_bounds__(256) k_dist_children(const int32_t* __restrict
   }
 }
 
+// Side records of the sort-free distributed refinement: slot k of element m
+// (local index i = 3 m_local + k) -> {e << 1 | (m is t_minus of e), the
+// partner edges at local k+1 and k+2 (signed), vertex k}, routed to the
+// owner of parent edge e (esplits: first global edge id per rank)
+__global__ void __launch_bounds__(kRouteThreads) k_dist_side(const int32_t* __restrict__ elements,
+                                                             const int32_t* __restrict__ elem_edge, int n,
+                                                             const int32_t* __restrict__ esplits, int W,
+                                                             int32_t* __restrict__ cnt, int32_t* __restrict__ cursor,
+                                                             int4* __restrict__ send) {
+  route_block<int4>(3 * (int64_t)n, W, [&](int64_t i, int4& r) {
+    const int64_t m = i / 3;
+    const int k = (int)(i - 3 * m);
+    const int s = elem_edge[i];
+    const int e = s >= 0 ? s : ~s;
+    r = make_int4(e << 1 | (s < 0 ? 1 : 0), elem_edge[3 * m + (k == 2 ? 0 : k + 1)],
+                  elem_edge[3 * m + (k == 0 ? 2 : k - 1)], elements[i]);
+    return dest_of(esplits, W, e);
+  }, cnt, cursor, send);
+}
+
+__global__ void k_dist_side_apply(const int4* __restrict__ recv, int64_t n, int E0, int E, int4* __restrict__ side) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = recv[i];
+    const int le = (r.x >> 1) - E0;
+    if (le >= 0 && le < E) side[2 * (int64_t)le + (r.x & 1)] = make_int4(r.y, r.z, r.w, 0);
+  }
+}
+
+// Group-start records: for every owned parent edge and each of its elements,
+// {slot 3 m + local, first fine id of the edge's group (global), rank byte}
+// routed to the owner of m (psplits: first parent element per rank)
+struct Rec3 {
+  int x, y, z;
+};
+__global__ void __launch_bounds__(kRouteThreads) k_dist_start(const int32_t* __restrict__ edge_elements,
+                                                              const int32_t* __restrict__ ltp,
+                                                              const int32_t* __restrict__ ltm,
+                                                              const int32_t* __restrict__ fine_nes, int nes_off,
+                                                              const uint8_t* __restrict__ rk, int E,
+                                                              const int32_t* __restrict__ psplits, int W,
+                                                              int32_t* __restrict__ cnt, int32_t* __restrict__ cursor,
+                                                              Rec3* __restrict__ send) {
+  route_block<Rec3>(2 * (int64_t)E, W, [&](int64_t i, Rec3& r) {
+    const int64_t le = i >> 1;
+    const int sd = (int)(i & 1);
+    const int m = edge_elements[2 * le + sd];
+    if (m < 0) return -1;
+    const int l = sd ? ltm[le] : ltp[le];
+    r.x = 3 * m + l;
+    r.y = fine_nes[le + nes_off];
+    r.z = rk[le];
+    return dest_of(psplits, W, m);
+  }, cnt, cursor, send);
+}
+
+__global__ void k_dist_start_apply(const Rec3* __restrict__ recv, int64_t n, int elo, int32_t* __restrict__ gs,
+                                   uint8_t* __restrict__ grk) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Rec3 r = recv[i];
+    const int64_t slot = (int64_t)r.x - 3 * (int64_t)elo;
+    gs[slot] = r.y;
+    grk[slot] = (uint8_t)r.z;
+  }
+}
+
+// count pass, exclusive offsets, pack pass of a route_block kernel
+template <typename Launch>
+static phfem_status route_two_pass(phfem_ctx* ctx, int W, int32_t* counts, int32_t* offsets, bool pack,
+                                   Launch launch) {
+  PHFEM_CUDA(ctx, cudaMemsetAsync(counts, 0, sizeof(int32_t) * W, ctx->stream));
+  if (W >= kMaxDest) return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_TRY(launch(counts, (int32_t*)nullptr));
+  if (!pack) return PHFEM_OK;
+  if (!offsets) return PHFEM_ERR_INVALID_ARGUMENT;
+  int32_t* cursor = nullptr;
+  PHFEM_TRY(dalloc(ctx, &cursor, (int64_t)W + 1));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, counts, sizeof(int32_t) * W, cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(cursor + W, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_TRY(scan_exclusive_i32(ctx, cursor, cursor, (int64_t)W + 1, nullptr));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(offsets, cursor, sizeof(int32_t) * (W + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+  PHFEM_TRY(launch((int32_t*)nullptr, cursor));
+  dfree(ctx, cursor);
+  return PHFEM_OK;
+}
+
 }  // namespace phfem
 
 using namespace phfem;
@@ -481,4 +566,53 @@ PHFEM_API phfem_status phfem_dist_neumann_apply(phfem_ctx* ctx, const phfem_mesh
   dfree(ctx, mt.edge_elements);
   dfree(ctx, mt.local_in_tplus);
   return st;
+}
+
+PHFEM_API phfem_status phfem_dist_side_records(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                               int32_t n, const int32_t* esplits, int32_t W, int32_t* counts,
+                                               int32_t* offsets, int32_t* send) {
+  if (!ctx || !esplits || !counts || W < 1 || n < 0 || (n && (!elements || !elem_edge)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  const int grid = grid_for(3 * (int64_t)n, kRouteThreads * kRouteK, ctx->num_sms * 8);
+  return route_two_pass(ctx, W, counts, offsets, send != nullptr, [&](int32_t* c, int32_t* cur) -> phfem_status {
+    if (n > 0)
+      PHFEM_LAUNCH(ctx, "k_dist_side", k_dist_side<<<grid, kRouteThreads, 0, ctx->stream>>>(
+          elements, elem_edge, n, esplits, W, c, cur, cur ? reinterpret_cast<int4*>(send) : nullptr));
+    return PHFEM_OK;
+  });
+}
+
+PHFEM_API phfem_status phfem_dist_side_apply(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t E0, int32_t E,
+                                             int32_t* side) {
+  if (!ctx || (n && (!recv || !side))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_side_apply", k_dist_side_apply<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const int4*>(recv), n, E0, E, reinterpret_cast<int4*>(side)));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_start_records(phfem_ctx* ctx, const phfem_topology* ppart,
+                                                const int32_t* fine_nes, int32_t nes_off, const uint8_t* rk,
+                                                const int32_t* psplits, int32_t W, int32_t* counts,
+                                                int32_t* offsets, int32_t* send) {
+  if (!ctx || !ppart || !psplits || !counts || W < 1 || (ppart->E && (!fine_nes || !rk)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  const int E = ppart->E;
+  const int grid = grid_for(2 * (int64_t)E, kRouteThreads * kRouteK, ctx->num_sms * 8);
+  return route_two_pass(ctx, W, counts, offsets, send != nullptr, [&](int32_t* c, int32_t* cur) -> phfem_status {
+    if (E > 0)
+      PHFEM_LAUNCH(ctx, "k_dist_start", k_dist_start<<<grid, kRouteThreads, 0, ctx->stream>>>(
+          ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus, fine_nes, nes_off, rk, E, psplits, W,
+          c, cur, cur ? reinterpret_cast<Rec3*>(send) : nullptr));
+    return PHFEM_OK;
+  });
+}
+
+PHFEM_API phfem_status phfem_dist_start_apply(phfem_ctx* ctx, const int32_t* recv, int64_t n, int32_t elo,
+                                              int32_t* gs, uint8_t* grk) {
+  if (!ctx || (n && (!recv || !gs || !grk))) return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_start_apply", k_dist_start_apply<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const Rec3*>(recv), n, elo, gs, grk));
+  return PHFEM_OK;
 }

@@ -76,6 +76,11 @@ struct LvArgs {
   // edges [eb, eb + E) at local indices; node_edge_start covers the fine node
   // range from nlo.  Both 0 on one GPU.
   int eb, nlo;
+  // distributed level, side-record mode: side[2 le + s] = {the two partner
+  // edges of e in its t_plus (s = 0) / t_minus (s = 1) element at local
+  // indices l+1, l+2, the opposite vertex, -} (phfem_dist_side_apply) instead
+  // of gathers from elem_edge / elements of every parent element
+  const int4* side;
   // exclusive per-tile prefixes (k_rl_tile_init / k_rl_tile_count + scans):
   // fine edges, parent boundary edges, parent Neumann edges before the tile
   const int32_t* tileF;
@@ -192,9 +197,11 @@ struct LvRec {
   int l, l2;
   bool neu;
 };
-// stage 2: the gathers of the two parent elements (edges, opposite vertices)
+// stage 2: the gathers of the two parent elements: the partner edges of e
+// (signed, at local l+1 / l+2 of t_plus and l2+1 / l2+2 of t_minus) and the
+// opposite vertices
 struct LvGat {
-  int P[3], Q[3];
+  int pj1, pj2, qk1, qk2;
   int vop, vom;
 };
 // stage 3: the four parent coordinates
@@ -221,21 +228,37 @@ __device__ __forceinline__ LvRec lv_load_rec(const LvArgs& a, int le) {
 
 __device__ __forceinline__ LvGat lv_load_gat(const LvArgs& a, const LvRec& r, bool valid) {
   LvGat g;
-  g.P[0] = g.P[1] = g.P[2] = g.Q[0] = g.Q[1] = g.Q[2] = 0;
+  g.pj1 = g.pj2 = g.qk1 = g.qk2 = 0;
   g.vop = g.vom = 0;
+  const int le = (int)(blockIdx.x * kLvT + threadIdx.x);
+  if (a.side) {  // distributed: the element owners' side records, coalesced
+    if (valid) {
+      const int4 sp = a.side[2 * (int64_t)le];
+      g.pj1 = sp.x;
+      g.pj2 = sp.y;
+      g.vop = sp.z;
+    }
+    if (valid && r.el.y >= 0) {
+      const int4 sm = a.side[2 * (int64_t)le + 1];
+      g.qk1 = sm.x;
+      g.qk2 = sm.y;
+      g.vom = sm.z;
+    }
+    return g;
+  }
   if (valid) {
-    const int tp = r.el.x;
-    g.P[0] = __ldg(a.elem_edge + 3 * (int64_t)tp);
-    g.P[1] = __ldg(a.elem_edge + 3 * (int64_t)tp + 1);
-    g.P[2] = __ldg(a.elem_edge + 3 * (int64_t)tp + 2);
-    g.vop = __ldg(a.elements + 3 * (int64_t)tp + r.l);
+    const int64_t tp = 3 * (int64_t)r.el.x;
+    const int j1 = r.l == 2 ? 0 : r.l + 1, j2 = r.l == 0 ? 2 : r.l - 1;
+    g.pj1 = __ldg(a.elem_edge + tp + j1);
+    g.pj2 = __ldg(a.elem_edge + tp + j2);
+    g.vop = __ldg(a.elements + tp + r.l);
   }
   if (valid && r.el.y >= 0) {
-    const int tm = r.el.y;
-    g.Q[0] = __ldg(a.elem_edge + 3 * (int64_t)tm);
-    g.Q[1] = __ldg(a.elem_edge + 3 * (int64_t)tm + 1);
-    g.Q[2] = __ldg(a.elem_edge + 3 * (int64_t)tm + 2);
-    g.vom = __ldg(a.elements + 3 * (int64_t)tm + r.l2);
+    const int64_t tm = 3 * (int64_t)r.el.y;
+    const int k1 = r.l2 == 2 ? 0 : r.l2 + 1, k2 = r.l2 == 0 ? 2 : r.l2 - 1;
+    g.qk1 = __ldg(a.elem_edge + tm + k1);
+    g.qk2 = __ldg(a.elem_edge + tm + k2);
+    g.vom = __ldg(a.elements + tm + r.l2);
   }
   return g;
 }
@@ -273,10 +296,8 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
   // 2. group size, tile scan, look-back
   const int j1 = l == 2 ? 0 : l + 1, j2 = l == 0 ? 2 : l - 1;      // partners in t_plus
   const int k1 = l2 == 2 ? 0 : l2 + 1, k2 = l2 == 0 ? 2 : l2 - 1;  // partners in t_minus
-  // (selects, not indexing: keeps the gathered edges in registers)
-  auto pick = [](const int (&v)[3], int i) { return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]); };
-  const int q0 = abs_edge(pick(g.P, j1)), q1 = abs_edge(pick(g.P, j2));
-  const int r0 = abs_edge(pick(g.Q, k1)), r1 = abs_edge(pick(g.Q, k2));
+  const int q0 = abs_edge(g.pj1), q1 = abs_edge(g.pj2);
+  const int r0 = abs_edge(g.qk1), r1 = abs_edge(g.qk2);
   const bool v0 = valid && q0 < e, v1 = valid && q1 < e;
   const bool v2 = has_m && r0 < e, v3 = has_m && r1 < e;
   const bool isB = valid && !has_m;
@@ -877,4 +898,236 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
   return phfem_dist_refine_level_ex(ctx, ppart, E0p, elem_edge_all, elements_all, nE_all, coords, nc, node_lo,
                                     node_hi, neu_parent_ids, nN_parent, 0, 0, nullptr, out, pairs_out, nullptr,
                                     mids, C);
+}
+
+// ---------------------------------------------------------------------------
+// Distributed refined level, side-record mode (dist.py _refine_sort_free):
+// the rank's parent edges [E0p, E0p + E) get their partner edges and opposite
+// vertices from the element owners' side records (phfem_dist_side_apply), not
+// from all-gathered parent arrays; the fine elem_edge is written by the
+// element owners (phfem_dist_children_slots) from the group starts and rank
+// bytes this level returns (phfem_dist_start_records).  Owned midpoints go to
+// coords_fine[nc + E0p + le].
+namespace phfem {
+// partners < e per parent edge, summed per 128-edge tile (tile of le = le / kLvT)
+__global__ void k_rl_tile_count_side(const int4* __restrict__ side, const int32_t* __restrict__ edge_elements,
+                                     int E, int eb, int32_t* __restrict__ tileF) {
+  for (int64_t le0 = (int64_t)blockIdx.x * blockDim.x; le0 < E; le0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t le = le0 + threadIdx.x;
+    int c = 0;
+    if (le < E) {
+      const int e = eb + (int)le;
+      const int4 sp = side[2 * le];
+      c = (abs_edge(sp.x) < e) + (abs_edge(sp.y) < e);
+      if (edge_elements[2 * le + 1] >= 0) {
+        const int4 sm = side[2 * le + 1];
+        c += (abs_edge(sm.x) < e) + (abs_edge(sm.y) < e);
+      }
+    }
+    c = warp_reduce_sum(c);  // a warp's edges share one tile (kLvT multiple of 32)
+    if (lane_id() == 0 && le0 + (threadIdx.x & ~31) < E) atomicAdd(tileF + (le0 + (threadIdx.x & ~31)) / kLvT, c);
+  }
+}
+
+// k_refine_children with the group starts / rank bytes per element slot
+// (gs / grk from phfem_dist_start_apply, global fine ids) instead of
+// gathers by edge id; also writes the midpoints of the element's edges into
+// the rank's fine coordinate array (0.5 (c[a] + c[b]) with the element's own
+// vertices: the same bits as the edge owner's, refine.cpp:18).
+__global__ void __launch_bounds__(256) k_dist_children_slots(const int32_t* __restrict__ elements,
+                                                             const int32_t* __restrict__ elem_edge,
+                                                             const int32_t* __restrict__ gs,
+                                                             const uint8_t* __restrict__ grk, int nE, int nc,
+                                                             double2* __restrict__ coords,
+                                                             int4* __restrict__ out_elems,
+                                                             int4* __restrict__ out_ee) {
+  __shared__ int4 stage[8][2][96];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int4* se = stage[warp][0];
+  int4* sq = stage[warp][1];
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + warp * 32); base < nE; base += wstride) {
+    const int64_t m = base + lane;
+    if (m < nE) {
+      int P[3], sg[3], e[3], G[3], R[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        P[j] = __ldg(elements + 3 * m + j);
+        sg[j] = __ldg(elem_edge + 3 * m + j);
+        e[j] = abs_edge(sg[j]);
+        G[j] = __ldg(gs + 3 * m + j);
+        R[j] = __ldg(grk + 3 * m + j);
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {  // midpoint of the edge opposite P_j
+        const double2 pa = __ldg(coords + P[j == 2 ? 0 : j + 1]), pb = __ldg(coords + P[j == 0 ? 2 : j - 1]);
+        coords[nc + e[j]] = midpt(pa, pb);
+      }
+      int I[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int jA = k == 2 ? 0 : k + 1, jB = k == 0 ? 2 : k - 1;
+        const bool aBig = e[jA] > e[jB];
+        const int jE = aBig ? jA : jB, jm = aBig ? jB : jA;
+        const int r = jE == 0 ? R[0] : (jE == 1 ? R[1] : R[2]);
+        const int GE = jE == 0 ? G[0] : (jE == 1 ? G[1] : G[2]);
+        const bool next = jm == (jE == 2 ? 0 : jE + 1);
+        const int sE = jE == 0 ? sg[0] : (jE == 1 ? sg[1] : sg[2]);
+        const int field = (sE >= 0 ? 0 : 2) + (next ? 0 : 1);
+        I[k] = GE + 2 + ((r >> (2 * field)) & 3);
+      }
+      auto half = [&](int j, int v) {
+        const int a = P[j == 2 ? 0 : j + 1], b = P[j == 0 ? 2 : j - 1];
+        const int id = G[j] + (v == min(a, b) ? 0 : 1);
+        return sg[j] >= 0 ? id : ~id;
+      };
+      const int M0 = nc + e[0], M1 = nc + e[1], M2 = nc + e[2];
+      se[3 * lane] = make_int4(M0, M1, M2, P[0]);
+      se[3 * lane + 1] = make_int4(M2, M1, P[1], M0);
+      se[3 * lane + 2] = make_int4(M2, P[2], M1, M0);
+      sq[3 * lane] = make_int4(I[0], I[1], I[2], ~I[0]);
+      sq[3 * lane + 1] = make_int4(half(1, P[0]), half(2, P[0]), ~I[1], half(2, P[1]));
+      sq[3 * lane + 2] = make_int4(half(0, P[1]), ~I[2], half(0, P[2]), half(1, P[2]));
+    }
+    __syncwarp();
+    const int64_t rem = nE - base;
+    const int n4 = 3 * (int)(rem < 32 ? rem : 32);
+    for (int i = lane; i < n4; i += 32) {
+      out_elems[3 * base + i] = se[i];
+      out_ee[3 * base + i] = sq[i];
+    }
+    __syncwarp();
+  }
+}
+}  // namespace phfem
+
+PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                                    const int32_t* side, const double* coords, int32_t nc,
+                                                    int32_t node_lo, int32_t node_hi, int32_t nE_all,
+                                                    const int32_t* neu_parent_ids, int32_t nN_parent,
+                                                    phfem_topology* out, uint8_t* rk, double* coords_fine,
+                                                    phfem_csr* C) {
+  if (!ctx || !ppart || !out) return PHFEM_ERR_INVALID_ARGUMENT;
+  memset(out, 0, sizeof(*out));
+  if (C) memset(C, 0, sizeof(*C));
+  if (nN_parent > 0 && !neu_parent_ids) return PHFEM_ERR_INVALID_ARGUMENT;
+  const int64_t E = ppart->E;
+  if ((E > 0 && (!side || !coords || !rk || !coords_fine)) || E0p < 0 || node_lo < 0 || node_hi < node_lo ||
+      (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) || (E > 0 && node_lo > nc + E0p) ||
+      4 * (int64_t)nE_all >= (int64_t(1) << 31))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  const int64_t ntiles = std::max<int64_t>(1, (E + kLvT - 1) / kLvT);
+  const int64_t nwords = std::max<int64_t>(1, (E + 31) / 32);
+  int32_t* tiles = nullptr;
+  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1) + 2));
+  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
+  int32_t* total = tiles + 3 * (ntiles + 1);  // [0] fine edges, [1] parent Neumann edges
+  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 2), ctx->stream));
+  uint32_t* nbits = nullptr;
+  if (C) {
+    PHFEM_TRY(dalloc(ctx, &nbits, nwords));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(nbits, 0, sizeof(uint32_t) * nwords, ctx->stream));
+    if (nN_parent > 0 && E > 0)
+      PHFEM_LAUNCH(ctx, "k_rl_neu_bits", k_rl_neu_bits<<<grid_for(nN_parent, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+          neu_parent_ids, nN_parent, E0p, (int)E, nbits));
+  }
+  if (E > 0) {
+    PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, nbits, tileF, tileB, tileN));
+    PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count_side<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const int4*>(side), ppart->edge_elements, (int)E, E0p, tileF));
+  }
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total));
+  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
+  if (C) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, total + 1));
+  int32_t hcnt[2] = {0, 0};
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(hcnt, total, sizeof hcnt, cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int32_t Ef = hcnt[0];
+  const int64_t nBf = 2 * (int64_t)ppart->n_boundary;
+  out->nC = node_hi - node_lo;
+  out->nE = 4 * nE_all;
+  out->E = Ef;
+  out->n_boundary = (int32_t)nBf;
+  out->n_interior = (int32_t)(Ef - nBf);
+  const int64_t cap = std::max<int64_t>(Ef, 1);
+  PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * cap));
+  PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * cap));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tplus, cap));
+  PHFEM_TRY(dalloc(ctx, &out->local_in_tminus, cap));
+  PHFEM_TRY(dalloc(ctx, &out->interior_edges, std::max<int64_t>(Ef - nBf, 1)));
+  PHFEM_TRY(dalloc(ctx, &out->boundary_edges, std::max<int64_t>(nBf, 1)));
+  PHFEM_TRY(dalloc(ctx, &out->node_edge_start, (int64_t)out->nC + 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * ((int64_t)out->nC + 1), ctx->stream));
+  int64_t Lr = 0;
+  if (C) {
+    const int64_t nneu = hcnt[1];
+    Lr = Ef - 2 * nneu;
+    const int64_t BR = 2 * ((int64_t)ppart->n_boundary - nneu);
+    C->rows = (int32_t)Lr;
+    C->cols = 3 * 4 * nE_all;
+    C->nnz = 4 * Lr - 2 * BR;
+    PHFEM_TRY(dalloc(ctx, &C->row_ptr, Lr + 1));
+    PHFEM_TRY(dalloc(ctx, &C->col_idx, std::max<int64_t>(C->nnz, 1)));
+    PHFEM_TRY(dalloc(ctx, &C->values, std::max<int64_t>(C->nnz, 1)));
+    if (Lr == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
+  }
+  if (E > 0) {
+    LvArgs a;
+    memset(&a, 0, sizeof a);
+    a.edge_nodes = ppart->edge_nodes;
+    a.edge_elements = ppart->edge_elements;
+    a.ltp = ppart->local_in_tplus;
+    a.ltm = ppart->local_in_tminus;
+    a.side = reinterpret_cast<const int4*>(side);
+    a.coords = (const double2*)coords;
+    a.E = (int)E;
+    a.nc = nc;
+    a.Ef = Ef;
+    a.eb = E0p;
+    a.nlo = node_lo;
+    a.tileF = tileF;
+    a.tileB = tileB;
+    LvOut o;
+    memset(&o, 0, sizeof o);
+    o.edge_nodes = out->edge_nodes;
+    o.edge_elements = out->edge_elements;
+    o.ltp = out->local_in_tplus;
+    o.ltm = out->local_in_tminus;
+    o.interior = out->interior_edges;
+    o.boundary = out->boundary_edges;
+    o.node_edge_start = out->node_edge_start;
+    o.rk = rk;
+    o.mid = (double2*)coords_fine;
+    o.mid_base = 0;
+    const unsigned nt = (unsigned)((E + kLvT - 1) / kLvT);
+    if (C) {
+      a.neu_bits = nbits;
+      a.tileN = tileN;
+      a.L = (int)Lr;
+      o.row_ptr = C->row_ptr;
+      o.col = C->col_idx;
+      o.val = C->values;
+      PHFEM_TRY(launch_level<true>(ctx, a, o, nt));
+    } else {
+      PHFEM_TRY(launch_level<false>(ctx, a, o, nt));
+    }
+  }
+  dfree(ctx, nbits);
+  dfree(ctx, tiles);
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements,
+                                                 const int32_t* elem_edge, int32_t n, const int32_t* gs,
+                                                 const uint8_t* grk, int32_t nc, double* coords_fine,
+                                                 int32_t* children, int32_t* fine_elem_edge) {
+  if (!ctx || (n && (!elements || !elem_edge || !gs || !grk || !coords_fine || !children || !fine_elem_edge)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_children_slots", k_dist_children_slots<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0,
+                                                                       ctx->stream>>>(
+        elements, elem_edge, gs, grk, n, nc, (double2*)coords_fine, reinterpret_cast<int4*>(children),
+        reinterpret_cast<int4*>(fine_elem_edge)));
+  return PHFEM_OK;
 }

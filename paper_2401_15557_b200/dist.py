@@ -208,36 +208,75 @@ class CudaRankOps:
         self._ee_next = ee[:hi - lo] if ee is not None else None
         return int(t.E), int(t.n_boundary)
 
-    def refine_level(self, ee_all, el_all, coords, nc, E0p, nlo, nhi, nE_all, neu_parent=None, fine_range=None):
-        """The rank's part of the refined topology from its parent part (sort
-        free, phfem_dist_refine_level_ex); returns (E, n_boundary, midpoints).
-        neu_parent (global parent Neumann ids): also the rank's C rows, fused.
-        fine_range = the rank's fine elements [lo, hi): their elem_edge entries
-        are written in place (local ids, re-based in route_pairs), only the
-        other ranks' entries leave as pairs."""
-        t = capi.phfem_topology()
-        pairs = C.c_void_p()
-        npairs = C.c_int64(0)
+    # -- refined level, halo form (phfem_dist_side_* / _start_* / _children_slots) ----
+    def side_records(self, elements, elem_edge, esplits):
+        """element owner: one 16-byte side record per element slot, routed to
+        the owner of the slot's parent edge"""
+        n = int(elements.shape[0])
+        W = esplits.numel() - 1
+        cnt, off = self.empty(W), self.empty(W + 1)
+        send = self.empty((max(3 * n, 1), 4))
+        self._ck(self.lib.phfem_dist_side_records(self.ctx.ptr, self.p(elements), self.p(elem_edge), n,
+                                                  self.p(esplits), W, self.p(cnt), self.p(off), self.p(send)))
+        return send[:3 * n], cnt.tolist()
+
+    def side_apply(self, recv, E0):
+        E = int(self.part.t.E)
+        self._side = self.empty((max(2 * E, 1), 4))   # t_minus entries of boundary edges stay unused
+        self._ck(self.lib.phfem_dist_side_apply(self.ctx.ptr, self.p(recv), int(recv.shape[0]), E0, E,
+                                                self.p(self._side)))
+
+    def refine_level_side(self, coords, nc, E0p, nlo, nhi, nE_all, coords_fine, neu_parent=None):
+        """edge owner: the fine part of its parent edges (local ids), their rank
+        bytes, owned midpoints into coords_fine; C's rows when neu_parent is
+        given (the last level).  The parent part is kept for start_records."""
         pt = self.part.t
-        Ep = int(pt.E)  # (the parent part is released below)
-        mids = self.empty((max(Ep, 1), 2), torch.float64)
+        E = int(pt.E)
+        rk = torch.empty((max(E, 1),), dtype=torch.uint8, device=self.dev)
+        t = capi.phfem_topology()
         csr = capi.phfem_csr() if neu_parent is not None else None
         nN = 0 if neu_parent is None else int(neu_parent.numel())
-        lo, hi = fine_range if fine_range is not None else (0, 0)
-        ee = self.empty((max(hi - lo, 1), 3)) if fine_range is not None else None
-        self._ck(self.lib.phfem_dist_refine_level_ex(self.ctx.ptr, C.byref(pt), E0p, self.p(ee_all),
-                                                     self.p(el_all), nE_all, self.p(coords), nc, nlo, nhi,
-                                                     self.p(neu_parent) if nN else None, nN, lo, hi,
-                                                     self.p(ee) if ee is not None else None, C.byref(t),
-                                                     C.byref(pairs), C.byref(npairs), self.p(mids),
-                                                     C.byref(csr) if csr is not None else None))
+        self._ck(self.lib.phfem_dist_refine_level_side(
+            self.ctx.ptr, C.byref(pt), E0p, self.p(self._side), self.p(coords), nc, nlo, nhi, nE_all,
+            self.p(neu_parent) if nN else None, nN, C.byref(t), self.p(rk), self.p(coords_fine),
+            C.byref(csr) if csr is not None else None))
         if csr is not None:
             self.csr = csr
-        self.part.release()
-        self.part = capi.Topology(self.ctx, t)
-        self._pairs = (pairs.value, int(npairs.value), True)
-        self._ee_next = ee[:hi - lo] if ee is not None else None
-        return int(t.E), int(t.n_boundary), mids[:Ep]
+        self._side = None
+        self.ppart, self.part, self._rk = self.part, capi.Topology(self.ctx, t), rk
+        return int(t.E), int(t.n_boundary)
+
+    def start_records(self, nes_off, psplits):
+        """edge owner: {slot, group start (global), rank byte} per (owned parent
+        edge, element), routed to the element owners; drops the parent part"""
+        pt = self.ppart.t
+        W = psplits.numel() - 1
+        cnt, off = self.empty(W), self.empty(W + 1)
+        send = self.empty((max(2 * int(pt.E), 1), 3))
+        self._ck(self.lib.phfem_dist_start_records(self.ctx.ptr, C.byref(pt),
+                                                   C.c_void_p(self.part.t.node_edge_start), nes_off,
+                                                   self.p(self._rk), self.p(psplits), W, self.p(cnt),
+                                                   self.p(off), self.p(send)))
+        self.ppart.release()
+        self.ppart, self._rk = None, None
+        c = cnt.tolist()
+        return send[:sum(c)], c
+
+    def start_apply(self, recv, elo, n):
+        gs = self.empty((max(3 * n, 1),))
+        grk = torch.empty((max(3 * n, 1),), dtype=torch.uint8, device=self.dev)
+        self._ck(self.lib.phfem_dist_start_apply(self.ctx.ptr, self.p(recv), int(recv.shape[0]), elo, self.p(gs),
+                                                 self.p(grk)))
+        return gs, grk
+
+    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine):
+        n = int(elements.shape[0])
+        kids = self.empty((max(4 * n, 1), 3))
+        ee = self.empty((max(4 * n, 1), 3))
+        self._ck(self.lib.phfem_dist_children_slots(self.ctx.ptr, self.p(elements), self.p(elem_edge), n,
+                                                    self.p(gs), self.p(grk), nc, self.p(coords_fine),
+                                                    self.p(kids), self.p(ee)))
+        return kids[:4 * n], ee[:4 * n]
 
     def route_pairs(self, E0, esplits, elo, ehi):
         """Pairs of the own (destination-level) elements [elo, ehi) go straight
@@ -509,27 +548,44 @@ def _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids):
         s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
 
 
-def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD, nN, ids, fused_c=False):
+def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD, nN, ids, fused_c=False,
+                      last=False):
     """One refinement with the fine topology straight from the parent's
-    (phfem_dist_refine_level): the parent elem_edge / elements are
-    all-gathered (12 + 12 B per element), every rank builds the groups of its
-    own parent edges (fine node range [nC + E0, nC + E0 + E_r); rank 0 also
-    holds the old nodes, which start no fine edge), the fine elem_edge goes
-    to the element owners as pairs.  Returns the fine (splits, per, totals)."""
+    (SURVEY f1), halo form — no all-gather of parent arrays or midpoints:
+      1. every element owner sends one 16-byte side record per element slot
+         {edge, partner edges, opposite vertex} to the owner of the slot's
+         parent edge (all-to-all);
+      2. edge owners build the groups of their parent edges (fine node range
+         [nC + E0, nC + E0 + E_r); rank 0 also holds the old nodes) and write
+         their midpoints into their fine coordinate array;
+      3. edge owners send {slot, group start, rank byte} per (edge, element)
+         back to the element owners (all-to-all, after the fine counts are
+         all-gathered);
+      4. element owners write the children rows, the fine elem_edge and the
+         midpoints of their own elements' edges (same bits) locally.
+    Coordinates stay replicated only while another level follows (the owned
+    midpoints are all-gathered then); after the last level every rank holds
+    the coordinates its elements and edges reference.  Returns the fine
+    (splits, per, totals)."""
     tr = getattr(comm, "trace", None) or (lambda w: None)
-    ee_all = _gather_rows(comm, [s.elem_edge for s in states])
-    el_all = _gather_rows(comm, [s.elements for s in states])
-    tr("gather")
+    E0s = _all_E0(states, comm, per)
+    edge_splits = np.asarray(E0s + [Etot], dtype=np.int32)
+    sides = [s.ops.side_records(s.elements, s.elem_edge, s.ops.as_tensor(edge_splits)) for s in states]
+    recvs = comm.all_to_all_v([x[0] for x in sides], [x[1] for x in sides])
+    tr("side")
+    for s, rv, (E0, _) in zip(states, recvs, per):
+        s.ops.side_apply(rv, E0)
     # fine node ranges from every rank's parent edge offset
-    fsplits = np.asarray([0] + [nC + e for e in _all_E0(states, comm, per)[1:]] + [nC + Etot], dtype=np.int64)
-    counts, mids = [], []
-    for s, (E0, _), ea, la, i in zip(states, per, ee_all, el_all, ids):
+    fsplits = np.asarray([0] + [nC + e for e in E0s[1:]] + [nC + Etot], dtype=np.int64)
+    counts = []
+    for s, (E0, _), i in zip(states, per, ids):
         r = s.rank
         neu = i[nD:].to(torch.int32).contiguous() if fused_c else None
-        Ef, Bf, m = s.ops.refine_level(ea, la, s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, neu,
-                                       fine_range=(4 * s.elo, 4 * s.ehi))
+        cf = torch.empty((nC + Etot, 2), dtype=torch.float64, device=s.coords.device)
+        cf[:nC] = s.coords[:nC]
+        s.coords_fine = cf
+        Ef, Bf = s.ops.refine_level_side(s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, cf, neu)
         counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
-        mids.append(m)
     tr("level")
     gath = comm.all_gather(counts)
     fper = []
@@ -539,17 +595,27 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
         fper.append((E0f, B0f))
         s.ops.rebase_part(E0f)
     Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
-    fes = 4 * esplits
-    routed = [s.ops.route_pairs(E0f, s.ops.as_tensor(fes), 4 * s.elo, 4 * s.ehi) for s, (E0f, _) in zip(states, fper)]
-    recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
-    tr("route")
-    gm = _gather_rows(comm, mids)
-    for s, rv, m, i in zip(states, recvs, gm, ids):
-        kids = s.ops.children(s.elements, s.elem_edge, nC)   # parent elem_edge of the own elements
+    starts = [s.ops.start_records(nC + E0 - int(fsplits[s.rank]), s.ops.as_tensor(esplits))
+              for s, (E0, _) in zip(states, per)]
+    recvs = comm.all_to_all_v([x[0] for x in starts], [x[1] for x in starts])
+    tr("start")
+    for s, rv, i in zip(states, recvs, ids):
+        gs, grk = s.ops.start_apply(rv, s.elo, s.ehi - s.elo)
+        kids, ee = s.ops.children_slots(s.elements, s.elem_edge, gs, grk, nC, s.coords_fine)
         s.dirichlet, s.neumann = _bisect(s.dirichlet, i[:nD], nC), _bisect(s.neumann, i[nD:], nC)
-        s.coords, s.elements = torch.cat([s.coords, m], 0).contiguous(), kids
+        s.elements, s.elem_edge = kids, ee
         s.elo, s.ehi = 4 * s.elo, 4 * s.ehi
-        s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
+    own = [s.coords_fine[nC + int(edge_splits[s.rank]):nC + int(edge_splits[s.rank + 1])] for s in states]
+    if last:
+        for s, m in zip(states, own):
+            s.nc_parent, s.mid_own = nC, m
+            s.coords = s.coords_fine
+    else:
+        gm = _gather_rows(comm, [m.contiguous() for m in own])
+        for s, m in zip(states, gm):
+            s.coords = torch.cat([s.coords[:nC], m], 0).contiguous()
+    for s in states:
+        s.coords_fine = None
     tr("refine")
     return fsplits.astype(np.int32), fper, (Ef_tot, Bf_tot)
 
@@ -580,7 +646,8 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         if sort_free:
             # the last level also produces C's rows (fused, from the parent Neumann edges)
             splits, per, (Etot_f, Btot_f) = _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot,
-                                                              esplits, nD, nN, ids, fused_c=lvl == levels - 1)
+                                                              esplits, nD, nN, ids, fused_c=lvl == levels - 1,
+                                                              last=lvl == levels - 1)
         else:
             _refine_sorted(states, comm, nC, splits, per, Etot, nD, nN, ids)
         nC, nE = nC + Etot, 4 * nE
@@ -649,7 +716,11 @@ def rank_slice(s: RankState) -> dict:
     out["bd"] = s.bd.cpu().numpy()
     for k in ("B", "D", "M", "M0", "load"):
         out[k] = s.blocks[k].cpu().numpy().reshape(-1)
-    out["coords"] = s.coords.cpu().numpy()
+    if getattr(s, "mid_own", None) is not None:  # after a halo-form last level: parent nodes + owned midpoints
+        out["coords_parent"] = s.coords[:s.nc_parent].cpu().numpy()
+        out["mid_own"] = s.mid_own.cpu().numpy()
+    else:
+        out["coords"] = s.coords.cpu().numpy()
     out["elements"] = s.elements.cpu().numpy()
     out["dirichlet"] = s.dirichlet.cpu().numpy()
     out["neumann"] = s.neumann.cpu().numpy()
@@ -665,8 +736,12 @@ def concat_slices(sl: list) -> dict:
         out[k] = np.concatenate([x[k] for x in sl])
     out["node_edge_start"] = np.concatenate([x["node_edge_start"][:-1] for x in sl] + [sl[-1]["node_edge_start"][-1:]])
     out["C_row_ptr"] = np.concatenate([x["C_row_ptr"][:-1] for x in sl] + [sl[-1]["C_row_ptr"][-1:]])
-    for k in ("coords", "dirichlet", "neumann"):
+    for k in ("dirichlet", "neumann"):
         out[k] = sl[0][k]
+    if "mid_own" in sl[0]:
+        out["coords"] = np.concatenate([sl[0]["coords_parent"]] + [x["mid_own"] for x in sl])
+    else:
+        out["coords"] = sl[0]["coords"]
     return out
 
 

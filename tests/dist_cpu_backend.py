@@ -188,6 +188,143 @@ class NumpyRankOps:
         self.pairs = pairs
         return Ef, int(b.sum()), torch.as_tensor(mids)
 
+    # -- refined level, halo form (the ops of dist._refine_sort_free) ------------------------
+    def side_records(self, elements, elem_edge, esplits):
+        el = elements.numpy().reshape(-1, 3).astype(np.int64)
+        ee = elem_edge.numpy().reshape(-1, 3).astype(np.int64)
+        sg = ee.reshape(-1)
+        e = np.where(sg >= 0, sg, ~sg)
+        rec = np.stack([(e << 1) | (sg < 0), ee[:, [1, 2, 0]].reshape(-1), ee[:, [2, 0, 1]].reshape(-1),
+                        el.reshape(-1)], 1)
+        sp = esplits.numpy().astype(np.int64)
+        d = self._dest(sp, e)
+        order = np.argsort(d, kind="stable")
+        W = len(sp) - 1
+        return torch.as_tensor(rec[order].astype(np.int32)), np.bincount(d, minlength=W)[:W].tolist()
+
+    def side_apply(self, recv, E0):
+        E = self.num_edges()
+        side = np.zeros((2 * max(E, 1), 3), np.int64)
+        r = recv.numpy().astype(np.int64).reshape(-1, 4)
+        side[2 * ((r[:, 0] >> 1) - E0) + (r[:, 0] & 1)] = r[:, 1:4]
+        self._side = side
+
+    def refine_level_side(self, coords, nc, E0p, nlo, nhi, nE_all, coords_fine, neu_parent=None):
+        """Groups of the own parent edges from the side records (partners at
+        local l+1, l+2 of t_plus / t_minus): two halves (the one at the smaller
+        old node first), then the interior edges to mu(e') for partners e' < e,
+        ascending e'; rank bytes as the level kernel packs them."""
+        p = self.part
+        c = coords.numpy()
+        cf = coords_fine.numpy()
+        sd = self._side
+        E = len(p.ltp)
+        rows, isb = [], []
+        nes = np.zeros(nhi - nlo + 1, np.int32)
+        rk = np.zeros(max(E, 1), np.uint8)
+        mid = lambda u, v: [0.5 * (u[0] + v[0]), 0.5 * (u[1] + v[1])]
+        for le in range(E):
+            e = E0p + le
+            a, b = (int(x) for x in p.edge_nodes[le])
+            tp, tm = (int(x) for x in p.edge_elements[le])
+            l = int(p.ltp[le])
+            l2 = int(p.ltm[le]) if tm >= 0 else 0
+            mu = nc + e
+            nes[mu - nlo] = len(rows)
+            cf[mu] = mid(c[a], c[b])
+            j1, j2, k1, k2 = (l + 1) % 3, (l + 2) % 3, (l2 + 1) % 3, (l2 + 2) % 3
+            h1 = (a, mu, 4 * tp + 1 + j1, 2, 4 * tm + 1 + k2 if tm >= 0 else -1, 1 if tm >= 0 else -1)
+            h2 = (mu, b, 4 * tp + 1 + j2, 1, 4 * tm + 1 + k1 if tm >= 0 else -1, 2 if tm >= 0 else -1)
+            halves = [h1, h2] if a < b else [h2, h1]
+            absd = lambda x: int(x) if x >= 0 else ~int(x)
+            q0, q1, vop = absd(sd[2 * le][0]), absd(sd[2 * le][1]), int(sd[2 * le][2])
+            part = [(q0, q0 < e, (mu, nc + q0, 4 * tp, j2, 4 * tp + 1 + j2, 0), mid(c[b], c[vop])),
+                    (q1, q1 < e, (nc + q1, mu, 4 * tp, j1, 4 * tp + 1 + j1, 0), mid(c[vop], c[a]))]
+            if tm >= 0:
+                r0, r1, vom = absd(sd[2 * le + 1][0]), absd(sd[2 * le + 1][1]), int(sd[2 * le + 1][2])
+                part += [(r0, r0 < e, (mu, nc + r0, 4 * tm, k2, 4 * tm + 1 + k2, 0), mid(c[a], c[vom])),
+                         (r1, r1 < e, (nc + r1, mu, 4 * tm, k1, 4 * tm + 1 + k1, 0), mid(c[vom], c[b]))]
+            else:
+                part += [(0, False, None, None), (0, False, None, None)]
+            code = 0
+            for i, (q, v, _, pm) in enumerate(part):
+                if v:
+                    code |= sum(1 for (q2, v2, _, _) in part if v2 and q2 < q) << (2 * i)
+                    cf[nc + q] = pm   # the partner midpoint (same bits as its owner's)
+            rk[le] = code
+            cand = sorted((q, row) for q, v, row, _ in part if v)
+            group = halves + [x for _, x in cand]
+            rows += group
+            isb += [tm < 0, tm < 0] + [False] * (len(group) - 2)
+        if E:
+            nes[nhi - nlo] = len(rows)
+        r = np.asarray(rows, np.int64).reshape(-1, 6)
+        Ef = len(r)
+        q = _Part()
+        q.edge_nodes = r[:, 0:2].astype(np.int32)
+        q.edge_elements = r[:, [2, 4]].astype(np.int32)
+        q.ltp = r[:, 3].astype(np.int32)
+        q.ltm = r[:, 5].astype(np.int32)
+        ids = np.arange(Ef)
+        b = np.asarray(isb, bool)
+        q.interior, q.boundary = ids[~b].astype(np.int32), ids[b].astype(np.int32)
+        q.nes, q.nlo = nes, nlo
+        self.ppart, self.part, self._rk = p, q, rk
+        return Ef, int(b.sum())
+
+    def start_records(self, nes_off, psplits):
+        p, nes = self.ppart, self.part.nes
+        recs = []
+        for le in range(len(p.ltp)):
+            for m, l in ((p.edge_elements[le][0], p.ltp[le]), (p.edge_elements[le][1], p.ltm[le])):
+                if m >= 0:
+                    recs.append((3 * int(m) + int(l), int(nes[le + nes_off]), int(self._rk[le])))
+        r = np.asarray(recs, np.int64).reshape(-1, 3)
+        sp = psplits.numpy().astype(np.int64)
+        d = self._dest(sp, r[:, 0] // 3)
+        order = np.argsort(d, kind="stable")
+        W = len(sp) - 1
+        self.ppart = self._rk = None
+        return torch.as_tensor(r[order].astype(np.int32)), np.bincount(d, minlength=W)[:W].tolist()
+
+    def start_apply(self, recv, elo, n):
+        gs = np.zeros(3 * n, np.int64)
+        grk = np.zeros(3 * n, np.int64)
+        r = recv.numpy().astype(np.int64).reshape(-1, 3)
+        gs[r[:, 0] - 3 * elo] = r[:, 1]
+        grk[r[:, 0] - 3 * elo] = r[:, 2]
+        return gs, grk
+
+    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine):
+        el = elements.numpy().reshape(-1, 3).astype(np.int64)
+        ee = elem_edge.numpy().reshape(-1, 3).astype(np.int64)
+        cf = coords_fine.numpy()
+        kids, fee = [], []
+        for m in range(len(el)):
+            P, sg = el[m], ee[m]
+            e = np.where(sg >= 0, sg, ~sg)
+            G, R = gs[3 * m:3 * m + 3], grk[3 * m:3 * m + 3]
+            for j in range(3):
+                a, b = P[(j + 1) % 3], P[(j + 2) % 3]
+                cf[nc + e[j]] = [0.5 * (cf[a][0] + cf[b][0]), 0.5 * (cf[a][1] + cf[b][1])]
+            I = []
+            for k in range(3):
+                jA, jB = (k + 1) % 3, (k + 2) % 3
+                jE, jm = (jA, jB) if e[jA] > e[jB] else (jB, jA)
+                field = (0 if sg[jE] >= 0 else 2) + (0 if jm == (jE + 1) % 3 else 1)
+                I.append(int(G[jE]) + 2 + ((int(R[jE]) >> (2 * field)) & 3))
+
+            def half(j, v):
+                a, b = P[(j + 1) % 3], P[(j + 2) % 3]
+                i = int(G[j]) + (0 if v == min(a, b) else 1)
+                return i if sg[j] >= 0 else ~i
+            M0, M1, M2 = nc + e[0], nc + e[1], nc + e[2]
+            kids += [[M0, M1, M2], [P[0], M2, M1], [P[1], M0, M2], [P[2], M1, M0]]
+            fee += [[I[0], I[1], I[2]], [~I[0], half(1, P[0]), half(2, P[0])],
+                    [~I[1], half(2, P[1]), half(0, P[1])], [~I[2], half(0, P[2]), half(1, P[2])]]
+        return (torch.as_tensor(np.asarray(kids, np.int64).reshape(-1, 3).astype(np.int32)),
+                torch.as_tensor(np.asarray(fee, np.int64).reshape(-1, 3).astype(np.int32)))
+
     def num_edges(self):
         return len(self.part.ltp)
 

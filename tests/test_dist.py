@@ -151,3 +151,34 @@ def test_sampled_key_histogram_local_ranks(monkeypatch, W):
     topo = ot.arrays()
     for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "elem_edge"):
         assert np.array_equal(np.asarray(got[k]).reshape(-1), topo[k].reshape(-1)), k
+
+
+@pytest.mark.parametrize("W,case,levels", [(3, "lshape-L1-3levels", 3), (5, "square-L3", 1),
+                                           (4, "stress-L3", 1)])
+def test_halo_refine_local_ranks_equal_oracle(W, case, levels):
+    """The halo form of the sort-free refinement (side records -> edge owners,
+    group starts -> element owners, coordinates only where referenced after
+    the last level) with W emulated NumPy ranks: every output == the C oracle
+    on the whole mesh, coordinates included (parent nodes + the ranks' owned
+    midpoints)."""
+    from paper_2401_15557_b200 import dist
+    from dist_cpu_backend import NumpyRankOps
+    hm = dict((c[0], c[1]) for c in CASES)[case]()
+    comm = dist.LocalComm(W)
+    states = dist.make_states(hm, comm, lambda r: NumpyRankOps())
+    args = G.config_fields(1)
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *args)
+    got = dist.collect(states)
+    fine = O.refine_levels(hm, levels)
+    om, ot = O.build_topology(fine)
+    oc = O.classify_edges(om, ot)
+    topo = ot.arrays()
+    for k in ("edge_nodes", "edge_elements", "local_in_tplus", "local_in_tminus", "elem_edge",
+              "interior_edges", "boundary_edges"):
+        assert np.array_equal(np.asarray(got[k]).reshape(-1), topo[k].reshape(-1)), k
+    for a, b in zip((got["C_row_ptr"], got["C_col_idx"], got["C_values"]), O.assemble_constraint(om, ot, oc)["csr"]):
+        assert np.array_equal(a, b)
+    load = O.assemble_load(fine, args[1], 0.0) + O.assemble_neumann(om, ot, oc, args[2], 0.0)
+    assert np.array_equal(got["load"], load)
+    assert np.array_equal(got["coords"], fine.coords)
+    assert np.array_equal(got["elements"], fine.elements)
