@@ -865,4 +865,9 @@ def pipeline(ctx: Context, mesh: DeviceMesh, levels: int, coeffs: phfem_coeffs, 
     out = phfem_pipeline_out()
     ctx.check(ctx.lib.phfem_pipeline_ex(ctx.ptr, C.byref(mesh.m), levels, C.byref(coeffs), C.byref(f),
                                         C.byref(g), C.byref(uD), t, flags, C.byref(out)))
-    return PipelineResult(ctx, out)
+    res = PipelineResult(ctx, out)
+    # with levels = 0 the result's mesh is the input's buffers: keep the input
+    # alive as long as the result (a temporary DeviceMesh would otherwise be
+    # released underneath it — found by guard mode, tests/test_guard.py)
+    res._input = mesh
+    return res

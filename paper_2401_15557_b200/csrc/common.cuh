@@ -62,6 +62,23 @@ struct phfem_ctx {
   // Lowered only to exercise the multi-sub-bucket tile path on small meshes
   // (env PHFEM_EG_MAX_BS at ctx creation, or phfem_ctx_set_eg_max_bs)
   int eg_max_bs = 8;
+  // guard mode (env PHFEM_GUARD=1 at ctx creation; the device check that
+  // stands in for compute-sanitizer, which this pool does not allow): every
+  // block gets kGuardBytes red zones on both sides filled with 0xA5 and its
+  // payload poisoned (PHFEM_GUARD_POISON, default 0xff: NaN / -1), blocks are
+  // never recycled, and every free checks the red zones on the device; the
+  // first violated block's serial is reported by errors_fetch / ctx_sync.
+  bool guard = false;
+  int guard_poison = 0xff;
+  unsigned int* guard_bad = nullptr;  // device: min serial of a violated block (~0u: none)
+  unsigned int guard_serial = 0;
+  struct GuardBlock {
+    void* base;
+    size_t bytes, total;
+    unsigned serial;
+  };
+  std::unordered_map<void*, GuardBlock> guard_blocks;
+  std::unordered_map<unsigned, size_t> guard_sizes;  // serial -> payload bytes (reports)
 };
 
 namespace phfem {
@@ -132,6 +149,8 @@ class KTimer {
 // Reset the device error words (async) / fetch them (sync).
 phfem_status errors_reset(phfem_ctx* ctx);
 phfem_status errors_fetch(phfem_ctx* ctx);
+// guard mode: report a red-zone violation seen so far (synchronises)
+phfem_status guard_check(phfem_ctx* ctx);
 
 inline int grid_for(int64_t n, int block, int max_blocks) {
   int64_t g = (n + block - 1) / block;

@@ -38,7 +38,66 @@ phfem_status errors_fetch(phfem_ctx* ctx) {
   PHFEM_CUDA(ctx, cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(phfem_dev_errors),
                                   cudaMemcpyDeviceToHost, ctx->stream));
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->guard) return guard_check(ctx);
   return PHFEM_OK;
+}
+
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardFill = 0xA5;
+
+// red zones [a0, a0 + n0) and [a1, a1 + n1) must still hold kGuardFill
+__global__ void k_guard_check(const unsigned char* __restrict__ a0, size_t n0, const unsigned char* __restrict__ a1,
+                              size_t n1, unsigned serial, unsigned int* __restrict__ bad) {
+  bool ok = true;
+  for (size_t i = threadIdx.x; i < n0; i += blockDim.x) ok &= a0[i] == kGuardFill;
+  for (size_t i = threadIdx.x; i < n1; i += blockDim.x) ok &= a1[i] == kGuardFill;
+  if (!ok) atomicMin(bad, serial);
+}
+
+phfem_status guard_check(phfem_ctx* ctx) {
+  unsigned int h = ~0u;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&h, ctx->guard_bad, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (h != ~0u) {
+    auto it = ctx->guard_sizes.find(h);
+    return set_error(ctx, PHFEM_ERR_CUDA,
+                     "phfem guard: out-of-bounds write into the red zone of device block #%u (%zu bytes)", h,
+                     it == ctx->guard_sizes.end() ? (size_t)0 : it->second);
+  }
+  return PHFEM_OK;
+}
+
+static phfem_status guard_alloc(phfem_ctx* ctx, void** p, size_t bytes) {
+  const size_t payload = (bytes + 255) / 256 * 256;
+  const size_t total = payload + 2 * kGuardBytes;
+  void* base = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&base, total, ctx->pool, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, PHFEM_ERR_OOM, "phfem: device allocation of %zu bytes failed (%s)", bytes,
+                     cudaGetErrorString(e));
+  }
+  unsigned char* b = (unsigned char*)base;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(b, kGuardFill, total, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(b + kGuardBytes, ctx->guard_poison, bytes, ctx->stream));
+  *p = b + kGuardBytes;
+  const unsigned serial = ++ctx->guard_serial;
+  ctx->guard_blocks[*p] = {base, bytes, total, serial};
+  ctx->guard_sizes[serial] = bytes;
+  return PHFEM_OK;
+}
+
+static bool guard_free(phfem_ctx* ctx, void* p) {
+  auto it = ctx->guard_blocks.find(p);
+  if (it == ctx->guard_blocks.end()) return false;
+  const auto g = it->second;
+  const unsigned char* b = (const unsigned char*)g.base;
+  const unsigned char* tail = (const unsigned char*)p + g.bytes;
+  k_guard_check<<<1, 256, 0, ctx->stream>>>(b, kGuardBytes, tail, g.total - kGuardBytes - g.bytes, g.serial,
+                                            ctx->guard_bad);
+  cudaFreeAsync(g.base, ctx->stream);
+  ctx->guard_blocks.erase(it);
+  return true;
 }
 
 phfem_status smem_optin(phfem_ctx* ctx, const void* fn, size_t bytes, const char* name) {
@@ -59,6 +118,7 @@ static size_t round_size(size_t bytes) {
 
 phfem_status raw_alloc(phfem_ctx* ctx, void** p, size_t bytes) {
   *p = nullptr;
+  if (ctx->guard) return guard_alloc(ctx, p, bytes);
   const size_t sz = round_size(bytes);
   auto it = ctx->cache.find(sz);
   if (it != ctx->cache.end() && !it->second.empty()) {
@@ -84,6 +144,7 @@ phfem_status raw_alloc(phfem_ctx* ctx, void** p, size_t bytes) {
 }
 
 void raw_free(phfem_ctx* ctx, void* p) {
+  if (ctx->guard && guard_free(ctx, p)) return;
   auto it = ctx->block_size.find(p);
   if (it == ctx->block_size.end()) {  // not ours: hand back to the stream-ordered pool
     cudaFreeAsync(p, ctx->stream);
@@ -244,6 +305,8 @@ PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** ou
       return PHFEM_ERR_NO_DEVICE;  // sm_100a code only
     }
   }
+  if (const char* gd = getenv("PHFEM_GUARD")) ctx->guard = gd[0] == '1';
+  if (const char* gp = getenv("PHFEM_GUARD_POISON")) ctx->guard_poison = (int)strtol(gp, nullptr, 0) & 0xff;
   if (const char* bs = getenv("PHFEM_EG_MAX_BS")) {
     const int v = atoi(bs);
     if (v >= 1 && v <= 8) ctx->eg_max_bs = v;
@@ -278,6 +341,14 @@ PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** ou
     delete ctx;
     return PHFEM_ERR_OOM;
   }
+  if (ctx->guard) {
+    if (cudaMalloc((void**)&ctx->guard_bad, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemset(ctx->guard_bad, 0xff, sizeof(unsigned int)) != cudaSuccess) {
+      cudaGetLastError();
+      delete ctx;
+      return PHFEM_ERR_OOM;
+    }
+  }
   *out = ctx;
   return PHFEM_OK;
 }
@@ -286,6 +357,13 @@ PHFEM_API void phfem_ctx_destroy(phfem_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->guard) {
+    std::vector<void*> live;
+    for (auto& kv : ctx->guard_blocks) live.push_back(kv.first);
+    for (void* q : live) guard_free(ctx, q);
+    if (guard_check(ctx) != PHFEM_OK) fprintf(stderr, "%s\n", ctx->message.c_str());
+    cudaFree(ctx->guard_bad);
+  }
   cache_flush(ctx);
   for (auto& r : ctx->recs) {
     cudaEventDestroy(r.a);
@@ -316,6 +394,7 @@ PHFEM_API phfem_status phfem_ctx_set_eg_max_bs(phfem_ctx* ctx, int max_bs) {
 
 PHFEM_API phfem_status phfem_ctx_sync(phfem_ctx* ctx) {
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->guard) return guard_check(ctx);
   return PHFEM_OK;
 }
 

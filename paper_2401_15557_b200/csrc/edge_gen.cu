@@ -269,7 +269,13 @@ __device__ __forceinline__ int4 eg_record(int nd, int bloc, int32_t lo, uint64_t
 // run detection + block scan, look-back, then every run start emits its edge.
 constexpr int kTileNodes = 256;
 constexpr int kTileThreads = 256;
-constexpr int kTileCap = 10 * kTileNodes;  // items kept in SMEM (10 per node)
+#ifndef PHFEM_TILE_PER_NODE
+#define PHFEM_TILE_PER_NODE 10
+#endif
+#ifndef PHFEM_TILE_MIN_BLOCKS
+#define PHFEM_TILE_MIN_BLOCKS 1  // (measured: 5 blocks spill, 8 items per node overflow the fast path: both slower)
+#endif
+constexpr int kTileCap = PHFEM_TILE_PER_NODE * kTileNodes;  // items kept in SMEM (10 per node)
 
 struct TileSmem {
   uint64_t buf1[kTileCap + 4];  // + 4 all-ones keys: the rank loop reads past the last segment
@@ -556,7 +562,7 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
 }
 
 // P.nb here = number of tiles; boff has one entry per bucket (+1).
-__global__ void __launch_bounds__(kTileThreads) k_eg_tile(const uint64_t* __restrict__ items,
+__global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile(const uint64_t* __restrict__ items,
                                                           const int32_t* __restrict__ boff,
                                                           int nbuckets, EgParams P, uint64_t* g1,
                                                           uint64_t* g2, uint8_t* gnode,
