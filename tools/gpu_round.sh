@@ -19,4 +19,4 @@ echo "ncu launch exit $?" >> gpurun_out/ncu_launch_$tag.log
 timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:k_eg_tile$|k_rl_level|k_volume|k_refine_children|k_eg_emit' \
    -s 24 -c 6 -o gpurun_out/prof_step_$tag python tools/profile_step.py 13 > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full exit $?" >> gpurun_out/ncu_full_$tag.log
-tail -3 gpurun_out/pytest_gpu_$tag.log gpurun_out/smoke_$tag.log gpurun_out/bench_$tag.err gpurun_out/ncu_launch_$tag.log gpurun_out/ncu_full_$tag.log
+for f in pytest_gpu_$tag.log smoke_$tag.log bench_$tag.err ncu_launch_$tag.log ncu_full_$tag.log; do tail -n 3 gpurun_out/$f; done
