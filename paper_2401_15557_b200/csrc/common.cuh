@@ -35,6 +35,7 @@ struct phfem_ctx {
   bool own_stream = false;
   cudaMemPool_t pool = nullptr;
   phfem_dev_errors* derr = nullptr;   // device
+  phfem_dev_errors* dderr = nullptr;  // device: errors deferred to the end of a pipeline call
   phfem_dev_errors* herr = nullptr;   // pinned host mirror
   int64_t launches = 0;
   int num_sms = 148;

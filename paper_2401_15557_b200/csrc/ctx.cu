@@ -253,11 +253,47 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t* in, i
   }
 }
 
+// Small arrays (tile counts, bucket offsets of small meshes): one CTA walks
+// the array in 4096-entry chunks with a carry — one launch instead of three
+// (the three-launch scan cost ~15 us even for a few hundred entries, 28 of
+// them per config-2 pipeline).
+constexpr int64_t kScanSmall = 8 * kScanTile;
+__global__ void __launch_bounds__(kScanThreads) k_scan_small(const int32_t* in, int32_t* out, int64_t n,
+                                                             int32_t* total) {
+  __shared__ int32_t sm[33];
+  int32_t carry = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += kScanTile) {
+    const int64_t base = c0 + (int64_t)threadIdx.x * kScanPer;
+    int32_t v[kScanPer];
+    int32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      v[k] = base + k < n ? in[base + k] : 0;
+      s += v[k];
+    }
+    int32_t tot;
+    int32_t ex = carry + block_exclusive_scan(s, sm, &tot);
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      if (base + k < n) out[base + k] = ex;
+      ex += v[k];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
 phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
                                 int32_t* total_dev) {
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   if (n == 0) {
     if (total_dev) PHFEM_CUDA(ctx, cudaMemsetAsync(total_dev, 0, sizeof(int32_t), ctx->stream));
+    return PHFEM_OK;
+  }
+  if (n <= kScanSmall) {  // in == out is fine: every thread reads its entries before writing them
+    KTimer kt(ctx, "scan");
+    k_scan_small<<<1, kScanThreads, 0, ctx->stream>>>(in, out, n, total_dev);
+    PHFEM_CHECK_LAUNCH(ctx);
     return PHFEM_OK;
   }
   int32_t* sums = nullptr;
@@ -336,6 +372,7 @@ PHFEM_API phfem_status phfem_ctx_create(int device, void* stream, phfem_ctx** ou
   uint64_t threshold = UINT64_MAX;
   cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
   if (cudaMalloc((void**)&ctx->derr, sizeof(phfem_dev_errors)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->dderr, sizeof(phfem_dev_errors)) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->herr, sizeof(phfem_dev_errors)) != cudaSuccess) {
     cudaGetLastError();
     delete ctx;
@@ -371,6 +408,7 @@ PHFEM_API void phfem_ctx_destroy(phfem_ctx* ctx) {
   }
   for (auto e : ctx->free_events) cudaEventDestroy(e);
   cudaFree(ctx->derr);
+  cudaFree(ctx->dderr);
   cudaFreeHost(ctx->herr);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   cudaStreamSynchronize(nullptr);

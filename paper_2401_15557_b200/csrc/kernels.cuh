@@ -94,7 +94,7 @@ phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
 // defer_elements: the children rows are left to the refined-level pass
 // (write_elems below), which writes them together with the fine elem_edge
 phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
-                             phfem_mesh* out, bool write_mid, bool defer_elements = false);
+                             phfem_mesh* out, bool write_mid, bool defer_elements = false, phfem_dev_errors* deferred = nullptr);
 phfem_status refine_topology_impl(phfem_ctx* ctx, const phfem_mesh* parent,
                                   const phfem_topology* ptopo, const phfem_mesh* fine,
                                   phfem_topology* out, double* mid, bool write_elems = false);

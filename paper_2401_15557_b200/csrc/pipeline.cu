@@ -41,6 +41,9 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   // topology from the parent's (no sort) unless the generic path is forced
   Trace tr(ctx);
   tr("start");
+  // red_refine's boundary-pair checks of every level land in dderr, read once
+  // with the pipeline's final error fetch (one host sync less per level)
+  PHFEM_CUDA(ctx, cudaMemsetAsync(ctx->dderr, 0xff, sizeof(phfem_dev_errors), ctx->stream));
   phfem_topology topo;
   bool have_cls_C = false;
   phfem_status st;
@@ -66,7 +69,7 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
     // the sort-free paths write the midpoint nodes themselves (coalesced)
     const bool generic = (flags & PHFEM_PIPE_GENERIC_EG) != 0;
     // sort-free levels: children rows + fine elem_edge come from the level pass
-    if (st == PHFEM_OK) st = red_refine_impl(ctx, &cur, &topo, &next, generic, !generic);
+    if (st == PHFEM_OK) st = red_refine_impl(ctx, &cur, &topo, &next, generic, !generic, ctx->dderr);
     double* mid = next.coords;  // the level kernels write nodes nc..nc+E-1
     tr("red_refine");
     phfem_topology fine_topo;
@@ -125,7 +128,10 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   if (!have_cls_C) PHFEM_TRY(constraint_csr_into(ctx, &out->mesh, &out->topo, &out->cls, &out->C));
   PHFEM_TRY(dirichlet_into(ctx, &out->mesh, &out->topo, &out->cls, uD, t, out->bd));
   tr("neumann+C+dirichlet");
+  unsigned long long dmisc = ~0ull;
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&dmisc, &ctx->dderr->misc, sizeof dmisc, cudaMemcpyDeviceToHost, ctx->stream));
   PHFEM_TRY(errors_fetch(ctx));
+  if (dmisc != ~0ull) return set_error(ctx, PHFEM_ERR_MISMATCH, "red_refine: topology does not match mesh");
   PHFEM_TRY(volume_errors(ctx, true, true));
   PHFEM_TRY(neu_flux_error(ctx, &out->mesh, &out->topo, &out->cls));
   return PHFEM_OK;

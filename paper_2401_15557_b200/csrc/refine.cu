@@ -105,8 +105,10 @@ PHFEM_API void phfem_mesh_release(phfem_ctx* ctx, phfem_mesh* m) {
 namespace phfem {
 // write_mid = false: the midpoint nodes nc..nc+E-1 are left to the fused
 // refined-level kernel (refine_topo.cu), which writes them coalesced.
+// deferred != nullptr (pipeline): the boundary-pair mismatch goes to that
+// error block, checked once at the end of the pipeline — no host sync here
 phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
-                             phfem_mesh* out, bool write_mid, bool defer_elements) {
+                             phfem_mesh* out, bool write_mid, bool defer_elements, phfem_dev_errors* deferred) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !mesh || !topo) return PHFEM_ERR_INVALID_ARGUMENT;
   if (topo->nE != mesh->nE || topo->nC != mesh->nC)
@@ -132,7 +134,11 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
         (double2*)out->coords, (int4*)out->elements, write_mid ? 1 : 0));
   }
   const int64_t nb = (int64_t)mesh->nD + mesh->nN;
-  if (nb > 0) {
+  if (nb > 0 && deferred) {
+    PHFEM_LAUNCH(ctx, "k_refine_boundary", k_refine_boundary<<<grid_for(nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        mesh->dirichlet, mesh->nD, mesh->neumann, mesh->nN, topo->node_edge_start,
+        topo->edge_nodes, (int)nC, (int4*)out->dirichlet, (int4*)out->neumann, deferred));
+  } else if (nb > 0) {
     PHFEM_TRY(errors_reset(ctx));
     PHFEM_LAUNCH(ctx, "k_refine_boundary", k_refine_boundary<<<grid_for(nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
         mesh->dirichlet, mesh->nD, mesh->neumann, mesh->nN, topo->node_edge_start,
