@@ -583,6 +583,22 @@ phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements, 
                                        int32_t n, const int32_t* gs, const uint8_t* grk, int32_t nc,
                                        double* coords_fine, int32_t* children, int32_t* fine_elem_edge);
 
+/* Peer-window forms of steps 1-2 and 4-5 above (one kernel each: the record
+ * is computed and stored straight into its final slot of the owner's array,
+ * mapped into this rank — CUDA IPC across GPUs over NVLink, or the emulated
+ * ranks' arrays on one GPU): peer_side[d] = rank d's side array ([2 E_d][4]),
+ * peer_gs[d] / peer_grk[d] = rank d's per-slot arrays; W device pointers
+ * each, in device memory.  remote[W] (device) receives the number of records
+ * this rank stored into each other rank's window.  The caller fences (kernel
+ * completion on every rank) before the owners read.                        */
+phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge, int32_t n,
+                                 const int32_t* esplits, int32_t W, int32_t self, int32_t* const* peer_side,
+                                 int32_t* remote);
+phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                  int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                  int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
+                                  int32_t* remote);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

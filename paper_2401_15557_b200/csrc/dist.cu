@@ -329,6 +329,60 @@ __global__ void k_dist_start_apply(const Rec3* __restrict__ recv, int64_t n, int
   }
 }
 
+// ---- peer-window forms (fused compute + exchange over NVLink peer memory) --
+// The owner's receive array is mapped into every rank (CUDA IPC; on one GPU
+// the emulated ranks' arrays): the producing kernel stores each record
+// straight into its final slot there — no count pass, no send buffer, no
+// all-to-all, no apply pass.  remote[d] counts the records stored into rank
+// d's window by this rank (d != self), for the byte accounting.
+__device__ __forceinline__ void count_remote(int d, int self, int32_t* remote) {
+  const unsigned peers = __match_any_sync(__activemask(), d);
+  if (d != self && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(remote + d, __popc(peers));
+}
+
+__global__ void __launch_bounds__(256) k_dist_side_p2p(const int32_t* __restrict__ elements,
+                                                       const int32_t* __restrict__ elem_edge, int n,
+                                                       const int32_t* __restrict__ esplits, int W, int self,
+                                                       int4* const* __restrict__ peer_side, int32_t* remote) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * (int64_t)n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / 3;
+    const int k = (int)(i - 3 * m);
+    const int s = elem_edge[i];
+    const int e = s >= 0 ? s : ~s;
+    const int d = dest_of(esplits, W, e);
+    const int4 r = make_int4(elem_edge[3 * m + (k == 2 ? 0 : k + 1)], elem_edge[3 * m + (k == 0 ? 2 : k - 1)],
+                             elements[i], 0);
+    peer_side[d][2 * (int64_t)(e - __ldg(esplits + d)) + (s < 0 ? 1 : 0)] = r;
+    count_remote(d, self, remote);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restrict__ edge_elements,
+                                                        const int32_t* __restrict__ ltp,
+                                                        const int32_t* __restrict__ ltm,
+                                                        const int32_t* __restrict__ fine_nes, int nes_off,
+                                                        const uint8_t* __restrict__ rk, int E,
+                                                        const int32_t* __restrict__ psplits, int W, int self,
+                                                        int32_t* const* __restrict__ peer_gs,
+                                                        uint8_t* const* __restrict__ peer_grk, int32_t* remote) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * (int64_t)E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t le = i >> 1;
+    const int sd = (int)(i & 1);
+    const int m = edge_elements[2 * le + sd];
+    int d = -1;
+    if (m >= 0) {
+      const int l = sd ? ltm[le] : ltp[le];
+      d = dest_of(psplits, W, m);
+      const int64_t slot = 3 * (int64_t)(m - __ldg(psplits + d)) + l;
+      peer_gs[d][slot] = fine_nes[le + nes_off];
+      peer_grk[d][slot] = rk[le];
+    }
+    if (d >= 0) count_remote(d, self, remote);
+  }
+}
+
 // count pass, exclusive offsets, pack pass of a route_block kernel
 template <typename Launch>
 static phfem_status route_two_pass(phfem_ctx* ctx, int W, int32_t* counts, int32_t* offsets, bool pack,
@@ -614,5 +668,36 @@ PHFEM_API phfem_status phfem_dist_start_apply(phfem_ctx* ctx, const int32_t* rec
   if (n > 0)
     PHFEM_LAUNCH(ctx, "k_dist_start_apply", k_dist_start_apply<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
         reinterpret_cast<const Rec3*>(recv), n, elo, gs, grk));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                           int32_t n, const int32_t* esplits, int32_t W, int32_t self,
+                                           int32_t* const* peer_side, int32_t* remote) {
+  if (!ctx || !esplits || !peer_side || !remote || W < 1 || self < 0 || self >= W || n < 0 ||
+      (n && (!elements || !elem_edge)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_side_p2p", k_dist_side_p2p<<<grid_for(3 * (int64_t)n, 256, ctx->num_sms * 8), 256, 0,
+                                                           ctx->stream>>>(
+        elements, elem_edge, n, esplits, W, self, reinterpret_cast<int4* const*>(peer_side), remote));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                            int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                            int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
+                                            int32_t* remote) {
+  if (!ctx || !ppart || !psplits || !peer_gs || !peer_grk || !remote || W < 1 || self < 0 || self >= W ||
+      (ppart->E && (!fine_nes || !rk)))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
+  const int E = ppart->E;
+  if (E > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_start_p2p", k_dist_start_p2p<<<grid_for(2 * (int64_t)E, 256, ctx->num_sms * 8), 256, 0,
+                                                             ctx->stream>>>(
+        ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus, fine_nes, nes_off, rk, E, psplits, W,
+        self, peer_gs, peer_grk, remote));
   return PHFEM_OK;
 }

@@ -76,6 +76,7 @@ class TorchComm:
         self.dist = dist
         self.world = dist.get_world_size()
         self.ranks = [dist.get_rank()]
+        self._open = []
 
     def all_reduce(self, ts: list, op: str):
         o = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}[op]
@@ -85,6 +86,29 @@ class TorchComm:
         out = [torch.empty_like(ts[0]) for _ in range(self.world)]
         self.dist.all_gather(out, ts[0])
         return [out]
+
+    def window(self, ts: list) -> list:
+        """Peer window: every rank's tensor mapped into this process (CUDA IPC
+        through torch's storage sharing; over NVLink between GPUs).  Returns,
+        per local state, the W tensors in rank order."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        objs = [None] * self.world
+        self.dist.all_gather_object(objs, reduce_tensor(ts[0]))
+        me = self.ranks[0]
+        views = [ts[0] if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
+        self._open.append(views)
+        return [views]
+
+    def fence(self):
+        """every rank's peer stores complete and visible before anyone reads"""
+        torch.cuda.synchronize()
+        self.dist.barrier()
+
+    def close_windows(self):
+        self._open = []
+
+    def account(self, remote: list, rec_bytes: int):
+        pass
 
     def all_to_all_v(self, sends: list, counts: list) -> list:
         send, sc = sends[0], [int(c) for c in counts[0]]
@@ -114,6 +138,19 @@ class LocalComm:
     def all_gather(self, ts: list) -> list:
         return [[t.clone() for t in ts] for _ in ts]
 
+    def window(self, ts: list) -> list:
+        """Peer window of the emulated ranks: their tensors live on one device."""
+        return [list(ts) for _ in ts]
+
+    def fence(self):
+        pass  # the emulated ranks' kernels run in order on one stream
+
+    def close_windows(self):
+        pass
+
+    def account(self, remote: list, rec_bytes: int):
+        pass
+
     def all_to_all_v(self, sends: list, counts: list) -> list:
         offs = [np.concatenate([[0], np.cumsum([int(c) for c in cs])]).astype(np.int64) for cs in counts]
         return [torch.cat([sends[s][offs[s][d]:offs[s][d + 1]] for s in range(self.world)], 0)
@@ -136,6 +173,9 @@ def balanced_splits(hist: np.ndarray, bins: np.ndarray, world: int) -> np.ndarra
 # at least HIST_SAMPLE_MIN_ELEMENTS elements (module constants: tests force it)
 HIST_SAMPLE = 8
 HIST_SAMPLE_MIN_ELEMENTS = 1 << 20
+# halo exchanges of the refined level through peer windows (CUDA backends);
+# False: the all-to-all form (tests run both)
+P2P = True
 
 
 def element_splits(nE: int, world: int) -> np.ndarray:
@@ -277,6 +317,41 @@ class CudaRankOps:
                                                     self.p(gs), self.p(grk), nc, self.p(coords_fine),
                                                     self.p(kids), self.p(ee)))
         return kids[:4 * n], ee[:4 * n]
+
+    # -- peer-window forms (phfem_dist_side_p2p / _start_p2p) ---------------------------
+    def _ptrs(self, ts):
+        return torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=self.dev)
+
+    def side_alloc(self):
+        self._side = self.empty((max(2 * int(self.part.t.E), 1), 4))
+        return self._side
+
+    def side_p2p(self, elements, elem_edge, esplits, peers, me):
+        """side records stored straight into the edge owners' side arrays"""
+        n, W = int(elements.shape[0]), len(peers)
+        ptrs, remote = self._ptrs(peers), self.empty(W)
+        self._ck(self.lib.phfem_dist_side_p2p(self.ctx.ptr, self.p(elements), self.p(elem_edge), n, self.p(esplits),
+                                              W, me, self.p(ptrs), self.p(remote)))
+        self._keep = ptrs
+        return remote
+
+    def start_alloc(self, n):
+        self._gs = self.empty((max(3 * n, 1),))
+        self._grk = torch.empty((max(3 * n, 1),), dtype=torch.uint8, device=self.dev)
+        return self._gs, self._grk
+
+    def start_p2p(self, nes_off, psplits, peers_gs, peers_grk, me):
+        """group-start records stored straight into the element owners' slots"""
+        pt = self.ppart.t
+        W = len(peers_gs)
+        pg, pr, remote = self._ptrs(peers_gs), self._ptrs(peers_grk), self.empty(W)
+        self._ck(self.lib.phfem_dist_start_p2p(self.ctx.ptr, C.byref(pt), C.c_void_p(self.part.t.node_edge_start),
+                                               nes_off, self.p(self._rk), self.p(psplits), W, me, self.p(pg),
+                                               self.p(pr), self.p(remote)))
+        self._keep = (pg, pr)
+        self.ppart.release()
+        self.ppart, self._rk = None, None
+        return remote
 
     def route_pairs(self, E0, esplits, elo, ehi):
         """Pairs of the own (destination-level) elements [elo, ehi) go straight
@@ -570,11 +645,21 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     tr = getattr(comm, "trace", None) or (lambda w: None)
     E0s = _all_E0(states, comm, per)
     edge_splits = np.asarray(E0s + [Etot], dtype=np.int32)
-    sides = [s.ops.side_records(s.elements, s.elem_edge, s.ops.as_tensor(edge_splits)) for s in states]
-    recvs = comm.all_to_all_v([x[0] for x in sides], [x[1] for x in sides])
+    # peer windows when the backend has them (CUDA ranks): one kernel per
+    # exchange stores every record into its final slot on the owner
+    p2p = P2P and hasattr(states[0].ops, "side_p2p")
+    if p2p:
+        wins = comm.window([s.ops.side_alloc() for s in states])
+        rem = [s.ops.side_p2p(s.elements, s.elem_edge, s.ops.as_tensor(edge_splits), w, s.rank)
+               for s, w in zip(states, wins)]
+        comm.fence()
+        comm.account(rem, 16)
+    else:
+        sides = [s.ops.side_records(s.elements, s.elem_edge, s.ops.as_tensor(edge_splits)) for s in states]
+        recvs = comm.all_to_all_v([x[0] for x in sides], [x[1] for x in sides])
+        for s, rv, (E0, _) in zip(states, recvs, per):
+            s.ops.side_apply(rv, E0)
     tr("side")
-    for s, rv, (E0, _) in zip(states, recvs, per):
-        s.ops.side_apply(rv, E0)
     # fine node ranges from every rank's parent edge offset
     fsplits = np.asarray([0] + [nC + e for e in E0s[1:]] + [nC + Etot], dtype=np.int64)
     counts = []
@@ -595,12 +680,21 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
         fper.append((E0f, B0f))
         s.ops.rebase_part(E0f)
     Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
-    starts = [s.ops.start_records(nC + E0 - int(fsplits[s.rank]), s.ops.as_tensor(esplits))
-              for s, (E0, _) in zip(states, per)]
-    recvs = comm.all_to_all_v([x[0] for x in starts], [x[1] for x in starts])
+    if p2p:
+        bufs = [s.ops.start_alloc(s.ehi - s.elo) for s in states]
+        wg, wr = comm.window([b[0] for b in bufs]), comm.window([b[1] for b in bufs])
+        rem = [s.ops.start_p2p(nC + E0 - int(fsplits[s.rank]), s.ops.as_tensor(esplits), g_, r_, s.rank)
+               for s, (E0, _), g_, r_ in zip(states, per, wg, wr)]
+        comm.fence()
+        comm.account(rem, 5)
+    else:
+        starts = [s.ops.start_records(nC + E0 - int(fsplits[s.rank]), s.ops.as_tensor(esplits))
+                  for s, (E0, _) in zip(states, per)]
+        recvs = comm.all_to_all_v([x[0] for x in starts], [x[1] for x in starts])
+        bufs = [s.ops.start_apply(rv, s.elo, s.ehi - s.elo) for s, rv in zip(states, recvs)]
+    comm.close_windows()
     tr("start")
-    for s, rv, i in zip(states, recvs, ids):
-        gs, grk = s.ops.start_apply(rv, s.elo, s.ehi - s.elo)
+    for s, (gs, grk), i in zip(states, bufs, ids):
         kids, ee = s.ops.children_slots(s.elements, s.elem_edge, gs, grk, nC, s.coords_fine)
         s.dirichlet, s.neumann = _bisect(s.dirichlet, i[:nD], nC), _bisect(s.neumann, i[nD:], nC)
         s.elements, s.elem_edge = kids, ee

@@ -48,12 +48,18 @@ def check_equal(d, ref):
 @pytest.mark.gpu
 @pytest.mark.parametrize("W", [1, 2, 3, 4])
 @pytest.mark.parametrize("name,make,levels", CASES, ids=[c[0] for c in CASES])
-@pytest.mark.parametrize("sort_free", [True, False], ids=["sortfree", "sorted"])
-def test_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels, sort_free):
+@pytest.mark.parametrize("sort_free", ["p2p", "a2a", False], ids=["sortfree", "sortfree-a2a", "sorted"])
+def test_emulated_ranks_equal_single_gpu(ctx, monkeypatch, W, name, make, levels, sort_free):
+    """sortfree: the halo exchanges through peer windows (the CUDA default);
+    sortfree-a2a: the same through all-to-alls; sorted: a sort per level."""
     import torch
     from paper_2401_15557_b200 import capi, dist
     if not sort_free and (levels > 1 or W == 3):
         pytest.skip("sorted-level path: covered by the other cases")
+    if sort_free == "a2a" and W in (1, 3):
+        pytest.skip("all-to-all halo form: W = 2, 4")
+    monkeypatch.setattr(dist, "P2P", sort_free != "a2a")
+    sort_free = bool(sort_free)
     hm = make()
     args = G.config_fields(2)
     ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args, flags=capi.PIPE_GENERIC_EG).download()
@@ -182,3 +188,59 @@ def test_halo_refine_local_ranks_equal_oracle(W, case, levels):
     assert np.array_equal(got["load"], load)
     assert np.array_equal(got["coords"], fine.coords)
     assert np.array_equal(got["elements"], fine.elements)
+
+
+def _ipc_worker(rank, world, port, tmp, case, levels):
+    """One of 2 processes on the SAME GPU: collectives over gloo (CPU staging,
+    test-only), peer windows through CUDA IPC (torch storage sharing) — the
+    plumbing of the multi-GPU peer-window path, on the one GPU available."""
+    import torch
+    import torch.distributed as tdist
+    from paper_2401_15557_b200 import capi, dist
+
+    class StagedComm(dist.TorchComm):
+        def all_reduce(self, ts, op):
+            c = ts[0].cpu()
+            super().all_reduce([c], op)
+            ts[0].copy_(c)
+
+        def all_gather(self, ts):
+            out = super().all_gather([ts[0].cpu()])
+            return [[x.to(ts[0].device) for x in out[0]]]
+
+        def all_to_all_v(self, sends, counts):
+            return [super().all_to_all_v([sends[0].cpu()], counts)[0].to(sends[0].device)]
+
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        hm = dict((c[0], c[1]) for c in CASES)[case]()
+        comm = StagedComm()
+        tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+        states = dist.make_states(hm, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
+        states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, levels, *G.config_fields(2))
+        np.savez(os.path.join(tmp, f"rank{rank}.npz"), **dist.rank_slice(states[0]))
+        tdist.barrier()
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,levels", [("square-L3", 1), ("lshape-L1-3levels", 3)])
+def test_peer_windows_two_processes_one_gpu(ctx, tmp_path, case, levels):
+    """2 processes share the B200: the side / group-start records go through
+    CUDA-IPC peer windows (no kernel waits on another rank: the fences are
+    host barriers); the concatenated slices == the single-GPU pipeline."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2401_15557_b200 import capi, dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.start_processes(_ipc_worker, args=(2, port, str(tmp_path), case, levels), nprocs=2, join=True,
+                       start_method="spawn")
+    got = dist.concat_slices([dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(2)])
+    hm = dict((c[0], c[1]) for c in CASES)[case]()
+    dm = capi.DeviceMesh.upload(ctx, hm)
+    ref = capi.pipeline(ctx, dm, levels, *G.config_fields(2), flags=capi.PIPE_GENERIC_EG).download()
+    check_equal(got, ref)

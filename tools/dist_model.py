@@ -18,6 +18,8 @@ from paper_2401_15557_b200 import capi, dist, meshgen as G  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 13
+if "--a2a" in sys.argv:   # the all-to-all form of the halo exchanges instead of peer windows
+    dist.P2P = False
 BW = 900e9
 
 
@@ -41,6 +43,13 @@ class CountingComm(dist.LocalComm):
         for r in range(self.world):
             self.recv[self.phase][r] += tot - self.nb(ts[r])
         return super().all_gather(ts)
+
+    def account(self, remote, rec_bytes):
+        """peer-window stores: rank d receives what the others stored into it"""
+        for rem in remote:
+            r = rem.cpu().tolist()
+            for d in range(self.world):
+                self.recv[self.phase][d] += int(r[d]) * rec_bytes
 
     def all_to_all_v(self, sends, counts):
         out = super().all_to_all_v(sends, counts)
@@ -84,7 +93,7 @@ top = []
 for r, c in enumerate(ctxs):
     prof = c.profile_read()
     kms.append(sum(v[0] for v in prof.values()))
-    top.append(sorted(((k, round(v[0], 3)) for k, v in prof.items()), key=lambda kv: -kv[1])[:14])
+    top.append(sorted(((k, round(v[0], 3), v[1]) for k, v in prof.items()), key=lambda kv: -kv[1])[:30])
 recv_tot = [sum(v[r] for v in comm.recv.values()) for r in range(W)]
 out = {
     "W": W, "step": f"square L{level - 1} -> L{level} ({nE} triangles), config-5 fields",
