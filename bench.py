@@ -795,6 +795,12 @@ def relaunch_under_torchrun(args) -> int:
     ranks ourselves — one process per GPU, the driver's own launch form — and
     return their exit code.  Rank 0 prints the one JSON line."""
     import socket
+    if not args.dry_run:
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has "
+                  f"{torch.cuda.device_count()}", file=sys.stderr, flush=True)
+            return 2
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]

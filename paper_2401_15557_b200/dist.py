@@ -76,7 +76,7 @@ class TorchComm:
         self.dist = dist
         self.world = dist.get_world_size()
         self.ranks = [dist.get_rank()]
-        self._open = []
+        self._win = {}
 
     def all_reduce(self, ts: list, op: str):
         o = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}[op]
@@ -87,16 +87,30 @@ class TorchComm:
         self.dist.all_gather(out, ts[0])
         return [out]
 
-    def window(self, ts: list) -> list:
+    def window(self, ts: list, key: str = "") -> list:
         """Peer window: every rank's tensor mapped into this process (CUDA IPC
         through torch's storage sharing; over NVLink between GPUs).  Returns,
-        per local state, the W tensors in rank order."""
+        per local state, the W tensors in rank order.  The mappings are cached
+        per key while every rank's buffer stays the same (one all-reduced
+        flag decides; opening IPC handles costs milliseconds, so a step must
+        not pay it)."""
+        t = ts[0]
+        if self.world == 1:
+            return [[t]]
+        st = t.untyped_storage()
+        sig = (st.data_ptr(), st.nbytes())
+        cached = self._win.get(key)
+        need = torch.tensor([0 if cached is not None and cached[0] == sig else 1], dtype=torch.int32,
+                            device=t.device)
+        self.dist.all_reduce(need, op=self.dist.ReduceOp.MAX)
+        if int(need.item()) == 0:
+            return [cached[1]]
         from torch.multiprocessing.reductions import reduce_tensor
         objs = [None] * self.world
-        self.dist.all_gather_object(objs, reduce_tensor(ts[0]))
+        self.dist.all_gather_object(objs, reduce_tensor(t))
         me = self.ranks[0]
-        views = [ts[0] if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
-        self._open.append(views)
+        views = [t if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
+        self._win[key] = (sig, views)
         return [views]
 
     def fence(self):
@@ -105,7 +119,7 @@ class TorchComm:
         self.dist.barrier()
 
     def close_windows(self):
-        self._open = []
+        pass  # mappings stay cached (see window)
 
     def account(self, remote: list, rec_bytes: int):
         pass
@@ -138,7 +152,7 @@ class LocalComm:
     def all_gather(self, ts: list) -> list:
         return [[t.clone() for t in ts] for _ in ts]
 
-    def window(self, ts: list) -> list:
+    def window(self, ts: list, key: str = "") -> list:
         """Peer window of the emulated ranks: their tensors live on one device."""
         return [list(ts) for _ in ts]
 
@@ -322,8 +336,16 @@ class CudaRankOps:
     def _ptrs(self, ts):
         return torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=self.dev)
 
+    def _buffer(self, name, n, shape_tail=(), dtype=torch.int32):
+        """persistent exchange buffer (the peer windows map it once)"""
+        b = getattr(self, name, None)
+        if b is None or b.shape[0] < n:
+            b = torch.empty((max(n, 1),) + shape_tail, dtype=dtype, device=self.dev)
+            setattr(self, name, b)
+        return b[:max(n, 1)]
+
     def side_alloc(self):
-        self._side = self.empty((max(2 * int(self.part.t.E), 1), 4))
+        self._side = self._buffer("_side_buf", 2 * int(self.part.t.E), (4,))
         return self._side
 
     def side_p2p(self, elements, elem_edge, esplits, peers, me):
@@ -336,8 +358,8 @@ class CudaRankOps:
         return remote
 
     def start_alloc(self, n):
-        self._gs = self.empty((max(3 * n, 1),))
-        self._grk = torch.empty((max(3 * n, 1),), dtype=torch.uint8, device=self.dev)
+        self._gs = self._buffer("_gs_buf", 3 * n)
+        self._grk = self._buffer("_grk_buf", 3 * n, dtype=torch.uint8)
         return self._gs, self._grk
 
     def start_p2p(self, nes_off, psplits, peers_gs, peers_grk, me):
@@ -649,7 +671,7 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     # exchange stores every record into its final slot on the owner
     p2p = P2P and hasattr(states[0].ops, "side_p2p")
     if p2p:
-        wins = comm.window([s.ops.side_alloc() for s in states])
+        wins = comm.window([s.ops.side_alloc() for s in states], "side")
         rem = [s.ops.side_p2p(s.elements, s.elem_edge, s.ops.as_tensor(edge_splits), w, s.rank)
                for s, w in zip(states, wins)]
         comm.fence()
@@ -682,7 +704,7 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
     if p2p:
         bufs = [s.ops.start_alloc(s.ehi - s.elo) for s in states]
-        wg, wr = comm.window([b[0] for b in bufs]), comm.window([b[1] for b in bufs])
+        wg, wr = comm.window([b[0] for b in bufs], "gs"), comm.window([b[1] for b in bufs], "grk")
         rem = [s.ops.start_p2p(nC + E0 - int(fsplits[s.rank]), s.ops.as_tensor(esplits), g_, r_, s.rank)
                for s, (E0, _), g_, r_ in zip(states, per, wg, wr)]
         comm.fence()
