@@ -599,6 +599,43 @@ phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology* ppart, c
                                   int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
                                   int32_t* remote);
 
+/* Distributed input level with peer windows (dist.py _edge_generation): key
+ * ranges aligned to 256-node tiles so that bucket b = max >> bs (bs =
+ * phfem_dist_bucket_bits, the same on every rank) has one owner (bsplits:
+ * first bucket per rank, W + 1, last = NB = ceil(nC / 2^bs)).
+ *  phfem_dist_bucket_hist    own occurrences per global bucket -> hist[NB]
+ *                            (the reference's node-range error, global ids);
+ *  phfem_dist_bucket_cursors from the all-gathered hist_all[W][NB]: this
+ *                            rank's cursor in every bucket (owner-local slot
+ *                            of its first item), its own bucket offsets
+ *                            boff_me[nb + 1] and item count (synchronises);
+ *  phfem_dist_scatter_p2p    packs every own occurrence and stores it into
+ *                            the owner's item array (peer_items[W], device
+ *                            pointer array) at its cursor — MSD bucket
+ *                            scatter fused with the exchange;
+ *  phfem_dist_dedup_items    the owner's tile / emit passes over its
+ *                            bucketed items (as phfem_dist_dedup_ex).       */
+int phfem_dist_bucket_bits(int32_t nC_all, int32_t nE_all);
+/* the dedup's pairs of other ranks' elements, re-based by E0, stored straight
+ * into the element owners' elem_edge (peer_ee[W]; esplits: first element per
+ * rank) — phfem_dist_route_pairs + the all-to-all + phfem_dist_apply_pairs
+ * in one kernel                                                             */
+phfem_status phfem_dist_pairs_p2p(phfem_ctx* ctx, const int32_t* pairs, int64_t n, int32_t E0,
+                                  const int32_t* esplits, int32_t W, int32_t self, int32_t* const* peer_ee,
+                                  int32_t* remote);
+phfem_status phfem_dist_bucket_hist(phfem_ctx* ctx, const int32_t* elements, int32_t n, int32_t elo,
+                                    int32_t nC_all, int32_t nE_all, int32_t* hist);
+phfem_status phfem_dist_bucket_cursors(phfem_ctx* ctx, const int32_t* hist_all, int32_t W, int64_t NB, int32_t me,
+                                       const int32_t* bsplits, int32_t* cursor, int32_t* boff_me,
+                                       int64_t* n_items_me);
+phfem_status phfem_dist_scatter_p2p(phfem_ctx* ctx, const int32_t* elements, int32_t n, int32_t elo,
+                                    int32_t nC_all, int32_t nE_all, int32_t* cursor, const int32_t* bsplits,
+                                    int32_t W, int32_t me, uint64_t* const* peer_items, int32_t* remote);
+phfem_status phfem_dist_dedup_items(phfem_ctx* ctx, uint64_t* items, int64_t n, const int32_t* boff,
+                                    int32_t node_lo, int32_t node_hi, int32_t nC_all, int32_t nE_all,
+                                    int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge,
+                                    phfem_topology* out, int32_t* pairs, int64_t* n_pairs);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

@@ -170,7 +170,9 @@ EXPORTED = [
     "phfem_dist_neumann_apply", "phfem_dist_children", "phfem_dist_midpoints",
     "phfem_dist_side_records", "phfem_dist_side_apply", "phfem_dist_refine_level_side",
     "phfem_dist_start_records", "phfem_dist_start_apply", "phfem_dist_children_slots",
-    "phfem_dist_side_p2p", "phfem_dist_start_p2p",
+    "phfem_dist_side_p2p", "phfem_dist_start_p2p", "phfem_dist_bucket_bits", "phfem_dist_bucket_hist",
+    "phfem_dist_pairs_p2p",
+    "phfem_dist_bucket_cursors", "phfem_dist_scatter_p2p", "phfem_dist_dedup_items",
     "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
     "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
     "phfem_error_multiplier", "phfem_midpoint_traces", "phfem_csc_to_csr", "phfem_csr_spmv",
@@ -311,6 +313,13 @@ def load_library(path: str = LIB_PATH):
         "phfem_dist_start_apply": (C.c_int, [vp, vp, i64, i32, vp, vp]),
         "phfem_dist_children_slots": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, vp, vp, vp]),
         "phfem_dist_side_p2p": (C.c_int, [vp, vp, vp, i32, vp, i32, i32, vp, vp]),
+        "phfem_dist_bucket_bits": (C.c_int, [i32, i32]),
+        "phfem_dist_pairs_p2p": (C.c_int, [vp, vp, i64, i32, vp, i32, i32, vp, vp]),
+        "phfem_dist_bucket_hist": (C.c_int, [vp, vp, i32, i32, i32, i32, vp]),
+        "phfem_dist_bucket_cursors": (C.c_int, [vp, vp, i32, i64, i32, vp, vp, vp, P(i64)]),
+        "phfem_dist_scatter_p2p": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp]),
+        "phfem_dist_dedup_items": (C.c_int, [vp, vp, i64, vp, i32, i32, i32, i32, i32, i32, vp,
+                                             P(phfem_topology), vp, P(i64)]),
         "phfem_dist_start_p2p": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, vp, i32, i32, vp, vp, vp]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),

@@ -335,15 +335,29 @@ __global__ void k_dist_start_apply(const Rec3* __restrict__ recv, int64_t n, int
 // straight into its final slot there — no count pass, no send buffer, no
 // all-to-all, no apply pass.  remote[d] counts the records stored into rank
 // d's window by this rank (d != self), for the byte accounting.
-__device__ __forceinline__ void count_remote(int d, int self, int32_t* remote) {
+// (per-block SMEM counters, flushed once per block: one global counter per
+// destination hit by every warp serialised the kernels at L2 — 0.3-0.5 ms)
+constexpr int kRemoteMax = 64;
+__device__ __forceinline__ void count_remote(int d, int self, int32_t* srem) {
   const unsigned peers = __match_any_sync(__activemask(), d);
-  if (d != self && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(remote + d, __popc(peers));
+  if (d != self && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(srem + (d & (kRemoteMax - 1)), __popc(peers));
+}
+__device__ __forceinline__ void remote_init(int32_t* srem) {
+  for (int i = threadIdx.x; i < kRemoteMax; i += blockDim.x) srem[i] = 0;
+  __syncthreads();
+}
+__device__ __forceinline__ void remote_flush(const int32_t* srem, int W, int32_t* remote) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < W && i < kRemoteMax; i += blockDim.x)
+    if (srem[i]) atomicAdd(remote + i, srem[i]);
 }
 
 __global__ void __launch_bounds__(256) k_dist_side_p2p(const int32_t* __restrict__ elements,
                                                        const int32_t* __restrict__ elem_edge, int n,
                                                        const int32_t* __restrict__ esplits, int W, int self,
                                                        int4* const* __restrict__ peer_side, int32_t* remote) {
+  __shared__ int32_t srem[kRemoteMax];
+  remote_init(srem);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * (int64_t)n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / 3;
@@ -354,8 +368,9 @@ __global__ void __launch_bounds__(256) k_dist_side_p2p(const int32_t* __restrict
     const int4 r = make_int4(elem_edge[3 * m + (k == 2 ? 0 : k + 1)], elem_edge[3 * m + (k == 0 ? 2 : k - 1)],
                              elements[i], 0);
     peer_side[d][2 * (int64_t)(e - __ldg(esplits + d)) + (s < 0 ? 1 : 0)] = r;
-    count_remote(d, self, remote);
+    count_remote(d, self, srem);
   }
+  remote_flush(srem, W, remote);
 }
 
 __global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restrict__ edge_elements,
@@ -366,6 +381,8 @@ __global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restric
                                                         const int32_t* __restrict__ psplits, int W, int self,
                                                         int32_t* const* __restrict__ peer_gs,
                                                         uint8_t* const* __restrict__ peer_grk, int32_t* remote) {
+  __shared__ int32_t srem[kRemoteMax];
+  remote_init(srem);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * (int64_t)E;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t le = i >> 1;
@@ -379,8 +396,30 @@ __global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restric
       peer_gs[d][slot] = fine_nes[le + nes_off];
       peer_grk[d][slot] = rk[le];
     }
-    if (d >= 0) count_remote(d, self, remote);
+    if (d >= 0) count_remote(d, self, srem);
   }
+  remote_flush(srem, W, remote);
+}
+
+// reverse pairs of the input level through peer windows: (slot 3m+l, local
+// edge or ~edge) of another rank's element -> global id stored straight into
+// that element owner's elem_edge (esplits: first element per rank)
+__global__ void __launch_bounds__(256) k_dist_pairs_p2p(const int2* __restrict__ pairs, int64_t n, int E0,
+                                                        const int32_t* __restrict__ esplits, int W, int self,
+                                                        int32_t* const* __restrict__ peer_ee, int32_t* remote) {
+  __shared__ int32_t srem[kRemoteMax];
+  remote_init(srem);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 p = pairs[i];
+    int d = -1;
+    if (p.x >= 0) {
+      const int m = p.x / 3;
+      d = dest_of(esplits, W, m);
+      peer_ee[d][p.x - 3 * (int64_t)__ldg(esplits + d)] = p.y >= 0 ? p.y + E0 : ~(~p.y + E0);
+    }
+    if (d >= 0) count_remote(d, self, srem);
+  }
+  remote_flush(srem, W, remote);
 }
 
 // count pass, exclusive offsets, pack pass of a route_block kernel
@@ -674,7 +713,7 @@ PHFEM_API phfem_status phfem_dist_start_apply(phfem_ctx* ctx, const int32_t* rec
 PHFEM_API phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
                                            int32_t n, const int32_t* esplits, int32_t W, int32_t self,
                                            int32_t* const* peer_side, int32_t* remote) {
-  if (!ctx || !esplits || !peer_side || !remote || W < 1 || self < 0 || self >= W || n < 0 ||
+  if (!ctx || !esplits || !peer_side || !remote || W < 1 || W > kRemoteMax || self < 0 || self >= W || n < 0 ||
       (n && (!elements || !elem_edge)))
     return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
@@ -689,7 +728,7 @@ PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology
                                             int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
                                             int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
                                             int32_t* remote) {
-  if (!ctx || !ppart || !psplits || !peer_gs || !peer_grk || !remote || W < 1 || self < 0 || self >= W ||
+  if (!ctx || !ppart || !psplits || !peer_gs || !peer_grk || !remote || W < 1 || W > kRemoteMax || self < 0 || self >= W ||
       (ppart->E && (!fine_nes || !rk)))
     return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
@@ -699,5 +738,17 @@ PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology
                                                              ctx->stream>>>(
         ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus, fine_nes, nes_off, rk, E, psplits, W,
         self, peer_gs, peer_grk, remote));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_pairs_p2p(phfem_ctx* ctx, const int32_t* pairs, int64_t n, int32_t E0,
+                                            const int32_t* esplits, int32_t W, int32_t self, int32_t* const* peer_ee,
+                                            int32_t* remote) {
+  if (!ctx || (n && !pairs) || !esplits || !peer_ee || !remote || W < 1 || W > kRemoteMax || self < 0 || self >= W)
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_pairs_p2p", k_dist_pairs_p2p<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const int2*>(pairs), n, E0, esplits, W, self, peer_ee, remote));
   return PHFEM_OK;
 }

@@ -794,10 +794,18 @@ struct EgOwn {
   int32_t* npairs;  // device counter, zeroed by the caller
 };
 
+// items already scattered into their buckets by the senders (distributed
+// input level with peer windows): the bucket offsets and the item array
+struct EgPre {
+  const int32_t* boff;  // [nb + 1] exclusive bucket offsets
+  uint64_t* items;      // [nd] packed items, bucketed
+};
+
 template <typename Source>
 static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source source,
                             phfem_topology* out, int2* pairs, const char* who,
-                            const EgFuse* fuse = nullptr, const EgOwn* own = nullptr) {
+                            const EgFuse* fuse = nullptr, const EgOwn* own = nullptr,
+                            const EgPre* pre = nullptr) {
   const int64_t nC = P.nC;
   const int64_t cap_e = std::max<int64_t>(nd, 1);
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
@@ -825,8 +833,13 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 2 * (ntiles + 1), ctx->stream));
 
   const int nsub = kTileNodes >> P.bs;
-  PHFEM_TRY(source(0, bcount, (uint64_t*)nullptr));
-  PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
+  if (pre) {
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(boff, pre->boff, sizeof(int32_t) * ((int64_t)P.nb + 1), cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+  } else {
+    PHFEM_TRY(source(0, bcount, (uint64_t*)nullptr));
+    PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
+  }
   PHFEM_LAUNCH(ctx, "k_eg_tile_max", k_eg_tile_max<<<grid_for(ntiles, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
       boff, P.nb, nsub, ntiles, ctx->derr));
   int32_t* cursor = bcount;  // reuse as scatter cursor
@@ -849,14 +862,15 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   uint64_t *g1 = nullptr, *g2 = nullptr;
   uint8_t* gnode = nullptr;
   int4* rec = nullptr;
-  PHFEM_TRY(dalloc(ctx, &items, nd));
+  if (pre) items = pre->items;
+  else PHFEM_TRY(dalloc(ctx, &items, nd));
   PHFEM_TRY(dalloc(ctx, &rec, nd));
   if (max_tile > kTileCap) {  // some tile does not fit SMEM: global scratch
     PHFEM_TRY(dalloc(ctx, &g1, nd));
     PHFEM_TRY(dalloc(ctx, &g2, nd));
     PHFEM_TRY(dalloc(ctx, &gnode, nd));
   }
-  PHFEM_TRY(source(1, cursor, items));
+  if (!pre) PHFEM_TRY(source(1, cursor, items));
 
   EgOut o;
   memset(&o, 0, sizeof o);
@@ -929,7 +943,7 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
                                   cudaMemcpyDeviceToDevice, ctx->stream));
   PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[2], tileB + ntiles, sizeof(int32_t),
                                   cudaMemcpyDeviceToDevice, ctx->stream));
-  dfree(ctx, items);
+  if (!pre) dfree(ctx, items);
   dfree(ctx, rec);
   dfree(ctx, g1);
   dfree(ctx, g2);
@@ -1100,3 +1114,186 @@ phfem_status build_topology_fused(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_
   return PHFEM_OK;
 }
 }  // namespace phfem
+
+// ---------------------------------------------------------------------------
+// Distributed input level with peer windows (dist.py _edge_generation, P2P):
+// key ranges aligned to 256-node tiles, so a bucket (2^bs max nodes) has one
+// owner and the bucket index max >> bs is global.  Every rank histograms its
+// own occurrences per global bucket (k_eg_count), the histograms are
+// all-gathered, every rank derives its private cursor inside each bucket
+// (owner-local bucket start + the lower ranks' counts), and ONE kernel packs
+// each occurrence and stores it straight into its slot of the owner's item
+// array (mapped peer window) — the MSD bucket scatter fused with the
+// exchange.  The owner then runs the tile / emit passes on its items.
+namespace phfem {
+__global__ void k_dist_bucket_total(const int32_t* __restrict__ hist_all, int W, int64_t NB,
+                                    int32_t* __restrict__ total) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < NB; b += (int64_t)gridDim.x * blockDim.x) {
+    int32_t t = 0;
+    for (int r = 0; r < W; ++r) t += hist_all[(int64_t)r * NB + b];
+    total[b] = t;
+  }
+}
+
+__device__ __forceinline__ int bucket_owner(const int32_t* __restrict__ bsplits, int W, int64_t b) {
+  int lo = 0, hi = W;  // last r with bsplits[r] <= b
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(bsplits + mid) <= b) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_dist_bucket_cursor(const int32_t* __restrict__ hist_all, int W, int64_t NB, int me,
+                                     const int32_t* __restrict__ gp, const int32_t* __restrict__ bsplits,
+                                     int32_t* __restrict__ cursor, int32_t* __restrict__ boff_me) {
+  const int64_t b0 = bsplits[me], b1 = bsplits[me + 1];
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= NB; b += (int64_t)gridDim.x * blockDim.x) {
+    if (b < NB) {
+      const int d = bucket_owner(bsplits, W, b);
+      int32_t c = gp[b] - gp[bsplits[d]];
+      for (int r = 0; r < me; ++r) c += hist_all[(int64_t)r * NB + b];
+      cursor[b] = c;
+    }
+    if (b >= b0 && b <= b1) boff_me[b - b0] = gp[b] - gp[b0];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dist_scatter_p2p(const int32_t* __restrict__ elements, int64_t n, int elo,
+                                                          EgParams P, int32_t* __restrict__ cursor,
+                                                          const int32_t* __restrict__ bsplits, int W, int me,
+                                                          uint64_t* const* __restrict__ peer_items,
+                                                          int32_t* __restrict__ remote) {
+  __shared__ int32_t srem[64];  // per-block remote counts (one global atomic per block and rank)
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) srem[i] = 0;
+  __syncthreads();
+  const uint32_t hl_mask = (1u << P.bs) - 1u;
+  for (int64_t m0 = (int64_t)blockIdx.x * blockDim.x; m0 < n; m0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = m0 + threadIdx.x;
+    const bool valid = m < n;
+    int t[3] = {0, 0, 0};
+    if (valid) {
+      t[0] = __ldg(elements + 3 * m);
+      t[1] = __ldg(elements + 3 * m + 1);
+      t[2] = __ldg(elements + 3 * m + 2);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      const int hi = a > b ? a : b;
+      const int lo = a > b ? b : a;
+      const unsigned key = valid ? ((unsigned)hi >> P.bs) : 0xffffffffu;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(grp) - 1;
+      int base = 0;
+      if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (valid) {
+        const int d = bucket_owner(bsplits, W, key);
+        const uint32_t occ = (uint32_t)(3 * ((int64_t)elo + m) + s);
+        peer_items[d][base + __popc(grp & lanemask_lt())] =
+            eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
+        if (d != me && (int)lane_id() == leader) atomicAdd(srem + (d & 63), __popc(grp));
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W && i < 64; i += blockDim.x)
+    if (srem[i]) atomicAdd(remote + i, srem[i]);
+}
+}  // namespace phfem
+
+PHFEM_API int phfem_dist_bucket_bits(int32_t nC_all, int32_t nE_all) {
+  const int tb = bits_for(std::max<int64_t>((int64_t)nC_all - 1, 1)) + bits_for(std::max<int64_t>(3 * (int64_t)nE_all - 1, 1)) + 1;
+  return std::min(8, 64 - tb);
+}
+
+PHFEM_API phfem_status phfem_dist_bucket_hist(phfem_ctx* ctx, const int32_t* elements, int32_t n, int32_t elo,
+                                              int32_t nC_all, int32_t nE_all, int32_t* hist) {
+  if (!ctx || !hist || n < 0 || (n && !elements)) return PHFEM_ERR_INVALID_ARGUMENT;
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, nC_all, nC_all, nE_all, 0, &P));
+  P.nE = n;
+  PHFEM_CUDA(ctx, cudaMemsetAsync(hist, 0, sizeof(int32_t) * P.nb, ctx->stream));
+  PHFEM_TRY(errors_reset(ctx));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_eg_count", k_eg_count<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        elements, P, hist, ctx->derr));
+  PHFEM_TRY(errors_fetch(ctx));
+  if (ctx->herr->misc != ~0ull)
+    return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE, "build_topology: element %lld has a node index outside 1..%lld",
+                     (long long)ctx->herr->misc + elo + 1, (long long)nC_all);
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_bucket_cursors(phfem_ctx* ctx, const int32_t* hist_all, int32_t W, int64_t NB,
+                                                 int32_t me, const int32_t* bsplits, int32_t* cursor,
+                                                 int32_t* boff_me, int64_t* n_items_me) {
+  if (!ctx || !hist_all || !bsplits || !cursor || !boff_me || !n_items_me || W < 1 || me < 0 || me >= W || NB < 1)
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  int32_t* gp = nullptr;
+  PHFEM_TRY(dalloc(ctx, &gp, NB + 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(gp + NB, 0, sizeof(int32_t), ctx->stream));
+  PHFEM_LAUNCH(ctx, "k_dist_bucket_total", k_dist_bucket_total<<<grid_for(NB, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      hist_all, W, NB, gp));
+  PHFEM_TRY(scan_exclusive_i32(ctx, gp, gp, NB + 1, nullptr));
+  PHFEM_LAUNCH(ctx, "k_dist_bucket_cursor", k_dist_bucket_cursor<<<grid_for(NB + 1, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      hist_all, W, NB, me, gp, bsplits, cursor, boff_me));
+  int32_t h[2];
+  int32_t b01[2];
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(b01, bsplits + me, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[0], gp + b01[0], sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[1], gp + b01[1], sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *n_items_me = (int64_t)h[1] - h[0];
+  dfree(ctx, gp);
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_scatter_p2p(phfem_ctx* ctx, const int32_t* elements, int32_t n, int32_t elo,
+                                              int32_t nC_all, int32_t nE_all, int32_t* cursor, const int32_t* bsplits,
+                                              int32_t W, int32_t me, uint64_t* const* peer_items, int32_t* remote) {
+  if (!ctx || !cursor || !bsplits || !peer_items || !remote || W < 1 || W > 64 || me < 0 || me >= W || n < 0 ||
+      (n && !elements))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, nC_all, nC_all, nE_all, 0, &P));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
+  if (n > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_scatter_p2p", k_dist_scatter_p2p<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        elements, n, elo, P, cursor, bsplits, W, me, peer_items, remote));
+  return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_dedup_items(phfem_ctx* ctx, uint64_t* items, int64_t n, const int32_t* boff,
+                                              int32_t node_lo, int32_t node_hi, int32_t nC_all, int32_t nE_all,
+                                              int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge,
+                                              phfem_topology* out, int32_t* pairs, int64_t* n_pairs) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || (!items && n) || !boff || !pairs || !self_elem_edge || !n_pairs || node_lo < 0 || node_hi < node_lo ||
+      node_hi > nC_all || self_lo < 0 || self_hi < self_lo || self_hi > nE_all ||
+      3 * (int64_t)nE_all >= (int64_t(1) << 31))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  *n_pairs = 0;
+  out->nC = node_hi - node_lo;
+  out->nE = nE_all;
+  EgParams P;
+  PHFEM_TRY(eg_params(ctx, (int64_t)node_hi - node_lo, nC_all, nE_all, node_lo, &P));
+  auto none = [&](int, int32_t*, uint64_t*) -> phfem_status { return PHFEM_OK; };
+  EgOwn own{self_elem_edge, 3 * (int64_t)self_lo, 3 * (int64_t)self_hi, nullptr};
+  EgPre pre{boff, items};
+  PHFEM_TRY(dalloc(ctx, &own.npairs, 1));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(own.npairs, 0, sizeof(int32_t), ctx->stream));
+  phfem_status st = eg_core(ctx, P, n, none, out, reinterpret_cast<int2*>(pairs), "dist_dedup", nullptr, &own, &pre);
+  int32_t np = 0;
+  if (st == PHFEM_OK) {
+    if (cudaMemcpyAsync(&np, own.npairs, sizeof np, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      st = cuda_fail(ctx, cudaGetLastError(), "dist_dedup: pair count");
+  }
+  dfree(ctx, own.npairs);
+  *n_pairs = np;
+  return st;
+}

@@ -243,6 +243,58 @@ class CudaRankOps:
                                                  self.p(cnt), self.p(off), self.p(send)))
         return send[:3 * (ehi - elo)], cnt.tolist()
 
+    # -- input level through peer windows (phfem_dist_bucket_* / scatter_p2p) ------
+    def bucket_bits(self, nC, nE):
+        return int(self.lib.phfem_dist_bucket_bits(nC, nE))
+
+    def bucket_hist(self, elements, elo, nC, nE, NB):
+        hist = self.empty((NB,))
+        self._ck(self.lib.phfem_dist_bucket_hist(self.ctx.ptr, self.p(elements), int(elements.shape[0]), elo, nC, nE,
+                                                 self.p(hist)))
+        return hist
+
+    def bucket_cursors(self, hist_all, me, bsplits):
+        W, NB = int(hist_all.shape[0]), int(hist_all.shape[1])
+        b = bsplits.cpu().tolist()
+        self._cursor = self.empty((NB,))
+        self._boff = self.empty((b[me + 1] - b[me] + 1,))
+        n = C.c_int64(0)
+        self._ck(self.lib.phfem_dist_bucket_cursors(self.ctx.ptr, self.p(hist_all.contiguous()), W, NB, me,
+                                                    self.p(bsplits), self.p(self._cursor), self.p(self._boff),
+                                                    C.byref(n)))
+        return int(n.value)
+
+    def items_alloc(self, n):
+        self._items = self._buffer("_items_buf", n, dtype=torch.int64)
+        return self._items
+
+    def scatter_p2p(self, elements, elo, nC, nE, bsplits, peers, me):
+        W = len(peers)
+        ptrs, remote = self._ptrs(peers), self.empty(W)
+        self._ck(self.lib.phfem_dist_scatter_p2p(self.ctx.ptr, self.p(elements), int(elements.shape[0]), elo, nC, nE,
+                                                 self.p(self._cursor), self.p(bsplits), W, me, self.p(ptrs),
+                                                 self.p(remote)))
+        self._keep = ptrs
+        return remote
+
+    def dedup_items(self, n, nlo, nhi, nC, nE, own_range):
+        """the owner's tile / emit passes over the items the ranks stored into
+        its window (own elements' elem_edge in place, the others as pairs)"""
+        pairs = self.empty((max(2 * n, 1), 2))
+        t = capi.phfem_topology()
+        npairs = C.c_int64(0)
+        lo, hi = own_range
+        ee = self._buffer("_ee_buf", hi - lo, (3,))  # persistent: the element owner's peer window
+        self._ck(self.lib.phfem_dist_dedup_items(self.ctx.ptr, self.p(self._items), n, self.p(self._boff), nlo, nhi,
+                                                 nC, nE, lo, hi, self.p(ee), C.byref(t), self.p(pairs),
+                                                 C.byref(npairs)))
+        self._cursor = self._boff = None
+        self.part = capi.Topology(self.ctx, t)
+        self.pairs = pairs[:int(npairs.value)]
+        self._pairs = (pairs.data_ptr(), int(npairs.value), False)
+        self._ee_next = ee[:hi - lo]
+        return int(t.E), int(t.n_boundary)
+
     def dedup(self, recv, nlo, nhi, nC, nE, own_range=None):
         """own_range = the rank's elements [lo, hi): their elem_edge entries are
         written in place (local ids, re-based in route_pairs); only the other
@@ -395,6 +447,33 @@ class CudaRankOps:
         self.pairs = None
         c = cnt.tolist()
         return send[:sum(c)], c
+
+    def ee_window(self):
+        return self._ee_next
+
+    def rebase_own_ee(self, E0, elo, ehi):
+        """own entries (local ids from the emit pass) -> global; must precede
+        the peers' stores into this window (they store global ids)"""
+        if E0 and ehi > elo:
+            self.rebase(self._ee_next.data_ptr(), 3 * (ehi - elo), E0, 2)
+
+    def pairs_p2p(self, E0, esplits, peers, me):
+        """the other ranks' entries stored straight into their elem_edge windows"""
+        ptr, n, owned = self._pairs
+        W = len(peers)
+        pp, remote = self._ptrs(peers), self.empty(W)
+        self._ck(self.lib.phfem_dist_pairs_p2p(self.ctx.ptr, C.c_void_p(ptr) if n else None, n, E0, self.p(esplits),
+                                               W, me, self.p(pp), self.p(remote)))
+        if owned:
+            self.ctx.free(ptr)
+        self._pairs = (0, 0, False)
+        self.pairs = None
+        self._keep = pp
+        return remote
+
+    def take_ee(self):
+        ee, self._ee_next = self._ee_next, None
+        return ee
 
     def apply_pairs(self, recv, elo, ehi):
         ee, self._ee_next = self._ee_next, None
@@ -557,17 +636,41 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
     comm.all_reduce(hists, "sum")
     splits = balanced_splits(hists[0].cpu().numpy(), bins, W)
     tr("hist")
-    # forward all-to-all of the occurrences, local dedup
-    packed = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(splits), pack=True) for s in states]
-    tr("pack")
-    recvs = comm.all_to_all_v([p[0] for p in packed], [p[1] for p in packed])
-    tr("a2a")
     eb = []
-    for s, rv in zip(states, recvs):
-        r = s.rank
-        E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE, own_range=(s.elo, s.ehi))
-        eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
-    tr("dedup")
+    p2p = P2P and hasattr(states[0].ops, "scatter_p2p")
+    if p2p:
+        # key ranges on 256-node tile boundaries: every MSD bucket has one owner
+        # and its global index is max >> bs; the ranks store their packed
+        # occurrences straight into the owners' bucket arrays (peer windows)
+        splits = np.asarray([0] + [int(x) // 256 * 256 for x in splits[1:-1]] + [nC], dtype=np.int32)
+        bs = states[0].ops.bucket_bits(nC, nE)
+        NB = (nC + (1 << bs) - 1) >> bs
+        bsplits = np.asarray([int(x) >> bs for x in splits[:-1]] + [NB], dtype=np.int32)
+        hists = [s.ops.bucket_hist(s.elements, s.elo, nC, nE, NB) for s in states]
+        gh = comm.all_gather(hists)
+        nitems = [s.ops.bucket_cursors(torch.stack(g), s.rank, s.ops.as_tensor(bsplits)) for s, g in zip(states, gh)]
+        wins = comm.window([s.ops.items_alloc(n) for s, n in zip(states, nitems)], "items")
+        rem = [s.ops.scatter_p2p(s.elements, s.elo, nC, nE, s.ops.as_tensor(bsplits), w, s.rank)
+               for s, w in zip(states, wins)]
+        comm.fence()
+        comm.account(rem, 8)
+        tr("scatter")
+        for s, n in zip(states, nitems):
+            r = s.rank
+            E_r, B_r = s.ops.dedup_items(n, int(splits[r]), int(splits[r + 1]), nC, nE, own_range=(s.elo, s.ehi))
+            eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
+        tr("dedup")
+    else:
+        # forward all-to-all of the occurrences, local dedup
+        packed = [s.ops.occurrences(s.elements, s.elo, s.ehi, s.ops.as_tensor(splits), pack=True) for s in states]
+        tr("pack")
+        recvs = comm.all_to_all_v([p[0] for p in packed], [p[1] for p in packed])
+        tr("a2a")
+        for s, rv in zip(states, recvs):
+            r = s.rank
+            E_r, B_r = s.ops.dedup(rv, int(splits[r]), int(splits[r + 1]), nC, nE, own_range=(s.elo, s.ehi))
+            eb.append(torch.tensor([E_r, B_r], dtype=torch.int64, device=s.coords.device))
+        tr("dedup")
     gath = comm.all_gather(eb)
     per = []
     for s, g in zip(states, gath):
@@ -576,13 +679,27 @@ def _edge_generation(states: List[RankState], comm, nC: int, nE: int, esplits: n
         per.append((E0, B0))
         s.ops.rebase_part(E0)
     Etot, Btot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
-    # reverse all-to-all: (element slot, global edge id) to the element owners
-    routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits), s.elo, s.ehi) for s, (E0, _) in zip(states, per)]
-    recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
-    tr("route")
-    for s, rv in zip(states, recvs):
-        s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
-    tr("pairs")
+    if p2p:
+        # (slot, global edge id) stored straight into the element owners' elem_edge
+        wins = comm.window([s.ops.ee_window() for s in states], "ee")
+        for s, (E0, _) in zip(states, per):
+            s.ops.rebase_own_ee(E0, s.elo, s.ehi)
+        comm.fence()   # every rank's own entries final before the peers store theirs
+        rem = [s.ops.pairs_p2p(E0, s.ops.as_tensor(esplits), w, s.rank)
+               for s, (E0, _), w in zip(states, per, wins)]
+        comm.fence()
+        comm.account(rem, 4)
+        for s in states:
+            s.elem_edge = s.ops.take_ee()
+        tr("pairs")
+    else:
+        # reverse all-to-all: (element slot, global edge id) to the element owners
+        routed = [s.ops.route_pairs(E0, s.ops.as_tensor(esplits), s.elo, s.ehi) for s, (E0, _) in zip(states, per)]
+        recvs = comm.all_to_all_v([x[0] for x in routed], [x[1] for x in routed])
+        tr("route")
+        for s, rv in zip(states, recvs):
+            s.elem_edge = s.ops.apply_pairs(rv, s.elo, s.ehi)
+        tr("pairs")
     return splits, per, (Etot, Btot)
 
 

@@ -25,7 +25,11 @@ CASES = [("crisscross-L1", lambda: O.refine_levels(G.crisscross_square(), 1), 1)
          ("stress-L3", lambda: O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 3), 3)), 1),
          ("fan-30", lambda: G.fan(30, True), 1),
          ("crisscross-L1-2levels", lambda: O.refine_levels(G.crisscross_square(), 1), 2),
-         ("lshape-L1-3levels", lambda: O.refine_levels(G.lshape_6tri(), 1), 3)]
+         ("lshape-L1-3levels", lambda: O.refine_levels(G.lshape_6tri(), 1), 3),
+         # > 256 W nodes: the tile-aligned key ranges of the peer-window input
+         # level give every rank edges of its own (smaller meshes: one owner)
+         ("square-L6", lambda: O.refine_levels(G.square_2tri(), 6), 1),
+         ("stress-L6", lambda: O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 6), 6)), 1)]
 
 
 def check_equal(d, ref):
