@@ -574,6 +574,28 @@ phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* 
                                           int32_t node_lo, int32_t node_hi, int32_t nE_all,
                                           const int32_t* neu_parent_ids, int32_t nN_parent,
                                           phfem_topology* out, uint8_t* rk, double* coords_fine, phfem_csr* C);
+/* phfem_dist_refine_level_side in two halves, so that the rank's fine
+ * offsets are known before the level kernel writes: _count (tile counts from
+ * the side records; Ef = the rank's fine edges, nneu = its parent Neumann
+ * edges when with_C; synchronises; *plan for _run) and _run (f_off = the
+ * rank's first global fine edge id, nnz_off = its first C entry, written
+ * straight into the fine lists, node_edge_start and C's row pointers; frees
+ * the plan).  phfem_dist_classify_ex: retained_pos / retained_edges with the
+ * rank's first retained row r_off and first edge id e_off added.           */
+phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p, const int32_t* side,
+                                    const int32_t* neu_parent_ids, int32_t nN_parent, int with_C, int32_t* Ef,
+                                    int32_t* nneu, void** plan);
+phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc, int32_t node_lo,
+                                  int32_t node_hi, int32_t nE_all, int32_t f_off, int32_t nnz_off,
+                                  phfem_topology* out, uint8_t* rk, double* coords_fine, phfem_csr* C);
+/* assemble_dirichlet of a rank whose retained positions start at r_off:
+ * out[0 .. L) holds rows r_off .. r_off + L                               */
+phfem_status phfem_dist_dirichlet(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* part,
+                                  const phfem_classification* cls, const phfem_field* uD, double t, int32_t r_off,
+                                  double* out);
+phfem_status phfem_dist_classify_ex(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                    const int32_t* dir_ids_local, int32_t nD, const int32_t* neu_ids_local,
+                                    int32_t nN, int32_t r_off, int32_t e_off, phfem_classification* out);
 phfem_status phfem_dist_start_records(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
                                       int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
                                       int32_t* counts, int32_t* offsets, int32_t* send);

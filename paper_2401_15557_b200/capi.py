@@ -171,7 +171,7 @@ EXPORTED = [
     "phfem_dist_side_records", "phfem_dist_side_apply", "phfem_dist_refine_level_side",
     "phfem_dist_start_records", "phfem_dist_start_apply", "phfem_dist_children_slots",
     "phfem_dist_side_p2p", "phfem_dist_start_p2p", "phfem_dist_bucket_bits", "phfem_dist_bucket_hist",
-    "phfem_dist_pairs_p2p",
+    "phfem_dist_pairs_p2p", "phfem_dist_dirichlet", "phfem_dist_level_count", "phfem_dist_level_run", "phfem_dist_classify_ex",
     "phfem_dist_bucket_cursors", "phfem_dist_scatter_p2p", "phfem_dist_dedup_items",
     "phfem_from_triplets", "phfem_saddle_matrix", "phfem_step_matrix",
     "phfem_constraint_residual", "phfem_exact_multiplier", "phfem_error_l2", "phfem_error_h1",
@@ -314,6 +314,14 @@ def load_library(path: str = LIB_PATH):
         "phfem_dist_children_slots": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, vp, vp, vp]),
         "phfem_dist_side_p2p": (C.c_int, [vp, vp, vp, i32, vp, i32, i32, vp, vp]),
         "phfem_dist_bucket_bits": (C.c_int, [i32, i32]),
+        "phfem_dist_dirichlet": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(phfem_classification),
+                                           P(phfem_field), dbl, i32, vp]),
+        "phfem_dist_level_count": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, i32, C.c_int, P(i32), P(i32),
+                                             P(vp)]),
+        "phfem_dist_level_run": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, i32, i32, P(phfem_topology), vp, vp,
+                                           P(phfem_csr)]),
+        "phfem_dist_classify_ex": (C.c_int, [vp, P(phfem_topology), i32, vp, i32, vp, i32, i32, i32,
+                                             P(phfem_classification)]),
         "phfem_dist_pairs_p2p": (C.c_int, [vp, vp, i64, i32, vp, i32, i32, vp, vp]),
         "phfem_dist_bucket_hist": (C.c_int, [vp, vp, i32, i32, i32, i32, vp]),
         "phfem_dist_bucket_cursors": (C.c_int, [vp, vp, i32, i64, i32, vp, vp, vp, P(i64)]),

@@ -502,15 +502,17 @@ __global__ void k_dirichlet(const double2* __restrict__ coords, const int32_t* _
   }
 }
 
+// r_off: the classification's retained positions start at r_off (a rank of
+// the distributed pipeline with global positions); out holds rows r_off..
 phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                             const phfem_classification* cls, const phfem_field* uD, double t,
-                            double* out, const double* samples) {
+                            double* out, const double* samples, int32_t r_off) {
   if (cls->L > 0)
     PHFEM_CUDA(ctx, cudaMemsetAsync(out, 0, sizeof(double) * cls->L, ctx->stream));
   if (cls->nD == 0) return PHFEM_OK;
   PHFEM_LAUNCH(ctx, "k_dirichlet", k_dirichlet<<<grid_for(cls->nD, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
       (const double2*)mesh->coords, topo->edge_nodes, cls->dirichlet_edge_ids, cls->nD,
-      cls->retained_pos, *uD, t, out, samples));
+      cls->retained_pos, *uD, t, out - r_off, samples));
   return PHFEM_OK;
 }
 
@@ -682,4 +684,11 @@ PHFEM_API phfem_status phfem_assemble_dirichlet(phfem_ctx* ctx, const phfem_mesh
                                                 const phfem_field* uD, double t, double* out) {
   if (!ctx || !mesh || !topo || !cls || !uD) return PHFEM_ERR_INVALID_ARGUMENT;
   return dirichlet_into(ctx, mesh, topo, cls, uD, t, out);
+}
+
+PHFEM_API phfem_status phfem_dist_dirichlet(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* part,
+                                            const phfem_classification* cls, const phfem_field* uD, double t,
+                                            int32_t r_off, double* out) {
+  if (!ctx || !mesh || !part || !cls || !uD || (cls->L > 0 && !out) || r_off < 0) return PHFEM_ERR_INVALID_ARGUMENT;
+  return phfem::dirichlet_into(ctx, mesh, part, cls, uD, t, out, nullptr, r_off);
 }

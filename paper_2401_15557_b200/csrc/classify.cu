@@ -79,10 +79,12 @@ __global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
 
 // CTA of 256 threads per block of 1024 edges; thread t owns 4 consecutive
 // edges, all inside bitmap word t/8.
+// r_off / e_off: the rank's first retained row / first global edge id
+// (distributed final level with the offsets known up front; 0 otherwise)
 __global__ void __launch_bounds__(256) k_cls_retained(const uint32_t* __restrict__ bits,
                                                       const int32_t* __restrict__ pre_neu,
                                                       int E, int32_t* __restrict__ rpos,
-                                                      int32_t* __restrict__ redges) {
+                                                      int32_t* __restrict__ redges, int r_off, int e_off) {
   __shared__ int32_t wpre[32];
   const int blk = blockIdx.x;
   const int nwords = (E + 31) >> 5;
@@ -107,14 +109,17 @@ __global__ void __launch_bounds__(256) k_cls_retained(const uint32_t* __restrict
     r[q] = neu ? -1 : (int)(e0 + q) - before;
     before += neu;
   }
+  int g[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) g[q] = r[q] < 0 ? -1 : r[q] + r_off;
   if (e0 + 3 < E) {
-    *reinterpret_cast<int4*>(rpos + e0) = make_int4(r[0], r[1], r[2], r[3]);
+    *reinterpret_cast<int4*>(rpos + e0) = make_int4(g[0], g[1], g[2], g[3]);
   } else {
-    for (int q = 0; q < 4 && e0 + q < E; ++q) rpos[e0 + q] = r[q];
+    for (int q = 0; q < 4 && e0 + q < E; ++q) rpos[e0 + q] = g[q];
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q)
-    if (r[q] >= 0 && e0 + q < E) redges[r[q]] = (int)(e0 + q);
+    if (r[q] >= 0 && e0 + q < E) redges[r[q]] = (int)(e0 + q) + e_off;
 }
 
 }  // namespace phfem
@@ -137,7 +142,8 @@ namespace phfem {
 // the ascending boundary list; with_retained also retained_pos / _edges
 static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topology* topo,
                                               phfem_classification* out, int nblk,
-                                              bool with_retained, int bnd_base = 0) {
+                                              bool with_retained, int bnd_base = 0, int r_off = 0,
+                                              int e_off = 0) {
   const int E = topo->E;
   int32_t* pre_bnd = out->block_prefix;
   int32_t* pre_neu = out->block_prefix + nblk + 1;
@@ -147,7 +153,7 @@ static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topolo
   PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
   if (nblk > 0 && with_retained) {
     PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
-                                                         out->retained_pos, out->retained_edges));
+                                                         out->retained_pos, out->retained_edges, r_off, e_off));
   }
   return PHFEM_OK;
 }
@@ -210,13 +216,13 @@ namespace phfem {
 // Distributed ranks (dist.cu): the Neumann bitmap and the owned id lists are
 // set; block prefixes, retained_pos / retained_edges and L follow.
 phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo,
-                                      phfem_classification* out, int bnd_base) {
+                                      phfem_classification* out, int bnd_base, int r_off, int e_off) {
   const int E = topo->E;
   const int nblk = (E + kEdgeBlock - 1) / kEdgeBlock;
   PHFEM_TRY(dalloc(ctx, &out->retained_pos, E));
   PHFEM_TRY(dalloc(ctx, &out->retained_edges, E));
   PHFEM_TRY(dalloc(ctx, &out->block_prefix, 2 * ((int64_t)nblk + 1)));
-  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, true, bnd_base));
+  PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, true, bnd_base, r_off, e_off));
   int32_t nneu = 0;
   PHFEM_CUDA(ctx, cudaMemcpyAsync(&nneu, out->block_prefix + nblk + 1 + nblk, sizeof(int32_t),
                                   cudaMemcpyDeviceToHost, ctx->stream));

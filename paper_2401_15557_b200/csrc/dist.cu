@@ -553,15 +553,15 @@ PHFEM_API phfem_status phfem_dist_resolve(phfem_ctx* ctx, const phfem_topology* 
 
 namespace phfem {
 phfem_status classify_lists_from_bits(phfem_ctx* ctx, const phfem_topology* topo, phfem_classification* out,
-                                      int bnd_base);
+                                      int bnd_base, int r_off, int e_off);
 }
 
 // dir_ids / neu_ids: the rank's edges, LOCAL ids; E0 = global id of the
 // part's first edge (its boundary list holds global ids after re-basing).
-PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
-                                           const int32_t* dir_ids, int32_t nD,
-                                           const int32_t* neu_ids, int32_t nN,
-                                           phfem_classification* out) {
+PHFEM_API phfem_status phfem_dist_classify_ex(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                              const int32_t* dir_ids, int32_t nD, const int32_t* neu_ids,
+                                              int32_t nN, int32_t r_off, int32_t e_off,
+                                              phfem_classification* out) {
   memset(out, 0, sizeof(*out));
   if (!ctx || !part) return PHFEM_ERR_INVALID_ARGUMENT;
   const int E = part->E;
@@ -602,7 +602,14 @@ PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology*
   PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   dfree(ctx, dup);
   out->flags = hdup ? PHFEM_CLS_DUP_NEUMANN : 0;
-  return classify_lists_from_bits(ctx, part, out, E0);
+  return classify_lists_from_bits(ctx, part, out, E0, r_off, e_off);
+}
+
+PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
+                                           const int32_t* dir_ids, int32_t nD,
+                                           const int32_t* neu_ids, int32_t nN,
+                                           phfem_classification* out) {
+  return phfem_dist_classify_ex(ctx, part, E0, dir_ids, nD, neu_ids, nN, 0, 0, out);
 }
 
 PHFEM_API phfem_status phfem_dist_neumann_table(phfem_ctx* ctx, const phfem_topology* part,

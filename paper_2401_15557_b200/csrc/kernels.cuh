@@ -84,7 +84,7 @@ phfem_status neumann_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_to
                           double* out, int accumulate, bool check, const double* samples = nullptr);
 phfem_status dirichlet_into(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* topo,
                             const phfem_classification* cls, const phfem_field* uD, double t,
-                            double* out, const double* samples = nullptr);
+                            double* out, const double* samples = nullptr, int32_t r_off = 0);
 phfem_status constraint_csr_into(phfem_ctx* ctx, const phfem_mesh* mesh,
                                  const phfem_topology* topo, const phfem_classification* cls,
                                  phfem_csr* out);

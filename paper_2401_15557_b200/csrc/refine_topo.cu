@@ -81,6 +81,10 @@ struct LvArgs {
   // indices l+1, l+2, the opposite vertex, -} (phfem_dist_side_apply) instead
   // of gathers from elem_edge / elements of every parent element
   const int4* side;
+  // distributed level with the fine offsets known up front: global ids
+  // written directly (fine edge ids in the lists and node_edge_start, C row
+  // pointers) — no re-basing pass; 0 on one GPU
+  int f_off, nnz_off;
   // exclusive per-tile prefixes (k_rl_tile_init / k_rl_tile_count + scans):
   // fine edges, parent boundary edges, parent Neumann edges before the tile
   const int32_t* tileF;
@@ -369,8 +373,8 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
   const int N0 = kFull ? __ldg(a.tileN + tile) : 0;
   __syncthreads();
   if (valid) {
-    o.node_edge_start[mu - a.nlo] = F0 + i0;
-    if (le == a.E - 1) o.node_edge_start[mu - a.nlo + 1] = a.Ef;
+    o.node_edge_start[mu - a.nlo] = a.f_off + F0 + i0;
+    if (le == a.E - 1) o.node_edge_start[mu - a.nlo + 1] = a.f_off + a.Ef;
   }
 
   // 5. coalesced stores of the tile's fine edges [F0, F0 + nf)
@@ -387,8 +391,8 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
     o.ltp[f] = lp;
     o.ltm[f] = lm;
     const int sl = ms >> 8;  // arithmetic shift: boundary slots stay negative
-    if (sl < 0) o.boundary[off_bnd + ~sl] = f;
-    else o.interior[off_int + sl] = f;
+    if (sl < 0) o.boundary[off_bnd + ~sl] = a.f_off + f;
+    else o.interior[off_int + sl] = a.f_off + f;
     if (o.self_ee) {  // distributed, own fine elements written in place
       const int64_t s0 = 3 * (int64_t)el2.x + lp;
       const int64_t s1 = lm >= 0 ? 3 * (int64_t)el2.y + lm : -1;
@@ -417,7 +421,7 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
         const int rs = off_rs + (rr & 0xffff);
         const double len = s.len[i];
         if (o.redges) o.redges[rp] = f;
-        o.row_ptr[rp] = rs;
+        o.row_ptr[rp] = a.nnz_off + rs;
         // columns {0,1,2} \ {local}, ascending: T+ DOFs, then T- DOFs
         const int c0 = lp == 0 ? 1 : 0, c1 = lp == 2 ? 1 : 2;
         const double vp = len * 0.5;  // assembly.cpp:160
@@ -431,7 +435,7 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
           __stcs(reinterpret_cast<double2*>(o.val + rs + 2), make_double2(vm, vm));
           n = 4;
         }
-        if (rp == a.L - 1) o.row_ptr[a.L] = rs + n;
+        if (rp == a.L - 1) o.row_ptr[a.L] = a.nnz_off + rs + n;
       }
     }
   }
@@ -1001,91 +1005,170 @@ __global__ void __launch_bounds__(256) k_dist_children_slots(const int32_t* __re
 }
 }  // namespace phfem
 
-PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
-                                                    const int32_t* side, const double* coords, int32_t nc,
-                                                    int32_t node_lo, int32_t node_hi, int32_t nE_all,
-                                                    const int32_t* neu_parent_ids, int32_t nN_parent,
-                                                    phfem_topology* out, uint8_t* rk, double* coords_fine,
-                                                    phfem_csr* C) {
-  if (!ctx || !ppart || !out) return PHFEM_ERR_INVALID_ARGUMENT;
-  memset(out, 0, sizeof(*out));
-  if (C) memset(C, 0, sizeof(*C));
+namespace phfem {
+static __global__ void k_fill_lv(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+}  // namespace phfem
+
+// Count half of the side-mode level: tile counts from the side records,
+// fine edges Ef and parent Neumann edges of the rank (synchronises); the
+// plan carries the tile prefixes to phfem_dist_level_run.
+struct phfem_dist_level_plan {
+  phfem_topology ppart;
+  int32_t E0p;
+  const int32_t* side;
+  int64_t ntiles;
+  int32_t* tiles;
+  uint32_t* nbits;
+  int32_t Ef, nneu;
+  bool with_C;
+};
+
+PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                              const int32_t* side, const int32_t* neu_parent_ids, int32_t nN_parent,
+                                              int with_C, int32_t* Ef_out, int32_t* nneu_out, void** plan_out) {
+  if (!ctx || !ppart || !Ef_out || !nneu_out || !plan_out || E0p < 0) return PHFEM_ERR_INVALID_ARGUMENT;
+  *plan_out = nullptr;
   if (nN_parent > 0 && !neu_parent_ids) return PHFEM_ERR_INVALID_ARGUMENT;
   const int64_t E = ppart->E;
-  if ((E > 0 && (!side || !coords || !rk || !coords_fine)) || E0p < 0 || node_lo < 0 || node_hi < node_lo ||
-      (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) || (E > 0 && node_lo > nc + E0p) ||
-      4 * (int64_t)nE_all >= (int64_t(1) << 31))
-    return PHFEM_ERR_INVALID_ARGUMENT;
+  if (E > 0 && !side) return PHFEM_ERR_INVALID_ARGUMENT;
   const int64_t ntiles = std::max<int64_t>(1, (E + kLvT - 1) / kLvT);
   const int64_t nwords = std::max<int64_t>(1, (E + 31) / 32);
-  int32_t* tiles = nullptr;
-  PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1) + 2));
-  int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
-  int32_t* total = tiles + 3 * (ntiles + 1);  // [0] fine edges, [1] parent Neumann edges
-  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 2), ctx->stream));
-  uint32_t* nbits = nullptr;
-  if (C) {
-    PHFEM_TRY(dalloc(ctx, &nbits, nwords));
-    PHFEM_CUDA(ctx, cudaMemsetAsync(nbits, 0, sizeof(uint32_t) * nwords, ctx->stream));
-    if (nN_parent > 0 && E > 0)
-      PHFEM_LAUNCH(ctx, "k_rl_neu_bits", k_rl_neu_bits<<<grid_for(nN_parent, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-          neu_parent_ids, nN_parent, E0p, (int)E, nbits));
+  phfem_dist_level_plan* pl = new phfem_dist_level_plan();
+  pl->ppart = *ppart;
+  pl->E0p = E0p;
+  pl->side = side;
+  pl->ntiles = ntiles;
+  pl->with_C = with_C != 0;
+  auto fail = [&](phfem_status st) {
+    dfree(ctx, pl->tiles);
+    dfree(ctx, pl->nbits);
+    delete pl;
+    return st;
+  };
+  phfem_status st = dalloc(ctx, &pl->tiles, 3 * (ntiles + 1) + 2);
+  if (st != PHFEM_OK) return fail(st);
+  int32_t *tileF = pl->tiles, *tileB = pl->tiles + (ntiles + 1), *tileN = pl->tiles + 2 * (ntiles + 1);
+  int32_t* total = pl->tiles + 3 * (ntiles + 1);
+  if (cudaMemsetAsync(pl->tiles, 0, sizeof(int32_t) * (3 * (ntiles + 1) + 2), ctx->stream) != cudaSuccess)
+    return fail(cuda_fail(ctx, cudaGetLastError(), "level count memset"));
+  if (pl->with_C) {
+    if ((st = dalloc(ctx, &pl->nbits, nwords)) != PHFEM_OK) return fail(st);
+    cudaMemsetAsync(pl->nbits, 0, sizeof(uint32_t) * nwords, ctx->stream);
+    if (nN_parent > 0 && E > 0) {
+      KTimer kt(ctx, "k_rl_neu_bits");
+      k_rl_neu_bits<<<grid_for(nN_parent, 256, ctx->num_sms), 256, 0, ctx->stream>>>(neu_parent_ids, nN_parent, E0p,
+                                                                                      (int)E, pl->nbits);
+      ctx->launches++;
+    }
   }
   if (E > 0) {
-    PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, nbits, tileF, tileB, tileN));
-    PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count_side<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        reinterpret_cast<const int4*>(side), ppart->edge_elements, (int)E, E0p, tileF));
+    {
+      KTimer kt(ctx, "k_rl_tile_init");
+      k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, pl->nbits, tileF, tileB, tileN);
+      ctx->launches++;
+    }
+    KTimer kt(ctx, "k_rl_tile_count");
+    k_rl_tile_count_side<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const int4*>(side), ppart->edge_elements, (int)E, E0p, tileF);
+    ctx->launches++;
   }
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total));
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
-  if (C) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, total + 1));
+  if (cudaGetLastError() != cudaSuccess) return fail(set_error(ctx, PHFEM_ERR_CUDA, "level count launch failed"));
+  if ((st = scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total)) != PHFEM_OK) return fail(st);
+  if ((st = scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr)) != PHFEM_OK) return fail(st);
+  if (pl->with_C && (st = scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, total + 1)) != PHFEM_OK) return fail(st);
   int32_t hcnt[2] = {0, 0};
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(hcnt, total, sizeof hcnt, cudaMemcpyDeviceToHost, ctx->stream));
-  PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  const int32_t Ef = hcnt[0];
+  if (cudaMemcpyAsync(hcnt, total, sizeof hcnt, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return fail(cuda_fail(ctx, cudaGetLastError(), "level count"));
+  pl->Ef = hcnt[0];
+  pl->nneu = pl->with_C ? hcnt[1] : 0;
+  *Ef_out = pl->Ef;
+  *nneu_out = pl->nneu;
+  *plan_out = pl;
+  return PHFEM_OK;
+}
+
+// Run half: the level kernel with the rank's fine offsets (f_off: first
+// global fine edge id; nnz_off: first C entry) written straight into the
+// fine lists, node_edge_start and C's row pointers; frees the plan.
+PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc,
+                                            int32_t node_lo, int32_t node_hi, int32_t nE_all, int32_t f_off,
+                                            int32_t nnz_off, phfem_topology* out, uint8_t* rk, double* coords_fine,
+                                            phfem_csr* C) {
+  phfem_dist_level_plan* pl = (phfem_dist_level_plan*)plan;
+  if (!ctx || !pl || !out) return PHFEM_ERR_INVALID_ARGUMENT;
+  memset(out, 0, sizeof(*out));
+  if (C) memset(C, 0, sizeof(*C));
+  const phfem_topology* ppart = &pl->ppart;
+  const int64_t E = ppart->E;
+  const int32_t E0p = pl->E0p;
+  phfem_status st = PHFEM_OK;
+  if ((E > 0 && (!coords || !rk || !coords_fine)) || node_lo < 0 || node_hi < node_lo ||
+      (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) || (E > 0 && node_lo > nc + E0p) ||
+      4 * (int64_t)nE_all >= (int64_t(1) << 31) || (C != nullptr) != pl->with_C)
+    st = PHFEM_ERR_INVALID_ARGUMENT;
+  const int64_t ntiles = pl->ntiles;
+  int32_t *tileF = pl->tiles, *tileB = pl->tiles + (ntiles + 1), *tileN = pl->tiles + 2 * (ntiles + 1);
+  const int32_t Ef = pl->Ef;
   const int64_t nBf = 2 * (int64_t)ppart->n_boundary;
-  out->nC = node_hi - node_lo;
-  out->nE = 4 * nE_all;
-  out->E = Ef;
-  out->n_boundary = (int32_t)nBf;
-  out->n_interior = (int32_t)(Ef - nBf);
-  const int64_t cap = std::max<int64_t>(Ef, 1);
-  PHFEM_TRY(dalloc(ctx, &out->edge_nodes, 2 * cap));
-  PHFEM_TRY(dalloc(ctx, &out->edge_elements, 2 * cap));
-  PHFEM_TRY(dalloc(ctx, &out->local_in_tplus, cap));
-  PHFEM_TRY(dalloc(ctx, &out->local_in_tminus, cap));
-  PHFEM_TRY(dalloc(ctx, &out->interior_edges, std::max<int64_t>(Ef - nBf, 1)));
-  PHFEM_TRY(dalloc(ctx, &out->boundary_edges, std::max<int64_t>(nBf, 1)));
-  PHFEM_TRY(dalloc(ctx, &out->node_edge_start, (int64_t)out->nC + 1));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(out->node_edge_start, 0, sizeof(int32_t) * ((int64_t)out->nC + 1), ctx->stream));
   int64_t Lr = 0;
-  if (C) {
-    const int64_t nneu = hcnt[1];
-    Lr = Ef - 2 * nneu;
-    const int64_t BR = 2 * ((int64_t)ppart->n_boundary - nneu);
-    C->rows = (int32_t)Lr;
-    C->cols = 3 * 4 * nE_all;
-    C->nnz = 4 * Lr - 2 * BR;
-    PHFEM_TRY(dalloc(ctx, &C->row_ptr, Lr + 1));
-    PHFEM_TRY(dalloc(ctx, &C->col_idx, std::max<int64_t>(C->nnz, 1)));
-    PHFEM_TRY(dalloc(ctx, &C->values, std::max<int64_t>(C->nnz, 1)));
-    if (Lr == 0) PHFEM_CUDA(ctx, cudaMemsetAsync(C->row_ptr, 0, sizeof(int32_t), ctx->stream));
+  if (st == PHFEM_OK) {
+    out->nC = node_hi - node_lo;
+    out->nE = 4 * nE_all;
+    out->E = Ef;
+    out->n_boundary = (int32_t)nBf;
+    out->n_interior = (int32_t)(Ef - nBf);
+    const int64_t cap = std::max<int64_t>(Ef, 1);
+    auto al = [&](int32_t** p, int64_t n) { if (st == PHFEM_OK) st = dalloc(ctx, p, n); };
+    al(&out->edge_nodes, 2 * cap);
+    al(&out->edge_elements, 2 * cap);
+    al(&out->local_in_tplus, cap);
+    al(&out->local_in_tminus, cap);
+    al(&out->interior_edges, std::max<int64_t>(Ef - nBf, 1));
+    al(&out->boundary_edges, std::max<int64_t>(nBf, 1));
+    al(&out->node_edge_start, (int64_t)out->nC + 1);
+    if (st == PHFEM_OK) {  // nodes that start no fine edge (rank 0's old nodes; an empty range): f_off
+      KTimer kt(ctx, "k_fill_lv");
+      k_fill_lv<<<grid_for((int64_t)out->nC + 1, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+          out->node_edge_start, (int64_t)out->nC + 1, f_off);
+      ctx->launches++;
+    }
+    if (st == PHFEM_OK && C) {
+      Lr = Ef - 2 * (int64_t)pl->nneu;
+      const int64_t BR = 2 * ((int64_t)ppart->n_boundary - pl->nneu);
+      C->rows = (int32_t)Lr;
+      C->cols = 3 * 4 * nE_all;
+      C->nnz = 4 * Lr - 2 * BR;
+      al(&C->row_ptr, Lr + 1);
+      al(&C->col_idx, std::max<int64_t>(C->nnz, 1));
+      if (st == PHFEM_OK) st = dalloc(ctx, &C->values, std::max<int64_t>(C->nnz, 1));
+      if (st == PHFEM_OK && Lr == 0) {  // no rows: the one row pointer is the rank's first entry
+        KTimer kt(ctx, "k_fill_lv");
+        k_fill_lv<<<1, 32, 0, ctx->stream>>>(C->row_ptr, 1, nnz_off);
+        ctx->launches++;
+      }
+    }
   }
-  if (E > 0) {
+  if (st == PHFEM_OK && E > 0) {
     LvArgs a;
     memset(&a, 0, sizeof a);
     a.edge_nodes = ppart->edge_nodes;
     a.edge_elements = ppart->edge_elements;
     a.ltp = ppart->local_in_tplus;
     a.ltm = ppart->local_in_tminus;
-    a.side = reinterpret_cast<const int4*>(side);
+    a.side = reinterpret_cast<const int4*>(pl->side);
     a.coords = (const double2*)coords;
     a.E = (int)E;
     a.nc = nc;
     a.Ef = Ef;
     a.eb = E0p;
     a.nlo = node_lo;
+    a.f_off = f_off;
+    a.nnz_off = nnz_off;
     a.tileF = tileF;
     a.tileB = tileB;
     LvOut o;
@@ -1102,20 +1185,34 @@ PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_
     o.mid_base = 0;
     const unsigned nt = (unsigned)((E + kLvT - 1) / kLvT);
     if (C) {
-      a.neu_bits = nbits;
+      a.neu_bits = pl->nbits;
       a.tileN = tileN;
       a.L = (int)Lr;
       o.row_ptr = C->row_ptr;
       o.col = C->col_idx;
       o.val = C->values;
-      PHFEM_TRY(launch_level<true>(ctx, a, o, nt));
+      st = launch_level<true>(ctx, a, o, nt);
     } else {
-      PHFEM_TRY(launch_level<false>(ctx, a, o, nt));
+      st = launch_level<false>(ctx, a, o, nt);
     }
   }
-  dfree(ctx, nbits);
-  dfree(ctx, tiles);
-  return PHFEM_OK;
+  dfree(ctx, pl->nbits);
+  dfree(ctx, pl->tiles);
+  delete pl;
+  return st;
+}
+
+PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                                    const int32_t* side, const double* coords, int32_t nc,
+                                                    int32_t node_lo, int32_t node_hi, int32_t nE_all,
+                                                    const int32_t* neu_parent_ids, int32_t nN_parent,
+                                                    phfem_topology* out, uint8_t* rk, double* coords_fine,
+                                                    phfem_csr* C) {
+  if (!ctx || !ppart || !out) return PHFEM_ERR_INVALID_ARGUMENT;
+  int32_t Ef = 0, nneu = 0;
+  void* plan = nullptr;
+  PHFEM_TRY(phfem_dist_level_count(ctx, ppart, E0p, side, neu_parent_ids, nN_parent, C != nullptr, &Ef, &nneu, &plan));
+  return phfem_dist_level_run(ctx, plan, coords, nc, node_lo, node_hi, nE_all, 0, 0, out, rk, coords_fine, C);
 }
 
 PHFEM_API phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements,

@@ -352,6 +352,33 @@ class CudaRankOps:
         self.ppart, self.part, self._rk = self.part, capi.Topology(self.ctx, t), rk
         return int(t.E), int(t.n_boundary)
 
+    def level_count(self, E0p, neu_parent=None):
+        """count half of the level: (fine edges, parent Neumann edges) of the rank"""
+        Ef, nneu, plan = C.c_int32(0), C.c_int32(0), C.c_void_p()
+        nN = 0 if neu_parent is None else int(neu_parent.numel())
+        self._ck(self.lib.phfem_dist_level_count(self.ctx.ptr, C.byref(self.part.t), E0p, self.p(self._side),
+                                                 self.p(neu_parent) if nN else None, nN,
+                                                 1 if neu_parent is not None else 0, C.byref(Ef), C.byref(nneu),
+                                                 C.byref(plan)))
+        self._plan, self._plan_C = plan, neu_parent is not None
+        return int(Ef.value), int(nneu.value)
+
+    def level_run(self, coords, nc, nlo, nhi, nE_all, coords_fine, f_off, nnz_off):
+        """run half: the fine part with GLOBAL ids (f_off, nnz_off) — no re-basing"""
+        E = int(self.part.t.E)
+        rk = torch.empty((max(E, 1),), dtype=torch.uint8, device=self.dev)
+        t = capi.phfem_topology()
+        csr = capi.phfem_csr() if self._plan_C else None
+        plan, self._plan = self._plan, None
+        self._ck(self.lib.phfem_dist_level_run(self.ctx.ptr, plan, self.p(coords), nc, nlo, nhi, nE_all, f_off,
+                                               nnz_off, C.byref(t), self.p(rk), self.p(coords_fine),
+                                               C.byref(csr) if csr is not None else None))
+        if csr is not None:
+            self.csr = csr
+        self._side = None
+        self.ppart, self.part, self._rk = self.part, capi.Topology(self.ctx, t), rk
+        return int(t.E), int(t.n_boundary)
+
     def start_records(self, nes_off, psplits):
         """edge owner: {slot, group start (global), rank byte} per (owned parent
         edge, element), routed to the element owners; drops the parent part"""
@@ -515,12 +542,14 @@ class CudaRankOps:
         return out[:4 * n]
 
     # -- classification, C, boundary vectors, blocks ------------------------------------------
-    def classify(self, dir_ids_local, neu_ids_local, E0):
+    def classify(self, dir_ids_local, neu_ids_local, E0, R0=None):
+        """R0 given (offsets known before): retained positions / edges global at once"""
         c = capi.phfem_classification()
-        self._ck(self.lib.phfem_dist_classify(self.ctx.ptr, C.byref(self.part.t), E0, self.p(dir_ids_local),
-                                              dir_ids_local.numel(), self.p(neu_ids_local), neu_ids_local.numel(),
-                                              C.byref(c)))
+        self._ck(self.lib.phfem_dist_classify_ex(self.ctx.ptr, C.byref(self.part.t), E0, self.p(dir_ids_local),
+                                                 dir_ids_local.numel(), self.p(neu_ids_local), neu_ids_local.numel(),
+                                                 0 if R0 is None else R0, 0 if R0 is None else E0, C.byref(c)))
         self.cls = capi.Classification(self.ctx, c)
+        self._r_off = R0 or 0
         return int(c.L)
 
     def constraint(self, mview):
@@ -537,8 +566,10 @@ class CudaRankOps:
 
     def dirichlet(self, mview, uD, t):
         bd = self.empty((max(self.cls.c.L, 1),), torch.float64)
-        self._ck(self.lib.phfem_assemble_dirichlet(self.ctx.ptr, C.byref(mview), C.byref(self.part.t),
-                                                   C.byref(self.cls.c), C.byref(uD), t, self.p(bd)))
+        # retained positions global when the classification got R0
+        self._ck(self.lib.phfem_dist_dirichlet(self.ctx.ptr, C.byref(mview), C.byref(self.part.t),
+                                               C.byref(self.cls.c), C.byref(uD), t, getattr(self, "_r_off", 0),
+                                               self.p(bd)))
         return bd[:self.cls.c.L]
 
     def volume(self, mview, coeffs, f, t):
@@ -570,14 +601,16 @@ class CudaRankOps:
     def num_edges(self) -> int:
         return int(self.part.t.E)
 
-    def rebase_results(self, E0, R0, nnz0):
-        """rank-local retained positions / retained edges / CSR row pointers -> global"""
+    def rebase_results(self, E0, R0, nnz0, retained=True, row_ptr=True):
+        """rank-local retained positions / retained edges / CSR row pointers -> global
+        (skipped for what the level / classification already wrote globally)"""
         c, m = self.cls.c, self.csr
-        if c.E:
+        if retained and c.E:
             self.rebase(c.retained_pos, c.E, R0, 1)
-        if c.L:
+        if retained and c.L:
             self.rebase(c.retained_edges, c.L, E0)
-        self.rebase(m.row_ptr, m.rows + 1, nnz0)
+        if row_ptr:
+            self.rebase(m.row_ptr, m.rows + 1, nnz0)
 
     # -- results -----------------------------------------------------------------------------------
     def part_arrays(self) -> dict:
@@ -801,24 +834,48 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     tr("side")
     # fine node ranges from every rank's parent edge offset
     fsplits = np.asarray([0] + [nC + e for e in E0s[1:]] + [nC + Etot], dtype=np.int64)
-    counts = []
-    for s, (E0, _), i in zip(states, per, ids):
-        r = s.rank
-        neu = i[nD:].to(torch.int32).contiguous() if fused_c else None
+    for s in states:
         cf = torch.empty((nC + Etot, 2), dtype=torch.float64, device=s.coords.device)
         cf[:nC] = s.coords[:nC]
         s.coords_fine = cf
-        Ef, Bf = s.ops.refine_level_side(s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE, cf, neu)
-        counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
-    tr("level")
-    gath = comm.all_gather(counts)
+    neus = [i[nD:].to(torch.int32).contiguous() if fused_c else None for i in ids]
     fper = []
-    for s, gc in zip(states, gath):
-        allc = torch.stack(gc).cpu().numpy()
-        E0f, B0f = int(allc[:s.rank, 0].sum()), int(allc[:s.rank, 1].sum())
-        fper.append((E0f, B0f))
-        s.ops.rebase_part(E0f)
-    Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
+    if hasattr(states[0].ops, "level_count"):
+        # count half first: every rank's fine offsets (edges, C rows / entries)
+        # are all-gathered before the level kernel writes, so it writes global
+        # ids — no re-basing pass over the fine part or C's row pointers
+        counts = []
+        for s, (E0, _), neu in zip(states, per, neus):
+            Ef_r, nneu_r = s.ops.level_count(E0, neu)
+            Bf_r = 2 * int(s.ops.part.t.n_boundary)
+            counts.append(torch.tensor([Ef_r, Bf_r, nneu_r], dtype=torch.int64, device=s.coords.device))
+        gath = comm.all_gather(counts)
+        for s, gc in zip(states, gath):
+            allc = torch.stack(gc).cpu().numpy()
+            r = s.rank
+            E0f, B0f = int(allc[:r, 0].sum()), int(allc[:r, 1].sum())
+            N0f = 2 * int(allc[:r, 2].sum())            # fine Neumann edges before the rank
+            R0 = E0f - N0f                              # retained rows before it
+            nnz0 = 4 * R0 - 2 * (B0f - N0f) if fused_c else 0
+            fper.append((E0f, B0f))
+            s.ops.level_run(s.coords, nC, int(fsplits[r]), int(fsplits[r + 1]), nE, s.coords_fine, E0f, nnz0)
+            s.fine_offsets = (E0f, R0) if fused_c else None
+        Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
+    else:
+        counts = []
+        for s, (E0, _), neu in zip(states, per, neus):
+            r = s.rank
+            Ef, Bf = s.ops.refine_level_side(s.coords, nC, E0, int(fsplits[r]), int(fsplits[r + 1]), nE,
+                                             s.coords_fine, neu)
+            counts.append(torch.tensor([Ef, Bf], dtype=torch.int64, device=s.coords.device))
+        gath = comm.all_gather(counts)
+        for s, gc in zip(states, gath):
+            allc = torch.stack(gc).cpu().numpy()
+            E0f, B0f = int(allc[:s.rank, 0].sum()), int(allc[:s.rank, 1].sum())
+            fper.append((E0f, B0f))
+            s.ops.rebase_part(E0f)
+        Ef_tot, Bf_tot = int(allc[:, 0].sum()), int(allc[:, 1].sum())
+    tr("level")
     if p2p:
         bufs = [s.ops.start_alloc(s.ehi - s.elo) for s in states]
         wg, wr = comm.window([b[0] for b in bufs], "gs"), comm.window([b[1] for b in bufs], "grk")
@@ -902,7 +959,9 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         own_n = (nl >= 0) & (nl < E_r) & (i[nD:] >= 0)
         s.neu_pos = torch.nonzero(own_n).flatten()
         s.neu_local = nl[own_n].to(torch.int32).contiguous()
-        Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local, E0)], dtype=torch.int64,
+        fo = getattr(s, "fine_offsets", None)
+        Ls.append(torch.tensor([s.ops.classify(s.dir_local, s.neu_local, E0, fo[1]) if fo else
+                                s.ops.classify(s.dir_local, s.neu_local, E0)], dtype=torch.int64,
                                device=s.coords.device))
     tr("classify")
     gl = comm.all_gather(Ls)
@@ -917,7 +976,10 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
         s.ops.constraint(mview)
         s.bd = s.ops.dirichlet(mview, uD, t)
-        s.ops.rebase_results(E0, R0, nnz0)
+        fo = getattr(s, "fine_offsets", None)
+        if fo is not None:
+            assert fo == (E0, R0), (fo, E0, R0)  # the level's offsets == the classification's
+        s.ops.rebase_results(E0, R0, nnz0, retained=fo is None, row_ptr=fo is None)
         s.E0, s.R0 = E0, R0
         s.blocks = s.ops.volume(mview, coeffs, f, t)
         s.mview = mview

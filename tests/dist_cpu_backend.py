@@ -473,7 +473,8 @@ class NumpyRankOps:
             for cc in range(3):
                 L[tp - elo, cc] = L[tp - elo, cc] + acc[cc]
 
-    def rebase_results(self, E0, R0, nnz0):
+    def rebase_results(self, E0, R0, nnz0, retained=True, row_ptr=True):
+        assert retained and row_ptr  # this backend has no count / run level: offsets are always applied here
         rp = self.cls["retained_pos"]
         self.cls["retained_pos"] = np.where(rp >= 0, rp + R0, -1).astype(np.int32)
         self.cls["retained_edges"] = self.cls["retained_edges"] + E0
