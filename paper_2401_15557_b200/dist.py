@@ -77,6 +77,11 @@ class TorchComm:
         self.world = dist.get_world_size()
         self.ranks = [dist.get_rank()]
         self._win = {}
+        # the last level's volume pass on a side stream (tested bit-exact;
+        # measured at N = 1: 20.96 -> 20.84 ms, 21.18 with a high-priority
+        # main stream — the small kernels and NCCL's of the synchronising
+        # phases queue behind its CTAs), so off unless asked for
+        self.overlap_volume = False
 
     def all_reduce(self, ts: list, op: str):
         o = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}[op]
@@ -583,6 +588,37 @@ class CudaRankOps:
         out["load"] = load[:n]
         return out
 
+    def volume_start(self, mview, coeffs, f, t):
+        """the blocks + load of the own elements on a side stream, so they
+        overlap the host-synchronised classification / resolve / Neumann phases
+        of the last level (they need only the own elements and coordinates)"""
+        main = torch.cuda.current_stream(self.dev)
+        if getattr(self, "_side_stream", None) is None:
+            self._side_stream = torch.cuda.Stream(device=self.dev)
+            self._side_ctx = capi.Context(self.ctx.device, stream=self._side_stream.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self._side_stream.wait_event(ev)
+        n = mview.nE
+        out = {k: self.empty((max(n, 1), 9), torch.float64) for k in ("B", "D", "M", "M0")}
+        load = self.empty((max(n, 1), 3), torch.float64)
+        for x in list(out.values()) + [load]:
+            x.record_stream(self._side_stream)
+        self._side_keep = (mview, self.p(out["B"]))
+        self._side_ctx.check(self.lib.phfem_assemble_volume_load(
+            self._side_ctx.ptr, C.byref(mview), C.byref(coeffs), C.byref(f), t, self.p(out["B"]), self.p(out["D"]),
+            self.p(out["M"]), self.p(out["M0"]), self.p(load)))
+        self._vol_done = torch.cuda.Event()
+        self._vol_done.record(self._side_stream)
+        out = {k: v[:n] for k, v in out.items()}
+        out["load"] = load[:n]
+        return out
+
+    def volume_join(self):
+        if getattr(self, "_vol_done", None) is not None:
+            torch.cuda.current_stream(self.dev).wait_event(self._vol_done)
+            self._vol_done = None
+
     def neumann_table(self, neu_ids_local, nN_all, positions):
         """rows {a, b, t_plus, led} of the owned Neumann edges at their global
         list positions (others zero)."""
@@ -947,7 +983,14 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
         else:
             splits, per, (Etot, Btot) = _edge_generation(states, comm, nC, nE, esplits)
         tr("refine")
-    # final level
+    # final level: the blocks + load first, overlapped with what follows when
+    # the backend and communicator allow (side stream; the rest synchronises
+    # the host several times)
+    overlap = getattr(comm, "overlap_volume", False) and hasattr(states[0].ops, "volume_start")
+    for s in states:
+        s.mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
+        if overlap:
+            s.blocks = s.ops.volume_start(s.mview, coeffs, f, t)
     nD, nN = int(states[0].dirichlet.shape[0]), int(states[0].neumann.shape[0])
     ids = _resolve(states, comm, splits, per, nD, nN)
     Ls = []
@@ -973,7 +1016,7 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
                    "nnz": 4 * int(L_all.sum()) - 2 * (Btot - (Etot - int(L_all.sum())))}
         N0 = E0 - R0                      # Neumann edges before the rank
         nnz0 = 4 * R0 - 2 * (B0 - N0)     # retained boundary rows hold 2 entries
-        mview = s.ops.mesh_view(s.coords, nC, s.elements, s.ehi - s.elo, nE)
+        mview = s.mview
         s.ops.constraint(mview)
         s.bd = s.ops.dirichlet(mview, uD, t)
         fo = getattr(s, "fine_offsets", None)
@@ -981,8 +1024,8 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
             assert fo == (E0, R0), (fo, E0, R0)  # the level's offsets == the classification's
         s.ops.rebase_results(E0, R0, nnz0, retained=fo is None, row_ptr=fo is None)
         s.E0, s.R0 = E0, R0
-        s.blocks = s.ops.volume(mview, coeffs, f, t)
-        s.mview = mview
+        if not overlap:
+            s.blocks = s.ops.volume(mview, coeffs, f, t)
     tr("C+bd+volume")
     # Neumann: owners publish {a, b, t_plus, led}; element owners add b + LN
     all_neu = ids[0][nD:]
@@ -991,6 +1034,8 @@ def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels
     if nN:
         comm.all_reduce(tables, "sum")
     for s, tb in zip(states, tables):
+        if overlap:
+            s.ops.volume_join()
         s.ops.neumann_apply(s.mview, tb, dup, s.elo, s.ehi, g, t, s.blocks["load"])
     tr("neumann")
     tr.dump()

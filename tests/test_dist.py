@@ -248,3 +248,23 @@ def test_peer_windows_two_processes_one_gpu(ctx, tmp_path, case, levels):
     dm = capi.DeviceMesh.upload(ctx, hm)
     ref = capi.pipeline(ctx, dm, levels, *G.config_fields(2), flags=capi.PIPE_GENERIC_EG).download()
     check_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [1, 3])
+def test_volume_on_side_stream_equal_single_gpu(ctx, W):
+    """The last level's blocks + load on a side stream (overlapping the
+    host-synchronised classification / resolve / Neumann phases, the NCCL
+    default) give the same bits; Neumann data joins the side stream first."""
+    import torch
+    from paper_2401_15557_b200 import capi, dist
+    hm = O.refine_levels(G.square_2tri(), 6)
+    args = G.config_fields(1)   # g != 0: the Neumann update must wait for the side-stream load
+    ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), 1, *args, flags=capi.PIPE_GENERIC_EG).download()
+    tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    comm = dist.LocalComm(W)
+    comm.overlap_volume = True
+    states = dist.make_states(hm, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, 1, *args)
+    torch.cuda.synchronize()
+    check_equal(dist.collect(states), ref)
