@@ -441,6 +441,7 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   // scatter the items the histogram pass kept in registers
 #pragma unroll
   for (int k = 0; k < kTilePer; ++k) {
+    if (k * T >= n) break;  // block-uniform: no predicated-off trips for the empty slots
     if (tid + k * T < n) {
       const int pos = atomicAdd(&sm.cur[ndr[k]], 1);
       sm.buf1[pos] = itr[k];
@@ -591,11 +592,13 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
   if (fast) {
 #pragma unroll
     for (int k = 0; k < kTilePer; ++k) {
+      if (k * kTileThreads >= n) break;  // block-uniform (~6 of the 10 slots hold items on refined meshes)
       const int p = tid + k * kTileThreads;
       itr[k] = p < n ? __ldg(items + s + p) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < kTilePer; ++k) {
+      if (k * kTileThreads >= n) break;
       const int p = tid + k * kTileThreads;
       ndr[k] = 0;
       if (p < n) {
