@@ -119,7 +119,18 @@ class TorchComm:
         return [views]
 
     def fence(self):
-        """every rank's peer stores complete and visible before anyone reads"""
+        """every rank's peer stores complete and visible before anyone reads.
+        NCCL: a one-element all-reduce on the stream — it completes on a rank
+        only after every rank's preceding kernels (the peer stores) finished,
+        and orders the reader's next kernels after it, with no host sync.
+        Other backends: device synchronise + barrier.  One rank: nothing."""
+        if self.world == 1:
+            return
+        if self.dist.get_backend() == "nccl":
+            if getattr(self, "_fence_t", None) is None:
+                self._fence_t = torch.zeros(1, dtype=torch.int32, device=torch.cuda.current_device())
+            self.dist.all_reduce(self._fence_t)
+            return
         torch.cuda.synchronize()
         self.dist.barrier()
 
@@ -950,7 +961,7 @@ def _all_E0(states, comm, per) -> list:
     """E0 of every rank (each rank knows only its own from `per`)."""
     ts = [torch.tensor([E0], dtype=torch.int64, device=s.coords.device) for s, (E0, _) in zip(states, per)]
     g = comm.all_gather(ts)[0]
-    return [int(x.item()) for x in g]
+    return [int(x) for x in torch.cat(g).cpu().tolist()]
 
 
 def distributed_pipeline(states: List[RankState], comm, nC: int, nE: int, levels: int, coeffs, f, g, uD,
