@@ -765,6 +765,10 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
   if (st == PHFEM_OK && p->neu.cap > 0) {
     st = dalloc(ctx, &p->neu_vals0, 3 * (int64_t)p->neu.cap);
     if (st == PHFEM_OK) st = dalloc(ctx, &p->neu_vals1, 3 * (int64_t)p->neu.cap);
+    if (st == PHFEM_OK) {
+      cudaMemsetAsync(p->neu_vals0, 0, sizeof(double) * 3 * p->neu.cap, ctx->stream);
+      cudaMemsetAsync(p->neu_vals1, 0, sizeof(double) * 3 * p->neu.cap, ctx->stream);
+    }
   }
   const int nwords = (topo->E + 31) / 32;
   if (st == PHFEM_OK) st = dalloc(ctx, &p->dir_bits, std::max(nwords, 1));
@@ -823,6 +827,10 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
             a, topo->edge_nodes, topo->local_in_tplus, topo->E, p->rowt, p->rowh);
         ctx->launches++;
       }
+      // (measured: the Dirichlet rows folded into k_cn_rows — a per-plan
+      // midpoint table and the u_D evaluation inlined there — made it
+      // 0.099 -> 0.138 ms: registers for every row; the 2-row k_cn_edges
+      // launch stays)
       if (cudaGetLastError() != cudaSuccess) st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan setup failed");
       if (st == PHFEM_OK) st = smem_optin(ctx, (const void*)k_cn_tma, kCnTmaSmem, "k_cn_tma smem opt-in");
       if (st == PHFEM_OK)
@@ -859,7 +867,8 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
   if (!ctx || !p || n < 0) return PHFEM_ERR_INVALID_ARGUMENT;
   const double t0 = n * p->k;        // load_at_time: t = n * k (parabolic.cpp:61)
   const double t1 = (n + 1) * p->k;
-  if (p->neu.nN > 0) {
+  // g = 0: LN = (len * 0) kR = +0 every step — the zero-initialised values stand
+  if (p->neu.nN > 0 && p->g.kind != PHFEM_FLUX_ZERO) {
     PHFEM_TRY(neu_table_eval(ctx, &p->neu, &p->mesh, &p->topo, &p->cls, &p->g, t0, p->neu_vals0));
     PHFEM_TRY(neu_table_eval(ctx, &p->neu, &p->mesh, &p->topo, &p->cls, &p->g, t1, p->neu_vals1));
   }
