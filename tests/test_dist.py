@@ -268,3 +268,34 @@ def test_volume_on_side_stream_equal_single_gpu(ctx, W):
     states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, 1, *args)
     torch.cuda.synchronize()
     check_equal(dist.collect(states), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [3, 8])
+def test_emulated_ranks_at_scale(ctx, W):
+    """The sharded L10 -> L11 step (8.4 M triangles; the peer-window input
+    level, halo-form refinement with global ids written directly) over W
+    emulated ranks == the single-GPU pipeline, every output bit for bit."""
+    import torch
+    from paper_2401_15557_b200 import capi, dist
+    base = capi.DeviceMesh.upload(ctx, G.square_2tri())
+    for _ in range(10):
+        t = capi.build_topology(ctx, base)
+        nxt = capi.red_refine(ctx, base, t)
+        t.release()
+        base.release()
+        base = nxt
+    hm = base.download()
+    base.release()
+    args = G.config_fields(5)
+    res = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), 1, *args)
+    ref = res.download()
+    res.release()
+    tctx = capi.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    comm = dist.LocalComm(W)
+    states = dist.make_states(hm, comm, lambda r: dist.CudaRankOps(tctx, "cuda:0"))
+    states, nC, nE = dist.distributed_pipeline(states, comm, hm.nC, hm.nE, 1, *args)
+    got = dist.collect(states)
+    for s in states:
+        s.ops.release()
+    check_equal(got, ref)
