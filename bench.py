@@ -286,10 +286,13 @@ def build_input(ctx, level):
 
 def run_ours_sharded(args, rank, world, local):
     """N > 1: the same step (L12 resident -> L13 outputs) sharded over the
-    ranks (paper_2401_15557_b200/dist.py): element ranges,
-    key-range all-to-all edge dedup over NCCL, replicated midpoints.  Every
-    rank keeps its slices; value = total L13 triangles / max-over-ranks time.
-    The refined level is built sort-free from the parent's topology."""
+    ranks: element ranges x tile-aligned key ranges, the bulk
+    exchanges as peer-window kernels storing into the owners' arrays (CUDA IPC
+    over NVLink), NCCL for the small collectives and the fences; the refined
+    level sort-free in halo form.  --orch cpp (default): the host orchestration
+    in C++ (csrc/dist_run.cu, phfem_dist_pipeline, its own NCCL communicator);
+    --orch python: dist.py's.  Every rank keeps its slices; value = total L13
+    triangles / max-over-ranks time."""
     import torch
     from paper_2401_15557_b200 import capi, dist, meshgen as G
     torch.cuda.set_device(local)
@@ -297,21 +300,42 @@ def run_ours_sharded(args, rank, world, local):
     ctx = capi.Context(local, stream=torch.cuda.current_stream(dev).cuda_stream)
     fields = G.config_fields(5)
     hm = build_input(ctx, args.level - 1).download()   # L12 input (untimed), replicated
-    comm = dist.TorchComm()
     es = dist.element_splits(hm.nE, world)
     inp = dict(coords=torch.as_tensor(hm.coords).to(dev), elements=torch.as_tensor(hm.elements[es[rank]:es[rank + 1]]).to(dev),
                dirichlet=torch.as_tensor(hm.dirichlet).to(dev), neumann=torch.as_tensor(hm.neumann).to(dev))
-    ops = dist.CudaRankOps(ctx, dev)
+    hist_sample = dist.HIST_SAMPLE if hm.nE >= dist.HIST_SAMPLE_MIN_ELEMENTS else 1
+    if args.orch == "cpp":
+        import torch.distributed as tdist
+        uid = [capi.DistComm.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            tdist.broadcast_object_list(uid, src=0)
+        ccomm = capi.DistComm.nccl(uid[0], rank, world, local)
+        mv = capi.phfem_mesh()
+        mv.coords, mv.elements = inp["coords"].data_ptr(), inp["elements"].data_ptr()
+        mv.dirichlet, mv.neumann = inp["dirichlet"].data_ptr(), inp["neumann"].data_ptr()
+        mv.nC, mv.nE, mv.nD, mv.nN, mv.owned = hm.nC, int(es[rank + 1] - es[rank]), hm.dirichlet.shape[0], \
+            hm.neumann.shape[0], 0
 
-    def step():
-        st = [dist.RankState(rank=rank, ops=ops, coords=inp["coords"], elements=inp["elements"],
-                             elo=int(es[rank]), ehi=int(es[rank + 1]), dirichlet=inp["dirichlet"],
-                             neumann=inp["neumann"])]
-        st, nC, nE = dist.distributed_pipeline(st, comm, hm.nC, hm.nE, 1, *fields)
-        n_own = st[0].ehi - st[0].elo
-        step.stats = st[0].stats
-        ops.release()
-        return nC, nE, n_own
+        def step():
+            o = capi.dist_pipeline(ccomm, [ctx], [mv], hm.nC, hm.nE, 1, *fields, hist_sample=hist_sample)[0]
+            x = o.o
+            step.stats = {"E": x.E, "L": x.L, "nnz": 4 * x.L - 2 * (x.n_boundary - (x.E - x.L))}
+            res = x.nC, x.nE, x.ehi - x.elo
+            o.release()
+            return res
+    else:
+        comm = dist.TorchComm()
+        ops = dist.CudaRankOps(ctx, dev)
+
+        def step():
+            st = [dist.RankState(rank=rank, ops=ops, coords=inp["coords"], elements=inp["elements"],
+                                 elo=int(es[rank]), ehi=int(es[rank + 1]), dirichlet=inp["dirichlet"],
+                                 neumann=inp["neumann"])]
+            st, nC, nE = dist.distributed_pipeline(st, comm, hm.nC, hm.nE, 1, *fields)
+            n_own = st[0].ehi - st[0].elo
+            step.stats = st[0].stats
+            ops.release()
+            return nC, nE, n_own
 
     for _ in range(args.warmup):
         nC, nE, n_own = step()
@@ -351,10 +375,12 @@ def run_ours_sharded(args, rank, world, local):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} ({nE} triangles): "
                                "EG+RF+EG+AS, config-2 coefficients, sharded",
-                   "parallelism": f"element-range x key-range sharding over {world} GPUs (NCCL all-to-all)",
-                   "refined_edge_generation": "input level: key-range all-to-all dedup; refined level: "
-                                              "from the parent topology (SURVEY f1, all-gathered parent "
-                                              "elem_edge / elements, no occurrence exchange)",
+                   "parallelism": f"element-range x key-range sharding over {world} GPUs (peer-window "
+                                  "exchange kernels over CUDA IPC / NVLink; NCCL for small collectives + fences)",
+                   "orchestration": "C++ (phfem_dist_pipeline)" if args.orch == "cpp" else "Python (dist.py)",
+                   "refined_edge_generation": "input level: occurrences stored into the key owners' buckets, "
+                                              "owner dedup; refined level: sort-free from the parent topology "
+                                              "(SURVEY f1), halo form (side records / group starts)",
                    "triangles": nE, "own_triangles_rank0": n_own, "l2": "inputs larger than L2 (no flush)"},
         "pipeline_roofline": {"compulsory_bytes_per_step": compulsory, "achieved_gbs": round(gbs, 1),
                               "peak": peak * world, "peak_kind": peak_kind, "frac": round(gbs / (peak * world), 4)},
@@ -854,6 +880,8 @@ def main():
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling period (0 = off)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) pipeline even at N = 1")
+    ap.add_argument("--orch", default="cpp", choices=["cpp", "python"],
+                    help="sharded pipeline: host orchestration in C++ (phfem_dist_pipeline) or dist.py")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent single-GPU replicas instead of the sharded pipeline")
     ap.add_argument("--generic-eg", action="store_true",

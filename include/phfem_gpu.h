@@ -658,6 +658,48 @@ phfem_status phfem_dist_dedup_items(phfem_ctx* ctx, uint64_t* items, int64_t n, 
                                     int32_t self_lo, int32_t self_hi, int32_t* self_elem_edge,
                                     phfem_topology* out, int32_t* pairs, int64_t* n_pairs);
 
+/* ---- sharded pipeline, host orchestration in C++ (csrc/dist_run.cu) -------
+ * The whole distributed step (dist.py distributed_pipeline: peer-window input
+ * level, `levels` sort-free halo-form refinements, classification, C, bD,
+ * blocks, load = b + LN) in one call, with no Python between the kernels.
+ * Communicator: _local(W) emulates W ranks in this process on one device
+ * (ctxs[0..W) — may all be the same context; meshes[r] = rank r's view);
+ * _nccl makes this process rank `rank` of `world` (one GPU each; unique id
+ * from rank 0's phfem_dist_nccl_unique_id, 128 bytes, shared out of band;
+ * ctxs[0] / meshes[0] only): bulk exchanges are peer-window kernels into
+ * CUDA-IPC-mapped buffers of the owners, NCCL (resolved at run time from the
+ * process's libnccl.so.2) carries the small collectives and the fences.
+ * Rank r's mesh: replicated coords [nC_all] and boundary lists, its elements
+ * [nE_all r / W, nE_all (r+1) / W).  hist_sample > 1: the key-range histogram
+ * over every hist_sample-th element (ranges only balance work).  Outputs: one
+ * phfem_dist_rank_out per driven rank, global ids; concatenating the ranks'
+ * slices gives the single-GPU pipeline's arrays bit for bit.               */
+typedef struct phfem_dist_comm phfem_dist_comm;
+typedef struct phfem_dist_rank_out {
+  phfem_topology part;          /* the rank's edges (global ids); node_edge_start of its key range */
+  phfem_classification cls;     /* retained_pos [part.E] / retained_edges [cls.L], global */
+  phfem_csr C;                  /* the rank's rows (global row pointers and columns) */
+  double *bd, *B, *D, *M, *M0, *load;  /* [cls.L], [n][9] x 4, [n][3]; n = ehi - elo */
+  int32_t* elem_edge;           /* [n][3] */
+  int32_t* elements;            /* [n][3] */
+  double* coords;               /* [nC][2]: all valid when coords_all, else [0, nc_parent) and [mid_lo, mid_hi) */
+  int32_t* dirichlet;           /* [nD][2] final boundary lists (replicated) */
+  int32_t* neumann;             /* [nN][2] */
+  int64_t mid_lo, mid_hi;
+  int32_t elo, ehi, E0, R0, E, n_boundary, L, nC, nE, nD, nN, nc_parent, coords_all, reserved;
+} phfem_dist_rank_out;
+phfem_status phfem_dist_comm_local(int32_t W, phfem_dist_comm** out);
+phfem_status phfem_dist_nccl_unique_id(void* uid128);
+phfem_status phfem_dist_comm_nccl(const void* uid128, int32_t rank, int32_t world, int32_t device,
+                                  phfem_dist_comm** out);
+void phfem_dist_comm_destroy(phfem_dist_comm* comm);
+const char* phfem_dist_comm_message(const phfem_dist_comm* comm);
+phfem_status phfem_dist_pipeline(phfem_dist_comm* comm, phfem_ctx** ctxs, const phfem_mesh* meshes, int32_t nC_all,
+                                 int32_t nE_all, int32_t levels, const phfem_coeffs* coeffs, const phfem_field* f,
+                                 const phfem_field* g, const phfem_field* uD, double t, int32_t hist_sample,
+                                 phfem_dist_rank_out* outs);
+void phfem_dist_rank_out_release(phfem_ctx* ctx, phfem_dist_rank_out* out);
+
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):
  * n random operand pairs; out[0] = fast divisions that differ from IEEE '/'
  * (must be 0: the element kernels rely on it for bit-exact blocks), out[1] =

@@ -139,6 +139,15 @@ class phfem_pipeline_out(C.Structure):
                 ("M0", C.c_void_p), ("load", C.c_void_p), ("bd", C.c_void_p)]
 
 
+class phfem_dist_rank_out(C.Structure):
+    _fields_ = [("part", phfem_topology), ("cls", phfem_classification), ("C", phfem_csr),
+                ("bd", C.c_void_p), ("B", C.c_void_p), ("D", C.c_void_p), ("M", C.c_void_p), ("M0", C.c_void_p),
+                ("load", C.c_void_p), ("elem_edge", C.c_void_p), ("elements", C.c_void_p), ("coords", C.c_void_p),
+                ("dirichlet", C.c_void_p), ("neumann", C.c_void_p), ("mid_lo", C.c_int64), ("mid_hi", C.c_int64)] + \
+        [(n, C.c_int32) for n in ("elo", "ehi", "E0", "R0", "E", "n_boundary", "L", "nC", "nE", "nD", "nN",
+                                  "nc_parent", "coords_all", "reserved")]
+
+
 _HOST_FIELDS = ["coords", "elements", "dirichlet", "neumann", "edge_nodes", "edge_elements",
                 "local_in_tplus", "local_in_tminus", "interior_edges", "boundary_edges",
                 "elem_edge", "dirichlet_edge_ids", "neumann_edge_ids", "retained_edges",
@@ -179,7 +188,8 @@ EXPORTED = [
     "phfem_mesh_load_text", "phfem_mesh_load_dir", "phfem_mesh_format", "phfem_mesh_save_dir",
     "phfem_topology_csv", "phfem_topology_csv_file", "phfem_text_free", "phfem_dist_refine_level",
     "phfem_assemble_volume_load", "phfem_format_g", "phfem_format_g_host", "phfem_dist_refine_level_ex",
-    "phfem_dist_dedup_ex",
+    "phfem_dist_dedup_ex", "phfem_dist_comm_local", "phfem_dist_nccl_unique_id", "phfem_dist_comm_nccl",
+    "phfem_dist_comm_destroy", "phfem_dist_comm_message", "phfem_dist_pipeline", "phfem_dist_rank_out_release",
 ]
 PIPE_GENERIC_EG = 1
 
@@ -331,6 +341,14 @@ def load_library(path: str = LIB_PATH):
         "phfem_dist_start_p2p": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, vp, i32, i32, vp, vp, vp]),
         "phfem_topology_csv": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), P(vp), P(C.c_size_t)]),
         "phfem_topology_csv_file": (C.c_int, [vp, P(phfem_mesh), P(phfem_topology), C.c_char_p]),
+        "phfem_dist_comm_local": (C.c_int, [i32, P(vp)]),
+        "phfem_dist_nccl_unique_id": (C.c_int, [vp]),
+        "phfem_dist_comm_nccl": (C.c_int, [vp, i32, i32, i32, P(vp)]),
+        "phfem_dist_comm_destroy": (None, [vp]),
+        "phfem_dist_comm_message": (C.c_char_p, [vp]),
+        "phfem_dist_pipeline": (C.c_int, [vp, vp, P(phfem_mesh), i32, i32, i32, P(phfem_coeffs), P(phfem_field),
+                                          P(phfem_field), P(phfem_field), dbl, i32, P(phfem_dist_rank_out)]),
+        "phfem_dist_rank_out_release": (None, [vp, P(phfem_dist_rank_out)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -891,3 +909,112 @@ def pipeline(ctx: Context, mesh: DeviceMesh, levels: int, coeffs: phfem_coeffs, 
     # released underneath it — found by guard mode, tests/test_guard.py)
     res._input = mesh
     return res
+
+
+# ---- sharded pipeline, C++ orchestration (csrc/dist_run.cu) -------------------------
+class DistComm:
+    """phfem_dist_comm: `local(W)` emulates W ranks in this process (one
+    device); `nccl(uid, rank, world, device)` makes this process one rank of
+    an NCCL communicator (uid = `nccl_unique_id()` of rank 0, shared out of
+    band, e.g. with torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, ptr, world: int, local: bool):
+        self.lib, self.ptr, self.world, self.local = load_library(), ptr, world, local
+
+    @classmethod
+    def local_ranks(cls, W: int) -> "DistComm":
+        lib = load_library()
+        p = C.c_void_p()
+        if lib.phfem_dist_comm_local(W, C.byref(p)) != OK:
+            raise ValueError(f"phfem_dist_comm_local({W}) failed")
+        return cls(p, W, True)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = load_library()
+        buf = C.create_string_buffer(128)
+        if lib.phfem_dist_nccl_unique_id(buf) != OK:
+            raise PhfemError(ERR_CUDA, "ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, world: int, device: int) -> "DistComm":
+        lib = load_library()
+        p = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        st = lib.phfem_dist_comm_nccl(buf, rank, world, device, C.byref(p))
+        if st != OK:
+            raise PhfemError(st, f"phfem_dist_comm_nccl(rank {rank} of {world}) failed with status {st}")
+        return cls(p, world, False)
+
+    def close(self):
+        if self.ptr:
+            self.lib.phfem_dist_comm_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DistRankOut:
+    """One rank's outputs of dist_pipeline (device memory of its ctx)."""
+
+    def __init__(self, ctx: Context, o: phfem_dist_rank_out):
+        self.ctx, self.o = ctx, o
+
+    def rank_slice(self) -> dict:
+        """dist.rank_slice's layout (host arrays, global ids): dist.concat_slices
+        of the ranks' slices is the single-GPU pipeline's output."""
+        x, o = self.ctx, self.o
+        d = Topology(x, o.part, owner=False).download()
+        d.pop("elem_edge")
+        n = o.ehi - o.elo
+        d["elem_edge"] = x.to_host(o.elem_edge, (n, 3), np.int32)
+        d["retained_pos"] = x.to_host(o.cls.retained_pos, (o.cls.E,), np.int32)
+        d["retained_edges"] = x.to_host(o.cls.retained_edges, (o.cls.L,), np.int32)
+        d["C_row_ptr"] = x.to_host(o.C.row_ptr, (o.C.rows + 1,), np.int32)
+        d["C_col_idx"] = x.to_host(o.C.col_idx, (o.C.nnz,), np.int32)
+        d["C_values"] = x.to_host(o.C.values, (o.C.nnz,), np.float64)
+        d["bd"] = x.to_host(o.bd, (o.cls.L,), np.float64)
+        for k in ("B", "D", "M", "M0"):
+            d[k] = x.to_host(getattr(o, k), (9 * n,), np.float64)
+        d["load"] = x.to_host(o.load, (3 * n,), np.float64)
+        if o.coords_all:
+            d["coords"] = x.to_host(o.coords, (o.nC, 2), np.float64)
+        else:
+            d["coords_parent"] = x.to_host(o.coords, (o.nc_parent, 2), np.float64)
+            d["mid_own"] = x.to_host((o.coords or 0) + 16 * o.mid_lo, (o.mid_hi - o.mid_lo, 2), np.float64)
+        d["elements"] = x.to_host(o.elements, (n, 3), np.int32)
+        d["dirichlet"] = x.to_host(o.dirichlet, (o.nD, 2), np.int32)
+        d["neumann"] = x.to_host(o.neumann, (o.nN, 2), np.int32)
+        return d
+
+    def release(self):
+        if self.ctx.ptr:
+            self.ctx.lib.phfem_dist_rank_out_release(self.ctx.ptr, C.byref(self.o))
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def dist_pipeline(comm: DistComm, ctxs, meshes, nC: int, nE: int, levels: int, coeffs: phfem_coeffs,
+                  f: phfem_field, g: phfem_field, uD: phfem_field, t: float = 0.0,
+                  hist_sample: int = 1) -> list:
+    """phfem_dist_pipeline: the sharded step with the orchestration in C++.
+    ctxs / meshes: one per driven rank (local: W, NCCL: 1); meshes[r] is a
+    phfem_mesh (replicated coords / boundary lists, rank r's elements)."""
+    n = comm.world if comm.local else 1
+    assert len(ctxs) == n and len(meshes) == n
+    ca = (C.c_void_p * n)(*[c.ptr.value for c in ctxs])
+    ma = (phfem_mesh * n)(*meshes)
+    outs = (phfem_dist_rank_out * n)()
+    st = ctxs[0].lib.phfem_dist_pipeline(comm.ptr, ca, ma, nC, nE, levels, C.byref(coeffs), C.byref(f), C.byref(g),
+                                         C.byref(uD), t, hist_sample, outs)
+    ctxs[0].check(st)
+    return [DistRankOut(c, outs[i]) for i, c in enumerate(ctxs)]
