@@ -657,6 +657,8 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
   const int64_t vbase = (int64_t)out.node_base + (int64_t)tile * kTileNodes;
   const bool fused = out.rpos != nullptr;
   __shared__ unsigned long long nscan[33];
+  __shared__ int32_t ccol[kEmitThreads / 32][128];  // C staging, one 32-row block per warp
+  __shared__ double cval[kEmitThreads / 32][128];
   int nrun = fused ? out.tileN[tile] : 0;  // Neumann edges before the trip (global)
   for (int i00 = 0; i00 < ne; i00 += 4 * kEmitThreads) {
     const int i0 = i00 + threadIdx.x;
@@ -682,64 +684,92 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
       }
       nrun = base;
     }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+      if (i00 + u * kEmitThreads + 32 * warp >= ne) break;  // warp-uniform (C staging below)
       const int i = i0 + u * kEmitThreads;
-      if (i >= ne) break;
+      const bool ok = i < ne;
       const int32_t e = E0 + i;
-      const int32_t v = (int32_t)(vbase + (r[u].x & 0xff));
-      const int32_t bpos = B0 + (r[u].x >> 8);  // boundary edges before e
-      const uint32_t z = (uint32_t)r[u].z;
-      const uint32_t occ_f = z >> 1;
-      const int m_f = (int)(occ_f / 3u);
-      const int l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
-      reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(v, r[u].y) : make_int2(r[u].y, v);
-      out.ltp[e] = l_f;
-      if (r[u].w >= 0) {
-        const uint32_t occ_g = (uint32_t)r[u].w;
-        const int m_g = (int)(occ_g / 3u);
-        const int l_g = (int)((occ_g % 3u + 2u) % 3u);
-        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
-        out.ltm[e] = l_g;
-        eg_slots(out, e, 3 * (int64_t)m_f + l_f, 3 * (int64_t)m_g + l_g);
-        out.interior[e - bpos] = e;
-      } else {
-        reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
-        out.ltm[e] = -1;
-        eg_slots(out, e, 3 * (int64_t)m_f + l_f, -1);
-        out.boundary[bpos] = e;
-      }
-      if (fused) {  // classify_edges + assemble_constraint (edge_topology.cpp:165-173; assembly.cpp:144-168)
-        const bool neu = r[u].w == -2;
-        const int nl = nb4[u];
-        if (neu) {
-          out.rpos[e] = -1;
+      int m_f = 0, l_f = 0, m_g = 0, l_g = -1, rs = 0, nn = 0;
+      bool row = false;
+      double len = 0.0;
+      if (ok) {
+        const int32_t v = (int32_t)(vbase + (r[u].x & 0xff));
+        const int32_t bpos = B0 + (r[u].x >> 8);  // boundary edges before e
+        const uint32_t z = (uint32_t)r[u].z;
+        const uint32_t occ_f = z >> 1;
+        m_f = (int)(occ_f / 3u);
+        l_f = (int)((occ_f % 3u + 2u) % 3u);  // slot s -> local (s + 2) % 3
+        reinterpret_cast<int2*>(out.edge_nodes)[e] = (z & 1u) ? make_int2(v, r[u].y) : make_int2(r[u].y, v);
+        out.ltp[e] = l_f;
+        if (r[u].w >= 0) {
+          const uint32_t occ_g = (uint32_t)r[u].w;
+          m_g = (int)(occ_g / 3u);
+          l_g = (int)((occ_g % 3u + 2u) % 3u);
+          reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, m_g);
+          out.ltm[e] = l_g;
+          eg_slots(out, e, 3 * (int64_t)m_f + l_f, 3 * (int64_t)m_g + l_g);
+          out.interior[e - bpos] = e;
         } else {
-          const int rp = e - nl;
-          const int rs = 4 * rp - 2 * (bpos - nl);  // retained boundary rows hold 2 entries
-          out.rpos[e] = rp;
-          out.redges[rp] = e;
-          out.row_ptr[rp] = rs;
-          const int a = (z & 1u) ? v : r[u].y, b = (z & 1u) ? r[u].y : v;
-          const double2 pa = out.coords[a], pb = out.coords[b];
-          const double dx = pb.x - pa.x, dy = pb.y - pa.y;
-          const double len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
-          const int c0 = l_f == 0 ? 1 : 0, c1 = l_f == 2 ? 1 : 2;
-          const double vp = len * 0.5;  // assembly.cpp:160
-          *reinterpret_cast<int2*>(out.col + rs) = make_int2(3 * m_f + c0, 3 * m_f + c1);
-          __stcs(reinterpret_cast<double2*>(out.val + rs), make_double2(vp, vp));
-          int nn = 2;
-          if (r[u].w >= 0) {
-            const uint32_t occ_g = (uint32_t)r[u].w;
-            const int m_g = (int)(occ_g / 3u);
-            const int l_g = (int)((occ_g % 3u + 2u) % 3u);
-            const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
-            const double vm = -len * 0.5;  // assembly.cpp:164
-            *reinterpret_cast<int2*>(out.col + rs + 2) = make_int2(3 * m_g + d0, 3 * m_g + d1);
-            __stcs(reinterpret_cast<double2*>(out.val + rs + 2), make_double2(vm, vm));
-            nn = 4;
+          reinterpret_cast<int2*>(out.edge_elements)[e] = make_int2(m_f, -1);
+          out.ltm[e] = -1;
+          eg_slots(out, e, 3 * (int64_t)m_f + l_f, -1);
+          out.boundary[bpos] = e;
+        }
+        if (fused) {  // classify_edges + assemble_constraint (edge_topology.cpp:165-173; assembly.cpp:144-168)
+          const bool neu = r[u].w == -2;
+          const int nl = nb4[u];
+          if (neu) {
+            out.rpos[e] = -1;
+          } else {
+            const int rp = e - nl;
+            rs = 4 * rp - 2 * (bpos - nl);  // retained boundary rows hold 2 entries
+            nn = r[u].w >= 0 ? 4 : 2;
+            row = true;
+            out.rpos[e] = rp;
+            out.redges[rp] = e;
+            out.row_ptr[rp] = rs;
+            if (rp == out.L - 1) out.row_ptr[out.L] = rs + nn;
+            const int a = (z & 1u) ? v : r[u].y, b = (z & 1u) ? r[u].y : v;
+            const double2 pa = out.coords[a], pb = out.coords[b];
+            const double dx = pb.x - pa.x, dy = pb.y - pa.y;
+            len = sqrt(dx * dx + dy * dy);  // edge_topology.cpp:183
           }
-          if (rp == out.L - 1) out.row_ptr[out.L] = rs + nn;
+        }
+      }
+      if (fused) {
+        // the warp's rows own contiguous C entries: staged per warp, stored
+        // line by line (a direct per-row store half-writes every sector per
+        // instruction — measured as the larger part of this kernel's time)
+        const unsigned rows = __ballot_sync(0xffffffffu, row);
+        if (rows) {
+          const int fl = __ffs(rows) - 1, ll = 31 - __clz(rows);
+          const int rs0 = __shfl_sync(0xffffffffu, rs, fl);
+          const int cnt = __shfl_sync(0xffffffffu, rs + nn, ll) - rs0;
+          if (row) {
+            const int k = rs - rs0;
+            const int c0 = l_f == 0 ? 1 : 0, c1 = l_f == 2 ? 1 : 2;
+            const double vp = len * 0.5;  // assembly.cpp:160
+            ccol[warp][k] = 3 * m_f + c0;
+            ccol[warp][k + 1] = 3 * m_f + c1;
+            cval[warp][k] = vp;
+            cval[warp][k + 1] = vp;
+            if (nn == 4) {
+              const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
+              const double vm = -len * 0.5;  // assembly.cpp:164
+              ccol[warp][k + 2] = 3 * m_g + d0;
+              ccol[warp][k + 3] = 3 * m_g + d1;
+              cval[warp][k + 2] = vm;
+              cval[warp][k + 3] = vm;
+            }
+          }
+          __syncwarp();
+          for (int k = lane; k < cnt; k += 32) {
+            out.col[rs0 + k] = ccol[warp][k];
+            __stcs(out.val + rs0 + k, cval[warp][k]);
+          }
+          __syncwarp();
         }
       }
     }
