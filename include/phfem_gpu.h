@@ -588,6 +588,60 @@ phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topology* ppart,
 phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc, int32_t node_lo,
                                   int32_t node_hi, int32_t nE_all, int32_t f_off, int32_t nnz_off,
                                   phfem_topology* out, uint8_t* rk, double* coords_fine, phfem_csr* C);
+/* _run_ex: also the rank's rows of the classification on the last level —
+ * retained_pos [Ef] (global rows from r_off, -1 for Neumann) and
+ * retained_edges [Ef - 2 nneu] (global fine ids), ctx memory, both or
+ * neither, C required; phfem_dist_classify_given then completes the
+ * classification around them (Neumann bitmap, the rank's id lists, flags)
+ * and takes ownership.  phfem_dist_children_slots_ex: midpoints of the parent
+ * edges [own_lo, own_hi) are skipped (the rank's level kernel wrote them).  */
+/* Local mode of the halo exchanges (the C++ orchestration's default): the
+ * side record / group start of an element slot whose edge AND element belong
+ * to the same rank is not stored at all — the level kernel / children pass
+ * gather it from the rank's own arrays instead (at W = 1 no record moves).
+ * phfem_dist_local names those arrays: the rank's elements and elem_edge
+ * (global signed ids) for its global element range [elo, ehi).            */
+typedef struct phfem_dist_local {
+  const int32_t* elements;
+  const int32_t* elem_edge;
+  int32_t elo, ehi;
+  int32_t no_remote; /* 1: no other rank holds elements (W = 1): no side record exists */
+  int32_t reserved;
+} phfem_dist_local;
+phfem_status phfem_dist_side_p2p_ex(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge, int32_t n,
+                                    const int32_t* esplits, int32_t W, int32_t self, int32_t* const* peer_side,
+                                    int32_t* remote, int skip_self);
+phfem_status phfem_dist_start_p2p_ex(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                     int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                     int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
+                                     int32_t* remote, int skip_self);
+phfem_status phfem_dist_level_count_ex(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p, const int32_t* side,
+                                       const phfem_dist_local* local, const int32_t* neu_parent_ids,
+                                       int32_t nN_parent, int with_C, int32_t* Ef, int32_t* nneu, void** plan);
+phfem_status phfem_dist_level_run_ex(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc, int32_t node_lo,
+                                     int32_t node_hi, int32_t nE_all, int32_t f_off, int32_t nnz_off, int32_t r_off,
+                                     phfem_topology* out, uint8_t* rk, double* coords_fine, phfem_csr* C,
+                                     int32_t* retained_pos, int32_t* retained_edges);
+phfem_status phfem_dist_classify_given(phfem_ctx* ctx, const phfem_topology* part, const int32_t* dir_ids_local,
+                                       int32_t nD, const int32_t* neu_ids_local, int32_t nN, int32_t* retained_pos,
+                                       int32_t* retained_edges, int32_t L, phfem_classification* out);
+/* children_slots_ex: fine_nes != NULL (local mode): the group starts / rank
+ * bytes of the slots whose parent edge is the rank's own (own_lo..own_hi)
+ * come from its fine node_edge_start (fine_nes[e - own_lo + nes_off], as
+ * phfem_dist_start_p2p) and rk[e - own_lo], not from gs / grk.             */
+phfem_status phfem_dist_children_slots_ex(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                          int32_t n, const int32_t* gs, const uint8_t* grk, int32_t nc,
+                                          int32_t own_lo, int32_t own_hi, const int32_t* fine_nes, int32_t nes_off,
+                                          const uint8_t* rk, double* coords_fine, int32_t* children,
+                                          int32_t* fine_elem_edge);
+/* phfem_assemble_volume_load in two halves (_start: reset the ctx error block
+ * and launch, no synchronisation; _finish: fetch it and raise the reference's
+ * errors) so the caller can enqueue other work while the element pass runs;
+ * nothing in between may use the ctx error block.                          */
+phfem_status phfem_dist_volume_start(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_coeffs* c,
+                                     const phfem_field* f, double t, double* B, double* D, double* M, double* M0,
+                                     double* load);
+phfem_status phfem_dist_volume_finish(phfem_ctx* ctx);
 /* assemble_dirichlet of a rank whose retained positions start at r_off:
  * out[0 .. L) holds rows r_off .. r_off + L                               */
 phfem_status phfem_dist_dirichlet(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_topology* part,
@@ -694,10 +748,11 @@ phfem_status phfem_dist_comm_nccl(const void* uid128, int32_t rank, int32_t worl
                                   phfem_dist_comm** out);
 void phfem_dist_comm_destroy(phfem_dist_comm* comm);
 const char* phfem_dist_comm_message(const phfem_dist_comm* comm);
+#define PHFEM_DIST_NO_LOCAL 1 /* flags: every slot's side record / group start through the windows */
 phfem_status phfem_dist_pipeline(phfem_dist_comm* comm, phfem_ctx** ctxs, const phfem_mesh* meshes, int32_t nC_all,
                                  int32_t nE_all, int32_t levels, const phfem_coeffs* coeffs, const phfem_field* f,
                                  const phfem_field* g, const phfem_field* uD, double t, int32_t hist_sample,
-                                 phfem_dist_rank_out* outs);
+                                 int32_t flags, phfem_dist_rank_out* outs);
 void phfem_dist_rank_out_release(phfem_ctx* ctx, phfem_dist_rank_out* out);
 
 /* ---- device self-test of the fast-math building blocks (csrc/fastmath.cuh):

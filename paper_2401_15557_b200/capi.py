@@ -190,7 +190,11 @@ EXPORTED = [
     "phfem_assemble_volume_load", "phfem_format_g", "phfem_format_g_host", "phfem_dist_refine_level_ex",
     "phfem_dist_dedup_ex", "phfem_dist_comm_local", "phfem_dist_nccl_unique_id", "phfem_dist_comm_nccl",
     "phfem_dist_comm_destroy", "phfem_dist_comm_message", "phfem_dist_pipeline", "phfem_dist_rank_out_release",
+    "phfem_dist_level_run_ex", "phfem_dist_classify_given", "phfem_dist_children_slots_ex",
+    "phfem_dist_side_p2p_ex", "phfem_dist_start_p2p_ex", "phfem_dist_level_count_ex",
+    "phfem_dist_volume_start", "phfem_dist_volume_finish",
 ]
+DIST_NO_LOCAL = 1
 PIPE_GENERIC_EG = 1
 
 _lib = None
@@ -347,8 +351,22 @@ def load_library(path: str = LIB_PATH):
         "phfem_dist_comm_destroy": (None, [vp]),
         "phfem_dist_comm_message": (C.c_char_p, [vp]),
         "phfem_dist_pipeline": (C.c_int, [vp, vp, P(phfem_mesh), i32, i32, i32, P(phfem_coeffs), P(phfem_field),
-                                          P(phfem_field), P(phfem_field), dbl, i32, P(phfem_dist_rank_out)]),
+                                          P(phfem_field), P(phfem_field), dbl, i32, i32, P(phfem_dist_rank_out)]),
+        "phfem_dist_volume_start": (C.c_int, [vp, P(phfem_mesh), P(phfem_coeffs), P(phfem_field), dbl, vp, vp, vp,
+                                              vp, vp]),
+        "phfem_dist_volume_finish": (C.c_int, [vp]),
+        "phfem_dist_side_p2p_ex": (C.c_int, [vp, vp, vp, i32, vp, i32, i32, vp, vp, C.c_int]),
+        "phfem_dist_start_p2p_ex": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, vp, i32, i32, vp, vp, vp,
+                                              C.c_int]),
+        "phfem_dist_level_count_ex": (C.c_int, [vp, P(phfem_topology), i32, vp, vp, vp, i32, C.c_int, P(i32),
+                                                P(i32), P(vp)]),
         "phfem_dist_rank_out_release": (None, [vp, P(phfem_dist_rank_out)]),
+        "phfem_dist_level_run_ex": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, P(phfem_topology), vp,
+                                              vp, P(phfem_csr), vp, vp]),
+        "phfem_dist_classify_given": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, i32, vp, vp, i32,
+                                                P(phfem_classification)]),
+        "phfem_dist_children_slots_ex": (C.c_int, [vp, vp, vp, i32, vp, vp, i32, i32, i32, vp, i32, vp, vp, vp,
+                                                   vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -1005,7 +1023,7 @@ class DistRankOut:
 
 def dist_pipeline(comm: DistComm, ctxs, meshes, nC: int, nE: int, levels: int, coeffs: phfem_coeffs,
                   f: phfem_field, g: phfem_field, uD: phfem_field, t: float = 0.0,
-                  hist_sample: int = 1) -> list:
+                  hist_sample: int = 1, flags: int = 0) -> list:
     """phfem_dist_pipeline: the sharded step with the orchestration in C++.
     ctxs / meshes: one per driven rank (local: W, NCCL: 1); meshes[r] is a
     phfem_mesh (replicated coords / boundary lists, rank r's elements)."""
@@ -1015,6 +1033,6 @@ def dist_pipeline(comm: DistComm, ctxs, meshes, nC: int, nE: int, levels: int, c
     ma = (phfem_mesh * n)(*meshes)
     outs = (phfem_dist_rank_out * n)()
     st = ctxs[0].lib.phfem_dist_pipeline(comm.ptr, ca, ma, nC, nE, levels, C.byref(coeffs), C.byref(f), C.byref(g),
-                                         C.byref(uD), t, hist_sample, outs)
+                                         C.byref(uD), t, hist_sample, flags, outs)
     ctxs[0].check(st)
     return [DistRankOut(c, outs[i]) for i, c in enumerate(ctxs)]

@@ -596,6 +596,35 @@ PHFEM_API phfem_status phfem_assemble_volume_load(phfem_ctx* ctx, const phfem_me
   return volume_errors(ctx, true, true);
 }
 
+// phfem_assemble_volume_load in two halves, so that a caller can enqueue
+// other work while the element pass runs: _start resets the ctx error block
+// and launches (no synchronisation); _finish fetches it and raises the
+// reference's errors.  Nothing between the two may use the ctx error block
+// (the sharded pipeline runs its classification / bD / Neumann tables there).
+PHFEM_API phfem_status phfem_dist_volume_start(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem_coeffs* c,
+                                               const phfem_field* f, double t, double* B, double* D, double* M,
+                                               double* M0, double* load) {
+  if (!ctx || !mesh || !c || !f || (!load && mesh->nE)) return PHFEM_ERR_INVALID_ARGUMENT;
+  VolArgs a = make_vol_args(mesh);
+  a.coeffs = *c;
+  a.B = B;
+  a.D = D;
+  a.M = M;
+  a.M0 = M0;
+  a.f = *f;
+  a.t = t;
+  a.load = load;
+  a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0) && aligned16(load);
+  PHFEM_TRY(errors_reset(ctx));
+  return launch_volume(ctx, a, true, true);
+}
+
+PHFEM_API phfem_status phfem_dist_volume_finish(phfem_ctx* ctx) {
+  if (!ctx) return PHFEM_ERR_INVALID_ARGUMENT;
+  PHFEM_TRY(errors_fetch(ctx));
+  return volume_errors(ctx, true, true);
+}
+
 PHFEM_API phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mesh,
                                            const phfem_field* f, double t, double* out) {
   if (!ctx || !mesh || !f || (!out && mesh->nE)) return PHFEM_ERR_INVALID_ARGUMENT;

@@ -172,7 +172,7 @@ __global__ void k_dist_neu_bits(const int32_t* __restrict__ neu_ids, int nN, int
     const int e = neu_ids[i] - E0;
     if (e < 0 || e >= E) continue;
     const uint32_t bit = 1u << (e & 31);
-    if (atomicOr(&bits[e >> 5], bit) & bit) *dup = 1;
+    if ((atomicOr(&bits[e >> 5], bit) & bit) && dup) *dup = 1;
   }
 }
 
@@ -355,7 +355,8 @@ __device__ __forceinline__ void remote_flush(const int32_t* srem, int W, int32_t
 __global__ void __launch_bounds__(256) k_dist_side_p2p(const int32_t* __restrict__ elements,
                                                        const int32_t* __restrict__ elem_edge, int n,
                                                        const int32_t* __restrict__ esplits, int W, int self,
-                                                       int4* const* __restrict__ peer_side, int32_t* remote) {
+                                                       int4* const* __restrict__ peer_side, int32_t* remote,
+                                                       int skip_self) {
   __shared__ int32_t srem[kRemoteMax];
   remote_init(srem);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * (int64_t)n;
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(256) k_dist_side_p2p(const int32_t* __restrict
     const int s = elem_edge[i];
     const int e = s >= 0 ? s : ~s;
     const int d = dest_of(esplits, W, e);
+    if (skip_self && d == self) continue;  // local mode: the level kernel gathers it
     const int4 r = make_int4(elem_edge[3 * m + (k == 2 ? 0 : k + 1)], elem_edge[3 * m + (k == 0 ? 2 : k - 1)],
                              elements[i], 0);
     peer_side[d][2 * (int64_t)(e - __ldg(esplits + d)) + (s < 0 ? 1 : 0)] = r;
@@ -380,7 +382,8 @@ __global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restric
                                                         const uint8_t* __restrict__ rk, int E,
                                                         const int32_t* __restrict__ psplits, int W, int self,
                                                         int32_t* const* __restrict__ peer_gs,
-                                                        uint8_t* const* __restrict__ peer_grk, int32_t* remote) {
+                                                        uint8_t* const* __restrict__ peer_grk, int32_t* remote,
+                                                        int skip_self) {
   __shared__ int32_t srem[kRemoteMax];
   remote_init(srem);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * (int64_t)E;
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(256) k_dist_start_p2p(const int32_t* __restric
     if (m >= 0) {
       const int l = sd ? ltm[le] : ltp[le];
       d = dest_of(psplits, W, m);
+      if (skip_self && d == self) continue;  // local mode: the children pass gathers it
       const int64_t slot = 3 * (int64_t)(m - __ldg(psplits + d)) + l;
       peer_gs[d][slot] = fine_nes[le + nes_off];
       peer_grk[d][slot] = rk[le];
@@ -605,6 +609,43 @@ PHFEM_API phfem_status phfem_dist_classify_ex(phfem_ctx* ctx, const phfem_topolo
   return classify_lists_from_bits(ctx, part, out, E0, r_off, e_off);
 }
 
+// The same when the (fused) level kernel already wrote retained_pos [part->E]
+// / retained_edges [L] (global rows / ids, ctx memory: ownership moves into
+// *out): only the Neumann bitmap and the rank's id lists remain.  No host
+// synchronisation (the sharded pipeline overlaps it with the element pass);
+// flags stay 0 — the caller, which holds the global Neumann list, sets
+// PHFEM_CLS_DUP_NEUMANN.
+PHFEM_API phfem_status phfem_dist_classify_given(phfem_ctx* ctx, const phfem_topology* part,
+                                                 const int32_t* dir_ids, int32_t nD, const int32_t* neu_ids,
+                                                 int32_t nN, int32_t* retained_pos, int32_t* retained_edges,
+                                                 int32_t L, phfem_classification* out) {
+  memset(out, 0, sizeof(*out));
+  if (!ctx || !part || L < 0 || L > part->E || (part->E && !retained_pos) || (L && !retained_edges) ||
+      (nD && !dir_ids) || (nN && !neu_ids))
+    return PHFEM_ERR_INVALID_ARGUMENT;
+  const int E = part->E;
+  const int nwords = (E + 31) / 32;
+  out->E = E;
+  out->L = L;
+  out->retained_pos = retained_pos;
+  out->retained_edges = retained_edges;
+  PHFEM_TRY(dalloc(ctx, &out->neumann_bits, nwords));
+  PHFEM_CUDA(ctx, cudaMemsetAsync(out->neumann_bits, 0, sizeof(uint32_t) * std::max(nwords, 1), ctx->stream));
+  if (nN > 0)
+    PHFEM_LAUNCH(ctx, "k_dist_neu_bits", k_dist_neu_bits<<<grid_for(nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        neu_ids, nN, 0, E, out->neumann_bits, nullptr));
+  // the ids are the rank's own already (local, list order): plain copies
+  PHFEM_TRY(dalloc(ctx, &out->dirichlet_edge_ids, nD));
+  PHFEM_TRY(dalloc(ctx, &out->neumann_edge_ids, nN));
+  if (nD) PHFEM_CUDA(ctx, cudaMemcpyAsync(out->dirichlet_edge_ids, dir_ids, sizeof(int32_t) * nD,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+  if (nN) PHFEM_CUDA(ctx, cudaMemcpyAsync(out->neumann_edge_ids, neu_ids, sizeof(int32_t) * nN,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+  out->nD = nD;
+  out->nN = nN;
+  return PHFEM_OK;
+}
+
 PHFEM_API phfem_status phfem_dist_classify(phfem_ctx* ctx, const phfem_topology* part, int32_t E0,
                                            const int32_t* dir_ids, int32_t nD,
                                            const int32_t* neu_ids, int32_t nN,
@@ -717,9 +758,9 @@ PHFEM_API phfem_status phfem_dist_start_apply(phfem_ctx* ctx, const int32_t* rec
   return PHFEM_OK;
 }
 
-PHFEM_API phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
-                                           int32_t n, const int32_t* esplits, int32_t W, int32_t self,
-                                           int32_t* const* peer_side, int32_t* remote) {
+PHFEM_API phfem_status phfem_dist_side_p2p_ex(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                              int32_t n, const int32_t* esplits, int32_t W, int32_t self,
+                                              int32_t* const* peer_side, int32_t* remote, int skip_self) {
   if (!ctx || !esplits || !peer_side || !remote || W < 1 || W > kRemoteMax || self < 0 || self >= W || n < 0 ||
       (n && (!elements || !elem_edge)))
     return PHFEM_ERR_INVALID_ARGUMENT;
@@ -727,14 +768,20 @@ PHFEM_API phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elemen
   if (n > 0)
     PHFEM_LAUNCH(ctx, "k_dist_side_p2p", k_dist_side_p2p<<<grid_for(3 * (int64_t)n, 256, ctx->num_sms * 8), 256, 0,
                                                            ctx->stream>>>(
-        elements, elem_edge, n, esplits, W, self, reinterpret_cast<int4* const*>(peer_side), remote));
+        elements, elem_edge, n, esplits, W, self, reinterpret_cast<int4* const*>(peer_side), remote, skip_self));
   return PHFEM_OK;
 }
 
-PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
-                                            int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
-                                            int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
-                                            int32_t* remote) {
+PHFEM_API phfem_status phfem_dist_side_p2p(phfem_ctx* ctx, const int32_t* elements, const int32_t* elem_edge,
+                                           int32_t n, const int32_t* esplits, int32_t W, int32_t self,
+                                           int32_t* const* peer_side, int32_t* remote) {
+  return phfem_dist_side_p2p_ex(ctx, elements, elem_edge, n, esplits, W, self, peer_side, remote, 0);
+}
+
+PHFEM_API phfem_status phfem_dist_start_p2p_ex(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                               int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                               int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
+                                               int32_t* remote, int skip_self) {
   if (!ctx || !ppart || !psplits || !peer_gs || !peer_grk || !remote || W < 1 || W > kRemoteMax || self < 0 || self >= W ||
       (ppart->E && (!fine_nes || !rk)))
     return PHFEM_ERR_INVALID_ARGUMENT;
@@ -744,8 +791,15 @@ PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology
     PHFEM_LAUNCH(ctx, "k_dist_start_p2p", k_dist_start_p2p<<<grid_for(2 * (int64_t)E, 256, ctx->num_sms * 8), 256, 0,
                                                              ctx->stream>>>(
         ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus, fine_nes, nes_off, rk, E, psplits, W,
-        self, peer_gs, peer_grk, remote));
+        self, peer_gs, peer_grk, remote, skip_self));
   return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_start_p2p(phfem_ctx* ctx, const phfem_topology* ppart, const int32_t* fine_nes,
+                                            int32_t nes_off, const uint8_t* rk, const int32_t* psplits, int32_t W,
+                                            int32_t self, int32_t* const* peer_gs, uint8_t* const* peer_grk,
+                                            int32_t* remote) {
+  return phfem_dist_start_p2p_ex(ctx, ppart, fine_nes, nes_off, rk, psplits, W, self, peer_gs, peer_grk, remote, 0);
 }
 
 PHFEM_API phfem_status phfem_dist_pairs_p2p(phfem_ctx* ctx, const int32_t* pairs, int64_t n, int32_t E0,

@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -45,22 +46,31 @@ phfem_status phfem_dist_pairs_p2p(phfem_ctx*, const int32_t*, int64_t, int32_t, 
                                   int32_t* const*, int32_t*);
 phfem_status phfem_dist_resolve(phfem_ctx*, const phfem_topology*, int32_t, int32_t, const int32_t*, int32_t,
                                 int32_t, int32_t*, unsigned long long*);
-phfem_status phfem_dist_side_p2p(phfem_ctx*, const int32_t*, const int32_t*, int32_t, const int32_t*, int32_t,
-                                 int32_t, int32_t* const*, int32_t*);
-phfem_status phfem_dist_level_count(phfem_ctx*, const phfem_topology*, int32_t, const int32_t*, const int32_t*,
-                                    int32_t, int, int32_t*, int32_t*, void**);
-phfem_status phfem_dist_level_run(phfem_ctx*, void*, const double*, int32_t, int32_t, int32_t, int32_t, int32_t,
-                                  int32_t, phfem_topology*, uint8_t*, double*, phfem_csr*);
-phfem_status phfem_dist_start_p2p(phfem_ctx*, const phfem_topology*, const int32_t*, int32_t, const uint8_t*,
-                                  const int32_t*, int32_t, int32_t, int32_t* const*, uint8_t* const*, int32_t*);
-phfem_status phfem_dist_children_slots(phfem_ctx*, const int32_t*, const int32_t*, int32_t, const int32_t*,
-                                       const uint8_t*, int32_t, double*, int32_t*, int32_t*);
+phfem_status phfem_dist_side_p2p_ex(phfem_ctx*, const int32_t*, const int32_t*, int32_t, const int32_t*, int32_t,
+                                    int32_t, int32_t* const*, int32_t*, int);
+phfem_status phfem_dist_level_count_ex(phfem_ctx*, const phfem_topology*, int32_t, const int32_t*,
+                                       const phfem_dist_local*, const int32_t*, int32_t, int, int32_t*, int32_t*,
+                                       void**);
+phfem_status phfem_dist_level_run_ex(phfem_ctx*, void*, const double*, int32_t, int32_t, int32_t, int32_t, int32_t,
+                                     int32_t, int32_t, phfem_topology*, uint8_t*, double*, phfem_csr*, int32_t*,
+                                     int32_t*);
+phfem_status phfem_dist_classify_given(phfem_ctx*, const phfem_topology*, const int32_t*, int32_t, const int32_t*,
+                                       int32_t, int32_t*, int32_t*, int32_t, phfem_classification*);
+phfem_status phfem_dist_children_slots_ex(phfem_ctx*, const int32_t*, const int32_t*, int32_t, const int32_t*,
+                                          const uint8_t*, int32_t, int32_t, int32_t, const int32_t*, int32_t,
+                                          const uint8_t*, double*, int32_t*, int32_t*);
+phfem_status phfem_dist_start_p2p_ex(phfem_ctx*, const phfem_topology*, const int32_t*, int32_t, const uint8_t*,
+                                     const int32_t*, int32_t, int32_t, int32_t* const*, uint8_t* const*, int32_t*,
+                                     int);
 phfem_status phfem_dist_classify_ex(phfem_ctx*, const phfem_topology*, int32_t, const int32_t*, int32_t,
                                     const int32_t*, int32_t, int32_t, int32_t, phfem_classification*);
 phfem_status phfem_dist_dirichlet(phfem_ctx*, const phfem_mesh*, const phfem_topology*,
                                   const phfem_classification*, const phfem_field*, double, int32_t, double*);
 phfem_status phfem_dist_neumann_table(phfem_ctx*, const phfem_topology*, int32_t, const int32_t*, int32_t,
                                       int32_t*);
+phfem_status phfem_dist_volume_start(phfem_ctx*, const phfem_mesh*, const phfem_coeffs*, const phfem_field*, double,
+                                     double*, double*, double*, double*, double*);
+phfem_status phfem_dist_volume_finish(phfem_ctx*);
 phfem_status phfem_dist_neumann_apply(phfem_ctx*, const phfem_mesh*, const int32_t*, int32_t, int32_t, int32_t,
                                       int32_t, const phfem_field*, double, double*);
 }
@@ -115,6 +125,9 @@ struct phfem_dist_comm {
   };
   std::map<std::string, Win> win;
   int32_t* fence_dev = nullptr;
+  void* pin = nullptr;  // pinned host staging of the resolved boundary ids
+  size_t pin_cap = 0;
+  cudaEvent_t ev = nullptr;
   std::string message;
 };
 
@@ -329,6 +342,9 @@ struct RS {
   phfem_csr C;
   bool have_C = false;
   int R0 = -1;                     // known up front after a fused last level
+  int32_t* rpos = nullptr;         // fused last level: retained_pos [E] / retained_edges [L] (global)
+  int32_t* redges = nullptr;
+  int32_t Lr = 0;
   int64_t mid_lo = 0, mid_hi = 0;  // the rank's owned midpoints in coords (last level)
   int32_t nc_parent = 0;
 };
@@ -410,6 +426,8 @@ PHFEM_API void phfem_dist_comm_destroy(phfem_dist_comm* c) {
       if (p) cudaFree(p);
   }
   if (c->fence_dev) cudaFree(c->fence_dev);
+  if (c->pin) cudaFreeHost(c->pin);
+  if (c->ev) cudaEventDestroy(c->ev);
   if (c->nccl) nccl_api().destroy(c->nccl);
   delete c;
 }
@@ -441,9 +459,19 @@ namespace {
 // backend, P2P = True, sort_free = True)
 phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, int32_t nE_all, int32_t levels,
                            const phfem_coeffs* coeffs, const phfem_field* f, const phfem_field* g,
-                           const phfem_field* uD, double t, int32_t hist_sample, phfem_dist_rank_out* outs,
-                           std::vector<RS>& S) {
+                           const phfem_field* uD, double t, int32_t hist_sample, int32_t flags,
+                           phfem_dist_rank_out* outs, std::vector<RS>& S) {
   Comm* c = R.c;
+  // PHFEM_DIST_TRACE=1: host-side phase times (ms since the call started)
+  const bool trace = getenv("PHFEM_DIST_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "[dist-trace] %-28s %8.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
+  // local mode: slots whose element and edge are this rank's move through no window
+  const int local_mode = (flags & PHFEM_DIST_NO_LOCAL) ? 0 : 1;
   const int nl = R.n(), W = c->world;
   auto& ctx = R.ctx;
   int64_t nC = nC_all, nE = nE_all;
@@ -509,6 +537,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     for (int r = 1; r < W; ++r) splits[r] = sp[r] / 256 * 256;  // 256-node tiles: one owner per bucket
     splits[W] = (int32_t)nC;
   }
+  tr("hist+splits");
   const int bs = phfem_dist_bucket_bits((int32_t)nC, (int32_t)nE);
   const int64_t NB = (nC + (1 << bs) - 1) >> bs;
   std::vector<int32_t> bsp(W + 1);
@@ -534,6 +563,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     dfree(ctx[i], histb[i]);
     dfree(ctx[i], hall[i]);
   }
+  tr("bucket cursors");
   std::vector<void*> itbuf, eebuf;
   std::vector<void**> itpeers, eepeers;
   {
@@ -547,6 +577,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     PHFEM_TRY(phfem_dist_scatter_p2p(ctx[i], S[i].elements, own(S[i]), S[i].elo, (int32_t)nC, (int32_t)nE, cursor[i],
                                      bspd[i], W, S[i].r, (uint64_t* const*)itpeers[i], remote[i]));
   PHFEM_TRY(fence(R));
+  tr("scatter");
   std::vector<int32_t*> pairs(nl);
   std::vector<int64_t> npairs(nl);
   std::vector<std::vector<int64_t>> eb(nl);
@@ -561,6 +592,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     dfree(ctx[i], cursor[i]);
     dfree(ctx[i], boff[i]);
   }
+  tr("dedup");
   std::vector<int64_t> ebg;
   PHFEM_TRY(allgather_host(R, eb, ebg));
   int64_t Etot = 0, Btot = 0;
@@ -594,49 +626,85 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     S[i].own_ee = false;
   }
 
+  tr("pairs");
   // ---- boundary pairs -> global ids on every rank + the reference's first error
-  auto resolve = [&](std::vector<int32_t>& ids) -> phfem_status {
+  // resolve in two halves: _enqueue (kernels, all-reduces, the copy of the
+  // ids into pinned host memory, an event) and _wait (the event, the
+  // reference's first error) — the last level enqueues the element pass in
+  // between, so the host waits for the ids while the GPU keeps working
+  struct Resolve {
+    std::vector<void*> idd, errd;
+    std::vector<int32_t*> prd;
+    int n = 0;
+  } rv;
+  auto resolve_enqueue = [&]() -> phfem_status {
     const int nD = (int)hdir.size() / 2, nN = (int)hneu.size() / 2, n = nD + nN;
-    ids.assign(n, -1);
+    rv.n = n;
+    rv.idd.assign(nl, nullptr);
+    rv.errd.assign(nl, nullptr);
+    rv.prd.assign(nl, nullptr);
     if (n == 0) return PHFEM_OK;
     std::vector<int32_t> pr(hdir);
     pr.insert(pr.end(), hneu.begin(), hneu.end());
-    std::vector<void*> idd(nl), errd(nl);
-    std::vector<int32_t*> prd(nl);
     for (int i = 0; i < nl; ++i) {
-      PHFEM_TRY(upload(ctx[i], pr, &prd[i]));
+      PHFEM_TRY(upload(ctx[i], pr, &rv.prd[i]));
       int32_t* d = nullptr;
       unsigned long long* e = nullptr;
       PHFEM_TRY(dalloc(ctx[i], &d, n));
       PHFEM_TRY(dalloc(ctx[i], &e, 1));
       PHFEM_CUDA(ctx[i], cudaMemsetAsync(d, 0xff, sizeof(int32_t) * n, R.st(i)));
       PHFEM_CUDA(ctx[i], cudaMemsetAsync(e, 0xff, sizeof(unsigned long long), R.st(i)));
-      PHFEM_TRY(phfem_dist_resolve(ctx[i], &S[i].part, splits[S[i].r], S[i].E0, prd[i], n, 0, d, e));
-      idd[i] = d;
-      errd[i] = e;
+      PHFEM_TRY(phfem_dist_resolve(ctx[i], &S[i].part, splits[S[i].r], S[i].E0, rv.prd[i], n, 0, d, e));
+      rv.idd[i] = d;
+      rv.errd[i] = e;
     }
-    PHFEM_TRY(allreduce_dev(R, idd, n, kMax));
-    PHFEM_TRY(allreduce_dev(R, errd, 1, kMinU64));
-    unsigned long long key = ~0ull;
-    PHFEM_CUDA(ctx[0], cudaMemcpyAsync(ids.data(), idd[0], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, R.st(0)));
-    PHFEM_CUDA(ctx[0], cudaMemcpyAsync(&key, errd[0], sizeof key, cudaMemcpyDeviceToHost, R.st(0)));
-    PHFEM_CUDA(ctx[0], cudaStreamSynchronize(R.st(0)));
+    PHFEM_TRY(allreduce_dev(R, rv.idd, n, kMax));
+    PHFEM_TRY(allreduce_dev(R, rv.errd, 1, kMinU64));
+    const size_t need = sizeof(int32_t) * n + 16;
+    if (c->pin_cap < need) {
+      PHFEM_TRY(R.sync_all());
+      if (c->pin) cudaFreeHost(c->pin);
+      c->pin = nullptr;
+      c->pin_cap = 0;
+      PHFEM_CUDA(ctx[0], cudaMallocHost(&c->pin, need + need / 2));
+      c->pin_cap = need + need / 2;
+    }
+    if (!c->ev) PHFEM_CUDA(ctx[0], cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
+    PHFEM_CUDA(ctx[0], cudaMemcpyAsync(c->pin, rv.errd[0], 8, cudaMemcpyDeviceToHost, R.st(0)));
+    PHFEM_CUDA(ctx[0], cudaMemcpyAsync((char*)c->pin + 16, rv.idd[0], sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                                       R.st(0)));
+    PHFEM_CUDA(ctx[0], cudaEventRecord(c->ev, R.st(0)));
     for (int i = 0; i < nl; ++i) {
-      int32_t* d = (int32_t*)idd[i];
-      unsigned long long* e = (unsigned long long*)errd[i];
-      dfree(ctx[i], d);
+      int32_t* d = (int32_t*)rv.idd[i];
+      unsigned long long* e = (unsigned long long*)rv.errd[i];
+      dfree(ctx[i], d);  // stream-ordered: after the copy
       dfree(ctx[i], e);
-      dfree(ctx[i], prd[i]);
+      dfree(ctx[i], rv.prd[i]);
     }
+    return PHFEM_OK;
+  };
+  auto resolve_wait = [&](std::vector<int32_t>& ids) -> phfem_status {
+    const int nD = (int)hdir.size() / 2, n = rv.n;
+    ids.assign(n, -1);
+    if (n == 0) return PHFEM_OK;
+    PHFEM_CUDA(ctx[0], cudaEventSynchronize(c->ev));
+    unsigned long long key = 0;
+    memcpy(&key, c->pin, 8);
+    memcpy(ids.data(), (char*)c->pin + 16, sizeof(int32_t) * n);
     if (key != ~0ull) {
       const int64_t pos = (int64_t)(key >> 2);
       const bool interior = key & 1;
       const bool is_d = pos < nD;
       const int32_t* pp = is_d ? &hdir[2 * pos] : &hneu[2 * (pos - nD)];
-      return set_error(ctx[0], interior ? PHFEM_ERR_INTERIOR_BOUNDARY : PHFEM_ERR_NOT_AN_EDGE, "%s pair (%d,%d) %s", is_d ? "dirichlet" : "neumann", pp[0] + 1,
-                       pp[1] + 1, interior ? "resolves to an interior edge" : "is not an edge");
+      return set_error(ctx[0], interior ? PHFEM_ERR_INTERIOR_BOUNDARY : PHFEM_ERR_NOT_AN_EDGE, "%s pair (%d,%d) %s",
+                       is_d ? "dirichlet" : "neumann", pp[0] + 1, pp[1] + 1,
+                       interior ? "resolves to an interior edge" : "is not an edge");
     }
     return PHFEM_OK;
+  };
+  auto resolve = [&](std::vector<int32_t>& ids) -> phfem_status {
+    PHFEM_TRY(resolve_enqueue());
+    return resolve_wait(ids);
   };
 
   // ---- refinements: sort-free, halo form through peer windows
@@ -649,17 +717,20 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     std::vector<void*> sdbuf;
     std::vector<void**> sdpeers;
     std::vector<int32_t*> edgesp(nl);
+    const bool no_remote = local_mode && W == 1;  // one rank in local mode: no record to move
     {
       std::vector<size_t> by(nl);
-      for (int i = 0; i < nl; ++i) by[i] = 32 * (size_t)S[i].part.E;
+      for (int i = 0; i < nl; ++i) by[i] = no_remote ? 0 : 32 * (size_t)S[i].part.E;
       PHFEM_TRY(window(R, "side", by, sdbuf, sdpeers));
     }
     for (int i = 0; i < nl; ++i) {
       PHFEM_TRY(upload(ctx[i], E0s, &edgesp[i]));
-      PHFEM_TRY(phfem_dist_side_p2p(ctx[i], S[i].elements, S[i].ee, own(S[i]), edgesp[i], W, S[i].r,
-                                    (int32_t* const*)sdpeers[i], remote[i]));
+      if (!no_remote)
+        PHFEM_TRY(phfem_dist_side_p2p_ex(ctx[i], S[i].elements, S[i].ee, own(S[i]), edgesp[i], W, S[i].r,
+                                         (int32_t* const*)sdpeers[i], remote[i], local_mode));
     }
     PHFEM_TRY(fence(R));
+  tr("side");
     // 2. level count -> fine offsets (all-gathered) -> level run with global ids
     std::vector<int64_t> fsp(W + 1);
     fsp[0] = 0;
@@ -676,11 +747,13 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
       PHFEM_CUDA(ctx[i], cudaMemcpyAsync(cfine[i], s.coords, sizeof(double) * 2 * nC, cudaMemcpyDeviceToDevice, R.st(i)));
       if (last && nN) PHFEM_TRY(upload(ctx[i], neu_ids, &neud));
       int32_t Ef = 0, nneu = 0;
-      PHFEM_TRY(phfem_dist_level_count(ctx[i], &s.part, s.E0, (const int32_t*)sdbuf[i], last ? neud : nullptr,
-                                       last ? nN : 0, last ? 1 : 0, &Ef, &nneu, &plans[i]));
+      phfem_dist_local loc{s.elements, s.ee, s.elo, s.ehi, W == 1 ? 1 : 0, 0};
+      PHFEM_TRY(phfem_dist_level_count_ex(ctx[i], &s.part, s.E0, (const int32_t*)sdbuf[i], local_mode ? &loc : nullptr,
+                                          last ? neud : nullptr, last ? nN : 0, last ? 1 : 0, &Ef, &nneu, &plans[i]));
       dfree(ctx[i], neud);
       cnt[i] = {Ef, 2 * (int64_t)s.part.n_boundary, nneu};
     }
+  tr("level count");
     std::vector<int64_t> cg;
     PHFEM_TRY(allgather_host(R, cnt, cg));
     std::vector<int32_t> fE0s(W + 1, 0), fB0s(W + 1, 0);
@@ -702,8 +775,14 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
       memset(&fpart[i], 0, sizeof(phfem_topology));
       phfem_csr Cl;
       memset(&Cl, 0, sizeof Cl);
-      PHFEM_TRY(phfem_dist_level_run(ctx[i], plans[i], s.coords, (int32_t)nC, (int32_t)fsp[r], (int32_t)fsp[r + 1],
-                                     (int32_t)nE, E0f, nnz0, &fpart[i], rk[i], cfine[i], last ? &Cl : nullptr));
+      if (last) {  // the classification's retained arrays too (global rows / ids)
+        s.Lr = (int32_t)(cg[3 * r] - 2 * cg[3 * r + 2]);
+        PHFEM_TRY(dalloc(ctx[i], &s.rpos, std::max<int64_t>(cg[3 * r], 1)));
+        PHFEM_TRY(dalloc(ctx[i], &s.redges, std::max(s.Lr, 1)));
+      }
+      PHFEM_TRY(phfem_dist_level_run_ex(ctx[i], plans[i], s.coords, (int32_t)nC, (int32_t)fsp[r], (int32_t)fsp[r + 1],
+                                        (int32_t)nE, E0f, nnz0, last ? (int32_t)R0 : 0, &fpart[i], rk[i], cfine[i],
+                                        last ? &Cl : nullptr, s.rpos, s.redges));
       plans[i] = nullptr;
       if (last) {
         s.C = Cl;
@@ -711,25 +790,27 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
         s.R0 = (int32_t)R0;
       }
     }
+  tr("level run");
     // 3. group starts into the element owners' slot arrays
     std::vector<void*> gsbuf, grbuf;
     std::vector<void**> gspeers, grpeers;
     {
       std::vector<size_t> b4(nl), b1(nl);
       for (int i = 0; i < nl; ++i) {
-        b4[i] = 12 * (size_t)own(S[i]);
-        b1[i] = 3 * (size_t)own(S[i]);
+        b4[i] = no_remote ? 0 : 12 * (size_t)own(S[i]);
+        b1[i] = no_remote ? 0 : 3 * (size_t)own(S[i]);
       }
       PHFEM_TRY(window(R, "gs", b4, gsbuf, gspeers));
       PHFEM_TRY(window(R, "grk", b1, grbuf, grpeers));
     }
-    for (int i = 0; i < nl; ++i) {
+    for (int i = 0; i < nl && !no_remote; ++i) {
       RS& s = S[i];
-      PHFEM_TRY(phfem_dist_start_p2p(ctx[i], &s.part, fpart[i].node_edge_start, (int32_t)(nC + s.E0 - fsp[s.r]),
-                                     rk[i], espd[i], W, s.r, (int32_t* const*)gspeers[i], (uint8_t* const*)grpeers[i],
-                                     remote[i]));
+      PHFEM_TRY(phfem_dist_start_p2p_ex(ctx[i], &s.part, fpart[i].node_edge_start, (int32_t)(nC + s.E0 - fsp[s.r]),
+                                        rk[i], espd[i], W, s.r, (int32_t* const*)gspeers[i],
+                                        (uint8_t* const*)grpeers[i], remote[i], local_mode));
     }
     PHFEM_TRY(fence(R));
+  tr("start");
     // 4. children, fine elem_edge, midpoints of the own elements' edges
     for (int i = 0; i < nl; ++i) {
       RS& s = S[i];
@@ -737,8 +818,11 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
       int32_t *kids = nullptr, *fee = nullptr;
       PHFEM_TRY(dalloc(ctx[i], &kids, 12 * (int64_t)std::max(n, 1)));
       PHFEM_TRY(dalloc(ctx[i], &fee, 12 * (int64_t)std::max(n, 1)));
-      PHFEM_TRY(phfem_dist_children_slots(ctx[i], s.elements, s.ee, n, (const int32_t*)gsbuf[i],
-                                          (const uint8_t*)grbuf[i], (int32_t)nC, cfine[i], kids, fee));
+      // midpoints of the edges this rank owns: written by its level kernel
+      PHFEM_TRY(phfem_dist_children_slots_ex(ctx[i], s.elements, s.ee, n, (const int32_t*)gsbuf[i],
+                                             (const uint8_t*)grbuf[i], (int32_t)nC, E0s[s.r], E0s[s.r + 1],
+                                             local_mode ? fpart[i].node_edge_start : nullptr,
+                                             (int32_t)(nC + s.E0 - fsp[s.r]), rk[i], cfine[i], kids, fee));
       phfem_topology_release(ctx[i], &s.part);
       s.part = fpart[i];
       dfree(ctx[i], rk[i]);
@@ -752,6 +836,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
       s.elo *= 4;
       s.ehi *= 4;
     }
+  tr("children");
     // boundary lists bisected (refine.cpp:39-50)
     {
       std::vector<int32_t> nd, nn;
@@ -822,50 +907,86 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     Btot = fB0s[W];
   }
 
+  tr("levels done");
   // ---- last level: classification, C, bD, blocks, load = b + LN
-  std::vector<int32_t> ids;
-  PHFEM_TRY(resolve(ids));
+  PHFEM_TRY(resolve_enqueue());
   const int nD = (int)hdir.size() / 2, nN = (int)hneu.size() / 2;
-  std::vector<std::vector<int64_t>> Lv(nl);
-  std::vector<phfem_classification> cls(nl);
-  std::vector<std::vector<int32_t>> neu_pos(nl), neu_loc(nl);
+  // the blocks + load next: the host waits for the ids and enqueues the
+  // classification / bD / Neumann tables while the element pass runs
+  std::vector<phfem_mesh> mv(nl);
+  for (int i = 0; i < nl; ++i) {
+    RS& s = S[i];
+    phfem_dist_rank_out& o = outs[i];
+    memset(&mv[i], 0, sizeof(phfem_mesh));
+    mv[i].coords = s.coords;
+    mv[i].elements = s.elements;
+    mv[i].nC = (int32_t)nC;
+    mv[i].nE = own(s);
+    const int64_t n = std::max<int64_t>(own(s), 1);
+    PHFEM_TRY(dalloc(ctx[i], &o.B, 9 * n));
+    PHFEM_TRY(dalloc(ctx[i], &o.D, 9 * n));
+    PHFEM_TRY(dalloc(ctx[i], &o.M, 9 * n));
+    PHFEM_TRY(dalloc(ctx[i], &o.M0, 9 * n));
+    PHFEM_TRY(dalloc(ctx[i], &o.load, 3 * n));
+    if (own(s)) PHFEM_TRY(phfem_dist_volume_start(ctx[i], &mv[i], coeffs, f, t, o.B, o.D, o.M, o.M0, o.load));
+    if (c->local && nl > 1 && own(s))  // emulated ranks share contexts: one error block each time
+      PHFEM_TRY(phfem_dist_volume_finish(ctx[i]));
+  }
+  tr("volume enqueued");
+  std::vector<int32_t> ids;
+  PHFEM_TRY(resolve_wait(ids));
+  // the rank's id lists and Neumann table positions
+  std::vector<std::vector<int32_t>> dl(nl), neu_loc(nl);
+  std::vector<int32_t*> dld(nl), nld(nl), fulld(nl);
   for (int i = 0; i < nl; ++i) {
     RS& s = S[i];
     const int Er = s.part.E;
-    std::vector<int32_t> dl;
+    std::vector<int32_t> full(std::max(nN, 1), -1);
     for (int k = 0; k < nD; ++k)
-      if (ids[k] >= 0 && ids[k] - s.E0 >= 0 && ids[k] - s.E0 < Er) dl.push_back(ids[k] - s.E0);
+      if (ids[k] >= 0 && ids[k] - s.E0 >= 0 && ids[k] - s.E0 < Er) dl[i].push_back(ids[k] - s.E0);
     for (int k = 0; k < nN; ++k) {
       const int v = ids[nD + k];
       if (v >= 0 && v - s.E0 >= 0 && v - s.E0 < Er) {
-        neu_pos[i].push_back(k);
         neu_loc[i].push_back(v - s.E0);
+        full[k] = v - s.E0;
       }
     }
-    int32_t *dld = nullptr, *nld = nullptr;
-    PHFEM_TRY(upload(ctx[i], dl, &dld));
-    PHFEM_TRY(upload(ctx[i], neu_loc[i], &nld));
-    memset(&cls[i], 0, sizeof(phfem_classification));
-    const bool fused = s.R0 >= 0;
-    PHFEM_TRY(phfem_dist_classify_ex(ctx[i], &s.part, s.E0, dld, (int32_t)dl.size(), nld,
-                                     (int32_t)neu_loc[i].size(), fused ? s.R0 : 0, fused ? s.E0 : 0, &cls[i]));
-    outs[i].cls = cls[i];  // owned by the output from here (released with it on error)
-    dfree(ctx[i], dld);
-    dfree(ctx[i], nld);
-    Lv[i] = {cls[i].L};
+    PHFEM_TRY(upload(ctx[i], dl[i], &dld[i]));
+    PHFEM_TRY(upload(ctx[i], neu_loc[i], &nld[i]));
+    PHFEM_TRY(upload(ctx[i], full, &fulld[i]));
   }
-  std::vector<int64_t> Lg;
-  PHFEM_TRY(allgather_host(R, Lv, Lg));
-  int64_t Ltot = 0;
-  for (int r = 0; r < W; ++r) Ltot += Lg[r];
-  bool dup = false;
+  tr("lists");
+  bool dup = false;  // a Neumann pair listed twice (global list; phfem_dist_neumann_apply's order)
   {
     std::vector<int32_t> nv(ids.begin() + nD, ids.end());
     std::sort(nv.begin(), nv.end());
     dup = std::adjacent_find(nv.begin(), nv.end()) != nv.end();
   }
+  std::vector<std::vector<int64_t>> Lv(nl);
+  std::vector<phfem_classification> cls(nl);
+  for (int i = 0; i < nl; ++i) {
+    RS& s = S[i];
+    memset(&cls[i], 0, sizeof(phfem_classification));
+    if (s.rpos) {  // retained arrays from the fused level kernel
+      PHFEM_TRY(phfem_dist_classify_given(ctx[i], &s.part, dld[i], (int32_t)dl[i].size(), nld[i],
+                                          (int32_t)neu_loc[i].size(), s.rpos, s.redges, s.Lr, &cls[i]));
+      s.rpos = s.redges = nullptr;  // owned by the classification now
+      cls[i].flags = dup ? PHFEM_CLS_DUP_NEUMANN : 0;
+    } else {
+      PHFEM_TRY(phfem_dist_classify_ex(ctx[i], &s.part, s.E0, dld[i], (int32_t)dl[i].size(), nld[i],
+                                       (int32_t)neu_loc[i].size(), 0, 0, &cls[i]));
+    }
+    outs[i].cls = cls[i];  // owned by the output from here (released with it on error)
+    dfree(ctx[i], dld[i]);
+    dfree(ctx[i], nld[i]);
+    Lv[i] = {cls[i].L};
+  }
+  tr("classified");
+  std::vector<int64_t> Lg;
+  PHFEM_TRY(allgather_host(R, Lv, Lg));
+  int64_t Ltot = 0;
+  for (int r = 0; r < W; ++r) Ltot += Lg[r];
   std::vector<void*> tables(nl);
-  std::vector<phfem_mesh> mv(nl);
   for (int i = 0; i < nl; ++i) {
     RS& s = S[i];
     phfem_dist_rank_out& o = outs[i];
@@ -875,11 +996,6 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     const int64_t nnz0 = 4 * R0 - 2 * ((int64_t)s.B0 - N0);  // retained boundary rows hold 2 entries
     if (s.R0 >= 0 && s.R0 != R0)
       return set_error(ctx[i], PHFEM_ERR_MISMATCH, "dist: level offsets disagree with the classification");
-    memset(&mv[i], 0, sizeof(phfem_mesh));
-    mv[i].coords = s.coords;
-    mv[i].elements = s.elements;
-    mv[i].nC = (int32_t)nC;
-    mv[i].nE = own(s);
     if (!s.have_C) {  // no refinement: C from the sort-built part (columns 3 m, m global)
       phfem_mesh mc = mv[i];
       mc.nE = (int32_t)nE;
@@ -893,28 +1009,19 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
       if (cls[i].L && s.E0) PHFEM_TRY(phfem_dist_add_offset(ctx[i], cls[i].retained_edges, cls[i].L, s.E0, 0));
       if (nnz0) PHFEM_TRY(phfem_dist_add_offset(ctx[i], s.C.row_ptr, (int64_t)s.C.rows + 1, (int32_t)nnz0, 0));
     }
-    const int64_t n = std::max<int64_t>(own(s), 1);
-    PHFEM_TRY(dalloc(ctx[i], &o.B, 9 * n));
-    PHFEM_TRY(dalloc(ctx[i], &o.D, 9 * n));
-    PHFEM_TRY(dalloc(ctx[i], &o.M, 9 * n));
-    PHFEM_TRY(dalloc(ctx[i], &o.M0, 9 * n));
-    PHFEM_TRY(dalloc(ctx[i], &o.load, 3 * n));
-    if (own(s)) PHFEM_TRY(phfem_assemble_volume_load(ctx[i], &mv[i], coeffs, f, t, o.B, o.D, o.M, o.M0, o.load));
     // Neumann: the owners publish {a, b, t_plus, led}; element owners add b + LN
     int32_t* tb = nullptr;
     PHFEM_TRY(dalloc(ctx[i], &tb, 4 * (int64_t)std::max(nN, 1)));
     PHFEM_CUDA(ctx[i], cudaMemsetAsync(tb, 0, sizeof(int32_t) * 4 * std::max(nN, 1), R.st(i)));
-    if (nN) {
-      std::vector<int32_t> full(nN, -1);
-      for (size_t k = 0; k < neu_pos[i].size(); ++k) full[neu_pos[i][k]] = neu_loc[i][k];
-      int32_t* fd = nullptr;
-      PHFEM_TRY(upload(ctx[i], full, &fd));
-      PHFEM_TRY(phfem_dist_neumann_table(ctx[i], &s.part, 0, fd, nN, tb));
-      dfree(ctx[i], fd);
-    }
+    if (nN) PHFEM_TRY(phfem_dist_neumann_table(ctx[i], &s.part, 0, fulld[i], nN, tb));
+    dfree(ctx[i], fulld[i]);
     tables[i] = tb;
   }
+  tr("bd+tables");
   if (nN) PHFEM_TRY(allreduce_dev(R, tables, 4 * (int64_t)nN, kSum));
+  if (!(c->local && nl > 1))  // the element pass's errors (degenerate element, non-finite load)
+    for (int i = 0; i < nl; ++i)
+      if (own(S[i])) PHFEM_TRY(phfem_dist_volume_finish(ctx[i]));
   for (int i = 0; i < nl; ++i) {
     RS& s = S[i];
     phfem_dist_rank_out& o = outs[i];
@@ -979,7 +1086,10 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     for (int r = 0; r < S[i].r; ++r) R0 += Lg[r];
     outs[i].R0 = (int32_t)R0;
   }
-  return R.sync_all();
+  tr("outputs");
+  const phfem_status st = R.sync_all();
+  tr("synchronised");
+  return st;
 }
 
 }  // namespace
@@ -987,7 +1097,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
 PHFEM_API phfem_status phfem_dist_pipeline(phfem_dist_comm* c, phfem_ctx** ctxs, const phfem_mesh* meshes,
                                            int32_t nC_all, int32_t nE_all, int32_t levels,
                                            const phfem_coeffs* coeffs, const phfem_field* f, const phfem_field* g,
-                                           const phfem_field* uD, double t, int32_t hist_sample,
+                                           const phfem_field* uD, double t, int32_t hist_sample, int32_t flags,
                                            phfem_dist_rank_out* outs) {
   if (!c || !ctxs || !meshes || !coeffs || !f || !g || !uD || !outs || levels < 0 || levels > 8)
     return PHFEM_ERR_INVALID_ARGUMENT;
@@ -1002,7 +1112,8 @@ PHFEM_API phfem_status phfem_dist_pipeline(phfem_dist_comm* c, phfem_ctx** ctxs,
     memset(&s.part, 0, sizeof s.part);
     memset(&s.C, 0, sizeof s.C);
   }
-  const phfem_status st = dist_pipeline(R, meshes, nC_all, nE_all, levels, coeffs, f, g, uD, t, hist_sample, outs, S);
+  const phfem_status st =
+      dist_pipeline(R, meshes, nC_all, nE_all, levels, coeffs, f, g, uD, t, hist_sample, flags, outs, S);
   if (st != PHFEM_OK) {
     // leave nothing behind: partial per-rank state and outputs
     cudaDeviceSynchronize();
@@ -1013,6 +1124,8 @@ PHFEM_API phfem_status phfem_dist_pipeline(phfem_dist_comm* c, phfem_ctx** ctxs,
       if (s.own_ee) dfree(R.ctx[i], s.ee);
       if (s.own_elements) dfree(R.ctx[i], s.elements);
       if (s.own_coords) dfree(R.ctx[i], s.coords);
+      dfree(R.ctx[i], s.rpos);
+      dfree(R.ctx[i], s.redges);
       phfem_dist_rank_out_release(R.ctx[i], &outs[i]);
     }
     if (!c->message.empty() && R.ctx[0]->message.empty()) R.ctx[0]->message = c->message;

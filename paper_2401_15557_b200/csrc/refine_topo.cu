@@ -81,10 +81,16 @@ struct LvArgs {
   // indices l+1, l+2, the opposite vertex, -} (phfem_dist_side_apply) instead
   // of gathers from elem_edge / elements of every parent element
   const int4* side;
+  // local mode (side records of the rank's own element slots not stored):
+  // those elements' rows / elem_edge [own_hi - own_lo][3] from own_el / own_ee
+  const int32_t* own_el;
+  const int32_t* own_ee;
+  int own_lo, own_hi;
   // distributed level with the fine offsets known up front: global ids
   // written directly (fine edge ids in the lists and node_edge_start, C row
   // pointers) — no re-basing pass; 0 on one GPU
   int f_off, nnz_off;
+  int r_off;  // global retained row of the rank's first row (distributed fused classification)
   // exclusive per-tile prefixes (k_rl_tile_init / k_rl_tile_count + scans):
   // fine edges, parent boundary edges, parent Neumann edges before the tile
   const int32_t* tileF;
@@ -173,6 +179,20 @@ __global__ void k_rl_tile_init(int E, int eb, int ntiles, const int32_t* __restr
   }
 }
 
+// side record {partner at l+1, partner at l+2, opposite vertex, -} of parent
+// edge le in element t (local index l, sd 0 t_plus / 1 t_minus): the stored
+// record, or in local mode a gather from the rank's own element arrays
+__device__ __forceinline__ int4 side_of(const int4* __restrict__ side, int64_t le, int sd, int t, int l,
+                                        const int32_t* __restrict__ own_el, const int32_t* __restrict__ own_ee,
+                                        int own_lo, int own_hi) {
+  if (own_el && t >= own_lo && t < own_hi) {
+    const int64_t b = 3 * (int64_t)(t - own_lo);
+    return make_int4(__ldg(own_ee + b + (l == 2 ? 0 : l + 1)), __ldg(own_ee + b + (l == 0 ? 2 : l - 1)),
+                     __ldg(own_el + b + l), 0);
+  }
+  return side[2 * le + sd];
+}
+
 __device__ __forceinline__ void warp_add(int32_t* ctr, int key, int v) {
   const unsigned g = __match_any_sync(__activemask(), key);
   if ((int)lane_id() == __ffs(g) - 1) atomicAdd(ctr + key, v * __popc(g));
@@ -235,15 +255,15 @@ __device__ __forceinline__ LvGat lv_load_gat(const LvArgs& a, const LvRec& r, bo
   g.pj1 = g.pj2 = g.qk1 = g.qk2 = 0;
   g.vop = g.vom = 0;
   const int le = (int)(blockIdx.x * kLvT + threadIdx.x);
-  if (a.side) {  // distributed: the element owners' side records, coalesced
+  if (a.side) {  // distributed: the element owners' side records, coalesced (local mode: own slots gathered)
     if (valid) {
-      const int4 sp = a.side[2 * (int64_t)le];
+      const int4 sp = side_of(a.side, le, 0, r.el.x, r.l, a.own_el, a.own_ee, a.own_lo, a.own_hi);
       g.pj1 = sp.x;
       g.pj2 = sp.y;
       g.vop = sp.z;
     }
     if (valid && r.el.y >= 0) {
-      const int4 sm = a.side[2 * (int64_t)le + 1];
+      const int4 sm = side_of(a.side, le, 1, r.el.y, r.l2, a.own_el, a.own_ee, a.own_lo, a.own_hi);
       g.qk1 = sm.x;
       g.qk2 = sm.y;
       g.vom = sm.z;
@@ -415,12 +435,12 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
     }
     if (kFull) {
       const int rr = s.rr[i];
-      if (o.rpos) o.rpos[f] = rr < 0 ? -1 : off_rp + (rr >> 16);
+      if (o.rpos) o.rpos[f] = rr < 0 ? -1 : a.r_off + off_rp + (rr >> 16);
       if (rr >= 0) {
         const int rp = off_rp + (rr >> 16);
         const int rs = off_rs + (rr & 0xffff);
         const double len = s.len[i];
-        if (o.redges) o.redges[rp] = f;
+        if (o.redges) o.redges[rp] = a.f_off + f;
         o.row_ptr[rp] = a.nnz_off + rs;
         // columns {0,1,2} \ {local}, ascending: T+ DOFs, then T- DOFs
         const int c0 = lp == 0 ? 1 : 0, c1 = lp == 2 ? 1 : 2;
@@ -915,15 +935,24 @@ PHFEM_API phfem_status phfem_dist_refine_level(phfem_ctx* ctx, const phfem_topol
 namespace phfem {
 // partners < e per parent edge, summed per 128-edge tile (tile of le = le / kLvT)
 __global__ void k_rl_tile_count_side(const int4* __restrict__ side, const int32_t* __restrict__ edge_elements,
-                                     int E, int eb, int32_t* __restrict__ tileF) {
+                                     const int32_t* __restrict__ ltp, const int32_t* __restrict__ ltm,
+                                     const int32_t* __restrict__ own_el, const int32_t* __restrict__ own_ee,
+                                     int own_lo, int own_hi, int E, int eb, int32_t* __restrict__ tileF) {
   for (int64_t le0 = (int64_t)blockIdx.x * blockDim.x; le0 < E; le0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t le = le0 + threadIdx.x;
     int c = 0;
     if (le < E) {
       const int e = eb + (int)le;
-      const int4 sp = side[2 * le];
-      c = (abs_edge(sp.x) < e) + (abs_edge(sp.y) < e);
-      if (edge_elements[2 * le + 1] >= 0) {
+      // local mode: the rank's own elements were counted by the element pass
+      // (k_rl_tile_count over them); only the other ranks' sides here
+      const int2 el = reinterpret_cast<const int2*>(edge_elements)[le];
+      const bool lp = own_el && el.x >= own_lo && el.x < own_hi;
+      const bool lm = own_el && el.y >= own_lo && el.y < own_hi;
+      if (!lp) {
+        const int4 sp = side[2 * le];
+        c = (abs_edge(sp.x) < e) + (abs_edge(sp.y) < e);
+      }
+      if (el.y >= 0 && !lm) {
         const int4 sm = side[2 * le + 1];
         c += (abs_edge(sm.x) < e) + (abs_edge(sm.y) < e);
       }
@@ -942,6 +971,9 @@ __global__ void __launch_bounds__(256) k_dist_children_slots(const int32_t* __re
                                                              const int32_t* __restrict__ elem_edge,
                                                              const int32_t* __restrict__ gs,
                                                              const uint8_t* __restrict__ grk, int nE, int nc,
+                                                             int own_lo, int own_hi,
+                                                             const int32_t* __restrict__ fine_nes, int nes_off,
+                                                             const uint8_t* __restrict__ rk_own,
                                                              double2* __restrict__ coords,
                                                              int4* __restrict__ out_elems,
                                                              int4* __restrict__ out_ee) {
@@ -959,11 +991,17 @@ __global__ void __launch_bounds__(256) k_dist_children_slots(const int32_t* __re
         P[j] = __ldg(elements + 3 * m + j);
         sg[j] = __ldg(elem_edge + 3 * m + j);
         e[j] = abs_edge(sg[j]);
-        G[j] = __ldg(gs + 3 * m + j);
-        R[j] = __ldg(grk + 3 * m + j);
+        if (fine_nes && e[j] >= own_lo && e[j] < own_hi) {  // local mode: the rank's own edge
+          G[j] = __ldg(fine_nes + (e[j] - own_lo) + nes_off);
+          R[j] = __ldg(rk_own + (e[j] - own_lo));
+        } else {
+          G[j] = __ldg(gs + 3 * m + j);
+          R[j] = __ldg(grk + 3 * m + j);
+        }
       }
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {  // midpoint of the edge opposite P_j
+      for (int j = 0; j < 3; ++j) {  // midpoint of the edge opposite P_j (the owner's level wrote its own)
+        if (e[j] >= own_lo && e[j] < own_hi) continue;
         const double2 pa = __ldg(coords + P[j == 2 ? 0 : j + 1]), pb = __ldg(coords + P[j == 0 ? 2 : j - 1]);
         coords[nc + e[j]] = midpt(pa, pb);
       }
@@ -1019,6 +1057,7 @@ struct phfem_dist_level_plan {
   phfem_topology ppart;
   int32_t E0p;
   const int32_t* side;
+  phfem_dist_local local;  // elements == NULL: every slot has a side record
   int64_t ntiles;
   int32_t* tiles;
   uint32_t* nbits;
@@ -1026,9 +1065,10 @@ struct phfem_dist_level_plan {
   bool with_C;
 };
 
-PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
-                                              const int32_t* side, const int32_t* neu_parent_ids, int32_t nN_parent,
-                                              int with_C, int32_t* Ef_out, int32_t* nneu_out, void** plan_out) {
+PHFEM_API phfem_status phfem_dist_level_count_ex(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                                 const int32_t* side, const phfem_dist_local* local,
+                                                 const int32_t* neu_parent_ids, int32_t nN_parent, int with_C,
+                                                 int32_t* Ef_out, int32_t* nneu_out, void** plan_out) {
   if (!ctx || !ppart || !Ef_out || !nneu_out || !plan_out || E0p < 0) return PHFEM_ERR_INVALID_ARGUMENT;
   *plan_out = nullptr;
   if (nN_parent > 0 && !neu_parent_ids) return PHFEM_ERR_INVALID_ARGUMENT;
@@ -1040,6 +1080,14 @@ PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topolo
   pl->ppart = *ppart;
   pl->E0p = E0p;
   pl->side = side;
+  memset(&pl->local, 0, sizeof pl->local);
+  if (local && local->ehi > local->elo) {
+    if (!local->elements || !local->elem_edge) {
+      delete pl;
+      return PHFEM_ERR_INVALID_ARGUMENT;
+    }
+    pl->local = *local;
+  }
   pl->ntiles = ntiles;
   pl->with_C = with_C != 0;
   auto fail = [&](phfem_status st) {
@@ -1071,10 +1119,19 @@ PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topolo
           (int)E, E0p, (int)ntiles, ppart->boundary_edges, ppart->n_boundary, pl->nbits, tileF, tileB, tileN);
       ctx->launches++;
     }
-    KTimer kt(ctx, "k_rl_tile_count");
-    k_rl_tile_count_side<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        reinterpret_cast<const int4*>(side), ppart->edge_elements, (int)E, E0p, tileF);
-    ctx->launches++;
+    if (pl->local.elements) {  // the rank's own elements: element pass (coalesced), as on one GPU
+      KTimer kt(ctx, "k_rl_tile_count");
+      k_rl_tile_count<<<grid_for(pl->local.ehi - pl->local.elo, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          pl->local.elem_edge, pl->local.ehi - pl->local.elo, E0p, (int)E, tileF);
+      ctx->launches++;
+    }
+    if (!pl->local.elements || !pl->local.no_remote) {
+      KTimer kt(ctx, "k_rl_tile_count_side");
+      k_rl_tile_count_side<<<grid_for(E, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          reinterpret_cast<const int4*>(side), ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus,
+          pl->local.elements, pl->local.elem_edge, pl->local.elo, pl->local.ehi, (int)E, E0p, tileF);
+      ctx->launches++;
+    }
   }
   if (cudaGetLastError() != cudaSuccess) return fail(set_error(ctx, PHFEM_ERR_CUDA, "level count launch failed"));
   if ((st = scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total)) != PHFEM_OK) return fail(st);
@@ -1092,13 +1149,21 @@ PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topolo
   return PHFEM_OK;
 }
 
+PHFEM_API phfem_status phfem_dist_level_count(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
+                                              const int32_t* side, const int32_t* neu_parent_ids, int32_t nN_parent,
+                                              int with_C, int32_t* Ef_out, int32_t* nneu_out, void** plan_out) {
+  return phfem_dist_level_count_ex(ctx, ppart, E0p, side, nullptr, neu_parent_ids, nN_parent, with_C, Ef_out,
+                                   nneu_out, plan_out);
+}
+
 // Run half: the level kernel with the rank's fine offsets (f_off: first
 // global fine edge id; nnz_off: first C entry) written straight into the
 // fine lists, node_edge_start and C's row pointers; frees the plan.
-PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc,
-                                            int32_t node_lo, int32_t node_hi, int32_t nE_all, int32_t f_off,
-                                            int32_t nnz_off, phfem_topology* out, uint8_t* rk, double* coords_fine,
-                                            phfem_csr* C) {
+PHFEM_API phfem_status phfem_dist_level_run_ex(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc,
+                                               int32_t node_lo, int32_t node_hi, int32_t nE_all, int32_t f_off,
+                                               int32_t nnz_off, int32_t r_off, phfem_topology* out, uint8_t* rk,
+                                               double* coords_fine, phfem_csr* C, int32_t* retained_pos,
+                                               int32_t* retained_edges) {
   phfem_dist_level_plan* pl = (phfem_dist_level_plan*)plan;
   if (!ctx || !pl || !out) return PHFEM_ERR_INVALID_ARGUMENT;
   memset(out, 0, sizeof(*out));
@@ -1109,7 +1174,8 @@ PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const do
   phfem_status st = PHFEM_OK;
   if ((E > 0 && (!coords || !rk || !coords_fine)) || node_lo < 0 || node_hi < node_lo ||
       (E > 0 && (int64_t)node_hi != (int64_t)nc + E0p + E) || (E > 0 && node_lo > nc + E0p) ||
-      4 * (int64_t)nE_all >= (int64_t(1) << 31) || (C != nullptr) != pl->with_C)
+      4 * (int64_t)nE_all >= (int64_t(1) << 31) || (C != nullptr) != pl->with_C ||
+      (retained_pos != nullptr) != (retained_edges != nullptr) || (retained_pos && !C) || r_off < 0)
     st = PHFEM_ERR_INVALID_ARGUMENT;
   const int64_t ntiles = pl->ntiles;
   int32_t *tileF = pl->tiles, *tileB = pl->tiles + (ntiles + 1), *tileN = pl->tiles + 2 * (ntiles + 1);
@@ -1161,6 +1227,10 @@ PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const do
     a.ltp = ppart->local_in_tplus;
     a.ltm = ppart->local_in_tminus;
     a.side = reinterpret_cast<const int4*>(pl->side);
+    a.own_el = pl->local.elements;
+    a.own_ee = pl->local.elem_edge;
+    a.own_lo = pl->local.elo;
+    a.own_hi = pl->local.ehi;
     a.coords = (const double2*)coords;
     a.E = (int)E;
     a.nc = nc;
@@ -1169,6 +1239,7 @@ PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const do
     a.nlo = node_lo;
     a.f_off = f_off;
     a.nnz_off = nnz_off;
+    a.r_off = r_off;
     a.tileF = tileF;
     a.tileB = tileB;
     LvOut o;
@@ -1191,6 +1262,8 @@ PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const do
       o.row_ptr = C->row_ptr;
       o.col = C->col_idx;
       o.val = C->values;
+      o.rpos = retained_pos;      // global rows (r_off) / global edge ids (f_off)
+      o.redges = retained_edges;
       st = launch_level<true>(ctx, a, o, nt);
     } else {
       st = launch_level<false>(ctx, a, o, nt);
@@ -1200,6 +1273,14 @@ PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const do
   dfree(ctx, pl->tiles);
   delete pl;
   return st;
+}
+
+PHFEM_API phfem_status phfem_dist_level_run(phfem_ctx* ctx, void* plan, const double* coords, int32_t nc,
+                                            int32_t node_lo, int32_t node_hi, int32_t nE_all, int32_t f_off,
+                                            int32_t nnz_off, phfem_topology* out, uint8_t* rk, double* coords_fine,
+                                            phfem_csr* C) {
+  return phfem_dist_level_run_ex(ctx, plan, coords, nc, node_lo, node_hi, nE_all, f_off, nnz_off, 0, out, rk,
+                                 coords_fine, C, nullptr, nullptr);
 }
 
 PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_topology* ppart, int32_t E0p,
@@ -1215,16 +1296,26 @@ PHFEM_API phfem_status phfem_dist_refine_level_side(phfem_ctx* ctx, const phfem_
   return phfem_dist_level_run(ctx, plan, coords, nc, node_lo, node_hi, nE_all, 0, 0, out, rk, coords_fine, C);
 }
 
-PHFEM_API phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements,
-                                                 const int32_t* elem_edge, int32_t n, const int32_t* gs,
-                                                 const uint8_t* grk, int32_t nc, double* coords_fine,
-                                                 int32_t* children, int32_t* fine_elem_edge) {
-  if (!ctx || (n && (!elements || !elem_edge || !gs || !grk || !coords_fine || !children || !fine_elem_edge)))
+PHFEM_API phfem_status phfem_dist_children_slots_ex(phfem_ctx* ctx, const int32_t* elements,
+                                                    const int32_t* elem_edge, int32_t n, const int32_t* gs,
+                                                    const uint8_t* grk, int32_t nc, int32_t own_lo, int32_t own_hi,
+                                                    const int32_t* fine_nes, int32_t nes_off, const uint8_t* rk,
+                                                    double* coords_fine, int32_t* children, int32_t* fine_elem_edge) {
+  if (!ctx || (n && (!elements || !elem_edge || !gs || !grk || !coords_fine || !children || !fine_elem_edge)) ||
+      (fine_nes && own_hi > own_lo && !rk))
     return PHFEM_ERR_INVALID_ARGUMENT;
   if (n > 0)
     PHFEM_LAUNCH(ctx, "k_dist_children_slots", k_dist_children_slots<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0,
                                                                        ctx->stream>>>(
-        elements, elem_edge, gs, grk, n, nc, (double2*)coords_fine, reinterpret_cast<int4*>(children),
-        reinterpret_cast<int4*>(fine_elem_edge)));
+        elements, elem_edge, gs, grk, n, nc, own_lo, own_hi, fine_nes, nes_off, rk, (double2*)coords_fine,
+        reinterpret_cast<int4*>(children), reinterpret_cast<int4*>(fine_elem_edge)));
   return PHFEM_OK;
+}
+
+PHFEM_API phfem_status phfem_dist_children_slots(phfem_ctx* ctx, const int32_t* elements,
+                                                 const int32_t* elem_edge, int32_t n, const int32_t* gs,
+                                                 const uint8_t* grk, int32_t nc, double* coords_fine,
+                                                 int32_t* children, int32_t* fine_elem_edge) {
+  return phfem_dist_children_slots_ex(ctx, elements, elem_edge, n, gs, grk, nc, 0, 0, nullptr, 0, nullptr,
+                                      coords_fine, children, fine_elem_edge);
 }

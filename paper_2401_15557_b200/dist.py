@@ -418,13 +418,14 @@ class CudaRankOps:
                                                  self.p(grk)))
         return gs, grk
 
-    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine):
+    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine, own=(0, 0)):
+        """own: the rank's parent edge range (their midpoints: its level kernel's)"""
         n = int(elements.shape[0])
         kids = self.empty((max(4 * n, 1), 3))
         ee = self.empty((max(4 * n, 1), 3))
-        self._ck(self.lib.phfem_dist_children_slots(self.ctx.ptr, self.p(elements), self.p(elem_edge), n,
-                                                    self.p(gs), self.p(grk), nc, self.p(coords_fine),
-                                                    self.p(kids), self.p(ee)))
+        self._ck(self.lib.phfem_dist_children_slots_ex(self.ctx.ptr, self.p(elements), self.p(elem_edge), n,
+                                                       self.p(gs), self.p(grk), nc, int(own[0]), int(own[1]), None,
+                                                       0, None, self.p(coords_fine), self.p(kids), self.p(ee)))
         return kids[:4 * n], ee[:4 * n]
 
     # -- peer-window forms (phfem_dist_side_p2p / _start_p2p) ---------------------------
@@ -938,7 +939,8 @@ def _refine_sort_free(states, comm, nC, nE, splits, per, Etot, Btot, esplits, nD
     comm.close_windows()
     tr("start")
     for s, (gs, grk), i in zip(states, bufs, ids):
-        kids, ee = s.ops.children_slots(s.elements, s.elem_edge, gs, grk, nC, s.coords_fine)
+        kids, ee = s.ops.children_slots(s.elements, s.elem_edge, gs, grk, nC, s.coords_fine,
+                                        own=(int(edge_splits[s.rank]), int(edge_splits[s.rank + 1])))
         s.dirichlet, s.neumann = _bisect(s.dirichlet, i[:nD], nC), _bisect(s.neumann, i[nD:], nC)
         s.elements, s.elem_edge = kids, ee
         s.elo, s.ehi = 4 * s.elo, 4 * s.ehi

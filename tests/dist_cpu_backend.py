@@ -295,7 +295,7 @@ class NumpyRankOps:
         grk[r[:, 0] - 3 * elo] = r[:, 2]
         return gs, grk
 
-    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine):
+    def children_slots(self, elements, elem_edge, gs, grk, nc, coords_fine, own=(0, 0)):
         el = elements.numpy().reshape(-1, 3).astype(np.int64)
         ee = elem_edge.numpy().reshape(-1, 3).astype(np.int64)
         cf = coords_fine.numpy()
@@ -305,6 +305,8 @@ class NumpyRankOps:
             e = np.where(sg >= 0, sg, ~sg)
             G, R = gs[3 * m:3 * m + 3], grk[3 * m:3 * m + 3]
             for j in range(3):
+                if own[0] <= e[j] < own[1]:
+                    continue  # the owner's level pass wrote it
                 a, b = P[(j + 1) % 3], P[(j + 2) % 3]
                 cf[nc + e[j]] = [0.5 * (cf[a][0] + cf[b][0]), 0.5 * (cf[a][1] + cf[b][1])]
             I = []

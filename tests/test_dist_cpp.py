@@ -33,13 +33,13 @@ def _rank_meshes(capi, dm, W):
     return out
 
 
-def run_cpp(ctx, hm, W, levels, args, hist_sample=1):
+def run_cpp(ctx, hm, W, levels, args, hist_sample=1, flags=0):
     from paper_2401_15557_b200 import capi, dist
     dm = capi.DeviceMesh.upload(ctx, hm)
     comm = capi.DistComm.local_ranks(W)
     try:
         outs = capi.dist_pipeline(comm, [ctx] * W, _rank_meshes(capi, dm, W), hm.nC, hm.nE, levels, *args,
-                                  hist_sample=hist_sample)
+                                  hist_sample=hist_sample, flags=flags)
         got = dist.concat_slices([o.rank_slice() for o in outs])
         for o in outs:
             o.release()
@@ -52,12 +52,16 @@ def run_cpp(ctx, hm, W, levels, args, hist_sample=1):
 @pytest.mark.gpu
 @pytest.mark.parametrize("W", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("name,make,levels", CASES, ids=[c[0] for c in CASES])
-def test_cpp_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels):
+@pytest.mark.parametrize("mode", ["local", "windows"])
+def test_cpp_emulated_ranks_equal_single_gpu(ctx, W, name, make, levels, mode):
+    """local: slots whose element and edge share a rank are gathered from its
+    own arrays (the default); windows: every slot's record through the peer
+    windows (PHFEM_DIST_NO_LOCAL)"""
     from paper_2401_15557_b200 import capi
     hm = make()
     args = G.config_fields(2)
     ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args, flags=capi.PIPE_GENERIC_EG).download()
-    check_equal(run_cpp(ctx, hm, W, levels, args), ref)
+    check_equal(run_cpp(ctx, hm, W, levels, args, flags=0 if mode == "local" else capi.DIST_NO_LOCAL), ref)
 
 
 @pytest.mark.gpu
@@ -135,7 +139,8 @@ def test_cpp_nccl_single_rank(ctx):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("W", [8])
-def test_cpp_emulated_ranks_at_scale(ctx, W):
+@pytest.mark.parametrize("mode", ["local", "windows"])
+def test_cpp_emulated_ranks_at_scale(ctx, W, mode):
     """the L10 -> L11 sharded step (8.4 M triangles, sampled key histogram) over
     W emulated ranks == the single-GPU pipeline, every output bit for bit"""
     from paper_2401_15557_b200 import capi
@@ -152,7 +157,7 @@ def test_cpp_emulated_ranks_at_scale(ctx, W):
     res = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), 1, *args)
     ref = res.download()
     res.release()
-    check_equal(run_cpp(ctx, hm, W, 1, args, hist_sample=8), ref)
+    check_equal(run_cpp(ctx, hm, W, 1, args, hist_sample=8, flags=0 if mode == "local" else capi.DIST_NO_LOCAL), ref)
 
 
 def test_cpp_local_comm_host_state():
@@ -162,3 +167,21 @@ def test_cpp_local_comm_host_state():
     c.close()
     with pytest.raises(ValueError):
         capi.DistComm.local_ranks(0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,levels", [(1, 0), (1, 1), (2, 1)])
+def test_cpp_degenerate_element_error(ctx, W, levels):
+    """the element pass's error (deferred past the classification / bD /
+    Neumann-table enqueue) is the reference's: two nodes of an element at one
+    point"""
+    from paper_2401_15557_b200 import capi
+    hm = O.refine_levels(G.square_2tri(), 2)
+    a, b = int(hm.elements[3][0]), int(hm.elements[3][1])
+    coords = hm.coords.copy()
+    coords[b] = coords[a]
+    bad = capi.HostMesh(coords, hm.elements, hm.dirichlet, hm.neumann)
+    with pytest.raises(capi.PhfemError, match="degenerate"):
+        run_cpp(ctx, bad, W, levels, G.config_fields(2))
+    ref = capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *G.config_fields(2)).download()
+    check_equal(run_cpp(ctx, hm, W, levels, G.config_fields(2)), ref)
