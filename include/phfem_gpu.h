@@ -748,6 +748,14 @@ phfem_status phfem_dist_comm_nccl(const void* uid128, int32_t rank, int32_t worl
                                   phfem_dist_comm** out);
 void phfem_dist_comm_destroy(phfem_dist_comm* comm);
 const char* phfem_dist_comm_message(const phfem_dist_comm* comm);
+/* Exchange statistics (cost model, tools/dist_model_cpp.py): enable (and
+ * clear); read returns the number of phases, names[k] (valid until the next
+ * pipeline call) and bytes[k][W] = bytes each rank received in phase k
+ * (peer-window records stored into it, the other ranks' parts of
+ * all-gathers, 2 (W-1)/W of all-reduced buffers; NCCL: what this rank sent
+ * to each).  Enabled statistics synchronise after every exchange.           */
+phfem_status phfem_dist_comm_set_stats(phfem_dist_comm* comm, int enable);
+int phfem_dist_comm_stats(const phfem_dist_comm* comm, int max_phases, const char** names, int64_t* bytes);
 #define PHFEM_DIST_NO_LOCAL 1 /* flags: every slot's side record / group start through the windows */
 phfem_status phfem_dist_pipeline(phfem_dist_comm* comm, phfem_ctx** ctxs, const phfem_mesh* meshes, int32_t nC_all,
                                  int32_t nE_all, int32_t levels, const phfem_coeffs* coeffs, const phfem_field* f,

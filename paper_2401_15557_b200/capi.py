@@ -192,7 +192,7 @@ EXPORTED = [
     "phfem_dist_comm_destroy", "phfem_dist_comm_message", "phfem_dist_pipeline", "phfem_dist_rank_out_release",
     "phfem_dist_level_run_ex", "phfem_dist_classify_given", "phfem_dist_children_slots_ex",
     "phfem_dist_side_p2p_ex", "phfem_dist_start_p2p_ex", "phfem_dist_level_count_ex",
-    "phfem_dist_volume_start", "phfem_dist_volume_finish",
+    "phfem_dist_volume_start", "phfem_dist_volume_finish", "phfem_dist_comm_set_stats", "phfem_dist_comm_stats",
 ]
 DIST_NO_LOCAL = 1
 PIPE_GENERIC_EG = 1
@@ -355,6 +355,8 @@ def load_library(path: str = LIB_PATH):
         "phfem_dist_volume_start": (C.c_int, [vp, P(phfem_mesh), P(phfem_coeffs), P(phfem_field), dbl, vp, vp, vp,
                                               vp, vp]),
         "phfem_dist_volume_finish": (C.c_int, [vp]),
+        "phfem_dist_comm_set_stats": (C.c_int, [vp, C.c_int]),
+        "phfem_dist_comm_stats": (C.c_int, [vp, C.c_int, P(C.c_char_p), P(i64)]),
         "phfem_dist_side_p2p_ex": (C.c_int, [vp, vp, vp, i32, vp, i32, i32, vp, vp, C.c_int]),
         "phfem_dist_start_p2p_ex": (C.c_int, [vp, P(phfem_topology), vp, i32, vp, vp, i32, i32, vp, vp, vp,
                                               C.c_int]),
@@ -964,6 +966,17 @@ class DistComm:
         if st != OK:
             raise PhfemError(st, f"phfem_dist_comm_nccl(rank {rank} of {world}) failed with status {st}")
         return cls(p, world, False)
+
+    def set_stats(self, enable: bool):
+        self.lib.phfem_dist_comm_set_stats(self.ptr, 1 if enable else 0)
+
+    def stats(self) -> dict:
+        """{phase: [bytes received per rank]} since set_stats(True)"""
+        n = 64
+        names = (C.c_char_p * n)()
+        b = (C.c_int64 * (n * self.world))()
+        k = self.lib.phfem_dist_comm_stats(self.ptr, n, names, b)
+        return {names[i].decode(): [int(b[i * self.world + r]) for r in range(self.world)] for i in range(k)}
 
     def close(self):
         if self.ptr:

@@ -128,6 +128,13 @@ struct phfem_dist_comm {
   void* pin = nullptr;  // pinned host staging of the resolved boundary ids
   size_t pin_cap = 0;
   cudaEvent_t ev = nullptr;
+  // exchange statistics (phfem_dist_comm_stats): bytes each local rank
+  // RECEIVED per phase — peer-window records the other ranks stored into it,
+  // the other ranks' parts of all-gathers, 2 (W-1)/W of all-reduced buffers
+  bool stats = false;
+  std::string phase = "input";
+  std::vector<std::string> phase_names;
+  std::vector<std::vector<int64_t>> recv;
   std::string message;
 };
 
@@ -170,10 +177,42 @@ struct Ranks {
   }
 };
 
+void stat_add(Comm* c, int rank, int64_t bytes) {
+  if (!c->stats || bytes == 0) return;
+  size_t k = 0;
+  while (k < c->phase_names.size() && c->phase_names[k] != c->phase) ++k;
+  if (k == c->phase_names.size()) {
+    c->phase_names.push_back(c->phase);
+    c->recv.emplace_back(c->world, 0);
+  }
+  c->recv[k][rank] += bytes;
+}
+// peer-window stores: remote[i][d] records of rec_bytes each went to rank d
+phfem_status stat_windows(Ranks& R, const std::vector<int32_t*>& remote, int64_t rec_bytes) {
+  Comm* c = R.c;
+  if (!c->stats) return PHFEM_OK;
+  std::vector<int32_t> h(c->world);
+  for (int i = 0; i < R.n(); ++i) {
+    DC_CUDA(c, R.ctx[i], cudaMemcpy(h.data(), remote[i], sizeof(int32_t) * c->world, cudaMemcpyDeviceToHost));
+    for (int d = 0; d < c->world; ++d)
+      if (c->local) stat_add(c, d, h[d] * rec_bytes);
+      else if (d != c->rank) stat_add(c, d, h[d] * rec_bytes);  // (NCCL: what this rank sent)
+  }
+  return PHFEM_OK;
+}
+void stat_collective(Ranks& R, int64_t bytes_per_rank, bool reduce) {
+  Comm* c = R.c;
+  for (int i = 0; i < R.n(); ++i) {
+    const int r = c->local ? i : c->rank;
+    stat_add(c, r, reduce ? 2 * (c->world - 1) * bytes_per_rank / c->world : (c->world - 1) * bytes_per_rank);
+  }
+}
+
 // all-gather of n int64 per rank to the host (every local rank sees all W*n)
 phfem_status allgather_host(Ranks& R, const std::vector<std::vector<int64_t>>& in, std::vector<int64_t>& out) {
   Comm* c = R.c;
   const int n = (int)in[0].size();
+  stat_collective(R, 8 * (int64_t)n, false);
   out.assign((size_t)c->world * n, 0);
   if (c->local || c->world == 1) {
     for (int r = 0; r < c->world; ++r)
@@ -196,6 +235,7 @@ phfem_status allgather_host(Ranks& R, const std::vector<std::vector<int64_t>>& i
 enum RedOp { kSum, kMax, kMinU64 };
 phfem_status allreduce_dev(Ranks& R, const std::vector<void*>& bufs, int64_t n, RedOp op) {
   Comm* c = R.c;
+  stat_collective(R, (op == kMinU64 ? 8 : 4) * n, true);
   if (n == 0 || c->world == 1) return PHFEM_OK;
   if (!c->local) {
     if (op == kMinU64)
@@ -229,6 +269,7 @@ phfem_status allreduce_dev(Ranks& R, const std::vector<void*>& bufs, int64_t n, 
 // all-gather of `bytes` per rank into out[W * bytes] on every local rank (device)
 phfem_status allgather_dev(Ranks& R, const std::vector<const void*>& in, size_t bytes, const std::vector<void*>& out) {
   Comm* c = R.c;
+  stat_collective(R, (int64_t)bytes, false);
   if (c->local || c->world == 1) {
     PHFEM_TRY(R.sync_all());
     for (int d = 0; d < R.n(); ++d)
@@ -434,6 +475,24 @@ PHFEM_API void phfem_dist_comm_destroy(phfem_dist_comm* c) {
 
 PHFEM_API const char* phfem_dist_comm_message(const phfem_dist_comm* c) { return c ? c->message.c_str() : ""; }
 
+PHFEM_API phfem_status phfem_dist_comm_set_stats(phfem_dist_comm* c, int enable) {
+  if (!c) return PHFEM_ERR_INVALID_ARGUMENT;
+  c->stats = enable != 0;
+  c->phase_names.clear();
+  c->recv.clear();
+  return PHFEM_OK;
+}
+
+PHFEM_API int phfem_dist_comm_stats(const phfem_dist_comm* c, int max_phases, const char** names, int64_t* bytes) {
+  if (!c) return -1;
+  const int n = std::min<int>(max_phases, (int)c->phase_names.size());
+  for (int k = 0; k < n; ++k) {
+    names[k] = c->phase_names[k].c_str();
+    for (int r = 0; r < c->world; ++r) bytes[(int64_t)k * c->world + r] = c->recv[k][r];
+  }
+  return n;
+}
+
 PHFEM_API void phfem_dist_rank_out_release(phfem_ctx* ctx, phfem_dist_rank_out* o) {
   if (!ctx || !o) return;
   phfem_topology_release(ctx, &o->part);
@@ -466,10 +525,12 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
   const bool trace = getenv("PHFEM_DIST_TRACE") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
   auto tr = [&](const char* what) {
+    c->phase = std::string("after ") + what;
     if (trace)
       fprintf(stderr, "[dist-trace] %-28s %8.3f ms\n", what,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
   };
+  c->phase = "start";
   // local mode: slots whose element and edge are this rank's move through no window
   const int local_mode = (flags & PHFEM_DIST_NO_LOCAL) ? 0 : 1;
   const int nl = R.n(), W = c->world;
@@ -577,6 +638,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     PHFEM_TRY(phfem_dist_scatter_p2p(ctx[i], S[i].elements, own(S[i]), S[i].elo, (int32_t)nC, (int32_t)nE, cursor[i],
                                      bspd[i], W, S[i].r, (uint64_t* const*)itpeers[i], remote[i]));
   PHFEM_TRY(fence(R));
+  PHFEM_TRY(stat_windows(R, remote, 8));
   tr("scatter");
   std::vector<int32_t*> pairs(nl);
   std::vector<int64_t> npairs(nl);
@@ -620,6 +682,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
     PHFEM_TRY(phfem_dist_pairs_p2p(ctx[i], pairs[i], npairs[i], S[i].E0, espd[i], W, S[i].r,
                                    (int32_t* const*)eepeers[i], remote[i]));
   PHFEM_TRY(fence(R));
+  PHFEM_TRY(stat_windows(R, remote, 4));
   for (int i = 0; i < nl; ++i) {
     dfree(ctx[i], pairs[i]);
     S[i].ee = (int32_t*)eebuf[i];  // the window (persistent; copied out when it is an output)
@@ -730,6 +793,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
                                          (int32_t* const*)sdpeers[i], remote[i], local_mode));
     }
     PHFEM_TRY(fence(R));
+    if (!no_remote) PHFEM_TRY(stat_windows(R, remote, 16));
   tr("side");
     // 2. level count -> fine offsets (all-gathered) -> level run with global ids
     std::vector<int64_t> fsp(W + 1);
@@ -810,6 +874,7 @@ phfem_status dist_pipeline(Ranks& R, const phfem_mesh* meshes, int32_t nC_all, i
                                         (uint8_t* const*)grpeers[i], remote[i], local_mode));
     }
     PHFEM_TRY(fence(R));
+    if (!no_remote) PHFEM_TRY(stat_windows(R, remote, 5));
   tr("start");
     // 4. children, fine elem_edge, midpoints of the own elements' edges
     for (int i = 0; i < nl; ++i) {

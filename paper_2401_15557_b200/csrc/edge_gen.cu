@@ -203,8 +203,17 @@ __device__ __forceinline__ void eg_slots(const EgOut& o, int32_t e, int64_t s0, 
     if (own0) o.self_ee[s0 - o.self_lo3] = e;
     if (s1 >= 0 && own1) o.self_ee[s1 - o.self_lo3] = ~e;
     const int k = (own0 ? 0 : 1) + (own1 ? 0 : 1);
-    if (k) {
-      int at = atomicAdd(o.npairs, k);
+    // slots of other ranks' elements: one cursor atomic per warp, not per edge
+    const unsigned am = __activemask();
+    const unsigned b1 = __ballot_sync(am, k >= 1), b2 = __ballot_sync(am, k == 2);
+    const int total = __popc(b1) + __popc(b2);
+    if (total) {
+      const int leader = __ffs(am) - 1;
+      int base = 0;
+      if ((int)lane_id() == leader) base = atomicAdd(o.npairs, total);
+      base = __shfl_sync(am, base, leader);
+      const unsigned lt = lanemask_lt();
+      int at = base + __popc(b1 & lt) + __popc(b2 & lt);
       if (!own0) o.pairs[at++] = make_int2((int)s0, e);
       if (!own1) o.pairs[at] = make_int2((int)s1, ~e);
     }
