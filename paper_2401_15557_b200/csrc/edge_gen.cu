@@ -571,6 +571,100 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
   }
 }
 
+// Column fast path (every node <= kColK occurrences — refined meshes have
+// <= 12): one thread per max node.  The counting-sort scatter puts node t's
+// j-th occurrence at col[j][t] (column-major: the threads of a warp touch
+// consecutive words at every step, no bank conflicts), the thread sorts its
+// column by insertion (<= 16 keys, ~6 on refined meshes), walks its runs
+// (the reference's two error checks, edges, boundary edges), and after one
+// packed block scan of (edges, boundary edges) per node emits its records at
+// their tile-local slots — no per-item rank loop, no neighbour pass, no
+// per-warp ballot pass (half the instructions of eg_tile_fast).
+#ifndef PHFEM_TILE_COL
+#define PHFEM_TILE_COL 1
+#endif
+constexpr int kColK = 16;
+static_assert(kColK * kTileNodes <= 2 * kTileCap + 4, "the columns alias buf1 / buf2");
+
+__device__ __forceinline__ void eg_tile_col(const EgParams& P, TileSmem& sm, int4* __restrict__ rec,
+                                            int32_t* __restrict__ tileE, int32_t* __restrict__ tileB,
+                                            const EgOut& out, phfem_dev_errors* err,
+                                            const uint64_t (&itr)[kTilePer], const int (&ndr)[kTilePer]) {
+  const int tid = threadIdx.x;
+  const int T = blockDim.x;
+  const int tile = sm.tile;
+  const int nsub = kTileNodes >> P.bs;
+  const int64_t s = sm.sbo[0];
+  const int n = sm.sbo[nsub] - (int)s;
+  const int ob = P.occ_bits;
+  const int lsh = ob + 1;
+  const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
+  uint64_t* col = sm.buf1;  // [kColK][kTileNodes], aliases buf1 / buf2
+  // scatter into the columns (sm.cur zeroed before the histogram)
+#pragma unroll
+  for (int k = 0; k < kTilePer; ++k) {
+    if (k * T >= n) break;  // block-uniform
+    if (tid + k * T < n) {
+      const int j = atomicAdd(&sm.cur[ndr[k]], 1);
+      col[j * kTileNodes + ndr[k]] = itr[k];
+    }
+  }
+  __syncthreads();
+  const int c = sm.cnt[tid];
+  uint64_t* my = col + tid;
+  // insertion sort of the node's occurrences; key = (min node, occurrence,
+  // dir) = the reference's stable order (the max-node bits are shared)
+  for (int i = 1; i < c; ++i) {
+    const uint64_t x = my[i * kTileNodes];
+    int j = i - 1;
+    uint64_t y = my[j * kTileNodes];
+    while (y > x) {
+      my[(j + 1) * kTileNodes] = y;
+      if (--j < 0) break;
+      y = my[j * kTileNodes];
+    }
+    my[(j + 1) * kTileNodes] = x;
+  }
+  // runs of equal min node = edges (edge_topology.cpp:82-99 checks)
+  const uint64_t v_glob = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + tid;
+  int ne = 0, nb = 0;
+  for (int i = 0; i < c;) {
+    const uint64_t f = my[i * kTileNodes];
+    const uint64_t lo = (f >> lsh) & lomask;
+    int len = 1;
+    while (i + len < c && ((my[(i + len) * kTileNodes] >> lsh) & lomask) == lo) ++len;
+    if (len > 2 || (len == 2 && ((f ^ my[(i + 1) * kTileNodes]) & 1ull) == 0))
+      atomicMin(&err->topo, (v_glob << 33) | (lo << 2) | (len > 2 ? 0ull : (2ull | (f & 1ull))));
+    ++ne;
+    nb += len == 1;
+    i += len;
+  }
+  unsigned long long agg;
+  const unsigned long long ex = block_exclusive_scan(((unsigned long long)ne << 32) | nb, sm.scan, &agg);
+  int32_t e = (int32_t)(ex >> 32);                // tile-local edge index of the node's first edge
+  int32_t bl = (int32_t)(ex & 0xffffffffu);       // tile-local boundary edges before it
+  const int64_t v_me = (int64_t)tile * kTileNodes + tid;
+  if (v_me < P.nC) out.node_edge_start[v_me] = e;  // tile-local (k_eg_emit adds the tile offset)
+  for (int i = 0; i < c;) {
+    const uint64_t f = my[i * kTileNodes];
+    const uint64_t lo = (f >> lsh) & lomask;
+    const uint64_t g = i + 1 < c ? my[(i + 1) * kTileNodes] : 0ull;
+    const bool two = i + 1 < c && ((g >> lsh) & lomask) == lo;
+    int len = two ? 2 : 1;
+    while (i + len < c && ((my[(i + len) * kTileNodes] >> lsh) & lomask) == lo) ++len;  // (error case)
+    const bool neu = !two && out.neu_keys && neu_pair_has(out, (int)lo, (int32_t)v_glob);
+    if (neu) atomicAdd(&out.tileN[tile], 1);
+    rec[s + e] = eg_record(tid, bl, (int32_t)lo, f, two ? g : 0ull, two, ob, neu);
+    ++e;
+    bl += !two;
+    i += len;
+  }
+  if (tid == 0) {
+    tileE[tile] = (int32_t)(agg >> 32);
+    tileB[tile] = (int32_t)(agg & 0xffffffffu);
+  }
+}
+
 // P.nb here = number of tiles; boff has one entry per bucket (+1).
 __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile(const uint64_t* __restrict__ items,
                                                           const int32_t* __restrict__ boff,
@@ -586,6 +680,7 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
   if (tid == 0) sm.tile = blockIdx.x;
   sm.cnt[tid] = 0;
   sm.nedge[tid] = 0;
+  sm.cur[tid] = 0;  // the column path's per-node cursors
   __syncthreads();
   const int nsub = kTileNodes >> P.bs;
   for (int i = tid; i <= nsub; i += blockDim.x)
@@ -625,7 +720,12 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
         atomicAdd(&sm.cnt[ndr[k]], 1);
       }
     }
-    fast = __syncthreads_and(sm.cnt[tid] <= 32);
+    const int cme = sm.cnt[tid];
+    fast = __syncthreads_and(cme <= 32);
+    if (PHFEM_TILE_COL && fast && __syncthreads_and(cme <= kColK)) {
+      eg_tile_col(P, sm, rec, tileE, tileB, out, err, itr, ndr);
+      return;
+    }
   }
   if (fast) {
     eg_tile_fast(items, P, sm, rec, tileE, tileB, out, err, itr, ndr);
