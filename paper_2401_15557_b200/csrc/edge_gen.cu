@@ -282,7 +282,7 @@ constexpr int kTileThreads = 256;
 #define PHFEM_TILE_PER_NODE 10
 #endif
 #ifndef PHFEM_TILE_MIN_BLOCKS
-#define PHFEM_TILE_MIN_BLOCKS 1  // (measured: 5 blocks spill, 8 items per node overflow the fast path: both slower)
+#define PHFEM_TILE_MIN_BLOCKS 4  // 4 x 256 threads at <= 64 registers (5 blocks spill)
 #endif
 constexpr int kTileCap = PHFEM_TILE_PER_NODE * kTileNodes;  // items kept in SMEM (10 per node)
 
@@ -584,46 +584,35 @@ __device__ __forceinline__ void eg_tile_fast(const uint64_t* __restrict__ items,
 #define PHFEM_TILE_COL 1
 #endif
 constexpr int kColK = 16;
-static_assert(kColK * kTileNodes <= 2 * kTileCap + 4, "the columns alias buf1 / buf2");
+// row 0 of the aliased region: zero sentinels (no key is below 0), the
+// columns start at row 1
+static_assert((kColK + 1) * kTileNodes <= 2 * kTileCap + 4, "the columns alias buf1 / buf2");
 
 __device__ __forceinline__ void eg_tile_col(const EgParams& P, TileSmem& sm, int4* __restrict__ rec,
                                             int32_t* __restrict__ tileE, int32_t* __restrict__ tileB,
-                                            const EgOut& out, phfem_dev_errors* err,
-                                            const uint64_t (&itr)[kTilePer], const int (&ndr)[kTilePer]) {
+                                            const EgOut& out, phfem_dev_errors* err, const int c) {
   const int tid = threadIdx.x;
-  const int T = blockDim.x;
   const int tile = sm.tile;
-  const int nsub = kTileNodes >> P.bs;
   const int64_t s = sm.sbo[0];
-  const int n = sm.sbo[nsub] - (int)s;
   const int ob = P.occ_bits;
   const int lsh = ob + 1;
   const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
-  uint64_t* col = sm.buf1;  // [kColK][kTileNodes], aliases buf1 / buf2
-  // scatter into the columns (sm.cur zeroed before the histogram)
-#pragma unroll
-  for (int k = 0; k < kTilePer; ++k) {
-    if (k * T >= n) break;  // block-uniform
-    if (tid + k * T < n) {
-      const int j = atomicAdd(&sm.cur[ndr[k]], 1);
-      col[j * kTileNodes + ndr[k]] = itr[k];
-    }
-  }
-  __syncthreads();
-  const int c = sm.cnt[tid];
+  // node t's occurrences in column t of rows 1..c (k_eg_tile scattered them),
+  // row 0 = zero sentinels (no key is below 0)
+  uint64_t* col = sm.buf1 + kTileNodes;
   uint64_t* my = col + tid;
   // insertion sort of the node's occurrences; key = (min node, occurrence,
   // dir) = the reference's stable order (the max-node bits are shared)
   for (int i = 1; i < c; ++i) {
-    const uint64_t x = my[i * kTileNodes];
-    int j = i - 1;
-    uint64_t y = my[j * kTileNodes];
-    while (y > x) {
-      my[(j + 1) * kTileNodes] = y;
-      if (--j < 0) break;
-      y = my[j * kTileNodes];
+    uint64_t* q = my + i * kTileNodes;
+    const uint64_t x = *q;
+    uint64_t y = q[-kTileNodes];
+    while (y > x) {  // the zero sentinel row ends the walk
+      *q = y;
+      q -= kTileNodes;
+      y = q[-kTileNodes];
     }
-    my[(j + 1) * kTileNodes] = x;
+    *q = x;
   }
   // runs of equal min node = edges (edge_topology.cpp:82-99 checks)
   const uint64_t v_glob = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + tid;
@@ -700,32 +689,48 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
       const int p = tid + k * kTileThreads;
       itr[k] = p < n ? __ldg(items + s + p) : 0ull;
     }
+    const int64_t s_lo = s;
 #pragma unroll
     for (int k = 0; k < kTilePer; ++k) {
       if (k * kTileThreads >= n) break;
       const int p = tid + k * kTileThreads;
       ndr[k] = 0;
       if (p < n) {
-        int sub = 0;
-        if (nsub > 1) {
-          int lo = 0, hi = nsub - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sm.sbo[mid] - s <= p) lo = mid;
-            else hi = mid - 1;
-          }
-          sub = lo;
-        }
+        int sub = 0;  // sub-bucket of position p (nsub <= 256 >> bs, uniform trip count)
+        for (int m = 1; m < nsub; ++m) sub += p >= sm.sbo[m] - (int)s_lo;
         ndr[k] = (sub << P.bs) | (int)(itr[k] >> P.total_bits);
-        atomicAdd(&sm.cnt[ndr[k]], 1);
       }
     }
-    const int cme = sm.cnt[tid];
-    fast = __syncthreads_and(cme <= 32);
-    if (PHFEM_TILE_COL && fast && __syncthreads_and(cme <= kColK)) {
-      eg_tile_col(P, sm, rec, tileE, tileB, out, err, itr, ndr);
-      return;
+    int cme;
+    if (PHFEM_TILE_COL) {
+      // straight into the node columns: the per-node cursor is the histogram
+      uint64_t* col = sm.buf1 + kTileNodes;
+      sm.buf1[tid] = 0ull;  // sentinel row
+#pragma unroll
+      for (int k = 0; k < kTilePer; ++k) {
+        if (k * kTileThreads >= n) break;
+        if (tid + k * kTileThreads < n) {
+          const int j = atomicAdd(&sm.cur[ndr[k]], 1);
+          if (j < kColK) col[j * kTileNodes + ndr[k]] = itr[k];
+        }
+      }
+      __syncthreads();
+      cme = sm.cur[tid];
+      if (__syncthreads_and(cme <= kColK)) {
+        eg_tile_col(P, sm, rec, tileE, tileB, out, err, cme);
+        return;
+      }
+      sm.cnt[tid] = cme;  // the histogram for the paths below
+    } else {
+#pragma unroll
+      for (int k = 0; k < kTilePer; ++k) {
+        if (k * kTileThreads >= n) break;
+        if (tid + k * kTileThreads < n) atomicAdd(&sm.cnt[ndr[k]], 1);
+      }
+      __syncthreads();
+      cme = sm.cnt[tid];
     }
+    fast = __syncthreads_and(cme <= 32);
   }
   if (fast) {
     eg_tile_fast(items, P, sm, rec, tileE, tileB, out, err, itr, ndr);
