@@ -14,14 +14,16 @@
 //                       [max-node low bits | min node | occurrence index | dir]
 //                     and scattered into its bucket (warp-aggregated cursor)
 //   D  k_eg_tile      one CTA per tile of 256 max nodes (256 >> bs buckets):
-//                     counting sort by max node in SMEM, rank sort inside each
-//                     node's segment (the packed value orders by (max, min,
-//                     occurrence) = the reference's stable order), run
+//                     the items grouped by max node in SMEM, each node's
+//                     occurrences sorted (the packed value orders by (max,
+//                     min, occurrence) = the reference's stable order), run
 //                     detection with the reference's two error checks, one
 //                     16-byte record per edge at a tile-local slot (carrying
 //                     the tile-local boundary prefix) and per-tile edge /
-//                     boundary / Neumann counts.  Fast path (tile in SMEM,
-//                     every node <= 32 occurrences) and a general path
+//                     boundary / Neumann counts.  Column path (every node
+//                     <= 16 occurrences: one thread per node, per-node SMEM
+//                     columns, insertion sort), item-parallel fast path (<= 32:
+//                     counting sort + in-segment rank sort) and a general path
 //                     (global scratch for oversized tiles or segments).
 //   E  scans          of the per-tile counts (no look-back: tiny arrays)
 //   F  k_eg_emit      one CTA per tile: records -> edge_nodes, edge_elements,
