@@ -657,18 +657,13 @@ __device__ __forceinline__ void eg_tile_col(const EgParams& P, TileSmem& sm, int
 }
 
 // P.nb here = number of tiles; boff has one entry per bucket (+1).
-__global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile(const uint64_t* __restrict__ items,
-                                                          const int32_t* __restrict__ boff,
-                                                          int nbuckets, EgParams P, uint64_t* g1,
-                                                          uint64_t* g2, uint8_t* gnode,
-                                                          int4* __restrict__ rec,
-                                                          int32_t* __restrict__ tileE,
-                                                          int32_t* __restrict__ tileB, EgOut out,
-                                                          phfem_dev_errors* err) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
+__device__ __forceinline__ void eg_tile_body(TileSmem& sm, int tile, bool try_col,
+                                             const uint64_t* __restrict__ items, const int32_t* __restrict__ boff,
+                                             int nbuckets, const EgParams& P, uint64_t* g1, uint64_t* g2,
+                                             uint8_t* gnode, int4* __restrict__ rec, int32_t* __restrict__ tileE,
+                                             int32_t* __restrict__ tileB, const EgOut& out, phfem_dev_errors* err) {
   const int tid = threadIdx.x;
-  if (tid == 0) sm.tile = blockIdx.x;
+  if (tid == 0) sm.tile = tile;
   sm.cnt[tid] = 0;
   sm.nedge[tid] = 0;
   sm.cur[tid] = 0;  // the column path's per-node cursors
@@ -704,7 +699,7 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
       }
     }
     int cme;
-    if (PHFEM_TILE_COL) {
+    if (try_col) {
       // straight into the node columns: the per-node cursor is the histogram
       uint64_t* col = sm.buf1 + kTileNodes;
       sm.buf1[tid] = 0ull;  // sentinel row
@@ -744,6 +739,153 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
     eg_tile<true>(items, P, sm, g1, g2, gnode, rec, tileE, tileB, out, err);
   else
     eg_tile<false>(items, P, sm, g1, g2, gnode, rec, tileE, tileB, out, err);
+}
+
+// One tile per CTA, every path (PHFEM_TILE_SPLIT=0).
+__global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile(const uint64_t* __restrict__ items,
+                                                          const int32_t* __restrict__ boff,
+                                                          int nbuckets, EgParams P, uint64_t* g1,
+                                                          uint64_t* g2, uint8_t* gnode,
+                                                          int4* __restrict__ rec,
+                                                          int32_t* __restrict__ tileE,
+                                                          int32_t* __restrict__ tileB, EgOut out,
+                                                          phfem_dev_errors* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
+  eg_tile_body(sm, blockIdx.x, PHFEM_TILE_COL != 0, items, boff, nbuckets, P, g1, g2, gnode, rec, tileE, tileB,
+               out, err);
+}
+
+// The tiles k_eg_tile_col left (a node with > kColK occurrences): a
+// persistent grid over the device-side list, the item-parallel / general paths.
+__global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile_list(
+    const int32_t* __restrict__ list, const int32_t* __restrict__ count, const uint64_t* __restrict__ items,
+    const int32_t* __restrict__ boff, int nbuckets, EgParams P, uint64_t* g1, uint64_t* g2, uint8_t* gnode,
+    int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
+    phfem_dev_errors* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
+  const int nl = *count;
+  for (int w = blockIdx.x; w < nl; w += gridDim.x) {
+    eg_tile_body(sm, list[w], false, items, boff, nbuckets, P, g1, g2, gnode, rec, tileE, tileB, out, err);
+    __syncthreads();
+  }
+}
+
+// Column kernel (PHFEM_TILE_SPLIT=1, the default): only the column path, in
+// 30 KB of SMEM and 32 registers, without the register-staged items of the
+// other paths (7 resident CTAs instead of 4); a tile with a node of more than
+// kColK2 occurrences is handed to k_eg_tile_list.
+#ifndef PHFEM_TILE_SPLIT
+#define PHFEM_TILE_SPLIT 1
+#endif
+#ifndef PHFEM_COL_MIN_BLOCKS
+#define PHFEM_COL_MIN_BLOCKS 7
+#endif
+#ifndef PHFEM_COL_K
+#define PHFEM_COL_K 13  // occurrences per node (refined meshes: <= 12); 14 rows of 2 KB: 7 CTAs per SM
+#endif
+constexpr int kColK2 = PHFEM_COL_K;
+struct ColSmem {
+  uint64_t col[(kColK2 + 1) * kTileNodes];  // row 0: zero sentinels; node t's j-th occurrence at [j + 1][t]
+  int32_t cur[kTileNodes];
+  int32_t sbo[kTileNodes + 1];
+  unsigned long long scan[33];
+};
+
+__global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_col(
+    const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets, EgParams P,
+    int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
+    phfem_dev_errors* err, int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ColSmem& sm = *reinterpret_cast<ColSmem*>(smraw);
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  sm.cur[tid] = 0;
+  sm.col[tid] = 0ull;
+  const int nsub = kTileNodes >> P.bs;
+  for (int i = tid; i <= nsub; i += blockDim.x) sm.sbo[i] = boff[min(tile * nsub + i, nbuckets)];
+  __syncthreads();
+  const int s = sm.sbo[0];
+  const int n = sm.sbo[nsub] - s;
+  if (n > kColK2 * kTileNodes) {  // block-uniform
+    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = tile;
+    return;
+  }
+  for (int p = tid; p < n; p += kTileThreads) {
+    const uint64_t it = __ldg(items + s + p);
+    int sub = 0;
+    if (nsub > 1) {  // sub-bucket of position p
+      int lo = 0, hi = nsub - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sm.sbo[mid] - s <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      sub = lo;
+    }
+    const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
+    const int j = atomicAdd(&sm.cur[nd], 1);
+    if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it;
+  }
+  __syncthreads();
+  const int c = sm.cur[tid];
+  if (!__syncthreads_and(c <= kColK2)) {
+    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = tile;
+    return;
+  }
+  const int ob = P.occ_bits;
+  const int lsh = ob + 1;
+  const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
+  uint64_t* my = sm.col + kTileNodes + tid;
+  for (int i = 1; i < c; ++i) {  // insertion sort, the zero row ends every walk
+    uint64_t* q = my + i * kTileNodes;
+    const uint64_t x = *q;
+    uint64_t y = q[-kTileNodes];
+    while (y > x) {
+      *q = y;
+      q -= kTileNodes;
+      y = q[-kTileNodes];
+    }
+    *q = x;
+  }
+  const uint64_t v_glob = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + tid;
+  int ne = 0, nb = 0;
+  for (int i = 0; i < c;) {
+    const uint64_t f = my[i * kTileNodes];
+    const uint64_t lo = (f >> lsh) & lomask;
+    int len = 1;
+    while (i + len < c && ((my[(i + len) * kTileNodes] >> lsh) & lomask) == lo) ++len;
+    if (len > 2 || (len == 2 && ((f ^ my[(i + 1) * kTileNodes]) & 1ull) == 0))
+      atomicMin(&err->topo, (v_glob << 33) | (lo << 2) | (len > 2 ? 0ull : (2ull | (f & 1ull))));
+    ++ne;
+    nb += len == 1;
+    i += len;
+  }
+  unsigned long long agg;
+  const unsigned long long ex = block_exclusive_scan(((unsigned long long)ne << 32) | nb, sm.scan, &agg);
+  int32_t e = (int32_t)(ex >> 32);
+  int32_t bl = (int32_t)(ex & 0xffffffffu);
+  const int64_t v_me = (int64_t)tile * kTileNodes + tid;
+  if (v_me < P.nC) out.node_edge_start[v_me] = e;
+  for (int i = 0; i < c;) {
+    const uint64_t f = my[i * kTileNodes];
+    const uint64_t lo = (f >> lsh) & lomask;
+    const uint64_t g = i + 1 < c ? my[(i + 1) * kTileNodes] : 0ull;
+    const bool two = i + 1 < c && ((g >> lsh) & lomask) == lo;
+    int len = two ? 2 : 1;
+    while (i + len < c && ((my[(i + len) * kTileNodes] >> lsh) & lomask) == lo) ++len;
+    const bool neu = !two && out.neu_keys && neu_pair_has(out, (int)lo, (int32_t)v_glob);
+    if (neu) atomicAdd(&out.tileN[tile], 1);
+    rec[s + e] = eg_record(tid, bl, (int32_t)lo, f, two ? g : 0ull, two, ob, neu);
+    ++e;
+    bl += !two;
+    i += len;
+  }
+  if (tid == 0) {
+    tileE[tile] = (int32_t)(agg >> 32);
+    tileB[tile] = (int32_t)(agg & 0xffffffffu);
+  }
 }
 
 // E ------------------------------------------------------------------------
@@ -1051,9 +1193,24 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   EgParams PT = P;
   PT.nb = ntiles;
   const size_t smem = sizeof(TileSmem);
-  PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile, smem, "k_eg_tile smem opt-in"));
-  PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
-      items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+  if (PHFEM_TILE_SPLIT) {
+    // column kernel over every tile, then the list of tiles it handed back
+    int32_t* fb = nullptr;
+    PHFEM_TRY(dalloc(ctx, &fb, (int64_t)ntiles + 1));
+    PHFEM_CUDA(ctx, cudaMemsetAsync(fb, 0, sizeof(int32_t), ctx->stream));
+    const size_t csmem = sizeof(ColSmem);
+    PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_col, csmem, "k_eg_tile_col smem opt-in"));
+    PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile_col<<<ntiles, kTileThreads, csmem, ctx->stream>>>(
+        items, boff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb));
+    PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_list, smem, "k_eg_tile_list smem opt-in"));
+    PHFEM_LAUNCH(ctx, "k_eg_tile_list", k_eg_tile_list<<<ctx->num_sms * 4, kTileThreads, smem, ctx->stream>>>(
+        fb + 1, fb, items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+    dfree(ctx, fb);
+  } else {
+    PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile, smem, "k_eg_tile smem opt-in"));
+    PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
+        items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+  }
   PHFEM_TRY(scan_exclusive_i32(ctx, tileE, tileE, (int64_t)ntiles + 1, nullptr));
   PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, (int64_t)ntiles + 1, nullptr));
   if (fuse) {  // sizes of the classification / C before the emit pass writes them
