@@ -789,10 +789,14 @@ constexpr int kColK2 = PHFEM_COL_K;
 struct ColSmem {
   uint64_t col[(kColK2 + 1) * kTileNodes];  // row 0: zero sentinels; node t's j-th occurrence at [j + 1][t]
   int32_t cur[kTileNodes];
-  int32_t sbo[kTileNodes + 1];
+  int32_t sbo[kTileNodes / 2 + 1];  // bs >= 1: at most 128 sub-buckets per tile
   unsigned long long scan[33];
 };
 
+// Thread = node.  (Measured and dropped: slots ordered by occurrence count, so
+// that a warp's 32 nodes sort / walk equally many occurrences — an extra
+// histogram pass and the slot indirection cost more than the divergence they
+// remove: L12 tile 0.885 -> 0.990 ms.)
 __global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_col(
     const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets, EgParams P,
     int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
