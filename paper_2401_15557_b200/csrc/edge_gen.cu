@@ -843,15 +843,21 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_
   const uint64_t lomask = (1ull << P.lo_bits) - 1ull;
   uint64_t* my = sm.col + kTileNodes + tid;
   for (int i = 1; i < c; ++i) {  // insertion sort, the zero row ends every walk
-    uint64_t* q = my + i * kTileNodes;
-    const uint64_t x = *q;
-    uint64_t y = q[-kTileNodes];
-    while (y > x) {
-      *q = y;
-      q -= kTileNodes;
-      y = q[-kTileNodes];
+    uint64_t* r = my + (i - 1) * kTileNodes;
+    const uint64_t x = r[kTileNodes];
+    uint64_t y0 = *r;
+    // two shifts per trip with alternating registers: no copies of the
+    // loop-carried key (the load of the next one is hoisted above the store)
+    while (y0 > x) {
+      r[kTileNodes] = y0;
+      const uint64_t y1 = r[-kTileNodes];
+      r -= kTileNodes;
+      if (!(y1 > x)) break;
+      r[kTileNodes] = y1;
+      y0 = r[-kTileNodes];
+      r -= kTileNodes;
     }
-    *q = x;
+    r[kTileNodes] = x;
   }
   const uint64_t v_glob = (uint64_t)P.node_base + (uint64_t)tile * kTileNodes + tid;
   int ne = 0, nb = 0;
