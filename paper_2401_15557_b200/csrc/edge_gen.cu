@@ -41,6 +41,9 @@ struct EgParams {
   int lo_bits, occ_bits, total_bits, bs;
   int nb;
   int32_t node_base;  // first max node of the range (0 for a whole mesh)
+  // fixed-capacity bucket layout (0: contiguous): bucket b owns items
+  // [b fcap, b fcap + fill_b), tile t's records start at t nsub fcap
+  int32_t fcap;
 };
 
 static int bits_for(int64_t max_value) {  // bits to represent 0..max_value
@@ -116,6 +119,66 @@ __global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ 
         items[base + rank] = eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
       }
     }
+  }
+}
+
+// C (fixed-capacity layout, no count pass): every bucket owns kTileCap / nsub
+// slots, its cursor starts at b * fcap; the node-range check of the count
+// pass is made here (first bad element -> misc) and the fullest bucket's
+// fill is reported (counters[3]) — above fcap the caller falls back to the
+// counted layout.
+__global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restrict__ elements,
+                                                          EgParams P, int32_t* __restrict__ cursor,
+                                                          uint64_t* __restrict__ items, phfem_dev_errors* err) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t hl_mask = (1u << P.bs) - 1u;
+  unsigned fill_max = 0;
+  for (int64_t m0 = (int64_t)blockIdx.x * blockDim.x; m0 < P.nE; m0 += stride) {
+    const int64_t m = m0 + threadIdx.x;
+    bool valid = m < P.nE;
+    int t[3] = {0, 0, 0};
+    if (valid) {
+      t[0] = __ldg(elements + 3 * m);
+      t[1] = __ldg(elements + 3 * m + 1);
+      t[2] = __ldg(elements + 3 * m + 2);
+      if ((unsigned)t[0] >= (unsigned)P.nC || (unsigned)t[1] >= (unsigned)P.nC ||
+          (unsigned)t[2] >= (unsigned)P.nC) {
+        atomicMin(&err->misc, (unsigned long long)m);
+        valid = false;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      const int hi = a > b ? a : b;
+      const int lo = a > b ? b : a;
+      const unsigned key = valid ? ((unsigned)hi >> P.bs) : 0xffffffffu;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(grp) - 1;
+      int base = 0;
+      if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (valid) {
+        const int rank = __popc(grp & lanemask_lt());
+        const int64_t at = (int64_t)base + rank;
+        const int64_t end = ((int64_t)key + 1) * P.fcap;
+        if (at < end) {
+          const uint32_t occ = (uint32_t)(3 * m + s);
+          items[at] = eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
+        }
+        fill_max = max(fill_max, (unsigned)(at + 1 - (end - P.fcap)));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fill_max = max(fill_max, __shfl_xor_sync(0xffffffffu, fill_max, o));
+  if (lane_id() == 0 && fill_max) atomicMax(&err->counters[3], (unsigned long long)fill_max);
+}
+
+__global__ void k_eg_fixed_init(int32_t* __restrict__ boff, int32_t* __restrict__ cursor, int nb, int fcap) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+    boff[b] = b * fcap;
+    if (b < nb) cursor[b] = b * fcap;
   }
 }
 
@@ -669,8 +732,20 @@ __device__ __forceinline__ void eg_tile_body(TileSmem& sm, int tile, bool try_co
   sm.cur[tid] = 0;  // the column path's per-node cursors
   __syncthreads();
   const int nsub = kTileNodes >> P.bs;
-  for (int i = tid; i <= nsub; i += blockDim.x)
-    sm.sbo[i] = boff[min(sm.tile * nsub + i, nbuckets)];
+  if (P.fcap) {  // fixed layout, compacted by k_eg_tile_list: boff = the bucket fills
+    if (tid == 0) {
+      int at = tile * nsub * P.fcap;
+      for (int i = 0; i < nsub; ++i) {
+        sm.sbo[i] = at;
+        const int b = tile * nsub + i;
+        if (b < nbuckets) at += boff[b] - b * P.fcap;
+      }
+      sm.sbo[nsub] = at;
+    }
+  } else {
+    for (int i = tid; i <= nsub; i += blockDim.x)
+      sm.sbo[i] = boff[min(sm.tile * nsub + i, nbuckets)];
+  }
   __syncthreads();
   const int64_t s = sm.sbo[0];
   const int n = sm.sbo[nsub] - (int)s;
@@ -759,15 +834,37 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
 // The tiles k_eg_tile_col left (a node with > kColK occurrences): a
 // persistent grid over the device-side list, the item-parallel / general paths.
 __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile_list(
-    const int32_t* __restrict__ list, const int32_t* __restrict__ count, const uint64_t* __restrict__ items,
+    const int32_t* __restrict__ list, const int32_t* __restrict__ count, uint64_t* __restrict__ items,
     const int32_t* __restrict__ boff, int nbuckets, EgParams P, uint64_t* g1, uint64_t* g2, uint8_t* gnode,
     int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
     phfem_dev_errors* err) {
   extern __shared__ __align__(16) unsigned char smraw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
   const int nl = *count;
+  const int nsub = kTileNodes >> P.bs;
   for (int w = blockIdx.x; w < nl; w += gridDim.x) {
-    eg_tile_body(sm, list[w], false, items, boff, nbuckets, P, g1, g2, gnode, rec, tileE, tileB, out, err);
+    const int tile = list[w];
+    if (P.fcap) {
+      // fixed layout (boff = the bucket fills): close the gaps between the
+      // tile's sub-buckets so its items are contiguous (staged through SMEM:
+      // the ranges may overlap)
+      int at = boff[tile * nsub] - tile * nsub * P.fcap;
+      for (int i = 1; i < nsub; ++i) {
+        const int b = tile * nsub + i;
+        if (b >= nbuckets) break;
+        const int cnt = boff[b] - b * P.fcap;
+        const int64_t src = (int64_t)b * P.fcap, dst = (int64_t)tile * nsub * P.fcap + at;
+        if (src != dst && cnt > 0) {  // block-uniform
+          for (int p = threadIdx.x; p < cnt; p += blockDim.x) sm.buf1[p] = items[src + p];
+          __syncthreads();
+          for (int p = threadIdx.x; p < cnt; p += blockDim.x) items[dst + p] = sm.buf1[p];
+          __syncthreads();
+        }
+        at += cnt;
+      }
+      __syncthreads();
+    }
+    eg_tile_body(sm, tile, false, items, boff, nbuckets, P, g1, g2, gnode, rec, tileE, tileB, out, err);
     __syncthreads();
   }
 }
@@ -810,27 +907,45 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_
   const int nsub = kTileNodes >> P.bs;
   for (int i = tid; i <= nsub; i += blockDim.x) sm.sbo[i] = boff[min(tile * nsub + i, nbuckets)];
   __syncthreads();
-  const int s = sm.sbo[0];
-  const int n = sm.sbo[nsub] - s;
-  if (n > kColK2 * kTileNodes) {  // block-uniform
-    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = tile;
-    return;
-  }
-  for (int p = tid; p < n; p += kTileThreads) {
-    const uint64_t it = __ldg(items + s + p);
-    int sub = 0;
-    if (nsub > 1) {  // sub-bucket of position p
-      int lo = 0, hi = nsub - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sm.sbo[mid] - s <= p) lo = mid;
-        else hi = mid - 1;
+  int s;  // the tile's first record slot
+  if (P.fcap) {
+    // fixed layout (boff = the bucket fills): each sub-bucket read from its own slots
+    s = tile * nsub * P.fcap;
+    for (int sub = 0; sub < nsub; ++sub) {
+      const int b = tile * nsub + sub;
+      if (b >= nbuckets) break;
+      const int base = b * P.fcap;
+      const int cnt = sm.sbo[sub] - base;
+      for (int p = tid; p < cnt; p += kTileThreads) {
+        const uint64_t it = __ldg(items + base + p);
+        const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
+        const int j = atomicAdd(&sm.cur[nd], 1);
+        if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it;
       }
-      sub = lo;
     }
-    const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
-    const int j = atomicAdd(&sm.cur[nd], 1);
-    if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it;
+  } else {
+    s = sm.sbo[0];
+    const int n = sm.sbo[nsub] - s;
+    if (n > kColK2 * kTileNodes) {  // block-uniform
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = tile;
+      return;
+    }
+    for (int p = tid; p < n; p += kTileThreads) {
+      const uint64_t it = __ldg(items + s + p);
+      int sub = 0;
+      if (nsub > 1) {  // sub-bucket of position p
+        int lo = 0, hi = nsub - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.sbo[mid] - s <= p) lo = mid;
+          else hi = mid - 1;
+        }
+        sub = lo;
+      }
+      const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
+      const int j = atomicAdd(&sm.cur[nd], 1);
+      if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it;
+    }
   }
   __syncthreads();
   const int c = sm.cur[tid];
@@ -1103,10 +1218,15 @@ struct EgPre {
 };
 
 template <typename Source>
+#ifndef PHFEM_EG_FIXED
+#define PHFEM_EG_FIXED 1
+#endif
+// fixed_elements: the mesh's elements when the occurrences come from them —
+// then the fixed-capacity bucket layout (no count pass) is tried first
 static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source source,
                             phfem_topology* out, int2* pairs, const char* who,
                             const EgFuse* fuse = nullptr, const EgOwn* own = nullptr,
-                            const EgPre* pre = nullptr) {
+                            const EgPre* pre = nullptr, const int32_t* fixed_elements = nullptr) {
   const int64_t nC = P.nC;
   const int64_t cap_e = std::max<int64_t>(nd, 1);
   PHFEM_TRY(dalloc(ctx, &out->node_edge_start, nC + 1));
@@ -1134,21 +1254,14 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
   PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 2 * (ntiles + 1), ctx->stream));
 
   const int nsub = kTileNodes >> P.bs;
-  if (pre) {
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(boff, pre->boff, sizeof(int32_t) * ((int64_t)P.nb + 1), cudaMemcpyDeviceToDevice,
-                                    ctx->stream));
-  } else {
-    PHFEM_TRY(source(0, bcount, (uint64_t*)nullptr));
-    PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
-  }
-  PHFEM_LAUNCH(ctx, "k_eg_tile_max", k_eg_tile_max<<<grid_for(ntiles, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
-      boff, P.nb, nsub, ntiles, ctx->derr));
-  int32_t* cursor = bcount;  // reuse as scatter cursor
-  PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, boff, sizeof(int32_t) * P.nb, cudaMemcpyDeviceToDevice,
-                                  ctx->stream));
-  PHFEM_TRY(errors_fetch(ctx));
-  if (ctx->herr->misc != ~0ull) {
+  int32_t* cursor = bcount;  // the scatter cursors (fixed layout: also the bucket fills)
+  uint64_t* items = nullptr;
+  uint64_t *g1 = nullptr, *g2 = nullptr;
+  uint8_t* gnode = nullptr;
+  int4* rec = nullptr;
+  auto range_error = [&]() -> phfem_status {
     const long long m = (long long)ctx->herr->misc;
+    dfree(ctx, items); dfree(ctx, rec);
     dfree(ctx, bcount); dfree(ctx, boff); dfree(ctx, tiles);
     phfem_topology_release(ctx, out);
     if (pairs)
@@ -1156,22 +1269,62 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     return set_error(ctx, PHFEM_ERR_OUT_OF_RANGE,
                      "build_topology: element %lld has a node index outside 1..%lld", m + 1,
                      (long long)nC);
+  };
+  // Fixed-capacity layout first (elements as the source, column tile kernel):
+  // every bucket owns kTileCap / nsub item slots, so the scatter needs no
+  // count pass / scan; a bucket over its capacity (some tile could not be
+  // processed in SMEM anyway) falls back to the counted layout below.
+  const int fcap = kTileCap / nsub;
+  bool fixed = fixed_elements && !pre && PHFEM_EG_FIXED && PHFEM_TILE_SPLIT &&
+               (int64_t)P.nb * fcap < (int64_t(1) << 31) - kTileCap;
+  if (fixed) {
+    const int64_t capn = (int64_t)P.nb * fcap;
+    PHFEM_LAUNCH(ctx, "k_eg_fixed_init", k_eg_fixed_init<<<grid_for((int64_t)P.nb + 1, 256, ctx->num_sms * 4), 256, 0,
+                                                           ctx->stream>>>(boff, cursor, P.nb, fcap));
+    PHFEM_TRY(dalloc(ctx, &items, capn));
+    PHFEM_TRY(dalloc(ctx, &rec, capn));
+    P.fcap = fcap;
+    const int grid_e = grid_for(P.nE, 256, ctx->num_sms * 8);
+    PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter_fixed<<<grid_e, 256, 0, ctx->stream>>>(fixed_elements, P, cursor,
+                                                                                         items, ctx->derr));
+    PHFEM_TRY(errors_fetch(ctx));
+    if (ctx->herr->misc != ~0ull) return range_error();
+    if ((int64_t)ctx->herr->counters[3] > fcap) {  // a bucket over capacity: counted layout
+      dfree(ctx, items);
+      dfree(ctx, rec);
+      P.fcap = 0;
+      fixed = false;
+      PHFEM_CUDA(ctx, cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (P.nb + 1), ctx->stream));
+      PHFEM_TRY(errors_reset(ctx));
+    }
   }
-  const int64_t max_tile = (int64_t)ctx->herr->counters[3];
-
-  uint64_t* items = nullptr;
-  uint64_t *g1 = nullptr, *g2 = nullptr;
-  uint8_t* gnode = nullptr;
-  int4* rec = nullptr;
-  if (pre) items = pre->items;
-  else PHFEM_TRY(dalloc(ctx, &items, nd));
-  PHFEM_TRY(dalloc(ctx, &rec, nd));
-  if (max_tile > kTileCap) {  // some tile does not fit SMEM: global scratch
-    PHFEM_TRY(dalloc(ctx, &g1, nd));
-    PHFEM_TRY(dalloc(ctx, &g2, nd));
-    PHFEM_TRY(dalloc(ctx, &gnode, nd));
+  if (!fixed) {
+    if (pre) {
+      PHFEM_CUDA(ctx, cudaMemcpyAsync(boff, pre->boff, sizeof(int32_t) * ((int64_t)P.nb + 1), cudaMemcpyDeviceToDevice,
+                                      ctx->stream));
+    } else {
+      PHFEM_TRY(source(0, bcount, (uint64_t*)nullptr));
+      PHFEM_TRY(scan_exclusive_i32(ctx, bcount, boff, (int64_t)P.nb + 1, nullptr));
+    }
+    PHFEM_LAUNCH(ctx, "k_eg_tile_max", k_eg_tile_max<<<grid_for(ntiles, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        boff, P.nb, nsub, ntiles, ctx->derr));
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(cursor, boff, sizeof(int32_t) * P.nb, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+    PHFEM_TRY(errors_fetch(ctx));
+    if (ctx->herr->misc != ~0ull) return range_error();
+    const int64_t max_tile = (int64_t)ctx->herr->counters[3];
+    if (pre) items = pre->items;
+    else PHFEM_TRY(dalloc(ctx, &items, nd));
+    PHFEM_TRY(dalloc(ctx, &rec, nd));
+    if (max_tile > kTileCap) {  // some tile does not fit SMEM: global scratch
+      PHFEM_TRY(dalloc(ctx, &g1, nd));
+      PHFEM_TRY(dalloc(ctx, &g2, nd));
+      PHFEM_TRY(dalloc(ctx, &gnode, nd));
+    }
+    if (!pre) PHFEM_TRY(source(1, cursor, items));
   }
-  if (!pre) PHFEM_TRY(source(1, cursor, items));
+  // the tile kernels' bucket array: the fills in the fixed layout, else the offsets
+  const int32_t* tboff = fixed ? cursor : boff;
 
   EgOut o;
   memset(&o, 0, sizeof o);
@@ -1211,10 +1364,10 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     const size_t csmem = sizeof(ColSmem);
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_col, csmem, "k_eg_tile_col smem opt-in"));
     PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile_col<<<ntiles, kTileThreads, csmem, ctx->stream>>>(
-        items, boff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb));
+        items, tboff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb));
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_list, smem, "k_eg_tile_list smem opt-in"));
     PHFEM_LAUNCH(ctx, "k_eg_tile_list", k_eg_tile_list<<<ctx->num_sms * 4, kTileThreads, smem, ctx->stream>>>(
-        fb + 1, fb, items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+        fb + 1, fb, items, tboff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
     dfree(ctx, fb);
   } else {
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile, smem, "k_eg_tile smem opt-in"));
@@ -1296,6 +1449,7 @@ static phfem_status eg_params(phfem_ctx* ctx, int64_t nC_range, int64_t nC_all, 
   P->nC = (int32_t)nC_range;
   P->nE = (int32_t)nE_all;
   P->node_base = node_base;
+  P->fcap = 0;
   P->lo_bits = bits_for(std::max<int64_t>(nC_all - 1, 1));
   P->occ_bits = bits_for(std::max<int64_t>(3 * nE_all - 1, 1));
   P->total_bits = P->lo_bits + P->occ_bits + 1;
@@ -1329,7 +1483,7 @@ PHFEM_API phfem_status phfem_build_topology(phfem_ctx* ctx, const phfem_mesh* me
       PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter<<<grid_e, 256, 0, ctx->stream>>>(mesh->elements, P, counts, items));
     return PHFEM_OK;
   };
-  return eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology");
+  return eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology", nullptr, nullptr, nullptr, mesh->elements);
 }
 
 PHFEM_API phfem_status phfem_dist_dedup_ex(phfem_ctx* ctx, const int32_t* recs, int64_t n,
@@ -1420,7 +1574,8 @@ phfem_status build_topology_fused(phfem_ctx* ctx, const phfem_mesh* mesh, phfem_
     return PHFEM_OK;
   };
   EgFuse fuse{keys, cap, mesh->coords, cls, C, (int32_t)nE};
-  phfem_status st = eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology", &fuse);
+  phfem_status st = eg_core(ctx, P, 3 * nE, source, out, nullptr, "build_topology", &fuse, nullptr, nullptr,
+                            mesh->elements);
   dfree(ctx, keys);
   if (st != PHFEM_OK) return st;
   const int32_t L = cls->L;
