@@ -149,8 +149,11 @@ static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topolo
   int32_t* pre_neu = out->block_prefix + nblk + 1;
   PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
       out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, bnd_base, pre_bnd, pre_neu));
-  PHFEM_TRY(scan_exclusive_i32(ctx, pre_bnd, pre_bnd, nblk + 1, nullptr));
-  PHFEM_TRY(scan_exclusive_i32(ctx, pre_neu, pre_neu, nblk + 1, nullptr));
+  {
+    const int32_t* in[2] = {pre_bnd, pre_neu};
+    int32_t* io[2] = {pre_bnd, pre_neu};
+    PHFEM_TRY(scan_exclusive_i32_set(ctx, 2, in, io, nblk + 1, nullptr));
+  }
   if (nblk > 0 && with_retained) {
     PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
                                                          out->retained_pos, out->retained_edges, r_off, e_off));

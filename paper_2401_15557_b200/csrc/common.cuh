@@ -165,6 +165,9 @@ inline int grid_for(int64_t n, int block, int max_blocks) {
 // tile sums, downsweep).  out may alias in.  Writes the total to *total_dev.
 phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
                                 int32_t* total_dev);
+// up to 4 arrays of the same length, one launch per phase; in[a] == out[a] allowed
+phfem_status scan_exclusive_i32_set(phfem_ctx* ctx, int count, const int32_t* const* in, int32_t* const* out,
+                                    int64_t n, int32_t* const* total_dev);
 
 // Stable LSD radix sort of (key, u32 value) pairs over key bits [0, end_bit)
 // (radix_sort.cu; hand-written, no library sort).  Inputs are not modified.

@@ -283,6 +283,136 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_small(const int32_t* in, 
   if (threadIdx.x == 0 && total) *total = carry;
 }
 
+// Up to kScanSet arrays of the same length scanned by one launch per phase
+// (blockIdx.y / blockIdx.x = the array): the per-tile counts of the edge and
+// refinement passes come in threes, each scan a few microseconds of launch.
+constexpr int kScanSet = 4;
+struct ScanSet {
+  const int32_t* in[kScanSet];
+  int32_t* out[kScanSet];
+  int32_t* total[kScanSet];
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_small_set(ScanSet S, int64_t n) {
+  const int a = blockIdx.x;
+  const int32_t* in = S.in[a];
+  int32_t* out = S.out[a];
+  __shared__ int32_t sm[33];
+  int32_t carry = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += kScanTile) {
+    const int64_t base = c0 + (int64_t)threadIdx.x * kScanPer;
+    int32_t v[kScanPer];
+    int32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      v[k] = base + k < n ? in[base + k] : 0;
+      s += v[k];
+    }
+    int32_t tot;
+    int32_t ex = carry + block_exclusive_scan(s, sm, &tot);
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      if (base + k < n) out[base + k] = ex;
+      ex += v[k];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && S.total[a]) *S.total[a] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums_set(ScanSet S, int64_t n, int32_t* __restrict__ sums,
+                                                                     int64_t tiles) {
+  __shared__ int32_t sm[33];
+  const int a = blockIdx.y;
+  const int32_t* in = S.in[a];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) v += in[i];
+  }
+  int32_t tot;
+  block_exclusive_scan(v, sm, &tot);
+  if (threadIdx.x == 0) sums[a * tiles + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums_set(int32_t* sums, int64_t tiles, ScanSet S) {
+  __shared__ int32_t sm[33];
+  const int a = blockIdx.x;
+  int32_t* sa = sums + a * tiles;
+  int32_t carry = 0;
+  for (int64_t base = 0; base < tiles; base += kScanThreads) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < tiles ? sa[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(v, sm, &tot);
+    if (i < tiles) sa[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && S.total[a]) *S.total[a] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down_set(ScanSet S, int64_t n,
+                                                                const int32_t* __restrict__ sums, int64_t tiles) {
+  __shared__ int32_t sm[33];
+  const int a = blockIdx.y;
+  const int32_t* in = S.in[a];
+  int32_t* out = S.out[a];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  int32_t v[kScanPer];
+  int32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + k;
+    v[k] = i < n ? in[i] : 0;
+    s += v[k];
+  }
+  int32_t tot;
+  int32_t ex = block_exclusive_scan(s, sm, &tot) + sums[a * tiles + blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int64_t i = base + k;
+    if (i < n) out[i] = ex;
+    ex += v[k];
+  }
+}
+
+phfem_status scan_exclusive_i32_set(phfem_ctx* ctx, int count, const int32_t* const* in, int32_t* const* out,
+                                    int64_t n, int32_t* const* total_dev) {
+  if (count < 1 || count > kScanSet) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "scan set size");
+  ScanSet S;
+  memset(&S, 0, sizeof S);
+  for (int a = 0; a < count; ++a) {
+    S.in[a] = in[a];
+    S.out[a] = out[a];
+    S.total[a] = total_dev ? total_dev[a] : nullptr;
+  }
+  if (n == 0) {
+    for (int a = 0; a < count; ++a)
+      if (S.total[a]) PHFEM_CUDA(ctx, cudaMemsetAsync(S.total[a], 0, sizeof(int32_t), ctx->stream));
+    return PHFEM_OK;
+  }
+  if (n <= kScanSmall) {
+    KTimer kt(ctx, "scan");
+    k_scan_small_set<<<count, kScanThreads, 0, ctx->stream>>>(S, n);
+    PHFEM_CHECK_LAUNCH(ctx);
+    return PHFEM_OK;
+  }
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  int32_t* sums = nullptr;
+  PHFEM_TRY(dalloc(ctx, &sums, tiles * count));
+  KTimer kt(ctx, "scan");
+  k_scan_tile_sums_set<<<dim3((unsigned)tiles, count), kScanThreads, 0, ctx->stream>>>(S, n, sums, tiles);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan_sums_set<<<count, kScanThreads, 0, ctx->stream>>>(sums, tiles, S);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan_down_set<<<dim3((unsigned)tiles, count), kScanThreads, 0, ctx->stream>>>(S, n, sums, tiles);
+  PHFEM_CHECK_LAUNCH(ctx);
+  dfree(ctx, sums);
+  return PHFEM_OK;
+}
+
 phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out, int64_t n,
                                 int32_t* total_dev) {
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;

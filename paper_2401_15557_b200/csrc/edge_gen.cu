@@ -1374,10 +1374,12 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile<<<ntiles, kTileThreads, smem, ctx->stream>>>(
         items, boff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
   }
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileE, tileE, (int64_t)ntiles + 1, nullptr));
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, (int64_t)ntiles + 1, nullptr));
+  {
+    const int32_t* in[3] = {tileE, tileB, tileN};
+    int32_t* io[3] = {tileE, tileB, tileN};
+    PHFEM_TRY(scan_exclusive_i32_set(ctx, fuse ? 3 : 2, in, io, (int64_t)ntiles + 1, nullptr));
+  }
   if (fuse) {  // sizes of the classification / C before the emit pass writes them
-    PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, (int64_t)ntiles + 1, nullptr));
     int32_t h[3] = {0, 0, 0};
     PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[0], tileE + ntiles, 4, cudaMemcpyDeviceToHost, ctx->stream));
     PHFEM_CUDA(ctx, cudaMemcpyAsync(&h[1], tileB + ntiles, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -212,6 +212,48 @@ __global__ void k_rl_tile_count(const int32_t* __restrict__ elem_edge, int nE, i
   }
 }
 
+// k_rl_tile_init + k_rl_tile_count in one launch (blocks [0, blocksA) the
+// tile pass, the rest the element pass; tileF accumulated with atomics on
+// both sides, zeroed by the caller): one launch less per refinement level —
+// the small levels of a deep refinement are launch-bound.
+__global__ void k_rl_tile_prep(int E, int ntiles, const int32_t* __restrict__ boundary, int nB,
+                               const uint32_t* __restrict__ neu_bits, int32_t* __restrict__ tileF,
+                               int32_t* __restrict__ tileB, int32_t* __restrict__ tileN,
+                               const int32_t* __restrict__ elem_edge, int nE, int blocksA) {
+  if ((int)blockIdx.x < blocksA) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += blocksA * blockDim.x) {
+      const int64_t l0 = (int64_t)t * kLvT;
+      const int64_t l1 = l0 + kLvT < E ? l0 + kLvT : E;
+      atomicAdd(tileF + t, 2 * (int)(l1 - l0));
+      auto lower = [&](int64_t key) {
+        int l = 0, r = nB;
+        while (l < r) {
+          const int mid = (l + r) >> 1;
+          if (__ldg(boundary + mid) < key) l = mid + 1;
+          else r = mid;
+        }
+        return l;
+      };
+      tileB[t] = lower(l1) - lower(l0);
+      if (neu_bits) {
+        int c = 0;
+        for (int64_t w = l0 >> 5; w < (l1 + 31) >> 5; ++w) c += __popc(__ldg(neu_bits + w));
+        tileN[t] = c;
+      }
+    }
+    return;
+  }
+  const int64_t stride = (int64_t)(gridDim.x - blocksA) * blockDim.x;
+  for (int64_t m = (blockIdx.x - blocksA) * (int64_t)blockDim.x + threadIdx.x; m < nE; m += stride) {
+    const int x = abs_edge(__ldg(elem_edge + 3 * m)), y = abs_edge(__ldg(elem_edge + 3 * m + 1)),
+              z = abs_edge(__ldg(elem_edge + 3 * m + 2));
+    const int hi = max(x, max(y, z));
+    const int md = max(min(x, y), min(max(x, y), z));
+    if (md < E) warp_add(tileF, md / kLvT, 1);
+    if (hi < E) warp_add(tileF, hi / kLvT, 2);
+  }
+}
+
 #ifndef PHFEM_LV_MIN_BLOCKS
 #define PHFEM_LV_MIN_BLOCKS 7
 #endif
@@ -592,13 +634,18 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
   int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
   PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 3 * (ntiles + 1), ctx->stream));
   const uint32_t* nbits = pcls ? pcls->neumann_bits : nullptr;
-  PHFEM_LAUNCH(ctx, "k_rl_tile_init", k_rl_tile_init<<<grid_for(ntiles, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-      (int)E, 0, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN));
-  PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_count<<<grid_for(parent->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-      ptopo->elem_edge, parent->nE, 0, (int)E, tileF));
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, nullptr));
-  PHFEM_TRY(scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr));
-  if (pcls) PHFEM_TRY(scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, nullptr));
+  {
+    const int blocksA = grid_for(ntiles, 256, ctx->num_sms * 8);
+    const int blocksB = grid_for(parent->nE, 256, ctx->num_sms * 16);
+    PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_prep<<<blocksA + blocksB, 256, 0, ctx->stream>>>(
+        (int)E, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN, ptopo->elem_edge,
+        parent->nE, blocksA));
+  }
+  {
+    const int32_t* in[3] = {tileF, tileB, tileN};
+    int32_t* io[3] = {tileF, tileB, tileN};
+    PHFEM_TRY(scan_exclusive_i32_set(ctx, pcls ? 3 : 2, in, io, ntiles + 1, nullptr));
+  }
   LvArgs a;
   memset(&a, 0, sizeof a);
   a.edge_nodes = ptopo->edge_nodes;
@@ -1134,9 +1181,12 @@ PHFEM_API phfem_status phfem_dist_level_count_ex(phfem_ctx* ctx, const phfem_top
     }
   }
   if (cudaGetLastError() != cudaSuccess) return fail(set_error(ctx, PHFEM_ERR_CUDA, "level count launch failed"));
-  if ((st = scan_exclusive_i32(ctx, tileF, tileF, ntiles + 1, total)) != PHFEM_OK) return fail(st);
-  if ((st = scan_exclusive_i32(ctx, tileB, tileB, ntiles + 1, nullptr)) != PHFEM_OK) return fail(st);
-  if (pl->with_C && (st = scan_exclusive_i32(ctx, tileN, tileN, ntiles + 1, total + 1)) != PHFEM_OK) return fail(st);
+  {
+    const int32_t* in[3] = {tileF, tileB, tileN};
+    int32_t* io[3] = {tileF, tileB, tileN};
+    int32_t* tot[3] = {total, nullptr, total + 1};
+    if ((st = scan_exclusive_i32_set(ctx, pl->with_C ? 3 : 2, in, io, ntiles + 1, tot)) != PHFEM_OK) return fail(st);
+  }
   int32_t hcnt[2] = {0, 0};
   if (cudaMemcpyAsync(hcnt, total, sizeof hcnt, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
       cudaStreamSynchronize(ctx->stream) != cudaSuccess)
