@@ -29,7 +29,7 @@ constexpr int kVolWarps = kVolThreads / 32;
 constexpr int kVolMinBlocks = PHFEM_VOL_MIN_BLOCKS;
 
 __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base, int n_valid,
-                                           int per, const double* vals, double* buf, bool vec) {
+                                           int per, const double* vals, double* buf, int vec) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
 #pragma unroll
@@ -38,6 +38,26 @@ __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base,
   __syncwarp();
   const int count = n_valid * per;
   double* dst = g + base * per;
+#if PHFEM_VOL_ST256
+  // 32-byte streaming stores (STG.E.ENL2.256, sm_100): half the store
+  // instructions of the 16-byte form; the destination is 32-byte aligned
+  // when vec == 2 (chunk spans are multiples of 768 B).  Measured slower
+  // (k_volume 7.61 -> 7.87 ms at L13: the 32-byte-stride SMEM reads conflict;
+  // the store-only pattern gains nothing either, tools/micro/volpat.cu), so
+  // off by default
+  if (vec == 2) {
+    const int n4 = count >> 2;
+    for (int i = lane; i < n4; i += 32) {
+      const double2 lo = reinterpret_cast<const double2*>(buf)[2 * i];
+      const double2 hi = reinterpret_cast<const double2*>(buf)[2 * i + 1];
+      asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * i), "d"(lo.x), "d"(lo.y),
+                   "d"(hi.x), "d"(hi.y)
+                   : "memory");
+    }
+    for (int i = 4 * n4 + lane; i < count; i += 32) dst[i] = buf[i];
+    return;
+  }
+#endif
   if (vec) {
     const double2* src2 = reinterpret_cast<const double2*>(buf);
     double2* dst2 = reinterpret_cast<double2*>(dst);
@@ -158,6 +178,7 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
 }
 
 static bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+static bool aligned32(const void* p) { return p == nullptr || ((uintptr_t)p & 31u) == 0; }
 
 VolArgs make_vol_args(const phfem_mesh* mesh) {
   VolArgs a;
@@ -567,6 +588,7 @@ PHFEM_API phfem_status phfem_assemble_volume(phfem_ctx* ctx, const phfem_mesh* m
   a.M = M;
   a.M0 = M0;
   a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0);
+  if (a.vec && aligned32(B) && aligned32(D) && aligned32(M) && aligned32(M0)) a.vec = 2;
   PHFEM_TRY(errors_reset(ctx));
   PHFEM_TRY(launch_volume(ctx, a, true, false));
   PHFEM_TRY(errors_fetch(ctx));
@@ -590,6 +612,7 @@ PHFEM_API phfem_status phfem_assemble_volume_load(phfem_ctx* ctx, const phfem_me
   a.t = t;
   a.load = load;
   a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0) && aligned16(load);
+  if (a.vec && aligned32(B) && aligned32(D) && aligned32(M) && aligned32(M0) && aligned32(load)) a.vec = 2;
   PHFEM_TRY(errors_reset(ctx));
   PHFEM_TRY(launch_volume(ctx, a, true, true));
   PHFEM_TRY(errors_fetch(ctx));
@@ -615,6 +638,7 @@ PHFEM_API phfem_status phfem_dist_volume_start(phfem_ctx* ctx, const phfem_mesh*
   a.t = t;
   a.load = load;
   a.vec = aligned16(B) && aligned16(D) && aligned16(M) && aligned16(M0) && aligned16(load);
+  if (a.vec && aligned32(B) && aligned32(D) && aligned32(M) && aligned32(M0) && aligned32(load)) a.vec = 2;
   PHFEM_TRY(errors_reset(ctx));
   return launch_volume(ctx, a, true, true);
 }
@@ -633,6 +657,7 @@ PHFEM_API phfem_status phfem_assemble_load(phfem_ctx* ctx, const phfem_mesh* mes
   a.t = t;
   a.load = out;
   a.vec = aligned16(out);
+  if (a.vec && aligned32(out)) a.vec = 2;
   PHFEM_TRY(errors_reset(ctx));
   PHFEM_TRY(launch_volume(ctx, a, false, true));
   PHFEM_TRY(errors_fetch(ctx));

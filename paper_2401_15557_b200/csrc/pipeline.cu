@@ -121,7 +121,7 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   a.M = out->M;
   a.M0 = out->M0;
   a.load = out->load;
-  a.vec = 1;  // pool allocations are 256-byte aligned
+  a.vec = 2;  // pool allocations are 256-byte aligned (32-byte stores allowed)
   PHFEM_TRY(launch_volume(ctx, a, true, true));
   tr("volume+load");
   PHFEM_TRY(neumann_into(ctx, &out->mesh, &out->topo, &out->cls, g, t, out->load, 1, false));

@@ -1,0 +1,75 @@
+"""A/B of library builds on the config-5 step (L12 resident -> L13 outputs):
+per-kernel CUDA-event times (ctx profiling) and the step time, per variant,
+interleaved rounds so clock / thermal drift hits every variant alike.
+
+  python tools/ab_step.py [--level 13] [--rounds 3] [--steps 4] LIB [LIB ...]
+  (LIB: a path to a build of libphfem_b200.so, e.g. from tools/variants.sh)
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, os, sys, time
+sys.path.insert(0, %r)
+from bench import build_input
+from paper_2401_15557_b200 import capi, meshgen as G
+level, steps = %d, %d
+ctx = capi.Context(0)
+dm = build_input(ctx, level - 1)
+f = G.config_fields(5)
+for _ in range(2):
+    capi.pipeline(ctx, dm, 1, *f).release()
+ctx.sync()
+ctx.profile(True)
+ts = []
+for _ in range(steps):
+    ctx.sync(); t0 = time.perf_counter()
+    r = capi.pipeline(ctx, dm, 1, *f)
+    ctx.sync(); ts.append((time.perf_counter() - t0) * 1e3)
+    r.release()
+prof = ctx.profile_read()
+ctx.profile(False)
+print("RESULT " + json.dumps({"wall_ms": sorted(ts)[len(ts) // 2],
+      "kernels": {k: v[0] / steps for k, v in prof.items()}}))
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--level", type=int, default=13)
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("libs", nargs="+")
+    a = ap.parse_args()
+    res = {lib: [] for lib in a.libs}
+    for _ in range(a.rounds):
+        for lib in a.libs:
+            env = dict(os.environ, PHFEM_LIB=os.path.abspath(lib))
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.level, a.steps)], env=env,
+                                 capture_output=True, text=True, timeout=600)
+            line = [x for x in out.stdout.splitlines() if x.startswith("RESULT ")]
+            if not line:
+                print(lib, "FAILED", out.stderr[-2000:], flush=True)
+                continue
+            res[lib].append(json.loads(line[0][7:]))
+    for lib, rs in res.items():
+        if not rs:
+            continue
+        ks = {}
+        for r in rs:
+            for k, v in r["kernels"].items():
+                ks.setdefault(k, []).append(v)
+        kern = {k: min(v) for k, v in ks.items()}
+        tot = sum(kern.values())
+        top = sorted(kern.items(), key=lambda kv: -kv[1])[:8]
+        print(f"{os.path.basename(lib):32s} wall {min(r['wall_ms'] for r in rs):7.3f} ms  kernels {tot:7.3f} ms  " +
+              "  ".join(f"{k} {v:.3f}" for k, v in top), flush=True)
+
+
+if __name__ == "__main__":
+    main()
