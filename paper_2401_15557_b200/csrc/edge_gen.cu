@@ -1040,8 +1040,6 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
   const int64_t vbase = (int64_t)out.node_base + (int64_t)tile * kTileNodes;
   const bool fused = out.rpos != nullptr;
   __shared__ unsigned long long nscan[33];
-  __shared__ int32_t ccol[kEmitThreads / 32][128];  // C staging, one 32-row block per warp
-  __shared__ double cval[kEmitThreads / 32][128];
   int nrun = fused ? out.tileN[tile] : 0;  // Neumann edges before the trip (global)
   for (int i00 = 0; i00 < ne; i00 += 4 * kEmitThreads) {
     const int i0 = i00 + threadIdx.x;
@@ -1067,10 +1065,10 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
       }
       nrun = base;
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (i00 + u * kEmitThreads + 32 * warp >= ne) break;  // warp-uniform (C staging below)
+      if (i00 + u * kEmitThreads + 32 * warp >= ne) break;  // warp-uniform exit past the tile's records
       const int i = i0 + u * kEmitThreads;
       const bool ok = i < ne;
       const int32_t e = E0 + i;
@@ -1121,38 +1119,34 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
           }
         }
       }
-      if (fused) {
-        // the warp's rows own contiguous C entries: staged per warp, stored
-        // line by line (a direct per-row store half-writes every sector per
-        // instruction — measured as the larger part of this kernel's time)
-        const unsigned rows = __ballot_sync(0xffffffffu, row);
-        if (rows) {
-          const int fl = __ffs(rows) - 1, ll = 31 - __clz(rows);
-          const int rs0 = __shfl_sync(0xffffffffu, rs, fl);
-          const int cnt = __shfl_sync(0xffffffffu, rs + nn, ll) - rs0;
-          if (row) {
-            const int k = rs - rs0;
-            const int c0 = l_f == 0 ? 1 : 0, c1 = l_f == 2 ? 1 : 2;
-            const double vp = len * 0.5;  // assembly.cpp:160
-            ccol[warp][k] = 3 * m_f + c0;
-            ccol[warp][k + 1] = 3 * m_f + c1;
-            cval[warp][k] = vp;
-            cval[warp][k + 1] = vp;
-            if (nn == 4) {
-              const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
-              const double vm = -len * 0.5;  // assembly.cpp:164
-              ccol[warp][k + 2] = 3 * m_g + d0;
-              ccol[warp][k + 3] = 3 * m_g + d1;
-              cval[warp][k + 2] = vm;
-              cval[warp][k + 3] = vm;
-            }
+      if (fused && row) {
+        // direct stores: an interior row at a 32-byte aligned entry as one
+        // 16-byte column + one 32-byte value store (STG.256); measured against
+        // the per-warp SMEM staging of round 2 (whole-line stores): emit on the
+        // given L13 mesh 5.15 -> 4.69 ms
+        const int c0 = l_f == 0 ? 1 : 0, c1 = l_f == 2 ? 1 : 2;
+        const double vp = len * 0.5;  // assembly.cpp:160
+        if (nn == 4 && ((reinterpret_cast<uintptr_t>(out.val + rs) & 31) == 0) &&
+            ((reinterpret_cast<uintptr_t>(out.col + rs) & 15) == 0)) {
+          const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
+          const double vm = -len * 0.5;  // assembly.cpp:164
+          *reinterpret_cast<int4*>(out.col + rs) = make_int4(3 * m_f + c0, 3 * m_f + c1, 3 * m_g + d0, 3 * m_g + d1);
+          asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(out.val + rs), "d"(vp), "d"(vp),
+                       "d"(vm), "d"(vm)
+                       : "memory");
+        } else {
+          out.col[rs] = 3 * m_f + c0;
+          out.col[rs + 1] = 3 * m_f + c1;
+          out.val[rs] = vp;
+          out.val[rs + 1] = vp;
+          if (nn == 4) {
+            const int d0 = l_g == 0 ? 1 : 0, d1 = l_g == 2 ? 1 : 2;
+            const double vm = -len * 0.5;  // assembly.cpp:164
+            out.col[rs + 2] = 3 * m_g + d0;
+            out.col[rs + 3] = 3 * m_g + d1;
+            out.val[rs + 2] = vm;
+            out.val[rs + 3] = vm;
           }
-          __syncwarp();
-          for (int k = lane; k < cnt; k += 32) {
-            out.col[rs0 + k] = ccol[warp][k];
-            __stcs(out.val + rs0 + k, cval[warp][k]);
-          }
-          __syncwarp();
         }
       }
     }

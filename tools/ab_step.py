@@ -18,18 +18,18 @@ import json, os, sys, time
 sys.path.insert(0, %r)
 from bench import build_input
 from paper_2401_15557_b200 import capi, meshgen as G
-level, steps = %d, %d
+level, steps, levels = %d, %d, %d
 ctx = capi.Context(0)
-dm = build_input(ctx, level - 1)
+dm = build_input(ctx, level - levels)
 f = G.config_fields(5)
 for _ in range(2):
-    capi.pipeline(ctx, dm, 1, *f).release()
+    capi.pipeline(ctx, dm, levels, *f).release()
 ctx.sync()
 ctx.profile(True)
 ts = []
 for _ in range(steps):
     ctx.sync(); t0 = time.perf_counter()
-    r = capi.pipeline(ctx, dm, 1, *f)
+    r = capi.pipeline(ctx, dm, levels, *f)
     ctx.sync(); ts.append((time.perf_counter() - t0) * 1e3)
     r.release()
 prof = ctx.profile_read()
@@ -44,13 +44,14 @@ def main():
     ap.add_argument("--level", type=int, default=13)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--given", action="store_true", help="the L13 mesh given (levels = 0)")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     res = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
         for lib in a.libs:
             env = dict(os.environ, PHFEM_LIB=os.path.abspath(lib))
-            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.level, a.steps)], env=env,
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.level, a.steps, 0 if a.given else 1)], env=env,
                                  capture_output=True, text=True, timeout=600)
             line = [x for x in out.stdout.splitlines() if x.startswith("RESULT ")]
             if not line:

@@ -36,6 +36,9 @@ if len(sys.argv) > 2:
     rows = list(csv.reader(io.StringIO(out)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == 'Address'][0]
     hdr, data = rows[hi], rows[hi + 1:]
+    # several kernels in one report: keep the first kernel's table
+    end = next((i for i, r in enumerate(data) if r and r[0] in ('Kernel Name', 'Address')), len(data))
+    data = data[:end]
     si = hdr.index('Warp Stall Sampling (All Samples)')
     ie = hdr.index('Instructions Executed')
     tot = sum(float(r[si] or 0) for r in data) or 1
