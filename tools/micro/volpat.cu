@@ -85,6 +85,23 @@ int main() {
                moved / best / 1e6);
       }
     }
+  // stream count: the same chunk pattern into 1, 2, 3 or 4 of the block arrays
+  for (int ns = 1; ns <= 4; ++ns) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(e0);
+      if (ns == 1) k_pat<1, true><<<sms * 6, 128>>>(B, D, M, M0, L, el, nchunks, 0, 1);
+      if (ns == 2) k_pat<2, true><<<sms * 6, 128>>>(B, D, M, M0, L, el, nchunks, 0, 1);
+      if (ns == 3) k_pat<3, true><<<sms * 6, 128>>>(B, D, M, M0, L, el, nchunks, 0, 1);
+      if (ns == 4) k_pat<4, true><<<sms * 6, 128>>>(B, D, M, M0, L, el, nchunks, 0, 1);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("streams=%d (72 B/elem each) %7.3f ms %8.1f GB/s\n", ns, best, nE * 72.0 * ns / best / 1e6);
+  }
   for (int mult : {4, 6, 8}) {
     float best = 1e30f;
     for (int rep = 0; rep < 4; ++rep) {
