@@ -61,18 +61,6 @@ struct phfem_cn_plan {
   // boundary), and |E| * 0.5
   uint2* rowt = nullptr;
   double* rowh = nullptr;
-  // hybrid path: the non-Dirichlet rows again, grouped by owner tile — the
-  // 128-element tile holding the row's later element max(t_plus, t_minus);
-  // k_cn_hyb evaluates tile i's rows right after the tile, while the U of
-  // both elements is still in L2 (the separate row pass re-read all of U
-  // from DRAM).  trow[i] = first row of tile i (i <= nfull: the rows owned by
-  // the tail elements form the last group, for k_cn_rows); orid = row index
-  int32_t* trow = nullptr;
-  uint2* orowt = nullptr;
-  double* orowh = nullptr;
-  int32_t* orid = nullptr;
-  int64_t own_nfull = -1;         // full tiles the grouping was built for
-  int32_t own_rest0 = 0, own_n = 0;  // first row of the tail group, non-Dirichlet rows
   bool hybrid = false;  // k_cn_hyb (top block + coupling recomputed) instead of k_cn_tma
 };
 
@@ -371,40 +359,11 @@ __device__ __forceinline__ void cn_primal(const CnArgs& a, int64_t m, const doub
   }
 }
 
-// Multiplier row l from its record: 0.0 + sum over ascending columns — T+
-// DOFs, then T- DOFs — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor SpMV,
-// from_triplets' 0.0 +), + 0.5 (0.0 + 0.0) (parabolic.cpp:103, no Dirichlet data)
-__device__ __forceinline__ double cn_row_value(uint2 r, double h, double s_c, const double* __restrict__ W) {
-  const double cp = 0.0 + s_c * h;  // assembly.cpp:160
-  const int64_t p = 3 * (int64_t)(r.x >> 2);
-  const int lp = (int)(r.x & 3u);
-  double acc = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-    if (c != lp) acc += cp * __ldg(W + p + c);
-  if (r.y != kRowBnd) {
-    const int64_t q = 3 * (int64_t)(r.y >> 2);
-    const int lm = (int)(r.y & 3u);
-    const double cm = 0.0 + s_c * (-h);  // assembly.cpp:164: -len * 0.5 = -(len * 0.5)
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      if (c != lm) acc += cm * __ldg(W + q + c);
-  }
-  const double bdsum = 0.0 + 0.0;
-  return acc + 0.5 * bdsum;
-}
-
 struct CnStored {
   const double* top;
   const double* cpl;
   const double* lq;
   const int32_t* rp3;
-  // hybrid: multiplier rows grouped by owner tile (nullptr: k_cn_rows does them)
-  const int32_t* trow;
-  const uint2* orowt;
-  const double* orowh;
-  const int32_t* orid;
-  double s_c;
 };
 
 // warp-cooperative coalesced load of a per-element record of `per` elements
@@ -607,22 +566,20 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
   uint64_t* bar = reinterpret_cast<uint64_t*>(outb + 3 * kCnTile);
   const int tid = threadIdx.x;
   const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  uint64_t pol = 0, pol_u = 0;
+  uint64_t pol = 0;
   auto issue = [&](int64_t i) {
     const int s = (int)(i % kCnHStages);
     const int64_t base = ((int64_t)blockIdx.x + i * gridDim.x) * kCnTile;
     mbar_expect_tx(&bar[s], (unsigned)sizeof(CnHStage));
     bulk_load(stg[s].el, a.elements + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
     bulk_load(stg[s].lq, st.lq + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
-    bulk_load(stg[s].U, W + 3 * base, 3 * kCnTile * 8, &bar[s], pol_u);
+    bulk_load(stg[s].U, W + 3 * base, 3 * kCnTile * 8, &bar[s], pol);
     bulk_load(stg[s].rp, st.rp3 + 3 * base, 3 * kCnTile * 4, &bar[s], pol);
   };
   if (tid == 0) {
     for (int s = 0; s < kCnHStages; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
     pol = policy_evict_first();
-    // U stays for the tile's multiplier rows (gathered right after the tile)
-    pol_u = st.trow ? policy_evict_last() : pol;
     for (int64_t i = 0; i < my && i < kCnHStages; ++i) issue(i);
   }
   __syncthreads();
@@ -693,12 +650,6 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
     const double2* s2 = reinterpret_cast<const double2*>(outb);
     double2* d2 = reinterpret_cast<double2*>(rhs + 3 * base);
     for (int k = tid; k < 3 * kCnTile / 2; k += kCnTile) __stcs(d2 + k, s2[k]);
-    if (st.trow) {  // the multiplier rows owned by this tile (U of both elements L2-hot)
-      const int tile = (int)(base / kCnTile);
-      const int r1 = __ldg(st.trow + tile + 1);
-      for (int r = __ldg(st.trow + tile) + tid; r < r1; r += kCnTile)
-        __stcs(rhs + a.N + __ldcs(st.orid + r), cn_row_value(__ldcs(st.orowt + r), __ldcs(st.orowh + r), st.s_c, W));
-    }
     __syncthreads();  // outb free for the next tile
   }
 }
@@ -707,47 +658,31 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
 // Dirichlet ones: row l = 0.0 + sum over ascending columns — T+ DOFs, then T-
 // DOFs — of (0.0 + (-sign/2) C_lj) U_j (Eigen ColMajor SpMV, from_triplets'
 // 0.0 +), + 0.5 (0.0 + 0.0) (parabolic.cpp:103 with no Dirichlet data).
-// Multiplier rows from the stored row records (coalesced), except the
-// Dirichlet ones; rid: row indices of the records (the hybrid path's tail
-// group), nullptr: the records are rows 0..L-1
 __global__ void __launch_bounds__(256) k_cn_rows(const uint2* __restrict__ rowt, const double* __restrict__ rowh,
-                                                  const int32_t* __restrict__ rid, int L, double s_c,
-                                                  const double* __restrict__ W, double* __restrict__ rhs_rows) {
+                                                  int L, double s_c, const double* __restrict__ W,
+                                                  double* __restrict__ rhs_rows) {
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
        l += (int64_t)gridDim.x * blockDim.x) {
     const uint2 r = __ldcs(rowt + l);
     if (r.y == kRowDir) continue;
-    const double v = cn_row_value(r, __ldcs(rowh + l), s_c, W);
-    __stcs(rhs_rows + (rid ? (int64_t)__ldcs(rid + l) : l), v);
-  }
-}
-
-// Grouping of the non-Dirichlet rows by owner tile (plan time): count, then
-// place (the order inside a group is free: every row is evaluated on its own)
-__device__ __forceinline__ int cn_row_owner_tile(uint2 r, int64_t nfull) {
-  const uint32_t own = r.y < kRowDir ? max(r.x >> 2, r.y >> 2) : r.x >> 2;
-  return (int)min((int64_t)(own / kCnTile), nfull);
-}
-
-__global__ void k_cn_own_count(const uint2* __restrict__ rowt, int L, int64_t nfull, int32_t* __restrict__ cnt) {
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
-       l += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 r = rowt[l];
-    if (r.y != kRowDir) atomicAdd(cnt + cn_row_owner_tile(r, nfull), 1);
-  }
-}
-
-__global__ void k_cn_own_place(const uint2* __restrict__ rowt, const double* __restrict__ rowh, int L,
-                               int64_t nfull, int32_t* __restrict__ cursor, uint2* __restrict__ orowt,
-                               double* __restrict__ orowh, int32_t* __restrict__ orid) {
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
-       l += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 r = rowt[l];
-    if (r.y == kRowDir) continue;
-    const int at = atomicAdd(cursor + cn_row_owner_tile(r, nfull), 1);
-    orowt[at] = r;
-    orowh[at] = rowh[l];
-    orid[at] = (int32_t)l;
+    const double h = __ldcs(rowh + l);
+    const double cp = 0.0 + s_c * h;  // assembly.cpp:160
+    const int64_t p = 3 * (int64_t)(r.x >> 2);
+    const int lp = (int)(r.x & 3u);
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (c != lp) acc += cp * __ldg(W + p + c);
+    if (r.y != kRowBnd) {
+      const int64_t q = 3 * (int64_t)(r.y >> 2);
+      const int lm = (int)(r.y & 3u);
+      const double cm = 0.0 + s_c * (-h);  // assembly.cpp:164: -len * 0.5 = -(len * 0.5)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (c != lm) acc += cm * __ldg(W + q + c);
+    }
+    const double bdsum = 0.0 + 0.0;
+    __stcs(rhs_rows + l, acc + 0.5 * bdsum);
   }
 }
 
@@ -804,38 +739,6 @@ __global__ void k_set_bits(const int32_t* __restrict__ ids, int n, uint32_t* __r
 }  // namespace phfem
 
 using namespace phfem;
-
-// Group the plan's non-Dirichlet rows by owner tile for k_cn_hyb (see
-// phfem_cn_plan::trow); one host read of the two group totals.
-static phfem_status cn_group_rows(phfem_ctx* ctx, phfem_cn_plan* p, int64_t nfull) {
-  const int L = p->cls.L;
-  int32_t* cursor = nullptr;
-  PHFEM_TRY(dalloc(ctx, &p->trow, nfull + 2));
-  PHFEM_TRY(dalloc(ctx, &p->orowt, (int64_t)L));
-  PHFEM_TRY(dalloc(ctx, &p->orowh, (int64_t)L));
-  PHFEM_TRY(dalloc(ctx, &p->orid, (int64_t)L));
-  PHFEM_TRY(dalloc(ctx, &cursor, nfull + 1));
-  PHFEM_CUDA(ctx, cudaMemsetAsync(p->trow, 0, sizeof(int32_t) * (nfull + 2), ctx->stream));
-  PHFEM_LAUNCH(ctx, "k_cn_own_count", k_cn_own_count<<<grid_for(L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-      p->rowt, L, nfull, p->trow));
-  phfem_status st = scan_exclusive_i32(ctx, p->trow, p->trow, nfull + 1, p->trow + nfull + 1);
-  if (st == PHFEM_OK)
-    st = cudaMemcpyAsync(cursor, p->trow, sizeof(int32_t) * (nfull + 1), cudaMemcpyDeviceToDevice, ctx->stream) ==
-                 cudaSuccess ? PHFEM_OK : set_error(ctx, PHFEM_ERR_CUDA, "cn plan: row grouping copy failed");
-  if (st == PHFEM_OK) {
-    PHFEM_LAUNCH(ctx, "k_cn_own_place", k_cn_own_place<<<grid_for(L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        p->rowt, p->rowh, L, nfull, cursor, p->orowt, p->orowh, p->orid));
-    int32_t h[2] = {0, 0};
-    if (cudaMemcpyAsync(h, p->trow + nfull, sizeof h, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
-      st = set_error(ctx, PHFEM_ERR_CUDA, "cn plan: row grouping failed");
-    p->own_rest0 = h[0];
-    p->own_n = h[1];
-    p->own_nfull = nfull;
-  }
-  dfree(ctx, cursor);
-  return st;
-}
 
 PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* mesh,
                                             const phfem_topology* topo,
@@ -924,10 +827,6 @@ PHFEM_API phfem_status phfem_cn_plan_create(phfem_ctx* ctx, const phfem_mesh* me
             a, topo->edge_nodes, topo->local_in_tplus, topo->E, p->rowt, p->rowh);
         ctx->launches++;
       }
-      if (st == PHFEM_OK && p->hybrid && cls->L > 0) {
-        const char* ow = getenv("PHFEM_CN_OWN_ROWS");  // "0": separate row pass (A/B runs)
-        if (!(ow && ow[0] == '0')) st = cn_group_rows(ctx, p, nE / kCnTile);
-      }
       // (measured: the Dirichlet rows folded into k_cn_rows — a per-plan
       // midpoint table and the u_D evaluation inlined there — made it
       // 0.099 -> 0.138 ms: registers for every row; the 2-row k_cn_edges
@@ -960,10 +859,6 @@ PHFEM_API void phfem_cn_plan_destroy(phfem_ctx* ctx, phfem_cn_plan* p) {
   dfree(ctx, p->rp3);
   dfree(ctx, p->rowt);
   dfree(ctx, p->rowh);
-  dfree(ctx, p->trow);
-  dfree(ctx, p->orowt);
-  dfree(ctx, p->orowh);
-  dfree(ctx, p->orid);
   delete p;
 }
 
@@ -1011,18 +906,10 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     } else if (a.f.kind == PHFEM_FIELD_SINSIN) {
       c0 = c1 = a.f.p[0];
     }
-    CnStored st{p->top, p->cpl, p->lq, p->rp3, nullptr, nullptr, nullptr, nullptr, a.s_c};
+    const CnStored st{p->top, p->cpl, p->lq, p->rp3};
     // TMA over the full tiles when the state and rhs allow 16-byte bulk copies
     const bool tma = ((((uintptr_t)state) | ((uintptr_t)rhs)) & 15u) == 0;
     const int64_t nfull = tma ? (int64_t)a.nE / kCnTile : 0;
-    // hybrid: the multiplier rows ride along with their owner tiles
-    const bool own = nfull > 0 && p->hybrid && p->trow && p->own_nfull == nfull;
-    if (own) {
-      st.trow = p->trow;
-      st.orowt = p->orowt;
-      st.orowh = p->orowh;
-      st.orid = p->orid;
-    }
     if (nfull > 0 && p->hybrid) {
       // 4 CTAs (16 warps) per SM: registers (122) and the 4-stage ring allow it;
       // the recompute is latency-bound, so residency matters more than depth
@@ -1047,17 +934,16 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     }
     // (measured: running the rows on a side stream next to the element pass
     // gains nothing — both are DRAM-bound)
+    // (measured: the rows grouped by owner tile at plan time and evaluated
+    // inside k_cn_hyb right after their tile, U kept in L2 by an evict-last
+    // policy — bit-identical, but the row loads and U gathers add a dependent
+    // latency chain to every tile of a kernel with 16 warps per SM: hybrid
+    // pass 0.256 + rows 0.097 ms -> 0.457 ms; dropped)
     // (measured: the rows on a side stream beside the hybrid element pass,
     // 3 or 4 element CTAs per SM: step 0.373 ms either way)
-    if (own) {  // only the rows owned by tail elements are left
-      const int n = p->own_n - p->own_rest0;
-      if (n > 0)
-        PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-            p->orowt + p->own_rest0, p->orowh + p->own_rest0, p->orid + p->own_rest0, n, a.s_c, state, rhs + a.N));
-    } else if (p->cls.L > 0) {
+    if (p->cls.L > 0)
       PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-          p->rowt, p->rowh, nullptr, p->cls.L, a.s_c, state, rhs + a.N));
-    }
+          p->rowt, p->rowh, p->cls.L, a.s_c, state, rhs + a.N));
     if (p->cls.nD > 0)
       PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->cls.nD, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
           a, p->topo.edge_nodes, p->topo.local_in_tplus, p->cls.nD, p->cls.dirichlet_edge_ids, state, rhs));

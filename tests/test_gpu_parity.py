@@ -382,28 +382,6 @@ def test_cn_rhs_tail_tile_and_unaligned_state(ctx, aligned):
         ctx.free(r)
 
 
-@pytest.mark.parametrize("mesh", ["square_l6", "fan_tail"])
-def test_cn_rhs_rows_grouped_same_bits(ctx, monkeypatch, mesh):
-    """The hybrid kernel evaluates the multiplier rows with their owner tiles
-    (rows grouped at plan time); the separate row pass (PHFEM_CN_OWN_ROWS=0)
-    must give the same bits, tail-element rows included (fan: 6.5 tiles)."""
-    hm = O.refine_levels(G.square_2tri(), 6) if mesh == "square_l6" else O.refine_levels(G.fan(13), 3)
-    coeffs, f, g, _ = G.config_fields(3)
-    uD = capi.field(capi.FIELD_AFFINE, 0.5, 1.0, -2.0, 3.0)
-    dm = capi.DeviceMesh.upload(ctx, hm)
-    topo = capi.build_topology(ctx, dm)
-    cls = capi.classify_edges(ctx, topo, dm)
-    monkeypatch.setenv("PHFEM_CN_MODE", "hybrid")
-    monkeypatch.setenv("PHFEM_CN_OWN_ROWS", "0")
-    sep = capi.CNPlan(ctx, dm, topo, cls, coeffs, f, g, uD, 1e-3)
-    monkeypatch.setenv("PHFEM_CN_OWN_ROWS", "1")
-    grp = capi.CNPlan(ctx, dm, topo, cls, coeffs, f, g, uD, 1e-3)
-    W = G.uniform_pm1(13, grp.n_state)
-    for n in (0, 5):
-        a, b = sep.rhs(n, W), grp.rhs(n, W)
-        assert a.tobytes() == b.tobytes()
-
-
 # ------------------------------------------------------------------ large sizes
 def test_large_refinement_properties(ctx):
     """Square L11 (8.4 M triangles, config 3's mesh) on the device only:
