@@ -27,6 +27,10 @@ constexpr int kVolWarps = kVolThreads / 32;
 #define PHFEM_VOL_MIN_BLOCKS 6
 #endif
 constexpr int kVolMinBlocks = PHFEM_VOL_MIN_BLOCKS;
+#ifndef PHFEM_VOL_ITERS
+#define PHFEM_VOL_ITERS 3
+#endif
+constexpr int kVolIters = PHFEM_VOL_ITERS;  // 32-element chunks per warp (grid sizing)
 
 __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base, int n_valid,
                                            int per, const double* vals, double* buf, int vec) {
@@ -149,8 +153,15 @@ __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a
 phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool load) {
   if (a.nE == 0) return PHFEM_OK;
   const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
-  const int grid = (int)std::min<int64_t>((nchunks + kVolWarps - 1) / kVolWarps,
-                                          (int64_t)ctx->num_sms * 8 * 4);
+  // about kVolIters chunks per warp: a grid of many short-lived CTAs spreads
+  // the concurrently written addresses over several windows of every output
+  // stream — measured at L13: 32 CTAs per SM (36 chunks per warp) 7.62 ms,
+  // 1024 / 2048 / 4096 per SM (7 / 3.5 / 1.7 chunks) 6.96 / 6.84 / 7.06 ms,
+  // one chunk per warp 8.05 ms (no software pipelining left)
+  const int64_t per_cta = (int64_t)kVolWarps * kVolIters;
+  const int grid = (int)std::max<int64_t>(std::min<int64_t>((nchunks + kVolWarps - 1) / kVolWarps,
+                                                            (int64_t)ctx->num_sms * 8),
+                                          (nchunks + per_cta - 1) / per_cta);
   const int fk = !load ? kKindGeneric : (a.samples ? kKindSamples : field_kind_spec(a.f));
   const int ck = a.coeffs.kind == PHFEM_COEFF_CENTROID_POLY ? PHFEM_COEFF_CENTROID_POLY : PHFEM_COEFF_CONST;
 #define PHFEM_VOL(B, L, F, K) \

@@ -91,6 +91,11 @@ struct CnArgs {
 };
 
 constexpr int kCnThreads = 128;
+// k_cn_rows grid (measured at L11: 8 CTAs per SM 0.099 ms; 32 / 128 / 1024
+// per SM 0.106 / 0.107 / 0.111 ms)
+#ifndef PHFEM_CNR_GRID_MULT
+#define PHFEM_CNR_GRID_MULT 8
+#endif
 #ifndef PHFEM_CN_MIN_BLOCKS
 #define PHFEM_CN_MIN_BLOCKS 1
 #endif
@@ -942,7 +947,7 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     // (measured: the rows on a side stream beside the hybrid element pass,
     // 3 or 4 element CTAs per SM: step 0.373 ms either way)
     if (p->cls.L > 0)
-      PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * PHFEM_CNR_GRID_MULT), 256, 0, ctx->stream>>>(
           p->rowt, p->rowh, p->cls.L, a.s_c, state, rhs + a.N));
     if (p->cls.nD > 0)
       PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->cls.nD, 256, ctx->num_sms), 256, 0, ctx->stream>>>(

@@ -127,6 +127,11 @@ __global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ 
 // pass is made here (first bad element -> misc) and the fullest bucket's
 // fill is reported (counters[3]) — above fcap the caller falls back to the
 // counted layout.
+// (measured at L12: 8 CTAs per SM 0.320 ms, 32 / 128 / 512 per SM 0.325 /
+// 0.400 / 0.844 ms — the bucket cursors' atomics, not the stores, bound it)
+#ifndef PHFEM_SC_GRID_MULT
+#define PHFEM_SC_GRID_MULT 8
+#endif
 __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restrict__ elements,
                                                           EgParams P, int32_t* __restrict__ cursor,
                                                           uint64_t* __restrict__ items, phfem_dev_errors* err) {
@@ -1278,7 +1283,7 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     PHFEM_TRY(dalloc(ctx, &items, capn));
     PHFEM_TRY(dalloc(ctx, &rec, capn));
     P.fcap = fcap;
-    const int grid_e = grid_for(P.nE, 256, ctx->num_sms * 8);
+    const int grid_e = grid_for(P.nE, 256, ctx->num_sms * PHFEM_SC_GRID_MULT);
     PHFEM_LAUNCH(ctx, "k_eg_scatter", k_eg_scatter_fixed<<<grid_e, 256, 0, ctx->stream>>>(fixed_elements, P, cursor,
                                                                                          items, ctx->derr));
     PHFEM_TRY(errors_fetch(ctx));

@@ -254,6 +254,12 @@ __global__ void k_rl_tile_prep(int E, int ntiles, const int32_t* __restrict__ bo
   }
 }
 
+// k_refine_children grid: 64 CTAs per SM (~14 element rows per thread at
+// L12 -> L13) — measured 0.827 ms at 16 per SM, 0.753 at 64, 0.757 at 256,
+// 0.793 at 1024 (more concurrent store windows, as for k_volume)
+#ifndef PHFEM_CH_GRID_MULT
+#define PHFEM_CH_GRID_MULT 64
+#endif
 #ifndef PHFEM_LV_MIN_BLOCKS
 #define PHFEM_LV_MIN_BLOCKS 7
 #endif
@@ -292,11 +298,10 @@ __device__ __forceinline__ LvRec lv_load_rec(const LvArgs& a, int le) {
   return r;
 }
 
-__device__ __forceinline__ LvGat lv_load_gat(const LvArgs& a, const LvRec& r, bool valid) {
+__device__ __forceinline__ LvGat lv_load_gat(const LvArgs& a, const LvRec& r, bool valid, int le) {
   LvGat g;
   g.pj1 = g.pj2 = g.qk1 = g.qk2 = 0;
   g.vop = g.vom = 0;
-  const int le = (int)(blockIdx.x * kLvT + threadIdx.x);
   if (a.side) {  // distributed: the element owners' side records, coalesced (local mode: own slots gathered)
     if (valid) {
       const int4 sp = side_of(a.side, le, 0, r.el.x, r.l, a.own_el, a.own_ee, a.own_lo, a.own_hi);
@@ -527,7 +532,7 @@ __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a
   const int le = blockIdx.x * kLvT + threadIdx.x;
   const bool valid = le < a.E;
   const LvRec r = lv_load_rec<kFull>(a, le);
-  const LvGat g = lv_load_gat(a, r, valid);
+  const LvGat g = lv_load_gat(a, r, valid, le);
   const LvCrd c = lv_load_crd(a, r, g, valid);
   lv_tile<kFull>(a, o, s, blockIdx.x, r, g, c);
 }
@@ -707,7 +712,7 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
     PHFEM_TRY(launch_level<false>(ctx, a, o, ntiles));
   }
   if (write_elems && parent->nE > 0)
-    PHFEM_LAUNCH(ctx, "k_refine_children", k_refine_children<<<grid_for(parent->nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH(ctx, "k_refine_children", k_refine_children<<<grid_for(parent->nE, 256, ctx->num_sms * PHFEM_CH_GRID_MULT), 256, 0, ctx->stream>>>(
         parent->elements, ptopo->elem_edge, topo->node_edge_start, rk, parent->nE, parent->nC,
         (int4*)fine->elements, (int4*)topo->elem_edge));
   dfree(ctx, rk);
