@@ -899,14 +899,11 @@ struct ColSmem {
 // that a warp's 32 nodes sort / walk equally many occurrences — an extra
 // histogram pass and the slot indirection cost more than the divergence they
 // remove: L12 tile 0.885 -> 0.990 ms.)
-__global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_col(
-    const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets, EgParams P,
-    int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
-    phfem_dev_errors* err, int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  ColSmem& sm = *reinterpret_cast<ColSmem*>(smraw);
+__device__ __forceinline__ void eg_tile_col_body(
+    int tile, ColSmem& sm, const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets,
+    const EgParams& P, int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB,
+    const EgOut& out, phfem_dev_errors* err, int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count) {
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
   sm.cur[tid] = 0;
   sm.col[tid] = 0ull;
   const int nsub = kTileNodes >> P.bs;
@@ -1018,6 +1015,23 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_
   }
 }
 
+__global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_col(
+    const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets, EgParams P,
+    int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
+    phfem_dev_errors* err, int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count, int ntiles) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ColSmem& sm = *reinterpret_cast<ColSmem*>(smraw);
+#if PHFEM_COL_GRID_MULT
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    eg_tile_col_body(tile, sm, items, boff, nbuckets, P, rec, tileE, tileB, out, err, fb_list, fb_count);
+    __syncthreads();  // the tile's SMEM columns read before the next tile fills them
+  }
+#else
+  (void)ntiles;
+  eg_tile_col_body(blockIdx.x, sm, items, boff, nbuckets, P, rec, tileE, tileB, out, err, fb_list, fb_count);
+#endif
+}
+
 // E ------------------------------------------------------------------------
 // One CTA per tile: the tile's edge records (consecutive, tile-local) become
 // the final outputs at the scanned tile offsets — coalesced record reads and
@@ -1031,14 +1045,19 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
                                                           int nbuckets, int nsub,
                                                           const int32_t* __restrict__ tileE,
                                                           const int32_t* __restrict__ tileB, int nC,
-                                                          EgOut out) {
+                                                          EgOut out, int ntiles) {
+#if PHFEM_EMIT_GRID_MULT
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  __syncthreads();  // nscan of the previous tile consumed
+#else
   const int tile = blockIdx.x;
+#endif
   const int64_t s = boff[min(tile * nsub, nbuckets)];
   const int E0 = tileE[tile], ne = tileE[tile + 1] - E0;
   const int B0 = tileB[tile];
   const int64_t vme = (int64_t)tile * kTileNodes + threadIdx.x;
   if (vme < nC) out.node_edge_start[vme] += E0;
-  if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
+  if (tile == ntiles - 1 && threadIdx.x == 0) out.node_edge_start[nC] = E0 + ne;
   // one record per thread, 4 in flight: no scan (records carry their
   // tile-local boundary prefix); the fused classification + C also needs
   // the Neumann edges before each record: one packed block scan per trip
@@ -1156,6 +1175,9 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
       }
     }
   }
+#if PHFEM_EMIT_GRID_MULT
+  }
+#endif
 }
 
 __global__ void k_eg_tile_max(const int32_t* __restrict__ boff, int nbuckets, int nsub, int ntiles,
@@ -1362,8 +1384,13 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     PHFEM_CUDA(ctx, cudaMemsetAsync(fb, 0, sizeof(int32_t), ctx->stream));
     const size_t csmem = sizeof(ColSmem);
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_col, csmem, "k_eg_tile_col smem opt-in"));
-    PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile_col<<<ntiles, kTileThreads, csmem, ctx->stream>>>(
-        items, tboff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb));
+#if PHFEM_COL_GRID_MULT
+    const int64_t col_grid = std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * PHFEM_COL_GRID_MULT);
+#else
+    const int64_t col_grid = ntiles;
+#endif
+    PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile_col<<<(unsigned)col_grid, kTileThreads, csmem, ctx->stream>>>(
+        items, tboff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb, (int)ntiles));
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_list, smem, "k_eg_tile_list smem opt-in"));
     PHFEM_LAUNCH(ctx, "k_eg_tile_list", k_eg_tile_list<<<ctx->num_sms * 4, kTileThreads, smem, ctx->stream>>>(
         fb + 1, fb, items, tboff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
@@ -1406,8 +1433,13 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     o.val = C->values;
     o.L = (int)L;
   }
-  PHFEM_LAUNCH(ctx, "k_eg_emit", k_eg_emit<<<ntiles, kEmitThreads, 0, ctx->stream>>>(
-      rec, boff, P.nb, nsub, tileE, tileB, (int)nC, o));
+#if PHFEM_EMIT_GRID_MULT
+  const int64_t emit_grid = std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * PHFEM_EMIT_GRID_MULT);
+#else
+  const int64_t emit_grid = ntiles;
+#endif
+  PHFEM_LAUNCH(ctx, "k_eg_emit", k_eg_emit<<<(unsigned)emit_grid, kEmitThreads, 0, ctx->stream>>>(
+      rec, boff, P.nb, nsub, tileE, tileB, (int)nC, o, (int)ntiles));
   // totals ride back with the error words (low 32 bits of counters 0 / 2)
   PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[0], tileE + ntiles, sizeof(int32_t),
                                   cudaMemcpyDeviceToDevice, ctx->stream));
