@@ -12,6 +12,11 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+// grid of the peer-window exchange kernels (CTAs per SM)
+#ifndef PHFEM_P2P_GRID_MULT
+#define PHFEM_P2P_GRID_MULT 8
+#endif
+
 namespace phfem {
 
 __device__ __forceinline__ int dest_of(const int32_t* __restrict__ splits, int W, int v) {
@@ -766,7 +771,7 @@ PHFEM_API phfem_status phfem_dist_side_p2p_ex(phfem_ctx* ctx, const int32_t* ele
     return PHFEM_ERR_INVALID_ARGUMENT;
   PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_side_p2p", k_dist_side_p2p<<<grid_for(3 * (int64_t)n, 256, ctx->num_sms * 8), 256, 0,
+    PHFEM_LAUNCH(ctx, "k_dist_side_p2p", k_dist_side_p2p<<<grid_for(3 * (int64_t)n, 256, ctx->num_sms * PHFEM_P2P_GRID_MULT), 256, 0,
                                                            ctx->stream>>>(
         elements, elem_edge, n, esplits, W, self, reinterpret_cast<int4* const*>(peer_side), remote, skip_self));
   return PHFEM_OK;
@@ -788,7 +793,7 @@ PHFEM_API phfem_status phfem_dist_start_p2p_ex(phfem_ctx* ctx, const phfem_topol
   PHFEM_CUDA(ctx, cudaMemsetAsync(remote, 0, sizeof(int32_t) * W, ctx->stream));
   const int E = ppart->E;
   if (E > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_start_p2p", k_dist_start_p2p<<<grid_for(2 * (int64_t)E, 256, ctx->num_sms * 8), 256, 0,
+    PHFEM_LAUNCH(ctx, "k_dist_start_p2p", k_dist_start_p2p<<<grid_for(2 * (int64_t)E, 256, ctx->num_sms * PHFEM_P2P_GRID_MULT), 256, 0,
                                                              ctx->stream>>>(
         ppart->edge_elements, ppart->local_in_tplus, ppart->local_in_tminus, fine_nes, nes_off, rk, E, psplits, W,
         self, peer_gs, peer_grk, remote, skip_self));

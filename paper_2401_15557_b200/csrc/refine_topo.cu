@@ -1376,7 +1376,7 @@ PHFEM_API phfem_status phfem_dist_children_slots_ex(phfem_ctx* ctx, const int32_
       (fine_nes && own_hi > own_lo && !rk))
     return PHFEM_ERR_INVALID_ARGUMENT;
   if (n > 0)
-    PHFEM_LAUNCH(ctx, "k_dist_children_slots", k_dist_children_slots<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0,
+    PHFEM_LAUNCH(ctx, "k_dist_children_slots", k_dist_children_slots<<<grid_for(n, 256, ctx->num_sms * PHFEM_CH_GRID_MULT), 256, 0,
                                                                        ctx->stream>>>(
         elements, elem_edge, gs, grk, n, nc, own_lo, own_hi, fine_nes, nes_off, rk, (double2*)coords_fine,
         reinterpret_cast<int4*>(children), reinterpret_cast<int4*>(fine_elem_edge)));
