@@ -884,6 +884,11 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
 #ifndef PHFEM_COL_MIN_BLOCKS
 #define PHFEM_COL_MIN_BLOCKS 7
 #endif
+// item loads in flight per thread in the column scatter (measured at L12 /
+// given L13: 1 -> 0.884 / 3.51 ms, 2 -> 0.866 / 3.44, 4 -> 0.855 / 3.40)
+#ifndef PHFEM_COL_LD
+#define PHFEM_COL_LD 4
+#endif
 #ifndef PHFEM_COL_K
 #define PHFEM_COL_K 13  // occurrences per node (refined meshes: <= 12); 14 rows of 2 KB: 7 CTAs per SM
 #endif
@@ -918,12 +923,29 @@ __device__ __forceinline__ void eg_tile_col_body(
       if (b >= nbuckets) break;
       const int base = b * P.fcap;
       const int cnt = sm.sbo[sub] - base;
+#if PHFEM_COL_LD > 1
+      // PHFEM_COL_LD item loads in flight per thread before their column slots
+      for (int p0 = tid; p0 < cnt; p0 += PHFEM_COL_LD * kTileThreads) {
+        uint64_t it[PHFEM_COL_LD];
+#pragma unroll
+        for (int u = 0; u < PHFEM_COL_LD; ++u)
+          if (p0 + u * kTileThreads < cnt) it[u] = __ldg(items + base + p0 + u * kTileThreads);
+#pragma unroll
+        for (int u = 0; u < PHFEM_COL_LD; ++u)
+          if (p0 + u * kTileThreads < cnt) {
+            const int nd = (sub << P.bs) | (int)(it[u] >> P.total_bits);
+            const int j = atomicAdd(&sm.cur[nd], 1);
+            if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it[u];
+          }
+      }
+#else
       for (int p = tid; p < cnt; p += kTileThreads) {
         const uint64_t it = __ldg(items + base + p);
         const int nd = (sub << P.bs) | (int)(it >> P.total_bits);
         const int j = atomicAdd(&sm.cur[nd], 1);
         if (j < kColK2) sm.col[(j + 1) * kTileNodes + nd] = it;
       }
+#endif
     }
   } else {
     s = sm.sbo[0];
