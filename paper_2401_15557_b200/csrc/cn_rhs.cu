@@ -92,7 +92,8 @@ struct CnArgs {
 
 constexpr int kCnThreads = 128;
 // k_cn_rows grid (measured at L11: 8 CTAs per SM 0.099 ms; 32 / 128 / 1024
-// per SM 0.106 / 0.107 / 0.111 ms)
+// per SM 0.106 / 0.107 / 0.111 ms; two rows per trip with the six U values
+// loaded unconditionally: 0.107 ms)
 #ifndef PHFEM_CNR_GRID_MULT
 #define PHFEM_CNR_GRID_MULT 8
 #endif
