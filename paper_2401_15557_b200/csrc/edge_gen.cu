@@ -153,6 +153,40 @@ __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restr
         valid = false;
       }
     }
+#if PHFEM_SC_BATCH
+    // the three occurrences' bucket claims issued back to back (three global
+    // atomics in flight per warp), then their slots
+    unsigned key[3], grp[3];
+    int base[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      key[s] = valid ? ((unsigned)(a > b ? a : b) >> P.bs) : 0xffffffffu;
+      grp[s] = __match_any_sync(0xffffffffu, key[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      base[s] = 0;
+      if (valid && (int)lane_id() == __ffs(grp[s]) - 1) base[s] = atomicAdd(&cursor[key[s]], __popc(grp[s]));
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      const int hi = a > b ? a : b;
+      const int lo = a > b ? b : a;
+      const int bs_ = __shfl_sync(0xffffffffu, base[s], __ffs(grp[s]) - 1);
+      if (valid) {
+        const int rank = __popc(grp[s] & lanemask_lt());
+        const int64_t at = (int64_t)bs_ + rank;
+        const int64_t end = ((int64_t)key[s] + 1) * P.fcap;
+        if (at < end) {
+          const uint32_t occ = (uint32_t)(3 * m + s);
+          items[at] = eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
+        }
+        fill_max = max(fill_max, (unsigned)(at + 1 - (end - P.fcap)));
+      }
+    }
+#else
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       const int a = t[s], b = t[(s + 1) % 3];
@@ -175,6 +209,7 @@ __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restr
         fill_max = max(fill_max, (unsigned)(at + 1 - (end - P.fcap)));
       }
     }
+#endif
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) fill_max = max(fill_max, __shfl_xor_sync(0xffffffffu, fill_max, o));
