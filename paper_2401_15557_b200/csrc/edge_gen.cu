@@ -127,11 +127,12 @@ __global__ void __launch_bounds__(256) k_eg_scatter(const int32_t* __restrict__ 
 // pass is made here (first bad element -> misc) and the fullest bucket's
 // fill is reported (counters[3]) — above fcap the caller falls back to the
 // counted layout.
-// (measured at L12: 8 CTAs per SM 0.320 ms, 32 / 128 / 512 per SM 0.325 /
-// 0.400 / 0.844 ms — the bucket cursors' atomics, not the stores, bound it;
-// the next element's vertex loads prefetched: no change, 0.319 ms)
+// (measured at L12 before the batched claims: 8 CTAs per SM 0.320 ms, 32 /
+// 128 / 512 per SM 0.325 / 0.400 / 0.844 ms — the bucket cursors' atomics,
+// not the stores, bound it; the next element's vertex loads prefetched: no
+// change; with the batched claims 8 / 16 per SM 0.298 / 0.296 ms)
 #ifndef PHFEM_SC_GRID_MULT
-#define PHFEM_SC_GRID_MULT 8
+#define PHFEM_SC_GRID_MULT 16
 #endif
 __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restrict__ elements,
                                                           EgParams P, int32_t* __restrict__ cursor,
@@ -153,9 +154,10 @@ __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restr
         valid = false;
       }
     }
-#if PHFEM_SC_BATCH
     // the three occurrences' bucket claims issued back to back (three global
-    // atomics in flight per warp), then their slots
+    // atomics in flight per warp), then their slots (measured: claim -> shuffle
+    // -> store per occurrence serialised the atomics' round trips; L12 scatter
+    // 0.319 -> 0.296 ms, given L13 1.244 -> 1.147 ms with 16 CTAs per SM)
     unsigned key[3], grp[3];
     int base[3];
 #pragma unroll
@@ -186,30 +188,6 @@ __global__ void __launch_bounds__(256) k_eg_scatter_fixed(const int32_t* __restr
         fill_max = max(fill_max, (unsigned)(at + 1 - (end - P.fcap)));
       }
     }
-#else
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int a = t[s], b = t[(s + 1) % 3];
-      const int hi = a > b ? a : b;
-      const int lo = a > b ? b : a;
-      const unsigned key = valid ? ((unsigned)hi >> P.bs) : 0xffffffffu;
-      const unsigned grp = __match_any_sync(0xffffffffu, key);
-      const int leader = __ffs(grp) - 1;
-      int base = 0;
-      if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (valid) {
-        const int rank = __popc(grp & lanemask_lt());
-        const int64_t at = (int64_t)base + rank;
-        const int64_t end = ((int64_t)key + 1) * P.fcap;
-        if (at < end) {
-          const uint32_t occ = (uint32_t)(3 * m + s);
-          items[at] = eg_pack(P, (uint32_t)hi & hl_mask, (uint32_t)lo, occ, a > b ? 1u : 0u);
-        }
-        fill_max = max(fill_max, (unsigned)(at + 1 - (end - P.fcap)));
-      }
-    }
-#endif
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) fill_max = max(fill_max, __shfl_xor_sync(0xffffffffu, fill_max, o));
