@@ -1697,17 +1697,28 @@ __global__ void __launch_bounds__(256) k_dist_scatter_p2p(const int32_t* __restr
       t[1] = __ldg(elements + 3 * m + 1);
       t[2] = __ldg(elements + 3 * m + 2);
     }
+    // the three claims in flight together (as in k_eg_scatter_fixed)
+    unsigned keys[3], grps[3];
+    int bases[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int a = t[s], b = t[(s + 1) % 3];
+      keys[s] = valid ? ((unsigned)(a > b ? a : b) >> P.bs) : 0xffffffffu;
+      grps[s] = __match_any_sync(0xffffffffu, keys[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      bases[s] = 0;
+      if (valid && (int)lane_id() == __ffs(grps[s]) - 1) bases[s] = atomicAdd(&cursor[keys[s]], __popc(grps[s]));
+    }
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       const int a = t[s], b = t[(s + 1) % 3];
       const int hi = a > b ? a : b;
       const int lo = a > b ? b : a;
-      const unsigned key = valid ? ((unsigned)hi >> P.bs) : 0xffffffffu;
-      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const unsigned key = keys[s], grp = grps[s];
       const int leader = __ffs(grp) - 1;
-      int base = 0;
-      if (valid && (int)lane_id() == leader) base = atomicAdd(&cursor[key], __popc(grp));
-      base = __shfl_sync(0xffffffffu, base, leader);
+      const int base = __shfl_sync(0xffffffffu, bases[s], leader);
       if (valid) {
         const int d = bucket_owner(bsplits, W, key);
         const uint32_t occ = (uint32_t)(3 * ((int64_t)elo + m) + s);
