@@ -247,7 +247,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "triangles/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"config5 pipeline sample: square L{level} -> L{level + 1}, "
                                f"{P} concurrent single-threaded samples", "triangles_per_sample": nE},
@@ -469,7 +469,7 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": "triangles/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config5: square L{args.level - 1} -> L{args.level} "
                                f"({s['nE']} triangles): EG+RF+EG+AS, config-2 coefficients",
