@@ -636,7 +636,12 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
         const int lo = i2 < j ? i2 : j, hi = i2 < j ? j : i2;  // B from the upper triangle
         const double bij = g.area * (rx[lo] * g.gx[hi] + ry[lo] * g.gy[hi]);
         const double t = (i2 == j ? ud : uo) + a.s_top * ((bij + dj[j]) + (i2 == j ? md : mo));
-        T[3 * j + i2] = 0.0 + 1.0 * t;  // from_triplets stores 0.0 + value
+        // from_triplets stores 0.0 + value; that only turns -0 into +0, and
+        // T / cv3 feed nothing but products added to an accumulator that
+        // starts at +0.0 — a +-0 product leaves it unchanged either way, so
+        // the add is dropped (same bits; hybrid pass
+        // 0.254 -> 0.249 ms at L11)
+        T[3 * j + i2] = t;
       }
     double cv3[3], lq[3];
     int rp[3];
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
       const double2 pa = v[(k + 1) % 3], pb = v[(k + 2) % 3];
       const double dx = pb.x - pa.x, dy = pb.y - pa.y;
       const double len = sqrt(dx * dx + dy * dy);
-      cv3[k] = 0.0 + a.s_ct * ((rpx[k] & 1) ? -len * 0.5 : len * 0.5);  // assembly.cpp:160,164
+      cv3[k] = a.s_ct * ((rpx[k] & 1) ? -len * 0.5 : len * 0.5);  // assembly.cpp:160,164 (0.0 + dropped, above)
       rp[k] = rpx[k] >> 1;  // -1 stays -1
       lq[k] = S.lq[3 * tid + k];
     }
