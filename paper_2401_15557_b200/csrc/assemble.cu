@@ -74,6 +74,8 @@ __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base,
 
 template <bool kBlocks, bool kLoad, int FK, int CK>
 __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a, phfem_dev_errors* err) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) double wbuf[kVolWarps][32 * 9];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* buf = wbuf[warp];
@@ -165,7 +167,7 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
   const int fk = !load ? kKindGeneric : (a.samples ? kKindSamples : field_kind_spec(a.f));
   const int ck = a.coeffs.kind == PHFEM_COEFF_CENTROID_POLY ? PHFEM_COEFF_CENTROID_POLY : PHFEM_COEFF_CONST;
 #define PHFEM_VOL(B, L, F, K) \
-  PHFEM_LAUNCH(ctx, "k_volume", (k_volume<B, L, F, K><<<grid, kVolThreads, 0, ctx->stream>>>(a, ctx->derr)))
+  PHFEM_LAUNCH_PDL(ctx, "k_volume", (k_volume<B, L, F, K>), grid, kVolThreads, 0, a, ctx->derr)
 #define PHFEM_VOL_CK(B, L, F)                                                            \
   do {                                                                                   \
     if (ck == PHFEM_COEFF_CENTROID_POLY) PHFEM_VOL(B, L, F, PHFEM_COEFF_CENTROID_POLY); \
@@ -369,6 +371,8 @@ __global__ void k_csc_fill(const double2* __restrict__ coords, const int32_t* __
 __global__ void k_neu_insert(const int32_t* __restrict__ neu_ids, int nN,
                              const int32_t* __restrict__ edge_elements, int cap,
                              int32_t* __restrict__ keys, int32_t* __restrict__ slot_of) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nN;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int m = edge_elements[2 * neu_ids[i]];
@@ -400,6 +404,8 @@ __device__ __forceinline__ void neu_entry(const NeuArgs& a, int64_t i, double t,
 }
 
 __global__ void k_neu_values(NeuArgs a, double t, int seq, phfem_dev_errors* err) {
+  pdl_wait();
+  pdl_trigger();
   if (seq) {  // exact list-order accumulation (duplicated pairs)
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     for (int64_t i = 0; i < a.nN; ++i) {
@@ -422,6 +428,8 @@ __global__ void k_neu_values(NeuArgs a, double t, int seq, phfem_dev_errors* err
 
 __global__ void k_neu_apply(const int32_t* __restrict__ keys, const double* __restrict__ vals,
                             int cap, double* __restrict__ out, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int m = keys[s];
@@ -519,6 +527,8 @@ __global__ void k_dirichlet(const double2* __restrict__ coords, const int32_t* _
                             const int32_t* __restrict__ dir_ids, int nD,
                             const int32_t* __restrict__ rpos, phfem_field uD, double t,
                             double* __restrict__ out, const double* __restrict__ samples) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nD;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int e = dir_ids[i];

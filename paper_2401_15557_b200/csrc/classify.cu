@@ -21,6 +21,8 @@ __global__ void k_cls_pairs(const int32_t* __restrict__ dir_pairs, int nD,
                             const int32_t* __restrict__ edge_elements, int nC,
                             int32_t* __restrict__ dir_ids, int32_t* __restrict__ neu_ids,
                             uint32_t* __restrict__ bits, phfem_dev_errors* err) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)nD + nN;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -54,6 +56,8 @@ __global__ void k_cls_pairs(const int32_t* __restrict__ dir_pairs, int nD,
 __global__ void k_cls_block_counts(const uint32_t* __restrict__ bits,
                                    const int32_t* __restrict__ boundary, int nB, int E, int nblk, int base,
                                    int32_t* __restrict__ cnt_bnd, int32_t* __restrict__ cnt_neu) {
+  pdl_wait();
+  pdl_trigger();
   const int blk = blockIdx.x * blockDim.x + threadIdx.x;
   if (blk > nblk) return;
   if (blk == nblk) {
@@ -85,6 +89,8 @@ __global__ void __launch_bounds__(256) k_cls_retained(const uint32_t* __restrict
                                                       const int32_t* __restrict__ pre_neu,
                                                       int E, int32_t* __restrict__ rpos,
                                                       int32_t* __restrict__ redges, int r_off, int e_off) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t wpre[32];
   const int blk = blockIdx.x;
   const int nwords = (E + 31) >> 5;
@@ -147,16 +153,16 @@ static phfem_status block_prefix_and_retained(phfem_ctx* ctx, const phfem_topolo
   const int E = topo->E;
   int32_t* pre_bnd = out->block_prefix;
   int32_t* pre_neu = out->block_prefix + nblk + 1;
-  PHFEM_LAUNCH(ctx, "k_cls_block_counts", k_cls_block_counts<<<grid_for(nblk + 1, 256, 1 << 20), 256, 0, ctx->stream>>>(
-      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, bnd_base, pre_bnd, pre_neu));
+  PHFEM_LAUNCH_PDL(ctx, "k_cls_block_counts", k_cls_block_counts, grid_for(nblk + 1, 256, 1 << 20), 256, 0,
+      out->neumann_bits, topo->boundary_edges, topo->n_boundary, E, nblk, bnd_base, pre_bnd, pre_neu);
   {
     const int32_t* in[2] = {pre_bnd, pre_neu};
     int32_t* io[2] = {pre_bnd, pre_neu};
     PHFEM_TRY(scan_exclusive_i32_set(ctx, 2, in, io, nblk + 1, nullptr));
   }
   if (nblk > 0 && with_retained) {
-    PHFEM_LAUNCH(ctx, "k_cls_retained", k_cls_retained<<<nblk, 256, 0, ctx->stream>>>(out->neumann_bits, pre_neu, E,
-                                                         out->retained_pos, out->retained_edges, r_off, e_off));
+    PHFEM_LAUNCH_PDL(ctx, "k_cls_retained", k_cls_retained, nblk, 256, 0, out->neumann_bits, pre_neu, E,
+                     out->retained_pos, out->retained_edges, r_off, e_off);
   }
   return PHFEM_OK;
 }
@@ -184,10 +190,10 @@ phfem_status classify_lists(phfem_ctx* ctx, const phfem_topology* topo, const ph
                                   ctx->stream));
   PHFEM_TRY(errors_reset(ctx));
   if ((int64_t)nD + nN > 0) {
-    PHFEM_LAUNCH(ctx, "k_cls_pairs", k_cls_pairs<<<grid_for((int64_t)nD + nN, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH_PDL(ctx, "k_cls_pairs", k_cls_pairs, grid_for((int64_t)nD + nN, 256, ctx->num_sms * 4), 256, 0,
         mesh->dirichlet, nD, mesh->neumann, nN, topo->node_edge_start, topo->edge_nodes,
         topo->edge_elements, topo->nC, out->dirichlet_edge_ids, out->neumann_edge_ids,
-        out->neumann_bits, ctx->derr));
+        out->neumann_bits, ctx->derr);
   }
   PHFEM_TRY(block_prefix_and_retained(ctx, topo, out, nblk, with_retained));
   // total Neumann count rides back with the error words (one sync)

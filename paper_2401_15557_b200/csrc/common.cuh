@@ -108,6 +108,38 @@ phfem_status cuda_fail(phfem_ctx* ctx, cudaError_t e, const char* where);
     PHFEM_CHECK_LAUNCH(ctx);                \
   } while (0)
 
+// Programmatic dependent launch (sm_90+).  A kernel launched through
+// PHFEM_LAUNCH_PDL may be scheduled while its predecessor on the stream is
+// still draining (its CTAs wait in pdl_wait() until the predecessor grid has
+// completed and its writes are visible), so the launch latency of a chain of
+// short kernels overlaps the previous kernel's tail.  Every kernel launched
+// that way calls pdl_wait() before its first global access and then
+// pdl_trigger() (its own dependents may launch once all its CTAs started);
+// both are no-ops in a normal launch.  PHFEM_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+// PDL-chained zero fill of int32 / 16-byte-aligned device copy (ctx.cu)
+phfem_status zero_i32(phfem_ctx* ctx, int32_t* p, int64_t n);
+phfem_status copy_d2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+#define PHFEM_LAUNCH_PDL(ctx, name, kern, grid, block, smem, ...)                               \
+  do {                                                                                          \
+    ::phfem::KTimer _kt(ctx, name);                                                             \
+    cudaLaunchConfig_t _cfg = {};                                                               \
+    _cfg.gridDim = dim3(grid);                                                                  \
+    _cfg.blockDim = dim3(block);                                                                \
+    _cfg.dynamicSmemBytes = (smem);                                                             \
+    _cfg.stream = (ctx)->stream;                                                                \
+    cudaLaunchAttribute _at[1];                                                                 \
+    _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                             \
+    _at[0].val.programmaticStreamSerializationAllowed = ::phfem::pdl_enabled() ? 1 : 0;         \
+    _cfg.attrs = _at;                                                                           \
+    _cfg.numAttrs = 1;                                                                          \
+    cudaLaunchKernelEx(&_cfg, kern, __VA_ARGS__);                                               \
+    PHFEM_CHECK_LAUNCH(ctx);                                                                    \
+  } while (0)
+
 #define PHFEM_TRY(expr)                 \
   do {                                  \
     phfem_status _s = (expr);           \

@@ -7,6 +7,46 @@
 
 namespace phfem {
 
+// Stream-ordered fill / copy as PDL-chained kernels (a memset / memcpy node
+// between two kernels would end the programmatic overlap of the chain).
+__global__ void k_zero_i32(int32_t* __restrict__ p, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0;
+}
+__global__ void k_copy16(int4* __restrict__ dst, const int4* __restrict__ src, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcs(src + i);
+}
+phfem_status zero_i32(phfem_ctx* ctx, int32_t* p, int64_t n) {
+  if (n <= 0) return PHFEM_OK;
+  PHFEM_LAUNCH_PDL(ctx, "k_zero_i32", k_zero_i32, grid_for(n, 256, ctx->num_sms * 8), 256, 0, p, n);
+  return PHFEM_OK;
+}
+phfem_status copy_d2d(phfem_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PHFEM_OK;
+  if (((uintptr_t)dst | (uintptr_t)src | bytes) & 15u) {
+    PHFEM_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    return PHFEM_OK;
+  }
+  const int64_t n = (int64_t)(bytes / 16);
+  PHFEM_LAUNCH_PDL(ctx, "k_copy16", k_copy16, grid_for(n, 256, ctx->num_sms * 32), 256, 0, (int4*)dst,
+                   (const int4*)src, n);
+  return PHFEM_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PHFEM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+
 phfem_status set_error(phfem_ctx* ctx, phfem_status st, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -260,6 +300,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t* in, i
 constexpr int64_t kScanSmall = 8 * kScanTile;
 __global__ void __launch_bounds__(kScanThreads) k_scan_small(const int32_t* in, int32_t* out, int64_t n,
                                                              int32_t* total) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t sm[33];
   int32_t carry = 0;
   for (int64_t c0 = 0; c0 < n; c0 += kScanTile) {
@@ -294,6 +336,8 @@ struct ScanSet {
 };
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_small_set(ScanSet S, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   const int a = blockIdx.x;
   const int32_t* in = S.in[a];
   int32_t* out = S.out[a];
@@ -322,6 +366,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_small_set(ScanSet S, int6
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums_set(ScanSet S, int64_t n, int32_t* __restrict__ sums,
                                                                      int64_t tiles) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t sm[33];
   const int a = blockIdx.y;
   const int32_t* in = S.in[a];
@@ -338,6 +384,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums_set(ScanSet S, 
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_sums_set(int32_t* sums, int64_t tiles, ScanSet S) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t sm[33];
   const int a = blockIdx.x;
   int32_t* sa = sums + a * tiles;
@@ -355,6 +403,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sums_set(int32_t* sums, i
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_down_set(ScanSet S, int64_t n,
                                                                 const int32_t* __restrict__ sums, int64_t tiles) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t sm[33];
   const int a = blockIdx.y;
   const int32_t* in = S.in[a];
@@ -394,21 +444,16 @@ phfem_status scan_exclusive_i32_set(phfem_ctx* ctx, int count, const int32_t* co
     return PHFEM_OK;
   }
   if (n <= kScanSmall) {
-    KTimer kt(ctx, "scan");
-    k_scan_small_set<<<count, kScanThreads, 0, ctx->stream>>>(S, n);
-    PHFEM_CHECK_LAUNCH(ctx);
+    PHFEM_LAUNCH_PDL(ctx, "scan", k_scan_small_set, count, kScanThreads, 0, S, n);
     return PHFEM_OK;
   }
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   int32_t* sums = nullptr;
   PHFEM_TRY(dalloc(ctx, &sums, tiles * count));
-  KTimer kt(ctx, "scan");
-  k_scan_tile_sums_set<<<dim3((unsigned)tiles, count), kScanThreads, 0, ctx->stream>>>(S, n, sums, tiles);
-  PHFEM_CHECK_LAUNCH(ctx);
-  k_scan_sums_set<<<count, kScanThreads, 0, ctx->stream>>>(sums, tiles, S);
-  PHFEM_CHECK_LAUNCH(ctx);
-  k_scan_down_set<<<dim3((unsigned)tiles, count), kScanThreads, 0, ctx->stream>>>(S, n, sums, tiles);
-  PHFEM_CHECK_LAUNCH(ctx);
+  PHFEM_LAUNCH_PDL(ctx, "scan", k_scan_tile_sums_set, dim3((unsigned)tiles, count), kScanThreads, 0, S, n, sums, tiles);
+  PHFEM_LAUNCH_PDL(ctx, "scan", k_scan_sums_set, count, kScanThreads, 0, sums, tiles, S);
+  PHFEM_LAUNCH_PDL(ctx, "scan", k_scan_down_set, dim3((unsigned)tiles, count), kScanThreads, 0, S, n,
+                   (const int32_t*)sums, tiles);
   dfree(ctx, sums);
   return PHFEM_OK;
 }
@@ -421,9 +466,7 @@ phfem_status scan_exclusive_i32(phfem_ctx* ctx, const int32_t* in, int32_t* out,
     return PHFEM_OK;
   }
   if (n <= kScanSmall) {  // in == out is fine: every thread reads its entries before writing them
-    KTimer kt(ctx, "scan");
-    k_scan_small<<<1, kScanThreads, 0, ctx->stream>>>(in, out, n, total_dev);
-    PHFEM_CHECK_LAUNCH(ctx);
+    PHFEM_LAUNCH_PDL(ctx, "scan", k_scan_small, 1, kScanThreads, 0, in, out, n, total_dev);
     return PHFEM_OK;
   }
   int32_t* sums = nullptr;

@@ -857,6 +857,8 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_TILE_MIN_BLOCKS) k_eg_tile
     const int32_t* __restrict__ boff, int nbuckets, EgParams P, uint64_t* g1, uint64_t* g2, uint8_t* gnode,
     int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
     phfem_dev_errors* err) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smraw);
   const int nl = *count;
@@ -1055,6 +1057,8 @@ __global__ void __launch_bounds__(kTileThreads, PHFEM_COL_MIN_BLOCKS) k_eg_tile_
     const uint64_t* __restrict__ items, const int32_t* __restrict__ boff, int nbuckets, EgParams P,
     int4* __restrict__ rec, int32_t* __restrict__ tileE, int32_t* __restrict__ tileB, EgOut out,
     phfem_dev_errors* err, int32_t* __restrict__ fb_list, int32_t* __restrict__ fb_count, int ntiles) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
   ColSmem& sm = *reinterpret_cast<ColSmem*>(smraw);
   // one CTA per tile (measured: a grid-stride loop over tiles with 16 / 64 /
@@ -1077,6 +1081,8 @@ __global__ void __launch_bounds__(kEmitThreads, PHFEM_EMIT_MIN_BLOCKS) k_eg_emit
                                                           const int32_t* __restrict__ tileE,
                                                           const int32_t* __restrict__ tileB, int nC,
                                                           EgOut out, int ntiles) {
+  pdl_wait();
+  pdl_trigger();
   // one CTA per tile (measured: a grid-stride loop over tiles with 16 / 64 /
   // 256 CTAs per SM, 0.68 / 0.62 / 0.58 ms against 0.57 at L12)
   const int tile = blockIdx.x;
@@ -1409,11 +1415,12 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     PHFEM_CUDA(ctx, cudaMemsetAsync(fb, 0, sizeof(int32_t), ctx->stream));
     const size_t csmem = sizeof(ColSmem);
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_col, csmem, "k_eg_tile_col smem opt-in"));
-    PHFEM_LAUNCH(ctx, "k_eg_tile", k_eg_tile_col<<<(unsigned)ntiles, kTileThreads, csmem, ctx->stream>>>(
-        items, tboff, P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb, (int)ntiles));
+    PHFEM_LAUNCH_PDL(ctx, "k_eg_tile", k_eg_tile_col, (unsigned)ntiles, kTileThreads, csmem,
+        (const uint64_t*)items, tboff, (int)P.nb, PT, rec, tileE, tileB, o, ctx->derr, fb + 1, fb, (int)ntiles);
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile_list, smem, "k_eg_tile_list smem opt-in"));
-    PHFEM_LAUNCH(ctx, "k_eg_tile_list", k_eg_tile_list<<<ctx->num_sms * 4, kTileThreads, smem, ctx->stream>>>(
-        fb + 1, fb, items, tboff, P.nb, PT, g1, g2, gnode, rec, tileE, tileB, o, ctx->derr));
+    PHFEM_LAUNCH_PDL(ctx, "k_eg_tile_list", k_eg_tile_list, ctx->num_sms * 4, kTileThreads, smem,
+        (const int32_t*)(fb + 1), (const int32_t*)fb, items, tboff, (int)P.nb, PT, g1, g2, gnode, rec,
+        tileE, tileB, o, ctx->derr);
     dfree(ctx, fb);
   } else {
     PHFEM_TRY(smem_optin(ctx, (const void*)k_eg_tile, smem, "k_eg_tile smem opt-in"));
@@ -1453,8 +1460,9 @@ static phfem_status eg_core(phfem_ctx* ctx, EgParams P, int64_t nd, Source sourc
     o.val = C->values;
     o.L = (int)L;
   }
-  PHFEM_LAUNCH(ctx, "k_eg_emit", k_eg_emit<<<(unsigned)ntiles, kEmitThreads, 0, ctx->stream>>>(
-      rec, boff, P.nb, nsub, tileE, tileB, (int)nC, o, (int)ntiles));
+  PHFEM_LAUNCH_PDL(ctx, "k_eg_emit", k_eg_emit, (unsigned)ntiles, kEmitThreads, 0,
+      (const int4*)rec, (const int32_t*)boff, (int)P.nb, (int)nsub, (const int32_t*)tileE, (const int32_t*)tileB,
+      (int)nC, o, (int)ntiles);
   // totals ride back with the error words (low 32 bits of counters 0 / 2)
   PHFEM_CUDA(ctx, cudaMemcpyAsync(&ctx->derr->counters[0], tileE + ntiles, sizeof(int32_t),
                                   cudaMemcpyDeviceToDevice, ctx->stream));

@@ -58,6 +58,8 @@ __global__ void k_refine_boundary(const int32_t* __restrict__ dpairs, int nD,
                                   const int32_t* __restrict__ edge_nodes, int nC,
                                   int4* __restrict__ dout, int4* __restrict__ nout,
                                   phfem_dev_errors* err) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)nD + nN;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -125,9 +127,7 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
   PHFEM_TRY(dalloc(ctx, &out->elements, 12 * nE));
   PHFEM_TRY(dalloc(ctx, &out->dirichlet, 4 * (int64_t)mesh->nD));
   PHFEM_TRY(dalloc(ctx, &out->neumann, 4 * (int64_t)mesh->nN));
-  if (nC > 0)
-    PHFEM_CUDA(ctx, cudaMemcpyAsync(out->coords, mesh->coords, sizeof(double) * 2 * nC,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  if (nC > 0) PHFEM_TRY(copy_d2d(ctx, out->coords, mesh->coords, sizeof(double) * 2 * nC));
   if (nE > 0 && !defer_elements) {
     PHFEM_LAUNCH(ctx, "k_refine_elements", k_refine_elements<<<grid_for(nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         (const double2*)mesh->coords, mesh->elements, topo->elem_edge, (int)nE, (int)nC,
@@ -135,9 +135,10 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
   }
   const int64_t nb = (int64_t)mesh->nD + mesh->nN;
   if (nb > 0 && deferred) {
-    PHFEM_LAUNCH(ctx, "k_refine_boundary", k_refine_boundary<<<grid_for(nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
-        mesh->dirichlet, mesh->nD, mesh->neumann, mesh->nN, topo->node_edge_start,
-        topo->edge_nodes, (int)nC, (int4*)out->dirichlet, (int4*)out->neumann, deferred));
+    PHFEM_LAUNCH_PDL(ctx, "k_refine_boundary", k_refine_boundary, grid_for(nb, 256, ctx->num_sms * 4), 256, 0,
+        (const int32_t*)mesh->dirichlet, (int)mesh->nD, (const int32_t*)mesh->neumann, (int)mesh->nN,
+        (const int32_t*)topo->node_edge_start, (const int32_t*)topo->edge_nodes, (int)nC, (int4*)out->dirichlet,
+        (int4*)out->neumann, deferred);
   } else if (nb > 0) {
     PHFEM_TRY(errors_reset(ctx));
     PHFEM_LAUNCH(ctx, "k_refine_boundary", k_refine_boundary<<<grid_for(nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(

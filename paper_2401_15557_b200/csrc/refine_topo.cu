@@ -220,6 +220,8 @@ __global__ void k_rl_tile_prep(int E, int ntiles, const int32_t* __restrict__ bo
                                const uint32_t* __restrict__ neu_bits, int32_t* __restrict__ tileF,
                                int32_t* __restrict__ tileB, int32_t* __restrict__ tileN,
                                const int32_t* __restrict__ elem_edge, int nE, int blocksA) {
+  pdl_wait();
+  pdl_trigger();
   if ((int)blockIdx.x < blocksA) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += blocksA * blockDim.x) {
       const int64_t l0 = (int64_t)t * kLvT;
@@ -528,6 +530,8 @@ __device__ __forceinline__ void lv_tile(const LvArgs& a, const LvOut& o, LvSmem<
 template <bool kFull>
 __global__ void __launch_bounds__(kLvT, PHFEM_LV_MIN_BLOCKS) k_rl_level(LvArgs a, LvOut o) {
   extern __shared__ __align__(16) unsigned char lv_smem[];  // dynamic: tiles may exceed 48 KB
+  pdl_wait();
+  pdl_trigger();
   LvSmem<kFull>& s = *reinterpret_cast<LvSmem<kFull>*>(lv_smem);
   const int le = blockIdx.x * kLvT + threadIdx.x;
   const bool valid = le < a.E;
@@ -556,6 +560,8 @@ __global__ void __launch_bounds__(256) k_refine_children(const int32_t* __restri
                                                          const uint8_t* __restrict__ rk, int nE, int nc,
                                                          int4* __restrict__ out_elems,
                                                          int4* __restrict__ out_ee) {
+  pdl_wait();
+  pdl_trigger();
   // rows staged per warp in SMEM, then stored as contiguous 512-byte warp
   // writes (a direct per-thread 48-byte row leaves every sector half written
   // per instruction: twice the L2 write transactions)
@@ -629,7 +635,7 @@ static phfem_status launch_level(phfem_ctx* ctx, const LvArgs& a, const LvOut& o
   const char* name = kFull ? "k_rl_level_full" : "k_rl_level";
   size_t smem = 0;
   PHFEM_TRY(lv_smem_bytes<kFull>(ctx, &smem));
-  PHFEM_LAUNCH(ctx, name, k_rl_level<kFull><<<(unsigned)ntiles, kLvT, smem, ctx->stream>>>(a, o));
+  PHFEM_LAUNCH_PDL(ctx, name, k_rl_level<kFull>, (unsigned)ntiles, kLvT, smem, a, o);
   return PHFEM_OK;
 }
 
@@ -653,14 +659,14 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
   int32_t* tiles = nullptr;
   PHFEM_TRY(dalloc(ctx, &tiles, 3 * (ntiles + 1)));
   int32_t *tileF = tiles, *tileB = tiles + (ntiles + 1), *tileN = tiles + 2 * (ntiles + 1);
-  PHFEM_CUDA(ctx, cudaMemsetAsync(tiles, 0, sizeof(int32_t) * 3 * (ntiles + 1), ctx->stream));
+  PHFEM_TRY(zero_i32(ctx, tiles, 3 * (ntiles + 1)));
   const uint32_t* nbits = pcls ? pcls->neumann_bits : nullptr;
   {
     const int blocksA = grid_for(ntiles, 256, ctx->num_sms * 8);
     const int blocksB = grid_for(parent->nE, 256, ctx->num_sms * 16);
-    PHFEM_LAUNCH(ctx, "k_rl_tile_count", k_rl_tile_prep<<<blocksA + blocksB, 256, 0, ctx->stream>>>(
+    PHFEM_LAUNCH_PDL(ctx, "k_rl_tile_count", k_rl_tile_prep, blocksA + blocksB, 256, 0,
         (int)E, (int)ntiles, ptopo->boundary_edges, ptopo->n_boundary, nbits, tileF, tileB, tileN, ptopo->elem_edge,
-        parent->nE, blocksA));
+        (int)parent->nE, blocksA);
   }
   {
     const int32_t* in[3] = {tileF, tileB, tileN};
@@ -712,9 +718,10 @@ static phfem_status refine_level_run(phfem_ctx* ctx, const phfem_mesh* parent,
     PHFEM_TRY(launch_level<false>(ctx, a, o, ntiles));
   }
   if (write_elems && parent->nE > 0)
-    PHFEM_LAUNCH(ctx, "k_refine_children", k_refine_children<<<grid_for(parent->nE, 256, ctx->num_sms * PHFEM_CH_GRID_MULT), 256, 0, ctx->stream>>>(
-        parent->elements, ptopo->elem_edge, topo->node_edge_start, rk, parent->nE, parent->nC,
-        (int4*)fine->elements, (int4*)topo->elem_edge));
+    PHFEM_LAUNCH_PDL(ctx, "k_refine_children", k_refine_children,
+        grid_for(parent->nE, 256, ctx->num_sms * PHFEM_CH_GRID_MULT), 256, 0,
+        (const int32_t*)parent->elements, (const int32_t*)ptopo->elem_edge, (const int32_t*)topo->node_edge_start,
+        (const uint8_t*)rk, (int)parent->nE, (int)parent->nC, (int4*)fine->elements, (int4*)topo->elem_edge);
   dfree(ctx, rk);
   dfree(ctx, tiles);
   return PHFEM_OK;
