@@ -569,6 +569,8 @@ template <int CK>
 __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs a, CnStored st, int64_t ntiles, double c0,
                                                      double c1, const double* __restrict__ W,
                                                      double* __restrict__ rhs) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char cn_smem[];
   CnHStage* stg = reinterpret_cast<CnHStage*>(cn_smem);
   double* outb = reinterpret_cast<double*>(cn_smem + kCnHStages * sizeof(CnHStage));
@@ -675,6 +677,8 @@ __global__ void __launch_bounds__(kCnTile, PHFEM_CN_HYB_BLOCKS) k_cn_hyb(CnArgs 
 __global__ void __launch_bounds__(256) k_cn_rows(const uint2* __restrict__ rowt, const double* __restrict__ rowh,
                                                   int L, double s_c, const double* __restrict__ W,
                                                   double* __restrict__ rhs_rows) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
        l += (int64_t)gridDim.x * blockDim.x) {
     const uint2 r = __ldcs(rowt + l);
@@ -709,6 +713,8 @@ __global__ void __launch_bounds__(256) k_cn_edges(CnArgs a, const int32_t* __res
                                                    const int32_t* __restrict__ ltp, int E,
                                                    const int32_t* __restrict__ ids,
                                                    const double* __restrict__ W, double* __restrict__ rhs) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = ids ? ids[i] : i;
@@ -929,11 +935,11 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
       // the recompute is latency-bound, so residency matters more than depth
       const int grid = (int)std::min<int64_t>(nfull, (int64_t)ctx->num_sms * PHFEM_CN_HYB_BLOCKS);
       if (a.c.kind == PHFEM_COEFF_CENTROID_POLY)
-        PHFEM_LAUNCH(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CENTROID_POLY><<<grid, kCnTile, kCnHybSmem, ctx->stream>>>(
-            a, st, nfull, c0, c1, state, rhs));
+        PHFEM_LAUNCH_PDL(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CENTROID_POLY>, grid, kCnTile, kCnHybSmem,
+            a, st, nfull, c0, c1, state, rhs);
       else
-        PHFEM_LAUNCH(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CONST><<<grid, kCnTile, kCnHybSmem, ctx->stream>>>(
-            a, st, nfull, c0, c1, state, rhs));
+        PHFEM_LAUNCH_PDL(ctx, "k_cn_hyb", k_cn_hyb<PHFEM_COEFF_CONST>, grid, kCnTile, kCnHybSmem,
+            a, st, nfull, c0, c1, state, rhs);
     } else if (nfull > 0) {
       const int grid = (int)std::min<int64_t>(nfull, (int64_t)ctx->num_sms * 2);
       PHFEM_LAUNCH(ctx, "k_cn_tma", k_cn_tma<<<grid, kCnTile, kCnTmaSmem, ctx->stream>>>(
@@ -956,11 +962,12 @@ PHFEM_API phfem_status phfem_cn_rhs(phfem_ctx* ctx, phfem_cn_plan* p, int n, con
     // (measured: the rows on a side stream beside the hybrid element pass,
     // 3 or 4 element CTAs per SM: step 0.373 ms either way)
     if (p->cls.L > 0)
-      PHFEM_LAUNCH(ctx, "k_cn_rows", k_cn_rows<<<grid_for(p->cls.L, 256, ctx->num_sms * PHFEM_CNR_GRID_MULT), 256, 0, ctx->stream>>>(
-          p->rowt, p->rowh, p->cls.L, a.s_c, state, rhs + a.N));
+      PHFEM_LAUNCH_PDL(ctx, "k_cn_rows", k_cn_rows, grid_for(p->cls.L, 256, ctx->num_sms * PHFEM_CNR_GRID_MULT), 256, 0,
+          (const uint2*)p->rowt, (const double*)p->rowh, (int)p->cls.L, a.s_c, state, rhs + a.N);
     if (p->cls.nD > 0)
-      PHFEM_LAUNCH(ctx, "k_cn_edges", k_cn_edges<<<grid_for(p->cls.nD, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-          a, p->topo.edge_nodes, p->topo.local_in_tplus, p->cls.nD, p->cls.dirichlet_edge_ids, state, rhs));
+      PHFEM_LAUNCH_PDL(ctx, "k_cn_edges", k_cn_edges, grid_for(p->cls.nD, 256, ctx->num_sms), 256, 0,
+          a, (const int32_t*)p->topo.edge_nodes, (const int32_t*)p->topo.local_in_tplus, (int)p->cls.nD,
+          (const int32_t*)p->cls.dirichlet_edge_ids, state, rhs);
     return PHFEM_OK;
   } else if (a.nE > 0) {
     const int64_t ntiles = ((int64_t)a.nE + kCnThreads - 1) / kCnThreads;
