@@ -57,9 +57,15 @@ __global__ void k_refine_boundary(const int32_t* __restrict__ dpairs, int nD,
                                   const int32_t* __restrict__ nes,
                                   const int32_t* __restrict__ edge_nodes, int nC,
                                   int4* __restrict__ dout, int4* __restrict__ nout,
-                                  phfem_dev_errors* err) {
+                                  phfem_dev_errors* err, int4* __restrict__ cdst = nullptr,
+                                  const int4* __restrict__ csrc = nullptr, int64_t ncopy = 0) {
   pdl_wait();
   pdl_trigger();
+  // the parent coordinates into the refined array (refine.cpp:16), in the
+  // same launch as the boundary pairs (one launch less per level)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncopy;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cdst[i] = __ldcs(csrc + i);
   const int64_t total = (int64_t)nD + nN;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -127,18 +133,23 @@ phfem_status red_refine_impl(phfem_ctx* ctx, const phfem_mesh* mesh, const phfem
   PHFEM_TRY(dalloc(ctx, &out->elements, 12 * nE));
   PHFEM_TRY(dalloc(ctx, &out->dirichlet, 4 * (int64_t)mesh->nD));
   PHFEM_TRY(dalloc(ctx, &out->neumann, 4 * (int64_t)mesh->nN));
-  if (nC > 0) PHFEM_TRY(copy_d2d(ctx, out->coords, mesh->coords, sizeof(double) * 2 * nC));
+  const int64_t nb = (int64_t)mesh->nD + mesh->nN;
+  // pipeline path: the coordinate copy rides in the boundary-pair launch
+  const bool fuse_copy = nb > 0 && deferred && nC > 0 &&
+                         (((uintptr_t)out->coords | (uintptr_t)mesh->coords) & 15u) == 0;
+  if (nC > 0 && !fuse_copy) PHFEM_TRY(copy_d2d(ctx, out->coords, mesh->coords, sizeof(double) * 2 * nC));
   if (nE > 0 && !defer_elements) {
     PHFEM_LAUNCH(ctx, "k_refine_elements", k_refine_elements<<<grid_for(nE, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         (const double2*)mesh->coords, mesh->elements, topo->elem_edge, (int)nE, (int)nC,
         (double2*)out->coords, (int4*)out->elements, write_mid ? 1 : 0));
   }
-  const int64_t nb = (int64_t)mesh->nD + mesh->nN;
   if (nb > 0 && deferred) {
-    PHFEM_LAUNCH_PDL(ctx, "k_refine_boundary", k_refine_boundary, grid_for(nb, 256, ctx->num_sms * 4), 256, 0,
+    const int64_t ncopy = fuse_copy ? (int64_t)nC : 0;  // 16-byte coordinate pairs
+    PHFEM_LAUNCH_PDL(ctx, "k_refine_boundary", k_refine_boundary,
+        grid_for(std::max<int64_t>(nb, ncopy), 256, ctx->num_sms * 32), 256, 0,
         (const int32_t*)mesh->dirichlet, (int)mesh->nD, (const int32_t*)mesh->neumann, (int)mesh->nN,
         (const int32_t*)topo->node_edge_start, (const int32_t*)topo->edge_nodes, (int)nC, (int4*)out->dirichlet,
-        (int4*)out->neumann, deferred);
+        (int4*)out->neumann, deferred, (int4*)out->coords, (const int4*)mesh->coords, ncopy);
   } else if (nb > 0) {
     PHFEM_TRY(errors_reset(ctx));
     PHFEM_LAUNCH(ctx, "k_refine_boundary", k_refine_boundary<<<grid_for(nb, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
