@@ -25,6 +25,10 @@
 //                     columns, insertion sort), item-parallel fast path (<= 32:
 //                     counting sort + in-segment rank sort) and a general path
 //                     (global scratch for oversized tiles or segments).
+//   (fixed-capacity layout, the default for element input: A and B are
+//    skipped — k_eg_fixed_init gives bucket b the item slots [b cap, ...),
+//    k_eg_scatter_fixed fills them and reports the fullest bucket; over
+//    capacity the counted layout above runs instead)
 //   E  scans          of the per-tile counts (no look-back: tiny arrays)
 //   F  k_eg_emit      one CTA per tile: records -> edge_nodes, edge_elements,
 //                     local indices, interior / boundary list slots, elem_edge,
