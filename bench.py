@@ -60,8 +60,11 @@ def kernel_bytes(name, s, p):
     nC, nE, E, L, nnz = s["nC"], s["nE"], s["E"], s["L"], s["nnz"]
     pC, pE, pEd = p["nC"], p["nE"], p["E"]
     return {
-        # B, D, M, M0 (4 x 72 B) + load (24 B) written; elements + coords read
-        "k_volume": 12 * nE + 16 * nC + 312 * nE,
+        # B, D, M, M0 (4 x 72 B) + load (24 B) written; the parent elements +
+        # parent coords read (the children's vertices are rebuilt from the
+        # parent, VolArgs::parents; PHFEM_VOL_PARENTS=0: 12 nE + 16 nC read)
+        "k_volume": (12 * nE + 16 * nC if os.environ.get("PHFEM_VOL_PARENTS") == "0"
+                     else 12 * pE + 16 * pC) + 312 * nE,
         # parent build_topology, sort pass: packed items in (3 x 8 B / element),
         # one 16-B edge record per edge + node_edge_start (4 B / node) out
         "k_eg_tile": 24 * pE + 16 * pEd + 4 * pC,

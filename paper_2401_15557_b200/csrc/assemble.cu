@@ -72,7 +72,11 @@ __device__ __forceinline__ void warp_store(double* __restrict__ g, int64_t base,
   }
 }
 
-template <bool kBlocks, bool kLoad, int FK, int CK>
+__device__ __forceinline__ double2 vol_mid(double2 p, double2 q) {
+  return make_double2(0.5 * (p.x + q.x), 0.5 * (p.y + q.y));  // refine.cpp:18
+}
+
+template <bool kBlocks, bool kLoad, int FK, int CK, bool kParent>
 __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a, phfem_dev_errors* err) {
   pdl_wait();
   pdl_trigger();
@@ -84,19 +88,31 @@ __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a
   // software pipeline: the vertex indices of chunk ch + 2 step and the
   // coordinates of chunk ch + step are in flight while chunk ch computes
   // (two chunks of coordinates in flight measured: config 4 unchanged at
-  // 10.27 ms with 5 CTAs/SM, 10.46 at 6; config 5 6.91 -> 7.20 / 7.61 ms)
+  // 10.27 ms with 5 CTAs/SM, 10.46 at 6; config 5 6.91 -> 7.20 / 7.61 ms).
+  // kParent: a chunk is 8 parents x 4 children (nE = 4 x parents, chunk bases
+  // are multiples of 32, so a group of 4 lanes is one parent); lane 4q + k
+  // (k = 1..3) loads parent vertex p_{k-1} and its coordinates, lane 4q idles;
+  // the group shares them by shuffles and recomputes the midpoints
+  const int k4 = lane & 3;
   auto ld_idx = [&](int64_t c, int& i0, int& i1, int& i2) {
     const int64_t m = c * 32 + lane;
     if (c < nchunks && m < a.nE) {
-      i0 = __ldg(a.elements + 3 * m);
-      i1 = __ldg(a.elements + 3 * m + 1);
-      i2 = __ldg(a.elements + 3 * m + 2);
+      if (kParent) {
+        i0 = k4 ? __ldg(a.parents + 3 * (m >> 2) + (k4 - 1)) : -2;
+      } else {
+        i0 = __ldg(a.elements + 3 * m);
+        i1 = __ldg(a.elements + 3 * m + 1);
+        i2 = __ldg(a.elements + 3 * m + 2);
+      }
     } else {
       i0 = -1;
     }
   };
   auto ld_xy = [&](int i0, int i1, int i2, double2& v0, double2& v1, double2& v2) {
-    if (i0 >= 0) {
+    if (kParent) {  // v0 only: this lane's parent vertex (a unit triangle on padding groups)
+      if (i0 >= 0) v0 = __ldg(a.coords + i0);
+      else v0 = make_double2(k4 == 2 ? 1.0 : 0.0, k4 == 3 ? 1.0 : 0.0);
+    } else if (i0 >= 0) {
       v0 = __ldg(a.coords + i0);
       v1 = __ldg(a.coords + i1);
       v2 = __ldg(a.coords + i2);
@@ -121,15 +137,26 @@ __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a
     double2 w0, w1, w2;
     ld_xy(n0, n1, n2, w0, w1, w2);
     ld_idx(ch + 2 * step, n0, n1, n2);
+    double2 c0 = v0, c1 = v1, c2 = v2;
+    if (kParent) {
+      const int g = lane & ~3;
+      const double2 p0 = make_double2(__shfl_sync(0xffffffffu, v0.x, g + 1), __shfl_sync(0xffffffffu, v0.y, g + 1));
+      const double2 p1 = make_double2(__shfl_sync(0xffffffffu, v0.x, g + 2), __shfl_sync(0xffffffffu, v0.y, g + 2));
+      const double2 p2 = make_double2(__shfl_sync(0xffffffffu, v0.x, g + 3), __shfl_sync(0xffffffffu, v0.y, g + 3));
+      const double2 m0 = vol_mid(p1, p2), m1 = vol_mid(p2, p0), m2 = vol_mid(p0, p1);
+      c0 = k4 == 0 ? m0 : k4 == 1 ? p0 : k4 == 2 ? p1 : p2;
+      c1 = k4 == 0 ? m1 : k4 == 1 ? m2 : k4 == 2 ? m0 : m1;
+      c2 = k4 == 0 ? m2 : k4 == 1 ? m1 : k4 == 2 ? m2 : m0;
+    }
     if (kLoad) {
       double bl[3];
-      element_load_dev<FK>(v0, v1, v2, a.f, a.t, bl, valid, m, err, a.samples);
+      element_load_dev<FK>(c0, c1, c2, a.f, a.t, bl, valid, m, err, a.samples);
       warp_store(a.load, base, n_valid, 3, bl, buf, a.vec);
     }
     if (kBlocks) {
-      const phfem_geom g = geometry_dev(v0.x, v0.y, v1.x, v1.y, v2.x, v2.y);
+      const phfem_geom g = geometry_dev(c0.x, c0.y, c1.x, c1.y, c2.x, c2.y);
       if (valid && !(g.t2 > 0.0)) atomicMin(&err->degenerate, (unsigned long long)m);
-      const phfem_coeff_values cv = coeffs_dev<CK>(a.coeffs, v0, v1, v2);
+      const phfem_coeff_values cv = coeffs_dev<CK>(a.coeffs, c0, c1, c2);
       double x[9];
       if (a.B) {
         phfem_stiffness(&g, &cv, x);
@@ -156,6 +183,7 @@ __global__ void __launch_bounds__(kVolThreads, kVolMinBlocks) k_volume(VolArgs a
 
 phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool load) {
   if (a.nE == 0) return PHFEM_OK;
+  if (a.parents && (a.nE & 3)) return set_error(ctx, PHFEM_ERR_INVALID_ARGUMENT, "k_volume: children count not 4 x parents");
   const int64_t nchunks = ((int64_t)a.nE + 31) / 32;
   // about kVolIters chunks per warp: a grid of many short-lived CTAs spreads
   // the concurrently written addresses over several windows of every output
@@ -168,8 +196,11 @@ phfem_status launch_volume(phfem_ctx* ctx, const VolArgs& a, bool blocks, bool l
                                           (nchunks + per_cta - 1) / per_cta);
   const int fk = !load ? kKindGeneric : (a.samples ? kKindSamples : field_kind_spec(a.f));
   const int ck = a.coeffs.kind == PHFEM_COEFF_CENTROID_POLY ? PHFEM_COEFF_CENTROID_POLY : PHFEM_COEFF_CONST;
-#define PHFEM_VOL(B, L, F, K) \
-  PHFEM_LAUNCH_PDL(ctx, "k_volume", (k_volume<B, L, F, K>), grid, kVolThreads, 0, a, ctx->derr)
+#define PHFEM_VOL(B, L, F, K)                                                                      \
+  do {                                                                                             \
+    if (a.parents) PHFEM_LAUNCH_PDL(ctx, "k_volume", (k_volume<B, L, F, K, true>), grid, kVolThreads, 0, a, ctx->derr); \
+    else PHFEM_LAUNCH_PDL(ctx, "k_volume", (k_volume<B, L, F, K, false>), grid, kVolThreads, 0, a, ctx->derr);         \
+  } while (0)
 #define PHFEM_VOL_CK(B, L, F)                                                            \
   do {                                                                                   \
     if (ck == PHFEM_COEFF_CENTROID_POLY) PHFEM_VOL(B, L, F, PHFEM_COEFF_CENTROID_POLY); \

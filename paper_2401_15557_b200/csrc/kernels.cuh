@@ -20,6 +20,13 @@ struct VolArgs {
   double* M0;
   double* load;
   const double* samples;  // host-sampled field values [3nE] (kind kKindSamples), else null
+  // non-null: `elements` are red_refine's children of these parent elements
+  // [3 nE/4] (refine.cpp:27-37: child 4p = (m0, m1, m2), 4p+1 = (p0, m2, m1),
+  // 4p+2 = (p1, m0, m2), 4p+3 = (p2, m1, m0)) and coords[0, parent nC) are the
+  // parent's nodes: k_volume gathers the 3 parent vertices and recomputes the
+  // midpoints 0.5 * (a + b) (refine.cpp:18, the same bits) instead of reading
+  // 12 B of elements and 3 coordinates per child
+  const int32_t* parents;
 };
 
 VolArgs make_vol_args(const phfem_mesh* mesh);

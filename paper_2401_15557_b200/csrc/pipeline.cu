@@ -46,6 +46,20 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   PHFEM_CUDA(ctx, cudaMemsetAsync(ctx->dderr, 0xff, sizeof(phfem_dev_errors), ctx->stream));
   phfem_topology topo;
   bool have_cls_C = false;
+  // the last level's parent mesh stays alive until the element pass: its
+  // elements and nodes let k_volume rebuild the children's vertices (3
+  // parent gathers per 4 children, VolArgs::parents); PHFEM_VOL_PARENTS=0
+  // reads the refined mesh instead
+  struct ParentKeep {
+    phfem_ctx* ctx;
+    phfem_mesh m;
+    bool live = false;
+    ~ParentKeep() {
+      if (live) phfem_mesh_release(ctx, &m);
+    }
+  } parent{ctx, {}};
+  const char* pv = getenv("PHFEM_VOL_PARENTS");
+  const bool vol_parents = !(pv && pv[0] == '0');
   phfem_status st;
   if (levels == 0) {  // the given mesh is the final one: classification + C fused into its edge pass
     st = build_topology_fused(ctx, &cur, &topo, &out->cls, &out->C);
@@ -93,7 +107,12 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
     tr("fine topology");
     phfem_classification_release(ctx, &pcls);
     phfem_topology_release(ctx, &topo);
-    phfem_mesh_release(ctx, &cur);
+    if (st == PHFEM_OK && l == levels - 1 && vol_parents) {
+      parent.m = cur;
+      parent.live = true;
+    } else {
+      phfem_mesh_release(ctx, &cur);
+    }
     tr("release parent");
     if (st != PHFEM_OK) return st;
     cur = next;
@@ -122,6 +141,7 @@ static phfem_status pipeline_impl(phfem_ctx* ctx, phfem_mesh cur, int levels,
   a.M0 = out->M0;
   a.load = out->load;
   a.vec = 2;  // pool allocations are 256-byte aligned (32-byte stores allowed)
+  if (parent.live && (int64_t)4 * parent.m.nE == nE) a.parents = parent.m.elements;
   PHFEM_TRY(launch_volume(ctx, a, true, true));
   tr("volume+load");
   PHFEM_TRY(neumann_into(ctx, &out->mesh, &out->topo, &out->cls, g, t, out->load, 1, false));

@@ -306,6 +306,33 @@ def test_pipeline_equals_pieces(ctx):
     rel_close(r["bd"], o["bd"])
 
 
+@pytest.mark.parametrize("case", ["lshape_l3", "stress_l5_l2", "square_l1"])
+def test_pipeline_volume_from_parents(ctx, monkeypatch, case):
+    """The pipeline's element pass rebuilds the refined children's vertices
+    from the last parent mesh (VolArgs::parents: 3 parent gathers per 4
+    children, midpoints 0.5 * (a + b) recomputed, refine.cpp:18,27-37).  Its
+    blocks and load must equal the oracle and the path that reads the refined
+    mesh (PHFEM_VOL_PARENTS=0) bit for bit: a partial last chunk (6 x 4^k
+    children), the permuted / jittered stress mesh, and a 2-parent level."""
+    if case == "lshape_l3":
+        hm, levels, cfg = G.lshape_6tri(), 3, 2
+    elif case == "stress_l5_l2":
+        hm, levels, cfg = O.orient_ccw(G.stress_transform(O.refine_levels(G.square_2tri(), 5), 5)), 2, 2
+    else:
+        hm, levels, cfg = G.square_2tri(), 1, 1
+    args = G.config_fields(cfg)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PHFEM_VOL_PARENTS", flag)
+        outs.append(capi.pipeline(ctx, capi.DeviceMesh.upload(ctx, hm), levels, *args).download())
+    o = O.pipeline(hm, levels, *args)
+    for k in ["B", "D", "M", "M0", "load"]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    for k in ["B", "D", "M", "M0"]:
+        assert np.array_equal(outs[0][k], o[k]), k
+    rel_close(outs[0]["load"], o["load"])
+
+
 def test_pipeline_config1_neumann(ctx):
     hm = G.square_2tri()
     args = G.config_fields(1)

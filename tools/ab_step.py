@@ -3,7 +3,9 @@ per-kernel CUDA-event times (ctx profiling) and the step time, per variant,
 interleaved rounds so clock / thermal drift hits every variant alike.
 
   python tools/ab_step.py [--level 13] [--rounds 3] [--steps 4] LIB [LIB ...]
-  (LIB: a path to a build of libphfem_b200.so, e.g. from tools/variants.sh)
+  (LIB: a path to a build of libphfem_b200.so, e.g. from tools/variants.sh,
+   optionally followed by @VAR=VAL[,VAR=VAL] environment settings, e.g.
+   paper_2401_15557_b200/libphfem_b200.so@PHFEM_VOL_PARENTS=0)
 """
 import argparse
 import json
@@ -50,7 +52,9 @@ def main():
     res = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
         for lib in a.libs:
-            env = dict(os.environ, PHFEM_LIB=os.path.abspath(lib))
+            path, _, kv = lib.partition("@")
+            env = dict(os.environ, PHFEM_LIB=os.path.abspath(path))
+            env.update(x.split("=", 1) for x in kv.split(",") if x)
             out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.level, a.steps, 0 if a.given else 1)], env=env,
                                  capture_output=True, text=True, timeout=600)
             line = [x for x in out.stdout.splitlines() if x.startswith("RESULT ")]
