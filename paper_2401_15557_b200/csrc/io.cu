@@ -23,7 +23,6 @@
 // the reference.  The first
 // error in the reference's order (file, row, check) is found as a minimum
 // over per-row keys; its message is rebuilt on the host from the text.
-#include <cub/device/device_scan.cuh>
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -785,6 +784,79 @@ struct Text {
   }
 };
 
+// Exclusive scan of the int64 line lengths (text offsets pass 2^31 bytes at
+// L12): tile sums, a one-CTA scan of them, downsweep -- the shape of
+// scan_exclusive_i32 (ctx.cu) over 64-bit values.
+constexpr int kScan64Threads = 1024;
+constexpr int kScan64Per = 4;
+constexpr int kScan64Tile = kScan64Threads * kScan64Per;
+
+__global__ void __launch_bounds__(kScan64Threads) k_scan64_tile_sums(const int64_t* __restrict__ in, int64_t n,
+                                                                     int64_t* __restrict__ sums) {
+  __shared__ int64_t sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScan64Tile;
+  int64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScan64Per; ++k) {
+    const int64_t i = base + (int64_t)k * kScan64Threads + threadIdx.x;
+    if (i < n) v += in[i];
+  }
+  int64_t tot;
+  block_exclusive_scan(v, sm, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScan64Threads) k_scan64_sums(int64_t* sums, int64_t n) {
+  __shared__ int64_t sm[33];
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += kScan64Threads) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < n ? sums[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_exclusive_scan(v, sm, &tot);
+    if (i < n) sums[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kScan64Threads) k_scan64_down(const int64_t* __restrict__ in,
+                                                                int64_t* __restrict__ out, int64_t n,
+                                                                const int64_t* __restrict__ sums) {
+  __shared__ int64_t sm[33];
+  const int64_t base = (int64_t)blockIdx.x * kScan64Tile + (int64_t)threadIdx.x * kScan64Per;
+  int64_t v[kScan64Per];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScan64Per; ++k) {
+    const int64_t i = base + k;
+    v[k] = i < n ? in[i] : 0;
+    s += v[k];
+  }
+  int64_t tot;
+  int64_t ex = block_exclusive_scan(s, sm, &tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScan64Per; ++k) {
+    const int64_t i = base + k;
+    if (i < n) out[i] = ex;
+    ex += v[k];
+  }
+}
+
+static phfem_status scan_exclusive_i64(phfem_ctx* ctx, const int64_t* in, int64_t* out, int64_t n) {
+  if (n <= 0) return PHFEM_OK;
+  const int64_t tiles = (n + kScan64Tile - 1) / kScan64Tile;
+  int64_t* sums = nullptr;
+  PHFEM_TRY(dalloc(ctx, &sums, tiles));
+  k_scan64_tile_sums<<<(unsigned)tiles, kScan64Threads, 0, ctx->stream>>>(in, n, sums);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan64_sums<<<1, kScan64Threads, 0, ctx->stream>>>(sums, tiles);
+  PHFEM_CHECK_LAUNCH(ctx);
+  k_scan64_down<<<(unsigned)tiles, kScan64Threads, 0, ctx->stream>>>(in, out, n, sums);
+  PHFEM_CHECK_LAUNCH(ctx);
+  dfree(ctx, sums);
+  return PHFEM_OK;
+}
+
 // Device text: line lengths (int64), one 64-bit scan, the bytes, one D2H.
 template <class LenFn, class WriteFn>
 static phfem_status device_text(phfem_ctx* ctx, int64_t rows, LenFn launch_len, WriteFn launch_write, Text* out) {
@@ -801,13 +873,7 @@ static phfem_status device_text(phfem_ctx* ctx, int64_t rows, LenFn launch_len, 
     PHFEM_TRY(dalloc(ctx, &off, rows + 1));
     PHFEM_TRY(launch_len(len));
     PHFEM_CUDA(ctx, cudaMemsetAsync(len + rows, 0, sizeof(int64_t), ctx->stream));
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, len, off, (int)(rows + 1), ctx->stream);
-    void* tmp = nullptr;
-    PHFEM_TRY(raw_alloc(ctx, &tmp, tb));
-    PHFEM_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp, tb, len, off, (int)(rows + 1), ctx->stream));
-    ctx->launches++;
-    raw_free(ctx, tmp);
+    PHFEM_TRY(scan_exclusive_i64(ctx, len, off, rows + 1));
     PHFEM_CUDA(ctx, cudaMemcpyAsync(&total, off + rows, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
     PHFEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     PHFEM_TRY(dalloc(ctx, &d, std::max<int64_t>(total, 1)));
