@@ -173,6 +173,24 @@ def test_gpu_io_large_round_trip(ctx):
     assert np.array_equal(back.coords, hm.coords) and np.array_equal(back.elements, hm.elements)
 
 
+@pytest.mark.gpu
+def test_gpu_io_text_offsets_past_one_scan_block(ctx):
+    """Square L11 (8.4 M element rows = 2049 scan tiles): the 64-bit line
+    offset scan (k_scan64_*) carries across more than one 1024-tile block.
+    The element text equals numpy's rendering of the 1-based ids (save_mesh,
+    mesh.cpp:170-180) and save -> load is the identity."""
+    hm = O.refine_levels(G.square_2tri(), 11)
+    dm = capi.DeviceMesh.upload(ctx, hm)
+    text = capi.save_mesh_text(ctx, dm)
+    ids = (hm.elements.astype(np.int64) + 1)
+    want = np.char.add(np.char.add(np.char.add(ids[:, 0].astype("S8"), b" "),
+                                   np.char.add(ids[:, 1].astype("S8"), b" ")),
+                       np.char.add(ids[:, 2].astype("S8"), b"\n"))
+    assert text[1] == b"".join(want.tolist())
+    back = capi.load_mesh_text(ctx, *text).download()
+    assert np.array_equal(back.coords, hm.coords) and np.array_equal(back.elements, hm.elements)
+
+
 # ---- the device "%.<P>g" formatter against glibc's printf ---------------------
 def _fmt_cases():
     import struct
