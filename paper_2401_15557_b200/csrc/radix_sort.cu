@@ -11,9 +11,11 @@
 //   scan          exclusive scan of the 256 x ntiles counts -> every
 //                 (digit, tile) pair's first output slot (stable by
 //                 construction: tiles in order inside a digit)
-//   k_rs_scatter  the tile again: stable in-tile ranks (items taken in index
-//                 order, 256 per round: per-warp __match_any peers + per-warp
-//                 digit counts in SMEM), the tile staged in SMEM in digit
+//   k_rs_scatter  the tile again: stable in-tile ranks (each warp owns a
+//                 contiguous chunk and ranks it with __match_any peers +
+//                 its own running digit counters in SMEM -- no block barrier
+//                 per round; one pass over the warps' counts then gives each
+//                 warp's first rank per digit), the tile staged in SMEM in digit
 //                 order, then written out so consecutive threads store
 //                 consecutive slots of one digit (coalesced runs instead of
 //                 one scattered 8-byte store per item)
@@ -73,16 +75,18 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K* __restrict__
   RsSmem<K>& sm = *reinterpret_cast<RsSmem<K>*>(rs_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
-  sm.run[tid] = 0;
   sm.gofs[tid] = offs[(int64_t)tid * ntiles + blockIdx.x];
 #pragma unroll
   for (int w = 0; w < kRsWarps; ++w) sm.wc[w][tid] = 0;
   K k[kRsItems];
   uint32_t v[kRsItems];
   int rk[kRsItems];
+  // warp w owns items [32 kRsItems w, 32 kRsItems (w + 1)) of the tile, 32
+  // consecutive ones per round: index order = (warp, round, lane)
+  const int64_t wbase = base + (int64_t)warp * (kRsItems * 32) + lane_id();
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
-    const int64_t i = base + r * kRsThreads + tid;
+    const int64_t i = wbase + r * 32;
     if (i < n) {
       k[r] = kin[i];
       v[r] = vin[i];
@@ -90,28 +94,29 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K* __restrict__
   }
   __syncthreads();
   const unsigned lt = lanemask_lt();
-  // stable ranks: round r holds items base + 256 r + [0, 256) in index order
+  // stable ranks inside the warp's chunk: the warp's own digit counters, no
+  // block barrier per round
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
-    const int64_t i = base + r * kRsThreads + tid;
+    const int64_t i = wbase + r * 32;
     const unsigned d = i < n ? (unsigned)(k[r] >> shift) & 0xffu : 0x100u;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d < 256u && lane_id() == (unsigned)(__ffs(peers) - 1)) sm.wc[warp][d] = __popc(peers);
-    __syncthreads();
-    if (d < 256u) {
-      int before = sm.run[d];
-      for (int w = 0; w < warp; ++w) before += sm.wc[w][d];
-      rk[r] = before + __popc(peers & lt);
-    }
-    __syncthreads();
-    int tot = 0;
+    if (d < 256u) rk[r] = sm.wc[warp][d] + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256u && lane_id() == (unsigned)(__ffs(peers) - 1)) sm.wc[warp][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // digit tid: the warps' counts -> each warp's first rank, and the tile count
+  {
+    int acc = 0;
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
-      tot += sm.wc[w][tid];
-      sm.wc[w][tid] = 0;
+      const int c = sm.wc[w][tid];
+      sm.wc[w][tid] = acc;
+      acc += c;
     }
-    sm.run[tid] += tot;
-    __syncthreads();
+    sm.run[tid] = acc;
   }
   // digit starts inside the tile, then the tile in digit order in SMEM
   int32_t total;
@@ -119,10 +124,10 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K* __restrict__
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
-    const int64_t i = base + r * kRsThreads + tid;
+    const int64_t i = wbase + r * 32;
     if (i < n) {
       const unsigned d = (unsigned)(k[r] >> shift) & 0xffu;
-      const int p = sm.tstart[d] + rk[r];
+      const int p = sm.tstart[d] + sm.wc[warp][d] + rk[r];
       sm.key[p] = k[r];
       sm.val[p] = v[r];
     }
