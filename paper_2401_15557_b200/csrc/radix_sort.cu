@@ -34,10 +34,14 @@ constexpr int kRsWarps = kRsThreads / 32;
 template <typename K>
 __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const K* __restrict__ keys, int64_t n, int shift,
                                                         int ntiles, int32_t* __restrict__ counts) {
-  __shared__ int32_t h[256];
-  h[threadIdx.x] = 0;
+  // per-warp digit counters: plain SMEM atomics (a same-digit warp serialises
+  // inside one instruction, cheaper than a __match_any per item)
+  __shared__ int32_t h[kRsWarps][256];
+#pragma unroll
+  for (int w = 0; w < kRsWarps; ++w) h[w][threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
+  const int warp = threadIdx.x >> 5;
   K k[kRsItems];  // all loads in flight before the first atomic
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
@@ -47,12 +51,13 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const K* __restrict__ ke
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
     const int64_t i = base + r * kRsThreads + threadIdx.x;
-    const unsigned d = i < n ? (unsigned)(k[r] >> shift) & 0xffu : 0x100u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d < 256u && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+    if (i < n) atomicAdd(&h[warp][(unsigned)(k[r] >> shift) & 0xffu], 1);
   }
   __syncthreads();
-  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  int32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kRsWarps; ++w) tot += h[w][threadIdx.x];
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = tot;
 }
 
 template <typename K>
