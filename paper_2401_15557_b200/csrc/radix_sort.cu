@@ -72,7 +72,7 @@ struct RsSmem {
 };
 
 template <typename K>
-__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(kRsThreads, 3) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            int64_t n, int shift, int ntiles,
                                                            const int32_t* __restrict__ offs, K* __restrict__ kout,
                                                            uint32_t* __restrict__ vout) {
